@@ -1,0 +1,495 @@
+"""oracle.driver -- TEST INFRASTRUCTURE ONLY (the checker, never the product).
+
+CPU restatement of the reference's stage drivers.  The reference ships the
+kernels but not the drivers, so this module restates
+them from the reference's normative text and calls the bit-exact C kernels
+of ``oracle.kernels`` for every kernel-level operation:
+
+* anls-stage      SPEC.md:165-242, PAPER.md:93-128 (Algorithm 1)
+* ipm-stage       SPEC.md:244-374, PAPER.md:136-366 (Algorithm 2, Eqs. 3-11)
+* Schur solve     SPEC.md:68-76, PAPER.md:464-530 (Eqs. 12-13)
+* two-stage       SPEC.md:376-451, PAPER.md:532-619 (Algorithm 3, Eqs. 14-18)
+
+Frozen open semantics (DESIGN.md "Frozen semantics" lists the same items):
+
+1. Warm mode: sweep 0 cold (mode 0), later sweeps mode 2 seeded with the
+   previous sweep's passive sets.
+2. Stage-1 stop: ||(x,y)_{k+1}-(x,y)_k|| <= eps_stol (1 + ||(x,y)_k||) checked
+   after every full sweep, or the sweep cap.
+3. Armijo uses the exact quartic expansion of the residual along the step
+   (phi is evaluated as phi(0) + dphi(alpha) with log1p barrier increments),
+   the same function as SPEC.md:310-327 evaluated without cancellation.
+4. Predictor reuses the last Newton solve's factors with the
+   right-hand side evaluated at the current point; it is skipped once
+   E(.;0) <= tol (it could only change mu, not the iterate).
+5. Relative KKT tolerance: eps_abs = tol_rel * max(1, E_primal(X0, Y0)).
+6. E uses Diag(y) for "s^T Diag(Y)".
+7. Nudge: an updated entry that is not strictly positive becomes
+   (1 - tau) times its previous value.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+from scipy.linalg import solve_triangular
+
+from oracle import kernels as K
+
+
+# ----------------------------------------------------------------------------
+# configuration
+# ----------------------------------------------------------------------------
+@dataclass
+class Stage1Config:
+    eps_stol: float = 1e-3
+    max_sweeps: int = 200
+    tol_kkt: float | None = None  # None -> 1e-12 * max(1, ||C^T d||_inf) per rhs
+    fixed_sweeps: int = 0  # >0: exactly this many sweeps, no step test
+
+
+@dataclass
+class IpmParams:
+    tau: float = 0.9
+    eta: float = 0.5
+    sigma_cap: float = 0.99
+    sigma_c: float = 0.01
+    eps_tol: float = 1e-6
+    max_iter: int = 500
+    max_backtracks: int = 60
+    fixed_iters: int = 0  # >0: run exactly this many inner iterations
+    barrier: str = "paper"  # "paper": one mu (PAPER Eq. 4); "balanced": see barrier_weights
+
+
+@dataclass
+class TransitionParams:
+    rho0_scale: float = 1e-6
+
+
+class OracleError(RuntimeError):
+    def __init__(self, kind, index=-1):
+        super().__init__(f"{kind} (index {index})")
+        self.kind, self.index = kind, index
+
+
+# ----------------------------------------------------------------------------
+# products (numpy/OpenBLAS, as in the reference's missing drivers)
+# ----------------------------------------------------------------------------
+def objective(X, Yt, M):
+    """1/2 ||X Y - M||_F^2 (Yt = Y^T, (m,k))."""
+    F = X @ Yt.T - M
+    return 0.5 * float(np.vdot(F, F))
+
+
+def gradients(X, Yt, M):
+    """graX = vec(Y F^T) -> (n,k) = F Y^T; graY = vec(X^T F) -> (m,k)."""
+    F = X @ Yt.T - M
+    return F, F @ Yt, F.T @ X
+
+
+def kkt_error(X, Yt, R, S, graX, graY, mu, wx=1.0, wy=1.0):
+    """SPEC.md:274 / PAPER Eq. 9 (Diag(y) reading)."""
+    st = math.sqrt(float(np.sum((graX - R) ** 2) + np.sum((graY - S) ** 2)))
+    cp = math.sqrt(float(np.sum((X * R - wx * mu) ** 2) + np.sum((Yt * S - wy * mu) ** 2)))
+    return max(st, cp)
+
+
+def kkt_error_primal_only(X, Yt, M):
+    """SPEC.md:420 / PAPER.md:633-639: E(x,y,max(graX,0),max(graY,0);0)."""
+    _, gX, gY = gradients(X, Yt, M)
+    return kkt_error(X, Yt, np.maximum(gX, 0.0), np.maximum(gY, 0.0), gX, gY, 0.0)
+
+
+def _nnls_tol(ctb, tol_kkt):
+    if tol_kkt is not None:
+        return np.full(ctb.shape[0], float(tol_kkt))
+    if ctb.shape[0] == 0:
+        return np.zeros(0)
+    return 1e-12 * np.maximum(1.0, np.abs(ctb).max(axis=1))
+
+
+def _raise_status(status, what):
+    bad = np.flatnonzero(status)
+    if bad.size:
+        i = int(bad[0])
+        kind = "MaxIterationsExceeded" if status[i] == 1 else "RankDeficientPassiveSet"
+        raise OracleError(f"{kind} in {what}", i)
+
+
+# ----------------------------------------------------------------------------
+# stage 1: ANLS (Algorithm 1)
+# ----------------------------------------------------------------------------
+def update_X(X, Yt, M, pX, mode, cfg, row_norm2):
+    """rows of X <- NNLS(C = Y^T, d = M_i,:)."""
+    ctc = Yt.T @ Yt
+    ctb = M @ Yt
+    tol = _nnls_tol(ctb, cfg.tol_kkt)
+    k = X.shape[1]
+    x, p, ch, r2, st = K.nnls_batch(ctc, ctb, row_norm2, pX, mode, tol, 3 * k)
+    _raise_status(st, "update_X")
+    return x, p, ch, r2
+
+
+def update_Y(X, Yt, M, pY, mode, cfg, col_norm2):
+    """columns of Y <- NNLS(C = X, d = M_:,j)."""
+    ctc = X.T @ X
+    ctb = M.T @ X
+    tol = _nnls_tol(ctb, cfg.tol_kkt)
+    k = X.shape[1]
+    y, p, ch, r2, st = K.nnls_batch(ctc, ctb, col_norm2, pY, mode, tol, 3 * k)
+    _raise_status(st, "update_Y")
+    return y, p, ch, r2
+
+
+@dataclass
+class Stage1Result:
+    X: np.ndarray
+    Yt: np.ndarray
+    pX: np.ndarray
+    pY: np.ndarray
+    sweeps: int
+    converged: bool
+    trace: list = field(default_factory=list)
+    changes_X: list = field(default_factory=list)
+    changes_Y: list = field(default_factory=list)
+    seconds: float = 0.0
+
+
+def run_stage1(M, X, Yt, cfg=None, pX=None, pY=None):
+    """SPEC.md:209 run_stage1.  X (n,k), Yt = Y^T (m,k).  Carries optional."""
+    cfg = cfg or Stage1Config()
+    t0 = time.perf_counter()
+    X = np.array(X, dtype=np.float64)
+    Yt = np.array(Yt, dtype=np.float64)
+    n, k = X.shape
+    m = Yt.shape[0]
+    have_carry = pX is not None
+    pX = np.zeros((n, k), bool) if pX is None else pX.copy()
+    pY = np.zeros((m, k), bool) if pY is None else pY.copy()
+    row_n2 = np.einsum("ij,ij->i", M, M)
+    col_n2 = np.einsum("ij,ij->j", M, M)
+    res = Stage1Result(X, Yt, pX, pY, 0, False)
+    nsweeps = cfg.fixed_sweeps if cfg.fixed_sweeps > 0 else cfg.max_sweeps
+    for sweep in range(nsweeps):
+        mode = 2 if (sweep > 0 or have_carry) else 0
+        Xn, pX, chX, _ = update_X(X, Yt, M, pX, mode, cfg, row_n2)
+        Yn, pY, chY, r2Y = update_Y(Xn, Yt, M, pY, mode, cfg, col_n2)
+        step = math.sqrt(float(np.sum((Xn - X) ** 2) + np.sum((Yn - Yt) ** 2)))
+        nrm = math.sqrt(float(np.sum(X ** 2) + np.sum(Yt ** 2)))
+        X, Yt = Xn, Yn
+        res.sweeps = sweep + 1
+        res.trace.append((time.perf_counter() - t0, 0.5 * float(np.sum(r2Y)), step))
+        res.changes_X.append(int(chX.sum()))
+        res.changes_Y.append(int(chY.sum()))
+        if cfg.fixed_sweeps <= 0 and step <= cfg.eps_stol * (1.0 + nrm):
+            res.converged = True
+            break
+    res.X, res.Yt, res.pX, res.pY = X, Yt, pX, pY
+    res.seconds = time.perf_counter() - t0
+    return res
+
+
+# ----------------------------------------------------------------------------
+# stage 2: interior point (Algorithm 2) with the Hessian switch (Algorithm 3)
+# ----------------------------------------------------------------------------
+@dataclass
+class IpmState:
+    X: np.ndarray
+    Yt: np.ndarray
+    R: np.ndarray
+    S: np.ndarray
+    mu: float
+    rho: float
+    flag: bool = False
+
+
+def transition(X, Yt, M, eps_tol, tp=None):
+    """SPEC.md:393 / PAPER Eqs. 14-18."""
+    tp = tp or TransitionParams()
+    big = max(float(X.max(initial=0.0)), float(Yt.max(initial=0.0)))
+    if big <= 0.0:
+        raise OracleError("DegenerateFactor")
+    rho0 = tp.rho0_scale * big
+    X = np.maximum(X, rho0)
+    Yt = np.maximum(Yt, rho0)
+    _, gX, gY = gradients(X, Yt, M)
+    R = np.full_like(X, np.abs(gX).max())
+    S = np.full_like(Yt, np.abs(gY).max())
+    n, k = X.shape
+    m = Yt.shape[0]
+    mu = (float(np.vdot(X, R)) + float(np.vdot(Yt, S))) / (n * k + m * k)
+    return IpmState(X, Yt, R, S, mu, eps_tol, False)
+
+
+def fraction_to_boundary(v, dv, tau):
+    """SPEC.md:301 / PAPER Eq. 6 for one stacked vector: min(1, min -tau v/dv)."""
+    neg = dv < 0.0
+    if not np.any(neg):
+        return 1.0
+    return float(min(1.0, np.min(-tau * v[neg] / dv[neg])))
+
+
+def _ftb2(a, da, b, db, tau):
+    return min(fraction_to_boundary(a.ravel(), da.ravel(), tau),
+               fraction_to_boundary(b.ravel(), db.ravel(), tau))
+
+
+@dataclass
+class Factorization:
+    X: np.ndarray
+    Yt: np.ndarray
+    F: np.ndarray
+    L: np.ndarray
+    Ls: np.ndarray  # lower Cholesky factor of the mk x mk Schur matrix
+    full: bool
+
+
+def schur_matrix(XtX, rho, S_over_Y, Sacc):
+    """blockdiag(X^T X + rho I + Diag(s_j/y_j)) - S."""
+    m, k = S_over_Y.shape
+    A = -Sacc
+    base = XtX + rho * np.eye(k)
+    for j in range(m):
+        sl = slice(j * k, (j + 1) * k)
+        A[sl, sl] += base + np.diag(S_over_Y[j])
+    return A
+
+
+def spd_factor(A):
+    """lower Cholesky; None when not positive definite."""
+    try:
+        return np.linalg.cholesky(A)
+    except np.linalg.LinAlgError:
+        return None
+
+
+def spd_solve_factored(Ls, b):
+    z = solve_triangular(Ls, b, lower=True, check_finite=False)
+    return solve_triangular(Ls.T, z, lower=False, check_finite=False)
+
+
+def barrier_weights(n, m, barrier):
+    """Per-block barrier weights (wx, wy): mu_X = wx*mu, mu_Y = wy*mu.
+
+    "paper": wx = wy = 1 (PAPER Eqs. 4, 9 and the merit function).
+    "balanced": n*wx = m*wy, (n*wx + m*wy)/(n+m) = 1.  With one mu and n != m
+    the perturbed KKT system has no solution: summing x_ip*graX_ip - y_pj*graY_pj
+    over one component gives 0 for any (X, Y) (scale invariance of XY), which
+    forces mu*(n - m) = 0 at a central point; the balanced weights restore it.
+    """
+    if barrier == "paper":
+        return 1.0, 1.0
+    if barrier == "balanced":
+        return (n + m) / (2.0 * n), (n + m) / (2.0 * m)
+    raise ValueError(barrier)
+
+
+def newton_direction(M, st: IpmState, F, gX, gY, full, wx=1.0, wy=1.0):
+    """R1 blocks, Schur reduction, mk x mk solve, back-sub.
+
+    Returns (dx, dy, dr, ds, gtp, fact) or None when the Schur matrix is not
+    positive definite (SchurNotPositiveDefinite; only expected with full C).
+    """
+    X, Yt, R, S, mu, rho = st.X, st.Yt, st.R, st.S, st.mu, st.rho
+    n, k = X.shape
+    YYt = Yt.T @ Yt
+    R1 = YYt[None] + rho * np.eye(k)[None] + np.einsum("ip,pq->ipq", R / X, np.eye(k))
+    L, bad = K.block_cholesky(R1)
+    if bad >= 0:
+        raise OracleError("NotPositiveDefinite", bad)
+    mux, muy = wx * mu, wy * mu
+    b1 = mux / X - gX
+    h = K.block_solve_lower(L, b1[:, :, None])[:, :, 0]
+    Sacc, racc = K.schur_reduce(X, Yt, L, h, F, full)
+    A = schur_matrix(X.T @ X, rho, S / Yt, Sacc)
+    Ls = spd_factor(A)
+    if Ls is None:
+        if full:
+            return None
+        raise OracleError("NotPositiveDefinite (Schur, Gauss-Newton)")
+    b2 = muy / Yt - gY
+    dy = spd_solve_factored(Ls, (b2 - racc).ravel()).reshape(Yt.shape)
+    dx = K.back_substitute(X, Yt, L, h, dy, F, full)
+    dr = mux / X - R - (R / X) * dx
+    ds = muy / Yt - S - (S / Yt) * dy
+    gtp = float(np.vdot(dx, gX - mux / X)) + float(np.vdot(dy, gY - muy / Yt))
+    return dx, dy, dr, ds, gtp, Factorization(X, Yt, F, L, Ls, full)
+
+
+def quartic_coeffs(X, Yt, dX, dYt, M):
+    """Inner products of A = XY-M, B = dX Y + X dY, C = dX dY (one pass over M)."""
+    A = X @ Yt.T - M
+    B = dX @ Yt.T + X @ dYt.T
+    C = dX @ dYt.T
+    return (float(np.vdot(A, A)), float(np.vdot(A, B)), float(np.vdot(B, B)),
+            float(np.vdot(A, C)), float(np.vdot(B, C)), float(np.vdot(C, C)))
+
+
+def merit_delta(coef, alpha, X, dX, Yt, dYt, mu, wx=1.0, wy=1.0):
+    """phi(x + a dx, y + a dy) - phi(x, y), evaluated without cancellation."""
+    _, ab, bb, ac, bc, cc = coef
+    quad = alpha * ab + alpha * alpha * (0.5 * bb + ac) + alpha ** 3 * bc + 0.5 * alpha ** 4 * cc
+    bx = float(np.sum(np.log1p(alpha * dX / X)))
+    by = float(np.sum(np.log1p(alpha * dYt / Yt)))
+    return quad - mu * (wx * bx + wy * by)
+
+
+def merit_phi(X, Yt, M, mu):
+    """SPEC.md:310."""
+    if np.any(X <= 0) or np.any(Yt <= 0):
+        raise OracleError("NonPositiveInput")
+    return objective(X, Yt, M) - mu * (float(np.sum(np.log(X))) + float(np.sum(np.log(Yt))))
+
+
+def _nudge(new, old, tau):
+    bad = ~(new > 0.0)
+    if np.any(bad):
+        new = np.where(bad, (1.0 - tau) * old, new)
+    return new
+
+
+@dataclass
+class IpmResult:
+    state: IpmState
+    iters: int
+    outer: int
+    converged: bool
+    E0: float
+    trace: list = field(default_factory=list)
+    armijo_t: list = field(default_factory=list)
+    flags: list = field(default_factory=list)
+    seconds: float = 0.0
+
+
+def predictor_sigma(st: IpmState, gX, gY, fact: Factorization, p: IpmParams):
+    """SPEC.md:328 / PAPER Eqs. 7-8, reusing the last Newton factorization."""
+    X, Yt, R, S = st.X, st.Yt, st.R, st.S
+    n, k = X.shape
+    m = Yt.shape[0]
+    b1 = -gX
+    h = K.block_solve_lower(fact.L, b1[:, :, None])[:, :, 0]
+    racc = K.rhs_reduce(fact.X, fact.Yt, fact.L, h, fact.F, fact.full)
+    dy = spd_solve_factored(fact.Ls, (-gY - racc).ravel()).reshape(Yt.shape)
+    dx = K.back_substitute(fact.X, fact.Yt, fact.L, h, dy, fact.F, fact.full)
+    dr = -R - (R / X) * dx
+    ds = -S - (S / Yt) * dy
+    a1 = _ftb2(X, dx, Yt, dy, 1.0)
+    a2 = _ftb2(R, dr, S, ds, 1.0)
+    nk = n * k + m * k
+    mu_aff = (float(np.vdot(X + a1 * dx, R + a2 * dr)) + float(np.vdot(Yt + a1 * dy, S + a2 * ds))) / nk
+    mu_bar = (float(np.vdot(X, R)) + float(np.vdot(Yt, S))) / nk
+    return min((mu_aff / mu_bar) ** 3, p.sigma_cap)
+
+
+def run_ipm(M, st: IpmState, p: IpmParams = None):
+    """SPEC.md:337 run_ipm: Algorithm 2 nested loops + Algorithm 3 switch."""
+    p = p or IpmParams()
+    t0 = time.perf_counter()
+    F, gX, gY = gradients(st.X, st.Yt, M)
+    E0 = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0)
+    res = IpmResult(st, 0, 0, False, E0)
+    cap = p.fixed_iters if p.fixed_iters > 0 else p.max_iter
+    tol = 0.0 if p.fixed_iters > 0 else p.eps_tol
+    fact = None
+    e_zero = E0
+    wx, wy = barrier_weights(st.X.shape[0], st.Yt.shape[0], p.barrier)
+    while e_zero > tol and res.iters < cap:
+        eps_mu = st.mu
+        while (kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, st.mu, wx, wy) > eps_mu
+               and res.iters < cap):
+            out = None
+            used_full = False
+            if st.flag:
+                out = newton_direction(M, st, F, gX, gY, True, wx, wy)
+                if out is None or out[4] >= 0.0:
+                    st.flag = False
+                    out = None
+                else:
+                    used_full = True
+            if out is None:
+                out = newton_direction(M, st, F, gX, gY, False, wx, wy)
+            dx, dy, dr, ds, gtp, fact = out
+            a1max = _ftb2(st.X, dx, st.Yt, dy, p.tau)
+            a2max = _ftb2(st.R, dr, st.S, ds, p.tau)
+            coef = quartic_coeffs(st.X, st.Yt, dx, dy, M)
+            t = 0
+            while True:
+                a1 = a1max / (2.0 ** t)
+                if merit_delta(coef, a1, st.X, dx, st.Yt, dy, st.mu, wx, wy) <= p.eta * a1 * gtp:
+                    break
+                t += 1
+                if t > p.max_backtracks:
+                    raise OracleError("LineSearchStall", res.iters)
+            st.X = _nudge(st.X + a1 * dx, st.X, p.tau)
+            st.Yt = _nudge(st.Yt + a1 * dy, st.Yt, p.tau)
+            st.R = _nudge(st.R + a2max * dr, st.R, p.tau)
+            st.S = _nudge(st.S + a2max * ds, st.S, p.tau)
+            res.iters += 1
+            res.armijo_t.append(t)
+            res.flags.append(used_full)
+            F, gX, gY = gradients(st.X, st.Yt, M)
+            e_zero = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0)
+            res.trace.append((time.perf_counter() - t0, 0.5 * float(np.vdot(F, F)), e_zero, st.mu,
+                              a1, a2max, t))
+        res.outer += 1
+        e_zero = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0)
+        if e_zero <= tol or res.iters >= cap:
+            break
+        if fact is None:  # no Newton solve yet: factor at the current point
+            fact = newton_direction(M, st, F, gX, gY, False, wx, wy)[5]
+        sigma = predictor_sigma(st, gX, gY, fact, p)
+        st.mu = sigma * st.mu
+        st.flag = sigma <= p.sigma_c
+    res.converged = e_zero <= tol
+    res.state = st
+    res.seconds = time.perf_counter() - t0
+    return res
+
+
+# ----------------------------------------------------------------------------
+# two-stage orchestrator (Algorithm 3)
+# ----------------------------------------------------------------------------
+@dataclass
+class SolveReport:
+    X: np.ndarray
+    Yt: np.ndarray
+    objective: float
+    kkt: float
+    eps_abs: float
+    stage1: Stage1Result
+    ipm: IpmResult | None
+    converged: bool
+    stage1_time: float
+    stage2_time: float
+
+
+def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1=None, ipm=None, tp=None, stage="two_stage",
+                  pX=None, pY=None, e_scale=None):
+    """SPEC.md:411 run_two_stage.  X0 (n,k), Y0 (k,m)."""
+    M = np.asarray(M, dtype=np.float64)
+    X0 = np.asarray(X0, dtype=np.float64)
+    Yt0 = np.ascontiguousarray(np.asarray(Y0, dtype=np.float64).T)
+    if e_scale is None:
+        e_scale = max(1.0, kkt_error_primal_only(X0, Yt0, M))
+    eps_abs = tol_rel * e_scale
+    p = ipm or IpmParams()
+    p.eps_tol = eps_abs
+    s1 = s1 or Stage1Config()
+    if stage == "ipm_only":
+        r1 = Stage1Result(X0.copy(), Yt0.copy(), np.zeros(X0.shape, bool),
+                          np.zeros(Yt0.shape, bool), 0, False)
+    else:
+        r1 = run_stage1(M, X0, Yt0, s1, pX, pY)
+    if stage == "anls_only":
+        X, Yt = r1.X, r1.Yt
+        return SolveReport(X, Yt, objective(X, Yt, M), kkt_error_primal_only(X, Yt, M), eps_abs,
+                           r1, None, kkt_error_primal_only(X, Yt, M) <= eps_abs, r1.seconds, 0.0)
+    st = transition(r1.X, r1.Yt, M, eps_abs, tp)
+    r2 = run_ipm(M, st, p)
+    X, Yt = r2.state.X, r2.state.Yt
+    F, gX, gY = gradients(X, Yt, M)
+    kkt = kkt_error(X, Yt, r2.state.R, r2.state.S, gX, gY, 0.0)
+    return SolveReport(X, Yt, objective(X, Yt, M), kkt, eps_abs, r1, r2, r2.converged,
+                       r1.seconds, r2.seconds)

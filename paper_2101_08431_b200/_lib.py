@@ -1,0 +1,69 @@
+"""ctypes binding of libnmfb200.so (include/nmfb200.h).
+
+The product path has no CPU fallback: if the library is missing or fails to
+load, every entry point raises ``NativeLibraryError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import NativeLibraryError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libnmfb200.so")
+
+P = ctypes.c_void_p
+L = ctypes.c_long
+I = ctypes.c_int
+D = ctypes.c_double
+
+# name -> argtypes (all return int status)
+SIGNATURES = {
+    "nmfb_surface_nnls_batch": [P, P, P, P, I, P, L, L, L, P, P, P, P, P, P, P, P],
+    "nmfb_surface_block_cholesky": [P, L, L, P, P, P],
+    "nmfb_surface_block_solve_lower": [P, P, L, L, L, I, P, P],
+    "nmfb_surface_schur_reduce": [P, P, P, P, P, L, L, L, I, P, P, P],
+    "nmfb_surface_rhs_reduce": [P, P, P, P, P, L, L, L, I, P, P],
+    "nmfb_surface_back_substitute": [P, P, P, P, P, P, L, L, L, I, P, P],
+}
+
+_lib = None
+
+
+def header_symbols() -> list[str]:
+    """Function names declared in include/nmfb200.h."""
+    import re
+
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "nmfb200.h")
+    with open(hdr) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(nmfb_[a-z0-9_]+)\s*\(", text)))
+
+
+def load(path: str | None = None):
+    """Load (once) and return the ctypes library object."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or SO_PATH
+    if not os.path.exists(path):
+        raise NativeLibraryError(
+            f"{path} not found: build it with `python -m paper_2101_08431_b200._build` "
+            "(there is no CPU fallback)")
+    try:
+        so = ctypes.CDLL(path)
+    except OSError as exc:  # pragma: no cover - depends on the box
+        raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
+    for name, argt in SIGNATURES.items():
+        fn = getattr(so, name)
+        fn.argtypes = argt
+        fn.restype = ctypes.c_int
+    _lib = so
+    return so
+
+
+def call(name: str, *args) -> None:
+    rc = getattr(load(), name)(*args)
+    if rc != 0:
+        raise NativeLibraryError(f"{name} returned {rc}")

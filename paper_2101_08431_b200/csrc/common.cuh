@@ -1,0 +1,76 @@
+// Shared helpers for the nmf-b200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define NMFB_MAX_K 16
+
+// Return codes of the C-ABI (0 = ok, negative = argument / launch error).
+enum {
+  NMFB_OK = 0,
+  NMFB_EINVAL = -1,
+  NMFB_ELAUNCH = -2,
+  NMFB_ENOMEM = -3,
+  NMFB_EUNSUPPORTED = -4,
+};
+
+#define NMFB_CHECK_LAUNCH()                                   \
+  do {                                                        \
+    cudaError_t e__ = cudaGetLastError();                     \
+    if (e__ != cudaSuccess) return NMFB_ELAUNCH;              \
+  } while (0)
+
+static inline int nmfb_blocks(long n, int threads, int cap = 148 * 32) {
+  long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum with a fixed reduction tree (deterministic for a fixed
+// blockDim).  `sh` needs blockDim.x/32 doubles.  Result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < nw ? sh[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = -1.0 / 0.0;
+  if (wid == 0) {
+    r = lane < nw ? sh[lane] : -1.0 / 0.0;
+    r = warp_max(r);
+  }
+  return r;
+}
