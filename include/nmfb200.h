@@ -68,6 +68,121 @@ int nmfb_surface_back_substitute(const double *x_rows, const double *y_cols, con
                                  const double *h, const double *dy_rows, const double *resid,
                                  long n, long m, long k, int full, double *dx, void *stream);
 
+
+/* ---- production entries (device-resident two-stage solver) ---------------
+ * Products over M (n x m, fp64 or fp32 when *_is_f32 != 0); reductions use a
+ * fixed decomposition (bit-reproducible).  `work` buffers are caller-owned
+ * scratch of at least the stated length (doubles). */
+
+/* out (rows, k) = scale * A B, A (rows, cols), B (cols, k); tol[i] =
+ * 1e-12 max(1, ||out_i||_inf) when tol != NULL.
+ * Replaces the driver products M Y^T (update_X) and F Y^T. */
+int nmfb_rowprod(const void *A, int a_is_f32, long rows, long cols, const double *B, long k,
+                 double *out, double *tol, double scale, void *stream);
+
+/* out (cols, k) = scale * A^T B, A (rows, cols), B (rows, k): X^T M (update_Y,
+ * SPEC.md:200), the Grams X^T X / Y Y^T, F^T X (graY).  work >= nmfb_colprod_work_len. */
+long nmfb_colprod_work_len(long rows, long cols, long k);
+int nmfb_colprod(const void *A, int a_is_f32, long rows, long cols, const double *B, long k,
+                 double *out, double *tol, double scale, double *work, long work_len,
+                 void *stream);
+
+/* btb of both half-sweeps: squared row and column norms of M. */
+int nmfb_sqnorms(const void *A, int a_is_f32, long rows, long cols, double *row_out,
+                 double *col_out, double *work, long work_len, void *stream);
+
+/* stats = [||Xn-X||^2 + ||Yn-Y||^2, ||X||^2 + ||Y||^2, sum r2] */
+int nmfb_stage1_stats(const double *Xo, const double *Xn, long nx, const double *Yo,
+                      const double *Yn, long ny, const double *r2, long nr, double *stats,
+                      double *work, long work_len, void *stream);
+
+/* *out = first index with st != 0, 0x7F7F7F7F when none (nnls status scan) */
+int nmfb_first_nonzero_i8(const int8_t *st, long len, int *out, void *stream);
+
+/* number of partial blocks used by the IPM reductions (work sizing) */
+int nmfb_ipm_reduce_blocks(void);
+
+/* F = X Y - M, graX = F Y^T, out[0] = ||F||^2 (SPEC.md:265 assemble_gradients) */
+int nmfb_residual(const void *M, int m_is_f32, long n, long m, long k, const double *X,
+                  const double *Yt, double *F, double *gX, double *out, double *work,
+                  void *stream);
+
+/* R1 blocks + block Cholesky + h = L^{-1}(mux/x - graX), g = L^{-T} h,
+ * Apk = packed R1^{-1}, XXpk = packed x x^T; *bad = first failing row (0x7F7F7F7F: none) */
+int nmfb_r1_factor(const double *GY, const double *X, const double *R, const double *gX,
+                   double mux, double rho, long n, long k, double *L, double *h, double *g,
+                   double *Apk, double *XXpk, int *bad, void *stream);
+
+/* h = L^{-1}(scale b1), g = L^{-T} h (predictor right-hand side with reused factors) */
+int nmfb_hg(const double *L, const double *b1, double b1_scale, long n, long k, double *h,
+            double *g, void *stream);
+
+/* out (ca, cb) = A^T B for A (rows, ca), B (rows, cb); work >= nmfb_atb_work_len */
+long nmfb_atb_work_len(long rows, long ca, long cb);
+int nmfb_atb(const double *A, long rows, long ca, const double *B, long cb, double *out,
+             double *work, long work_len, void *stream);
+
+/* P[i][(p,q,a)] = x_ip Rinv_i[q,a]  (full-Hessian coupling, n x k^3) */
+int nmfb_make_p(const double *X, const double *Apk, long n, long k, double *P, void *stream);
+
+/* A (mk, mk) lower block triangle = blockdiag(X^T X + rho I + Diag(s/y)) - S
+ * (S = schur_reduce's s_acc, _kernels_numba.py:72; W != NULL adds the full-C
+ * cross terms) */
+int nmfb_schur_assemble(const double *Yt, const double *S, long m, long k, const double *Zpk,
+                        const double *XtX, double rho, const double *W, double *A,
+                        void *stream);
+
+/* full-C residual term: A -= sum_i f_ij f_il Rinv_i (lower block triangle) */
+int nmfb_schur_term4(const double *F, long n, long m, long k, const double *Apk, double *A,
+                     void *stream);
+
+/* rhs = muy/y - graY - r_acc, r_acc_j = H y_j (+ (F^T g)_j when FtG != NULL)
+ * (rhs_reduce, _kernels_numba.py:146) */
+int nmfb_schur_rhs(const double *Yt, const double *gY, const double *H, const double *FtG,
+                   double muy, long m, long k, double *rhs, void *stream);
+
+/* back_substitute (_kernels_numba.py:181) + dr, ds + reductions:
+ * out = [(dx,dy).grad phi, alpha1_max, alpha2_max] */
+int nmfb_direction(const double *L, const double *Xf, const double *h, const double *Gdy,
+                   const double *FdY, const double *X, const double *R, const double *gX,
+                   double mux, const double *Yt, const double *S, const double *gY,
+                   const double *dY, double muy, double tau, long n, long m, long k, double *dX,
+                   double *dR, double *dS, double *out, double *work, long work_len,
+                   void *stream);
+
+/* Armijo in one pass over M: out = [AA, AB, BB, AC, BC, CC] for A = F,
+ * B = dX Y + X dY, C = dX dY (SPEC.md:319 armijo_search) */
+int nmfb_quartic(const double *F, long n, long m, long k, const double *X, const double *dX,
+                 const double *Yt, const double *dYt, double *out, double *work, void *stream);
+
+/* out[2t + {0,1}] = sum log1p(a_t dv/v) over X / Y, a_t = (*alpha_max) 2^-t */
+int nmfb_barrier_trials(const double *X, const double *dX, long nx, const double *Yt,
+                        const double *dYt, long ny, const double *alpha_max, int ntrials,
+                        double *out, double *work, long work_len, void *stream);
+
+/* v += alpha dv with the (1 - tau) nudge */
+int nmfb_step_nudge(double *v, const double *dv, long len, double alpha, double tau,
+                    void *stream);
+
+/* E (PAPER Eq. 9) ingredients, out[12]; R == NULL scores primal-only duals
+ * (SPEC.md:420 kkt_error_primal_only) */
+int nmfb_kkt_sums(const double *X, const double *R, const double *gX, long nx, const double *Yt,
+                  const double *S, const double *gY, long ny, double mux, double muy,
+                  double *out, double *work, void *stream);
+
+/* mu_aff numerator (PAPER Eq. 7) */
+int nmfb_affine_mu(const double *X, const double *dX, const double *R, const double *dR, long nx,
+                   const double *Yt, const double *dY, const double *S, const double *dS, long ny,
+                   double a1, double a2, double *out, double *work, void *stream);
+
+int nmfb_clamp_min(double *v, long len, double lo, void *stream);
+int nmfb_fill(double *v, long len, double c, void *stream);
+
+/* spd_solve: in-place lower Cholesky of A (N x N); *info = first
+ * non-positive pivot column or -1.  Then (L L^T) x = b in place on b. */
+int nmfb_dense_cholesky(double *A, long N, int *info, void *stream);
+int nmfb_dense_solve(const double *L, long N, double *b, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,35 @@ SIGNATURES = {
     "nmfb_surface_schur_reduce": [P, P, P, P, P, L, L, L, I, P, P, P],
     "nmfb_surface_rhs_reduce": [P, P, P, P, P, L, L, L, I, P, P],
     "nmfb_surface_back_substitute": [P, P, P, P, P, P, L, L, L, I, P, P],
+    # production entries
+    "nmfb_rowprod": [P, I, L, L, P, L, P, P, D, P],
+    "nmfb_colprod_work_len": [L, L, L],
+    "nmfb_colprod": [P, I, L, L, P, L, P, P, D, P, L, P],
+    "nmfb_sqnorms": [P, I, L, L, P, P, P, L, P],
+    "nmfb_stage1_stats": [P, P, L, P, P, L, P, L, P, P, L, P],
+    "nmfb_first_nonzero_i8": [P, L, P, P],
+    "nmfb_ipm_reduce_blocks": [],
+    "nmfb_residual": [P, I, L, L, L, P, P, P, P, P, P, P],
+    "nmfb_r1_factor": [P, P, P, P, D, D, L, L, P, P, P, P, P, P, P],
+    "nmfb_hg": [P, P, D, L, L, P, P, P],
+    "nmfb_atb_work_len": [L, L, L],
+    "nmfb_atb": [P, L, L, P, L, P, P, L, P],
+    "nmfb_make_p": [P, P, L, L, P, P],
+    "nmfb_schur_assemble": [P, P, L, L, P, P, D, P, P, P],
+    "nmfb_schur_term4": [P, L, L, L, P, P, P],
+    "nmfb_schur_rhs": [P, P, P, P, D, L, L, P, P],
+    "nmfb_direction": [P, P, P, P, P, P, P, P, D, P, P, P, P, D, D, L, L, L, P, P, P, P, P, L, P],
+    "nmfb_quartic": [P, L, L, L, P, P, P, P, P, P, P],
+    "nmfb_barrier_trials": [P, P, L, P, P, L, P, I, P, P, L, P],
+    "nmfb_step_nudge": [P, P, L, D, D, P],
+    "nmfb_kkt_sums": [P, P, P, L, P, P, P, L, D, D, P, P, P],
+    "nmfb_affine_mu": [P, P, P, P, L, P, P, P, P, L, D, D, P, P, P],
+    "nmfb_clamp_min": [P, L, D, P],
+    "nmfb_fill": [P, L, D, P],
+    "nmfb_dense_cholesky": [P, L, P, P],
+    "nmfb_dense_solve": [P, L, P, P],
 }
+RESTYPES = {"nmfb_colprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long}
 
 _lib = None
 
@@ -58,7 +86,7 @@ def load(path: str | None = None):
     for name, argt in SIGNATURES.items():
         fn = getattr(so, name)
         fn.argtypes = argt
-        fn.restype = ctypes.c_int
+        fn.restype = RESTYPES.get(name, ctypes.c_int)
     _lib = so
     return so
 

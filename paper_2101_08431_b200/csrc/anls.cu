@@ -1,0 +1,405 @@
+// Stage-1 (ANLS) production kernels: the HBM-streaming tall-skinny products
+// around the batched NNLS (PAPER Algorithm 1).
+//
+//   X-update:  ctb = M Y^T      (n x k)   k_rowprod   one pass over M rows
+//   Y-update:  ctb = (X^T M)^T  (m x k)   k_colprod   split-K partials over
+//                                                     row stripes + fixed-order sum
+//   Grams     YY^T, X^T X                 k_colprod on the factor itself
+//   norms     ||M_i,:||^2, ||M_:,j||^2    once per problem (btb)
+//   stats     step / norm / objective     fixed-tree block reductions
+//
+// All reductions use a fixed decomposition that depends only on the problem
+// shape, so results are bit-reproducible run to run.  M may be float64 or
+// float32 (config c5 stores M in fp32; products accumulate in fp64).
+#include "common.cuh"
+#include "nmfb200.h"
+
+namespace {
+
+template <typename T>
+struct Vec2;
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
+
+// ---------------------------------------------------------------------------
+// rowprod: out[i, :] = sum_j A[i, j] * B[j, :]   (A rows x cols, B cols x K)
+// One warp per ROWS_PER_WARP rows; lanes stride the columns in pairs so each
+// B row loaded into registers is reused for every row of the warp.
+// Optional: tol[i] = 1e-12 * max(1, max_p |out[i,p]|)  (SPEC.md:147 default).
+// ---------------------------------------------------------------------------
+template <int K, int R, typename T>
+__global__ void __launch_bounds__(256) k_rowprod(const T* __restrict__ A, long rows, long cols,
+                                                 const double* __restrict__ B,
+                                                 double* __restrict__ out,
+                                                 double* __restrict__ tol, double alpha_scale) {
+  const int lane = threadIdx.x & 31;
+  const long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long nwarps = ((long)gridDim.x * blockDim.x) >> 5;
+  for (long r0 = warp * R; r0 < rows; r0 += nwarps * R) {
+    double acc[R][K];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int p = 0; p < K; ++p) acc[r][p] = 0.0;
+    const bool pairs = (cols % 2 == 0);
+    if (pairs) {
+      using V = typename Vec2<T>::type;
+      for (long j = 2 * lane; j < cols; j += 64) {
+        double b0[K], b1[K];
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          b0[p] = __ldg(B + j * K + p);
+          b1[p] = __ldg(B + (j + 1) * K + p);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r0 + r < rows) {
+            const V a = *reinterpret_cast<const V*>(A + (r0 + r) * cols + j);
+            const double a0 = (double)a.x, a1 = (double)a.y;
+#pragma unroll
+            for (int p = 0; p < K; ++p) acc[r][p] = fma(a0, b0[p], fma(a1, b1[p], acc[r][p]));
+          }
+        }
+      }
+    } else {
+      for (long j = lane; j < cols; j += 32) {
+        double b0[K];
+#pragma unroll
+        for (int p = 0; p < K; ++p) b0[p] = __ldg(B + j * K + p);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r0 + r < rows) {
+            const double a0 = (double)A[(r0 + r) * cols + j];
+#pragma unroll
+            for (int p = 0; p < K; ++p) acc[r][p] = fma(a0, b0[p], acc[r][p]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double amax = 0.0;
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        const double v = warp_sum(acc[r][p]) * alpha_scale;
+        acc[r][p] = v;
+        amax = fmax(amax, fabs(v));
+      }
+      if (lane == 0 && r0 + r < rows) {
+#pragma unroll
+        for (int p = 0; p < K; ++p) out[(r0 + r) * K + p] = acc[r][p];
+        if (tol) tol[r0 + r] = 1e-12 * fmax(1.0, amax);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// colprod partials: part[s][j][p] = sum_{i in stripe s} A[i, j] * B[i, p]
+// (A rows x cols, B rows x K).  A CTA owns a 64-column tile and one row
+// stripe; B rows of the stripe are staged in shared memory and broadcast.
+// ---------------------------------------------------------------------------
+constexpr int CP_COLS = 64;   // columns per CTA (2 per thread, 32 threads per row group)
+constexpr int CP_ROWS = 64;   // staged B rows per step
+
+template <int K, typename T>
+__global__ void __launch_bounds__(256) k_colprod_partial(const T* __restrict__ A, long rows,
+                                                         long cols, const double* __restrict__ B,
+                                                         long stripe, double* __restrict__ part) {
+  __shared__ double sb[CP_ROWS * K];
+  __shared__ double red[8][CP_COLS * K / 2 + 1];
+  const int tid = threadIdx.x;
+  const int cl = tid & 31;       // column pair within the tile
+  const int rg = tid >> 5;       // row group (8 groups interleave the staged rows)
+  const long j0 = (long)blockIdx.x * CP_COLS + 2 * cl;
+  const long s = blockIdx.y;
+  const long i_beg = s * stripe;
+  const long i_end = min(rows, i_beg + stripe);
+  double acc0[K], acc1[K];
+#pragma unroll
+  for (int p = 0; p < K; ++p) acc0[p] = acc1[p] = 0.0;
+  for (long ib = i_beg; ib < i_end; ib += CP_ROWS) {
+    const int nr = (int)min((long)CP_ROWS, i_end - ib);
+    __syncthreads();
+    for (int e = tid; e < nr * K; e += 256) sb[e] = B[ib * K + e];
+    __syncthreads();
+    for (int r = rg; r < nr; r += 8) {
+      const long i = ib + r;
+      double a0 = 0.0, a1 = 0.0;
+      if (j0 + 1 < cols) {
+        if ((cols & 1) == 0) {
+          const typename Vec2<T>::type a = *reinterpret_cast<const typename Vec2<T>::type*>(A + i * cols + j0);
+          a0 = (double)a.x;
+          a1 = (double)a.y;
+        } else {
+          a0 = (double)A[i * cols + j0];
+          a1 = (double)A[i * cols + j0 + 1];
+        }
+      } else if (j0 < cols) {
+        a0 = (double)A[i * cols + j0];
+      }
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        const double b = sb[r * K + p];
+        acc0[p] = fma(a0, b, acc0[p]);
+        acc1[p] = fma(a1, b, acc1[p]);
+      }
+    }
+  }
+  // reduce the 8 row groups in a fixed order
+  for (int half = 0; half < 2; ++half) {
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < K; ++p) red[rg][(cl)*K + p] = half == 0 ? acc0[p] : acc1[p];
+    __syncthreads();
+    for (int e = tid; e < 32 * K; e += 256) {
+      double v = 0.0;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) v += red[g][e];
+      const int c = e / K, p = e % K;
+      const long j = (long)blockIdx.x * CP_COLS + 2 * c + half;
+      if (j < cols) part[(s * cols + j) * K + p] = v;
+    }
+  }
+}
+
+// out[e] = scale * sum_{s < nparts} part[s][e]  (fixed order); optional per-row
+// (of width K) tolerance as in k_rowprod.
+template <int K>
+__global__ void k_sum_partials(const double* __restrict__ part, int nparts, long len,
+                               double* __restrict__ out, double* __restrict__ tol,
+                               double scale) {
+  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row * K >= len) return;
+  double amax = 0.0;
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    double v = 0.0;
+    for (int s = 0; s < nparts; ++s) v += part[(long)s * len + row * K + p];
+    v *= scale;
+    out[row * K + p] = v;
+    amax = fmax(amax, fabs(v));
+  }
+  if (tol) tol[row] = 1e-12 * fmax(1.0, amax);
+}
+
+// ---------------------------------------------------------------------------
+// squared norms of rows and columns of M (btb; computed once per problem)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_row_sqnorm(const T* __restrict__ A, long rows, long cols,
+                             double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long nwarps = ((long)gridDim.x * blockDim.x) >> 5;
+  for (long i = warp; i < rows; i += nwarps) {
+    double acc = 0.0;
+    for (long j = lane; j < cols; j += 32) {
+      const double a = (double)A[i * cols + j];
+      acc = fma(a, a, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) out[i] = acc;
+  }
+}
+
+template <typename T>
+__global__ void k_col_sqnorm_partial(const T* __restrict__ A, long rows, long cols, long stripe,
+                                     double* __restrict__ part) {
+  const long j = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long s = blockIdx.y;
+  if (j >= cols) return;
+  const long i_end = min(rows, (s + 1) * stripe);
+  double acc = 0.0;
+  for (long i = s * stripe; i < i_end; ++i) {
+    const double a = (double)A[i * cols + j];
+    acc = fma(a, a, acc);
+  }
+  part[s * cols + j] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// fixed-tree sums of several dot products in one pass (stage-1 statistics)
+//   sums[0] = ||Xn - X||^2 + ||Yn - Y||^2, sums[1] = ||X||^2 + ||Y||^2,
+//   sums[2] = sum resid2   (all partials per CTA, then one CTA finishes)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_stage1_stats_partial(
+    const double* __restrict__ Xo, const double* __restrict__ Xn, long nx,
+    const double* __restrict__ Yo, const double* __restrict__ Yn, long ny,
+    const double* __restrict__ r2, long nr, double* __restrict__ part) {
+  __shared__ double sh[32];
+  double a = 0.0, b = 0.0, c = 0.0;
+  const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long nt = (long)gridDim.x * blockDim.x;
+  for (long e = tid; e < nx; e += nt) {
+    const double d = Xn[e] - Xo[e];
+    a = fma(d, d, a);
+    b = fma(Xo[e], Xo[e], b);
+  }
+  for (long e = tid; e < ny; e += nt) {
+    const double d = Yn[e] - Yo[e];
+    a = fma(d, d, a);
+    b = fma(Yo[e], Yo[e], b);
+  }
+  for (long e = tid; e < nr; e += nt) c += r2[e];
+  a = block_sum(a, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * 3 + 0] = a;
+  b = block_sum(b, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * 3 + 1] = b;
+  c = block_sum(c, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * 3 + 2] = c;
+}
+
+// one CTA: out[q] = sum_b part[b * nq + q] in a fixed tree
+__global__ void __launch_bounds__(256) k_finish_sums(const double* __restrict__ part, int nblocks,
+                                                     int nq, double* __restrict__ out) {
+  __shared__ double sh[32];
+  for (int q = 0; q < nq; ++q) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) v += part[(long)b * nq + q];
+    v = block_sum(v, sh);
+    if (threadIdx.x == 0) out[q] = v;
+  }
+}
+
+__global__ void k_first_nonzero_i8(const int8_t* __restrict__ st, long len, int* __restrict__ out) {
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += (long)gridDim.x * blockDim.x)
+    if (st[e] != 0) atomicMin(out, (int)e);
+}
+
+constexpr int ROWPROD_R = 2;
+
+template <int K, typename T>
+int launch_rowprod(const T* A, long rows, long cols, const double* B, double* out, double* tol,
+                   double scale, cudaStream_t st) {
+  const long warps = (rows + ROWPROD_R - 1) / ROWPROD_R;
+  const int blocks = nmfb_blocks(warps * 32, 256, 148 * 16);
+  k_rowprod<K, ROWPROD_R, T><<<blocks, 256, 0, st>>>(A, rows, cols, B, out, tol, scale);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+long colprod_stripe(long rows, long cols) {
+  // enough CTAs to cover the SMs several times, stripes of >= 256 rows
+  const long col_tiles = (cols + CP_COLS - 1) / CP_COLS;
+  long want = (148 * 8 + col_tiles - 1) / col_tiles;
+  long stripe = (rows + want - 1) / want;
+  if (stripe < 256) stripe = 256;
+  return stripe;
+}
+
+template <int K, typename T>
+int launch_colprod(const T* A, long rows, long cols, const double* B, double* out, double* tol,
+                   double scale, double* work, long work_len, cudaStream_t st) {
+  if (rows == 0) {
+    cudaMemsetAsync(out, 0, sizeof(double) * cols * K, st);
+    return NMFB_OK;
+  }
+  const long stripe = colprod_stripe(rows, cols);
+  const long ns = (rows + stripe - 1) / stripe;
+  if (ns * cols * K > work_len) return NMFB_ENOMEM;
+  dim3 grid((unsigned)((cols + CP_COLS - 1) / CP_COLS), (unsigned)ns);
+  k_colprod_partial<K, T><<<grid, 256, 0, st>>>(A, rows, cols, B, stripe, work);
+  k_sum_partials<K><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(work, (int)ns, cols * K, out,
+                                                                   tol, scale);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+}  // namespace
+
+#define NMFB_K_SWITCH(k, MACRO) \
+  switch (k) {                  \
+    MACRO(1) MACRO(2) MACRO(3) MACRO(4) MACRO(5) MACRO(6) MACRO(7) MACRO(8) MACRO(9) MACRO(10) \
+    MACRO(11) MACRO(12) MACRO(13) MACRO(14) MACRO(15) MACRO(16) \
+    default: return NMFB_EINVAL; \
+  }
+
+extern "C" long nmfb_colprod_work_len(long rows, long cols, long k) {
+  if (rows <= 0) return 1;
+  const long stripe = colprod_stripe(rows, cols);
+  return ((rows + stripe - 1) / stripe) * cols * k;
+}
+
+extern "C" int nmfb_rowprod(const void* A, int a_is_f32, long rows, long cols, const double* B,
+                            long k, double* out, double* tol, double scale, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rows < 0 || cols < 0) return NMFB_EINVAL;
+  if (rows == 0) return NMFB_OK;
+#define CASE(KK)                                                                               \
+  case KK:                                                                                     \
+    return a_is_f32 ? launch_rowprod<KK, float>((const float*)A, rows, cols, B, out, tol, scale, \
+                                                st)                                            \
+                    : launch_rowprod<KK, double>((const double*)A, rows, cols, B, out, tol,    \
+                                                 scale, st);
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+}
+
+extern "C" int nmfb_colprod(const void* A, int a_is_f32, long rows, long cols, const double* B,
+                            long k, double* out, double* tol, double scale, double* work,
+                            long work_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rows < 0 || cols < 0) return NMFB_EINVAL;
+  if (cols == 0) return NMFB_OK;
+#define CASE(KK)                                                                                \
+  case KK:                                                                                      \
+    return a_is_f32 ? launch_colprod<KK, float>((const float*)A, rows, cols, B, out, tol, scale, \
+                                                work, work_len, st)                             \
+                    : launch_colprod<KK, double>((const double*)A, rows, cols, B, out, tol,     \
+                                                 scale, work, work_len, st);
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+}
+
+extern "C" int nmfb_sqnorms(const void* A, int a_is_f32, long rows, long cols, double* row_out,
+                            double* col_out, double* work, long work_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rows <= 0 || cols <= 0) return NMFB_EINVAL;
+  const int blocks = nmfb_blocks(rows * 32, 256, 148 * 16);
+  const long stripe = colprod_stripe(rows, cols);
+  const long ns = (rows + stripe - 1) / stripe;
+  if (ns * cols > work_len) return NMFB_ENOMEM;
+  dim3 grid((unsigned)((cols + 127) / 128), (unsigned)ns);
+  if (a_is_f32) {
+    k_row_sqnorm<float><<<blocks, 256, 0, st>>>((const float*)A, rows, cols, row_out);
+    k_col_sqnorm_partial<float><<<grid, 128, 0, st>>>((const float*)A, rows, cols, stripe, work);
+  } else {
+    k_row_sqnorm<double><<<blocks, 256, 0, st>>>((const double*)A, rows, cols, row_out);
+    k_col_sqnorm_partial<double><<<grid, 128, 0, st>>>((const double*)A, rows, cols, stripe, work);
+  }
+  k_sum_partials<1><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(work, (int)ns, cols, col_out,
+                                                                   nullptr, 1.0);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// stats[0] = ||dX||^2 + ||dY||^2, stats[1] = ||X_old||^2 + ||Y_old||^2, stats[2] = sum r2
+extern "C" int nmfb_stage1_stats(const double* Xo, const double* Xn, long nx, const double* Yo,
+                                 const double* Yn, long ny, const double* r2, long nr,
+                                 double* stats, double* work, long work_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int blocks = 296;
+  if (work_len < blocks * 3) return NMFB_ENOMEM;
+  k_stage1_stats_partial<<<blocks, 256, 0, st>>>(Xo, Xn, nx, Yo, Yn, ny, r2, nr, work);
+  k_finish_sums<<<1, 256, 0, st>>>(work, blocks, 3, stats);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// *out = first index with st != 0 (0x7F7F7F7F when none); out is set, not accumulated
+extern "C" int nmfb_first_nonzero_i8(const int8_t* st, long len, int* out, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemsetAsync(out, 0x7F, sizeof(int), s);
+  if (len <= 0) return NMFB_OK;
+  k_first_nonzero_i8<<<nmfb_blocks(len, 256, 148 * 4), 256, 0, s>>>(st, len, out);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}

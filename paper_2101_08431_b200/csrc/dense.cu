@@ -1,0 +1,298 @@
+// Dense SPD factor/solve of the mk x mk reduced (Schur) system
+// spd_solve / PAPER.md:517-527 (Eq. 12).  Right-looking blocked Cholesky,
+// lower, in place, row-major (lda = N), fp64:
+//
+//   for each 64-wide panel:  potrf of the diagonal tile in shared memory
+//                            trsm of the tiles below (one CTA per 64 rows)
+//                            syrk/gemm of the trailing lower triangle
+//                            (64x64 tiles, 4x4 register micro-tiles)
+//
+// A non-positive pivot stores its global column in *info (first one wins,
+// later kernels exit early); the host maps it to NotPositiveDefinite /
+// SchurNotPositiveDefinite.  No pivoting, no silent regularisation.
+// Triangular solves: a single-CTA blocked solver for small N, multi-CTA
+// (diagonal solve + GEMV sweep) for large N.
+#include "common.cuh"
+#include "nmfb200.h"
+
+namespace {
+
+constexpr int NB = 64;
+
+__global__ void __launch_bounds__(256) k_potrf_tile(double* __restrict__ A, long N, long k0,
+                                                   int nb, int* __restrict__ info) {
+  if (*info >= 0) return;
+  __shared__ double t[NB][NB + 1];
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < nb * nb; e += 256) {
+    const int r = e / nb, c = e % nb;
+    t[r][c] = (c <= r) ? A[(k0 + r) * N + k0 + c] : 0.0;
+  }
+  if (tid == 0) bad = -1;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    if (tid == 0) {
+      const double d = t[j][j];
+      if (!(d > 0.0)) {
+        bad = j;
+      } else {
+        t[j][j] = sqrt(d);
+      }
+    }
+    __syncthreads();
+    if (bad >= 0) break;
+    const double djj = t[j][j];
+    for (int r = j + 1 + tid; r < nb; r += 256) t[r][j] /= djj;
+    __syncthreads();
+    // trailing update of the tile: t[r][c] -= t[r][j] * t[c][j], j < c <= r
+    for (int e = tid; e < (nb - j - 1) * (nb - j - 1); e += 256) {
+      const int r = j + 1 + e / (nb - j - 1), c = j + 1 + e % (nb - j - 1);
+      if (c <= r) t[r][c] -= t[r][j] * t[c][j];
+    }
+    __syncthreads();
+  }
+  if (bad >= 0) {
+    if (tid == 0) atomicCAS(info, -1, (int)(k0 + bad));
+    return;
+  }
+  for (int e = tid; e < nb * nb; e += 256) {
+    const int r = e / nb, c = e % nb;
+    if (c <= r) A[(k0 + r) * N + k0 + c] = t[r][c];
+  }
+}
+
+// rows [k0+nb, N) of the panel: L21 = A21 * L11^{-T}; one CTA per 64 rows
+__global__ void __launch_bounds__(256) k_trsm_panel(double* __restrict__ A, long N, long k0,
+                                                    int nb, const int* __restrict__ info) {
+  if (*info >= 0) return;
+  extern __shared__ double dsm[];
+  double(*l11)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
+  double(*x)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
+  const int tid = threadIdx.x;
+  const long r0 = k0 + nb + (long)blockIdx.x * NB;
+  const int nr = (int)min((long)NB, N - r0);
+  for (int e = tid; e < nb * nb; e += 256) {
+    const int r = e / nb, c = e % nb;
+    l11[r][c] = (c <= r) ? A[(k0 + r) * N + k0 + c] : 0.0;
+  }
+  for (int e = tid; e < nr * nb; e += 256) {
+    const int r = e / nb, c = e % nb;
+    x[r][c] = A[(r0 + r) * N + k0 + c];
+  }
+  __syncthreads();
+  // column-oriented forward substitution on every row at once: x L11^T = a
+  for (int j = 0; j < nb; ++j) {
+    const double d = l11[j][j];
+    for (int r = tid; r < nr; r += 256) x[r][j] /= d;
+    __syncthreads();
+    for (int e = tid; e < nr * (nb - j - 1); e += 256) {
+      const int r = e / (nb - j - 1), c = j + 1 + e % (nb - j - 1);
+      x[r][c] -= x[r][j] * l11[c][j];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nr * nb; e += 256) {
+    const int r = e / nb, c = e % nb;
+    A[(r0 + r) * N + k0 + c] = x[r][c];
+  }
+}
+
+// trailing lower triangle: A[i, j] -= sum_p L[i, k0+p] L[j, k0+p] for tiles bi >= bj
+__global__ void __launch_bounds__(256) k_syrk_trailing(double* __restrict__ A, long N, long k0,
+                                                       int nb, const int* __restrict__ info) {
+  if (*info >= 0) return;
+  extern __shared__ double dsm[];
+  double(*li)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm);
+  double(*lj)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(dsm + NB * (NB + 1));
+  // map linear block id -> (bi, bj), bi >= bj, over the trailing tiles
+  const long t = blockIdx.x;
+  long bi = (long)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while (bi * (bi + 1) / 2 > t) --bi;
+  while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+  const long bj = t - bi * (bi + 1) / 2;
+  const long base = k0 + nb;
+  const long i0 = base + bi * NB, j0 = base + bj * NB;
+  const int ni = (int)min((long)NB, N - i0), nj = (int)min((long)NB, N - j0);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < NB * nb; e += 256) {
+    const int r = e / nb, c = e % nb;
+    li[r][c] = r < ni ? A[(i0 + r) * N + k0 + c] : 0.0;
+    lj[r][c] = r < nj ? A[(j0 + r) * N + k0 + c] : 0.0;
+  }
+  __syncthreads();
+  const int tr = (tid >> 4) * 4, tc = (tid & 15) * 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int p = 0; p < nb; ++p) {
+    double va[4], vb[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      va[a] = li[tr + a][p];
+      vb[a] = lj[tc + a][p];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma(va[a], vb[b], acc[a][b]);
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = tr + a, c = tc + b;
+      if (r < ni && c < nj && (i0 + r) >= (j0 + c)) A[(i0 + r) * N + j0 + c] -= acc[a][b];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// triangular solves with the factor (lower, row-major): forward L z = b,
+// backward L^T x = z, in place on b.  Single-CTA blocked variant.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_trsv_single(const double* __restrict__ L, long N,
+                                                      double* __restrict__ b, int trans) {
+  __shared__ double zb[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nw = blockDim.x >> 5;
+  const long nblk = (N + 31) / 32;
+  for (long bb = 0; bb < nblk; ++bb) {
+    const long blk = trans ? (nblk - 1 - bb) : bb;
+    const long c0 = blk * 32;
+    const int nc = (int)min(32L, N - c0);
+    // 1) warp 0 solves the 32x32 diagonal block
+    if (wid == 0) {
+      double v = lane < nc ? b[c0 + lane] : 0.0;
+      if (!trans) {
+        for (int j = 0; j < nc; ++j) {
+          const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * N + c0 + j];
+          if (lane == j) v = zj;
+          if (lane > j && lane < nc) v -= L[(c0 + lane) * N + c0 + j] * zj;
+        }
+      } else {
+        for (int j = nc - 1; j >= 0; --j) {
+          const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * N + c0 + j];
+          if (lane == j) v = zj;
+          if (lane < j) v -= L[(c0 + j) * N + c0 + lane] * zj;
+        }
+      }
+      if (lane < nc) {
+        b[c0 + lane] = v;
+        zb[lane] = v;
+      }
+    }
+    __syncthreads();
+    // 2) every warp updates the remaining rows
+    if (!trans) {
+      for (long r = c0 + nc + wid; r < N; r += nw) {
+        double s = lane < nc ? L[r * N + c0 + lane] * zb[lane] : 0.0;
+        s = warp_sum(s);
+        if (lane == 0) b[r] -= s;
+      }
+    } else {
+      // b[c] -= sum_{r in blk} L[r, c] z[r] for c < c0
+      for (long c = tid; c < c0; c += blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < nc; ++r) s = fma(L[(c0 + r) * N + c], zb[r], s);
+        b[c] -= s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// multi-CTA pieces for large N
+__global__ void k_trsv_diag(const double* __restrict__ L, long N, double* __restrict__ b, long c0,
+                            int nc, int trans) {
+  const int lane = threadIdx.x;
+  double v = lane < nc ? b[c0 + lane] : 0.0;
+  if (!trans) {
+    for (int j = 0; j < nc; ++j) {
+      const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * N + c0 + j];
+      if (lane == j) v = zj;
+      if (lane > j && lane < nc) v -= L[(c0 + lane) * N + c0 + j] * zj;
+    }
+  } else {
+    for (int j = nc - 1; j >= 0; --j) {
+      const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * N + c0 + j];
+      if (lane == j) v = zj;
+      if (lane < j) v -= L[(c0 + j) * N + c0 + lane] * zj;
+    }
+  }
+  if (lane < nc) b[c0 + lane] = v;
+}
+
+__global__ void k_trsv_update(const double* __restrict__ L, long N, double* __restrict__ b,
+                              long c0, int nc, int trans) {
+  const int lane = threadIdx.x & 31;
+  if (!trans) {
+    const long r = c0 + nc + (((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (r >= N) return;
+    double s = lane < nc ? L[r * N + c0 + lane] * b[c0 + lane] : 0.0;
+    s = warp_sum(s);
+    if (lane == 0) b[r] -= s;
+  } else {
+    const long c = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= c0) return;
+    double s = 0.0;
+    for (int r = 0; r < nc; ++r) s = fma(L[(c0 + r) * N + c], b[c0 + r], s);
+    b[c] -= s;
+  }
+}
+
+}  // namespace
+
+constexpr size_t kTwoTiles = 2 * NB * (NB + 1) * sizeof(double);
+
+extern "C" int nmfb_dense_cholesky(double* A, long N, int* info, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (N <= 0) return NMFB_EINVAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_trsm_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTwoTiles);
+    cudaFuncSetAttribute(k_syrk_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kTwoTiles);
+    attr = true;
+  }
+  cudaMemsetAsync(info, 0xFF, sizeof(int), st);  // -1: no failing pivot
+  for (long k0 = 0; k0 < N; k0 += NB) {
+    const int nb = (int)min((long)NB, N - k0);
+    k_potrf_tile<<<1, 256, 0, st>>>(A, N, k0, nb, info);
+    const long rest = N - k0 - nb;
+    if (rest > 0) {
+      const long tiles = (rest + NB - 1) / NB;
+      k_trsm_panel<<<(unsigned)tiles, 256, kTwoTiles, st>>>(A, N, k0, nb, info);
+      k_syrk_trailing<<<(unsigned)(tiles * (tiles + 1) / 2), 256, kTwoTiles, st>>>(A, N, k0, nb, info);
+    }
+  }
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// in-place solve (L L^T) x = b using the factor from nmfb_dense_cholesky
+extern "C" int nmfb_dense_solve(const double* L, long N, double* b, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (N <= 0) return NMFB_EINVAL;
+  if (N <= 4096) {
+    k_trsv_single<<<1, 1024, 0, st>>>(L, N, b, 0);
+    k_trsv_single<<<1, 1024, 0, st>>>(L, N, b, 1);
+  } else {
+    for (long c0 = 0; c0 < N; c0 += 32) {
+      const int nc = (int)min(32L, N - c0);
+      k_trsv_diag<<<1, 32, 0, st>>>(L, N, b, c0, nc, 0);
+      const long rest = N - c0 - nc;
+      if (rest > 0) k_trsv_update<<<(unsigned)((rest * 32 + 255) / 256), 256, 0, st>>>(L, N, b, c0, nc, 0);
+    }
+    const long nblk = (N + 31) / 32;
+    for (long bb = nblk - 1; bb >= 0; --bb) {
+      const long c0 = bb * 32;
+      const int nc = (int)min(32L, N - c0);
+      k_trsv_diag<<<1, 32, 0, st>>>(L, N, b, c0, nc, 1);
+      if (c0 > 0) k_trsv_update<<<(unsigned)((c0 + 255) / 256), 256, 0, st>>>(L, N, b, c0, nc, 1);
+    }
+  }
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}

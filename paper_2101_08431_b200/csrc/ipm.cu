@@ -1,0 +1,1069 @@
+// Stage-2 (interior point) production kernels, SPEC.md:244-374 / PAPER
+// Algorithm 2 and Eqs. 3-13.  Layouts: X, R, graX (n,k); Yt = Y^T, S, graY
+// (m,k) (y = vec(Y) is Yt row-major); M, F (n,m) row-major; L (n,k,k);
+// the reduced system A (mk,mk) row-major, index (j,p) = j*k + p.
+//
+// Key B200-first restructuring of the Schur reduction (PAPER.md:526 prices
+// it at O(n m^2 k^2) and the reference kernel loops exactly that way,
+// _kernels_numba.py:83-106):  with A_i = R1_i^{-1},
+//
+//   S_GN block (j,l) = sum_i (y_j^T A_i y_l) x_i x_i^T
+//                    = sum_{a,b} y_ja y_lb Z_ab,   Z_ab = sum_i A_i[a,b] x_i x_i^T
+//
+// so the n-contraction collapses to ONE small reduction Z (k^2 x k^2, O(n k^4))
+// followed by an O(m^2 k^3) expansion that streams A to HBM once.  The same
+// identity gives r_acc_j = H y_j with H = sum_i x_i (L_i^{-T} h_i)^T and the
+// back-substitution q_i = L_i^{-1} (sum_j y_j dy_j^T) x_i.  The full-Hessian
+// extra terms use W = F^T P (m x k^3 GEMM) and a residual-weighted SYRK.
+#include "common.cuh"
+#include "nmfb200.h"
+
+namespace {
+
+constexpr int KK_MAX = NMFB_MAX_K * (NMFB_MAX_K + 1) / 2;
+
+__device__ __forceinline__ int pk(int a, int b, int k) {
+  // packed index of (a, b), a <= b, row-major upper triangle
+  return a * k - a * (a - 1) / 2 + (b - a);
+}
+
+// ---------------------------------------------------------------------------
+// F = X Y - M, graX = F Y^T, fsq = ||F||^2 (partials per CTA)
+// ---------------------------------------------------------------------------
+template <int K, int R, typename T>
+__global__ void __launch_bounds__(256) k_residual_rows(const T* __restrict__ M, long n, long m,
+                                                       const double* __restrict__ X,
+                                                       const double* __restrict__ Yt,
+                                                       double* __restrict__ F,
+                                                       double* __restrict__ gX,
+                                                       double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31;
+  const long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long nwarps = ((long)gridDim.x * blockDim.x) >> 5;
+  double fsq = 0.0;
+  for (long r0 = warp * R; r0 < n; r0 += nwarps * R) {
+    double x[R][K], g[R][K];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        x[r][p] = (r0 + r < n) ? X[(r0 + r) * K + p] : 0.0;
+        g[r][p] = 0.0;
+      }
+    for (long j = lane; j < m; j += 32) {
+      double y[K];
+#pragma unroll
+      for (int p = 0; p < K; ++p) y[p] = __ldg(Yt + j * K + p);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r0 + r < n) {
+          double f = -(double)M[(r0 + r) * m + j];
+#pragma unroll
+          for (int p = 0; p < K; ++p) f = fma(x[r][p], y[p], f);
+          F[(r0 + r) * m + j] = f;
+          fsq = fma(f, f, fsq);
+#pragma unroll
+          for (int p = 0; p < K; ++p) g[r][p] = fma(f, y[p], g[r][p]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        const double v = warp_sum(g[r][p]);
+        if (lane == 0 && r0 + r < n) gX[(r0 + r) * K + p] = v;
+      }
+  }
+  fsq = block_sum(fsq, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = fsq;
+}
+
+// ---------------------------------------------------------------------------
+// per-row small linear algebra (thread per row i)
+// ---------------------------------------------------------------------------
+template <int K>
+__device__ __forceinline__ bool chol_row(double (&L)[K][K]) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double s = L[j][j];
+#pragma unroll
+    for (int p = 0; p < j; ++p) s -= L[j][p] * L[j][p];
+    if (!(s > 0.0)) return false;
+    const double d = sqrt(s);
+    L[j][j] = d;
+#pragma unroll
+    for (int i = j + 1; i < K; ++i) {
+      double t = L[i][j];
+#pragma unroll
+      for (int p = 0; p < j; ++p) t -= L[i][p] * L[j][p];
+      L[i][j] = t / d;
+    }
+  }
+  return true;
+}
+
+template <int K>
+__device__ __forceinline__ void fwd_row(const double (&L)[K][K], const double* b, double* z) {
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    double s = b[i];
+#pragma unroll
+    for (int p = 0; p < i; ++p) s -= L[i][p] * z[p];
+    z[i] = s / L[i][i];
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void bwd_row(const double (&L)[K][K], const double* b, double* z) {
+#pragma unroll
+  for (int i = K - 1; i >= 0; --i) {
+    double s = b[i];
+#pragma unroll
+    for (int p = i + 1; p < K; ++p) s -= L[p][i] * z[p];
+    z[i] = s / L[i][i];
+  }
+}
+
+// R1_i = YY^T + rho I + diag(r_i / x_i) = L_i L_i^T; h_i = L_i^{-1}(mux/x_i - graX_i);
+// g_i = L_i^{-T} h_i; Apk_i = packed R1_i^{-1}; XXpk_i = packed x_i x_i^T.
+template <int K>
+__global__ void __launch_bounds__(128) k_r1_factor(const double* __restrict__ GY,
+                                                   const double* __restrict__ X,
+                                                   const double* __restrict__ R,
+                                                   const double* __restrict__ gX, double mux,
+                                                   double rho, long n, double* __restrict__ Lout,
+                                                   double* __restrict__ h, double* __restrict__ g,
+                                                   double* __restrict__ Apk,
+                                                   double* __restrict__ XXpk,
+                                                   int* __restrict__ bad) {
+  __shared__ double gy[K * K];
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) gy[e] = GY[e];
+  __syncthreads();
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x[K], L[K][K], b[K], hv[K], gv[K];
+#pragma unroll
+  for (int p = 0; p < K; ++p) x[p] = X[i * K + p];
+#pragma unroll
+  for (int a = 0; a < K; ++a)
+#pragma unroll
+    for (int c = 0; c < K; ++c) L[a][c] = (c <= a) ? gy[a * K + c] : 0.0;
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    L[p][p] += rho + R[i * K + p] / x[p];
+    b[p] = mux / x[p] - gX[i * K + p];
+  }
+  if (!chol_row<K>(L)) {
+    atomicMin(bad, (int)i);
+    return;
+  }
+  fwd_row<K>(L, b, hv);
+  bwd_row<K>(L, hv, gv);
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    h[i * K + a] = hv[a];
+    g[i * K + a] = gv[a];
+#pragma unroll
+    for (int c = 0; c < K; ++c) Lout[(i * K + a) * K + c] = (c <= a) ? L[a][c] : 0.0;
+  }
+  // Linv = L^{-1} (lower), then R1^{-1} = Linv^T Linv
+  double Li[K][K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      if (a < c) {
+        Li[a][c] = 0.0;
+      } else {
+        double s = (a == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int p = 0; p < a; ++p)
+          if (p >= c) s -= L[a][p] * Li[p][c];
+        Li[a][c] = s / L[a][a];
+      }
+    }
+  }
+  constexpr int KKc = K * (K + 1) / 2;
+#pragma unroll
+  for (int a = 0; a < K; ++a)
+#pragma unroll
+    for (int c = a; c < K; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p < K; ++p)
+        if (p >= c) s = fma(Li[p][a], Li[p][c], s);
+      const int e = a * K - a * (a - 1) / 2 + (c - a);
+      Apk[i * KKc + e] = s;
+      XXpk[i * KKc + e] = x[a] * x[c];
+    }
+}
+
+// h = L^{-1} b1, g = L^{-T} h for a given right-hand side (predictor reuse)
+template <int K>
+__global__ void k_hg_rows(const double* __restrict__ Lin, const double* __restrict__ b1,
+                          double b1_scale, long n, double* __restrict__ h,
+                          double* __restrict__ g) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double L[K][K], b[K], hv[K], gv[K];
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    b[a] = b1_scale * b1[i * K + a];
+#pragma unroll
+    for (int c = 0; c < K; ++c) L[a][c] = Lin[(i * K + a) * K + c];
+  }
+  fwd_row<K>(L, b, hv);
+  bwd_row<K>(L, hv, gv);
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    h[i * K + a] = hv[a];
+    g[i * K + a] = gv[a];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic split-K C = A^T B:  part[s][a][b] = sum_{i in stripe s} A[i,a] B[i,b]
+// A (rows x ca), B (rows x cb) row-major fp64; 32x32 output tiles.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_atb_partial(const double* __restrict__ A, long rows,
+                                                     long ca, const double* __restrict__ B,
+                                                     long cb, long stripe,
+                                                     double* __restrict__ part) {
+  __shared__ double sa[32][33];
+  __shared__ double sb[32][33];
+  const int tid = threadIdx.x;
+  const long a0 = (long)blockIdx.x * 32, b0 = (long)blockIdx.y * 32;
+  const long s = blockIdx.z;
+  const long i_beg = s * stripe, i_end = min(rows, i_beg + stripe);
+  const int ta = tid >> 3, tb = (tid & 7) * 4;  // 32 rows of a x (8 x 4) cols of b
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (long ib = i_beg; ib < i_end; ib += 32) {
+    const int nr = (int)min(32L, i_end - ib);
+    __syncthreads();
+    for (int e = tid; e < 32 * 32; e += 256) {
+      const int r = e >> 5, c = e & 31;
+      sa[r][c] = (r < nr && a0 + c < ca) ? A[(ib + r) * ca + a0 + c] : 0.0;
+      sb[r][c] = (r < nr && b0 + c < cb) ? B[(ib + r) * cb + b0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int r = 0; r < nr; ++r) {
+      const double av = sa[r][ta];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(av, sb[r][tb + q], acc[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const long a = a0 + ta, b = b0 + tb + q;
+    if (a < ca && b < cb) part[(s * ca + a) * cb + b] = acc[q];
+  }
+}
+
+__global__ void k_sum_parts(const double* __restrict__ part, int nparts, long len,
+                            double* __restrict__ out) {
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= len) return;
+  double v = 0.0;
+  for (int s = 0; s < nparts; ++s) v += part[(long)s * len + e];
+  out[e] = v;
+}
+
+// ---------------------------------------------------------------------------
+// Schur assembly: A = blockdiag(X^T X + rho I + Diag(s_j / y_j)) - S
+// (lower block triangle j >= l written; diagonal blocks written in full)
+// S_GN(j,l)[p,q] = sum_a y_ja V_l[a][p][q],  V_l[a][p][q] = sum_b y_lb Z[a,b][p,q]
+// full: + sum_a y_ja W[l][p][q][a] + sum_a y_la W[j][q][p][a]   (term4 separate)
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(256) k_schur_assemble(
+    const double* __restrict__ Yt, const double* __restrict__ S, long m,
+    const double* __restrict__ Zpk, const double* __restrict__ XtX, double rho,
+    const double* __restrict__ W, int TL, long jchunk, double* __restrict__ A) {
+  extern __shared__ double V[];  // [TL][K][K][K]
+  constexpr int KK = K * (K + 1) / 2;
+  const long N = m * K;
+  const long l0 = (long)blockIdx.x * TL;
+  const int ntl = (int)min((long)TL, m - l0);
+  const int tid = threadIdx.x;
+  // V for the tile's columns l
+  for (int e = tid; e < ntl * K * K * K; e += blockDim.x) {
+    const int tl = e / (K * K * K);
+    const int rem = e % (K * K * K);
+    const int a = rem / (K * K), p = (rem / K) % K, q = rem % K;
+    const long l = l0 + tl;
+    double v = 0.0;
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+      const int ab = a <= b ? pk(a, b, K) : pk(b, a, K);
+      const int pq = p <= q ? pk(p, q, K) : pk(q, p, K);
+      v = fma(Yt[l * K + b], Zpk[ab * KK + pq], v);
+    }
+    V[e] = v;
+  }
+  __syncthreads();
+  const long j_beg = max(l0, (long)blockIdx.y * jchunk);
+  const long j_end = min(m, ((long)blockIdx.y + 1) * jchunk);
+  // each j contributes K rows (p) x ntl*K columns (tl, q)
+  const int per_j = K * ntl * K;
+  for (long e = tid; e < (j_end > j_beg ? (j_end - j_beg) : 0) * per_j; e += blockDim.x) {
+    const long j = j_beg + e / per_j;
+    const int rem = (int)(e % per_j);
+    const int p = rem / (ntl * K);
+    const int tl = (rem / K) % ntl;
+    const int q = rem % K;
+    const long l = l0 + tl;
+    if (j < l) continue;
+    double sv = 0.0;
+    const double* Vl = V + (long)tl * K * K * K;
+#pragma unroll
+    for (int a = 0; a < K; ++a) sv = fma(Yt[j * K + a], Vl[(a * K + p) * K + q], sv);
+    if (W) {
+      const double* Wl = W + l * K * K * K;
+      const double* Wj = W + j * K * K * K;
+#pragma unroll
+      for (int a = 0; a < K; ++a) {
+        sv = fma(Yt[j * K + a], Wl[(p * K + q) * K + a], sv);
+        sv = fma(Yt[l * K + a], Wj[(q * K + p) * K + a], sv);
+      }
+    }
+    double v = -sv;
+    if (j == l) {
+      v += XtX[p * K + q];
+      if (p == q) v += rho + S[j * K + p] / Yt[j * K + p];
+    }
+    A[(j * K + p) * N + l * K + q] = v;
+  }
+}
+
+// full Hessian term 4: A[(j,p),(l,q)] -= sum_i f_ij f_il Ainv_i[p,q], j >= l
+template <int K>
+__global__ void __launch_bounds__(256) k_schur_term4(const double* __restrict__ F, long n, long m,
+                                                     const double* __restrict__ Apk,
+                                                     double* __restrict__ A) {
+  constexpr int KK = K * (K + 1) / 2;
+  constexpr int PQC = 16;
+  __shared__ double fj[32][16], fl[32][16], ap[32][PQC];
+  const long tj = blockIdx.x, tl = blockIdx.y;
+  if (tj < tl) return;
+  const int pq0 = blockIdx.z * PQC;
+  const int npq = min(PQC, KK - pq0);
+  const int tid = threadIdx.x, jj = tid >> 4, ll = tid & 15;
+  const long j = tj * 16 + jj, l = tl * 16 + ll;
+  double acc[PQC];
+#pragma unroll
+  for (int c = 0; c < PQC; ++c) acc[c] = 0.0;
+  for (long ib = 0; ib < n; ib += 32) {
+    const int nr = (int)min(32L, n - ib);
+    __syncthreads();
+    for (int e = tid; e < 32 * 16; e += 256) {
+      const int r = e >> 4, c = e & 15;
+      const long jc = tj * 16 + c, lc = tl * 16 + c;
+      fj[r][c] = (r < nr && jc < m) ? F[(ib + r) * m + jc] : 0.0;
+      fl[r][c] = (r < nr && lc < m) ? F[(ib + r) * m + lc] : 0.0;
+      ap[r][c] = (r < nr && c < npq) ? Apk[(ib + r) * KK + pq0 + c] : 0.0;
+    }
+    __syncthreads();
+    for (int r = 0; r < nr; ++r) {
+      const double w = fj[r][jj] * fl[r][ll];
+#pragma unroll
+      for (int c = 0; c < PQC; ++c) acc[c] = fma(w, ap[r][c], acc[c]);
+    }
+  }
+  if (j >= m || l >= m || j < l) return;
+  const long N = m * K;
+  for (int c = 0; c < npq; ++c) {
+    // unpack pq0 + c -> (p, q), p <= q
+    int e = pq0 + c, p = 0;
+    while (e >= K - p) {
+      e -= K - p;
+      ++p;
+    }
+    const int q = p + e;
+    A[(j * K + p) * N + l * K + q] -= acc[c];
+    if (p != q) A[(j * K + q) * N + l * K + p] -= acc[c];
+  }
+}
+
+// P[i][(p,q,a)] = x_ip * Ainv_i[q,a]   (n x K^3, for W = F^T P)
+template <int K>
+__global__ void k_make_p(const double* __restrict__ X, const double* __restrict__ Apk, long n,
+                         double* __restrict__ P) {
+  constexpr int KK = K * (K + 1) / 2;
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * K * K * K) return;
+  const long i = e / (K * K * K);
+  const int rem = (int)(e % (K * K * K));
+  const int p = rem / (K * K), q = (rem / K) % K, a = rem % K;
+  const int qa = q <= a ? pk(q, a, K) : pk(a, q, K);
+  P[e] = X[i * K + p] * Apk[i * KK + qa];
+}
+
+// rhs of the reduced system: muy/y - graY - H y_j - [full] (F^T g)_j
+template <int K>
+__global__ void k_schur_rhs(const double* __restrict__ Yt, const double* __restrict__ gY,
+                            const double* __restrict__ H, const double* __restrict__ FtG,
+                            double muy, long m, double* __restrict__ rhs) {
+  const long j = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    double v = muy / Yt[j * K + p] - gY[j * K + p];
+    double ra = 0.0;
+#pragma unroll
+    for (int a = 0; a < K; ++a) ra = fma(H[p * K + a], Yt[j * K + a], ra);
+    if (FtG) ra += FtG[j * K + p];
+    rhs[j * K + p] = v - ra;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// back-substitution + dual directions + partial reductions (thread per row)
+//   q_i = L_i^{-1}(Gdy x_i + [full] (F dY)_i), dx_i = L_i^{-T}(h_i - q_i)
+//   dr = mux/x - r - (r/x) dx
+// partials per CTA: [gtp, a1min, a2min]
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(128) k_dir_rows(const double* __restrict__ Lin,
+                                                  const double* __restrict__ Xf,
+                                                  const double* __restrict__ h,
+                                                  const double* __restrict__ Gdy,
+                                                  const double* __restrict__ FdY,
+                                                  const double* __restrict__ X,
+                                                  const double* __restrict__ R,
+                                                  const double* __restrict__ gX, double mux,
+                                                  double tau, long n, double* __restrict__ dX,
+                                                  double* __restrict__ dR,
+                                                  double* __restrict__ part) {
+  __shared__ double gd[K * K];
+  __shared__ double sh[32];
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) gd[e] = Gdy[e];
+  __syncthreads();
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  double gtp = 0.0, a1 = 1.0 / 0.0, a2 = 1.0 / 0.0;
+  if (i < n) {
+    double L[K][K], v[K], q[K], t[K], dx[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a)
+#pragma unroll
+      for (int c = 0; c < K; ++c) L[a][c] = Lin[(i * K + a) * K + c];
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      double s = FdY ? FdY[i * K + a] : 0.0;
+#pragma unroll
+      for (int b = 0; b < K; ++b) s = fma(gd[a * K + b], Xf[i * K + b], s);
+      v[a] = s;
+    }
+    fwd_row<K>(L, v, q);
+#pragma unroll
+    for (int a = 0; a < K; ++a) t[a] = h[i * K + a] - q[a];
+    bwd_row<K>(L, t, dx);
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      const double x = X[i * K + a], r = R[i * K + a];
+      const double d = dx[a];
+      const double dr = mux / x - r - (r / x) * d;
+      dX[i * K + a] = d;
+      dR[i * K + a] = dr;
+      gtp = fma(d, gX[i * K + a] - mux / x, gtp);
+      if (d < 0.0) a1 = fmin(a1, -tau * x / d);
+      if (dr < 0.0) a2 = fmin(a2, -tau * r / dr);
+    }
+  }
+  gtp = block_sum(gtp, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * 3 + 0] = gtp;
+  __syncthreads();
+  a1 = -block_max(-a1, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * 3 + 1] = a1;
+  __syncthreads();
+  a2 = -block_max(-a2, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * 3 + 2] = a2;
+}
+
+// Y side: ds = muy/y - s - (s/y) dy (dy already solved); partials [gtp, a1min, a2min]
+__global__ void __launch_bounds__(256) k_dir_cols(const double* __restrict__ Yt,
+                                                  const double* __restrict__ S,
+                                                  const double* __restrict__ gY,
+                                                  const double* __restrict__ dY, double muy,
+                                                  double tau, long len,
+                                                  double* __restrict__ dS,
+                                                  double* __restrict__ part) {
+  __shared__ double sh[32];
+  double gtp = 0.0, a1 = 1.0 / 0.0, a2 = 1.0 / 0.0;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += (long)gridDim.x * blockDim.x) {
+    const double y = Yt[e], s = S[e], d = dY[e];
+    const double ds = muy / y - s - (s / y) * d;
+    dS[e] = ds;
+    gtp = fma(d, gY[e] - muy / y, gtp);
+    if (d < 0.0) a1 = fmin(a1, -tau * y / d);
+    if (ds < 0.0) a2 = fmin(a2, -tau * s / ds);
+  }
+  gtp = block_sum(gtp, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * 3 + 0] = gtp;
+  __syncthreads();
+  a1 = -block_max(-a1, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * 3 + 1] = a1;
+  __syncthreads();
+  a2 = -block_max(-a2, sh);
+  if (threadIdx.x == 0) part[blockIdx.x * 3 + 2] = a2;
+}
+
+// out = [gtp, a1max, a2max] from row and column partials (fixed order)
+__global__ void k_finish_dir(const double* __restrict__ prow, int nrow,
+                             const double* __restrict__ pcol, int ncol,
+                             double* __restrict__ out) {
+  __shared__ double sh[32];
+  double g = 0.0, a1 = 1.0, a2 = 1.0;
+  for (int b = threadIdx.x; b < nrow; b += blockDim.x) {
+    g += prow[b * 3];
+    a1 = fmin(a1, prow[b * 3 + 1]);
+    a2 = fmin(a2, prow[b * 3 + 2]);
+  }
+  double g2 = 0.0;
+  for (int b = threadIdx.x; b < ncol; b += blockDim.x) {
+    g2 += pcol[b * 3];
+    a1 = fmin(a1, pcol[b * 3 + 1]);
+    a2 = fmin(a2, pcol[b * 3 + 2]);
+  }
+  g = block_sum(g, sh);
+  __syncthreads();
+  g2 = block_sum(g2, sh);
+  __syncthreads();
+  a1 = -block_max(-a1, sh);
+  __syncthreads();
+  a2 = -block_max(-a2, sh);
+  if (threadIdx.x == 0) {
+    out[0] = g + g2;
+    out[1] = a1;
+    out[2] = a2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Armijo: one pass over (i, j) for the six inner products of
+//   A = F, B = dX Y + X dY, C = dX dY:  [AA, AB, BB, AC, BC, CC]
+// ---------------------------------------------------------------------------
+template <int K, int R>
+__global__ void __launch_bounds__(256) k_quartic_rows(const double* __restrict__ F, long n,
+                                                      long m, const double* __restrict__ X,
+                                                      const double* __restrict__ dX,
+                                                      const double* __restrict__ Yt,
+                                                      const double* __restrict__ dYt,
+                                                      double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31;
+  const long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long nwarps = ((long)gridDim.x * blockDim.x) >> 5;
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  for (long r0 = warp * R; r0 < n; r0 += nwarps * R) {
+    double x[R][K], dx[R][K];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        x[r][p] = (r0 + r < n) ? X[(r0 + r) * K + p] : 0.0;
+        dx[r][p] = (r0 + r < n) ? dX[(r0 + r) * K + p] : 0.0;
+      }
+    for (long j = lane; j < m; j += 32) {
+      double y[K], dy[K];
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        y[p] = __ldg(Yt + j * K + p);
+        dy[p] = __ldg(dYt + j * K + p);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r0 + r < n) {
+          const double a = F[(r0 + r) * m + j];
+          double b = 0.0, c = 0.0;
+#pragma unroll
+          for (int p = 0; p < K; ++p) {
+            b = fma(dx[r][p], y[p], fma(x[r][p], dy[p], b));
+            c = fma(dx[r][p], dy[p], c);
+          }
+          s[0] = fma(a, a, s[0]);
+          s[1] = fma(a, b, s[1]);
+          s[2] = fma(b, b, s[2]);
+          s[3] = fma(a, c, s[3]);
+          s[4] = fma(b, c, s[4]);
+          s[5] = fma(c, c, s[5]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const double v = block_sum(s[q], sh);
+    if (threadIdx.x == 0) part[blockIdx.x * 6 + q] = v;
+    __syncthreads();
+  }
+}
+
+// barrier increments for every backtracking trial t (blockIdx.y):
+//   part[t][b][0] = sum log1p(alpha_t dx/x), part[t][b][1] = same over y
+__global__ void __launch_bounds__(256) k_barrier_trials(const double* __restrict__ X,
+                                                        const double* __restrict__ dX, long nx,
+                                                        const double* __restrict__ Yt,
+                                                        const double* __restrict__ dYt, long ny,
+                                                        const double* __restrict__ alpha_max,
+                                                        double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int t = blockIdx.y;
+  const double alpha = ldexp(*alpha_max, -t);
+  double sx = 0.0, sy = 0.0;
+  const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long nt = (long)gridDim.x * blockDim.x;
+  for (long e = tid; e < nx; e += nt) sx += log1p(alpha * dX[e] / X[e]);
+  for (long e = tid; e < ny; e += nt) sy += log1p(alpha * dYt[e] / Yt[e]);
+  sx = block_sum(sx, sh);
+  __syncthreads();
+  sy = block_sum(sy, sh);
+  if (threadIdx.x == 0) {
+    part[((long)t * gridDim.x + blockIdx.x) * 2 + 0] = sx;
+    part[((long)t * gridDim.x + blockIdx.x) * 2 + 1] = sy;
+  }
+}
+
+// out[t*2 + c] = sum_b part[t][b][c]
+__global__ void k_finish_trials(const double* __restrict__ part, int nb, int nt,
+                                double* __restrict__ out) {
+  __shared__ double sh[32];
+  for (int t = 0; t < nt; ++t)
+    for (int c = 0; c < 2; ++c) {
+      double v = 0.0;
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) v += part[((long)t * nb + b) * 2 + c];
+      v = block_sum(v, sh);
+      if (threadIdx.x == 0) out[t * 2 + c] = v;
+      __syncthreads();
+    }
+}
+
+// v <- v + alpha dv, entries that are not strictly positive become (1-tau) v
+__global__ void k_step_nudge(double* __restrict__ v, const double* __restrict__ dv, long len,
+                             double alpha, double tau) {
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += (long)gridDim.x * blockDim.x) {
+    const double old = v[e];
+    const double nv = old + alpha * dv[e];
+    v[e] = (nv > 0.0) ? nv : (1.0 - tau) * old;
+  }
+}
+
+// KKT sums (PAPER Eq. 9) in one pass; partial layout per CTA (12 values):
+//  sums: 0 ||gX-R||^2  1 ||x.r - mux||^2  2 ||x.r||^2  3 x^T r
+//        4 ||gY-S||^2  5 ||y.s - muy||^2  6 ||y.s||^2  7 y^T s
+//  maxes: 8 max|gX|  9 max|gY|  10 max x  11 max y
+__global__ void __launch_bounds__(256) k_kkt_partial(const double* __restrict__ X,
+                                                     const double* __restrict__ R,
+                                                     const double* __restrict__ gX, long nx,
+                                                     const double* __restrict__ Yt,
+                                                     const double* __restrict__ S,
+                                                     const double* __restrict__ gY, long ny,
+                                                     double mux, double muy,
+                                                     double* __restrict__ part) {
+  __shared__ double sh[32];
+  double v[12];
+#pragma unroll
+  for (int q = 0; q < 12; ++q) v[q] = (q < 8) ? 0.0 : -1.0 / 0.0;
+  const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long nt = (long)gridDim.x * blockDim.x;
+  if (R) {
+    for (long e = tid; e < nx; e += nt) {
+      const double x = X[e], r = R[e], g = gX[e];
+      const double xr = x * r;
+      v[0] = fma(g - r, g - r, v[0]);
+      v[1] = fma(xr - mux, xr - mux, v[1]);
+      v[2] = fma(xr, xr, v[2]);
+      v[3] += xr;
+      v[8] = fmax(v[8], fabs(g));
+      v[10] = fmax(v[10], x);
+    }
+    for (long e = tid; e < ny; e += nt) {
+      const double y = Yt[e], s = S[e], g = gY[e];
+      const double ys = y * s;
+      v[4] = fma(g - s, g - s, v[4]);
+      v[5] = fma(ys - muy, ys - muy, v[5]);
+      v[6] = fma(ys, ys, v[6]);
+      v[7] += ys;
+      v[9] = fmax(v[9], fabs(g));
+      v[11] = fmax(v[11], y);
+    }
+  } else {  // primal-only scoring: r = max(gX,0), s = max(gY,0)
+    for (long e = tid; e < nx; e += nt) {
+      const double x = X[e], g = gX[e], r = fmax(g, 0.0);
+      const double xr = x * r;
+      v[0] = fma(g - r, g - r, v[0]);
+      v[1] = fma(xr - mux, xr - mux, v[1]);
+      v[2] = fma(xr, xr, v[2]);
+      v[3] += xr;
+      v[8] = fmax(v[8], fabs(g));
+      v[10] = fmax(v[10], x);
+    }
+    for (long e = tid; e < ny; e += nt) {
+      const double y = Yt[e], g = gY[e], s = fmax(g, 0.0);
+      const double ys = y * s;
+      v[4] = fma(g - s, g - s, v[4]);
+      v[5] = fma(ys - muy, ys - muy, v[5]);
+      v[6] = fma(ys, ys, v[6]);
+      v[7] += ys;
+      v[9] = fmax(v[9], fabs(g));
+      v[11] = fmax(v[11], y);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 12; ++q) {
+    const double r = q < 8 ? block_sum(v[q], sh) : block_max(v[q], sh);
+    if (threadIdx.x == 0) part[blockIdx.x * 12 + q] = r;
+    __syncthreads();
+  }
+}
+
+__global__ void k_finish_kkt(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  __shared__ double sh[32];
+  for (int q = 0; q < 12; ++q) {
+    double v = q < 8 ? 0.0 : -1.0 / 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+      v = q < 8 ? v + part[b * 12 + q] : fmax(v, part[b * 12 + q]);
+    v = q < 8 ? block_sum(v, sh) : block_max(v, sh);
+    if (threadIdx.x == 0) out[q] = v;
+    __syncthreads();
+  }
+}
+
+// mu_aff numerator: sum (x + a1 dx)(r + a2 dr) + sum (y + a1 dy)(s + a2 ds)
+__global__ void __launch_bounds__(256) k_affine_partial(const double* __restrict__ X,
+                                                        const double* __restrict__ dX,
+                                                        const double* __restrict__ R,
+                                                        const double* __restrict__ dR, long nx,
+                                                        const double* __restrict__ Yt,
+                                                        const double* __restrict__ dY,
+                                                        const double* __restrict__ S,
+                                                        const double* __restrict__ dS, long ny,
+                                                        double a1, double a2,
+                                                        double* __restrict__ part) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long nt = (long)gridDim.x * blockDim.x;
+  for (long e = tid; e < nx; e += nt) v = fma(X[e] + a1 * dX[e], R[e] + a2 * dR[e], v);
+  for (long e = tid; e < ny; e += nt) v = fma(Yt[e] + a1 * dY[e], S[e] + a2 * dS[e], v);
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = v;
+}
+
+// out[q] = sum_b part[b * nq + q]  (fixed order)
+__global__ void k_finish_cols(const double* __restrict__ part, int nb, int nq,
+                              double* __restrict__ out) {
+  __shared__ double sh[32];
+  for (int q = 0; q < nq; ++q) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) v += part[(long)b * nq + q];
+    v = block_sum(v, sh);
+    if (threadIdx.x == 0) out[q] = v;
+    __syncthreads();
+  }
+}
+
+__global__ void k_finish_sum1(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v += part[b];
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) *out = v;
+}
+
+__global__ void k_clamp_fill(double* __restrict__ v, long len, double lo) {
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += (long)gridDim.x * blockDim.x)
+    v[e] = fmax(v[e], lo);
+}
+
+__global__ void k_fill(double* __restrict__ v, long len, double c) {
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += (long)gridDim.x * blockDim.x)
+    v[e] = c;
+}
+
+constexpr int RED_BLOCKS = 296;  // fixed -> deterministic reductions
+
+}  // namespace
+
+#define NMFB_K_SWITCH(k, MACRO) \
+  switch (k) {                  \
+    MACRO(1) MACRO(2) MACRO(3) MACRO(4) MACRO(5) MACRO(6) MACRO(7) MACRO(8) MACRO(9) MACRO(10) \
+    MACRO(11) MACRO(12) MACRO(13) MACRO(14) MACRO(15) MACRO(16) \
+    default: return NMFB_EINVAL; \
+  }
+
+extern "C" int nmfb_ipm_reduce_blocks(void) { return RED_BLOCKS; }
+
+// F = X Y - M; graX = F Y^T; out[0] = ||F||^2.  work >= RED_BLOCKS.
+extern "C" int nmfb_residual(const void* M, int m_is_f32, long n, long m, long k, const double* X,
+                             const double* Yt, double* F, double* gX, double* out, double* work,
+                             void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0 || m <= 0) return NMFB_EINVAL;
+#define CASE(KK)                                                                          \
+  case KK:                                                                                \
+    if (m_is_f32)                                                                         \
+      k_residual_rows<KK, 2, float><<<RED_BLOCKS, 256, 0, st>>>((const float*)M, n, m, X, \
+                                                                Yt, F, gX, work);         \
+    else                                                                                  \
+      k_residual_rows<KK, 2, double><<<RED_BLOCKS, 256, 0, st>>>((const double*)M, n, m,  \
+                                                                 X, Yt, F, gX, work);     \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  k_finish_sum1<<<1, 256, 0, st>>>(work, RED_BLOCKS, out);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_r1_factor(const double* GY, const double* X, const double* R,
+                              const double* gX, double mux, double rho, long n, long k,
+                              double* L, double* h, double* g, double* Apk, double* XXpk,
+                              int* bad, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0) return NMFB_EINVAL;
+  cudaMemsetAsync(bad, 0x7F, sizeof(int), st);  // 0x7F7F7F7F: no failing row
+  const int blocks = (int)((n + 127) / 128);
+#define CASE(KK)                                                                               \
+  case KK:                                                                                     \
+    k_r1_factor<KK><<<blocks, 128, 0, st>>>(GY, X, R, gX, mux, rho, n, L, h, g, Apk, XXpk, bad); \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_hg(const double* L, const double* b1, double b1_scale, long n, long k,
+                       double* h, double* g, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0) return NMFB_EINVAL;
+  const int blocks = (int)((n + 127) / 128);
+#define CASE(KK)                                                               \
+  case KK:                                                                     \
+    k_hg_rows<KK><<<blocks, 128, 0, st>>>(L, b1, b1_scale, n, h, g);           \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" long nmfb_atb_work_len(long rows, long ca, long cb) {
+  const long tiles = ((ca + 31) / 32) * ((cb + 31) / 32);
+  long ns = (148 * 4 + tiles - 1) / tiles;
+  const long max_ns = (rows + 255) / 256;
+  if (ns > max_ns) ns = max_ns;
+  if (ns < 1) ns = 1;
+  return ns * ca * cb;
+}
+
+// out (ca x cb) = A^T B; A (rows x ca), B (rows x cb)
+extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, long cb,
+                        double* out, double* work, long work_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ca <= 0 || cb <= 0) return NMFB_EINVAL;
+  if (rows <= 0) {
+    cudaMemsetAsync(out, 0, sizeof(double) * ca * cb, st);
+    return NMFB_OK;
+  }
+  const long tiles = ((ca + 31) / 32) * ((cb + 31) / 32);
+  long ns = (148 * 4 + tiles - 1) / tiles;
+  const long max_ns = (rows + 255) / 256;
+  if (ns > max_ns) ns = max_ns;
+  if (ns < 1) ns = 1;
+  const long stripe = (rows + ns - 1) / ns;
+  ns = (rows + stripe - 1) / stripe;
+  dim3 grid((unsigned)((ca + 31) / 32), (unsigned)((cb + 31) / 32), (unsigned)ns);
+  if (ns == 1) {
+    k_atb_partial<<<grid, 256, 0, st>>>(A, rows, ca, B, cb, stripe, out);
+  } else {
+    if (ns * ca * cb > work_len) return NMFB_ENOMEM;
+    k_atb_partial<<<grid, 256, 0, st>>>(A, rows, ca, B, cb, stripe, work);
+    k_sum_parts<<<(unsigned)((ca * cb + 255) / 256), 256, 0, st>>>(work, (int)ns, ca * cb, out);
+  }
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_make_p(const double* X, const double* Apk, long n, long k, double* P,
+                           void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const long total = n * k * k * k;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+#define CASE(KK)                                                 \
+  case KK:                                                       \
+    k_make_p<KK><<<blocks, 256, 0, st>>>(X, Apk, n, P);          \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// Schur matrix assembly (lower block triangle).  W may be NULL (Gauss-Newton).
+extern "C" int nmfb_schur_assemble(const double* Yt, const double* S, long m, long k,
+                                   const double* Zpk, const double* XtX, double rho,
+                                   const double* W, double* A, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m <= 0) return NMFB_EINVAL;
+  const long k3 = k * k * k;
+  int TL = (int)(4096 / k3);  // <= 32 KB of V per CTA
+  if (TL < 1) TL = 1;
+  if (TL > 64) TL = 64;
+  const size_t smem = (size_t)TL * k3 * sizeof(double);
+  const long ltiles = (m + TL - 1) / TL;
+  // split the j range so that there are enough CTAs
+  long jsplit = (148 * 8 + ltiles - 1) / ltiles;
+  if (jsplit < 1) jsplit = 1;
+  long jchunk = (m + jsplit - 1) / jsplit;
+  if (jchunk < 1) jchunk = 1;
+  jsplit = (m + jchunk - 1) / jchunk;
+  dim3 grid((unsigned)ltiles, (unsigned)jsplit);
+#define CASE(KK)                                                                              \
+  case KK:                                                                                    \
+    cudaFuncSetAttribute(k_schur_assemble<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                         (int)smem);                                                          \
+    k_schur_assemble<KK><<<grid, 256, smem, st>>>(Yt, S, m, Zpk, XtX, rho, W, TL, jchunk, A); \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_schur_term4(const double* F, long n, long m, long k, const double* Apk,
+                                double* A, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const long kk = k * (k + 1) / 2;
+  const long tiles = (m + 15) / 16;
+  dim3 grid((unsigned)tiles, (unsigned)tiles, (unsigned)((kk + 15) / 16));
+#define CASE(KK)                                                       \
+  case KK:                                                             \
+    k_schur_term4<KK><<<grid, 256, 0, st>>>(F, n, m, Apk, A);          \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_schur_rhs(const double* Yt, const double* gY, const double* H,
+                              const double* FtG, double muy, long m, long k, double* rhs,
+                              void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned blocks = (unsigned)((m + 127) / 128);
+#define CASE(KK)                                                                  \
+  case KK:                                                                        \
+    k_schur_rhs<KK><<<blocks, 128, 0, st>>>(Yt, gY, H, FtG, muy, m, rhs);        \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// dx, dr, ds from dy; out = [gtp, a1max, a2max].  work >= 3*(ceil(n/128) + RED_BLOCKS)
+extern "C" int nmfb_direction(const double* L, const double* Xf, const double* h,
+                              const double* Gdy, const double* FdY, const double* X,
+                              const double* R, const double* gX, double mux, const double* Yt,
+                              const double* S, const double* gY, const double* dY, double muy,
+                              double tau, long n, long m, long k, double* dX, double* dR,
+                              double* dS, double* out, double* work, long work_len,
+                              void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int rb = (int)((n + 127) / 128);
+  if (work_len < 3L * (rb + RED_BLOCKS)) return NMFB_ENOMEM;
+#define CASE(KK)                                                                              \
+  case KK:                                                                                    \
+    k_dir_rows<KK><<<rb, 128, 0, st>>>(L, Xf, h, Gdy, FdY, X, R, gX, mux, tau, n, dX, dR, work); \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  k_dir_cols<<<RED_BLOCKS, 256, 0, st>>>(Yt, S, gY, dY, muy, tau, m * k, dS, work + 3 * rb);
+  k_finish_dir<<<1, 256, 0, st>>>(work, rb, work + 3 * rb, RED_BLOCKS, out);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// out[0..5] = [AA, AB, BB, AC, BC, CC]
+extern "C" int nmfb_quartic(const double* F, long n, long m, long k, const double* X,
+                            const double* dX, const double* Yt, const double* dYt, double* out,
+                            double* work, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+#define CASE(KK)                                                                           \
+  case KK:                                                                                 \
+    k_quartic_rows<KK, 2><<<RED_BLOCKS, 256, 0, st>>>(F, n, m, X, dX, Yt, dYt, work);      \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  k_finish_cols<<<1, 256, 0, st>>>(work, RED_BLOCKS, 6, out);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// out[2t], out[2t+1] = barrier increments over X and Y for alpha_max / 2^t, t < ntrials
+extern "C" int nmfb_barrier_trials(const double* X, const double* dX, long nx, const double* Yt,
+                                   const double* dYt, long ny, const double* alpha_max, int ntrials,
+                                   double* out, double* work, long work_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = 64;
+  if (work_len < 2L * nb * ntrials) return NMFB_ENOMEM;
+  dim3 grid(nb, ntrials);
+  k_barrier_trials<<<grid, 256, 0, st>>>(X, dX, nx, Yt, dYt, ny, alpha_max, work);
+  k_finish_trials<<<1, 256, 0, st>>>(work, nb, ntrials, out);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_step_nudge(double* v, const double* dv, long len, double alpha, double tau,
+                               void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (len <= 0) return NMFB_OK;
+  k_step_nudge<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, dv, len, alpha, tau);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// out[12]: see k_kkt_partial.  R == NULL -> primal-only duals max(g, 0).
+extern "C" int nmfb_kkt_sums(const double* X, const double* R, const double* gX, long nx,
+                             const double* Yt, const double* S, const double* gY, long ny,
+                             double mux, double muy, double* out, double* work, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  k_kkt_partial<<<RED_BLOCKS, 256, 0, st>>>(X, R, gX, nx, Yt, S, gY, ny, mux, muy, work);
+  k_finish_kkt<<<1, 256, 0, st>>>(work, RED_BLOCKS, out);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_affine_mu(const double* X, const double* dX, const double* R,
+                              const double* dR, long nx, const double* Yt, const double* dY,
+                              const double* S, const double* dS, long ny, double a1, double a2,
+                              double* out, double* work, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  k_affine_partial<<<RED_BLOCKS, 256, 0, st>>>(X, dX, R, dR, nx, Yt, dY, S, dS, ny, a1, a2, work);
+  k_finish_sum1<<<1, 256, 0, st>>>(work, RED_BLOCKS, out);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_clamp_min(double* v, long len, double lo, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (len <= 0) return NMFB_OK;
+  k_clamp_fill<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, len, lo);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_fill(double* v, long len, double c, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (len <= 0) return NMFB_OK;
+  k_fill<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, len, c);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}

@@ -230,6 +230,8 @@ __global__ void __launch_bounds__(128) k_nnls(const double* __restrict__ ctc_g,
   st_out[t] = (int8_t)st;
 }
 
+__global__ void k_set_int(int* p, int v) { *p = v; }
+
 // chain fixed point: seeds[t] <- passive[t-1]; flag if any seed changed.
 __global__ void k_chain_update(const uint8_t* __restrict__ p_out, uint8_t* __restrict__ seeds,
                                long nrhs, int k, int* __restrict__ changed) {
@@ -550,8 +552,7 @@ extern "C" int nmfb_surface_block_cholesky(const double* blocks_in, long nb, lon
   cudaStream_t stream = (cudaStream_t)stream_;
   if (k < 1 || k > NMFB_MAX_K || nb < 0) return NMFB_EINVAL;
   cudaMemsetAsync(out, 0, sizeof(double) * (size_t)nb * k * k, stream);
-  const int h_init = INT_MAX;
-  cudaMemcpyAsync(bad, &h_init, sizeof(int), cudaMemcpyHostToDevice, stream);
+  k_set_int<<<1, 1, 0, stream>>>(bad, INT_MAX);
   if (nb == 0) return NMFB_OK;
   const int threads = 128;
   const int blocks = (int)((nb + threads - 1) / threads);

@@ -1,0 +1,528 @@
+"""Device-resident two-stage NMF solver (the B200 hot path).
+
+Host control flow follows the reference specification's drivers one for one
+(PAPER Algorithms 1-3) and the frozen semantics listed in
+DESIGN.md; every numeric step runs in libnmfb200.so through the C-ABI of
+include/nmfb200.h.  The host reads back a handful of scalars per ANLS sweep
+and two small scalar blocks per IPM iteration (pinned memory) to drive the
+loop decisions; all vectors and matrices stay in HBM.
+
+There is no CPU fallback: a missing library or device raises
+NativeLibraryError.
+"""
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import (IpmParams, IpmResult, SolveReport, Stage1Config, Stage1Result,
+                     TransitionParams)
+from .errors import (DegenerateFactor, LineSearchStall, NativeLibraryError,
+                     NotPositiveDefinite, status_error)
+
+_NONE = 0x7F7F7F7F
+NTRIALS = 61  # t = 0..60
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def barrier_weights(n, m, barrier):
+    """Per-block barrier weights (wx, wy): mu_X = wx mu, mu_Y = wy mu.
+
+    "paper"   : wx = wy = 1 (PAPER Eqs. 4, 9 and the merit function).
+    "balanced": n wx = m wy and (n wx + m wy)/(n + m) = 1.  With a single mu
+    and n != m the perturbed KKT system has no solution (summing
+    x_ip graX_ip - y_pj graY_pj over one component vanishes for every (X, Y)
+    by the scale invariance of XY, which forces mu (n - m) = 0), so the
+    paper's inner loop can only drift along the scaling orbit; the balanced
+    weights restore a central path.  Opt-in extension, see DESIGN.md.
+    """
+    if barrier == "paper":
+        return 1.0, 1.0
+    if barrier == "balanced":
+        return (n + m) / (2.0 * n), (n + m) / (2.0 * m)
+    raise ValueError(f"unknown barrier {barrier!r}")
+
+
+class Problem:
+    """M resident on one GPU plus every scratch buffer the solver needs."""
+
+    def __init__(self, M, k, device=None):
+        if not torch.cuda.is_available():
+            raise NativeLibraryError("no CUDA device: the B200 solver has no CPU fallback")
+        self.lib = _lib.load()
+        self.dev = device or torch.device("cuda", torch.cuda.current_device())
+        if isinstance(M, np.ndarray):
+            if M.dtype not in (np.float64, np.float32):
+                M = M.astype(np.float64)
+            M = torch.from_numpy(np.ascontiguousarray(M))
+        self.M = M.to(self.dev).contiguous()
+        if self.M.dtype not in (torch.float64, torch.float32):
+            self.M = self.M.double()
+        self.f32 = int(self.M.dtype == torch.float32)
+        self.n, self.m = self.M.shape
+        self.k = int(k)
+        if not 1 <= self.k <= 16:
+            raise ValueError("k must be in [1, 16]")
+        n, m, k = self.n, self.m, self.k
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        L = self.lib
+        cw = max(L.nmfb_colprod_work_len(n, m, k), L.nmfb_colprod_work_len(n, k, k),
+                 L.nmfb_colprod_work_len(m, k, k), L.nmfb_colprod_work_len(n, m, 1), 4096)
+        self.cwork = torch.empty(cw, **f64)
+        nb = L.nmfb_ipm_reduce_blocks()
+        self.rwork = torch.empty(max(64 * 2 * NTRIALS, 12 * nb, 3 * ((n + 127) // 128 + nb), 4096),
+                                 **f64)
+        self.row_n2 = torch.empty(n, **f64)
+        self.col_n2 = torch.empty(m, **f64)
+        self._call("nmfb_sqnorms", _p(self.M), self.f32, n, m, _p(self.row_n2), _p(self.col_n2),
+                   _p(self.cwork), self.cwork.numel(), self.stream)
+        self.dscal = torch.zeros(256, **f64)
+        self.iscal = torch.zeros(16, dtype=torch.int32, device=self.dev)
+        self.hscal = torch.zeros(256, dtype=torch.float64).pin_memory()
+        self.hint = torch.zeros(16, dtype=torch.int32).pin_memory()
+        self.launches = 0
+
+    # -- plumbing -----------------------------------------------------------
+    @property
+    def stream(self):
+        return torch.cuda.current_stream(self.dev).cuda_stream
+
+    def _call(self, name, *args):
+        rc = getattr(self.lib, name)(*args)
+        self.launches += 1
+        if rc != 0:
+            raise NativeLibraryError(f"{name} returned {rc}")
+
+    def readback(self, nd, ni=0):
+        """Copy dscal[:nd] / iscal[:ni] to pinned host memory and wait."""
+        if nd:
+            self.hscal[:nd].copy_(self.dscal[:nd], non_blocking=True)
+        if ni:
+            self.hint[:ni].copy_(self.iscal[:ni], non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return self.hscal[:nd].numpy().copy(), self.hint[:ni].numpy().copy()
+
+    def buf(self, *shape, dtype=torch.float64):
+        return torch.empty(shape, dtype=dtype, device=self.dev)
+
+    def rowprod(self, A, rows, cols, B, k, out, tol=None, f32=0):
+        self._call("nmfb_rowprod", _p(A), f32, rows, cols, _p(B), k, _p(out), _p(tol), 1.0,
+                   self.stream)
+
+    def colprod(self, A, rows, cols, B, k, out, tol=None, f32=0):
+        self._call("nmfb_colprod", _p(A), f32, rows, cols, _p(B), k, _p(out), _p(tol), 1.0,
+                   _p(self.cwork), self.cwork.numel(), self.stream)
+
+    def to_dev(self, a):
+        if isinstance(a, torch.Tensor):
+            return a.to(device=self.dev, dtype=torch.float64).contiguous().clone()
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(self.dev)
+
+    # -- gradients / KKT -----------------------------------------------------
+    def gradients(self, X, Yt, F, gX, gY, out_index=0):
+        """F = XY - M, graX, graY; dscal[out_index] = ||F||^2."""
+        n, m, k = self.n, self.m, self.k
+        self._call("nmfb_residual", _p(self.M), self.f32, n, m, k, _p(X), _p(Yt), _p(F), _p(gX),
+                   _p(self.dscal[out_index:]), _p(self.rwork), self.stream)
+        self.colprod(F, n, m, X, k, gY)
+
+    def kkt_sums(self, X, R, gX, Yt, S, gY, mux, muy, at=16):
+        self._call("nmfb_kkt_sums", _p(X), _p(R), _p(gX), X.numel(), _p(Yt), _p(S), _p(gY),
+                   Yt.numel(), float(mux), float(muy), _p(self.dscal[at:]), _p(self.rwork),
+                   self.stream)
+
+
+def kkt_from_sums(v):
+    """(E(.;mu), E(.;0)) from the 12 sums of nmfb_kkt_sums (PAPER Eq. 9)."""
+    st = math.sqrt(max(v[0] + v[4], 0.0))
+    return max(st, math.sqrt(max(v[1] + v[5], 0.0))), max(st, math.sqrt(max(v[2] + v[6], 0.0)))
+
+
+# ============================================================================
+# stage 1 (Algorithm 1)
+# ============================================================================
+def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=None):
+    """SPEC.md:209 run_stage1 on the device.  X (n,k), Yt (m,k) device fp64.
+
+    Returns (X, Yt, pX, pY, Stage1Result-without-host-copies).
+    """
+    cfg = cfg or Stage1Config()
+    t0 = time.perf_counter()
+    n, m, k = P.n, P.m, P.k
+    X = X.clone()
+    Yt = Yt.clone()
+    have_carry = pX is not None
+    pX = torch.zeros((n, k), dtype=torch.uint8, device=P.dev) if pX is None else pX.to(torch.uint8).clone()
+    pY = torch.zeros((m, k), dtype=torch.uint8, device=P.dev) if pY is None else pY.to(torch.uint8).clone()
+    Xn, Yn = P.buf(n, k), P.buf(m, k)
+    pXn = torch.empty_like(pX)
+    pYn = torch.empty_like(pY)
+    ctbX, tolX, r2X = P.buf(n, k), P.buf(n), P.buf(n)
+    ctbY, tolY, r2Y = P.buf(m, k), P.buf(m), P.buf(m)
+    chX = P.buf(n, dtype=torch.int64)
+    chY = P.buf(m, dtype=torch.int64)
+    stX = P.buf(n, dtype=torch.int8)
+    stY = P.buf(m, dtype=torch.int8)
+    GY, GX = P.buf(k, k), P.buf(k, k)
+    tol_fixed = cfg.tol_kkt
+    res = Stage1Result(None, None, None, None, 0, False)
+    nsweeps = cfg.fixed_sweeps if cfg.fixed_sweeps > 0 else cfg.max_sweeps
+    s = P.stream
+    for sweep in range(nsweeps):
+        mode = 2 if (sweep > 0 or have_carry) else 0
+        # X-update: C = Y^T, d = rows of M
+        P.colprod(Yt, m, k, Yt, k, GY)
+        P.rowprod(P.M, n, m, Yt, k, ctbX, tolX, P.f32)
+        if tol_fixed is not None:
+            tolX.fill_(float(tol_fixed))
+        P._call("nmfb_surface_nnls_batch", _p(GY), _p(ctbX), _p(P.row_n2), _p(pX), mode,
+                _p(tolX), 3 * k, n, k, _p(Xn), _p(pXn), _p(chX), _p(r2X), _p(stX), None, None, s)
+        # Y-update: C = X, d = columns of M
+        P.colprod(Xn, n, k, Xn, k, GX)
+        P.colprod(P.M, n, m, Xn, k, ctbY, tolY, P.f32)
+        if tol_fixed is not None:
+            tolY.fill_(float(tol_fixed))
+        P._call("nmfb_surface_nnls_batch", _p(GX), _p(ctbY), _p(P.col_n2), _p(pY), mode,
+                _p(tolY), 3 * k, m, k, _p(Yn), _p(pYn), _p(chY), _p(r2Y), _p(stY), None, None, s)
+        P._call("nmfb_stage1_stats", _p(X), _p(Xn), n * k, _p(Yt), _p(Yn), m * k, _p(r2Y), m,
+                _p(P.dscal), _p(P.rwork), P.rwork.numel(), s)
+        P._call("nmfb_first_nonzero_i8", _p(stX), n, _p(P.iscal[0:]), s)
+        P._call("nmfb_first_nonzero_i8", _p(stY), m, _p(P.iscal[1:]), s)
+        v, iv = P.readback(3, 2)
+        for which, idx, st in (("update_X", int(iv[0]), stX), ("update_Y", int(iv[1]), stY)):
+            if idx != _NONE:
+                raise status_error(int(st[idx].item()), idx, which)
+        X, Xn = Xn, X
+        Yt, Yn = Yn, Yt
+        pX, pXn = pXn, pX
+        pY, pYn = pYn, pY
+        step, nrm = math.sqrt(v[0]), math.sqrt(v[1])
+        res.sweeps = sweep + 1
+        res.trace.append((time.perf_counter() - t0, 0.5 * v[2], step))
+        if cfg.fixed_sweeps <= 0 and step <= cfg.eps_stol * (1.0 + nrm):
+            res.converged = True
+            break
+    res.seconds = time.perf_counter() - t0
+    return X, Yt, pX, pY, res
+
+
+# ============================================================================
+# stage 2 (Algorithm 2 + the Hessian switch of Algorithm 3)
+# ============================================================================
+class IpmEngine:
+    """Device state and kernels of one interior-point solve."""
+
+    def __init__(self, P: Problem, X, Yt, R, S, mu, rho, p: IpmParams):
+        self.P, self.p = P, p
+        n, m, k = P.n, P.m, P.k
+        self.n, self.m, self.k = n, m, k
+        self.kk = k * (k + 1) // 2
+        self.X, self.Yt, self.R, self.S = X, Yt, R, S
+        self.mu, self.rho, self.flag = float(mu), float(rho), False
+        self.wx, self.wy = barrier_weights(n, m, p.barrier)
+        b = P.buf
+        self.F = [b(n, m), b(n, m)]
+        self.fi = 0  # index of F at the current point
+        self.gX, self.gY = b(n, k), b(m, k)
+        self.L, self.h, self.g = b(n, k, k), b(n, k), b(n, k)
+        self.Apk, self.XXpk = b(n, self.kk), b(n, self.kk)
+        self.Z = b(self.kk, self.kk)
+        self.GY, self.XtX, self.H, self.Gdy = b(k, k), b(k, k), b(k, k), b(k, k)
+        N = m * k
+        self.N = N
+        self.A = b(N, N)
+        self.rhs = b(N)
+        self.dX, self.dR, self.dS = b(n, k), b(n, k), b(m, k)
+        self.FtG, self.FdY = b(m, k), b(n, k)
+        self.Xf, self.Ytf = b(n, k), b(m, k)
+        self.have_fact = False
+        self.fact_full = False
+        self.fact_F = 0
+        self.Pbuf = None
+        self.W = None
+        aw = max(P.lib.nmfb_atb_work_len(n, self.kk, self.kk),
+                 P.lib.nmfb_atb_work_len(n, m, k ** 3), 1)
+        self.awork = b(aw)
+
+    # -- helpers -------------------------------------------------------------
+    @property
+    def Fcur(self):
+        return self.F[self.fi]
+
+    def refresh(self):
+        """Gradients + KKT sums at the current point -> (E_mu, E_0, fsq, sums)."""
+        P = self.P
+        if self.have_fact and self.fact_F == self.fi:
+            self.fi ^= 1  # keep the factorization's residual for the predictor
+        P.gradients(self.X, self.Yt, self.Fcur, self.gX, self.gY, out_index=0)
+        P.kkt_sums(self.X, self.R, self.gX, self.Yt, self.S, self.gY, self.wx * self.mu,
+                   self.wy * self.mu, at=16)
+        v, _ = P.readback(28)
+        e_mu, e_0 = kkt_from_sums(v[16:28])
+        return e_mu, e_0, v[0], v[16:28]
+
+    def _ensure_full_buffers(self):
+        if self.Pbuf is None:
+            self.Pbuf = self.P.buf(self.n, self.k ** 3)
+            self.W = self.P.buf(self.m, self.k ** 3)
+
+    def direction(self, full):
+        """Newton direction. Returns (gtp, a1max, a2max, info_ok)."""
+        P = self.P
+        n, m, k, N, s = self.n, self.m, self.k, self.N, P.stream
+        mux, muy = self.wx * self.mu, self.wy * self.mu
+        X, Yt, F = self.X, self.Yt, self.Fcur
+        P.colprod(Yt, m, k, Yt, k, self.GY)
+        P.colprod(X, n, k, X, k, self.XtX)
+        P._call("nmfb_r1_factor", _p(self.GY), _p(X), _p(self.R), _p(self.gX), mux, self.rho, n,
+                k, _p(self.L), _p(self.h), _p(self.g), _p(self.Apk), _p(self.XXpk),
+                _p(P.iscal[2:]), s)
+        P._call("nmfb_atb", _p(self.Apk), n, self.kk, _p(self.XXpk), self.kk, _p(self.Z),
+                _p(self.awork), self.awork.numel(), s)
+        P.colprod(X, n, k, self.g, k, self.H)
+        W = FtG = None
+        if full:
+            self._ensure_full_buffers()
+            P._call("nmfb_make_p", _p(X), _p(self.Apk), n, k, _p(self.Pbuf), s)
+            P._call("nmfb_atb", _p(F), n, m, _p(self.Pbuf), k ** 3, _p(self.W), _p(self.awork),
+                    self.awork.numel(), s)
+            P.colprod(F, n, m, self.g, k, self.FtG)
+            W, FtG = self.W, self.FtG
+        P._call("nmfb_schur_assemble", _p(Yt), _p(self.S), m, k, _p(self.Z), _p(self.XtX),
+                self.rho, _p(W), _p(self.A), s)
+        if full:
+            P._call("nmfb_schur_term4", _p(F), n, m, k, _p(self.Apk), _p(self.A), s)
+        P._call("nmfb_schur_rhs", _p(Yt), _p(self.gY), _p(self.H), _p(FtG), muy, m, k,
+                _p(self.rhs), s)
+        P._call("nmfb_dense_cholesky", _p(self.A), N, _p(P.iscal[3:]), s)
+        P._call("nmfb_dense_solve", _p(self.A), N, _p(self.rhs), s)
+        dY = self.rhs.view(m, k)
+        P.colprod(Yt, m, k, dY, k, self.Gdy)
+        FdY = None
+        if full:
+            P.rowprod(F, n, m, dY, k, self.FdY)
+            FdY = self.FdY
+        P._call("nmfb_direction", _p(self.L), _p(X), _p(self.h), _p(self.Gdy), _p(FdY), _p(X),
+                _p(self.R), _p(self.gX), mux, _p(Yt), _p(self.S), _p(self.gY), _p(dY), muy,
+                self.p.tau, n, m, k, _p(self.dX), _p(self.dR), _p(self.dS), _p(P.dscal[4:]),
+                _p(P.rwork), P.rwork.numel(), s)
+        return dY
+
+    def armijo_launch(self, dY):
+        """Quartic coefficients + all backtracking barrier sums in two launches."""
+        P, s = self.P, self.P.stream
+        n, m, k = self.n, self.m, self.k
+        P._call("nmfb_quartic", _p(self.Fcur), n, m, k, _p(self.X), _p(self.dX), _p(self.Yt),
+                _p(dY), _p(P.dscal[8:]), _p(P.rwork), s)
+        P._call("nmfb_barrier_trials", _p(self.X), _p(self.dX), n * k, _p(self.Yt), _p(dY), m * k,
+                _p(P.dscal[5:]), NTRIALS, _p(P.dscal[32:]), _p(P.rwork), P.rwork.numel(), s)
+
+    def remember_factorization(self, full):
+        self.Xf.copy_(self.X)
+        self.Ytf.copy_(self.Yt)
+        self.have_fact = True
+        self.fact_full = full
+        self.fact_F = self.fi
+
+    def predictor_sigma(self, sums):
+        """PAPER Eqs. 7-8 with the last Newton factorization."""
+        P, p = self.P, self.p
+        n, m, k, N, s = self.n, self.m, self.k, self.N, P.stream
+        full = self.fact_full
+        Ff = self.F[self.fact_F]
+        P._call("nmfb_hg", _p(self.L), _p(self.gX), -1.0, n, k, _p(self.h), _p(self.g), s)
+        P.colprod(self.Xf, n, k, self.g, k, self.H)
+        FtG = None
+        if full:
+            P.colprod(Ff, n, m, self.g, k, self.FtG)
+            FtG = self.FtG
+        P._call("nmfb_schur_rhs", _p(self.Ytf), _p(self.gY), _p(self.H), _p(FtG), 0.0, m, k,
+                _p(self.rhs), s)
+        P._call("nmfb_dense_solve", _p(self.A), N, _p(self.rhs), s)
+        dY = self.rhs.view(m, k)
+        P.colprod(self.Ytf, m, k, dY, k, self.Gdy)
+        FdY = None
+        if full:
+            P.rowprod(Ff, n, m, dY, k, self.FdY)
+            FdY = self.FdY
+        P._call("nmfb_direction", _p(self.L), _p(self.Xf), _p(self.h), _p(self.Gdy), _p(FdY),
+                _p(self.X), _p(self.R), _p(self.gX), 0.0, _p(self.Yt), _p(self.S), _p(self.gY),
+                _p(dY), 0.0, 1.0, n, m, k, _p(self.dX), _p(self.dR), _p(self.dS),
+                _p(P.dscal[4:]), _p(P.rwork), P.rwork.numel(), s)
+        v, _ = P.readback(8)
+        a1, a2 = v[5], v[6]
+        P._call("nmfb_affine_mu", _p(self.X), _p(self.dX), _p(self.R), _p(self.dR), n * k,
+                _p(self.Yt), _p(dY), _p(self.S), _p(self.dS), m * k, a1, a2, _p(P.dscal[0:]),
+                _p(P.rwork), s)
+        v, _ = P.readback(1)
+        nk = n * k + m * k
+        mu_aff = v[0] / nk
+        mu_bar = (sums[3] + sums[7]) / nk
+        return min((mu_aff / mu_bar) ** 3, p.sigma_cap)
+
+
+def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
+    """SPEC.md:337 run_ipm on the device (Algorithm 2 + Algorithm 3 switch).
+
+    X, Yt, R, S are device tensors updated in place.  Returns (engine, IpmResult).
+    """
+    p = p or IpmParams()
+    t0 = time.perf_counter()
+    eng = IpmEngine(P, X, Yt, R, S, mu, rho, p)
+    cap = p.fixed_iters if p.fixed_iters > 0 else p.max_iter
+    tol = 0.0 if p.fixed_iters > 0 else p.eps_tol
+    e_mu, e_zero, fsq, sums = eng.refresh()
+    res = IpmResult(0, 0, False, e_zero, eng.mu, False)
+    n, m, k = P.n, P.m, P.k
+    while e_zero > tol and res.iters < cap:
+        eps_mu = eng.mu
+        while e_mu > eps_mu and res.iters < cap:
+            used_full = False
+            ok = False
+            if eng.flag:
+                dY = eng.direction(True)
+                eng.armijo_launch(dY)
+                v, iv = P.readback(32 + 2 * NTRIALS, 4)
+                if int(iv[2]) != _NONE:
+                    raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
+                if int(iv[3]) < 0 and v[4] < 0.0:
+                    ok, used_full = True, True
+                    eng.remember_factorization(True)
+                else:
+                    eng.flag = False
+            if not ok:
+                dY = eng.direction(False)
+                eng.armijo_launch(dY)
+                v, iv = P.readback(32 + 2 * NTRIALS, 4)
+                if int(iv[2]) != _NONE:
+                    raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
+                if int(iv[3]) >= 0:
+                    raise NotPositiveDefinite("Gauss-Newton Schur matrix not positive definite",
+                                              int(iv[3]))
+                eng.remember_factorization(False)
+            gtp, a1max, a2max = v[4], v[5], v[6]
+            aa, ab, bb, ac, bc, cc = v[8:14]
+            bars = v[32:32 + 2 * NTRIALS]
+            t = 0
+            while True:
+                a1 = a1max / (2.0 ** t)
+                quad = a1 * ab + a1 * a1 * (0.5 * bb + ac) + a1 ** 3 * bc + 0.5 * a1 ** 4 * cc
+                dphi = quad - eng.mu * (eng.wx * bars[2 * t] + eng.wy * bars[2 * t + 1])
+                if dphi <= p.eta * a1 * gtp:
+                    break
+                t += 1
+                if t > p.max_backtracks:
+                    raise LineSearchStall(f"Armijo backtracking exceeded {p.max_backtracks}")
+            s = P.stream
+            P._call("nmfb_step_nudge", _p(eng.X), _p(eng.dX), n * k, a1, p.tau, s)
+            P._call("nmfb_step_nudge", _p(eng.Yt), _p(dY), m * k, a1, p.tau, s)
+            P._call("nmfb_step_nudge", _p(eng.R), _p(eng.dR), n * k, a2max, p.tau, s)
+            P._call("nmfb_step_nudge", _p(eng.S), _p(eng.dS), m * k, a2max, p.tau, s)
+            res.iters += 1
+            res.armijo_t.append(t)
+            res.flags.append(used_full)
+            e_mu, e_zero, fsq, sums = eng.refresh()
+            res.trace.append((time.perf_counter() - t0, 0.5 * fsq, e_zero, eng.mu, a1, a2max, t))
+        res.outer += 1
+        if e_zero <= tol or res.iters >= cap:
+            break
+        if not eng.have_fact:
+            eng.direction(False)
+            v, iv = P.readback(8, 4)
+            eng.remember_factorization(False)
+        sigma = eng.predictor_sigma(sums)
+        eng.mu = sigma * eng.mu
+        eng.flag = sigma <= p.sigma_c
+        e_mu, e_zero, fsq, sums = eng.refresh()
+    res.converged = e_zero <= tol
+    res.mu, res.flag = eng.mu, eng.flag
+    res.seconds = time.perf_counter() - t0
+    return eng, res
+
+
+def transition(P: Problem, X, Yt, eps_tol, tp: TransitionParams | None = None):
+    """SPEC.md:393 / PAPER Eqs. 14-18 on the device -> (X, Yt, R, S, mu, rho)."""
+    tp = tp or TransitionParams()
+    n, m, k, s = P.n, P.m, P.k, P.stream
+    X, Yt = X.clone(), Yt.clone()
+    F, gX, gY = P.buf(n, m), P.buf(n, k), P.buf(m, k)
+    # max over the concatenated (x, y)
+    P.gradients(X, Yt, F, gX, gY)
+    P.kkt_sums(X, None, gX, Yt, None, gY, 0.0, 0.0, at=16)
+    v, _ = P.readback(28)
+    big = max(v[26], v[27])
+    if not big > 0.0:
+        raise DegenerateFactor("X and Y are identically zero: transition undefined")
+    rho0 = tp.rho0_scale * big
+    P._call("nmfb_clamp_min", _p(X), n * k, rho0, s)
+    P._call("nmfb_clamp_min", _p(Yt), m * k, rho0, s)
+    P.gradients(X, Yt, F, gX, gY)
+    P.kkt_sums(X, None, gX, Yt, None, gY, 0.0, 0.0, at=16)
+    v, _ = P.readback(28)
+    R, S = P.buf(n, k), P.buf(m, k)
+    P._call("nmfb_fill", _p(R), n * k, float(v[24]), s)
+    P._call("nmfb_fill", _p(S), m * k, float(v[25]), s)
+    P.kkt_sums(X, R, gX, Yt, S, gY, 0.0, 0.0, at=16)
+    v, _ = P.readback(28)
+    mu = (v[19] + v[23]) / (n * k + m * k)
+    return X, Yt, R, S, mu, float(eps_tol)
+
+
+def kkt_error_primal_only_dev(P: Problem, X, Yt):
+    """SPEC.md:420 on the device."""
+    n, m, k = P.n, P.m, P.k
+    F, gX, gY = P.buf(n, m), P.buf(n, k), P.buf(m, k)
+    P.gradients(X, Yt, F, gX, gY)
+    P.kkt_sums(X, None, gX, Yt, None, gY, 0.0, 0.0, at=16)
+    v, _ = P.readback(28)
+    return kkt_from_sums(v[16:28])[1], 0.5 * v[0]
+
+
+def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1: Stage1Config | None = None,
+                  ipm: IpmParams | None = None, tp: TransitionParams | None = None,
+                  stage="two_stage", pX=None, pY=None, e_scale=None, problem: Problem | None = None):
+    """SPEC.md:411 run_two_stage (Algorithm 3) on the B200.
+
+    M (n,m) host or device array (fp64, or fp32 storage); X0 (n,k); Y0 (k,m).
+    Relative KKT tolerance: eps_abs = tol_rel * max(1, E_primal(X0, Y0)) unless
+    ``e_scale`` is given (frozen semantics 5).
+    """
+    X0n = X0 if isinstance(X0, torch.Tensor) else np.asarray(X0, dtype=np.float64)
+    k = X0n.shape[1]
+    P = problem or Problem(M, k)
+    X = P.to_dev(X0)
+    Yt = P.to_dev(Y0.T if not isinstance(Y0, torch.Tensor) else Y0.t())
+    if e_scale is None:
+        e_scale = max(1.0, kkt_error_primal_only_dev(P, X, Yt)[0])
+    eps_abs = tol_rel * e_scale
+    p = ipm or IpmParams()
+    p.eps_tol = eps_abs
+    s1 = s1 or Stage1Config()
+    if stage == "ipm_only":
+        r1 = Stage1Result(None, None, None, None, 0, False)
+        pXd = pYd = None
+    else:
+        pXd = None if pX is None else torch.as_tensor(np.asarray(pX, np.uint8)).to(P.dev)
+        pYd = None if pY is None else torch.as_tensor(np.asarray(pY, np.uint8)).to(P.dev)
+        X, Yt, pXd, pYd, r1 = run_stage1(P, X, Yt, s1, pXd, pYd)
+    r1.X, r1.Yt = X.cpu().numpy(), Yt.cpu().numpy()
+    r1.pX = None if pXd is None else pXd.bool().cpu().numpy()
+    r1.pY = None if pYd is None else pYd.bool().cpu().numpy()
+    if stage == "anls_only":
+        e0, f = kkt_error_primal_only_dev(P, X, Yt)
+        return SolveReport("Converged" if e0 <= eps_abs else "IterationCap", r1.X, r1.Yt, None,
+                           None, f, e0, eps_abs, r1, None, r1.seconds, 0.0)
+    X, Yt, R, S, mu, rho = transition(P, X, Yt, eps_abs, tp)
+    eng, r2 = run_ipm(P, X, Yt, R, S, mu, rho, p)
+    e_mu, e_zero, fsq, _ = eng.refresh()
+    status = "Converged" if r2.converged else "IterationCap"
+    return SolveReport(status, eng.X.cpu().numpy(), eng.Yt.cpu().numpy(), eng.R.cpu().numpy(),
+                       eng.S.cpu().numpy(), 0.5 * fsq, e_zero, eps_abs, r1, r2, r1.seconds,
+                       r2.seconds)
