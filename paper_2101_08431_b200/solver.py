@@ -57,6 +57,7 @@ class Problem:
         if not torch.cuda.is_available():
             raise NativeLibraryError("no CUDA device: the B200 solver has no CPU fallback")
         self.lib = _lib.load()
+        self.launches = 0
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         if isinstance(M, np.ndarray):
             if M.dtype not in (np.float64, np.float32):
@@ -87,7 +88,6 @@ class Problem:
         self.iscal = torch.zeros(16, dtype=torch.int32, device=self.dev)
         self.hscal = torch.zeros(256, dtype=torch.float64).pin_memory()
         self.hint = torch.zeros(16, dtype=torch.int32).pin_memory()
-        self.launches = 0
 
     # -- plumbing -----------------------------------------------------------
     @property
