@@ -183,6 +183,9 @@ int nmfb_fill(double *v, long len, double c, void *stream);
 int nmfb_dense_cholesky(double *A, long N, int *info, void *stream);
 int nmfb_dense_solve(const double *L, long N, double *b, void *stream);
 
+/* number of kernel launches issued by this library so far (host counter) */
+unsigned long long nmfb_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,7 +36,36 @@ from dataclasses import dataclass, field
 import numpy as np
 from scipy.linalg import solve_triangular
 
-from oracle import kernels as K
+from oracle import kernels as _KC
+from oracle import kernels_np as _KN
+
+
+class _Kernels:
+    """Kernel table used by the driver: the bit-exact C port by default;
+    ``set_schur_backend("numpy")`` swaps the Schur-side kernels for the
+    vectorised NumPy-backend formulation (CPU-baseline speed path)."""
+
+    def __init__(self):
+        self.set("c")
+
+    def set(self, which):
+        self.block_cholesky = _KC.block_cholesky
+        self.block_solve_lower = _KC.block_solve_lower
+        self.block_solve_lower_t = _KC.block_solve_lower_t
+        self.nnls_batch = _KC.nnls_batch
+        src = _KN if which == "numpy" else _KC
+        self.schur_reduce = src.schur_reduce
+        self.rhs_reduce = src.rhs_reduce
+        self.back_substitute = src.back_substitute
+        self.which = which
+
+
+K = _Kernels()
+
+
+def set_schur_backend(which: str) -> None:
+    """"c" (bit-exact port of _kernels_numba) or "numpy" (_kernels_numpy formulation)."""
+    K.set(which)
 
 
 # ----------------------------------------------------------------------------

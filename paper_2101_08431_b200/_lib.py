@@ -53,8 +53,10 @@ SIGNATURES = {
     "nmfb_fill": [P, L, D, P],
     "nmfb_dense_cholesky": [P, L, P, P],
     "nmfb_dense_solve": [P, L, P, P],
+    "nmfb_launch_count": [],
 }
-RESTYPES = {"nmfb_colprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long}
+RESTYPES = {"nmfb_colprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
+            "nmfb_launch_count": ctypes.c_ulonglong}
 
 _lib = None
 

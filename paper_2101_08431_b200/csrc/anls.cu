@@ -14,6 +14,10 @@
 #include "common.cuh"
 #include "nmfb200.h"
 
+unsigned long long g_nmfb_launches = 0;
+
+extern "C" unsigned long long nmfb_launch_count(void) { return g_nmfb_launches; }
+
 namespace {
 
 template <typename T>
@@ -281,7 +285,7 @@ int launch_rowprod(const T* A, long rows, long cols, const double* B, double* ou
                    double scale, cudaStream_t st) {
   const long warps = (rows + ROWPROD_R - 1) / ROWPROD_R;
   const int blocks = nmfb_blocks(warps * 32, 256, 148 * 16);
-  k_rowprod<K, ROWPROD_R, T><<<blocks, 256, 0, st>>>(A, rows, cols, B, out, tol, scale);
+  ++g_nmfb_launches, k_rowprod<K, ROWPROD_R, T><<<blocks, 256, 0, st>>>(A, rows, cols, B, out, tol, scale);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -306,8 +310,8 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
   const long ns = (rows + stripe - 1) / stripe;
   if (ns * cols * K > work_len) return NMFB_ENOMEM;
   dim3 grid((unsigned)((cols + CP_COLS - 1) / CP_COLS), (unsigned)ns);
-  k_colprod_partial<K, T><<<grid, 256, 0, st>>>(A, rows, cols, B, stripe, work);
-  k_sum_partials<K><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(work, (int)ns, cols * K, out,
+  ++g_nmfb_launches, k_colprod_partial<K, T><<<grid, 256, 0, st>>>(A, rows, cols, B, stripe, work);
+  ++g_nmfb_launches, k_sum_partials<K><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(work, (int)ns, cols * K, out,
                                                                    tol, scale);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
@@ -369,13 +373,13 @@ extern "C" int nmfb_sqnorms(const void* A, int a_is_f32, long rows, long cols, d
   if (ns * cols > work_len) return NMFB_ENOMEM;
   dim3 grid((unsigned)((cols + 127) / 128), (unsigned)ns);
   if (a_is_f32) {
-    k_row_sqnorm<float><<<blocks, 256, 0, st>>>((const float*)A, rows, cols, row_out);
-    k_col_sqnorm_partial<float><<<grid, 128, 0, st>>>((const float*)A, rows, cols, stripe, work);
+    ++g_nmfb_launches, k_row_sqnorm<float><<<blocks, 256, 0, st>>>((const float*)A, rows, cols, row_out);
+    ++g_nmfb_launches, k_col_sqnorm_partial<float><<<grid, 128, 0, st>>>((const float*)A, rows, cols, stripe, work);
   } else {
-    k_row_sqnorm<double><<<blocks, 256, 0, st>>>((const double*)A, rows, cols, row_out);
-    k_col_sqnorm_partial<double><<<grid, 128, 0, st>>>((const double*)A, rows, cols, stripe, work);
+    ++g_nmfb_launches, k_row_sqnorm<double><<<blocks, 256, 0, st>>>((const double*)A, rows, cols, row_out);
+    ++g_nmfb_launches, k_col_sqnorm_partial<double><<<grid, 128, 0, st>>>((const double*)A, rows, cols, stripe, work);
   }
-  k_sum_partials<1><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(work, (int)ns, cols, col_out,
+  ++g_nmfb_launches, k_sum_partials<1><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(work, (int)ns, cols, col_out,
                                                                    nullptr, 1.0);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
@@ -388,8 +392,8 @@ extern "C" int nmfb_stage1_stats(const double* Xo, const double* Xn, long nx, co
   cudaStream_t st = (cudaStream_t)stream;
   const int blocks = 296;
   if (work_len < blocks * 3) return NMFB_ENOMEM;
-  k_stage1_stats_partial<<<blocks, 256, 0, st>>>(Xo, Xn, nx, Yo, Yn, ny, r2, nr, work);
-  k_finish_sums<<<1, 256, 0, st>>>(work, blocks, 3, stats);
+  ++g_nmfb_launches, k_stage1_stats_partial<<<blocks, 256, 0, st>>>(Xo, Xn, nx, Yo, Yn, ny, r2, nr, work);
+  ++g_nmfb_launches, k_finish_sums<<<1, 256, 0, st>>>(work, blocks, 3, stats);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -399,7 +403,7 @@ extern "C" int nmfb_first_nonzero_i8(const int8_t* st, long len, int* out, void*
   cudaStream_t s = (cudaStream_t)stream;
   cudaMemsetAsync(out, 0x7F, sizeof(int), s);
   if (len <= 0) return NMFB_OK;
-  k_first_nonzero_i8<<<nmfb_blocks(len, 256, 148 * 4), 256, 0, s>>>(st, len, out);
+  ++g_nmfb_launches, k_first_nonzero_i8<<<nmfb_blocks(len, 256, 148 * 4), 256, 0, s>>>(st, len, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

@@ -5,6 +5,9 @@
 
 #define NMFB_MAX_K 16
 
+// kernel launches issued by this library (reported by bench.py as gpu_launches)
+extern unsigned long long g_nmfb_launches;
+
 // Return codes of the C-ABI (0 = ok, negative = argument / launch error).
 enum {
   NMFB_OK = 0,

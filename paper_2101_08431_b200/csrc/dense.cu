@@ -259,12 +259,12 @@ extern "C" int nmfb_dense_cholesky(double* A, long N, int* info, void* stream) {
   cudaMemsetAsync(info, 0xFF, sizeof(int), st);  // -1: no failing pivot
   for (long k0 = 0; k0 < N; k0 += NB) {
     const int nb = (int)min((long)NB, N - k0);
-    k_potrf_tile<<<1, 256, 0, st>>>(A, N, k0, nb, info);
+    ++g_nmfb_launches, k_potrf_tile<<<1, 256, 0, st>>>(A, N, k0, nb, info);
     const long rest = N - k0 - nb;
     if (rest > 0) {
       const long tiles = (rest + NB - 1) / NB;
-      k_trsm_panel<<<(unsigned)tiles, 256, kTwoTiles, st>>>(A, N, k0, nb, info);
-      k_syrk_trailing<<<(unsigned)(tiles * (tiles + 1) / 2), 256, kTwoTiles, st>>>(A, N, k0, nb, info);
+      ++g_nmfb_launches, k_trsm_panel<<<(unsigned)tiles, 256, kTwoTiles, st>>>(A, N, k0, nb, info);
+      ++g_nmfb_launches, k_syrk_trailing<<<(unsigned)(tiles * (tiles + 1) / 2), 256, kTwoTiles, st>>>(A, N, k0, nb, info);
     }
   }
   NMFB_CHECK_LAUNCH();
@@ -276,21 +276,21 @@ extern "C" int nmfb_dense_solve(const double* L, long N, double* b, void* stream
   cudaStream_t st = (cudaStream_t)stream;
   if (N <= 0) return NMFB_EINVAL;
   if (N <= 4096) {
-    k_trsv_single<<<1, 1024, 0, st>>>(L, N, b, 0);
-    k_trsv_single<<<1, 1024, 0, st>>>(L, N, b, 1);
+    ++g_nmfb_launches, k_trsv_single<<<1, 1024, 0, st>>>(L, N, b, 0);
+    ++g_nmfb_launches, k_trsv_single<<<1, 1024, 0, st>>>(L, N, b, 1);
   } else {
     for (long c0 = 0; c0 < N; c0 += 32) {
       const int nc = (int)min(32L, N - c0);
-      k_trsv_diag<<<1, 32, 0, st>>>(L, N, b, c0, nc, 0);
+      ++g_nmfb_launches, k_trsv_diag<<<1, 32, 0, st>>>(L, N, b, c0, nc, 0);
       const long rest = N - c0 - nc;
-      if (rest > 0) k_trsv_update<<<(unsigned)((rest * 32 + 255) / 256), 256, 0, st>>>(L, N, b, c0, nc, 0);
+      if (rest > 0) ++g_nmfb_launches, k_trsv_update<<<(unsigned)((rest * 32 + 255) / 256), 256, 0, st>>>(L, N, b, c0, nc, 0);
     }
     const long nblk = (N + 31) / 32;
     for (long bb = nblk - 1; bb >= 0; --bb) {
       const long c0 = bb * 32;
       const int nc = (int)min(32L, N - c0);
-      k_trsv_diag<<<1, 32, 0, st>>>(L, N, b, c0, nc, 1);
-      if (c0 > 0) k_trsv_update<<<(unsigned)((c0 + 255) / 256), 256, 0, st>>>(L, N, b, c0, nc, 1);
+      ++g_nmfb_launches, k_trsv_diag<<<1, 32, 0, st>>>(L, N, b, c0, nc, 1);
+      if (c0 > 0) ++g_nmfb_launches, k_trsv_update<<<(unsigned)((c0 + 255) / 256), 256, 0, st>>>(L, N, b, c0, nc, 1);
     }
   }
   NMFB_CHECK_LAUNCH();

@@ -808,15 +808,15 @@ extern "C" int nmfb_residual(const void* M, int m_is_f32, long n, long m, long k
 #define CASE(KK)                                                                          \
   case KK:                                                                                \
     if (m_is_f32)                                                                         \
-      k_residual_rows<KK, 2, float><<<RED_BLOCKS, 256, 0, st>>>((const float*)M, n, m, X, \
+      ++g_nmfb_launches, k_residual_rows<KK, 2, float><<<RED_BLOCKS, 256, 0, st>>>((const float*)M, n, m, X, \
                                                                 Yt, F, gX, work);         \
     else                                                                                  \
-      k_residual_rows<KK, 2, double><<<RED_BLOCKS, 256, 0, st>>>((const double*)M, n, m,  \
+      ++g_nmfb_launches, k_residual_rows<KK, 2, double><<<RED_BLOCKS, 256, 0, st>>>((const double*)M, n, m,  \
                                                                  X, Yt, F, gX, work);     \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
-  k_finish_sum1<<<1, 256, 0, st>>>(work, RED_BLOCKS, out);
+  ++g_nmfb_launches, k_finish_sum1<<<1, 256, 0, st>>>(work, RED_BLOCKS, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -831,7 +831,7 @@ extern "C" int nmfb_r1_factor(const double* GY, const double* X, const double* R
   const int blocks = (int)((n + 127) / 128);
 #define CASE(KK)                                                                               \
   case KK:                                                                                     \
-    k_r1_factor<KK><<<blocks, 128, 0, st>>>(GY, X, R, gX, mux, rho, n, L, h, g, Apk, XXpk, bad); \
+    ++g_nmfb_launches, k_r1_factor<KK><<<blocks, 128, 0, st>>>(GY, X, R, gX, mux, rho, n, L, h, g, Apk, XXpk, bad); \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
@@ -846,7 +846,7 @@ extern "C" int nmfb_hg(const double* L, const double* b1, double b1_scale, long 
   const int blocks = (int)((n + 127) / 128);
 #define CASE(KK)                                                               \
   case KK:                                                                     \
-    k_hg_rows<KK><<<blocks, 128, 0, st>>>(L, b1, b1_scale, n, h, g);           \
+    ++g_nmfb_launches, k_hg_rows<KK><<<blocks, 128, 0, st>>>(L, b1, b1_scale, n, h, g);           \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
@@ -881,11 +881,11 @@ extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, lo
   ns = (rows + stripe - 1) / stripe;
   dim3 grid((unsigned)((ca + 31) / 32), (unsigned)((cb + 31) / 32), (unsigned)ns);
   if (ns == 1) {
-    k_atb_partial<<<grid, 256, 0, st>>>(A, rows, ca, B, cb, stripe, out);
+    ++g_nmfb_launches, k_atb_partial<<<grid, 256, 0, st>>>(A, rows, ca, B, cb, stripe, out);
   } else {
     if (ns * ca * cb > work_len) return NMFB_ENOMEM;
-    k_atb_partial<<<grid, 256, 0, st>>>(A, rows, ca, B, cb, stripe, work);
-    k_sum_parts<<<(unsigned)((ca * cb + 255) / 256), 256, 0, st>>>(work, (int)ns, ca * cb, out);
+    ++g_nmfb_launches, k_atb_partial<<<grid, 256, 0, st>>>(A, rows, ca, B, cb, stripe, work);
+    ++g_nmfb_launches, k_sum_parts<<<(unsigned)((ca * cb + 255) / 256), 256, 0, st>>>(work, (int)ns, ca * cb, out);
   }
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
@@ -898,7 +898,7 @@ extern "C" int nmfb_make_p(const double* X, const double* Apk, long n, long k, d
   const unsigned blocks = (unsigned)((total + 255) / 256);
 #define CASE(KK)                                                 \
   case KK:                                                       \
-    k_make_p<KK><<<blocks, 256, 0, st>>>(X, Apk, n, P);          \
+    ++g_nmfb_launches, k_make_p<KK><<<blocks, 256, 0, st>>>(X, Apk, n, P);          \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
@@ -929,7 +929,7 @@ extern "C" int nmfb_schur_assemble(const double* Yt, const double* S, long m, lo
   case KK:                                                                                    \
     cudaFuncSetAttribute(k_schur_assemble<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                          (int)smem);                                                          \
-    k_schur_assemble<KK><<<grid, 256, smem, st>>>(Yt, S, m, Zpk, XtX, rho, W, TL, jchunk, A); \
+    ++g_nmfb_launches, k_schur_assemble<KK><<<grid, 256, smem, st>>>(Yt, S, m, Zpk, XtX, rho, W, TL, jchunk, A); \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
@@ -945,7 +945,7 @@ extern "C" int nmfb_schur_term4(const double* F, long n, long m, long k, const d
   dim3 grid((unsigned)tiles, (unsigned)tiles, (unsigned)((kk + 15) / 16));
 #define CASE(KK)                                                       \
   case KK:                                                             \
-    k_schur_term4<KK><<<grid, 256, 0, st>>>(F, n, m, Apk, A);          \
+    ++g_nmfb_launches, k_schur_term4<KK><<<grid, 256, 0, st>>>(F, n, m, Apk, A);          \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
@@ -960,7 +960,7 @@ extern "C" int nmfb_schur_rhs(const double* Yt, const double* gY, const double* 
   const unsigned blocks = (unsigned)((m + 127) / 128);
 #define CASE(KK)                                                                  \
   case KK:                                                                        \
-    k_schur_rhs<KK><<<blocks, 128, 0, st>>>(Yt, gY, H, FtG, muy, m, rhs);        \
+    ++g_nmfb_launches, k_schur_rhs<KK><<<blocks, 128, 0, st>>>(Yt, gY, H, FtG, muy, m, rhs);        \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
@@ -981,12 +981,12 @@ extern "C" int nmfb_direction(const double* L, const double* Xf, const double* h
   if (work_len < 3L * (rb + RED_BLOCKS)) return NMFB_ENOMEM;
 #define CASE(KK)                                                                              \
   case KK:                                                                                    \
-    k_dir_rows<KK><<<rb, 128, 0, st>>>(L, Xf, h, Gdy, FdY, X, R, gX, mux, tau, n, dX, dR, work); \
+    ++g_nmfb_launches, k_dir_rows<KK><<<rb, 128, 0, st>>>(L, Xf, h, Gdy, FdY, X, R, gX, mux, tau, n, dX, dR, work); \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
-  k_dir_cols<<<RED_BLOCKS, 256, 0, st>>>(Yt, S, gY, dY, muy, tau, m * k, dS, work + 3 * rb);
-  k_finish_dir<<<1, 256, 0, st>>>(work, rb, work + 3 * rb, RED_BLOCKS, out);
+  ++g_nmfb_launches, k_dir_cols<<<RED_BLOCKS, 256, 0, st>>>(Yt, S, gY, dY, muy, tau, m * k, dS, work + 3 * rb);
+  ++g_nmfb_launches, k_finish_dir<<<1, 256, 0, st>>>(work, rb, work + 3 * rb, RED_BLOCKS, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -998,11 +998,11 @@ extern "C" int nmfb_quartic(const double* F, long n, long m, long k, const doubl
   cudaStream_t st = (cudaStream_t)stream;
 #define CASE(KK)                                                                           \
   case KK:                                                                                 \
-    k_quartic_rows<KK, 2><<<RED_BLOCKS, 256, 0, st>>>(F, n, m, X, dX, Yt, dYt, work);      \
+    ++g_nmfb_launches, k_quartic_rows<KK, 2><<<RED_BLOCKS, 256, 0, st>>>(F, n, m, X, dX, Yt, dYt, work);      \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
-  k_finish_cols<<<1, 256, 0, st>>>(work, RED_BLOCKS, 6, out);
+  ++g_nmfb_launches, k_finish_cols<<<1, 256, 0, st>>>(work, RED_BLOCKS, 6, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -1015,8 +1015,8 @@ extern "C" int nmfb_barrier_trials(const double* X, const double* dX, long nx, c
   const int nb = 64;
   if (work_len < 2L * nb * ntrials) return NMFB_ENOMEM;
   dim3 grid(nb, ntrials);
-  k_barrier_trials<<<grid, 256, 0, st>>>(X, dX, nx, Yt, dYt, ny, alpha_max, work);
-  k_finish_trials<<<1, 256, 0, st>>>(work, nb, ntrials, out);
+  ++g_nmfb_launches, k_barrier_trials<<<grid, 256, 0, st>>>(X, dX, nx, Yt, dYt, ny, alpha_max, work);
+  ++g_nmfb_launches, k_finish_trials<<<1, 256, 0, st>>>(work, nb, ntrials, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -1025,7 +1025,7 @@ extern "C" int nmfb_step_nudge(double* v, const double* dv, long len, double alp
                                void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (len <= 0) return NMFB_OK;
-  k_step_nudge<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, dv, len, alpha, tau);
+  ++g_nmfb_launches, k_step_nudge<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, dv, len, alpha, tau);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -1035,8 +1035,8 @@ extern "C" int nmfb_kkt_sums(const double* X, const double* R, const double* gX,
                              const double* Yt, const double* S, const double* gY, long ny,
                              double mux, double muy, double* out, double* work, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  k_kkt_partial<<<RED_BLOCKS, 256, 0, st>>>(X, R, gX, nx, Yt, S, gY, ny, mux, muy, work);
-  k_finish_kkt<<<1, 256, 0, st>>>(work, RED_BLOCKS, out);
+  ++g_nmfb_launches, k_kkt_partial<<<RED_BLOCKS, 256, 0, st>>>(X, R, gX, nx, Yt, S, gY, ny, mux, muy, work);
+  ++g_nmfb_launches, k_finish_kkt<<<1, 256, 0, st>>>(work, RED_BLOCKS, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -1046,8 +1046,8 @@ extern "C" int nmfb_affine_mu(const double* X, const double* dX, const double* R
                               const double* S, const double* dS, long ny, double a1, double a2,
                               double* out, double* work, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  k_affine_partial<<<RED_BLOCKS, 256, 0, st>>>(X, dX, R, dR, nx, Yt, dY, S, dS, ny, a1, a2, work);
-  k_finish_sum1<<<1, 256, 0, st>>>(work, RED_BLOCKS, out);
+  ++g_nmfb_launches, k_affine_partial<<<RED_BLOCKS, 256, 0, st>>>(X, dX, R, dR, nx, Yt, dY, S, dS, ny, a1, a2, work);
+  ++g_nmfb_launches, k_finish_sum1<<<1, 256, 0, st>>>(work, RED_BLOCKS, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -1055,7 +1055,7 @@ extern "C" int nmfb_affine_mu(const double* X, const double* dX, const double* R
 extern "C" int nmfb_clamp_min(double* v, long len, double lo, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (len <= 0) return NMFB_OK;
-  k_clamp_fill<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, len, lo);
+  ++g_nmfb_launches, k_clamp_fill<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, len, lo);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -1063,7 +1063,7 @@ extern "C" int nmfb_clamp_min(double* v, long len, double lo, void* stream) {
 extern "C" int nmfb_fill(double* v, long len, double c, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (len <= 0) return NMFB_OK;
-  k_fill<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, len, c);
+  ++g_nmfb_launches, k_fill<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, len, c);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

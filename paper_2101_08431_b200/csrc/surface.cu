@@ -510,7 +510,7 @@ extern "C" int nmfb_surface_nnls_batch(const double* ctc, const double* ctb, con
   const int threads = 128;
   const int blocks = (int)((nrhs + threads - 1) / threads);
 #define LAUNCH_NNLS(KK, SEEDS, MODE)                                                        \
-  k_nnls<KK><<<blocks, threads, 0, stream>>>(ctc, ctb, btb, SEEDS, MODE, tol, max_changes, \
+  ++g_nmfb_launches, k_nnls<KK><<<blocks, threads, 0, stream>>>(ctc, ctb, btb, SEEDS, MODE, tol, max_changes, \
                                              nrhs, (int)k, x, passive, changes, resid2, status)
   if (warm_mode != 1) {
 #define CALL(KK) LAUNCH_NNLS(KK, warm_passive, warm_mode)
@@ -533,7 +533,7 @@ extern "C" int nmfb_surface_nnls_batch(const double* ctc, const double* ctb, con
   const int ub = (int)((nrhs + 255) / 256);
   for (long pass = 0; pass <= nrhs; ++pass) {
     cudaMemsetAsync(flag_scratch, 0, sizeof(int), stream);
-    k_chain_update<<<ub, 256, 0, stream>>>(passive, seed_scratch, nrhs, (int)k, flag_scratch);
+    ++g_nmfb_launches, k_chain_update<<<ub, 256, 0, stream>>>(passive, seed_scratch, nrhs, (int)k, flag_scratch);
     int h_flag = 0;
     cudaMemcpyAsync(&h_flag, flag_scratch, sizeof(int), cudaMemcpyDeviceToHost, stream);
     if (cudaStreamSynchronize(stream) != cudaSuccess) return NMFB_ELAUNCH;
@@ -552,14 +552,14 @@ extern "C" int nmfb_surface_block_cholesky(const double* blocks_in, long nb, lon
   cudaStream_t stream = (cudaStream_t)stream_;
   if (k < 1 || k > NMFB_MAX_K || nb < 0) return NMFB_EINVAL;
   cudaMemsetAsync(out, 0, sizeof(double) * (size_t)nb * k * k, stream);
-  k_set_int<<<1, 1, 0, stream>>>(bad, INT_MAX);
+  ++g_nmfb_launches, k_set_int<<<1, 1, 0, stream>>>(bad, INT_MAX);
   if (nb == 0) return NMFB_OK;
   const int threads = 128;
   const int blocks = (int)((nb + threads - 1) / threads);
-#define CALL(KK) k_block_chol<KK><<<blocks, threads, 0, stream>>>(blocks_in, nb, (int)k, out, bad)
+#define CALL(KK) ++g_nmfb_launches, k_block_chol<KK><<<blocks, threads, 0, stream>>>(blocks_in, nb, (int)k, out, bad)
   NMFB_DISPATCH_K(k, CALL);
 #undef CALL
-  k_zero_after_bad<<<nmfb_blocks(nb * k * k, 256), 256, 0, stream>>>(out, nb, (int)k, bad);
+  ++g_nmfb_launches, k_zero_after_bad<<<nmfb_blocks(nb * k * k, 256), 256, 0, stream>>>(out, nb, (int)k, bad);
   NMFB_CHECK_LAUNCH();
   // the caller maps INT_MAX -> -1 (no failing block)
   return NMFB_OK;
@@ -574,9 +574,9 @@ extern "C" int nmfb_surface_block_solve_lower(const double* l, const double* b, 
   const int threads = 128;
   const int blocks = (int)((work + threads - 1) / threads);
   if (transposed)
-    k_block_trsm<true><<<blocks, threads, 0, stream>>>(l, b, nb, (int)k, (int)r, z);
+    ++g_nmfb_launches, k_block_trsm<true><<<blocks, threads, 0, stream>>>(l, b, nb, (int)k, (int)r, z);
   else
-    k_block_trsm<false><<<blocks, threads, 0, stream>>>(l, b, nb, (int)k, (int)r, z);
+    ++g_nmfb_launches, k_block_trsm<false><<<blocks, threads, 0, stream>>>(l, b, nb, (int)k, (int)r, z);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -591,7 +591,7 @@ extern "C" int nmfb_surface_back_substitute(const double* x_rows, const double* 
   const int threads = 64;
   const int blocks = (int)((n + threads - 1) / threads);
 #define CALL(KK)                                                                        \
-  k_back_sub_exact<KK><<<blocks, threads, 0, stream>>>(x_rows, y_cols, l, h, dy, resid, n, \
+  ++g_nmfb_launches, k_back_sub_exact<KK><<<blocks, threads, 0, stream>>>(x_rows, y_cols, l, h, dy, resid, n, \
                                                        m, (int)k, full, dx)
   NMFB_DISPATCH_K(k, CALL);
 #undef CALL
@@ -609,7 +609,7 @@ extern "C" int nmfb_surface_rhs_reduce(const double* x_rows, const double* y_col
   const int threads = 64;
   const int blocks = (int)((m + threads - 1) / threads);
 #define CALL(KK)                                                                           \
-  k_rhs_reduce_exact<KK><<<blocks, threads, 0, stream>>>(x_rows, y_cols, l, h, resid, n, m, \
+  ++g_nmfb_launches, k_rhs_reduce_exact<KK><<<blocks, threads, 0, stream>>>(x_rows, y_cols, l, h, resid, n, m, \
                                                          (int)k, full, r_acc)
   NMFB_DISPATCH_K(k, CALL);
 #undef CALL
@@ -628,7 +628,7 @@ extern "C" int nmfb_surface_schur_reduce(const double* x_rows, const double* y_c
   const int threads = 64;
   const int blocks = (int)((work + threads - 1) / threads);
 #define CALL(KK)                                                                              \
-  k_schur_exact<KK><<<blocks, threads, 0, stream>>>(x_rows, y_cols, l, h, resid, n, m, (int)k, \
+  ++g_nmfb_launches, k_schur_exact<KK><<<blocks, threads, 0, stream>>>(x_rows, y_cols, l, h, resid, n, m, (int)k, \
                                                     full, s_acc, r_acc)
   NMFB_DISPATCH_K(k, CALL);
 #undef CALL

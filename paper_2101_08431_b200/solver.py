@@ -58,6 +58,8 @@ class Problem:
             raise NativeLibraryError("no CUDA device: the B200 solver has no CPU fallback")
         self.lib = _lib.load()
         self.launches = 0
+        self.instrument = set()
+        self.event_log = []
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         if isinstance(M, np.ndarray):
             if M.dtype not in (np.float64, np.float32):
@@ -95,7 +97,16 @@ class Problem:
         return torch.cuda.current_stream(self.dev).cuda_stream
 
     def _call(self, name, *args):
-        rc = getattr(self.lib, name)(*args)
+        if name in self.instrument:  # CUDA events on the launching stream (bench roofline)
+            st = torch.cuda.current_stream(self.dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            rc = getattr(self.lib, name)(*args)
+            e1.record(st)
+            self.event_log.append((e0, e1))
+        else:
+            rc = getattr(self.lib, name)(*args)
         self.launches += 1
         if rc != 0:
             raise NativeLibraryError(f"{name} returned {rc}")

@@ -1,0 +1,131 @@
+"""Solver-level GPU parity: the device two-stage solver vs the CPU oracle driver.
+
+Same seeded inputs and initial factors (paper_2101_08431_b200.data); the bar is
+north_star's: identical active sets and iteration counts, factors/objective
+within 1e-10 relative (stage 1) and identical Armijo/flag decisions with
+factors within 1e-8 relative after a fixed number of IPM iterations.
+"""
+import numpy as np
+import pytest
+
+from oracle import driver as D
+
+pytestmark = pytest.mark.gpu
+
+TOL_STAGE1 = 1e-10
+TOL_IPM = 1e-8
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - b).max() / max(1e-300, np.abs(b).max()))
+
+
+@pytest.fixture(scope="module")
+def mods():
+    from paper_2101_08431_b200 import data, solver
+    from paper_2101_08431_b200.config import IpmParams, Stage1Config
+
+    return data, solver, IpmParams, Stage1Config
+
+
+def _instance(data, name, n=None, m=None):
+    cfg = data.CONFIGS[name]
+    if cfg.kind == "peaks":
+        return data.peaks(n or cfg.n, m or cfg.m, cfg.k, cfg.seed)[:3]
+    return data.dense(n or cfg.n, m or cfg.m, cfg.k, cfg.seed)[:3]
+
+
+@pytest.mark.parametrize("name,n,m", [("c1", None, None), ("c2", None, None),
+                                      ("c3", None, 60), ("c4", 2000, 300)])
+def test_stage1_parity(mods, name, n, m):
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = _instance(data, name, n, m)
+    k = X0.shape[1]
+    cfg = Stage1Config(fixed_sweeps=8) if name == "c4" else Stage1Config()
+    P = solver.Problem(M, k)
+    X, Yt, pX, pY, r = solver.run_stage1(P, P.to_dev(X0), P.to_dev(Y0.T), cfg)
+    ro = D.run_stage1(M, X0, Y0.T.copy(), D.Stage1Config(fixed_sweeps=cfg.fixed_sweeps))
+    assert r.sweeps == ro.sweeps
+    assert np.array_equal(pX.bool().cpu().numpy(), ro.pX)
+    assert np.array_equal(pY.bool().cpu().numpy(), ro.pY)
+    assert rel(X.cpu().numpy(), ro.X) < TOL_STAGE1
+    assert rel(Yt.cpu().numpy(), ro.Yt) < TOL_STAGE1
+    assert abs(r.trace[-1][1] - ro.trace[-1][1]) <= TOL_STAGE1 * ro.trace[-1][1]
+
+
+def test_stage1_fp32_storage(mods):
+    """c5-style fp32 M (fp64 accumulate/solve) vs the fp64 oracle on the rounded M: 1e-4."""
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = data.dense(3000, 400, 16, 105)[:3]
+    M32 = M.astype(np.float32)
+    P = solver.Problem(M32, 16)
+    X, Yt, pX, pY, r = solver.run_stage1(P, P.to_dev(X0), P.to_dev(Y0.T), Stage1Config(fixed_sweeps=5))
+    ro = D.run_stage1(M32.astype(np.float64), X0, Y0.T.copy(), D.Stage1Config(fixed_sweeps=5))
+    assert rel(X.cpu().numpy(), ro.X) < 1e-4 and rel(Yt.cpu().numpy(), ro.Yt) < 1e-4
+
+
+@pytest.mark.parametrize("name,barrier,iters", [("c1", "paper", 40), ("c1", "balanced", 60),
+                                                ("c2", "balanced", 35)])
+def test_ipm_parity(mods, name, barrier, iters):
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = _instance(data, name)
+    k = X0.shape[1]
+    ro = D.run_stage1(M, X0, Y0.T.copy())
+    eps = 1e-7
+    st = D.transition(ro.X, ro.Yt, M, eps)
+    P = solver.Problem(M, k)
+    X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), eps)
+    assert abs(mu - st.mu) <= 1e-12 * st.mu
+    eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(fixed_iters=iters, barrier=barrier))
+    D.set_schur_backend("numpy")
+    try:
+        ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=iters, barrier=barrier))
+    finally:
+        D.set_schur_backend("c")
+    assert r.iters == ro2.iters and r.outer == ro2.outer
+    assert r.armijo_t == ro2.armijo_t
+    assert r.flags == ro2.flags
+    for a, b in ((eng.X, ro2.state.X), (eng.Yt, ro2.state.Yt)):
+        assert rel(a.cpu().numpy(), b) < TOL_IPM
+    assert abs(eng.mu - ro2.state.mu) <= TOL_IPM * ro2.state.mu
+
+
+def test_ipm_full_hessian_exercised(mods):
+    """c2 balanced switches to the full Hessian (sigma <= sigma_c) within 35 iterations."""
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = _instance(data, "c2")
+    ro = D.run_stage1(M, X0, Y0.T.copy())
+    P = solver.Problem(M, 3)
+    X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), 1e-7)
+    eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(fixed_iters=35, barrier="balanced"))
+    assert any(r.flags)
+
+
+def test_two_stage_c1(mods):
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = _instance(data, "c1")
+    rep = solver.run_two_stage(M, X0, Y0, tol_rel=1e-10, ipm=IpmParams(max_iter=80))
+    ref = D.run_two_stage(M, X0, Y0, tol_rel=1e-10, ipm=D.IpmParams(max_iter=80))
+    assert rep.stage1.sweeps == ref.stage1.sweeps
+    assert rep.ipm.iters == ref.ipm.iters and rep.ipm.armijo_t == ref.ipm.armijo_t
+    assert abs(rep.eps_abs - ref.eps_abs) <= 1e-12 * ref.eps_abs
+    assert rel(rep.X, ref.X) < TOL_IPM and rel(rep.Yt, ref.Yt) < TOL_IPM
+    assert abs(rep.final_objective - ref.objective) <= TOL_IPM * ref.objective
+
+
+def test_dense_k10_ipm_small(mods):
+    """Dense generator with k = 10 (c4 family) on a slice the oracle finishes quickly."""
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = data.dense(400, 40, 10, 104)[:3]
+    ro = D.run_stage1(M, X0, Y0.T.copy(), D.Stage1Config(fixed_sweeps=6))
+    st = D.transition(ro.X, ro.Yt, M, 1e-7)
+    P = solver.Problem(M, 10)
+    X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), 1e-7)
+    eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(fixed_iters=8))
+    D.set_schur_backend("numpy")
+    try:
+        ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=8))
+    finally:
+        D.set_schur_backend("c")
+    assert r.armijo_t == ro2.armijo_t and r.flags == ro2.flags
+    assert rel(eng.X.cpu().numpy(), ro2.state.X) < TOL_IPM
