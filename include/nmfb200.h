@@ -183,6 +183,22 @@ int nmfb_fill(double *v, long len, double c, void *stream);
 int nmfb_dense_cholesky(double *A, long N, int *info, void *stream);
 int nmfb_dense_solve(const double *L, long N, double *b, void *stream);
 
+/* Exact low-rank Gauss-Newton reduced-system solve (replaces the dense mk x mk
+ * spd_solve when the coupling is C-bar, PAPER Eq. 12): S = U Zb U^T with
+ * U = Y^T (x) I_k has rank <= k^2.
+ *   nmfb_d_factor:       D_j = X^T X + rho I + Diag(s_j/y_j) = LD_j LD_j^T, packed D_j^{-1}, y_j y_j^T
+ *   nmfb_lowrank_factor: LG = chol(G), G = U^T D^{-1} U; LH = chol(I - LG^T Zb LG); *info = -1 iff
+ *                        the reduced matrix is positive definite.  work >= 2 k^4 doubles (Zb kept
+ *                        in work[0, k^4) for the solves)
+ *   nmfb_lowrank_solve:  dy = (D - U Zb U^T)^{-1} rhs */
+int nmfb_d_factor(const double *XtX, const double *Yt, const double *S, double rho, long m,
+                  long k, double *LD, double *Dinvpk, double *YYpk, int *bad, void *stream);
+int nmfb_lowrank_factor(const double *Zpk, const double *Gpk, long k, double *LG, double *LH,
+                        double *work, int *info, void *stream);
+int nmfb_lowrank_solve(const double *LD, const double *Yt, const double *LG, const double *LH,
+                       const double *Zb, long m, long k, const double *rhs, double *dy, double *u,
+                       double *w, double *cwork, long cwork_len, void *stream);
+
 /* number of kernel launches issued by this library so far (host counter) */
 unsigned long long nmfb_launch_count(void);
 

@@ -90,6 +90,7 @@ class IpmParams:
     max_backtracks: int = 60
     fixed_iters: int = 0  # >0: run exactly this many inner iterations
     barrier: str = "paper"  # "paper": one mu (PAPER Eq. 4); "balanced": see barrier_weights
+    schur_solver: str = "dense"  # the oracle always factors the dense mk x mk matrix
 
 
 @dataclass

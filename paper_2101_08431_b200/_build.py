@@ -25,6 +25,7 @@ SOURCES = {
     "anls.cu": [],
     "ipm.cu": [],
     "dense.cu": [],
+    "lowrank.cu": [],
     "runtime.cu": [],
 }
 

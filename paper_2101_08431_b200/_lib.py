@@ -54,6 +54,9 @@ SIGNATURES = {
     "nmfb_dense_cholesky": [P, L, P, P],
     "nmfb_dense_solve": [P, L, P, P],
     "nmfb_launch_count": [],
+    "nmfb_d_factor": [P, P, P, D, L, L, P, P, P, P, P],
+    "nmfb_lowrank_factor": [P, P, L, P, P, P, P, P],
+    "nmfb_lowrank_solve": [P, P, P, P, P, L, L, P, P, P, P, P, L, P],
 }
 RESTYPES = {"nmfb_colprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
             "nmfb_launch_count": ctypes.c_ulonglong}

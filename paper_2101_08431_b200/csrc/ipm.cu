@@ -626,18 +626,17 @@ __global__ void __launch_bounds__(256) k_barrier_trials(const double* __restrict
   }
 }
 
-// out[t*2 + c] = sum_b part[t][b][c]
+// out[t*2 + c] = sum_b part[t][b][c]  (one warp per (t, c), fixed order)
 __global__ void k_finish_trials(const double* __restrict__ part, int nb, int nt,
                                 double* __restrict__ out) {
-  __shared__ double sh[32];
-  for (int t = 0; t < nt; ++t)
-    for (int c = 0; c < 2; ++c) {
-      double v = 0.0;
-      for (int b = threadIdx.x; b < nb; b += blockDim.x) v += part[((long)t * nb + b) * 2 + c];
-      v = block_sum(v, sh);
-      if (threadIdx.x == 0) out[t * 2 + c] = v;
-      __syncthreads();
-    }
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= 2 * nt) return;
+  const int t = w >> 1, c = w & 1;
+  double v = 0.0;
+  for (int b = lane; b < nb; b += 32) v += part[((long)t * nb + b) * 2 + c];
+  v = warp_sum(v);
+  if (lane == 0) out[t * 2 + c] = v;
 }
 
 // v <- v + alpha dv, entries that are not strictly positive become (1-tau) v
@@ -1016,7 +1015,7 @@ extern "C" int nmfb_barrier_trials(const double* X, const double* dX, long nx, c
   if (work_len < 2L * nb * ntrials) return NMFB_ENOMEM;
   dim3 grid(nb, ntrials);
   ++g_nmfb_launches, k_barrier_trials<<<grid, 256, 0, st>>>(X, dX, nx, Yt, dYt, ny, alpha_max, work);
-  ++g_nmfb_launches, k_finish_trials<<<1, 256, 0, st>>>(work, nb, ntrials, out);
+  ++g_nmfb_launches, k_finish_trials<<<(2 * ntrials * 32 + 255) / 256, 256, 0, st>>>(work, nb, ntrials, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

@@ -248,8 +248,16 @@ class IpmEngine:
         self.GY, self.XtX, self.H, self.Gdy = b(k, k), b(k, k), b(k, k), b(k, k)
         N = m * k
         self.N = N
-        self.A = b(N, N)
+        self.dense_gn = p.schur_solver == "dense"
+        self.A = None  # dense mk x mk reduced matrix: allocated on first full-C / dense use
         self.rhs = b(N)
+        self.dYbuf = b(m, k)
+        Q = k * k
+        self.LD, self.Dinvpk, self.YYpk = b(m, k, k), b(m, self.kk), b(m, self.kk)
+        self.Gpk = b(self.kk, self.kk)
+        self.LG, self.LH, self.lrwork = b(Q, Q), b(Q, Q), b(2 * Q * Q)
+        self.uvec, self.wvec = b(Q), b(Q)
+        self.fact_dense = False
         self.dX, self.dR, self.dS = b(n, k), b(n, k), b(m, k)
         self.FtG, self.FdY = b(m, k), b(n, k)
         self.Xf, self.Ytf = b(n, k), b(m, k)
@@ -284,14 +292,30 @@ class IpmEngine:
             self.Pbuf = self.P.buf(self.n, self.k ** 3)
             self.W = self.P.buf(self.m, self.k ** 3)
 
+    def _ensure_dense(self):
+        if self.A is None:
+            self.A = self.P.buf(self.N, self.N)
+
+    def lowrank_solve(self, rhs, dY, Yt):
+        P = self.P
+        P._call("nmfb_lowrank_solve", _p(self.LD), _p(Yt), _p(self.LG), _p(self.LH),
+                _p(self.lrwork), self.m, self.k, _p(rhs), _p(dY), _p(self.uvec), _p(self.wvec),
+                _p(P.cwork), P.cwork.numel(), P.stream)
+
     def direction(self, full):
-        """Newton direction. Returns (gtp, a1max, a2max, info_ok)."""
+        """Newton direction; scalars land in dscal[4:7], codes in iscal[2:4].
+
+        Gauss-Newton coupling: exact low-rank solve of the reduced system
+        (csrc/lowrank.cu); full coupling (or schur_solver="dense"): dense
+        mk x mk assembly + blocked Cholesky (csrc/ipm.cu, csrc/dense.cu).
+        """
         P = self.P
         n, m, k, N, s = self.n, self.m, self.k, self.N, P.stream
         mux, muy = self.wx * self.mu, self.wy * self.mu
         X, Yt, F = self.X, self.Yt, self.Fcur
         P.colprod(Yt, m, k, Yt, k, self.GY)
         P.colprod(X, n, k, X, k, self.XtX)
+        dense = full or self.dense_gn
         P._call("nmfb_r1_factor", _p(self.GY), _p(X), _p(self.R), _p(self.gX), mux, self.rho, n,
                 k, _p(self.L), _p(self.h), _p(self.g), _p(self.Apk), _p(self.XXpk),
                 _p(P.iscal[2:]), s)
@@ -306,15 +330,27 @@ class IpmEngine:
                     self.awork.numel(), s)
             P.colprod(F, n, m, self.g, k, self.FtG)
             W, FtG = self.W, self.FtG
-        P._call("nmfb_schur_assemble", _p(Yt), _p(self.S), m, k, _p(self.Z), _p(self.XtX),
-                self.rho, _p(W), _p(self.A), s)
-        if full:
-            P._call("nmfb_schur_term4", _p(F), n, m, k, _p(self.Apk), _p(self.A), s)
         P._call("nmfb_schur_rhs", _p(Yt), _p(self.gY), _p(self.H), _p(FtG), muy, m, k,
                 _p(self.rhs), s)
-        P._call("nmfb_dense_cholesky", _p(self.A), N, _p(P.iscal[3:]), s)
-        P._call("nmfb_dense_solve", _p(self.A), N, _p(self.rhs), s)
-        dY = self.rhs.view(m, k)
+        dY = self.dYbuf
+        if dense:
+            self._ensure_dense()
+            P._call("nmfb_schur_assemble", _p(Yt), _p(self.S), m, k, _p(self.Z), _p(self.XtX),
+                    self.rho, _p(W), _p(self.A), s)
+            if full:
+                P._call("nmfb_schur_term4", _p(F), n, m, k, _p(self.Apk), _p(self.A), s)
+            P._call("nmfb_dense_cholesky", _p(self.A), N, _p(P.iscal[3:]), s)
+            dY.copy_(self.rhs.view(m, k))
+            P._call("nmfb_dense_solve", _p(self.A), N, _p(dY), s)
+        else:
+            P._call("nmfb_d_factor", _p(self.XtX), _p(Yt), _p(self.S), self.rho, m, k,
+                    _p(self.LD), _p(self.Dinvpk), _p(self.YYpk), _p(P.iscal[4:]), s)
+            P._call("nmfb_atb", _p(self.YYpk), m, self.kk, _p(self.Dinvpk), self.kk, _p(self.Gpk),
+                    _p(self.awork), self.awork.numel(), s)
+            P._call("nmfb_lowrank_factor", _p(self.Z), _p(self.Gpk), k, _p(self.LG), _p(self.LH),
+                    _p(self.lrwork), _p(P.iscal[3:]), s)
+            self.lowrank_solve(self.rhs, dY, Yt)
+        self.last_dense = dense
         P.colprod(Yt, m, k, dY, k, self.Gdy)
         FdY = None
         if full:
@@ -340,6 +376,7 @@ class IpmEngine:
         self.Ytf.copy_(self.Yt)
         self.have_fact = True
         self.fact_full = full
+        self.fact_dense = self.last_dense
         self.fact_F = self.fi
 
     def predictor_sigma(self, sums):
@@ -356,8 +393,12 @@ class IpmEngine:
             FtG = self.FtG
         P._call("nmfb_schur_rhs", _p(self.Ytf), _p(self.gY), _p(self.H), _p(FtG), 0.0, m, k,
                 _p(self.rhs), s)
-        P._call("nmfb_dense_solve", _p(self.A), N, _p(self.rhs), s)
-        dY = self.rhs.view(m, k)
+        dY = self.dYbuf
+        if self.fact_dense:
+            dY.copy_(self.rhs.view(m, k))
+            P._call("nmfb_dense_solve", _p(self.A), N, _p(dY), s)
+        else:
+            self.lowrank_solve(self.rhs, dY, self.Ytf)
         P.colprod(self.Ytf, m, k, dY, k, self.Gdy)
         FdY = None
         if full:
@@ -411,9 +452,11 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
             if not ok:
                 dY = eng.direction(False)
                 eng.armijo_launch(dY)
-                v, iv = P.readback(32 + 2 * NTRIALS, 4)
+                v, iv = P.readback(32 + 2 * NTRIALS, 5)
                 if int(iv[2]) != _NONE:
                     raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
+                if not eng.last_dense and int(iv[4]) != _NONE:
+                    raise NotPositiveDefinite("R2 block not positive definite", int(iv[4]))
                 if int(iv[3]) >= 0:
                     raise NotPositiveDefinite("Gauss-Newton Schur matrix not positive definite",
                                               int(iv[3]))
