@@ -125,3 +125,37 @@ def test_dense_k10_ipm_small(mods):
         D.set_schur_backend("c")
     assert r.armijo_t == ro2.armijo_t and r.flags == ro2.flags
     assert rel(eng.X.cpu().numpy(), ro2.state.X) < TOL_IPM
+
+
+@pytest.mark.parametrize("solve", ["lowrank", "dense"])
+def test_device_newton_vs_dense_kkt(mods, solve):
+    """SPEC.md:593 acceptance 2 on the device: direction == dense solve of Eq. (10)."""
+    from tests.test_spec_oracle import _dense_kkt
+
+    data, solver, IpmParams, Stage1Config = mods
+    rng = np.random.default_rng(22)
+    checked = 0
+    for trial in range(30):
+        n, m, k = [(8, 4, 2), (12, 5, 2), (10, 6, 3), (40, 9, 4)][trial % 4]
+        X = rng.uniform(0.1, 1, (n, k))
+        Yt = rng.uniform(0.1, 1, (m, k))
+        M = rng.uniform(0, 1, (n, m))
+        R, S = rng.uniform(0.1, 1, (n, k)), rng.uniform(0.1, 1, (m, k))
+        mu, rho = float(rng.uniform(0.01, 0.5)), 1e-3
+        P = solver.Problem(M, k)
+        eng = solver.IpmEngine(P, P.to_dev(X), P.to_dev(Yt), P.to_dev(R), P.to_dev(S), mu, rho,
+                               IpmParams(schur_solver=solve))
+        eng.refresh()
+        for full in (False, True):
+            dY = eng.direction(full)
+            v, iv = P.readback(8, 5)
+            st = D.IpmState(X, Yt, R, S, mu, rho)
+            if int(iv[3]) >= 0:
+                assert full, "Gauss-Newton reduced system must be positive definite"
+                continue
+            ref = _dense_kkt(st, M, full)
+            got = (eng.dX.cpu().numpy(), dY.cpu().numpy(), eng.dR.cpu().numpy(), eng.dS.cpu().numpy())
+            for a, b in zip(got, ref):
+                assert np.abs(a - b).max() <= 1e-8 * max(1.0, np.abs(b).max()), (trial, full)
+            checked += 1
+    assert checked >= 30

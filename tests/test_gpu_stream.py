@@ -1,0 +1,32 @@
+"""Streaming column append (config c3 semantics) on the GPU vs the oracle session."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_stream_parity_small():
+    from oracle import driver as D
+    from oracle import stream as OS
+    from paper_2101_08431_b200 import data
+    from paper_2101_08431_b200.config import IpmParams
+    from paper_2101_08431_b200.stream import StreamSession
+
+    M, X0, Y0, _, _ = data.peaks(600, 60, 4, 103)
+    D.set_schur_backend("numpy")
+    try:
+        so = OS.OracleStream(M[:, :20], X0, Y0[:, :20], ipm_factory=lambda: D.IpmParams(fixed_iters=6))
+        sg = StreamSession(M[:, :20], X0, Y0[:, :20], ipm_factory=lambda: IpmParams(fixed_iters=6))
+        for m0 in range(20, 60, 10):
+            so.append(M[:, m0:m0 + 10])
+            sg.append(M[:, m0:m0 + 10])
+    finally:
+        D.set_schur_backend("c")
+    assert len(so.chunks) == len(sg.chunks) == 5
+    for (mo, _, ro), (mg, _, rg) in zip(so.chunks, sg.chunks):
+        assert mo == mg
+        assert ro.stage1.sweeps == rg.stage1.sweeps
+        assert np.array_equal(ro.stage1.pY, rg.stage1.pY)
+        assert ro.ipm.armijo_t == rg.ipm.armijo_t
+        rel = np.abs(rg.Yt - ro.Yt).max() / np.abs(ro.Yt).max()
+        assert rel < 1e-7, (mo, rel)
