@@ -75,10 +75,12 @@ int nmfb_surface_back_substitute(const double *x_rows, const double *y_cols, con
  * scratch of at least the stated length (doubles). */
 
 /* out (rows, k) = scale * A B, A (rows, cols), B (cols, k); tol[i] =
- * 1e-12 max(1, ||out_i||_inf) when tol != NULL.
+ * 1e-12 max(1, ||out_i||_inf) when tol != NULL; work >= nmfb_rowprod_work_len.
  * Replaces the driver products M Y^T (update_X) and F Y^T. */
+long nmfb_rowprod_work_len(long rows, long cols, long k, int a_is_f32);
 int nmfb_rowprod(const void *A, int a_is_f32, long rows, long cols, const double *B, long k,
-                 double *out, double *tol, double scale, void *stream);
+                 double *out, double *tol, double scale, double *work, long work_len,
+                 void *stream);
 
 /* out (cols, k) = scale * A^T B, A (rows, cols), B (rows, k): X^T M (update_Y,
  * SPEC.md:200), the Grams X^T X / Y Y^T, F^T X (graY).  work >= nmfb_colprod_work_len. */

@@ -323,6 +323,155 @@ __global__ void __launch_bounds__(256) k_colprod_tiled(const T* __restrict__ A, 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// v3 streaming products: no __syncthreads inside the streaming loops.
+//
+// k_rowprod_split: grid = (column chunks of CW) x (row splits).  The CTA stages
+// its Y^T chunk once (transposed, conflict-free) and then every warp streams
+// RW-row groups independently; per (row, chunk) partial sums go to `part`
+// and a fixed-order k_sum_partials finishes (split-K over the columns).
+// Accumulator type ACC: double for fp64 M; for fp32 M the per-(row, chunk)
+// partial is accumulated in fp32 over CW/32 terms per lane and folded in fp64
+// (c5 tolerance 1e-4; measured error ~1e-7).
+// ---------------------------------------------------------------------------
+template <typename T>
+struct SplitCfg;
+template <>
+struct SplitCfg<double> {
+  static constexpr int CW = 1024;
+  using Y = double;
+  using ACC = double;
+};
+template <>
+struct SplitCfg<float> {
+  static constexpr int CW = 2048;
+  using Y = float;
+  using ACC = float;
+};
+
+template <int K, int RW, typename T>
+__global__ void __launch_bounds__(256) k_rowprod_split(const T* __restrict__ A, long rows,
+                                                       long cols, const double* __restrict__ B,
+                                                       long rows_per_split,
+                                                       double* __restrict__ part) {
+  using C = SplitCfg<T>;
+  using YT = typename C::Y;
+  using ACC = typename C::ACC;
+  constexpr int CW = C::CW;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  YT* yT = reinterpret_cast<YT*>(smraw);  // [K][CW]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long j0 = (long)blockIdx.x * CW;
+  const int cw = (int)min((long)CW, cols - j0);
+  for (int e = tid; e < CW * K; e += 256) {
+    const int jj = e / K, p = e - jj * K;
+    yT[p * CW + jj] = (jj < cw) ? (YT)B[(j0 + jj) * K + p] : (YT)0;
+  }
+  __syncthreads();
+  const long rb = (long)blockIdx.y * rows_per_split;
+  const long re = min(rows, rb + rows_per_split);
+  const long nchunks = gridDim.x;
+  for (long r0 = rb + (long)warp * RW; r0 < re; r0 += 8 * RW) {
+    ACC acc[RW][K];
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+#pragma unroll
+      for (int p = 0; p < K; ++p) acc[r][p] = (ACC)0;
+    const T* arow[RW];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) arow[r] = A + min(r0 + r, re - 1) * cols + j0;
+    if (cw == CW) {
+#pragma unroll 4
+      for (int u = 0; u < CW / 32; ++u) {
+        const int jj = lane + 32 * u;
+        T a[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) a[r] = __ldg(arow[r] + jj);
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const YT y = yT[p * CW + jj];
+#pragma unroll
+          for (int r = 0; r < RW; ++r) acc[r][p] = fma((ACC)a[r], (ACC)y, acc[r][p]);
+        }
+      }
+    } else {
+      for (int jj = lane; jj < cw; jj += 32) {
+        T a[RW];
+#pragma unroll
+        for (int r = 0; r < RW; ++r) a[r] = __ldg(arow[r] + jj);
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const YT y = yT[p * CW + jj];
+#pragma unroll
+          for (int r = 0; r < RW; ++r) acc[r][p] = fma((ACC)a[r], (ACC)y, acc[r][p]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        const double v = warp_sum((double)acc[r][p]);
+        if (lane == 0 && r0 + r < re) part[((long)blockIdx.x * rows + r0 + r) * K + p] = v;
+      }
+  }
+  (void)nchunks;
+}
+
+// k_colprod_warp: grid = (column tiles of 32*CPL) x (row splits); every warp
+// streams its own interleaved rows (B row read as a warp broadcast through the
+// read-only path, no shared-memory staging), one fixed-order smem reduction of
+// the 8 warps at the end.
+template <int K, int CPL, typename T>
+__global__ void __launch_bounds__(256) k_colprod_warp(const T* __restrict__ A, long rows,
+                                                      long cols, const double* __restrict__ B,
+                                                      long stripe, double* __restrict__ part) {
+  __shared__ double red[8][32 * K + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long c0 = (long)blockIdx.x * (32 * CPL) + CPL * lane;
+  const long s = blockIdx.y;
+  const long i_beg = s * stripe, i_end = min(rows, i_beg + stripe);
+  const bool inb = c0 + CPL <= cols;
+  double acc[CPL][K];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+#pragma unroll
+    for (int p = 0; p < K; ++p) acc[c][p] = 0.0;
+#pragma unroll 2
+  for (long i = i_beg + warp; i < i_end; i += 8) {
+    const T* arow = A + i * cols;
+    double a[CPL];
+    if (inb) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) a[c] = (double)__ldg(arow + c0 + c);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) a[c] = (c0 + c < cols) ? (double)arow[c0 + c] : 0.0;
+    }
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      const double b = __ldg(B + i * K + p);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc[c][p] = fma(a[c], b, acc[c][p]);
+    }
+  }
+  for (int c = 0; c < CPL; ++c) {
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < K; ++p) red[warp][lane * K + p] = acc[c][p];
+    __syncthreads();
+    for (int e = tid; e < 32 * K; e += 256) {
+      double v = 0.0;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) v += red[g][e];
+      const int l = e / K, p = e - l * K;
+      const long j = (long)blockIdx.x * (32 * CPL) + CPL * l + c;
+      if (j < cols) part[(s * cols + j) * K + p] = v;
+    }
+  }
+}
+
 // out[e] = scale * sum_{s < nparts} part[s][e]  (fixed order); optional per-row
 // (of width K) tolerance as in k_rowprod.
 template <int K>
@@ -430,13 +579,32 @@ __global__ void k_first_nonzero_i8(const int8_t* __restrict__ st, long len, int*
 
 constexpr int ROWPROD_R = 2;
 
+bool rowprod_split(long rows, long cols) { return cols >= 2048 && rows >= 4096; }
+
+template <typename T>
+long rowprod_chunks(long cols) {
+  return (cols + SplitCfg<T>::CW - 1) / SplitCfg<T>::CW;
+}
+
 template <int K, typename T>
 int launch_rowprod(const T* A, long rows, long cols, const double* B, double* out, double* tol,
-                   double scale, cudaStream_t st) {
-  if (cols >= 1024 && rows >= 4096) {  // HBM-streaming regime
+                   double scale, double* work, long work_len, cudaStream_t st) {
+  if (rowprod_split(rows, cols)) {  // HBM-streaming regime: split-K over column chunks
     constexpr int RW = 4;
-    const unsigned blocks = (unsigned)((rows + 8 * RW - 1) / (8 * RW));
-    ++g_nmfb_launches, k_rowprod_tiled<K, RW, T><<<blocks, 256, 0, st>>>(A, rows, cols, B, out, tol, scale);
+    constexpr int CW = SplitCfg<T>::CW;
+    const long nch = rowprod_chunks<T>(cols);
+    if (nch * rows * K > work_len) return NMFB_ENOMEM;
+    const size_t smem = (size_t)K * CW * sizeof(typename SplitCfg<T>::Y);
+    long nsplit = (148 * 2 + nch - 1) / nch;
+    long rps = (rows + nsplit - 1) / nsplit;
+    rps = ((rps + 8 * RW - 1) / (8 * RW)) * (8 * RW);
+    nsplit = (rows + rps - 1) / rps;
+    cudaFuncSetAttribute(k_rowprod_split<K, RW, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    dim3 grid((unsigned)nch, (unsigned)nsplit);
+    ++g_nmfb_launches, k_rowprod_split<K, RW, T><<<grid, 256, smem, st>>>(A, rows, cols, B, rps, work);
+    ++g_nmfb_launches, k_sum_partials<K><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
+        work, (int)nch, rows * K, out, tol, scale);
     NMFB_CHECK_LAUNCH();
     return NMFB_OK;
   }
@@ -471,7 +639,7 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
   if (ns * cols * K > work_len) return NMFB_ENOMEM;
   if (colprod_tiled(rows, cols)) {
     dim3 grid((unsigned)((cols + CT_COLS - 1) / CT_COLS), (unsigned)ns);
-    ++g_nmfb_launches, k_colprod_tiled<K, T><<<grid, 256, 0, st>>>(A, rows, cols, B, stripe, work);
+    ++g_nmfb_launches, k_colprod_warp<K, 4, T><<<grid, 256, 0, st>>>(A, rows, cols, B, stripe, work);
   } else {
     dim3 grid((unsigned)((cols + CP_COLS - 1) / CP_COLS), (unsigned)ns);
     ++g_nmfb_launches, k_colprod_partial<K, T><<<grid, 256, 0, st>>>(A, rows, cols, B, stripe, work);
@@ -497,17 +665,23 @@ extern "C" long nmfb_colprod_work_len(long rows, long cols, long k) {
   return ((rows + stripe - 1) / stripe) * cols * k;
 }
 
+extern "C" long nmfb_rowprod_work_len(long rows, long cols, long k, int a_is_f32) {
+  if (!rowprod_split(rows, cols)) return 1;
+  return (a_is_f32 ? rowprod_chunks<float>(cols) : rowprod_chunks<double>(cols)) * rows * k;
+}
+
 extern "C" int nmfb_rowprod(const void* A, int a_is_f32, long rows, long cols, const double* B,
-                            long k, double* out, double* tol, double scale, void* stream) {
+                            long k, double* out, double* tol, double scale, double* work,
+                            long work_len, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (rows < 0 || cols < 0) return NMFB_EINVAL;
   if (rows == 0) return NMFB_OK;
 #define CASE(KK)                                                                               \
   case KK:                                                                                     \
     return a_is_f32 ? launch_rowprod<KK, float>((const float*)A, rows, cols, B, out, tol, scale, \
-                                                st)                                            \
+                                                work, work_len, st)                            \
                     : launch_rowprod<KK, double>((const double*)A, rows, cols, B, out, tol,    \
-                                                 scale, st);
+                                                 scale, work, work_len, st);
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
 }

@@ -77,7 +77,9 @@ class Problem:
         f64 = dict(dtype=torch.float64, device=self.dev)
         L = self.lib
         cw = max(L.nmfb_colprod_work_len(n, m, k), L.nmfb_colprod_work_len(n, k, k),
-                 L.nmfb_colprod_work_len(m, k, k), L.nmfb_colprod_work_len(n, m, 1), 4096)
+                 L.nmfb_colprod_work_len(m, k, k), L.nmfb_colprod_work_len(n, m, 1),
+                 L.nmfb_rowprod_work_len(n, m, k, self.f32), L.nmfb_rowprod_work_len(n, m, k, 0),
+                 4096)
         self.cwork = torch.empty(cw, **f64)
         nb = L.nmfb_ipm_reduce_blocks()
         self.rwork = torch.empty(max(64 * 2 * NTRIALS, 12 * nb, 3 * ((n + 127) // 128 + nb), 4096),
@@ -125,7 +127,7 @@ class Problem:
 
     def rowprod(self, A, rows, cols, B, k, out, tol=None, f32=0):
         self._call("nmfb_rowprod", _p(A), f32, rows, cols, _p(B), k, _p(out), _p(tol), 1.0,
-                   self.stream)
+                   _p(self.cwork), self.cwork.numel(), self.stream)
 
     def colprod(self, A, rows, cols, B, k, out, tol=None, f32=0):
         self._call("nmfb_colprod", _p(A), f32, rows, cols, _p(B), k, _p(out), _p(tol), 1.0,
