@@ -351,14 +351,17 @@ struct SplitCfg<float> {
 };
 
 template <int K, int RW, typename T>
-__global__ void __launch_bounds__(256) k_rowprod_split(const T* __restrict__ A, long rows,
-                                                       long cols, const double* __restrict__ B,
-                                                       long rows_per_split,
-                                                       double* __restrict__ part) {
+__global__ void __launch_bounds__(256, 2) k_rowprod_split(const T* __restrict__ A, long rows,
+                                                          long cols, const double* __restrict__ B,
+                                                          long rows_per_split,
+                                                          double* __restrict__ part) {
   using C = SplitCfg<T>;
   using YT = typename C::Y;
   using ACC = typename C::ACC;
+  using V = typename Vec2<T>::type;
+  using VY = typename Vec2<YT>::type;
   constexpr int CW = C::CW;
+  constexpr int UN = 2;  // column-pair iterations whose loads are issued together
   extern __shared__ __align__(16) unsigned char smraw[];
   YT* yT = reinterpret_cast<YT*>(smraw);  // [K][CW]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(256) k_rowprod_split(const T* __restrict__ A, 
   __syncthreads();
   const long rb = (long)blockIdx.y * rows_per_split;
   const long re = min(rows, rb + rows_per_split);
-  const long nchunks = gridDim.x;
+  const bool vec = (cw == CW) && ((cols & 1) == 0);
   for (long r0 = rb + (long)warp * RW; r0 < re; r0 += 8 * RW) {
     ACC acc[RW][K];
 #pragma unroll
@@ -381,18 +384,24 @@ __global__ void __launch_bounds__(256) k_rowprod_split(const T* __restrict__ A, 
     const T* arow[RW];
 #pragma unroll
     for (int r = 0; r < RW; ++r) arow[r] = A + min(r0 + r, re - 1) * cols + j0;
-    if (cw == CW) {
-#pragma unroll 4
-      for (int u = 0; u < CW / 32; ++u) {
-        const int jj = lane + 32 * u;
-        T a[RW];
+    if (vec) {
+      for (int u0 = 0; u0 < CW / 64; u0 += UN) {
+        V a[UN][RW];
 #pragma unroll
-        for (int r = 0; r < RW; ++r) a[r] = __ldg(arow[r] + jj);
+        for (int uu = 0; uu < UN; ++uu)
 #pragma unroll
-        for (int p = 0; p < K; ++p) {
-          const YT y = yT[p * CW + jj];
+          for (int r = 0; r < RW; ++r)
+            a[uu][r] = __ldg(reinterpret_cast<const V*>(arow[r] + 2 * lane + 64 * (u0 + uu)));
 #pragma unroll
-          for (int r = 0; r < RW; ++r) acc[r][p] = fma((ACC)a[r], (ACC)y, acc[r][p]);
+        for (int uu = 0; uu < UN; ++uu) {
+          const int jj = 2 * lane + 64 * (u0 + uu);
+#pragma unroll
+          for (int p = 0; p < K; ++p) {
+            const VY y = *reinterpret_cast<const VY*>(yT + p * CW + jj);
+#pragma unroll
+            for (int r = 0; r < RW; ++r)
+              acc[r][p] = fma((ACC)a[uu][r].x, (ACC)y.x, fma((ACC)a[uu][r].y, (ACC)y.y, acc[r][p]));
+          }
         }
       }
     } else {
@@ -416,7 +425,6 @@ __global__ void __launch_bounds__(256) k_rowprod_split(const T* __restrict__ A, 
         if (lane == 0 && r0 + r < re) part[((long)blockIdx.x * rows + r0 + r) * K + p] = v;
       }
   }
-  (void)nchunks;
 }
 
 // k_colprod_warp: grid = (column tiles of 32*CPL) x (row splits); every warp
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(256) k_rowprod_split(const T* __restrict__ A, 
 // read-only path, no shared-memory staging), one fixed-order smem reduction of
 // the 8 warps at the end.
 template <int K, int CPL, typename T>
-__global__ void __launch_bounds__(256) k_colprod_warp(const T* __restrict__ A, long rows,
+__global__ void __launch_bounds__(256, 2) k_colprod_warp(const T* __restrict__ A, long rows,
                                                       long cols, const double* __restrict__ B,
                                                       long stripe, double* __restrict__ part) {
   __shared__ double red[8][32 * K + 1];
@@ -442,9 +450,14 @@ __global__ void __launch_bounds__(256) k_colprod_warp(const T* __restrict__ A, l
   for (long i = i_beg + warp; i < i_end; i += 8) {
     const T* arow = A + i * cols;
     double a[CPL];
-    if (inb) {
+    if (inb && (cols & 1) == 0) {
+      using V = typename Vec2<T>::type;
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) a[c] = (double)__ldg(arow + c0 + c);
+      for (int c = 0; c < CPL; c += 2) {
+        const V v = __ldg(reinterpret_cast<const V*>(arow + c0 + c));
+        a[c] = (double)v.x;
+        a[c + 1] = (double)v.y;
+      }
     } else {
 #pragma unroll
       for (int c = 0; c < CPL; ++c) a[c] = (c0 + c < cols) ? (double)arow[c0 + c] : 0.0;
@@ -590,12 +603,12 @@ template <int K, typename T>
 int launch_rowprod(const T* A, long rows, long cols, const double* B, double* out, double* tol,
                    double scale, double* work, long work_len, cudaStream_t st) {
   if (rowprod_split(rows, cols)) {  // HBM-streaming regime: split-K over column chunks
-    constexpr int RW = 4;
+    constexpr int RW = (sizeof(T) == 4 || K <= 10) ? 4 : 2;
     constexpr int CW = SplitCfg<T>::CW;
     const long nch = rowprod_chunks<T>(cols);
     if (nch * rows * K > work_len) return NMFB_ENOMEM;
     const size_t smem = (size_t)K * CW * sizeof(typename SplitCfg<T>::Y);
-    long nsplit = (148 * 2 + nch - 1) / nch;
+    long nsplit = (148 * 2 * 4 + nch - 1) / nch;  // ~4 waves of 2 CTAs/SM: small tail
     long rps = (rows + nsplit - 1) / nsplit;
     rps = ((rps + 8 * RW - 1) / (8 * RW)) * (8 * RW);
     nsplit = (rows + rps - 1) / rps;
@@ -639,7 +652,9 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
   if (ns * cols * K > work_len) return NMFB_ENOMEM;
   if (colprod_tiled(rows, cols)) {
     dim3 grid((unsigned)((cols + CT_COLS - 1) / CT_COLS), (unsigned)ns);
-    ++g_nmfb_launches, k_colprod_warp<K, 4, T><<<grid, 256, 0, st>>>(A, rows, cols, B, stripe, work);
+    constexpr int CPL = K <= 10 ? 4 : 2;
+    dim3 gridw((unsigned)((cols + 32 * CPL - 1) / (32 * CPL)), (unsigned)ns);
+    ++g_nmfb_launches, k_colprod_warp<K, CPL, T><<<gridw, 256, 0, st>>>(A, rows, cols, B, stripe, work);
   } else {
     dim3 grid((unsigned)((cols + CP_COLS - 1) / CP_COLS), (unsigned)ns);
     ++g_nmfb_launches, k_colprod_partial<K, T><<<grid, 256, 0, st>>>(A, rows, cols, B, stripe, work);
