@@ -174,155 +174,7 @@ __global__ void __launch_bounds__(256) k_colprod_partial(const T* __restrict__ A
 }
 
 
-// ---------------------------------------------------------------------------
-// HBM-streaming row product (the X-update ctb = M Y^T at c4/c5 scale).
-// CTA = 8 warps x RW rows.  Y^T chunks of CW columns are staged TRANSPOSED in
-// shared memory (conflict-free: lanes read consecutive columns), so every y
-// value fetched from smem is reused for RW rows held in registers; M is read
-// once, coalesced, with RW * CW/32 independent loads in flight per lane.
-// ---------------------------------------------------------------------------
-constexpr int RP_CW = 256;
-
-template <int K, int RW, typename T>
-__global__ void __launch_bounds__(256) k_rowprod_tiled(const T* __restrict__ A, long rows,
-                                                       long cols, const double* __restrict__ B,
-                                                       double* __restrict__ out,
-                                                       double* __restrict__ tol, double scale) {
-  __shared__ double syT[K][RP_CW];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long r0 = (long)blockIdx.x * (8 * RW) + (long)warp * RW;
-  double acc[RW][K];
-#pragma unroll
-  for (int r = 0; r < RW; ++r)
-#pragma unroll
-    for (int p = 0; p < K; ++p) acc[r][p] = 0.0;
-  const T* arow[RW];
-#pragma unroll
-  for (int r = 0; r < RW; ++r) arow[r] = A + min(r0 + r, rows - 1) * cols;
-  for (long j0 = 0; j0 < cols; j0 += RP_CW) {
-    const int cw = (int)min((long)RP_CW, cols - j0);
-    __syncthreads();
-    for (int e = tid; e < cw * K; e += 256) {
-      const int jj = e / K, p = e - jj * K;
-      syT[p][jj] = B[(j0 + jj) * K + p];
-    }
-    __syncthreads();
-    if (cw == RP_CW) {
-      double a[RP_CW / 32][RW];
-#pragma unroll
-      for (int u = 0; u < RP_CW / 32; ++u)
-#pragma unroll
-        for (int r = 0; r < RW; ++r) a[u][r] = (double)__ldg(arow[r] + j0 + lane + 32 * u);
-#pragma unroll
-      for (int u = 0; u < RP_CW / 32; ++u) {
-        const int jj = lane + 32 * u;
-#pragma unroll
-        for (int p = 0; p < K; ++p) {
-          const double y = syT[p][jj];
-#pragma unroll
-          for (int r = 0; r < RW; ++r) acc[r][p] = fma(a[u][r], y, acc[r][p]);
-        }
-      }
-    } else {
-      for (int jj = lane; jj < cw; jj += 32) {
-        double a[RW];
-#pragma unroll
-        for (int r = 0; r < RW; ++r) a[r] = (double)__ldg(arow[r] + j0 + jj);
-#pragma unroll
-        for (int p = 0; p < K; ++p) {
-          const double y = syT[p][jj];
-#pragma unroll
-          for (int r = 0; r < RW; ++r) acc[r][p] = fma(a[r], y, acc[r][p]);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < RW; ++r) {
-    double amax = 0.0;
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const double v = warp_sum(acc[r][p]) * scale;
-      acc[r][p] = v;
-      amax = fmax(amax, fabs(v));
-    }
-    if (lane == 0 && r0 + r < rows) {
-#pragma unroll
-      for (int p = 0; p < K; ++p) out[(r0 + r) * K + p] = acc[r][p];
-      if (tol) tol[r0 + r] = 1e-12 * fmax(1.0, amax);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// HBM-streaming column product partials (the Y-update X^T M).  CTA = 8 warps =
-// 8 interleaved row groups over one row stripe; each warp covers 128
-// contiguous columns (4 per lane, two 2-wide vector loads); the B rows of the
-// stripe are staged in smem and read as warp-broadcasts.
-// ---------------------------------------------------------------------------
-constexpr int CT_COLS = 128;
-constexpr int CT_ROWS = 64;
-
-template <int K, typename T>
-__global__ void __launch_bounds__(256) k_colprod_tiled(const T* __restrict__ A, long rows,
-                                                       long cols, const double* __restrict__ B,
-                                                       long stripe, double* __restrict__ part) {
-  __shared__ double sb[CT_ROWS * K];
-  __shared__ double red[8][32 * K + 1];
-  using V = typename Vec2<T>::type;
-  const int tid = threadIdx.x, lane = tid & 31, rg = tid >> 5;
-  const long c0 = (long)blockIdx.x * CT_COLS + 4 * lane;
-  const long s = blockIdx.y;
-  const long i_beg = s * stripe, i_end = min(rows, i_beg + stripe);
-  const bool full4 = (c0 + 3 < cols) && ((cols & 1) == 0);
-  double acc[4][K];
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int p = 0; p < K; ++p) acc[c][p] = 0.0;
-  for (long ib = i_beg; ib < i_end; ib += CT_ROWS) {
-    const int nr = (int)min((long)CT_ROWS, i_end - ib);
-    __syncthreads();
-    for (int e = tid; e < nr * K; e += 256) sb[e] = B[ib * K + e];
-    __syncthreads();
-    for (int r = rg; r < nr; r += 8) {
-      const T* arow = A + (ib + r) * cols;
-      double a[4];
-      if (full4) {
-        const V v0 = *reinterpret_cast<const V*>(arow + c0);
-        const V v1 = *reinterpret_cast<const V*>(arow + c0 + 2);
-        a[0] = (double)v0.x;
-        a[1] = (double)v0.y;
-        a[2] = (double)v1.x;
-        a[3] = (double)v1.y;
-      } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) a[c] = (c0 + c < cols) ? (double)arow[c0 + c] : 0.0;
-      }
-#pragma unroll
-      for (int p = 0; p < K; ++p) {
-        const double b = sb[r * K + p];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[c][p] = fma(a[c], b, acc[c][p]);
-      }
-    }
-  }
-  for (int c = 0; c < 4; ++c) {
-    __syncthreads();
-#pragma unroll
-    for (int p = 0; p < K; ++p) red[rg][lane * K + p] = acc[c][p];
-    __syncthreads();
-    for (int e = tid; e < 32 * K; e += 256) {
-      double v = 0.0;
-#pragma unroll
-      for (int g = 0; g < 8; ++g) v += red[g][e];
-      const int l = e / K, p = e - l * K;
-      const long j = (long)blockIdx.x * CT_COLS + 4 * l + c;
-      if (j < cols) part[(s * cols + j) * K + p] = v;
-    }
-  }
-}
-
+constexpr int CT_COLS = 128;  // column tile of the streaming column product
 
 // ---------------------------------------------------------------------------
 // v3 streaming products: no __syncthreads inside the streaming loops.
