@@ -337,6 +337,211 @@ __global__ void __launch_bounds__(256, 2) k_colprod_warp(const T* __restrict__ A
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) streaming products.
+//
+// The tall-skinny products are dense contractions over the long axis with an
+// 8/16-wide output: on sm_100a the FP64 tensor pipe (DMMA) retires 256 MACs
+// per warp instruction, so the SIMT issue/register pressure that kept the
+// SIMT kernels latency-bound disappears and the loops become pure streams of
+// 16-byte loads.  fp32 M (config c5) is widened to fp64 in registers.
+//
+// Fragment layout (PTX m8n8k4 .f64): lane = 4 g + t; A[g][t], B[t][g],
+// C[g][2t + {0,1}].  Each lane loads a 2-wide vector of M and feeds it to two
+// MMAs by permuting the contraction (row product) or the output rows (column
+// product) inside each 8-column block, so every M byte is loaded once with
+// 16-byte (fp64) / 8-byte (fp32) accesses.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <typename T>
+__device__ __forceinline__ double2 ld2(const T* p);
+template <>
+__device__ __forceinline__ double2 ld2<double>(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+template <>
+__device__ __forceinline__ double2 ld2<float>(const float* p) {
+  const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+  return make_double2((double)v.x, (double)v.y);
+}
+
+constexpr int MMA_CW = 512;  // row product: columns per chunk (multiple of 8)
+
+// row product: part[chunk][row][p] = sum_{j in chunk} A[row][j] B[j][p]
+// B fragments are pre-arranged in smem in fragment order (conflict-free).
+template <int NT, typename T>
+__global__ void __launch_bounds__(256, 2) k_rowprod_mma(const T* __restrict__ A, long rows,
+                                                        long cols, const double* __restrict__ B,
+                                                        int K, long rows_per_split,
+                                                        double* __restrict__ part) {
+  constexpr int RT = 2;  // 8-row tiles per warp
+  extern __shared__ __align__(16) double sB[];  // [CW/8][2][NT][32]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const long j0 = (long)blockIdx.x * MMA_CW;
+  const int cw = (int)min((long)MMA_CW, cols - j0);
+  const int npair = (cw + 7) >> 3;
+  for (int e = tid; e < npair * 2 * NT * 32; e += 256) {
+    const int l = e & 31, se = (e >> 5) / NT, nt = (e >> 5) % NT;
+    const int sidx = se >> 1, ee = se & 1;
+    const long col = j0 + 8 * sidx + 2 * (l & 3) + ee;
+    const int pp = nt * 8 + (l >> 2);
+    sB[e] = (col < cols && pp < K) ? B[col * K + pp] : 0.0;
+  }
+  __syncthreads();
+  const long rb = (long)blockIdx.y * rows_per_split;
+  const long re = min(rows, rb + rows_per_split);
+  for (long r0 = rb + (long)warp * 8 * RT; r0 < re; r0 += 8 * 8 * RT) {
+    double acc[RT][NT][2];
+#pragma unroll
+    for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[rt][nt][0] = acc[rt][nt][1] = 0.0;
+    const T* arow[RT];
+#pragma unroll
+    for (int rt = 0; rt < RT; ++rt) arow[rt] = A + min(r0 + 8 * rt + g, re - 1) * cols + j0 + 2 * t;
+    constexpr int UN = 4;
+    const int nfull = cw >> 3;  // pairs whose 8 columns are all in range
+    int sp = 0;
+    for (; sp + UN <= nfull; sp += UN) {
+      double2 a[UN][RT];
+#pragma unroll
+      for (int u = 0; u < UN; ++u)
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt) a[u][rt] = ld2<T>(arow[rt] + 8 * (sp + u));
+#pragma unroll
+      for (int u = 0; u < UN; ++u)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double b0 = sB[((2 * (sp + u)) * NT + nt) * 32 + lane];
+          const double b1 = sB[((2 * (sp + u) + 1) * NT + nt) * 32 + lane];
+#pragma unroll
+          for (int rt = 0; rt < RT; ++rt) {
+            dmma(acc[rt][nt][0], acc[rt][nt][1], a[u][rt].x, b0);
+            dmma(acc[rt][nt][0], acc[rt][nt][1], a[u][rt].y, b1);
+          }
+        }
+    }
+    for (; sp < npair; ++sp) {
+      const bool ok = j0 + 8 * sp + 2 * t < cols;
+      double2 a[RT];
+#pragma unroll
+      for (int rt = 0; rt < RT; ++rt) a[rt] = ok ? ld2<T>(arow[rt] + 8 * sp) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double b0 = sB[((2 * sp) * NT + nt) * 32 + lane];
+        const double b1 = sB[((2 * sp + 1) * NT + nt) * 32 + lane];
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt) {
+          dmma(acc[rt][nt][0], acc[rt][nt][1], a[rt].x, b0);
+          dmma(acc[rt][nt][0], acc[rt][nt][1], a[rt].y, b1);
+        }
+      }
+    }
+#pragma unroll
+    for (int rt = 0; rt < RT; ++rt) {
+      const long row = r0 + 8 * rt + g;
+      if (row >= re) continue;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int pp = nt * 8 + 2 * t + c;
+          if (pp < K) part[((long)blockIdx.x * rows + row) * K + pp] = acc[rt][nt][c];
+        }
+    }
+  }
+}
+
+// column product: part[s][j][p] = sum_{i in stripe s} A[i][j] B[i][p].
+// A warp owns 32 output columns (2 double2 loads per lane per 4-row k-step,
+// each feeding an even- and an odd-column 8-row MMA tile).
+template <int NT, typename T>
+__global__ void __launch_bounds__(256, 2) k_colprod_mma(const T* __restrict__ A, long rows,
+                                                        long cols, const double* __restrict__ B,
+                                                        int K, long stripe,
+                                                        double* __restrict__ part) {
+  constexpr int RT2 = 2;  // 16-column groups per warp
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const long jw = (long)blockIdx.x * 256 + (long)warp * 32;  // warp's first column
+  const long s = blockIdx.y;
+  const long i_beg = s * stripe, i_end = min(rows, i_beg + stripe);
+  double acc[RT2][2][NT][2];
+#pragma unroll
+  for (int r = 0; r < RT2; ++r)
+#pragma unroll
+    for (int par = 0; par < 2; ++par)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[r][par][nt][0] = acc[r][par][nt][1] = 0.0;
+  bool colok[RT2];
+#pragma unroll
+  for (int r = 0; r < RT2; ++r) colok[r] = jw + 16 * r + 2 * g < cols;
+  const bool bok0 = g < K, bok1 = 8 + g < K;
+  constexpr int UN = 4;
+  long i0 = i_beg;
+  for (; i0 + 4 * UN <= i_end; i0 += 4 * UN) {
+    double2 a[UN][RT2];
+    double b[UN][NT];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const long i = i0 + 4 * u + t;
+#pragma unroll
+      for (int r = 0; r < RT2; ++r)
+        a[u][r] = colok[r] ? ld2<T>(A + i * cols + jw + 16 * r + 2 * g) : make_double2(0.0, 0.0);
+      b[u][0] = bok0 ? __ldg(B + i * K + g) : 0.0;
+      if (NT > 1) b[u][NT - 1] = bok1 ? __ldg(B + i * K + 8 + g) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UN; ++u)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int r = 0; r < RT2; ++r) {
+          dmma(acc[r][0][nt][0], acc[r][0][nt][1], a[u][r].x, b[u][nt]);
+          dmma(acc[r][1][nt][0], acc[r][1][nt][1], a[u][r].y, b[u][nt]);
+        }
+  }
+  for (; i0 < i_end; i0 += 4) {
+    const long i = i0 + t;
+    const bool rok = i < i_end;
+    double2 a[RT2];
+    double b[NT];
+#pragma unroll
+    for (int r = 0; r < RT2; ++r)
+      a[r] = (rok && colok[r]) ? ld2<T>(A + i * cols + jw + 16 * r + 2 * g) : make_double2(0.0, 0.0);
+    b[0] = (rok && bok0) ? __ldg(B + i * K + g) : 0.0;
+    if (NT > 1) b[NT - 1] = (rok && bok1) ? __ldg(B + i * K + 8 + g) : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int r = 0; r < RT2; ++r) {
+        dmma(acc[r][0][nt][0], acc[r][0][nt][1], a[r].x, b[nt]);
+        dmma(acc[r][1][nt][0], acc[r][1][nt][1], a[r].y, b[nt]);
+      }
+  }
+#pragma unroll
+  for (int r = 0; r < RT2; ++r)
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+      const long j = jw + 16 * r + 2 * g + par;
+      if (j >= cols) continue;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int pp = nt * 8 + 2 * t + c;
+          if (pp < K) part[(s * cols + j) * K + pp] = acc[r][par][nt][c];
+        }
+    }
+}
+
 // out[e] = scale * sum_{s < nparts} part[s][e]  (fixed order); optional per-row
 // (of width K) tolerance as in k_rowprod.
 template <int K>
@@ -454,6 +659,23 @@ long rowprod_chunks(long cols) {
 template <int K, typename T>
 int launch_rowprod(const T* A, long rows, long cols, const double* B, double* out, double* tol,
                    double scale, double* work, long work_len, cudaStream_t st) {
+  if (rowprod_split(rows, cols) && (cols % 2 == 0) && K >= 5) {  // tensor-core streaming path
+    constexpr int NT = (K + 7) / 8;
+    const long nch = (cols + MMA_CW - 1) / MMA_CW;
+    if (nch * rows * K > work_len) return NMFB_ENOMEM;
+    const size_t smem = (size_t)MMA_CW * NT * 8 * sizeof(double);
+    long nsplit = (148 * 2 * 4 + nch - 1) / nch;
+    long rps = (rows + nsplit - 1) / nsplit;
+    rps = ((rps + 127) / 128) * 128;
+    nsplit = (rows + rps - 1) / rps;
+    cudaFuncSetAttribute(k_rowprod_mma<NT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((unsigned)nch, (unsigned)nsplit);
+    ++g_nmfb_launches, k_rowprod_mma<NT, T><<<grid, 256, smem, st>>>(A, rows, cols, B, K, rps, work);
+    ++g_nmfb_launches, k_sum_partials<K><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
+        work, (int)nch, rows * K, out, tol, scale);
+    NMFB_CHECK_LAUNCH();
+    return NMFB_OK;
+  }
   if (rowprod_split(rows, cols)) {  // HBM-streaming regime: split-K over column chunks
     constexpr int RW = (sizeof(T) == 4 || K <= 10) ? 4 : 2;
     constexpr int CW = SplitCfg<T>::CW;
@@ -502,7 +724,11 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
   const long stripe = colprod_stripe(rows, cols);
   const long ns = (rows + stripe - 1) / stripe;
   if (ns * cols * K > work_len) return NMFB_ENOMEM;
-  if (colprod_tiled(rows, cols)) {
+  if (colprod_tiled(rows, cols) && (cols % 2 == 0) && K >= 5) {  // tensor-core streaming path
+    constexpr int NT = (K + 7) / 8;
+    dim3 gridm((unsigned)((cols + 255) / 256), (unsigned)ns);
+    ++g_nmfb_launches, k_colprod_mma<NT, T><<<gridm, 256, 0, st>>>(A, rows, cols, B, K, stripe, work);
+  } else if (colprod_tiled(rows, cols)) {
     dim3 grid((unsigned)((cols + CT_COLS - 1) / CT_COLS), (unsigned)ns);
     constexpr int CPL = K <= 10 ? 4 : 2;
     dim3 gridw((unsigned)((cols + 32 * CPL - 1) / (32 * CPL)), (unsigned)ns);
@@ -534,7 +760,9 @@ extern "C" long nmfb_colprod_work_len(long rows, long cols, long k) {
 
 extern "C" long nmfb_rowprod_work_len(long rows, long cols, long k, int a_is_f32) {
   if (!rowprod_split(rows, cols)) return 1;
-  return (a_is_f32 ? rowprod_chunks<float>(cols) : rowprod_chunks<double>(cols)) * rows * k;
+  const long mma = (cols + MMA_CW - 1) / MMA_CW;
+  const long simt = a_is_f32 ? rowprod_chunks<float>(cols) : rowprod_chunks<double>(cols);
+  return (mma > simt ? mma : simt) * rows * k;
 }
 
 extern "C" int nmfb_rowprod(const void* A, int a_is_f32, long rows, long cols, const double* B,

@@ -159,3 +159,30 @@ def test_device_newton_vs_dense_kkt(mods, solve):
                 assert np.abs(a - b).max() <= 1e-8 * max(1.0, np.abs(b).max()), (trial, full)
             checked += 1
     assert checked >= 30
+
+
+@pytest.mark.parametrize("shape,dt", [((8192, 4096, 10), "f64"), ((8200, 5002, 3), "f64"),
+                                      ((6000, 2304, 16), "f64"), ((8192, 4096, 16), "f32"),
+                                      ((4100, 3001, 7), "f64")])
+def test_streaming_products_large(mods, shape, dt):
+    """HBM-streaming product kernels (split-K / tensor-core paths) vs fp64 reference products."""
+    import torch
+
+    data, solver, IpmParams, Stage1Config = mods
+    n, m, k = shape
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n + m + k)
+    M = torch.rand((n, m), generator=g, device="cuda", dtype=torch.float64)
+    if dt == "f32":
+        M = M.float()
+    P = solver.Problem(M, k)
+    X = torch.rand((n, k), generator=g, device="cuda", dtype=torch.float64)
+    Yt = torch.rand((m, k), generator=g, device="cuda", dtype=torch.float64)
+    ctbX, ctbY = P.buf(n, k), P.buf(m, k)
+    P.rowprod(P.M, n, m, Yt, k, ctbX, None, P.f32)
+    P.colprod(P.M, n, m, X, k, ctbY, None, P.f32)
+    M64 = P.M.double()
+    refX, refY = M64 @ Yt, M64.t() @ X
+    tol = 1e-12 if dt == "f64" else 1e-5
+    assert float((ctbX - refX).abs().max() / refX.abs().max()) < tol
+    assert float((ctbY - refY).abs().max() / refY.abs().max()) < tol
