@@ -98,6 +98,9 @@ int nmfb_stage1_stats(const double *Xo, const double *Xn, long nx, const double 
                       const double *Yn, long ny, const double *r2, long nr, double *stats,
                       double *work, long work_len, void *stream);
 
+/* tol[r] = 1e-12 max(1, ||c_r||_inf) for a product already reduced across ranks */
+int nmfb_row_tol(const double *c, long rows, long k, double *tol, void *stream);
+
 /* *out = first index with st != 0, 0x7F7F7F7F when none (nnls status scan) */
 int nmfb_first_nonzero_i8(const int8_t *st, long len, int *out, void *stream);
 
@@ -144,7 +147,8 @@ int nmfb_schur_rhs(const double *Yt, const double *gY, const double *H, const do
                    double muy, long m, long k, double *rhs, void *stream);
 
 /* back_substitute (_kernels_numba.py:181) + dr, ds + reductions:
- * out = [(dx,dy).grad phi, alpha1_max, alpha2_max] */
+ * out = [(dx,dy).grad phi, alpha1_max, alpha2_max, row part of the first, column part]
+ * */
 int nmfb_direction(const double *L, const double *Xf, const double *h, const double *Gdy,
                    const double *FdY, const double *X, const double *R, const double *gX,
                    double mux, const double *Yt, const double *S, const double *gY,

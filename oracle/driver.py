@@ -105,6 +105,23 @@ class OracleError(RuntimeError):
 
 
 # ----------------------------------------------------------------------------
+# row sharding (paper_2101_08431_b200.dist): rows of M / X / R are local, Y / S
+# replicated; contractions over rows are summed across ranks (gloo on CPU).
+# ----------------------------------------------------------------------------
+def _red(comm, a, op="sum"):
+    """All-reduce a numpy array / float across ranks (identity without comm)."""
+    if comm is None or not comm.active:
+        return a
+    import torch
+
+    scalar = np.isscalar(a) or np.ndim(a) == 0
+    t = torch.as_tensor(np.array(a, dtype=np.float64, ndmin=1)).clone()
+    {"sum": comm.sum_, "max": comm.max_, "min": comm.min_}[op](t)
+    out = t.numpy()
+    return float(out[0]) if scalar else out.reshape(np.shape(a))
+
+
+# ----------------------------------------------------------------------------
 # products (numpy/OpenBLAS, as in the reference's missing drivers)
 # ----------------------------------------------------------------------------
 def objective(X, Yt, M):
@@ -113,23 +130,24 @@ def objective(X, Yt, M):
     return 0.5 * float(np.vdot(F, F))
 
 
-def gradients(X, Yt, M):
+def gradients(X, Yt, M, comm=None):
     """graX = vec(Y F^T) -> (n,k) = F Y^T; graY = vec(X^T F) -> (m,k)."""
     F = X @ Yt.T - M
-    return F, F @ Yt, F.T @ X
+    return F, F @ Yt, _red(comm, F.T @ X)
 
 
-def kkt_error(X, Yt, R, S, graX, graY, mu, wx=1.0, wy=1.0):
+def kkt_error(X, Yt, R, S, graX, graY, mu, wx=1.0, wy=1.0, comm=None):
     """SPEC.md:274 / PAPER Eq. 9 (Diag(y) reading)."""
-    st = math.sqrt(float(np.sum((graX - R) ** 2) + np.sum((graY - S) ** 2)))
-    cp = math.sqrt(float(np.sum((X * R - wx * mu) ** 2) + np.sum((Yt * S - wy * mu) ** 2)))
+    xs = _red(comm, np.array([np.sum((graX - R) ** 2), np.sum((X * R - wx * mu) ** 2)]))
+    st = math.sqrt(float(xs[0] + np.sum((graY - S) ** 2)))
+    cp = math.sqrt(float(xs[1] + np.sum((Yt * S - wy * mu) ** 2)))
     return max(st, cp)
 
 
-def kkt_error_primal_only(X, Yt, M):
+def kkt_error_primal_only(X, Yt, M, comm=None):
     """SPEC.md:420 / PAPER.md:633-639: E(x,y,max(graX,0),max(graY,0);0)."""
-    _, gX, gY = gradients(X, Yt, M)
-    return kkt_error(X, Yt, np.maximum(gX, 0.0), np.maximum(gY, 0.0), gX, gY, 0.0)
+    _, gX, gY = gradients(X, Yt, M, comm)
+    return kkt_error(X, Yt, np.maximum(gX, 0.0), np.maximum(gY, 0.0), gX, gY, 0.0, comm=comm)
 
 
 def _nnls_tol(ctb, tol_kkt):
@@ -140,8 +158,12 @@ def _nnls_tol(ctb, tol_kkt):
     return 1e-12 * np.maximum(1.0, np.abs(ctb).max(axis=1))
 
 
-def _raise_status(status, what):
+def _raise_status(status, what, comm=None):
     bad = np.flatnonzero(status)
+    if comm is not None and comm.active:  # every rank raises together
+        anybad = _red(comm, float(bad.size > 0), "max")
+        if anybad and not bad.size:
+            raise OracleError(f"status failure on another rank in {what}")
     if bad.size:
         i = int(bad[0])
         kind = "MaxIterationsExceeded" if status[i] == 1 else "RankDeficientPassiveSet"
@@ -151,21 +173,21 @@ def _raise_status(status, what):
 # ----------------------------------------------------------------------------
 # stage 1: ANLS (Algorithm 1)
 # ----------------------------------------------------------------------------
-def update_X(X, Yt, M, pX, mode, cfg, row_norm2):
-    """rows of X <- NNLS(C = Y^T, d = M_i,:)."""
+def update_X(X, Yt, M, pX, mode, cfg, row_norm2, comm=None):
+    """rows of X <- NNLS(C = Y^T, d = M_i,:) (rows are rank-local)."""
     ctc = Yt.T @ Yt
     ctb = M @ Yt
     tol = _nnls_tol(ctb, cfg.tol_kkt)
     k = X.shape[1]
     x, p, ch, r2, st = K.nnls_batch(ctc, ctb, row_norm2, pX, mode, tol, 3 * k)
-    _raise_status(st, "update_X")
+    _raise_status(st, "update_X", comm)
     return x, p, ch, r2
 
 
-def update_Y(X, Yt, M, pY, mode, cfg, col_norm2):
-    """columns of Y <- NNLS(C = X, d = M_:,j)."""
-    ctc = X.T @ X
-    ctb = M.T @ X
+def update_Y(X, Yt, M, pY, mode, cfg, col_norm2, comm=None):
+    """columns of Y <- NNLS(C = X, d = M_:,j) (Grams summed over ranks)."""
+    ctc = _red(comm, X.T @ X)
+    ctb = _red(comm, M.T @ X)
     tol = _nnls_tol(ctb, cfg.tol_kkt)
     k = X.shape[1]
     y, p, ch, r2, st = K.nnls_batch(ctc, ctb, col_norm2, pY, mode, tol, 3 * k)
@@ -187,8 +209,10 @@ class Stage1Result:
     seconds: float = 0.0
 
 
-def run_stage1(M, X, Yt, cfg=None, pX=None, pY=None):
-    """SPEC.md:209 run_stage1.  X (n,k), Yt = Y^T (m,k).  Carries optional."""
+def run_stage1(M, X, Yt, cfg=None, pX=None, pY=None, comm=None):
+    """SPEC.md:209 run_stage1.  X (n,k), Yt = Y^T (m,k).  Carries optional.
+
+    With ``comm``: M, X, pX are this rank's row block; Yt, pY replicated."""
     cfg = cfg or Stage1Config()
     t0 = time.perf_counter()
     X = np.array(X, dtype=np.float64)
@@ -199,15 +223,16 @@ def run_stage1(M, X, Yt, cfg=None, pX=None, pY=None):
     pX = np.zeros((n, k), bool) if pX is None else pX.copy()
     pY = np.zeros((m, k), bool) if pY is None else pY.copy()
     row_n2 = np.einsum("ij,ij->i", M, M)
-    col_n2 = np.einsum("ij,ij->j", M, M)
+    col_n2 = _red(comm, np.einsum("ij,ij->j", M, M))
     res = Stage1Result(X, Yt, pX, pY, 0, False)
     nsweeps = cfg.fixed_sweeps if cfg.fixed_sweeps > 0 else cfg.max_sweeps
     for sweep in range(nsweeps):
         mode = 2 if (sweep > 0 or have_carry) else 0
-        Xn, pX, chX, _ = update_X(X, Yt, M, pX, mode, cfg, row_n2)
-        Yn, pY, chY, r2Y = update_Y(Xn, Yt, M, pY, mode, cfg, col_n2)
-        step = math.sqrt(float(np.sum((Xn - X) ** 2) + np.sum((Yn - Yt) ** 2)))
-        nrm = math.sqrt(float(np.sum(X ** 2) + np.sum(Yt ** 2)))
+        Xn, pX, chX, _ = update_X(X, Yt, M, pX, mode, cfg, row_n2, comm)
+        Yn, pY, chY, r2Y = update_Y(Xn, Yt, M, pY, mode, cfg, col_n2, comm)
+        xs = _red(comm, np.array([np.sum((Xn - X) ** 2), np.sum(X ** 2)]))
+        step = math.sqrt(float(xs[0] + np.sum((Yn - Yt) ** 2)))
+        nrm = math.sqrt(float(xs[1] + np.sum(Yt ** 2)))
         X, Yt = Xn, Yn
         res.sweeps = sweep + 1
         res.trace.append((time.perf_counter() - t0, 0.5 * float(np.sum(r2Y)), step))
@@ -235,21 +260,22 @@ class IpmState:
     flag: bool = False
 
 
-def transition(X, Yt, M, eps_tol, tp=None):
+def transition(X, Yt, M, eps_tol, tp=None, comm=None):
     """SPEC.md:393 / PAPER Eqs. 14-18."""
     tp = tp or TransitionParams()
-    big = max(float(X.max(initial=0.0)), float(Yt.max(initial=0.0)))
+    big = max(_red(comm, float(X.max(initial=0.0)), "max"), float(Yt.max(initial=0.0)))
     if big <= 0.0:
         raise OracleError("DegenerateFactor")
     rho0 = tp.rho0_scale * big
     X = np.maximum(X, rho0)
     Yt = np.maximum(Yt, rho0)
-    _, gX, gY = gradients(X, Yt, M)
-    R = np.full_like(X, np.abs(gX).max())
+    _, gX, gY = gradients(X, Yt, M, comm)
+    R = np.full_like(X, _red(comm, float(np.abs(gX).max(initial=0.0)), "max"))
     S = np.full_like(Yt, np.abs(gY).max())
     n, k = X.shape
     m = Yt.shape[0]
-    mu = (float(np.vdot(X, R)) + float(np.vdot(Yt, S))) / (n * k + m * k)
+    n = int(_red(comm, float(n)))
+    mu = (_red(comm, float(np.vdot(X, R))) + float(np.vdot(Yt, S))) / (n * k + m * k)
     return IpmState(X, Yt, R, S, mu, eps_tol, False)
 
 
@@ -261,8 +287,8 @@ def fraction_to_boundary(v, dv, tau):
     return float(min(1.0, np.min(-tau * v[neg] / dv[neg])))
 
 
-def _ftb2(a, da, b, db, tau):
-    return min(fraction_to_boundary(a.ravel(), da.ravel(), tau),
+def _ftb2(a, da, b, db, tau, comm=None):
+    return min(_red(comm, fraction_to_boundary(a.ravel(), da.ravel(), tau), "min"),
                fraction_to_boundary(b.ravel(), db.ravel(), tau))
 
 
@@ -316,7 +342,7 @@ def barrier_weights(n, m, barrier):
     raise ValueError(barrier)
 
 
-def newton_direction(M, st: IpmState, F, gX, gY, full, wx=1.0, wy=1.0):
+def newton_direction(M, st: IpmState, F, gX, gY, full, wx=1.0, wy=1.0, comm=None):
     """R1 blocks, Schur reduction, mk x mk solve, back-sub.
 
     Returns (dx, dy, dr, ds, gtp, fact) or None when the Schur matrix is not
@@ -327,13 +353,14 @@ def newton_direction(M, st: IpmState, F, gX, gY, full, wx=1.0, wy=1.0):
     YYt = Yt.T @ Yt
     R1 = YYt[None] + rho * np.eye(k)[None] + np.einsum("ip,pq->ipq", R / X, np.eye(k))
     L, bad = K.block_cholesky(R1)
-    if bad >= 0:
+    if _red(comm, float(bad >= 0), "max"):
         raise OracleError("NotPositiveDefinite", bad)
     mux, muy = wx * mu, wy * mu
     b1 = mux / X - gX
     h = K.block_solve_lower(L, b1[:, :, None])[:, :, 0]
     Sacc, racc = K.schur_reduce(X, Yt, L, h, F, full)
-    A = schur_matrix(X.T @ X, rho, S / Yt, Sacc)
+    Sacc, racc = _red(comm, Sacc), _red(comm, racc)
+    A = schur_matrix(_red(comm, X.T @ X), rho, S / Yt, Sacc)
     Ls = spd_factor(A)
     if Ls is None:
         if full:
@@ -344,24 +371,25 @@ def newton_direction(M, st: IpmState, F, gX, gY, full, wx=1.0, wy=1.0):
     dx = K.back_substitute(X, Yt, L, h, dy, F, full)
     dr = mux / X - R - (R / X) * dx
     ds = muy / Yt - S - (S / Yt) * dy
-    gtp = float(np.vdot(dx, gX - mux / X)) + float(np.vdot(dy, gY - muy / Yt))
+    gtp = _red(comm, float(np.vdot(dx, gX - mux / X))) + float(np.vdot(dy, gY - muy / Yt))
     return dx, dy, dr, ds, gtp, Factorization(X, Yt, F, L, Ls, full)
 
 
-def quartic_coeffs(X, Yt, dX, dYt, M):
+def quartic_coeffs(X, Yt, dX, dYt, M, comm=None):
     """Inner products of A = XY-M, B = dX Y + X dY, C = dX dY (one pass over M)."""
     A = X @ Yt.T - M
     B = dX @ Yt.T + X @ dYt.T
     C = dX @ dYt.T
-    return (float(np.vdot(A, A)), float(np.vdot(A, B)), float(np.vdot(B, B)),
-            float(np.vdot(A, C)), float(np.vdot(B, C)), float(np.vdot(C, C)))
+    v = np.array([np.vdot(A, A), np.vdot(A, B), np.vdot(B, B), np.vdot(A, C), np.vdot(B, C),
+                  np.vdot(C, C)])
+    return tuple(float(x) for x in _red(comm, v))
 
 
-def merit_delta(coef, alpha, X, dX, Yt, dYt, mu, wx=1.0, wy=1.0):
+def merit_delta(coef, alpha, X, dX, Yt, dYt, mu, wx=1.0, wy=1.0, comm=None):
     """phi(x + a dx, y + a dy) - phi(x, y), evaluated without cancellation."""
     _, ab, bb, ac, bc, cc = coef
     quad = alpha * ab + alpha * alpha * (0.5 * bb + ac) + alpha ** 3 * bc + 0.5 * alpha ** 4 * cc
-    bx = float(np.sum(np.log1p(alpha * dX / X)))
+    bx = _red(comm, float(np.sum(np.log1p(alpha * dX / X))))
     by = float(np.sum(np.log1p(alpha * dYt / Yt)))
     return quad - mu * (wx * bx + wy * by)
 
@@ -393,61 +421,62 @@ class IpmResult:
     seconds: float = 0.0
 
 
-def predictor_sigma(st: IpmState, gX, gY, fact: Factorization, p: IpmParams):
+def predictor_sigma(st: IpmState, gX, gY, fact: Factorization, p: IpmParams, comm=None):
     """SPEC.md:328 / PAPER Eqs. 7-8, reusing the last Newton factorization."""
     X, Yt, R, S = st.X, st.Yt, st.R, st.S
     n, k = X.shape
     m = Yt.shape[0]
     b1 = -gX
     h = K.block_solve_lower(fact.L, b1[:, :, None])[:, :, 0]
-    racc = K.rhs_reduce(fact.X, fact.Yt, fact.L, h, fact.F, fact.full)
+    racc = _red(comm, K.rhs_reduce(fact.X, fact.Yt, fact.L, h, fact.F, fact.full))
     dy = spd_solve_factored(fact.Ls, (-gY - racc).ravel()).reshape(Yt.shape)
     dx = K.back_substitute(fact.X, fact.Yt, fact.L, h, dy, fact.F, fact.full)
     dr = -R - (R / X) * dx
     ds = -S - (S / Yt) * dy
-    a1 = _ftb2(X, dx, Yt, dy, 1.0)
-    a2 = _ftb2(R, dr, S, ds, 1.0)
-    nk = n * k + m * k
-    mu_aff = (float(np.vdot(X + a1 * dx, R + a2 * dr)) + float(np.vdot(Yt + a1 * dy, S + a2 * ds))) / nk
-    mu_bar = (float(np.vdot(X, R)) + float(np.vdot(Yt, S))) / nk
+    a1 = _ftb2(X, dx, Yt, dy, 1.0, comm)
+    a2 = _ftb2(R, dr, S, ds, 1.0, comm)
+    nk = int(_red(comm, float(n))) * k + m * k
+    xs = _red(comm, np.array([np.vdot(X + a1 * dx, R + a2 * dr), np.vdot(X, R)]))
+    mu_aff = (float(xs[0]) + float(np.vdot(Yt + a1 * dy, S + a2 * ds))) / nk
+    mu_bar = (float(xs[1]) + float(np.vdot(Yt, S))) / nk
     return min((mu_aff / mu_bar) ** 3, p.sigma_cap)
 
 
-def run_ipm(M, st: IpmState, p: IpmParams = None):
+def run_ipm(M, st: IpmState, p: IpmParams = None, comm=None):
     """SPEC.md:337 run_ipm: Algorithm 2 nested loops + Algorithm 3 switch."""
     p = p or IpmParams()
     t0 = time.perf_counter()
-    F, gX, gY = gradients(st.X, st.Yt, M)
-    E0 = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0)
+    F, gX, gY = gradients(st.X, st.Yt, M, comm)
+    E0 = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0, comm=comm)
     res = IpmResult(st, 0, 0, False, E0)
     cap = p.fixed_iters if p.fixed_iters > 0 else p.max_iter
     tol = 0.0 if p.fixed_iters > 0 else p.eps_tol
     fact = None
     e_zero = E0
-    wx, wy = barrier_weights(st.X.shape[0], st.Yt.shape[0], p.barrier)
+    wx, wy = barrier_weights(int(_red(comm, float(st.X.shape[0]))), st.Yt.shape[0], p.barrier)
     while e_zero > tol and res.iters < cap:
         eps_mu = st.mu
-        while (kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, st.mu, wx, wy) > eps_mu
+        while (kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, st.mu, wx, wy, comm) > eps_mu
                and res.iters < cap):
             out = None
             used_full = False
             if st.flag:
-                out = newton_direction(M, st, F, gX, gY, True, wx, wy)
+                out = newton_direction(M, st, F, gX, gY, True, wx, wy, comm)
                 if out is None or out[4] >= 0.0:
                     st.flag = False
                     out = None
                 else:
                     used_full = True
             if out is None:
-                out = newton_direction(M, st, F, gX, gY, False, wx, wy)
+                out = newton_direction(M, st, F, gX, gY, False, wx, wy, comm)
             dx, dy, dr, ds, gtp, fact = out
-            a1max = _ftb2(st.X, dx, st.Yt, dy, p.tau)
-            a2max = _ftb2(st.R, dr, st.S, ds, p.tau)
-            coef = quartic_coeffs(st.X, st.Yt, dx, dy, M)
+            a1max = _ftb2(st.X, dx, st.Yt, dy, p.tau, comm)
+            a2max = _ftb2(st.R, dr, st.S, ds, p.tau, comm)
+            coef = quartic_coeffs(st.X, st.Yt, dx, dy, M, comm)
             t = 0
             while True:
                 a1 = a1max / (2.0 ** t)
-                if merit_delta(coef, a1, st.X, dx, st.Yt, dy, st.mu, wx, wy) <= p.eta * a1 * gtp:
+                if merit_delta(coef, a1, st.X, dx, st.Yt, dy, st.mu, wx, wy, comm) <= p.eta * a1 * gtp:
                     break
                 t += 1
                 if t > p.max_backtracks:
@@ -459,17 +488,17 @@ def run_ipm(M, st: IpmState, p: IpmParams = None):
             res.iters += 1
             res.armijo_t.append(t)
             res.flags.append(used_full)
-            F, gX, gY = gradients(st.X, st.Yt, M)
-            e_zero = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0)
-            res.trace.append((time.perf_counter() - t0, 0.5 * float(np.vdot(F, F)), e_zero, st.mu,
-                              a1, a2max, t))
+            F, gX, gY = gradients(st.X, st.Yt, M, comm)
+            e_zero = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0, comm=comm)
+            res.trace.append((time.perf_counter() - t0, 0.5 * _red(comm, float(np.vdot(F, F))),
+                              e_zero, st.mu, a1, a2max, t))
         res.outer += 1
-        e_zero = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0)
+        e_zero = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0, comm=comm)
         if e_zero <= tol or res.iters >= cap:
             break
         if fact is None:  # no Newton solve yet: factor at the current point
-            fact = newton_direction(M, st, F, gX, gY, False, wx, wy)[5]
-        sigma = predictor_sigma(st, gX, gY, fact, p)
+            fact = newton_direction(M, st, F, gX, gY, False, wx, wy, comm)[5]
+        sigma = predictor_sigma(st, gX, gY, fact, p, comm)
         st.mu = sigma * st.mu
         st.flag = sigma <= p.sigma_c
     res.converged = e_zero <= tol
@@ -496,13 +525,14 @@ class SolveReport:
 
 
 def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1=None, ipm=None, tp=None, stage="two_stage",
-                  pX=None, pY=None, e_scale=None):
-    """SPEC.md:411 run_two_stage.  X0 (n,k), Y0 (k,m)."""
+                  pX=None, pY=None, e_scale=None, comm=None):
+    """SPEC.md:411 run_two_stage.  X0 (n,k), Y0 (k,m).  With ``comm`` M / X0 / pX
+    are this rank's row block (paper_2101_08431_b200.dist)."""
     M = np.asarray(M, dtype=np.float64)
     X0 = np.asarray(X0, dtype=np.float64)
     Yt0 = np.ascontiguousarray(np.asarray(Y0, dtype=np.float64).T)
     if e_scale is None:
-        e_scale = max(1.0, kkt_error_primal_only(X0, Yt0, M))
+        e_scale = max(1.0, kkt_error_primal_only(X0, Yt0, M, comm))
     eps_abs = tol_rel * e_scale
     p = ipm or IpmParams()
     p.eps_tol = eps_abs
@@ -511,15 +541,16 @@ def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1=None, ipm=None, tp=None, stage="t
         r1 = Stage1Result(X0.copy(), Yt0.copy(), np.zeros(X0.shape, bool),
                           np.zeros(Yt0.shape, bool), 0, False)
     else:
-        r1 = run_stage1(M, X0, Yt0, s1, pX, pY)
+        r1 = run_stage1(M, X0, Yt0, s1, pX, pY, comm)
     if stage == "anls_only":
         X, Yt = r1.X, r1.Yt
-        return SolveReport(X, Yt, objective(X, Yt, M), kkt_error_primal_only(X, Yt, M), eps_abs,
-                           r1, None, kkt_error_primal_only(X, Yt, M) <= eps_abs, r1.seconds, 0.0)
-    st = transition(r1.X, r1.Yt, M, eps_abs, tp)
-    r2 = run_ipm(M, st, p)
+        e = kkt_error_primal_only(X, Yt, M, comm)
+        return SolveReport(X, Yt, _red(comm, objective(X, Yt, M)), e, eps_abs,
+                           r1, None, e <= eps_abs, r1.seconds, 0.0)
+    st = transition(r1.X, r1.Yt, M, eps_abs, tp, comm)
+    r2 = run_ipm(M, st, p, comm)
     X, Yt = r2.state.X, r2.state.Yt
-    F, gX, gY = gradients(X, Yt, M)
-    kkt = kkt_error(X, Yt, r2.state.R, r2.state.S, gX, gY, 0.0)
-    return SolveReport(X, Yt, objective(X, Yt, M), kkt, eps_abs, r1, r2, r2.converged,
+    F, gX, gY = gradients(X, Yt, M, comm)
+    kkt = kkt_error(X, Yt, r2.state.R, r2.state.S, gX, gY, 0.0, comm=comm)
+    return SolveReport(X, Yt, _red(comm, objective(X, Yt, M)), kkt, eps_abs, r1, r2, r2.converged,
                        r1.seconds, r2.seconds)

@@ -34,6 +34,7 @@ SIGNATURES = {
     "nmfb_sqnorms": [P, I, L, L, P, P, P, L, P],
     "nmfb_stage1_stats": [P, P, L, P, P, L, P, L, P, P, L, P],
     "nmfb_first_nonzero_i8": [P, L, P, P],
+    "nmfb_row_tol": [P, L, L, P, P],
     "nmfb_ipm_reduce_blocks": [],
     "nmfb_residual": [P, I, L, L, L, P, P, P, P, P, P, P],
     "nmfb_r1_factor": [P, P, P, P, D, D, L, L, P, P, P, P, P, P, P],

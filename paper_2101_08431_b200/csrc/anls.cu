@@ -832,6 +832,23 @@ extern "C" int nmfb_stage1_stats(const double* Xo, const double* Xn, long nx, co
   return NMFB_OK;
 }
 
+__global__ void k_row_tol(const double* __restrict__ c, long rows, int k, double* __restrict__ tol) {
+  const long r = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double a = 0.0;
+  for (int p = 0; p < k; ++p) a = fmax(a, fabs(c[r * k + p]));
+  tol[r] = 1e-12 * fmax(1.0, a);
+}
+
+// tol[r] = 1e-12 max(1, ||c_r||_inf), for products reduced across ranks
+extern "C" int nmfb_row_tol(const double* c, long rows, long k, double* tol, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (rows <= 0) return NMFB_OK;
+  ++g_nmfb_launches, k_row_tol<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(c, rows, (int)k, tol);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
 // *out = first index with st != 0 (0x7F7F7F7F when none); out is set, not accumulated
 extern "C" int nmfb_first_nonzero_i8(const int8_t* st, long len, int* out, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;

@@ -538,6 +538,8 @@ __global__ void k_finish_dir(const double* __restrict__ prow, int nrow,
     out[0] = g + g2;
     out[1] = a1;
     out[2] = a2;
+    out[3] = g;   // row-block part (summed across ranks when M is row-sharded)
+    out[4] = g2;  // column part (replicated)
   }
 }
 

@@ -1,0 +1,85 @@
+"""Row sharding of M across the GPUs of one node.
+
+Rows of M (and of X, R, F, graX, the R1 factors) are partitioned in
+contiguous blocks; Y, S, graY and every k- or k^2-sized quantity are
+replicated.  The exchanges are exactly the contractions over rows:
+
+  stage 1, per sweep   X^T X (k x k) and X^T M (m x k)            sum
+                       step / norm statistics (X part)             sum
+                       NNLS status scan                            min
+  stage 2, per iter    ||F||^2, graY = F^T X, X^T X, H, Z          sum
+                       [full Hessian] W = F^T P, term-4 of A       sum
+                       KKT / Armijo / affine sums (X part)          sum
+                       fraction-to-boundary minima                 min
+                       maxima for the transition                   max
+
+The Y-side NNLS, the reduced (k^2 capacitance or dense mk) solve and all
+replicated updates run redundantly on every rank with identical inputs, so
+their (deterministic) results are identical everywhere and need no
+broadcast.  ``Comm`` wraps torch.distributed (NCCL on GPUs, gloo on CPU);
+``Comm.single()`` is the no-op used on one GPU.
+"""
+from __future__ import annotations
+
+import torch
+
+
+def row_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block of rows owned by ``rank`` (sizes differ by at most 1)."""
+    base, extra = divmod(n, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+class Comm:
+    def __init__(self, group=None, world: int = 1, rank: int = 0):
+        self.group, self.world, self.rank = group, world, rank
+
+    @classmethod
+    def single(cls):
+        return cls(None, 1, 0)
+
+    @classmethod
+    def from_env(cls):
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return cls(None, dist.get_world_size(), dist.get_rank())
+        return cls.single()
+
+    @property
+    def active(self):
+        return self.world > 1
+
+    @property
+    def root(self):
+        return self.rank == 0
+
+    def _ar(self, t: torch.Tensor, op):
+        if self.world == 1 or t.numel() == 0:
+            return t
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=op, group=self.group)
+        return t
+
+    def sum_(self, t):
+        import torch.distributed as dist
+
+        return self._ar(t, dist.ReduceOp.SUM) if self.world > 1 else t
+
+    def max_(self, t):
+        import torch.distributed as dist
+
+        return self._ar(t, dist.ReduceOp.MAX) if self.world > 1 else t
+
+    def min_(self, t):
+        import torch.distributed as dist
+
+        return self._ar(t, dist.ReduceOp.MIN) if self.world > 1 else t
+
+    def sum_float(self, v: float, device=None) -> float:
+        if self.world == 1:
+            return float(v)
+        t = torch.tensor([float(v)], dtype=torch.float64, device=device)
+        return float(self.sum_(t).item())

@@ -19,6 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .dist import Comm
 from .config import (IpmParams, IpmResult, SolveReport, Stage1Config, Stage1Result,
                      TransitionParams)
 from .errors import (DegenerateFactor, LineSearchStall, NativeLibraryError,
@@ -53,7 +54,8 @@ def barrier_weights(n, m, barrier):
 class Problem:
     """M resident on one GPU plus every scratch buffer the solver needs."""
 
-    def __init__(self, M, k, device=None):
+    def __init__(self, M, k, device=None, comm: Comm | None = None):
+        """M: this rank's row block when ``comm`` spans several GPUs (dist.py)."""
         if not torch.cuda.is_available():
             raise NativeLibraryError("no CUDA device: the B200 solver has no CPU fallback")
         self.lib = _lib.load()
@@ -70,6 +72,8 @@ class Problem:
             self.M = self.M.double()
         self.f32 = int(self.M.dtype == torch.float32)
         self.n, self.m = self.M.shape
+        self.comm = comm or Comm.single()
+        self.n_global = int(self.comm.sum_float(self.n, self.dev)) if self.comm.active else self.n
         self.k = int(k)
         if not 1 <= self.k <= 16:
             raise ValueError("k must be in [1, 16]")
@@ -88,6 +92,7 @@ class Problem:
         self.col_n2 = torch.empty(m, **f64)
         self._call("nmfb_sqnorms", _p(self.M), self.f32, n, m, _p(self.row_n2), _p(self.col_n2),
                    _p(self.cwork), self.cwork.numel(), self.stream)
+        self.comm.sum_(self.col_n2)
         self.dscal = torch.zeros(256, **f64)
         self.iscal = torch.zeros(16, dtype=torch.int32, device=self.dev)
         self.hscal = torch.zeros(256, dtype=torch.float64).pin_memory()
@@ -129,9 +134,27 @@ class Problem:
         self._call("nmfb_rowprod", _p(A), f32, rows, cols, _p(B), k, _p(out), _p(tol), 1.0,
                    _p(self.cwork), self.cwork.numel(), self.stream)
 
-    def colprod(self, A, rows, cols, B, k, out, tol=None, f32=0):
+    def colprod(self, A, rows, cols, B, k, out, tol=None, f32=0, reduce=False):
+        """out = A^T B.  reduce=True: A, B are row-sharded -> all-reduce (then tol)."""
+        if reduce and self.comm.active:
+            self._call("nmfb_colprod", _p(A), f32, rows, cols, _p(B), k, _p(out), None, 1.0,
+                       _p(self.cwork), self.cwork.numel(), self.stream)
+            self.comm.sum_(out)
+            if tol is not None:
+                self._call("nmfb_row_tol", _p(out), cols, k, _p(tol), self.stream)
+            return
         self._call("nmfb_colprod", _p(A), f32, rows, cols, _p(B), k, _p(out), _p(tol), 1.0,
                    _p(self.cwork), self.cwork.numel(), self.stream)
+
+    @property
+    def ny_local(self):
+        """Replicated (Y-side) terms of mixed reductions are counted on rank 0 only."""
+        return 1 if self.comm.root else 0
+
+    def reduce_kkt(self, at=16):
+        if self.comm.active:
+            self.comm.sum_(self.dscal[at:at + 8])
+            self.comm.max_(self.dscal[at + 8:at + 12])
 
     def to_dev(self, a):
         if isinstance(a, torch.Tensor):
@@ -144,12 +167,14 @@ class Problem:
         n, m, k = self.n, self.m, self.k
         self._call("nmfb_residual", _p(self.M), self.f32, n, m, k, _p(X), _p(Yt), _p(F), _p(gX),
                    _p(self.dscal[out_index:]), _p(self.rwork), self.stream)
-        self.colprod(F, n, m, X, k, gY)
+        self.comm.sum_(self.dscal[out_index:out_index + 1])
+        self.colprod(F, n, m, X, k, gY, reduce=True)
 
     def kkt_sums(self, X, R, gX, Yt, S, gY, mux, muy, at=16):
         self._call("nmfb_kkt_sums", _p(X), _p(R), _p(gX), X.numel(), _p(Yt), _p(S), _p(gY),
-                   Yt.numel(), float(mux), float(muy), _p(self.dscal[at:]), _p(self.rwork),
-                   self.stream)
+                   Yt.numel() * self.ny_local, float(mux), float(muy), _p(self.dscal[at:]),
+                   _p(self.rwork), self.stream)
+        self.reduce_kkt(at)
 
 
 def kkt_from_sums(v):
@@ -197,19 +222,27 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
             tolX.fill_(float(tol_fixed))
         P._call("nmfb_surface_nnls_batch", _p(GY), _p(ctbX), _p(P.row_n2), _p(pX), mode,
                 _p(tolX), 3 * k, n, k, _p(Xn), _p(pXn), _p(chX), _p(r2X), _p(stX), None, None, s)
-        # Y-update: C = X, d = columns of M
-        P.colprod(Xn, n, k, Xn, k, GX)
-        P.colprod(P.M, n, m, Xn, k, ctbY, tolY, P.f32)
+        # Y-update: C = X, d = columns of M; row contractions all-reduced
+        P.colprod(Xn, n, k, Xn, k, GX, reduce=True)
+        P.colprod(P.M, n, m, Xn, k, ctbY, tolY, P.f32, reduce=True)
         if tol_fixed is not None:
             tolY.fill_(float(tol_fixed))
         P._call("nmfb_surface_nnls_batch", _p(GX), _p(ctbY), _p(P.col_n2), _p(pY), mode,
                 _p(tolY), 3 * k, m, k, _p(Yn), _p(pYn), _p(chY), _p(r2Y), _p(stY), None, None, s)
-        P._call("nmfb_stage1_stats", _p(X), _p(Xn), n * k, _p(Yt), _p(Yn), m * k, _p(r2Y), m,
-                _p(P.dscal), _p(P.rwork), P.rwork.numel(), s)
+        ny = P.ny_local
+        P._call("nmfb_stage1_stats", _p(X), _p(Xn), n * k, _p(Yt), _p(Yn), m * k * ny, _p(r2Y),
+                m * ny, _p(P.dscal), _p(P.rwork), P.rwork.numel(), s)
         P._call("nmfb_first_nonzero_i8", _p(stX), n, _p(P.iscal[0:]), s)
         P._call("nmfb_first_nonzero_i8", _p(stY), m, _p(P.iscal[1:]), s)
+        P.comm.sum_(P.dscal[0:3])
+        if P.comm.active:  # any rank's failing row stops every rank
+            flag = (P.iscal[0:1] != _NONE).to(torch.int32)
+            P.comm.max_(flag)
+            P.iscal[0:1].masked_fill_(flag.bool() & (P.iscal[0:1] == _NONE), -1)
         v, iv = P.readback(3, 2)
         for which, idx, st in (("update_X", int(iv[0]), stX), ("update_Y", int(iv[1]), stY)):
+            if idx == -1:
+                raise status_error(-1, -1, which + " (another rank)")
             if idx != _NONE:
                 raise status_error(int(st[idx].item()), idx, which)
         X, Xn = Xn, X
@@ -239,7 +272,8 @@ class IpmEngine:
         self.kk = k * (k + 1) // 2
         self.X, self.Yt, self.R, self.S = X, Yt, R, S
         self.mu, self.rho, self.flag = float(mu), float(rho), False
-        self.wx, self.wy = barrier_weights(n, m, p.barrier)
+        self.wx, self.wy = barrier_weights(P.n_global, m, p.barrier)
+        self.comm = P.comm
         b = P.buf
         self.F = [b(n, m), b(n, m)]
         self.fi = 0  # index of F at the current point
@@ -316,21 +350,24 @@ class IpmEngine:
         mux, muy = self.wx * self.mu, self.wy * self.mu
         X, Yt, F = self.X, self.Yt, self.Fcur
         P.colprod(Yt, m, k, Yt, k, self.GY)
-        P.colprod(X, n, k, X, k, self.XtX)
+        P.colprod(X, n, k, X, k, self.XtX, reduce=True)
         dense = full or self.dense_gn
         P._call("nmfb_r1_factor", _p(self.GY), _p(X), _p(self.R), _p(self.gX), mux, self.rho, n,
                 k, _p(self.L), _p(self.h), _p(self.g), _p(self.Apk), _p(self.XXpk),
                 _p(P.iscal[2:]), s)
+        self.comm.min_(P.iscal[2:3])
         P._call("nmfb_atb", _p(self.Apk), n, self.kk, _p(self.XXpk), self.kk, _p(self.Z),
                 _p(self.awork), self.awork.numel(), s)
-        P.colprod(X, n, k, self.g, k, self.H)
+        self.comm.sum_(self.Z)
+        P.colprod(X, n, k, self.g, k, self.H, reduce=True)
         W = FtG = None
         if full:
             self._ensure_full_buffers()
             P._call("nmfb_make_p", _p(X), _p(self.Apk), n, k, _p(self.Pbuf), s)
             P._call("nmfb_atb", _p(F), n, m, _p(self.Pbuf), k ** 3, _p(self.W), _p(self.awork),
                     self.awork.numel(), s)
-            P.colprod(F, n, m, self.g, k, self.FtG)
+            self.comm.sum_(self.W)
+            P.colprod(F, n, m, self.g, k, self.FtG, reduce=True)
             W, FtG = self.W, self.FtG
         P._call("nmfb_schur_rhs", _p(Yt), _p(self.gY), _p(self.H), _p(FtG), muy, m, k,
                 _p(self.rhs), s)
@@ -340,7 +377,10 @@ class IpmEngine:
             P._call("nmfb_schur_assemble", _p(Yt), _p(self.S), m, k, _p(self.Z), _p(self.XtX),
                     self.rho, _p(W), _p(self.A), s)
             if full:
+                if self.comm.active and not self.comm.root:
+                    self.A.zero_()  # rank 0 carries the replicated part, others only term 4
                 P._call("nmfb_schur_term4", _p(F), n, m, k, _p(self.Apk), _p(self.A), s)
+                self.comm.sum_(self.A)
             P._call("nmfb_dense_cholesky", _p(self.A), N, _p(P.iscal[3:]), s)
             dY.copy_(self.rhs.view(m, k))
             P._call("nmfb_dense_solve", _p(self.A), N, _p(dY), s)
@@ -362,16 +402,31 @@ class IpmEngine:
                 _p(self.R), _p(self.gX), mux, _p(Yt), _p(self.S), _p(self.gY), _p(dY), muy,
                 self.p.tau, n, m, k, _p(self.dX), _p(self.dR), _p(self.dS), _p(P.dscal[4:]),
                 _p(P.rwork), P.rwork.numel(), s)
+        self.reduce_direction()
         return dY
+
+    def reduce_direction(self):
+        """[gtp, a1, a2, gtp_rows, gtp_cols] at dscal[4:9]: rows summed, minima min-reduced."""
+        if not self.comm.active:
+            return
+        d = self.P.dscal
+        self.comm.sum_(d[7:8])
+        self.comm.min_(d[5:7])
+        d[4:5].copy_(d[7:8] + d[8:9])
 
     def armijo_launch(self, dY):
         """Quartic coefficients + all backtracking barrier sums in two launches."""
         P, s = self.P, self.P.stream
         n, m, k = self.n, self.m, self.k
         P._call("nmfb_quartic", _p(self.Fcur), n, m, k, _p(self.X), _p(self.dX), _p(self.Yt),
-                _p(dY), _p(P.dscal[8:]), _p(P.rwork), s)
+                _p(dY), _p(P.dscal[10:]), _p(P.rwork), s)
         P._call("nmfb_barrier_trials", _p(self.X), _p(self.dX), n * k, _p(self.Yt), _p(dY), m * k,
                 _p(P.dscal[5:]), NTRIALS, _p(P.dscal[32:]), _p(P.rwork), P.rwork.numel(), s)
+        if self.comm.active:
+            self.comm.sum_(P.dscal[10:16])
+            bx = P.dscal[32:32 + 2 * NTRIALS].view(NTRIALS, 2)[:, 0].contiguous()
+            self.comm.sum_(bx)
+            P.dscal[32:32 + 2 * NTRIALS].view(NTRIALS, 2)[:, 0].copy_(bx)
 
     def remember_factorization(self, full):
         self.Xf.copy_(self.X)
@@ -388,10 +443,10 @@ class IpmEngine:
         full = self.fact_full
         Ff = self.F[self.fact_F]
         P._call("nmfb_hg", _p(self.L), _p(self.gX), -1.0, n, k, _p(self.h), _p(self.g), s)
-        P.colprod(self.Xf, n, k, self.g, k, self.H)
+        P.colprod(self.Xf, n, k, self.g, k, self.H, reduce=True)
         FtG = None
         if full:
-            P.colprod(Ff, n, m, self.g, k, self.FtG)
+            P.colprod(Ff, n, m, self.g, k, self.FtG, reduce=True)
             FtG = self.FtG
         P._call("nmfb_schur_rhs", _p(self.Ytf), _p(self.gY), _p(self.H), _p(FtG), 0.0, m, k,
                 _p(self.rhs), s)
@@ -410,13 +465,15 @@ class IpmEngine:
                 _p(self.X), _p(self.R), _p(self.gX), 0.0, _p(self.Yt), _p(self.S), _p(self.gY),
                 _p(dY), 0.0, 1.0, n, m, k, _p(self.dX), _p(self.dR), _p(self.dS),
                 _p(P.dscal[4:]), _p(P.rwork), P.rwork.numel(), s)
-        v, _ = P.readback(8)
+        self.reduce_direction()
+        v, _ = P.readback(9)
         a1, a2 = v[5], v[6]
         P._call("nmfb_affine_mu", _p(self.X), _p(self.dX), _p(self.R), _p(self.dR), n * k,
-                _p(self.Yt), _p(dY), _p(self.S), _p(self.dS), m * k, a1, a2, _p(P.dscal[0:]),
-                _p(P.rwork), s)
+                _p(self.Yt), _p(dY), _p(self.S), _p(self.dS), m * k * P.ny_local, a1, a2,
+                _p(P.dscal[0:]), _p(P.rwork), s)
+        self.comm.sum_(P.dscal[0:1])
         v, _ = P.readback(1)
-        nk = n * k + m * k
+        nk = P.n_global * k + m * k
         mu_aff = v[0] / nk
         mu_bar = (sums[3] + sums[7]) / nk
         return min((mu_aff / mu_bar) ** 3, p.sigma_cap)
@@ -464,7 +521,7 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                                               int(iv[3]))
                 eng.remember_factorization(False)
             gtp, a1max, a2max = v[4], v[5], v[6]
-            aa, ab, bb, ac, bc, cc = v[8:14]
+            aa, ab, bb, ac, bc, cc = v[10:16]
             bars = v[32:32 + 2 * NTRIALS]
             t = 0
             while True:
@@ -527,7 +584,7 @@ def transition(P: Problem, X, Yt, eps_tol, tp: TransitionParams | None = None):
     P._call("nmfb_fill", _p(S), m * k, float(v[25]), s)
     P.kkt_sums(X, R, gX, Yt, S, gY, 0.0, 0.0, at=16)
     v, _ = P.readback(28)
-    mu = (v[19] + v[23]) / (n * k + m * k)
+    mu = (v[19] + v[23]) / (P.n_global * k + m * k)
     return X, Yt, R, S, mu, float(eps_tol)
 
 
@@ -543,16 +600,19 @@ def kkt_error_primal_only_dev(P: Problem, X, Yt):
 
 def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1: Stage1Config | None = None,
                   ipm: IpmParams | None = None, tp: TransitionParams | None = None,
-                  stage="two_stage", pX=None, pY=None, e_scale=None, problem: Problem | None = None):
+                  stage="two_stage", pX=None, pY=None, e_scale=None, problem: Problem | None = None,
+                  comm: Comm | None = None):
     """SPEC.md:411 run_two_stage (Algorithm 3) on the B200.
 
     M (n,m) host or device array (fp64, or fp32 storage); X0 (n,k); Y0 (k,m).
     Relative KKT tolerance: eps_abs = tol_rel * max(1, E_primal(X0, Y0)) unless
-    ``e_scale`` is given (frozen semantics 5).
+    ``e_scale`` is given (frozen semantics 5).  With ``comm`` spanning
+    several GPUs, M / X0 / pX are this rank's row block (dist.row_range) and the
+    returned X / R are the local rows.
     """
     X0n = X0 if isinstance(X0, torch.Tensor) else np.asarray(X0, dtype=np.float64)
     k = X0n.shape[1]
-    P = problem or Problem(M, k)
+    P = problem or Problem(M, k, comm=comm)
     X = P.to_dev(X0)
     Yt = P.to_dev(Y0.T if not isinstance(Y0, torch.Tensor) else Y0.t())
     if e_scale is None:
