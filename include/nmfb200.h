@@ -166,6 +166,15 @@ int nmfb_barrier_trials(const double *X, const double *dX, long nx, const double
                         const double *dYt, long ny, const double *alpha_max, int ntrials,
                         double *out, double *work, long work_len, void *stream);
 
+/* Armijo acceptance on the device: reads the scalar block written by
+ * nmfb_direction / nmfb_quartic / nmfb_barrier_trials (gtp, alpha maxima, quartic
+ * coefficients, barrier sums) and writes alpha1, t, alpha2 (graph-capturable). */
+int nmfb_armijo_select(double *sc, double mu, double wx, double wy, double eta,
+                       int max_backtracks, void *stream);
+/* as nmfb_step_nudge with alpha read from device memory */
+int nmfb_step_nudge_dev(double *v, const double *dv, long len, const double *alpha, double tau,
+                        void *stream);
+
 /* v += alpha dv with the (1 - tau) nudge */
 int nmfb_step_nudge(double *v, const double *dv, long len, double alpha, double tau,
                     void *stream);

@@ -388,10 +388,11 @@ def quartic_coeffs(X, Yt, dX, dYt, M, comm=None):
 def merit_delta(coef, alpha, X, dX, Yt, dYt, mu, wx=1.0, wy=1.0, comm=None):
     """phi(x + a dx, y + a dy) - phi(x, y), evaluated without cancellation."""
     _, ab, bb, ac, bc, cc = coef
-    quad = alpha * ab + alpha * alpha * (0.5 * bb + ac) + alpha ** 3 * bc + 0.5 * alpha ** 4 * cc
+    a2, a3 = alpha * alpha, alpha * alpha * alpha
+    quad = alpha * ab + a2 * (0.5 * bb + ac) + a3 * bc + 0.5 * (a3 * alpha) * cc
     bx = _red(comm, float(np.sum(np.log1p(alpha * dX / X))))
     by = float(np.sum(np.log1p(alpha * dYt / Yt)))
-    return quad - mu * (wx * bx + wy * by)
+    return quad - mu * (wx * bx + wy * by)  # same evaluation order as the device selector
 
 
 def merit_phi(X, Yt, M, mu):

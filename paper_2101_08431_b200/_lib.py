@@ -49,6 +49,8 @@ SIGNATURES = {
     "nmfb_quartic": [P, L, L, L, P, P, P, P, P, P, P],
     "nmfb_barrier_trials": [P, P, L, P, P, L, P, I, P, P, L, P],
     "nmfb_step_nudge": [P, P, L, D, D, P],
+    "nmfb_armijo_select": [P, D, D, D, D, I, P],
+    "nmfb_step_nudge_dev": [P, P, L, P, D, P],
     "nmfb_kkt_sums": [P, P, P, L, P, P, P, L, D, D, P, P, P],
     "nmfb_affine_mu": [P, P, P, P, L, P, P, P, P, L, D, D, P, P, P],
     "nmfb_clamp_min": [P, L, D, P],

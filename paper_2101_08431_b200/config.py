@@ -34,6 +34,7 @@ class IpmParams:
     fixed_iters: int = 0  # > 0: exactly this many inner iterations (configs c4/c5)
     barrier: str = "paper"  # "paper" (one mu) | "balanced" (see solver.barrier_weights)
     schur_solver: str = "lowrank"  # Gauss-Newton reduced system: "lowrank" (exact, rank k^2) | "dense"
+    use_graphs: bool = True  # replay each Gauss-Newton iteration as a captured CUDA graph
 
 
 @dataclass

@@ -787,6 +787,52 @@ __global__ void k_fill(double* __restrict__ v, long len, double c) {
     v[e] = c;
 }
 
+// Armijo acceptance on the device (same arithmetic as the host loop in
+// solver.run_ipm): first t with dphi(a1max 2^-t) <= eta a 2^-t gtp.
+// sc layout: [4] gtp, [5] a1max, [6] a2max, [10..15] quartic, [32 + 2t (+1)] barrier sums.
+// Writes sc[1] = alpha1 (0 when stalled), sc[2] = t (max_bt + 1 when stalled), sc[3] = alpha2.
+__global__ void k_armijo_select(double* __restrict__ sc, double mu, double wx, double wy,
+                                double eta, int max_bt) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double gtp = sc[4], a1max = sc[5];
+  const double ab = sc[11], bb = sc[12], ac = sc[13], bc = sc[14], cc = sc[15];
+  int t = 0;
+  double a1 = a1max;
+  // explicit _rn operations: no FMA contraction, same evaluation order as the host
+  // expression a*ab + a*a*(0.5*bb + ac) + a*a*a*bc + 0.5*(a*a*a*a)*cc
+  const double c2 = __dadd_rn(__dmul_rn(0.5, bb), ac);
+  for (;;) {
+    a1 = a1max / ldexp(1.0, t);
+    const double a2 = __dmul_rn(a1, a1), a3 = __dmul_rn(a2, a1), a4 = __dmul_rn(a3, a1);
+    double quad = __dadd_rn(__dmul_rn(a1, ab), __dmul_rn(a2, c2));
+    quad = __dadd_rn(quad, __dmul_rn(a3, bc));
+    quad = __dadd_rn(quad, __dmul_rn(__dmul_rn(0.5, a4), cc));
+    const double bar = __dadd_rn(__dmul_rn(wx, sc[32 + 2 * t]), __dmul_rn(wy, sc[33 + 2 * t]));
+    const double dphi = __dsub_rn(quad, __dmul_rn(mu, bar));
+    if (dphi <= __dmul_rn(__dmul_rn(eta, a1), gtp)) break;
+    ++t;
+    if (t > max_bt) {
+      a1 = 0.0;
+      break;
+    }
+  }
+  sc[1] = a1;
+  sc[2] = (double)t;
+  sc[3] = (t > max_bt) ? 0.0 : sc[6];
+}
+
+// v += (*alpha) dv with the (1 - tau) nudge, alpha read from device memory
+__global__ void k_step_nudge_dev(double* __restrict__ v, const double* __restrict__ dv, long len,
+                                 const double* __restrict__ alpha, double tau) {
+  const double a = *alpha;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += (long)gridDim.x * blockDim.x) {
+    const double old = v[e];
+    const double nv = old + a * dv[e];
+    v[e] = (nv > 0.0) ? nv : (1.0 - tau) * old;
+  }
+}
+
 constexpr int RED_BLOCKS = 296;  // fixed -> deterministic reductions
 
 }  // namespace
@@ -1065,6 +1111,23 @@ extern "C" int nmfb_fill(double* v, long len, double c, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (len <= 0) return NMFB_OK;
   ++g_nmfb_launches, k_fill<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, len, c);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_armijo_select(double* sc, double mu, double wx, double wy, double eta,
+                                  int max_backtracks, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  ++g_nmfb_launches, k_armijo_select<<<1, 32, 0, st>>>(sc, mu, wx, wy, eta, max_backtracks);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_step_nudge_dev(double* v, const double* dv, long len, const double* alpha,
+                                   double tau, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (len <= 0) return NMFB_OK;
+  ++g_nmfb_launches, k_step_nudge_dev<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, dv, len, alpha, tau);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

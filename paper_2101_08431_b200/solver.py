@@ -61,7 +61,9 @@ class Problem:
         self.lib = _lib.load()
         self.launches = 0
         self.instrument = set()
-        self.event_log = []
+        self.event_log = []  # (start, end) events of instrumented launches
+        self.captured_events = []  # pairs recorded inside a graph being captured
+        self.event_times = []  # resolved durations (ms) of instrumented launches in graphs
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         if isinstance(M, np.ndarray):
             if M.dtype not in (np.float64, np.float32):
@@ -111,7 +113,10 @@ class Problem:
             e0.record(st)
             rc = getattr(self.lib, name)(*args)
             e1.record(st)
-            self.event_log.append((e0, e1))
+            if torch.cuda.is_current_stream_capturing():
+                self.captured_events.append((e0, e1))  # re-recorded by every graph replay
+            else:
+                self.event_log.append((e0, e1))
         else:
             rc = getattr(self.lib, name)(*args)
         self.launches += 1
@@ -300,6 +305,9 @@ class IpmEngine:
         self.have_fact = False
         self.fact_full = False
         self.fact_F = 0
+        self.graphs = {}
+        self.graph_pool = None
+        self.use_graphs = p.use_graphs and not P.comm.active and not self.dense_gn
         self.Pbuf = None
         self.W = None
         aw = max(P.lib.nmfb_atb_work_len(n, self.kk, self.kk),
@@ -311,17 +319,66 @@ class IpmEngine:
     def Fcur(self):
         return self.F[self.fi]
 
-    def refresh(self):
-        """Gradients + KKT sums at the current point -> (E_mu, E_0, fsq, sums)."""
+    def refresh_launch(self):
+        """Launch gradients + KKT sums at the current point (no host sync)."""
         P = self.P
         if self.have_fact and self.fact_F == self.fi:
             self.fi ^= 1  # keep the factorization's residual for the predictor
         P.gradients(self.X, self.Yt, self.Fcur, self.gX, self.gY, out_index=0)
         P.kkt_sums(self.X, self.R, self.gX, self.Yt, self.S, self.gY, self.wx * self.mu,
                    self.wy * self.mu, at=16)
-        v, _ = P.readback(28)
+
+    def refresh(self):
+        """Gradients + KKT sums at the current point -> (E_mu, E_0, fsq, sums)."""
+        self.refresh_launch()
+        v, _ = self.P.readback(28)
         e_mu, e_0 = kkt_from_sums(v[16:28])
         return e_mu, e_0, v[0], v[16:28]
+
+    # -- one Gauss-Newton inner iteration entirely on the device ---------------
+    def gn_iteration_launch(self):
+        """direction (GN) -> Armijo sums -> device Armijo selection -> update ->
+        gradients/KKT at the new point.  No host synchronisation, so the whole
+        sequence is captured once per (mu, F buffer) as a CUDA graph and replayed."""
+        P, p = self.P, self.p
+        n, m, k = self.n, self.m, self.k
+        dY = self.direction(False)
+        self.armijo_launch(dY)
+        s = P.stream
+        P._call("nmfb_armijo_select", _p(P.dscal), self.mu, self.wx, self.wy, p.eta,
+                p.max_backtracks, s)
+        self.remember_factorization(False)  # the factorization's X, Y (before the step)
+        a1p, a2p = P.dscal[1:2], P.dscal[3:4]
+        P._call("nmfb_step_nudge_dev", _p(self.X), _p(self.dX), n * k, _p(a1p), p.tau, s)
+        P._call("nmfb_step_nudge_dev", _p(self.Yt), _p(dY), m * k, _p(a1p), p.tau, s)
+        P._call("nmfb_step_nudge_dev", _p(self.R), _p(self.dR), n * k, _p(a2p), p.tau, s)
+        P._call("nmfb_step_nudge_dev", _p(self.S), _p(self.dS), m * k, _p(a2p), p.tau, s)
+        self.refresh_launch()
+
+    def gn_iteration_graph(self):
+        """Replay (capturing on first use) the GN iteration graph for the current state."""
+        key = (self.fi, self.mu)
+        g = self.graphs.get(key)
+        state = (self.fi, self.fact_F, self.have_fact, self.fact_full, self.fact_dense)
+        if g is None:
+            if len(self.graphs) > 8:
+                self.graphs.clear()
+            g = torch.cuda.CUDAGraph()
+            self.P.captured_events = []
+            with torch.cuda.graph(g, pool=self.graph_pool):
+                self.gn_iteration_launch()
+            self.graph_pool = g.pool()
+            self.graphs[key] = (g, self.P.captured_events)
+            self.P.captured_events = []
+            self.fi, self.fact_F, self.have_fact, self.fact_full, self.fact_dense = state
+        else:
+            g = g[0]
+        g.replay()
+        self.last_graph = key
+        # mirror the host-side bookkeeping the captured sequence performs
+        self.fact_F, self.have_fact, self.fact_full, self.fact_dense = state[0], True, False, False
+        self.last_dense = False
+        self.fi = state[0] ^ 1
 
     def _ensure_full_buffers(self):
         if self.Pbuf is None:
@@ -508,6 +565,29 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                     eng.remember_factorization(True)
                 else:
                     eng.flag = False
+            if not ok and eng.use_graphs:
+                eng.gn_iteration_graph()
+                v, iv = P.readback(28, 5)
+                for e0, e1 in eng.graphs[eng.last_graph][1]:
+                    P.event_times.append(e0.elapsed_time(e1))
+                if int(iv[2]) != _NONE:
+                    raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
+                if int(iv[4]) != _NONE:
+                    raise NotPositiveDefinite("R2 block not positive definite", int(iv[4]))
+                if int(iv[3]) >= 0:
+                    raise NotPositiveDefinite("Gauss-Newton Schur matrix not positive definite",
+                                              int(iv[3]))
+                t = int(v[2])
+                if t > p.max_backtracks:
+                    raise LineSearchStall(f"Armijo backtracking exceeded {p.max_backtracks}")
+                a1, a2max = v[1], v[3]
+                res.iters += 1
+                res.armijo_t.append(t)
+                res.flags.append(False)
+                e_mu, e_zero = kkt_from_sums(v[16:28])
+                fsq, sums = v[0], v[16:28]
+                res.trace.append((time.perf_counter() - t0, 0.5 * fsq, e_zero, eng.mu, a1, a2max, t))
+                continue
             if not ok:
                 dY = eng.direction(False)
                 eng.armijo_launch(dY)
@@ -526,7 +606,8 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
             t = 0
             while True:
                 a1 = a1max / (2.0 ** t)
-                quad = a1 * ab + a1 * a1 * (0.5 * bb + ac) + a1 ** 3 * bc + 0.5 * a1 ** 4 * cc
+                a2_, a3_ = a1 * a1, a1 * a1 * a1
+                quad = a1 * ab + a2_ * (0.5 * bb + ac) + a3_ * bc + 0.5 * (a3_ * a1) * cc
                 dphi = quad - eng.mu * (eng.wx * bars[2 * t] + eng.wy * bars[2 * t + 1])
                 if dphi <= p.eta * a1 * gtp:
                     break
