@@ -192,11 +192,12 @@ def run_b200(args):
     timed_entry = args.roofline_entry
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
 
-    def step():
+    def step(use_graphs=True):
         X, Yt, pX, pY, r1 = solver.run_stage1(P, X0d, Yt0d, Stage1Config())
         X, Yt, R, S, mu, rho = solver.transition(P, X, Yt, eps_abs)
-        eng, r2 = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(eps_tol=eps_abs,
-                                                                     max_iter=IPM_CAP))
+        eng, r2 = solver.run_ipm(P, X, Yt, R, S, mu, rho,
+                                 IpmParams(eps_tol=eps_abs, max_iter=IPM_CAP,
+                                           use_graphs=use_graphs))
         return r1.sweeps, r2.iters, r2.converged, r2.trace[-1][2] if r2.trace else float("nan")
 
     for _ in range(max(3, args.warmup)):
@@ -239,6 +240,17 @@ def run_b200(args):
     else:
         tot_units, tot_sw, tot_it = float(sweeps + iters), float(sweeps), float(iters)
     kt = [a.elapsed_time(b) for a, b in P.event_log] + list(P.event_times)
+    kt_note = "CUDA events around every launch of the entry inside the timed steps"
+    if P.graph_timing_failed or not kt:
+        # events inside replayed graphs were not timeable: re-run ONE step with graphs
+        # off right after the timed region and time the entry's launches there
+        P.event_log, P.event_times = [], []
+        step(use_graphs=False)
+        torch.cuda.synchronize()
+        kt = [a.elapsed_time(b) for a, b in P.event_log]
+        kt_note = ("CUDA events around the entry's launches in one extra step with graphs "
+                   "disabled, right after the timed region (events inside replayed graphs "
+                   "are not timeable)")
     P.instrument = set()
     value = tot_units / (total_ms / 1e3)
     # e2e through the public API with host inputs (H2D of M/X0/Y0, D2H of X, Y, R, S)
@@ -282,7 +294,7 @@ def run_b200(args):
         "converged": bool(conv), "final_kkt": kkt,
         "roofline": {"bound": "tensor", "kernel": timed_entry, "achieved": achieved,
                      "peak": fp64_peak, "unit": "TFLOP/s", "frac": (achieved / fp64_peak) if achieved else None,
-                     "traffic": None, "launches": len(kt), "avg_ms": avg_ms,
+                     "traffic": None, "launches": len(kt), "avg_ms": avg_ms, "timing": kt_note,
                      "algorithmic": f"(mk)^3/3 = {flops:.3e} FP64 flops per launch (N = mk = {N})",
                      "peak_source": "fp64 cuBLAS DGEMM 8192^3 measured live (MEASURED_PEAKS.json has no fp64 entry)"},
         "gpu_launches": int(launches),

@@ -64,6 +64,7 @@ class Problem:
         self.event_log = []  # (start, end) events of instrumented launches
         self.captured_events = []  # pairs recorded inside a graph being captured
         self.event_times = []  # resolved durations (ms) of instrumented launches in graphs
+        self.graph_timing_failed = False
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         if isinstance(M, np.ndarray):
             if M.dtype not in (np.float64, np.float32):
@@ -108,12 +109,14 @@ class Problem:
     def _call(self, name, *args):
         if name in self.instrument:  # CUDA events on the launching stream (bench roofline)
             st = torch.cuda.current_stream(self.dev)
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
+            cap = torch.cuda.is_current_stream_capturing()
+            ext = dict(external=True) if cap else {}
+            e0 = torch.cuda.Event(enable_timing=True, **ext)
+            e1 = torch.cuda.Event(enable_timing=True, **ext)
             e0.record(st)
             rc = getattr(self.lib, name)(*args)
             e1.record(st)
-            if torch.cuda.is_current_stream_capturing():
+            if cap:
                 self.captured_events.append((e0, e1))  # re-recorded by every graph replay
             else:
                 self.event_log.append((e0, e1))
@@ -569,7 +572,10 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                 eng.gn_iteration_graph()
                 v, iv = P.readback(28, 5)
                 for e0, e1 in eng.graphs[eng.last_graph][1]:
-                    P.event_times.append(e0.elapsed_time(e1))
+                    try:
+                        P.event_times.append(e0.elapsed_time(e1))
+                    except Exception:  # event nodes not timeable on this stack
+                        P.graph_timing_failed = True
                 if int(iv[2]) != _NONE:
                     raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
                 if int(iv[4]) != _NONE:
