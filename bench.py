@@ -212,7 +212,7 @@ def run_b200(args):
     clocks = Clocks(local)
     clocks.start()
     torch.cuda.synchronize()
-    launches0 = P.lib.nmfb_launch_count()
+    launches0 = P.lib.nmfb_launch_count() + P.graph_kernel_launches
     total_ms, sweeps, iters, conv, kkt = 0.0, 0, 0, True, 0.0
     stream = torch.cuda.current_stream()
     for _ in range(args.steps):
@@ -226,7 +226,7 @@ def run_b200(args):
         total_ms += e0.elapsed_time(e1)
         sweeps, iters, conv, kkt = sweeps + s, iters + i, conv and c, e
     torch.cuda.synchronize()
-    launches = P.lib.nmfb_launch_count() - launches0
+    launches = P.lib.nmfb_launch_count() + P.graph_kernel_launches - launches0
     clk = clocks.stop()
     if ws > 1:
         import torch.distributed as dist

@@ -65,6 +65,7 @@ class Problem:
         self.captured_events = []  # pairs recorded inside a graph being captured
         self.event_times = []  # resolved durations (ms) of instrumented launches in graphs
         self.graph_timing_failed = False
+        self.graph_kernel_launches = 0  # library kernels executed inside replayed graphs
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         if isinstance(M, np.ndarray):
             if M.dtype not in (np.float64, np.float32):
@@ -368,15 +369,17 @@ class IpmEngine:
                 self.graphs.clear()
             g = torch.cuda.CUDAGraph()
             self.P.captured_events = []
+            c0 = self.P.lib.nmfb_launch_count()
             with torch.cuda.graph(g, pool=self.graph_pool):
                 self.gn_iteration_launch()
+            nk = self.P.lib.nmfb_launch_count() - c0
             self.graph_pool = g.pool()
-            self.graphs[key] = (g, self.P.captured_events)
+            self.graphs[key] = (g, self.P.captured_events, nk)
             self.P.captured_events = []
             self.fi, self.fact_F, self.have_fact, self.fact_full, self.fact_dense = state
-        else:
-            g = g[0]
+        g, _, nk = self.graphs[key]
         g.replay()
+        self.P.graph_kernel_launches += nk  # kernels executed by this replay
         self.last_graph = key
         # mirror the host-side bookkeeping the captured sequence performs
         self.fact_F, self.have_fact, self.fact_full, self.fact_dense = state[0], True, False, False
