@@ -107,8 +107,9 @@ class Problem:
     def stream(self):
         return torch.cuda.current_stream(self.dev).cuda_stream
 
-    def _call(self, name, *args):
-        if name in self.instrument:  # CUDA events on the launching stream (bench roofline)
+    def _call(self, name, *args, tag=None):
+        if name in self.instrument or (tag is not None and tag in self.instrument):
+            # CUDA events on the launching stream (bench roofline)
             st = torch.cuda.current_stream(self.dev)
             cap = torch.cuda.is_current_stream_capturing()
             ext = dict(external=True) if cap else {}
@@ -143,17 +144,17 @@ class Problem:
         self._call("nmfb_rowprod", _p(A), f32, rows, cols, _p(B), k, _p(out), _p(tol), 1.0,
                    _p(self.cwork), self.cwork.numel(), self.stream)
 
-    def colprod(self, A, rows, cols, B, k, out, tol=None, f32=0, reduce=False):
+    def colprod(self, A, rows, cols, B, k, out, tol=None, f32=0, reduce=False, tag=None):
         """out = A^T B.  reduce=True: A, B are row-sharded -> all-reduce (then tol)."""
         if reduce and self.comm.active:
             self._call("nmfb_colprod", _p(A), f32, rows, cols, _p(B), k, _p(out), None, 1.0,
-                       _p(self.cwork), self.cwork.numel(), self.stream)
+                       _p(self.cwork), self.cwork.numel(), self.stream, tag=tag)
             self.comm.sum_(out)
             if tol is not None:
                 self._call("nmfb_row_tol", _p(out), cols, k, _p(tol), self.stream)
             return
         self._call("nmfb_colprod", _p(A), f32, rows, cols, _p(B), k, _p(out), _p(tol), 1.0,
-                   _p(self.cwork), self.cwork.numel(), self.stream)
+                   _p(self.cwork), self.cwork.numel(), self.stream, tag=tag)
 
     @property
     def ny_local(self):
@@ -177,7 +178,7 @@ class Problem:
         self._call("nmfb_residual", _p(self.M), self.f32, n, m, k, _p(X), _p(Yt), _p(F), _p(gX),
                    _p(self.dscal[out_index:]), _p(self.rwork), self.stream)
         self.comm.sum_(self.dscal[out_index:out_index + 1])
-        self.colprod(F, n, m, X, k, gY, reduce=True)
+        self.colprod(F, n, m, X, k, gY, reduce=True, tag="graY")
 
     def kkt_sums(self, X, R, gX, Yt, S, gY, mux, muy, at=16):
         self._call("nmfb_kkt_sums", _p(X), _p(R), _p(gX), X.numel(), _p(Yt), _p(S), _p(gY),
