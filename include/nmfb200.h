@@ -214,6 +214,24 @@ int nmfb_lowrank_solve(const double *LD, const double *Yt, const double *LG, con
                        const double *Zb, long m, long k, const double *rhs, double *dy, double *u,
                        double *w, double *cwork, long cwork_len, void *stream);
 
+/* Fused small-problem Gauss-Newton iteration (k <= 4, m k <= 2048; configs c1-c3):
+ * the same mathematics as the general entries in 3 + 3 kernels with deterministic
+ * last-CTA reductions.  tickets: 4 zero-initialised uint32 counters (self-resetting). */
+int nmfb_small_supported(long n, long m, long k);
+long nmfb_small_work_len(long n, long m, long k);
+int nmfb_small_direction(const double *X, const double *R, const double *gX, const double *Yt,
+                         const double *S, const double *gY, long n, long m, long k, double mux,
+                         double muy, double rho, double tau, double *L, double *h, double *LD,
+                         double *LG, double *LH, double *Zb, double *Z, double *H, double *XtX,
+                         double *dX, double *dR, double *dY, double *dS, double *Gdy, double *sc,
+                         int *iscal, double *work, unsigned int *tickets, void *stream);
+int nmfb_small_step_refresh(const void *M, int m_is_f32, long n, long m, long k, double *X,
+                            double *R, double *Yt, double *S, const double *dX, const double *dR,
+                            const double *dY, const double *dS, double *Xf, double *Ytf,
+                            double *Fold, double *Fnew, double *gX, double *gY, double mu,
+                            double wx, double wy, double eta, int max_bt, double tau, int ntrials,
+                            double *sc, double *work, unsigned int *tickets, void *stream);
+
 /* number of kernel launches issued by this library so far (host counter) */
 unsigned long long nmfb_launch_count(void);
 

@@ -26,6 +26,7 @@ SOURCES = {
     "ipm.cu": [],
     "dense.cu": [],
     "lowrank.cu": [],
+    "small.cu": [],
     "runtime.cu": [],
 }
 

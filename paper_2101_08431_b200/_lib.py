@@ -59,11 +59,15 @@ SIGNATURES = {
     "nmfb_dense_solve": [P, L, P, P],
     "nmfb_launch_count": [],
     "nmfb_d_factor": [P, P, P, D, L, L, P, P, P, P, P],
+    "nmfb_small_supported": [L, L, L],
+    "nmfb_small_work_len": [L, L, L],
+    "nmfb_small_direction": [P, P, P, P, P, P, L, L, L, D, D, D, D] + [P] * 19,
+    "nmfb_small_step_refresh": [P, I, L, L, L] + [P] * 14 + [D, D, D, D, I, D, I, P, P, P, P],
     "nmfb_lowrank_factor": [P, P, L, P, P, P, P, P],
     "nmfb_lowrank_solve": [P, P, P, P, P, L, L, P, P, P, P, P, L, P],
 }
 RESTYPES = {"nmfb_colprod_work_len": ctypes.c_long, "nmfb_rowprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
-            "nmfb_launch_count": ctypes.c_ulonglong}
+            "nmfb_launch_count": ctypes.c_ulonglong, "nmfb_small_work_len": ctypes.c_long}
 
 _lib = None
 

@@ -313,6 +313,12 @@ class IpmEngine:
         self.graphs = {}
         self.graph_pool = None
         self.use_graphs = p.use_graphs and not P.comm.active and not self.dense_gn
+        # fused small-problem iteration (csrc/small.cu) for c1-c3-sized problems
+        self.small = bool(P.lib.nmfb_small_supported(n, m, k)) and not P.comm.active \
+            and not self.dense_gn and p.fused_small
+        if self.small:
+            self.swork = b(max(P.lib.nmfb_small_work_len(n, m, k), 1))
+            self.tickets = torch.zeros(8, dtype=torch.int32, device=P.dev)
         self.Pbuf = None
         self.W = None
         aw = max(P.lib.nmfb_atb_work_len(n, self.kk, self.kk),
@@ -347,6 +353,24 @@ class IpmEngine:
         sequence is captured once per (mu, F buffer) as a CUDA graph and replayed."""
         P, p = self.P, self.p
         n, m, k = self.n, self.m, self.k
+        if self.small:
+            s = P.stream
+            P._call("nmfb_small_direction", _p(self.X), _p(self.R), _p(self.gX), _p(self.Yt),
+                    _p(self.S), _p(self.gY), n, m, k, self.wx * self.mu, self.wy * self.mu,
+                    self.rho, p.tau, _p(self.L), _p(self.h), _p(self.LD), _p(self.LG),
+                    _p(self.LH), _p(self.lrwork), _p(self.Z), _p(self.H), _p(self.XtX),
+                    _p(self.dX), _p(self.dR), _p(self.dYbuf), _p(self.dS), _p(self.Gdy),
+                    _p(P.dscal), _p(P.iscal[2:]), _p(self.swork), _p(self.tickets), s)
+            self.last_dense = False
+            self.remember_factorization_host(False)
+            fold, fnew = self.F[self.fi], self.F[self.fi ^ 1]
+            P._call("nmfb_small_step_refresh", _p(P.M), P.f32, n, m, k, _p(self.X), _p(self.R),
+                    _p(self.Yt), _p(self.S), _p(self.dX), _p(self.dR), _p(self.dYbuf),
+                    _p(self.dS), _p(self.Xf), _p(self.Ytf), _p(fold), _p(fnew), _p(self.gX),
+                    _p(self.gY), self.mu, self.wx, self.wy, p.eta, p.max_backtracks, p.tau,
+                    NTRIALS, _p(P.dscal), _p(self.swork), _p(self.tickets), s)
+            self.fi ^= 1
+            return
         dY = self.direction(False)
         self.armijo_launch(dY)
         s = P.stream
@@ -491,6 +515,13 @@ class IpmEngine:
             bx = P.dscal[32:32 + 2 * NTRIALS].view(NTRIALS, 2)[:, 0].contiguous()
             self.comm.sum_(bx)
             P.dscal[32:32 + 2 * NTRIALS].view(NTRIALS, 2)[:, 0].copy_(bx)
+
+    def remember_factorization_host(self, full):
+        """Bookkeeping only (the fused step kernel copies X, Y itself)."""
+        self.have_fact = True
+        self.fact_full = full
+        self.fact_dense = self.last_dense
+        self.fact_F = self.fi
 
     def remember_factorization(self, full):
         self.Xf.copy_(self.X)
