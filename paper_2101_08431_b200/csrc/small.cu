@@ -62,12 +62,16 @@ __global__ void __launch_bounds__(SX_THREADS) k_sx(
   __shared__ double gy[K * K];
   __shared__ double sA[SX_THREADS][KK], sXX[SX_THREADS][KK], sx[SX_THREADS][K], sg[SX_THREADS][K];
   const int tid = threadIdx.x;
-  // Y Y^T (replicated, fixed order)
-  for (int e = tid; e < K * K; e += blockDim.x) {
-    const int a = e / K, b = e % K;
-    double s = 0.0;
-    for (long j = 0; j < m; ++j) s = fma(Yt[j * K + a], Yt[j * K + b], s);
-    gy[e] = s;
+  // Y Y^T (replicated, fixed order): warp per entry, lanes stride the columns
+  {
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int e = wid; e < K * K; e += SX_THREADS / 32) {
+      const int a = e / K, b = e % K;
+      double s = 0.0;
+      for (long j = lane; j < m; j += 32) s = fma(Yt[j * K + a], Yt[j * K + b], s);
+      s = warp_sum(s);
+      if (lane == 0) gy[e] = s;
+    }
   }
   __syncthreads();
   const long i = (long)blockIdx.x * SX_THREADS + tid;
@@ -182,26 +186,33 @@ __global__ void __launch_bounds__(SX_THREADS) k_sx(
   }
 }
 
-// in-smem Cholesky of a Q x Q matrix (Q <= 16) by warp 0; returns pivot failure or -1
+// in-smem right-looking Cholesky of a Q x Q row-major matrix (Q <= 32) by
+// warp 0, lane = row; returns the failing pivot (-1: PD) in lane 0.  The strict
+// upper triangle is zeroed.
 __device__ int small_chol(double* A, int Q) {
   int fail = -1;
-  if (threadIdx.x == 0) {
-    for (int j = 0; j < Q && fail < 0; ++j) {
-      double s = A[j * Q + j];
-      for (int p = 0; p < j; ++p) s -= A[j * Q + p] * A[j * Q + p];
-      if (!(s > 0.0)) {
+  if (threadIdx.x < 32) {
+    const int r = threadIdx.x;
+    for (int j = 0; j < Q; ++j) {
+      const double pv = A[j * Q + j];
+      if (!(pv > 0.0)) {
         fail = j;
         break;
       }
-      const double d = sqrt(s);
-      A[j * Q + j] = d;
-      for (int r = j + 1; r < Q; ++r) {
-        double t = A[r * Q + j];
-        for (int p = 0; p < j; ++p) t -= A[r * Q + p] * A[j * Q + p];
-        A[r * Q + j] = t / d;
+      const double d = sqrt(pv);
+      __syncwarp();
+      if (r > j && r < Q) A[r * Q + j] /= d;
+      if (r == j) A[j * Q + j] = d;
+      __syncwarp();
+      if (r > j && r < Q) {
+        const double lrj = A[r * Q + j];
+        for (int c = j + 1; c <= r; ++c) A[r * Q + c] -= lrj * A[c * Q + j];
       }
-      for (int c = j + 1; c < Q; ++c) A[j * Q + c] = 0.0;
+      __syncwarp();
     }
+    __syncwarp();
+    if (r < Q)
+      for (int c = r + 1; c < Q; ++c) A[r * Q + c] = 0.0;
   }
   return fail;
 }
@@ -316,21 +327,33 @@ __global__ void __launch_bounds__(256) k_sy(
     for (int a = 0; a < K; ++a) t[j * K + a] = v[a];
   }
   __syncthreads();
-  // 3. G = sum_j (y_j y_j^T) (x) D_j^{-1} (unpacked Q x Q), Zb unpacked, u = U^T t
+  // 3. G = sum_j (y_j y_j^T) (x) D_j^{-1} (unpacked Q x Q), Zb unpacked, u = U^T t;
+  //    warp per entry, lanes stride j, fixed butterfly -> deterministic
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int e = wid; e < KK * KK + Q; e += nw) {
+    double s = 0.0;
+    if (e < KK * KK) {
+      const int ab = e / KK, pq = e % KK;
+      for (long j = lane; j < m; j += 32) s = fma(yy[j * KK + ab], dinv[j * KK + pq], s);
+    } else {
+      const int q = e - KK * KK, a = q / K, p = q % K;
+      for (long j = lane; j < m; j += 32) s = fma(Yt[j * K + a], t[j * K + p], s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      if (e < KK * KK)
+        T1[e] = s;  // packed G, unpacked below
+      else
+        u[e - KK * KK] = s;
+    }
+  }
+  __syncthreads();
   for (int e = tid; e < Q * Q; e += nt) {
     const int r = e / Q, c = e % Q;
     const int a = r / K, p = r % K, b = c / K, q = c % K;
     const int ab = pkx(a, b, K), pq = pkx(p, q, K);
-    double s = 0.0;
-    for (long j = 0; j < m; ++j) s = fma(yy[j * KK + ab], dinv[j * KK + pq], s);
-    G[e] = s;
+    G[e] = T1[ab * KK + pq];
     Zb[e] = Zpk[ab * KK + pq];
-  }
-  for (int e = tid; e < Q; e += nt) {
-    const int a = e / K, p = e % K;
-    double s = 0.0;
-    for (long j = 0; j < m; ++j) s = fma(Yt[j * K + a], t[j * K + p], s);
-    u[e] = s;
   }
   __syncthreads();
   // 4. LG = chol(G); H = I - LG^T Zb LG; LH = chol(H)
@@ -430,14 +453,14 @@ __global__ void __launch_bounds__(256) k_sy(
     }
   }
   __syncthreads();
-  for (int e = tid; e < K * K; e += nt) {  // Gdy = sum_j y_j dy_j^T
+  for (int e = wid; e < K * K; e += nw) {  // Gdy = sum_j y_j dy_j^T
     const int a = e / K, b = e % K;
     double s = 0.0;
-    for (long j = 0; j < m; ++j) s = fma(Yt[j * K + a], t[j * K + b], s);
-    Gdy[e] = s;
+    for (long j = lane; j < m; j += 32) s = fma(Yt[j * K + a], t[j * K + b], s);
+    s = warp_sum(s);
+    if (lane == 0) Gdy[e] = s;
   }
   // fixed-tree block reductions of the Y-side scalars
-  const int lane = tid & 31, wid = tid >> 5;
   gtp = warp_sum(gtp);
   a1 = warp_min(a1);
   a2 = warp_min(a2);
@@ -563,6 +586,9 @@ __global__ void __launch_bounds__(128) k_sdir(
 // entries; blocks [ntr, ntr + nq) the quartic partials over (i, j); the last
 // CTA sums the quartic partials.  sc = scalar block (alpha max at sc[5]).
 // ---------------------------------------------------------------------------
+constexpr int SARM_TG = 16;   // trials per group (one accumulator pair each)
+constexpr int SARM_CPG = 8;   // CTAs per trial group
+
 template <int K>
 __global__ void __launch_bounds__(256) k_sarm(
     const double* __restrict__ F, long n, long m, const double* __restrict__ X,
@@ -570,23 +596,50 @@ __global__ void __launch_bounds__(256) k_sarm(
     double* __restrict__ sc, int ntr, double* __restrict__ part,
     unsigned int* __restrict__ ticket) {
   __shared__ double sh[32];
-  const int tid = threadIdx.x;
-  if ((int)blockIdx.x < ntr) {
-    const int t = blockIdx.x;
-    const double alpha = ldexp(sc[5], -t);
-    double sx = 0.0, sy = 0.0;
-    for (long e = tid; e < n * K; e += blockDim.x) sx += log1p(alpha * dX[e] / X[e]);
-    for (long e = tid; e < m * K; e += blockDim.x) sy += log1p(alpha * dY[e] / Yt[e]);
-    sx = block_sum(sx, sh);
+  __shared__ double wred[8][2 * SARM_TG];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int ngroups = (ntr + SARM_TG - 1) / SARM_TG;
+  const int ntrial_ctas = ngroups * SARM_CPG;
+  double* tpart = part + 6 * 256;  // trial partials after the quartic partials
+  if ((int)blockIdx.x < ntrial_ctas) {
+    const int grp = blockIdx.x / SARM_CPG, sub = blockIdx.x % SARM_CPG;
+    const int t0 = grp * SARM_TG;
+    const double amax = sc[5];
+    double ax[SARM_TG], ay[SARM_TG];
+#pragma unroll
+    for (int q = 0; q < SARM_TG; ++q) ax[q] = ay[q] = 0.0;
+    const long nx = n * K, ntot = n * K + m * K;
+    for (long e = (long)sub * blockDim.x + tid; e < ntot; e += (long)SARM_CPG * blockDim.x) {
+      const bool isx = e < nx;
+      const double num = isx ? dX[e] : dY[e - nx], den = isx ? X[e] : Yt[e - nx];
+#pragma unroll
+      for (int q = 0; q < SARM_TG; ++q) {
+        if (t0 + q < ntr) {  // (alpha dv) / v, the oracle's association
+          const double v = log1p(ldexp(amax, -(t0 + q)) * num / den);
+          if (isx)
+            ax[q] += v;
+          else
+            ay[q] += v;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < SARM_TG; ++q) {
+      const double vx = warp_sum(ax[q]), vy = warp_sum(ay[q]);
+      if (lane == 0) {
+        wred[wid][2 * q] = vx;
+        wred[wid][2 * q + 1] = vy;
+      }
+    }
     __syncthreads();
-    sy = block_sum(sy, sh);
-    if (tid == 0) {
-      sc[32 + 2 * t] = sx;
-      sc[33 + 2 * t] = sy;
+    if (tid < 2 * SARM_TG) {
+      double v = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += wred[w][tid];
+      tpart[(long)blockIdx.x * 2 * SARM_TG + tid] = v;
     }
   } else {
-    const long qb = blockIdx.x - ntr, nq = gridDim.x - ntr;
-    double s[6] = {0, 0, 0, 0, 0, 0};
+    const long qb = blockIdx.x - ntrial_ctas, nq = gridDim.x - ntrial_ctas;
+    double sq[6] = {0, 0, 0, 0, 0, 0};
     for (long e = qb * blockDim.x + tid; e < n * m; e += nq * blockDim.x) {
       const long i = e / m, j = e - i * m;
       const double a = F[e];
@@ -598,30 +651,44 @@ __global__ void __launch_bounds__(256) k_sarm(
         b = fma(dx, y, fma(x, dy, b));
         c = fma(dx, dy, c);
       }
-      s[0] = fma(a, a, s[0]);
-      s[1] = fma(a, b, s[1]);
-      s[2] = fma(b, b, s[2]);
-      s[3] = fma(a, c, s[3]);
-      s[4] = fma(b, c, s[4]);
-      s[5] = fma(c, c, s[5]);
+      sq[0] = fma(a, a, sq[0]);
+      sq[1] = fma(a, b, sq[1]);
+      sq[2] = fma(b, b, sq[2]);
+      sq[3] = fma(a, c, sq[3]);
+      sq[4] = fma(b, c, sq[4]);
+      sq[5] = fma(c, c, sq[5]);
     }
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
-      const double v = block_sum(s[q], sh);
-      if (tid == 0) part[qb * 6 + q] = v;
-      __syncthreads();
+      const double v = warp_sum(sq[q]);
+      if (lane == 0) wred[wid][q] = v;
+    }
+    __syncthreads();
+    if (tid < 6) {
+      double v = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += wred[w][tid];
+      part[qb * 6 + tid] = v;
     }
   }
   if (last_cta(ticket)) {
+    const long nq = gridDim.x - ntrial_ctas;
     if (tid < 6) {
-      const long nq = gridDim.x - ntr;
       double v = 0.0;
       for (long b = 0; b < nq; ++b) v += part[b * 6 + tid];
       sc[10 + tid] = v;
     }
+    for (int e = tid; e < 2 * ntr; e += blockDim.x) {
+      const int t = e >> 1, c = e & 1;
+      const int grp = t / SARM_TG, q = t % SARM_TG;
+      double v = 0.0;
+      for (int sub = 0; sub < SARM_CPG; ++sub)
+        v += tpart[((long)(grp * SARM_CPG + sub)) * 2 * SARM_TG + 2 * q + c];
+      sc[32 + e] = v;
+    }
     __syncthreads();
     reset_ticket(ticket);
   }
+  (void)sh;
 }
 
 // ---------------------------------------------------------------------------
@@ -727,6 +794,8 @@ __global__ void __launch_bounds__(256) k_sres(
   const long r0 = (long)blockIdx.x * RB;
   const int nr = (int)min((long)RB, n - r0);
   double fsq = 0.0;
+  // X-part KKT terms (lane 0 of each row's warp): sums 0..3, maxes |g|, x
+  double k0 = 0.0, k1 = 0.0, k2 = 0.0, k3 = 0.0, kg = -1.0 / 0.0, kx = -1.0 / 0.0;
   for (int rr = wid; rr < nr; rr += (int)(blockDim.x >> 5)) {
     const long i = r0 + rr;
     double x[K], g[K];
@@ -746,13 +815,25 @@ __global__ void __launch_bounds__(256) k_sres(
       for (int p = 0; p < K; ++p) g[p] = fma(f, Yt[j * K + p], g[p]);
     }
 #pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const double v = warp_sum(g[p]);
-      if (lane == 0) gX[i * K + p] = v;
+    for (int p = 0; p < K; ++p) g[p] = warp_sum(g[p]);
+    if (lane == 0) {
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        gX[i * K + p] = g[p];
+        const double r = R[i * K + p];
+        const double xr = x[p] * r;
+        k0 = fma(g[p] - r, g[p] - r, k0);
+        k1 = fma(xr - mux, xr - mux, k1);
+        k2 = fma(xr, xr, k2);
+        k3 += xr;
+        kg = fmax(kg, fabs(g[p]));
+        kx = fmax(kx, x[p]);
+      }
     }
   }
   __syncthreads();
-  const long pbase = (long)blockIdx.x * (m * K + 1);
+  const long stride = m * K + 7;
+  const long pbase = (long)blockIdx.x * stride;
   for (long j = tid; j < m; j += blockDim.x) {
     double acc[K];
 #pragma unroll
@@ -767,48 +848,78 @@ __global__ void __launch_bounds__(256) k_sres(
   }
   fsq = block_sum(fsq, sh);
   if (tid == 0) part[pbase + m * K] = fsq;
+  __syncthreads();
+  k0 = block_sum(k0, sh);
+  if (tid == 0) part[pbase + m * K + 1] = k0;
+  __syncthreads();
+  k1 = block_sum(k1, sh);
+  if (tid == 0) part[pbase + m * K + 2] = k1;
+  __syncthreads();
+  k2 = block_sum(k2, sh);
+  if (tid == 0) part[pbase + m * K + 3] = k2;
+  __syncthreads();
+  k3 = block_sum(k3, sh);
+  if (tid == 0) part[pbase + m * K + 4] = k3;
+  __syncthreads();
+  kg = block_max(kg, sh);
+  if (tid == 0) part[pbase + m * K + 5] = kg;
+  __syncthreads();
+  kx = block_max(kx, sh);
+  if (tid == 0) part[pbase + m * K + 6] = kx;
   if (last_cta(ticket)) {
-    const long stride = m * K + 1;
-    for (long e = tid; e < m * K + 1; e += blockDim.x) {
-      double v = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) v += part[(long)b * stride + e];
+    __shared__ double xs[7];
+    for (long e = tid; e < stride; e += blockDim.x) {
+      const bool mx = (e >= m * K + 5);
+      double v = mx ? -1.0 / 0.0 : 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) {
+        const double q = part[(long)b * stride + e];
+        v = mx ? fmax(v, q) : v + q;
+      }
       if (e < m * K)
         gY[e] = v;
       else
-        sc[0] = v;
+        xs[e - m * K] = v;
     }
-    __threadfence_block();
     __syncthreads();
-    // KKT sums (nmfb_kkt_sums layout) over the full vectors
-    double v[12];
-#pragma unroll
-    for (int q = 0; q < 12; ++q) v[q] = (q < 8) ? 0.0 : -1.0 / 0.0;
-    for (long e = tid; e < n * K; e += blockDim.x) {
-      const double x = X[e], r = R[e], g = gX[e];
-      const double xr = x * r;
-      v[0] = fma(g - r, g - r, v[0]);
-      v[1] = fma(xr - mux, xr - mux, v[1]);
-      v[2] = fma(xr, xr, v[2]);
-      v[3] += xr;
-      v[8] = fmax(v[8], fabs(g));
-      v[10] = fmax(v[10], x);
-    }
+    // Y-part KKT sums over the (replicated) y, s, graY
+    double v4 = 0.0, v5 = 0.0, v6 = 0.0, v7 = 0.0, v9 = -1.0 / 0.0, v11 = -1.0 / 0.0;
     for (long e = tid; e < m * K; e += blockDim.x) {
       const double y = Yt[e], s = S[e], g = gY[e];
       const double ys = y * s;
-      v[4] = fma(g - s, g - s, v[4]);
-      v[5] = fma(ys - muy, ys - muy, v[5]);
-      v[6] = fma(ys, ys, v[6]);
-      v[7] += ys;
-      v[9] = fmax(v[9], fabs(g));
-      v[11] = fmax(v[11], y);
+      v4 = fma(g - s, g - s, v4);
+      v5 = fma(ys - muy, ys - muy, v5);
+      v6 = fma(ys, ys, v6);
+      v7 += ys;
+      v9 = fmax(v9, fabs(g));
+      v11 = fmax(v11, y);
     }
-#pragma unroll
-    for (int q = 0; q < 12; ++q) {
-      const double r = q < 8 ? block_sum(v[q], sh) : block_max(v[q], sh);
-      if (tid == 0) sc[16 + q] = r;
-      __syncthreads();
+    v4 = block_sum(v4, sh);
+    __syncthreads();
+    v5 = block_sum(v5, sh);
+    __syncthreads();
+    v6 = block_sum(v6, sh);
+    __syncthreads();
+    v7 = block_sum(v7, sh);
+    __syncthreads();
+    v9 = block_max(v9, sh);
+    __syncthreads();
+    v11 = block_max(v11, sh);
+    if (tid == 0) {
+      sc[0] = xs[0];
+      sc[16] = xs[1];
+      sc[17] = xs[2];
+      sc[18] = xs[3];
+      sc[19] = xs[4];
+      sc[20] = v4;
+      sc[21] = v5;
+      sc[22] = v6;
+      sc[23] = v7;
+      sc[24] = xs[5];
+      sc[25] = v9;
+      sc[26] = xs[6];
+      sc[27] = v11;
     }
+    __syncthreads();
     reset_ticket(ticket);
   }
 }
@@ -833,9 +944,9 @@ extern "C" long nmfb_small_work_len(long n, long m, long k) {
   const long kk = k * (k + 1) / 2;
   const long sx = ((n + SX_THREADS - 1) / SX_THREADS) * (kk * kk + 2 * k * k);
   const long rb = 32;
-  const long sres = ((n + rb - 1) / rb) * (m * k + 1);
+  const long sres = ((n + rb - 1) / rb) * (m * k + 7);
   const long sdir = ((n + 127) / 128) * 3;
-  const long sarm = 6 * 256;
+  const long sarm = 6 * 256 + 64 * 2 * 16;
   long w = sx;
   if (sres > w) w = sres;
   if (sdir > w) w = sdir;
@@ -895,12 +1006,13 @@ extern "C" int nmfb_small_step_refresh(const void* M, int m_is_f32, long n, long
   cudaStream_t st = (cudaStream_t)stream;
   if (!nmfb_small_supported(n, m, k)) return NMFB_EUNSUPPORTED;
   const int nq = 64;
+  const int ntc = ((ntrials + SARM_TG - 1) / SARM_TG) * SARM_CPG;
   const int RB = 32;
   const size_t tile = (size_t)RB * m * sizeof(double);
   const unsigned br = (unsigned)((n + RB - 1) / RB);
 #define CASE(KK_)                                                                                   \
   case KK_:                                                                                         \
-    ++g_nmfb_launches, k_sarm<KK_><<<ntrials + nq, 256, 0, st>>>(Fold, n, m, X, dX, Yt, dY, sc,     \
+    ++g_nmfb_launches, k_sarm<KK_><<<ntc + nq, 256, 0, st>>>(Fold, n, m, X, dX, Yt, dY, sc,        \
                                                                  ntrials, work, tickets + 2);       \
     ++g_nmfb_launches, k_sstep<<<nmfb_blocks((n + m) * KK_, 256, 148 * 4), 256, 0, st>>>(           \
         sc, mu, wx, wy, eta, max_bt, tau, X, R, dX, dR, n * KK_, Yt, S, dY, dS, m * KK_, Xf, Ytf);  \
