@@ -46,6 +46,25 @@ __device__ __forceinline__ void reset_ticket(unsigned int* ticket) {
   if (threadIdx.x == 0) *ticket = 0u;
 }
 
+// sum_b part[b * stride + e] in block order, with 16 loads in flight per batch
+__device__ __forceinline__ double sum_over_blocks(const double* part, long nb, long stride, long e,
+                                                  bool is_max = false) {
+  double acc = is_max ? -1.0 / 0.0 : 0.0;
+  long b = 0;
+  for (; b + 16 <= nb; b += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = part[(b + u) * stride + e];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc = is_max ? fmax(acc, v[u]) : acc + v[u];
+  }
+  for (; b < nb; ++b) {
+    const double q = part[b * stride + e];
+    acc = is_max ? fmax(acc, q) : acc + q;
+  }
+  return acc;
+}
+
 // ---------------------------------------------------------------------------
 // k_sx: thread per row; partial reductions per CTA of Z (kk x kk), H (K x K),
 // X^T X (K x K); the last CTA writes the totals.
@@ -173,8 +192,7 @@ __global__ void __launch_bounds__(SX_THREADS) k_sx(
   }
   if (last_cta(ticket)) {
     for (int e = tid; e < NOUT; e += blockDim.x) {
-      double s = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) s += part[(long)b * NOUT + e];
+      const double s = sum_over_blocks(part, gridDim.x, NOUT, e);
       if (e < KK * KK)
         Zout[e] = s;
       else if (e < KK * KK + K * K)
@@ -564,17 +582,34 @@ __global__ void __launch_bounds__(128) k_sdir(
     part[blockIdx.x * 3 + 2] = m2;
   }
   if (last_cta(ticket)) {
-    if (threadIdx.x == 0) {
-      double g = 0.0, m1 = 1.0, m2 = 1.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) {
-        g += part[b * 3];
-        m1 = fmin(m1, part[b * 3 + 1]);
-        m2 = fmin(m2, part[b * 3 + 2]);
+    __shared__ double fin[3];
+    if (threadIdx.x < 3) {
+      // minima via max of negatives; sums in block order
+      const int q = threadIdx.x;
+      double v;
+      if (q == 0) {
+        v = sum_over_blocks(part, gridDim.x, 3, 0);
+      } else {
+        v = 1.0;
+        long b = 0;
+        const long nb = gridDim.x;
+        for (; b + 16 <= nb; b += 16) {
+          double w[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) w[u] = part[(b + u) * 3 + q];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v = fmin(v, w[u]);
+        }
+        for (; b < nb; ++b) v = fmin(v, part[b * 3 + q]);
       }
-      out[0] = g + ysc[0];
-      out[1] = fmin(m1, ysc[1]);
-      out[2] = fmin(m2, ysc[2]);
-      out[3] = g;
+      fin[q] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      out[0] = fin[0] + ysc[0];
+      out[1] = fmin(fin[1], ysc[1]);
+      out[2] = fmin(fin[2], ysc[2]);
+      out[3] = fin[0];
       out[4] = ysc[0];
       *ticket = 0u;
     }
@@ -587,7 +622,7 @@ __global__ void __launch_bounds__(128) k_sdir(
 // CTA sums the quartic partials.  sc = scalar block (alpha max at sc[5]).
 // ---------------------------------------------------------------------------
 constexpr int SARM_TG = 16;   // trials per group (one accumulator pair each)
-constexpr int SARM_CPG = 8;   // CTAs per trial group
+constexpr int SARM_CPG = 32;  // CTAs per trial group
 
 template <int K>
 __global__ void __launch_bounds__(256) k_sarm(
@@ -672,18 +707,12 @@ __global__ void __launch_bounds__(256) k_sarm(
   }
   if (last_cta(ticket)) {
     const long nq = gridDim.x - ntrial_ctas;
-    if (tid < 6) {
-      double v = 0.0;
-      for (long b = 0; b < nq; ++b) v += part[b * 6 + tid];
-      sc[10 + tid] = v;
-    }
+    if (tid < 6) sc[10 + tid] = sum_over_blocks(part, nq, 6, tid);
     for (int e = tid; e < 2 * ntr; e += blockDim.x) {
       const int t = e >> 1, c = e & 1;
       const int grp = t / SARM_TG, q = t % SARM_TG;
-      double v = 0.0;
-      for (int sub = 0; sub < SARM_CPG; ++sub)
-        v += tpart[((long)(grp * SARM_CPG + sub)) * 2 * SARM_TG + 2 * q + c];
-      sc[32 + e] = v;
+      sc[32 + e] = sum_over_blocks(tpart + (long)grp * SARM_CPG * 2 * SARM_TG + 2 * q + c,
+                                   SARM_CPG, 2 * SARM_TG, 0);
     }
     __syncthreads();
     reset_ticket(ticket);
@@ -870,11 +899,7 @@ __global__ void __launch_bounds__(256) k_sres(
     __shared__ double xs[7];
     for (long e = tid; e < stride; e += blockDim.x) {
       const bool mx = (e >= m * K + 5);
-      double v = mx ? -1.0 / 0.0 : 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) {
-        const double q = part[(long)b * stride + e];
-        v = mx ? fmax(v, q) : v + q;
-      }
+      const double v = sum_over_blocks(part, gridDim.x, stride, e, mx);
       if (e < m * K)
         gY[e] = v;
       else
@@ -946,7 +971,7 @@ extern "C" long nmfb_small_work_len(long n, long m, long k) {
   const long rb = 32;
   const long sres = ((n + rb - 1) / rb) * (m * k + 7);
   const long sdir = ((n + 127) / 128) * 3;
-  const long sarm = 6 * 256 + 64 * 2 * 16;
+  const long sarm = 6 * 256 + 4 * 32 * 2 * 16;
   long w = sx;
   if (sres > w) w = sres;
   if (sdir > w) w = sdir;
