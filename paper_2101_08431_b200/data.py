@@ -109,27 +109,34 @@ def init_factors(n, m, k, seed):
     return rng.uniform(0.0, 1.0, (n, k)), rng.uniform(0.0, 1.0, (k, m))
 
 
-def dense_device(n, m, k, seed, device, dtype, row_block=8192):
+def dense_device(n, m, k, seed, device, dtype, row_block=8192, rows=None):
     """Device-side dense generator for c5-sized M (torch Philox, row blocks).
 
-    Returns (M_dev, X0, Y0) with X0 (n,k), Y0 (k,m) float64 host arrays drawn
-    from PCG64(seed) and M_dev a torch tensor of the requested dtype.  The
-    truth factors come from a separate device generator seeded with ``seed``.
+    Returns (M_dev, X0, Y0): M_dev holds rows [a, b) of M (all rows when
+    ``rows`` is None) in the requested dtype; X0 (rows, k) and Y0 (k, m) are
+    float64 host arrays from PCG64(seed).  The truth factors come from a
+    device generator seeded with ``seed``; the |N(0, 1e-2)| noise of row block
+    r comes from its own generator seeded (seed, r), so any row range (a rank's
+    shard) is generated independently and identically to the full matrix.
     """
     import torch
 
+    a, b = (0, n) if rows is None else rows
     g = torch.Generator(device=device)
     g.manual_seed(int(seed))
     Xt = torch.rand((n, k), generator=g, device=device, dtype=torch.float64)
     Yt = torch.rand((k, m), generator=g, device=device, dtype=torch.float64)
-    M = torch.empty((n, m), device=device, dtype=dtype)
-    for i0 in range(0, n, row_block):
-        i1 = min(n, i0 + row_block)
+    M = torch.empty((b - a, m), device=device, dtype=dtype)
+    gb = torch.Generator(device=device)
+    for r in range(a // row_block, (b + row_block - 1) // row_block):
+        i0, i1 = r * row_block, min(n, (r + 1) * row_block)
+        gb.manual_seed(int(seed) * 1000003 + r)
         blk = Xt[i0:i1] @ Yt
-        blk += torch.randn((i1 - i0, m), generator=g, device=device, dtype=torch.float64).abs_() * 1e-2
-        M[i0:i1] = blk.to(dtype)
+        blk += torch.randn((i1 - i0, m), generator=gb, device=device, dtype=torch.float64).abs_() * 1e-2
+        lo, hi = max(i0, a), min(i1, b)
+        M[lo - a:hi - a] = blk[lo - i0:hi - i0].to(dtype)
         del blk
     rng = np.random.Generator(np.random.PCG64(seed))
-    X0 = rng.uniform(0.0, 1.0, (n, k))
+    X0 = rng.uniform(0.0, 1.0, (n, k))[a:b]
     Y0 = rng.uniform(0.0, 1.0, (k, m))
     return M, X0, Y0
