@@ -277,9 +277,9 @@ def run_b200(args):
     peaks, peak_src = _peaks()
     fp64_peak = measure_fp64_peak(dev)
     avg_ms = float(np.mean(kt)) if kt else float("nan")
-    # graY = F^T X over the residual F (n x m fp64) of the IPM gradient pass:
-    # algorithmic bytes = F read + X read + graY write (+ partials, not counted)
-    nbytes = cfg.n * cfg.m * 8 + cfg.n * cfg.k * 8 + cfg.m * cfg.k * 8
+    # nmfb_small_step_refresh = Armijo sums over F + step + F/graX/graY/KKT at the new
+    # point: algorithmic bytes = F read (quartic) + M read + F write (+ O((n+m)k) vectors)
+    nbytes = 3 * cfg.n * cfg.m * 8 + 12 * (cfg.n + cfg.m) * cfg.k * 8
     achieved = nbytes / (avg_ms * 1e-3) / 1e9 if kt else None
     line = {
         "metric": _metric(), "value": value,
@@ -294,13 +294,14 @@ def run_b200(args):
         "ipm_iters_per_s": tot_it / (total_ms / 1e3),
         "time_to_tol_s": total_ms / 1e3 / args.steps,
         "converged": bool(conv), "final_kkt": kkt,
-        "roofline": {"bound": "hbm", "kernel": f"{timed_entry} (nmfb_colprod: graY = F^T X)",
+        "roofline": {"bound": "hbm", "kernel": f"{timed_entry} (k_sarm + k_sstep + k_sres: "
+                                               "quartic, update, residual/gradients/KKT)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
                      "traffic": None, "launches": len(kt), "avg_ms": avg_ms, "timing": kt_note,
                      "algorithmic_bytes": nbytes, "peak_source": peak_src,
-                     "note": "c2's 2.4 MB F is L2-resident within a step: latency-bound; see aux "
-                             "for the HBM-bound c4 products"},
+                     "note": "c2's M and F (2.4 MB each) are L2-resident within a step: the "
+                             "entry is latency-bound; aux reports the HBM-bound c4 products"},
         "fp64_dgemm_tflops_measured": fp64_peak,
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -445,7 +446,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--roofline-entry", default="graY")
+    ap.add_argument("--roofline-entry", default="nmfb_small_step_refresh")
     ap.add_argument("--no-aux", dest="aux", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

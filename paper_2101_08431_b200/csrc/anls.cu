@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(256, 2) k_rowprod_mma(const T* __restrict__ A,
     const T* arow[RT];
 #pragma unroll
     for (int rt = 0; rt < RT; ++rt) arow[rt] = A + min(r0 + 8 * rt + g, re - 1) * cols + j0 + 2 * t;
-    constexpr int UN = 4;
+    constexpr int UN = 8;
     const int nfull = cw >> 3;  // pairs whose 8 columns are all in range
     int sp = 0;
     for (; sp + UN <= nfull; sp += UN) {
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(256, 2) k_colprod_mma(const T* __restrict__ A,
 #pragma unroll
   for (int r = 0; r < RT2; ++r) colok[r] = jw + 16 * r + 2 * g < cols;
   const bool bok0 = g < K, bok1 = 8 + g < K;
-  constexpr int UN = 4;
+  constexpr int UN = 8;
   long i0 = i_beg;
   for (; i0 + 4 * UN <= i_end; i0 += 4 * UN) {
     double2 a[UN][RT2];
