@@ -232,6 +232,18 @@ int nmfb_small_step_refresh(const void *M, int m_is_f32, long n, long m, long k,
                             double wx, double wy, double eta, int max_bt, double tau, int ntrials,
                             double *sc, double *work, unsigned int *tickets, void *stream);
 
+/* Residual-free IPM pieces for large M (no n x m workspace; csrc/ipm.cu):
+ *   grad[r] = V[r] G - MV[r], part[b] = partial <V, MV>   (graX = X YY^T - M Y^T and
+ *   graY = Y^T XX - (X^T M)^T);  sc[0] = ||M||^2 - 2<X, M Y^T> + <XX, YY>;
+ *   sc[10..15] = quartic Armijo coefficients from k x k Grams and traces. */
+int nmfb_ffree_grad_rows(const double *V, const double *G, const double *MV, long rows, long k,
+                         double *grad, double *part, void *stream);
+int nmfb_ffree_fsq(const double *part, double mnorm2, const double *XX, const double *YY, long k,
+                   double *sc, double *xm_out, void *stream);
+int nmfb_ffree_quartic(const double *A1, const double *A2, const double *XX, const double *B1,
+                       const double *B2, const double *YY, const double *Dgx, const double *Dgy,
+                       const double *Dmd, long k, double *sc, void *stream);
+
 /* number of kernel launches issued by this library so far (host counter) */
 unsigned long long nmfb_launch_count(void);
 

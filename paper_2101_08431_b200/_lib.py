@@ -59,6 +59,9 @@ SIGNATURES = {
     "nmfb_dense_solve": [P, L, P, P],
     "nmfb_launch_count": [],
     "nmfb_d_factor": [P, P, P, D, L, L, P, P, P, P, P],
+    "nmfb_ffree_grad_rows": [P, P, P, L, L, P, P, P],
+    "nmfb_ffree_fsq": [P, D, P, P, L, P, P, P],
+    "nmfb_ffree_quartic": [P, P, P, P, P, P, P, P, P, L, P, P],
     "nmfb_small_supported": [L, L, L],
     "nmfb_small_work_len": [L, L, L],
     "nmfb_small_direction": [P, P, P, P, P, P, L, L, L, D, D, D, D] + [P] * 19,

@@ -1131,3 +1131,125 @@ extern "C" int nmfb_step_nudge_dev(double* v, const double* dv, long len, const 
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Residual-free ("F-free") gradients and Armijo coefficients for large M.
+// With F = X Y - M (never formed):
+//   graX = X (Y Y^T) - M Y^T,   graY = (X^T X) Y - X^T M   (rows of Y^T)
+//   ||F||^2 = ||M||^2 - 2 <X, M Y^T> + <X^T X, Y Y^T>
+// and, for A = F, B = dX Y + X dY, C = dX dY with the k x k Grams
+//   A1 = dX^T dX, A2 = dX^T X, XX = X^T X, B1 = dY dY^T, B2 = Y dY^T, YY = Y Y^T:
+//   AB = <dX, graX> + <dY, graY>            AC = tr(A2 B2) - <dX, M dY^T>
+//   BB = tr(A1 YY) + tr(XX B1) + 2 tr(A2 B2^T)
+//   BC = tr(A1 B2^T) + tr(A2^T B1)           CC = tr(A1 B1)
+// so an IPM iteration streams M three times (M Y^T, X^T M, M dY^T) and needs
+// no n x m workspace (64 GB at config c5).
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void k_ffree_grad_rows(const double* __restrict__ V, const double* __restrict__ G,
+                                  const double* __restrict__ MV, long rows,
+                                  double* __restrict__ grad, double* __restrict__ part) {
+  // grad[r] = V[r] G - MV[r]; part[block] = sum_r <V[r], MV[r]>
+  __shared__ double g[K * K];
+  __shared__ double sh[32];
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) g[e] = G[e];
+  __syncthreads();
+  double dot = 0.0;
+  for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (long)gridDim.x * blockDim.x) {
+    double v[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p) v[p] = V[r * K + p];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p < K; ++p) s = fma(v[p], g[p * K + q], s);
+      const double mv = MV[r * K + q];
+      grad[r * K + q] = s - mv;
+      dot = fma(v[q], mv, dot);
+    }
+  }
+  dot = block_sum(dot, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = dot;
+}
+
+// sc[0] = ||M||^2 - 2 xm + <XX, YY>  (fsq)
+__global__ void k_ffree_fsq(const double* __restrict__ part, int nb, double mnorm2,
+                            const double* __restrict__ XX, const double* __restrict__ YY, int k,
+                            double* __restrict__ sc, double* __restrict__ xm_out) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v += part[b];
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    if (XX && YY)  // the replicated <X^T X, Y Y^T> term (rank 0 only when row-sharded)
+      for (int e = 0; e < k * k; ++e) t = fma(XX[e], YY[e], t);
+    if (xm_out) *xm_out = v;
+    sc[0] = mnorm2 - 2.0 * v + t;
+  }
+}
+
+// quartic coefficients from Grams and dot products -> sc[10..15]
+// dots: [0] <dX, graX>, [1] <dY, graY>, [2] <dX, M dY^T>  (traces of k x k products)
+__global__ void k_ffree_quartic(const double* __restrict__ A1, const double* __restrict__ A2,
+                                const double* __restrict__ XX, const double* __restrict__ B1,
+                                const double* __restrict__ B2, const double* __restrict__ YY,
+                                const double* __restrict__ Dgx, const double* __restrict__ Dgy,
+                                const double* __restrict__ Dmd, int k, double* __restrict__ sc) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  auto tr = [k](const double* P, const double* Q, bool qt) {  // tr(P Q) or tr(P Q^T)
+    double s = 0.0;
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) s = fma(P[a * k + b], qt ? Q[a * k + b] : Q[b * k + a], s);
+    return s;
+  };
+  auto diag = [k](const double* P) {
+    double s = 0.0;
+    for (int a = 0; a < k; ++a) s += P[a * k + a];
+    return s;
+  };
+  const double ab = diag(Dgx) + diag(Dgy);
+  const double ac = tr(A2, B2, false) - diag(Dmd);
+  const double bb = tr(A1, YY, false) + tr(XX, B1, false) + 2.0 * tr(A2, B2, true);
+  const double bc = tr(A1, B2, true) + tr(A2, B1, true);
+  const double cc = tr(A1, B1, false);
+  sc[10] = sc[0];
+  sc[11] = ab;
+  sc[12] = bb;
+  sc[13] = ac;
+  sc[14] = bc;
+  sc[15] = cc;
+}
+
+extern "C" int nmfb_ffree_grad_rows(const double* V, const double* G, const double* MV, long rows,
+                                    long k, double* grad, double* part, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+#define CASE(KK)                                                                             \
+  case KK:                                                                                   \
+    ++g_nmfb_launches, k_ffree_grad_rows<KK><<<RED_BLOCKS, 256, 0, st>>>(V, G, MV, rows, grad, part); \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_ffree_fsq(const double* part, double mnorm2, const double* XX,
+                              const double* YY, long k, double* sc, double* xm_out, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  ++g_nmfb_launches, k_ffree_fsq<<<1, 256, 0, st>>>(part, RED_BLOCKS, mnorm2, XX, YY, (int)k, sc, xm_out);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_ffree_quartic(const double* A1, const double* A2, const double* XX,
+                                  const double* B1, const double* B2, const double* YY,
+                                  const double* Dgx, const double* Dgy, const double* Dmd, long k,
+                                  double* sc, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  ++g_nmfb_launches, k_ffree_quartic<<<1, 32, 0, st>>>(A1, A2, XX, B1, B2, YY, Dgx, Dgy, Dmd, (int)k, sc);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}

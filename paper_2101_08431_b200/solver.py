@@ -97,6 +97,7 @@ class Problem:
         self._call("nmfb_sqnorms", _p(self.M), self.f32, n, m, _p(self.row_n2), _p(self.col_n2),
                    _p(self.cwork), self.cwork.numel(), self.stream)
         self.comm.sum_(self.col_n2)
+        self.mnorm2_local = float(self.row_n2.sum().item())  # ||M_rank||^2 (F-free objective)
         self.dscal = torch.zeros(256, **f64)
         self.iscal = torch.zeros(16, dtype=torch.int32, device=self.dev)
         self.hscal = torch.zeros(256, dtype=torch.float64).pin_memory()
@@ -179,6 +180,35 @@ class Problem:
                    _p(self.dscal[out_index:]), _p(self.rwork), self.stream)
         self.comm.sum_(self.dscal[out_index:out_index + 1])
         self.colprod(F, n, m, X, k, gY, reduce=True, tag="graY")
+
+    @property
+    def free_residual_default(self):
+        """Use the residual-free formulation when an n x m fp64 residual is large."""
+        return self.n * self.m >= (1 << 25)
+
+    def gradients_free(self, X, Yt, gX, gY, ws, out_index=0):
+        """graX, graY and ||F||^2 without forming F (csrc/ipm.cu "F-free"):
+        three small Grams plus M Y^T and X^T M (two streaming passes over M)."""
+        n, m, k, s = self.n, self.m, self.k, self.stream
+        self.colprod(Yt, m, k, Yt, k, ws["GY"])
+        self.colprod(X, n, k, X, k, ws["XX"], reduce=True)
+        self.rowprod(self.M, n, m, Yt, k, ws["MY"], None, self.f32)
+        self.colprod(self.M, n, m, X, k, ws["MX"], None, self.f32, reduce=True)
+        self._call("nmfb_ffree_grad_rows", _p(X), _p(ws["GY"]), _p(ws["MY"]), n, k, _p(gX),
+                   _p(ws["part"]), s)
+        self._call("nmfb_ffree_fsq", _p(ws["part"]), self.mnorm2_local,
+                   _p(ws["XX"]) if self.comm.root else None, _p(ws["GY"]), k,
+                   _p(self.dscal[out_index:]), None, s)
+        self.comm.sum_(self.dscal[out_index:out_index + 1])
+        self._call("nmfb_ffree_grad_rows", _p(Yt), _p(ws["XX"]), _p(ws["MX"]), m, k, _p(gY),
+                   _p(ws["part2"]), s)
+
+    def free_workspace(self):
+        n, m, k = self.n, self.m, self.k
+        nb = self.lib.nmfb_ipm_reduce_blocks()
+        ws = {"GY": self.buf(k, k), "XX": self.buf(k, k), "MY": self.buf(n, k),
+              "MX": self.buf(m, k), "part": self.buf(nb), "part2": self.buf(nb)}
+        return ws
 
     def kkt_sums(self, X, R, gX, Yt, S, gY, mux, muy, at=16):
         self._call("nmfb_kkt_sums", _p(X), _p(R), _p(gX), X.numel(), _p(Yt), _p(S), _p(gY),
@@ -285,7 +315,13 @@ class IpmEngine:
         self.wx, self.wy = barrier_weights(P.n_global, m, p.barrier)
         self.comm = P.comm
         b = P.buf
-        self.F = [b(n, m), b(n, m)]
+        self.ffree = (p.residual == "free") or (p.residual == "auto" and P.free_residual_default)
+        self.F = [None, None] if self.ffree else [b(n, m), b(n, m)]
+        if self.ffree:
+            self.fws = P.free_workspace()
+            self.MdY = b(n, k)
+            self.A1, self.A2, self.B1, self.B2 = b(k, k), b(k, k), b(k, k), b(k, k)
+            self.Dgx, self.Dgy, self.Dmd = b(k, k), b(k, k), b(k, k)
         self.fi = 0  # index of F at the current point
         self.gX, self.gY = b(n, k), b(m, k)
         self.L, self.h, self.g = b(n, k, k), b(n, k), b(n, k)
@@ -315,14 +351,15 @@ class IpmEngine:
         self.use_graphs = p.use_graphs and not P.comm.active and not self.dense_gn
         # fused small-problem iteration (csrc/small.cu) for c1-c3-sized problems
         self.small = bool(P.lib.nmfb_small_supported(n, m, k)) and not P.comm.active \
-            and not self.dense_gn and p.fused_small
+            and not self.dense_gn and p.fused_small and not self.ffree
         if self.small:
             self.swork = b(max(P.lib.nmfb_small_work_len(n, m, k), 1))
             self.tickets = torch.zeros(8, dtype=torch.int32, device=P.dev)
         self.Pbuf = None
         self.W = None
         aw = max(P.lib.nmfb_atb_work_len(n, self.kk, self.kk),
-                 P.lib.nmfb_atb_work_len(n, m, k ** 3), 1)
+                 P.lib.nmfb_atb_work_len(m, self.kk, self.kk),
+                 0 if self.ffree else P.lib.nmfb_atb_work_len(n, m, k ** 3), 1)
         self.awork = b(aw)
 
     # -- helpers -------------------------------------------------------------
@@ -333,6 +370,11 @@ class IpmEngine:
     def refresh_launch(self):
         """Launch gradients + KKT sums at the current point (no host sync)."""
         P = self.P
+        if self.ffree:
+            P.gradients_free(self.X, self.Yt, self.gX, self.gY, self.fws, out_index=0)
+            P.kkt_sums(self.X, self.R, self.gX, self.Yt, self.S, self.gY, self.wx * self.mu,
+                       self.wy * self.mu, at=16)
+            return
         if self.have_fact and self.fact_F == self.fi:
             self.fi ^= 1  # keep the factorization's residual for the predictor
         P.gradients(self.X, self.Yt, self.Fcur, self.gX, self.gY, out_index=0)
@@ -506,12 +548,38 @@ class IpmEngine:
         """Quartic coefficients + all backtracking barrier sums in two launches."""
         P, s = self.P, self.P.stream
         n, m, k = self.n, self.m, self.k
+        if self.ffree:
+            self._armijo_free(dY)
+            return
         P._call("nmfb_quartic", _p(self.Fcur), n, m, k, _p(self.X), _p(self.dX), _p(self.Yt),
                 _p(dY), _p(P.dscal[10:]), _p(P.rwork), s)
         P._call("nmfb_barrier_trials", _p(self.X), _p(self.dX), n * k, _p(self.Yt), _p(dY), m * k,
                 _p(P.dscal[5:]), NTRIALS, _p(P.dscal[32:]), _p(P.rwork), P.rwork.numel(), s)
         if self.comm.active:
             self.comm.sum_(P.dscal[10:16])
+            bx = P.dscal[32:32 + 2 * NTRIALS].view(NTRIALS, 2)[:, 0].contiguous()
+            self.comm.sum_(bx)
+            P.dscal[32:32 + 2 * NTRIALS].view(NTRIALS, 2)[:, 0].copy_(bx)
+
+    def _armijo_free(self, dY):
+        """Quartic coefficients from k x k Grams + one streaming pass M dY^T."""
+        P, s = self.P, self.P.stream
+        n, m, k = self.n, self.m, self.k
+        X, Yt, dX = self.X, self.Yt, self.dX
+        P.rowprod(P.M, n, m, dY, k, self.MdY, None, P.f32)
+        P.colprod(dX, n, k, dX, k, self.A1, reduce=True)
+        P.colprod(dX, n, k, X, k, self.A2, reduce=True)
+        P.colprod(dY, m, k, dY, k, self.B1)
+        P.colprod(Yt, m, k, dY, k, self.B2)
+        P.colprod(dX, n, k, self.gX, k, self.Dgx, reduce=True)
+        P.colprod(dY, m, k, self.gY, k, self.Dgy)
+        P.colprod(dX, n, k, self.MdY, k, self.Dmd, reduce=True)
+        P._call("nmfb_ffree_quartic", _p(self.A1), _p(self.A2), _p(self.XtX), _p(self.B1),
+                _p(self.B2), _p(self.GY), _p(self.Dgx), _p(self.Dgy), _p(self.Dmd), k,
+                _p(P.dscal), s)
+        P._call("nmfb_barrier_trials", _p(X), _p(dX), n * k, _p(Yt), _p(dY), m * k,
+                _p(P.dscal[5:]), NTRIALS, _p(P.dscal[32:]), _p(P.rwork), P.rwork.numel(), s)
+        if self.comm.active:
             bx = P.dscal[32:32 + 2 * NTRIALS].view(NTRIALS, 2)[:, 0].contiguous()
             self.comm.sum_(bx)
             P.dscal[32:32 + 2 * NTRIALS].view(NTRIALS, 2)[:, 0].copy_(bx)
@@ -674,7 +742,9 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
             eng.remember_factorization(False)
         sigma = eng.predictor_sigma(sums)
         eng.mu = sigma * eng.mu
-        eng.flag = sigma <= p.sigma_c
+        # the full-Hessian coupling needs the dense mk x mk system and the residual F;
+        # in residual-free mode (very large M) the Gauss-Newton coupling is kept
+        eng.flag = sigma <= p.sigma_c and not eng.ffree
         e_mu, e_zero, fsq, sums = eng.refresh()
     res.converged = e_zero <= tol
     res.mu, res.flag = eng.mu, eng.flag
@@ -687,9 +757,15 @@ def transition(P: Problem, X, Yt, eps_tol, tp: TransitionParams | None = None):
     tp = tp or TransitionParams()
     n, m, k, s = P.n, P.m, P.k, P.stream
     X, Yt = X.clone(), Yt.clone()
-    F, gX, gY = P.buf(n, m), P.buf(n, k), P.buf(m, k)
+    gX, gY = P.buf(n, k), P.buf(m, k)
+    if P.free_residual_default:
+        ws = P.free_workspace()
+        grad = lambda: P.gradients_free(X, Yt, gX, gY, ws)  # noqa: E731
+    else:
+        F = P.buf(n, m)
+        grad = lambda: P.gradients(X, Yt, F, gX, gY)  # noqa: E731
     # max over the concatenated (x, y)
-    P.gradients(X, Yt, F, gX, gY)
+    grad()
     P.kkt_sums(X, None, gX, Yt, None, gY, 0.0, 0.0, at=16)
     v, _ = P.readback(28)
     big = max(v[26], v[27])
@@ -698,7 +774,7 @@ def transition(P: Problem, X, Yt, eps_tol, tp: TransitionParams | None = None):
     rho0 = tp.rho0_scale * big
     P._call("nmfb_clamp_min", _p(X), n * k, rho0, s)
     P._call("nmfb_clamp_min", _p(Yt), m * k, rho0, s)
-    P.gradients(X, Yt, F, gX, gY)
+    grad()
     P.kkt_sums(X, None, gX, Yt, None, gY, 0.0, 0.0, at=16)
     v, _ = P.readback(28)
     R, S = P.buf(n, k), P.buf(m, k)
@@ -713,8 +789,11 @@ def transition(P: Problem, X, Yt, eps_tol, tp: TransitionParams | None = None):
 def kkt_error_primal_only_dev(P: Problem, X, Yt):
     """SPEC.md:420 on the device."""
     n, m, k = P.n, P.m, P.k
-    F, gX, gY = P.buf(n, m), P.buf(n, k), P.buf(m, k)
-    P.gradients(X, Yt, F, gX, gY)
+    gX, gY = P.buf(n, k), P.buf(m, k)
+    if P.free_residual_default:
+        P.gradients_free(X, Yt, gX, gY, P.free_workspace())
+    else:
+        P.gradients(X, Yt, P.buf(n, m), gX, gY)
     P.kkt_sums(X, None, gX, Yt, None, gY, 0.0, 0.0, at=16)
     v, _ = P.readback(28)
     return kkt_from_sums(v[16:28])[1], 0.5 * v[0]

@@ -67,11 +67,12 @@ def test_stage1_fp32_storage(mods):
     assert rel(X.cpu().numpy(), ro.X) < 1e-4 and rel(Yt.cpu().numpy(), ro.Yt) < 1e-4
 
 
-@pytest.mark.parametrize("name,barrier,iters,eps,solve", [
-    ("c1", "paper", 40, 1e-7, "lowrank"), ("c1", "balanced", 60, 1e-7, "lowrank"),
-    ("c1", "balanced", 50, 1e-5, "lowrank"),  # switches to the full Hessian at it 28, 29, 47
-    ("c1", "balanced", 50, 1e-5, "dense"), ("c2", "balanced", 35, 1e-6, "lowrank")])
-def test_ipm_parity(mods, name, barrier, iters, eps, solve):
+@pytest.mark.parametrize("name,barrier,iters,eps,solve,resid", [
+    ("c1", "paper", 40, 1e-7, "lowrank", "auto"), ("c1", "balanced", 60, 1e-7, "lowrank", "auto"),
+    ("c1", "balanced", 50, 1e-5, "lowrank", "auto"),  # full Hessian at it 28, 29, 47
+    ("c1", "balanced", 50, 1e-5, "dense", "auto"), ("c2", "balanced", 35, 1e-6, "lowrank", "auto"),
+    ("c1", "paper", 40, 1e-7, "lowrank", "free"), ("c2", "paper", 30, 1e-6, "lowrank", "free")])
+def test_ipm_parity(mods, name, barrier, iters, eps, solve, resid):
     data, solver, IpmParams, Stage1Config = mods
     M, X0, Y0 = _instance(data, name)
     k = X0.shape[1]
@@ -81,7 +82,8 @@ def test_ipm_parity(mods, name, barrier, iters, eps, solve):
     X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), eps)
     assert abs(mu - st.mu) <= 1e-12 * st.mu
     eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho,
-                            IpmParams(fixed_iters=iters, barrier=barrier, schur_solver=solve))
+                            IpmParams(fixed_iters=iters, barrier=barrier, schur_solver=solve,
+                                      residual=resid))
     D.set_schur_backend("numpy")
     try:
         ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=iters, barrier=barrier))
@@ -117,7 +119,7 @@ def test_dense_k10_ipm_small(mods):
     st = D.transition(ro.X, ro.Yt, M, 1e-7)
     P = solver.Problem(M, 10)
     X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), 1e-7)
-    eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(fixed_iters=8))
+    eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(fixed_iters=8, residual="free"))
     D.set_schur_backend("numpy")
     try:
         ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=8))
