@@ -545,21 +545,47 @@ __global__ void __launch_bounds__(256, 2) k_colprod_mma(const T* __restrict__ A,
 // out[e] = scale * sum_{s < nparts} part[s][e]  (fixed order); optional per-row
 // (of width K) tolerance as in k_rowprod.
 template <int K>
-__global__ void k_sum_partials(const double* __restrict__ part, int nparts, long len,
-                               double* __restrict__ out, double* __restrict__ tol,
-                               double scale) {
-  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row * K >= len) return;
-  double amax = 0.0;
-#pragma unroll
-  for (int p = 0; p < K; ++p) {
+__global__ void __launch_bounds__(256) k_sum_partials(const double* __restrict__ part, int nparts,
+                                                      long len, double* __restrict__ out,
+                                                      double* __restrict__ tol, double scale) {
+  // element-parallel (coalesced) fixed-order sum; a CTA covers RB whole rows so
+  // the per-row tolerance is finished from shared memory
+  constexpr int RB = 256 / K;
+  __shared__ double sv[RB * K];
+  const long row0 = (long)blockIdx.x * RB;
+  const long e0 = row0 * K;
+  const int t = threadIdx.x;
+  const long e = e0 + t;
+  if (t < RB * K && e < len) {
     double v = 0.0;
-    for (int s = 0; s < nparts; ++s) v += part[(long)s * len + row * K + p];
+    int s = 0;
+    for (; s + 8 <= nparts; s += 8) {
+      double w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w[u] = part[(long)(s + u) * len + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v += w[u];
+    }
+    for (; s < nparts; ++s) v += part[(long)s * len + e];
     v *= scale;
-    out[row * K + p] = v;
-    amax = fmax(amax, fabs(v));
+    out[e] = v;
+    sv[t] = v;
   }
-  if (tol) tol[row] = 1e-12 * fmax(1.0, amax);
+  if (!tol) return;
+  __syncthreads();
+  const long r = row0 + t;
+  if (t < RB && r * K < len) {
+    double amax = 0.0;
+#pragma unroll
+    for (int p = 0; p < K; ++p) amax = fmax(amax, fabs(sv[t * K + p]));
+    tol[r] = 1e-12 * fmax(1.0, amax);
+  }
+}
+
+// grid for k_sum_partials over `rows` rows of width K
+template <int K>
+inline unsigned sum_grid(long rows) {
+  return (unsigned)((rows + (256 / K) - 1) / (256 / K));
 }
 
 // ---------------------------------------------------------------------------
@@ -671,7 +697,7 @@ int launch_rowprod(const T* A, long rows, long cols, const double* B, double* ou
     cudaFuncSetAttribute(k_rowprod_mma<NT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((unsigned)nch, (unsigned)nsplit);
     ++g_nmfb_launches, k_rowprod_mma<NT, T><<<grid, 256, smem, st>>>(A, rows, cols, B, K, rps, work);
-    ++g_nmfb_launches, k_sum_partials<K><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
+    ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(
         work, (int)nch, rows * K, out, tol, scale);
     NMFB_CHECK_LAUNCH();
     return NMFB_OK;
@@ -690,7 +716,7 @@ int launch_rowprod(const T* A, long rows, long cols, const double* B, double* ou
                          (int)smem);
     dim3 grid((unsigned)nch, (unsigned)nsplit);
     ++g_nmfb_launches, k_rowprod_split<K, RW, T><<<grid, 256, smem, st>>>(A, rows, cols, B, rps, work);
-    ++g_nmfb_launches, k_sum_partials<K><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
+    ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(
         work, (int)nch, rows * K, out, tol, scale);
     NMFB_CHECK_LAUNCH();
     return NMFB_OK;
@@ -737,7 +763,7 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
     dim3 grid((unsigned)((cols + CP_COLS - 1) / CP_COLS), (unsigned)ns);
     ++g_nmfb_launches, k_colprod_partial<K, T><<<grid, 256, 0, st>>>(A, rows, cols, B, stripe, work);
   }
-  ++g_nmfb_launches, k_sum_partials<K><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(work, (int)ns, cols * K, out,
+  ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(cols), 256, 0, st>>>(work, (int)ns, cols * K, out,
                                                                    tol, scale);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
@@ -813,7 +839,7 @@ extern "C" int nmfb_sqnorms(const void* A, int a_is_f32, long rows, long cols, d
     ++g_nmfb_launches, k_row_sqnorm<double><<<blocks, 256, 0, st>>>((const double*)A, rows, cols, row_out);
     ++g_nmfb_launches, k_col_sqnorm_partial<double><<<grid, 128, 0, st>>>((const double*)A, rows, cols, stripe, work);
   }
-  ++g_nmfb_launches, k_sum_partials<1><<<(unsigned)((cols + 127) / 128), 128, 0, st>>>(work, (int)ns, cols, col_out,
+  ++g_nmfb_launches, k_sum_partials<1><<<sum_grid<1>(cols), 256, 0, st>>>(work, (int)ns, cols, col_out,
                                                                    nullptr, 1.0);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;

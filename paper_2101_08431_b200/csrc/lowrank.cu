@@ -170,25 +170,23 @@ __global__ void k_d_correct(const double* __restrict__ LD, const double* __restr
   for (int a = 0; a < K; ++a) t[j * K + a] += v[a];
 }
 
-// in-place lower Cholesky of a Q x Q row-major matrix by one CTA; returns pivot
-// failure column or -1 (valid in every thread)
+// in-place lower Cholesky of a Q x Q row-major matrix (smem or global) by one
+// CTA, two barriers per column; returns the failing pivot column or -1 (all threads)
 __device__ int cta_cholesky(double* A, int Q, int* sfail) {
   const int tid = threadIdx.x, nt = blockDim.x;
   if (tid == 0) *sfail = -1;
   __syncthreads();
   for (int j = 0; j < Q; ++j) {
-    if (tid == 0) {
-      const double d = A[j * Q + j];
-      if (!(d > 0.0))
-        *sfail = j;
-      else
-        A[j * Q + j] = sqrt(d);
+    const double pv = A[j * Q + j];
+    if (!(pv > 0.0)) {
+      if (tid == 0) *sfail = j;
+      break;  // uniform: every thread read the same pivot
     }
+    const double rd = 1.0 / sqrt(pv);
+    // column j below the diagonal, then the trailing lower triangle
+    for (int r = j + 1 + tid; r < Q; r += nt) A[r * Q + j] *= rd;
     __syncthreads();
-    if (*sfail >= 0) break;
-    const double djj = A[j * Q + j];
-    for (int r = j + 1 + tid; r < Q; r += nt) A[r * Q + j] /= djj;
-    __syncthreads();
+    if (tid == 0) A[j * Q + j] = pv * rd;
     const int rem = Q - j - 1;
     for (int e = tid; e < rem * rem; e += nt) {
       const int r = j + 1 + e / rem, c = j + 1 + e % rem;
@@ -196,113 +194,162 @@ __device__ int cta_cholesky(double* A, int Q, int* sfail) {
     }
     __syncthreads();
   }
+  __syncthreads();
   const int f = *sfail;
   __syncthreads();
   return f;
 }
 
-// one CTA: LG = chol(G), H = I - LG^T Zb LG, LH = chol(H).  work: 3 Q^2 doubles.
+// one CTA: LG = chol(G), H = I - LG^T Zb LG, LH = chol(H).  work: 2 Q^2 doubles
+// (Zb kept in work[0, Q^2) for the solves).  Small Q works in shared memory.
 __global__ void __launch_bounds__(1024) k_lowrank_factor(const double* __restrict__ Zpk,
                                                          const double* __restrict__ Gpk, int k,
                                                          double* __restrict__ LG,
                                                          double* __restrict__ LH,
                                                          double* __restrict__ Zb,
-                                                         double* __restrict__ T1,
-                                                         int* __restrict__ info) {
+                                                         double* __restrict__ T1g,
+                                                         int* __restrict__ info, int use_smem) {
+  extern __shared__ double smf[];
   __shared__ int sfail;
   const int Q = k * k, KK = k * (k + 1) / 2;
   const int tid = threadIdx.x, nt = blockDim.x;
+  double* A = use_smem ? smf : LG;            // G -> L_G, later H -> L_H
+  double* T1 = use_smem ? smf + Q * Q : T1g;  // Zb L_G
   for (int e = tid; e < Q * Q; e += nt) {
     const int r = e / Q, c = e % Q;
     const int a = r / k, p = r % k, b = c / k, q = c % k;
     const int ab = pkx(a, b, k), pq = pkx(p, q, k);
     Zb[e] = Zpk[ab * KK + pq];
-    LG[e] = (c <= r) ? Gpk[ab * KK + pq] : 0.0;
+    A[e] = (c <= r) ? Gpk[ab * KK + pq] : 0.0;
   }
   __syncthreads();
-  int f = cta_cholesky(LG, Q, &sfail);
+  int f = cta_cholesky(A, Q, &sfail);
   if (f >= 0) {
     if (tid == 0) *info = 1000000 + f;  // G singular: Y^T rank deficient
     return;
   }
-  for (int e = tid; e < Q * Q; e += nt) {  // zero the strict upper part left by the factor
+  for (int e = tid; e < Q * Q; e += nt) {  // publish L_G (strict upper zero)
     const int r = e / Q, c = e % Q;
-    if (c > r) LG[e] = 0.0;
+    const double v = (c <= r) ? A[e] : 0.0;
+    A[e] = v;
+    if (use_smem) LG[e] = v;
   }
   __syncthreads();
-  // T1 = Zb LG
+  // T1 = Zb L_G
   for (int e = tid; e < Q * Q; e += nt) {
     const int r = e / Q, c = e % Q;
-    double s = 0.0;
-    for (int t = c; t < Q; ++t) s = fma(Zb[r * Q + t], LG[t * Q + c], s);
-    T1[e] = s;
+    double acc = 0.0;
+    for (int t = c; t < Q; ++t) acc = fma(Zb[r * Q + t], A[t * Q + c], acc);
+    T1[e] = acc;
   }
   __syncthreads();
-  // H = I - LG^T T1 (lower part)
+  // H = I - L_G^T T1 (lower part) -> LH (global), then back into A for the factorisation
   for (int e = tid; e < Q * Q; e += nt) {
     const int r = e / Q, c = e % Q;
-    if (c > r) {
-      LH[e] = 0.0;
-      continue;
+    double v = 0.0;
+    if (c <= r) {
+      double acc = 0.0;
+      for (int t = r; t < Q; ++t) acc = fma(A[t * Q + r], T1[t * Q + c], acc);
+      v = (r == c ? 1.0 : 0.0) - acc;
     }
-    double s = 0.0;
-    for (int t = r; t < Q; ++t) s = fma(LG[t * Q + r], T1[t * Q + c], s);
-    LH[e] = (r == c ? 1.0 : 0.0) - s;
+    LH[e] = v;
   }
   __syncthreads();
-  f = cta_cholesky(LH, Q, &sfail);
+  double* B = use_smem ? smf : LH;
+  if (use_smem)
+    for (int e = tid; e < Q * Q; e += nt) B[e] = LH[e];
+  __syncthreads();
+  f = cta_cholesky(B, Q, &sfail);
+  if (use_smem)
+    for (int e = tid; e < Q * Q; e += nt) LH[e] = B[e];
   if (tid == 0) *info = f;  // -1: reduced system positive definite
 }
 
-// one CTA: w = LG^{-T} LH^{-T} LH^{-1} LG^T Zb u   (u, w: Q vectors; scratch 2Q)
-__global__ void __launch_bounds__(256) k_lowrank_apply(const double* __restrict__ LG,
-                                                       const double* __restrict__ LH,
+// blocked in-CTA triangular solve with a row-major lower factor L (Q x Q):
+// trans = 0: L z = b, trans = 1: L^T z = b; z overwrites b (shared memory).
+__device__ void cta_trsv(const double* L, int Q, double* b, int trans) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int nblk = (Q + 31) / 32;
+  for (int bb = 0; bb < nblk; ++bb) {
+    const int blk = trans ? (nblk - 1 - bb) : bb;
+    const int c0 = blk * 32, nc = min(32, Q - c0);
+    if (wid == 0) {
+      double v = lane < nc ? b[c0 + lane] : 0.0;
+      if (!trans) {
+        for (int j = 0; j < nc; ++j) {
+          const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * Q + c0 + j];
+          if (lane == j) v = zj;
+          if (lane > j && lane < nc) v -= L[(c0 + lane) * Q + c0 + j] * zj;
+        }
+      } else {
+        for (int j = nc - 1; j >= 0; --j) {
+          const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * Q + c0 + j];
+          if (lane == j) v = zj;
+          if (lane < j) v -= L[(c0 + j) * Q + c0 + lane] * zj;
+        }
+      }
+      if (lane < nc) b[c0 + lane] = v;
+    }
+    __syncthreads();
+    if (!trans) {
+      for (int r = c0 + nc + wid; r < Q; r += nw) {
+        double acc = lane < nc ? L[r * Q + c0 + lane] * b[c0 + lane] : 0.0;
+        acc = warp_sum(acc);
+        if (lane == 0) b[r] -= acc;
+      }
+    } else {
+      for (int c = tid; c < c0; c += blockDim.x) {
+        double acc = 0.0;
+        for (int r = 0; r < nc; ++r) acc = fma(L[(c0 + r) * Q + c], b[c0 + r], acc);
+        b[c] -= acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// one CTA: w = LG^{-T} LH^{-T} LH^{-1} LG^T Zb u   (u, w: Q vectors).  With
+// use_smem the two factors are staged in shared memory first (latency-bound
+// substitution steps then hit smem instead of L2).
+__global__ void __launch_bounds__(256) k_lowrank_apply(const double* __restrict__ LGg,
+                                                       const double* __restrict__ LHg,
                                                        const double* __restrict__ Zb, int k,
                                                        const double* __restrict__ u,
-                                                       double* __restrict__ w) {
+                                                       double* __restrict__ w, int use_smem) {
   extern __shared__ double sm[];
   const int Q = k * k;
   double* a = sm;
   double* b = sm + Q;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int r = tid; r < Q; r += nt) {  // a = Zb u
-    double s = 0.0;
-    for (int c = 0; c < Q; ++c) s = fma(Zb[r * Q + c], u[c], s);
-    a[r] = s;
+  const double* LG = LGg;
+  const double* LH = LHg;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  if (use_smem) {
+    double* sg = sm + 2 * Q;
+    double* shh = sg + Q * Q;
+    for (int e = tid; e < Q * Q; e += blockDim.x) {
+      sg[e] = LGg[e];
+      shh[e] = LHg[e];
+    }
+    LG = sg;
+    LH = shh;
+  }
+  for (int r = wid; r < Q; r += nw) {  // a = Zb u (warp per row, coalesced)
+    double acc = 0.0;
+    for (int c = lane; c < Q; c += 32) acc = fma(Zb[r * Q + c], u[c], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) a[r] = acc;
   }
   __syncthreads();
-  for (int r = tid; r < Q; r += nt) {  // b = LG^T a
-    double s = 0.0;
-    for (int t = r; t < Q; ++t) s = fma(LG[t * Q + r], a[t], s);
-    b[r] = s;
+  for (int r = tid; r < Q; r += blockDim.x) {  // b = LG^T a
+    double acc = 0.0;
+    for (int t = r; t < Q; ++t) acc = fma(LG[t * Q + r], a[t], acc);
+    b[r] = acc;
   }
   __syncthreads();
-  // a = LH^{-1} b (forward), then b = LH^{-T} a (backward), then a = LG^{-T} b
-  if (tid < 32) {
-    for (int i = 0; i < Q; ++i) {
-      double s = 0.0;
-      for (int p = tid; p < i; p += 32) s = fma(LH[i * Q + p], a[p], s);
-      s = warp_sum(s);
-      if (tid == 0) a[i] = (b[i] - s) / LH[i * Q + i];
-      __syncwarp();
-    }
-    for (int i = Q - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int p = i + 1 + tid; p < Q; p += 32) s = fma(LH[p * Q + i], b[p], s);
-      s = warp_sum(s);
-      if (tid == 0) b[i] = (a[i] - s) / LH[i * Q + i];
-      __syncwarp();
-    }
-    for (int i = Q - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int p = i + 1 + tid; p < Q; p += 32) s = fma(LG[p * Q + i], a[p], s);
-      s = warp_sum(s);
-      if (tid == 0) a[i] = (b[i] - s) / LG[i * Q + i];
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  for (int r = tid; r < Q; r += nt) w[r] = a[r];
+  cta_trsv(LH, Q, b, 0);
+  cta_trsv(LH, Q, b, 1);
+  cta_trsv(LG, Q, b, 1);
+  for (int r = tid; r < Q; r += blockDim.x) w[r] = b[r];
 }
 
 }  // namespace
@@ -336,8 +383,12 @@ extern "C" int nmfb_lowrank_factor(const double* Zpk, const double* Gpk, long k,
                                    double* LH, double* work, int* info, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const long Q = k * k;
-  ++g_nmfb_launches, k_lowrank_factor<<<1, 1024, 0, st>>>(Zpk, Gpk, (int)k, LG, LH, work,
-                                                          work + Q * Q, info);
+  const size_t smem = (size_t)2 * Q * Q * sizeof(double);
+  const int use_smem = smem <= 200 * 1024;
+  if (use_smem)
+    cudaFuncSetAttribute(k_lowrank_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ++g_nmfb_launches, k_lowrank_factor<<<1, 1024, use_smem ? smem : 0, st>>>(
+      Zpk, Gpk, (int)k, LG, LH, work, work + Q * Q, info, use_smem);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -359,7 +410,12 @@ extern "C" int nmfb_lowrank_solve(const double* LD, const double* Yt, const doub
   int rc = nmfb_colprod(Yt, 0, m, k, dy, k, u, nullptr, 1.0, cwork, cwork_len, stream);
   if (rc != NMFB_OK) return rc;
   const long Q = k * k;
-  ++g_nmfb_launches, k_lowrank_apply<<<1, 256, 2 * Q * sizeof(double), st>>>(LG, LH, Zb, (int)k, u, w);
+  const size_t sm_full = (size_t)(2 * Q + 2 * Q * Q) * sizeof(double);
+  const int apply_smem = sm_full <= 200 * 1024;
+  const size_t sm_apply = apply_smem ? sm_full : 2 * Q * sizeof(double);
+  if (apply_smem)
+    cudaFuncSetAttribute(k_lowrank_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply);
+  ++g_nmfb_launches, k_lowrank_apply<<<1, 256, sm_apply, st>>>(LG, LH, Zb, (int)k, u, w, apply_smem);
 #define CASE(KK)                                                                           \
   case KK:                                                                                 \
     ++g_nmfb_launches, k_d_correct<KK><<<blocks, 128, 0, st>>>(LD, Yt, w, m, dy);          \
