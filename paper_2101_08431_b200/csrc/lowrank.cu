@@ -171,9 +171,12 @@ __global__ void k_d_correct(const double* __restrict__ LD, const double* __restr
 }
 
 // in-place lower Cholesky of a Q x Q row-major matrix (smem or global) by one
-// CTA, two barriers per column; returns the failing pivot column or -1 (all threads)
+// CTA, two barriers per column; warps own rows of the trailing update and lanes
+// its columns (no integer division, contiguous accesses).  Returns the failing
+// pivot column or -1 (in every thread).
 __device__ int cta_cholesky(double* A, int Q, int* sfail) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int nw = nt >> 5;
   if (tid == 0) *sfail = -1;
   __syncthreads();
   for (int j = 0; j < Q; ++j) {
@@ -183,14 +186,12 @@ __device__ int cta_cholesky(double* A, int Q, int* sfail) {
       break;  // uniform: every thread read the same pivot
     }
     const double rd = 1.0 / sqrt(pv);
-    // column j below the diagonal, then the trailing lower triangle
     for (int r = j + 1 + tid; r < Q; r += nt) A[r * Q + j] *= rd;
     __syncthreads();
     if (tid == 0) A[j * Q + j] = pv * rd;
-    const int rem = Q - j - 1;
-    for (int e = tid; e < rem * rem; e += nt) {
-      const int r = j + 1 + e / rem, c = j + 1 + e % rem;
-      if (c <= r) A[r * Q + c] -= A[r * Q + j] * A[c * Q + j];
+    for (int r = j + 1 + wid; r < Q; r += nw) {
+      const double lrj = A[r * Q + j];
+      for (int c = j + 1 + lane; c <= r; c += 32) A[r * Q + c] -= lrj * A[c * Q + j];
     }
     __syncthreads();
   }
@@ -198,6 +199,60 @@ __device__ int cta_cholesky(double* A, int Q, int* sfail) {
   const int f = *sfail;
   __syncthreads();
   return f;
+}
+
+// C[r][c] (Q x Q) += sum over the lower-triangular factor, 2x2 register tiles:
+//   mode 0: T1 = Zb L       (T1[r][c] = sum_{t >= c} Zb[r][t] L[t][c])
+//   mode 1: H  = I - L^T T1 (H[r][c]  = delta - sum_{t >= r} L[t][r] T1[t][c], c <= r)
+__device__ void cta_tri_gemm(const double* Zb_or_L, const double* Lm, double* out, int Q, int mode) {
+  const int half = (Q + 1) / 2;
+  for (int e = threadIdx.x; e < half * half; e += blockDim.x) {
+    const int r0 = 2 * (e / half), c0 = 2 * (e % half);
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    if (mode == 0) {
+      for (int t = c0; t < Q; ++t) {
+        const double z0 = Zb_or_L[r0 * Q + t];
+        const double z1 = (r0 + 1 < Q) ? Zb_or_L[(r0 + 1) * Q + t] : 0.0;
+        const double l0 = Lm[t * Q + c0];
+        const double l1 = (c0 + 1 < Q && t >= c0 + 1) ? Lm[t * Q + c0 + 1] : 0.0;
+        acc[0][0] = fma(z0, l0, acc[0][0]);
+        acc[0][1] = fma(z0, l1, acc[0][1]);
+        acc[1][0] = fma(z1, l0, acc[1][0]);
+        acc[1][1] = fma(z1, l1, acc[1][1]);
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+          if (r0 + a < Q && c0 + b < Q) out[(r0 + a) * Q + c0 + b] = acc[a][b];
+    } else {
+      if (c0 > r0 + 1) {  // strictly upper tile: zeros
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+            if (r0 + a < Q && c0 + b < Q) out[(r0 + a) * Q + c0 + b] = 0.0;
+        continue;
+      }
+      for (int t = r0; t < Q; ++t) {
+        const double l0 = Zb_or_L[t * Q + r0];
+        const double l1 = (r0 + 1 < Q && t >= r0 + 1) ? Zb_or_L[t * Q + r0 + 1] : 0.0;
+        const double t0 = Lm[t * Q + c0];
+        const double t1 = (c0 + 1 < Q) ? Lm[t * Q + c0 + 1] : 0.0;
+        acc[0][0] = fma(l0, t0, acc[0][0]);
+        acc[0][1] = fma(l0, t1, acc[0][1]);
+        acc[1][0] = fma(l1, t0, acc[1][0]);
+        acc[1][1] = fma(l1, t1, acc[1][1]);
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int r = r0 + a, c = c0 + b;
+          if (r < Q && c < Q) out[r * Q + c] = (c <= r) ? ((r == c ? 1.0 : 0.0) - acc[a][b]) : 0.0;
+        }
+    }
+  }
 }
 
 // one CTA: LG = chol(G), H = I - LG^T Zb LG, LH = chol(H).  work: 2 Q^2 doubles
@@ -235,25 +290,10 @@ __global__ void __launch_bounds__(1024) k_lowrank_factor(const double* __restric
     if (use_smem) LG[e] = v;
   }
   __syncthreads();
-  // T1 = Zb L_G
-  for (int e = tid; e < Q * Q; e += nt) {
-    const int r = e / Q, c = e % Q;
-    double acc = 0.0;
-    for (int t = c; t < Q; ++t) acc = fma(Zb[r * Q + t], A[t * Q + c], acc);
-    T1[e] = acc;
-  }
+  // T1 = Zb L_G, then H = I - L_G^T T1 (lower part) -> LH (global)
+  cta_tri_gemm(Zb, A, T1, Q, 0);
   __syncthreads();
-  // H = I - L_G^T T1 (lower part) -> LH (global), then back into A for the factorisation
-  for (int e = tid; e < Q * Q; e += nt) {
-    const int r = e / Q, c = e % Q;
-    double v = 0.0;
-    if (c <= r) {
-      double acc = 0.0;
-      for (int t = r; t < Q; ++t) acc = fma(A[t * Q + r], T1[t * Q + c], acc);
-      v = (r == c ? 1.0 : 0.0) - acc;
-    }
-    LH[e] = v;
-  }
+  cta_tri_gemm(A, T1, LH, Q, 1);
   __syncthreads();
   double* B = use_smem ? smf : LH;
   if (use_smem)
