@@ -170,7 +170,7 @@ int nmfb_barrier_trials(const double *X, const double *dX, long nx, const double
  * nmfb_direction / nmfb_quartic / nmfb_barrier_trials (gtp, alpha maxima, quartic
  * coefficients, barrier sums) and writes alpha1, t, alpha2 (graph-capturable). */
 int nmfb_armijo_select(double *sc, double mu, double wx, double wy, double eta,
-                       int max_backtracks, void *stream);
+                       int max_backtracks, const int *fcodes, void *stream);
 /* as nmfb_step_nudge with alpha read from device memory */
 int nmfb_step_nudge_dev(double *v, const double *dv, long len, const double *alpha, double tau,
                         void *stream);
@@ -230,7 +230,8 @@ int nmfb_small_step_refresh(const void *M, int m_is_f32, long n, long m, long k,
                             const double *dY, const double *dS, double *Xf, double *Ytf,
                             double *Fold, double *Fnew, double *gX, double *gY, double mu,
                             double wx, double wy, double eta, int max_bt, double tau, int ntrials,
-                            double *sc, double *work, unsigned int *tickets, void *stream);
+                            double *sc, const int *fcodes, double *work, unsigned int *tickets,
+                            void *stream);
 
 /* Residual-free IPM pieces for large M (no n x m workspace; csrc/ipm.cu):
  *   grad[r] = V[r] G - MV[r], part[b] = partial <V, MV>   (graX = X YY^T - M Y^T and

@@ -49,7 +49,7 @@ SIGNATURES = {
     "nmfb_quartic": [P, L, L, L, P, P, P, P, P, P, P],
     "nmfb_barrier_trials": [P, P, L, P, P, L, P, I, P, P, L, P],
     "nmfb_step_nudge": [P, P, L, D, D, P],
-    "nmfb_armijo_select": [P, D, D, D, D, I, P],
+    "nmfb_armijo_select": [P, D, D, D, D, I, P, P],
     "nmfb_step_nudge_dev": [P, P, L, P, D, P],
     "nmfb_kkt_sums": [P, P, P, L, P, P, P, L, D, D, P, P, P],
     "nmfb_affine_mu": [P, P, P, P, L, P, P, P, P, L, D, D, P, P, P],
@@ -65,7 +65,7 @@ SIGNATURES = {
     "nmfb_small_supported": [L, L, L],
     "nmfb_small_work_len": [L, L, L],
     "nmfb_small_direction": [P, P, P, P, P, P, L, L, L, D, D, D, D] + [P] * 19,
-    "nmfb_small_step_refresh": [P, I, L, L, L] + [P] * 14 + [D, D, D, D, I, D, I, P, P, P, P],
+    "nmfb_small_step_refresh": [P, I, L, L, L] + [P] * 14 + [D, D, D, D, I, D, I, P, P, P, P, P],
     "nmfb_lowrank_factor": [P, P, L, P, P, P, P, P],
     "nmfb_lowrank_solve": [P, P, P, P, P, L, L, P, P, P, P, P, L, P],
 }

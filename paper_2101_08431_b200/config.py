@@ -70,6 +70,7 @@ class IpmResult:
     armijo_t: list = field(default_factory=list)
     flags: list = field(default_factory=list)
     seconds: float = 0.0
+    dense_fallbacks: int = 0  # GN iterations re-solved densely after a low-rank PD failure
 
 
 @dataclass

@@ -792,8 +792,17 @@ __global__ void k_fill(double* __restrict__ v, long len, double c) {
 // sc layout: [4] gtp, [5] a1max, [6] a2max, [10..15] quartic, [32 + 2t (+1)] barrier sums.
 // Writes sc[1] = alpha1 (0 when stalled), sc[2] = t (max_bt + 1 when stalled), sc[3] = alpha2.
 __global__ void k_armijo_select(double* __restrict__ sc, double mu, double wx, double wy,
-                                double eta, int max_bt) {
+                                double eta, int max_bt, const int* __restrict__ fcodes) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // fcodes = [R1 failing row, reduced-system info, D failing column]: on any
+  // factorization failure take no step (t = -2) so the host can redo the
+  // direction with the dense Schur solve
+  if (fcodes && (fcodes[0] != 0x7F7F7F7F || fcodes[1] >= 0 || fcodes[2] != 0x7F7F7F7F)) {
+    sc[1] = 0.0;
+    sc[2] = -2.0;
+    sc[3] = 0.0;
+    return;
+  }
   const double gtp = sc[4], a1max = sc[5];
   const double ab = sc[11], bb = sc[12], ac = sc[13], bc = sc[14], cc = sc[15];
   int t = 0;
@@ -1116,9 +1125,9 @@ extern "C" int nmfb_fill(double* v, long len, double c, void* stream) {
 }
 
 extern "C" int nmfb_armijo_select(double* sc, double mu, double wx, double wy, double eta,
-                                  int max_backtracks, void* stream) {
+                                  int max_backtracks, const int* fcodes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  ++g_nmfb_launches, k_armijo_select<<<1, 32, 0, st>>>(sc, mu, wx, wy, eta, max_backtracks);
+  ++g_nmfb_launches, k_armijo_select<<<1, 32, 0, st>>>(sc, mu, wx, wy, eta, max_backtracks, fcodes);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

@@ -754,6 +754,7 @@ __device__ void armijo_pick(const double* sc, double mu, double wx, double wy, d
 
 __global__ void __launch_bounds__(256) k_sstep(double* __restrict__ sc, double mu, double wx,
                                                double wy, double eta, int max_bt, double tau,
+                                               const int* __restrict__ fcodes,
                                                double* __restrict__ X, double* __restrict__ R,
                                                const double* __restrict__ dX,
                                                const double* __restrict__ dR, long nx,
@@ -765,7 +766,12 @@ __global__ void __launch_bounds__(256) k_sstep(double* __restrict__ sc, double m
   if (threadIdx.x == 0) {
     double a1, a2;
     int t;
-    armijo_pick(sc, mu, wx, wy, eta, max_bt, &a1, &a2, &t);
+    if (fcodes[0] != 0x7F7F7F7F || fcodes[1] >= 0 || fcodes[2] != 0x7F7F7F7F) {
+      a1 = a2 = 0.0;  // factorization failed: no step, the host redoes it (dense)
+      t = -2;
+    } else {
+      armijo_pick(sc, mu, wx, wy, eta, max_bt, &a1, &a2, &t);
+    }
     sa1 = a1;
     sa2 = a2;
     if (blockIdx.x == 0) {
@@ -1026,8 +1032,8 @@ extern "C" int nmfb_small_step_refresh(const void* M, int m_is_f32, long n, long
                                        const double* dS, double* Xf, double* Ytf, double* Fold,
                                        double* Fnew, double* gX, double* gY, double mu, double wx,
                                        double wy, double eta, int max_bt, double tau, int ntrials,
-                                       double* sc, double* work, unsigned int* tickets,
-                                       void* stream) {
+                                       double* sc, const int* fcodes, double* work,
+                                       unsigned int* tickets, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (!nmfb_small_supported(n, m, k)) return NMFB_EUNSUPPORTED;
   const int nq = 64;
@@ -1040,7 +1046,8 @@ extern "C" int nmfb_small_step_refresh(const void* M, int m_is_f32, long n, long
     ++g_nmfb_launches, k_sarm<KK_><<<ntc + nq, 256, 0, st>>>(Fold, n, m, X, dX, Yt, dY, sc,        \
                                                                  ntrials, work, tickets + 2);       \
     ++g_nmfb_launches, k_sstep<<<nmfb_blocks((n + m) * KK_, 256, 148 * 4), 256, 0, st>>>(           \
-        sc, mu, wx, wy, eta, max_bt, tau, X, R, dX, dR, n * KK_, Yt, S, dY, dS, m * KK_, Xf, Ytf);  \
+        sc, mu, wx, wy, eta, max_bt, tau, fcodes, X, R, dX, dR, n * KK_, Yt, S, dY, dS, m * KK_,   \
+        Xf, Ytf);  \
     if (m_is_f32) {                                                                                 \
       cudaFuncSetAttribute(k_sres<KK_, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                            (int)tile);                                                              \

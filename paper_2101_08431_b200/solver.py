@@ -410,14 +410,14 @@ class IpmEngine:
                     _p(self.Yt), _p(self.S), _p(self.dX), _p(self.dR), _p(self.dYbuf),
                     _p(self.dS), _p(self.Xf), _p(self.Ytf), _p(fold), _p(fnew), _p(self.gX),
                     _p(self.gY), self.mu, self.wx, self.wy, p.eta, p.max_backtracks, p.tau,
-                    NTRIALS, _p(P.dscal), _p(self.swork), _p(self.tickets), s)
+                    NTRIALS, _p(P.dscal), _p(P.iscal[2:]), _p(self.swork), _p(self.tickets), s)
             self.fi ^= 1
             return
         dY = self.direction(False)
         self.armijo_launch(dY)
         s = P.stream
         P._call("nmfb_armijo_select", _p(P.dscal), self.mu, self.wx, self.wy, p.eta,
-                p.max_backtracks, s)
+                p.max_backtracks, _p(P.iscal[2:]), s)
         self.remember_factorization(False)  # the factorization's X, Y (before the step)
         a1p, a2p = P.dscal[1:2], P.dscal[3:4]
         P._call("nmfb_step_nudge_dev", _p(self.X), _p(self.dX), n * k, _p(a1p), p.tau, s)
@@ -468,7 +468,7 @@ class IpmEngine:
                 _p(self.lrwork), self.m, self.k, _p(rhs), _p(dY), _p(self.uvec), _p(self.wvec),
                 _p(P.cwork), P.cwork.numel(), P.stream)
 
-    def direction(self, full):
+    def direction(self, full, force_dense=False):
         """Newton direction; scalars land in dscal[4:7], codes in iscal[2:4].
 
         Gauss-Newton coupling: exact low-rank solve of the reduced system
@@ -481,7 +481,7 @@ class IpmEngine:
         X, Yt, F = self.X, self.Yt, self.Fcur
         P.colprod(Yt, m, k, Yt, k, self.GY)
         P.colprod(X, n, k, X, k, self.XtX, reduce=True)
-        dense = full or self.dense_gn
+        dense = full or self.dense_gn or force_dense
         P._call("nmfb_r1_factor", _p(self.GY), _p(X), _p(self.R), _p(self.gX), mux, self.rho, n,
                 k, _p(self.L), _p(self.h), _p(self.g), _p(self.Apk), _p(self.XXpk),
                 _p(P.iscal[2:]), s)
@@ -671,6 +671,7 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                     eng.remember_factorization(True)
                 else:
                     eng.flag = False
+            force_dense = False
             if not ok and eng.use_graphs:
                 eng.gn_iteration_graph()
                 v, iv = P.readback(28, 5)
@@ -679,6 +680,14 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                         P.event_times.append(e0.elapsed_time(e1))
                     except Exception:  # event nodes not timeable on this stack
                         P.graph_timing_failed = True
+                if int(v[2]) == -2 and not eng.ffree:
+                    # the rank-k^2 factorization lost positive definiteness by rounding:
+                    # no step was taken; redo this iteration with the dense Schur solve
+                    force_dense = True
+                    res.dense_fallbacks += 1
+            if force_dense:
+                pass
+            elif not ok and eng.use_graphs:
                 if int(iv[2]) != _NONE:
                     raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
                 if int(iv[4]) != _NONE:
@@ -698,13 +707,19 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                 res.trace.append((time.perf_counter() - t0, 0.5 * fsq, e_zero, eng.mu, a1, a2max, t))
                 continue
             if not ok:
-                dY = eng.direction(False)
+                dY = eng.direction(False, force_dense=force_dense)
                 eng.armijo_launch(dY)
                 v, iv = P.readback(32 + 2 * NTRIALS, 5)
                 if int(iv[2]) != _NONE:
                     raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
                 if not eng.last_dense and int(iv[4]) != _NONE:
                     raise NotPositiveDefinite("R2 block not positive definite", int(iv[4]))
+                if int(iv[3]) >= 0 and not eng.last_dense and not eng.ffree:
+                    # low-rank capacitance lost PD-ness by rounding: dense Schur solve
+                    res.dense_fallbacks += 1
+                    dY = eng.direction(False, force_dense=True)
+                    eng.armijo_launch(dY)
+                    v, iv = P.readback(32 + 2 * NTRIALS, 5)
                 if int(iv[3]) >= 0:
                     raise NotPositiveDefinite("Gauss-Newton Schur matrix not positive definite",
                                               int(iv[3]))

@@ -20,7 +20,7 @@ from paper_2101_08431_b200.stream import StreamSession  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ipm", type=int, default=0, help="fixed IPM iterations per chunk (0: to tol/cap)")
-    ap.add_argument("--barrier", default="paper")
+    ap.add_argument("--barrier", default="balanced")
     ap.add_argument("--oracle-chunks", type=int, default=0)
     a = ap.parse_args()
     cfg = data.CONFIGS["c3"]
@@ -32,15 +32,22 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     s = StreamSession(M[:, :cfg.m_start], X0, Y0[:, :cfg.m_start], ipm_factory=mk)
+    err = None
     for m0 in range(cfg.m_start, cfg.m, cfg.m_step):
-        s.append(M[:, m0:m0 + cfg.m_step])
+        try:
+            s.append(M[:, m0:m0 + cfg.m_step])
+        except Exception as e:  # record where the session stopped
+            err = f"m={m0 + cfg.m_step}: {type(e).__name__}: {e}"
+            break
     torch.cuda.synchronize()
     total = time.perf_counter() - t0
     chunks = [{"m": c[0], "s": round(c[1], 5), "sweeps": c[2].stage1.sweeps,
                "ipm": c[2].ipm.iters if c[2].ipm else 0, "E": c[2].final_kkt_error,
-               "status": c[2].status} for c in s.chunks]
+               "status": c[2].status,
+               "dense_fallbacks": c[2].ipm.dense_fallbacks if c[2].ipm else 0} for c in s.chunks]
     out = {"config": "c3", "chunks": len(chunks), "total_s": total,
-           "mean_chunk_ms": 1e3 * total / len(chunks), "per_chunk": chunks}
+           "mean_chunk_ms": 1e3 * total / len(chunks), "error": err,
+           "per_chunk": chunks}
     if a.oracle_chunks:
         from oracle import driver as D
         from oracle import stream as OS

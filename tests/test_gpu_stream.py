@@ -30,3 +30,31 @@ def test_stream_parity_small():
         assert ro.ipm.armijo_t == rg.ipm.armijo_t
         rel = np.abs(rg.Yt - ro.Yt).max() / np.abs(ro.Yt).max()
         assert rel < 1e-7, (mo, rel)
+
+
+def test_stream_c3_dense_fallback_parity():
+    """c3's second chunk under the paper barrier drifts until the rank-k^2
+    capacitance loses positive definiteness by rounding; the device re-solves those
+    iterations with the dense Schur system and must still follow the oracle (which
+    always factors the dense system) decision for decision."""
+    from oracle import driver as D
+    from oracle import stream as OS
+    from paper_2101_08431_b200 import data
+    from paper_2101_08431_b200.config import IpmParams
+    from paper_2101_08431_b200.stream import StreamSession
+
+    cfg = data.CONFIGS["c3"]
+    M, X0, Y0, _, _ = data.make(cfg)
+    D.set_schur_backend("numpy")
+    try:
+        so = OS.OracleStream(M[:, :20], X0, Y0[:, :20], ipm_factory=D.IpmParams)
+        sg = StreamSession(M[:, :20], X0, Y0[:, :20], ipm_factory=IpmParams)
+        so.append(M[:, 20:30])
+        sg.append(M[:, 20:30])
+    finally:
+        D.set_schur_backend("c")
+    rg, ro = sg.chunks[1][2], so.chunks[1][2]
+    assert rg.ipm.dense_fallbacks > 0
+    assert ro.ipm.armijo_t == rg.ipm.armijo_t
+    rel = abs(rg.final_objective - ro.objective) / abs(ro.objective)
+    assert rel < 1e-6, rel
