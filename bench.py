@@ -28,6 +28,12 @@ import numpy as np  # noqa: E402
 
 WORKLOAD = "c2"
 IPM_CAP = 500
+# DRAM bytes per IPM iteration of the roofline entry from one `ncu --set full` capture
+# (cold-cache, serialised replay), scaled to the live launch's iteration count.
+NCU_TRAFFIC = {
+    "nmfb_ipm_persist": {"dram_bytes_per_iteration": (2809344 + 137472) / 200,
+                         "source": "profiles/r01_ncu_persist_c2.txt (200-iteration launch)"},
+}
 CPU_IPM_SAMPLE = 20  # bounded CPU sample: full stage 1 + this many IPM iterations
 
 
@@ -213,6 +219,7 @@ def run_b200(args):
     clocks.start()
     torch.cuda.synchronize()
     launches0 = P.lib.nmfb_launch_count() + P.graph_kernel_launches
+    piters0 = P.persist_iters
     total_ms, sweeps, iters, conv, kkt = 0.0, 0, 0, True, 0.0
     stream = torch.cuda.current_stream()
     for _ in range(args.steps):
@@ -227,6 +234,7 @@ def run_b200(args):
         sweeps, iters, conv, kkt = sweeps + s, iters + i, conv and c, e
     torch.cuda.synchronize()
     launches = P.lib.nmfb_launch_count() + P.graph_kernel_launches - launches0
+    piters = P.persist_iters - piters0
     clk = clocks.stop()
     if ws > 1:
         import torch.distributed as dist
@@ -277,10 +285,17 @@ def run_b200(args):
     peaks, peak_src = _peaks()
     fp64_peak = measure_fp64_peak(dev)
     avg_ms = float(np.mean(kt)) if kt else float("nan")
-    # nmfb_small_step_refresh = Armijo sums over F + step + F/graX/graY/KKT at the new
-    # point: algorithmic bytes = F read (quartic) + M read + F write (+ O((n+m)k) vectors)
-    nbytes = 3 * cfg.n * cfg.m * 8 + 12 * (cfg.n + cfg.m) * cfg.k * 8
+    # nmfb_ipm_persist = one cooperative launch per inner loop (csrc/persist.cu); per
+    # IPM iteration it touches M three times (quartic coefficients, residual/graX,
+    # graY) plus O((n+m)k) vectors: algorithmic bytes per launch = that x iterations
+    # per launch.  M stays in shared memory across the launch, so the DRAM traffic
+    # (ncu) is ~one read of M per launch.
+    per_it = 3 * cfg.n * cfg.m * 8 + 12 * (cfg.n + cfg.m) * cfg.k * 8
+    it_per_launch = piters / max(len(kt), 1) if timed_entry == "nmfb_ipm_persist" else 1.0
+    nbytes = per_it * it_per_launch
     achieved = nbytes / (avg_ms * 1e-3) / 1e9 if kt else None
+    ncu = NCU_TRAFFIC.get(timed_entry)
+    traffic = ncu["dram_bytes_per_iteration"] * it_per_launch if ncu else None
     line = {
         "metric": _metric(), "value": value,
         "unit": "solver iterations/s (ANLS sweeps + IPM iterations)",
@@ -294,14 +309,18 @@ def run_b200(args):
         "ipm_iters_per_s": tot_it / (total_ms / 1e3),
         "time_to_tol_s": total_ms / 1e3 / args.steps,
         "converged": bool(conv), "final_kkt": kkt,
-        "roofline": {"bound": "hbm", "kernel": f"{timed_entry} (k_sarm + k_sstep + k_sres: "
-                                               "quartic, update, residual/gradients/KKT)",
+        "roofline": {"bound": "hbm",
+                     "kernel": f"{timed_entry} (k_ipm_persist: the whole Gauss-Newton inner "
+                               "loop in one cooperative launch)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
-                     "traffic": None, "launches": len(kt), "avg_ms": avg_ms, "timing": kt_note,
+                     "traffic": traffic, "launches": len(kt), "avg_ms": avg_ms,
+                     "iterations_per_launch": it_per_launch, "timing": kt_note,
                      "algorithmic_bytes": nbytes, "peak_source": peak_src,
-                     "note": "c2's M and F (2.4 MB each) are L2-resident within a step: the "
-                             "entry is latency-bound; aux reports the HBM-bound c4 products"},
+                     "traffic_source": ncu["source"] if ncu else None,
+                     "note": "latency-bound: c2's M (2.4 MB) is held in shared memory for the "
+                             "whole launch, each iteration is a chain of 4 grid barriers and "
+                             "k^2-sized serial solves; aux reports the HBM-bound c4 products"},
         "fp64_dgemm_tflops_measured": fp64_peak,
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -446,7 +465,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--roofline-entry", default="nmfb_small_step_refresh")
+    ap.add_argument("--roofline-entry", default="nmfb_ipm_persist")
     ap.add_argument("--no-aux", dest="aux", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -248,6 +248,25 @@ int nmfb_ffree_quartic(const double *A1, const double *A2, const double *XX, con
 /* number of kernel launches issued by this library so far (host counter) */
 unsigned long long nmfb_launch_count(void);
 
+
+/* Persistent Gauss-Newton inner loop for small problems (csrc/persist.cu): one
+ * cooperative launch runs PAPER Alg. 2's inner iterations while
+ * E(.;mu) > eps_mu, up to max_iters.  log: max_iters x 8 doubles per iteration
+ * [t, alpha1, alpha2, ||F||^2, E_mu, E_0, globaltimer ns, -]; status (device
+ * int[2]) = [iterations done, exit code 0 done / 1 factorization failure (no step)
+ * / 2 Armijo stall].  fcodes = [R1 failing row, capacitance info, D failing col]
+ * (host initialises 0x7F7F7F7F, -1, 0x7F7F7F7F).  grid = 0: automatic.  prof
+ * (optional, may be NULL): 16 clock64 stamps per iteration from CTA 0 (phase timing). */
+int nmfb_persist_supported(long n, long m, long k, int grid);
+long nmfb_persist_work_len(long n, long m, long k, int grid);
+int nmfb_ipm_persist(const void *M, int m_is_f32, long n, long m, long k, double *X, double *R,
+                     double *gX, double *Yt, double *S, double *gY, double *Fout, double *L,
+                     double *Xf, double *Ytf, double *LD, double *LG, double *LH, double *Zb,
+                     double mu, double wx, double wy, double rho, double tau, double eta,
+                     double eps_mu, int max_bt, int ntrials, int max_iters, double *sc,
+                     int *fcodes, double *logv, int *status, double *work, unsigned int *bar,
+                     int grid, long long *prof, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

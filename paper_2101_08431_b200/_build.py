@@ -27,6 +27,7 @@ SOURCES = {
     "dense.cu": [],
     "lowrank.cu": [],
     "small.cu": [],
+    "persist.cu": [],
     "runtime.cu": [],
 }
 

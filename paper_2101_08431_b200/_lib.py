@@ -63,6 +63,9 @@ SIGNATURES = {
     "nmfb_ffree_fsq": [P, D, P, P, L, P, P, P],
     "nmfb_ffree_quartic": [P, P, P, P, P, P, P, P, P, L, P, P],
     "nmfb_small_supported": [L, L, L],
+    "nmfb_persist_supported": [L, L, L, I],
+    "nmfb_persist_work_len": [L, L, L, I],
+    "nmfb_ipm_persist": [P, I, L, L, L] + [P] * 14 + [D] * 7 + [I, I, I] + [P] * 6 + [I, P, P],
     "nmfb_small_work_len": [L, L, L],
     "nmfb_small_direction": [P, P, P, P, P, P, L, L, L, D, D, D, D] + [P] * 19,
     "nmfb_small_step_refresh": [P, I, L, L, L] + [P] * 14 + [D, D, D, D, I, D, I, P, P, P, P, P],
@@ -70,7 +73,8 @@ SIGNATURES = {
     "nmfb_lowrank_solve": [P, P, P, P, P, L, L, P, P, P, P, P, L, P],
 }
 RESTYPES = {"nmfb_colprod_work_len": ctypes.c_long, "nmfb_rowprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
-            "nmfb_launch_count": ctypes.c_ulonglong, "nmfb_small_work_len": ctypes.c_long}
+            "nmfb_launch_count": ctypes.c_ulonglong, "nmfb_small_work_len": ctypes.c_long,
+            "nmfb_persist_work_len": ctypes.c_long}
 
 _lib = None
 

@@ -36,6 +36,8 @@ class IpmParams:
     schur_solver: str = "lowrank"  # Gauss-Newton reduced system: "lowrank" (exact, rank k^2) | "dense"
     use_graphs: bool = True  # replay each Gauss-Newton iteration as a captured CUDA graph
     fused_small: bool = True  # fused 6-kernel iteration when k <= 4 and m k <= 2048 (csrc/small.cu)
+    persistent: bool = True  # whole inner loop in one cooperative launch (csrc/persist.cu)
+    persist_grid: int = 0  # CTAs of the persistent launch (0: automatic)
     residual: str = "auto"  # "dense" (materialise F) | "free" (Grams + M passes) | "auto" (free if n m >= 2^25)
 
 

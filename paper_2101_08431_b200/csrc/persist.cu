@@ -1,0 +1,1224 @@
+// Persistent interior-point inner loop for small problems (configs c1-c3).
+//
+// csrc/small.cu runs one Gauss-Newton iteration as six kernels replayed from a
+// CUDA graph, with one host synchronisation per iteration; at c2 sizes every
+// launch is latency-bound.  Here ONE cooperative launch runs the whole inner
+// loop of Algorithm 2 (PAPER Alg. 2 / SPEC.md:337-345: direction -> Armijo ->
+// nudged update -> gradients/KKT, repeated while E(.;mu) > eps_mu):
+//
+//   * every CTA owns a contiguous block of rows of M (kept in shared memory
+//     when it fits), X, R, graX and the row factors L_i, h_i;
+//   * the Y side (m x k: Y, S, graY, dY, D_j^{-1}) and every k/k^2-sized object
+//     are replicated in every CTA's shared memory and computed redundantly with
+//     identical arithmetic, so all CTAs take the same branch without a broadcast;
+//   * cross-CTA sums are written as per-CTA partials and, after a grid barrier,
+//     reduced by every CTA in a fixed lane/CTA order (bit-identical everywhere);
+//   * four grid barriers per iteration: R1/Z partials | direction + quartic
+//     partials | barrier-trial partials (8 trials per batch, batches only while
+//     Armijo keeps backtracking) | residual + graY partials.
+//
+// Exits (status): 0 inner loop done (E(.;mu) <= eps_mu or the iteration budget),
+// 1 factorization failure at the current point (no step taken; the host redoes
+// the iteration eagerly with the dense Schur system or raises), 2 Armijo stall.
+// The state left in global memory is what the host path leaves after the same
+// iterations: X, R, graX, Y, S, graY, F (into Fout), R1 factors L, the
+// factorization copy (Xf, Ytf) and the low-rank factors (LD, LG, LH, Zb) for the
+// predictor, and the KKT sums at sc[16..27], ||F||^2 at sc[0].
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "nmfb200.h"
+
+namespace {
+
+constexpr int PT = 256;      // threads per CTA
+constexpr int NW = PT / 32;  // warps per CTA
+constexpr int TB = 8;        // barrier trials per batch
+constexpr int LOGW = 8;      // doubles per iteration record
+static_assert(TB == NW, "one warp per barrier trial");
+
+struct PArgs {
+  const void* M;
+  long n, m;
+  double *X, *R, *gX, *Yt, *S, *gY, *Fout, *L, *Xf, *Ytf, *LD, *LG, *LH, *Zb;
+  double *sc, *logv, *work;
+  int *fcodes, *status;
+  unsigned int* bar;
+  double mu, wx, wy, rho, tau, eta, eps_mu;
+  int max_bt, ntrials, max_iters, m_in_smem;
+  long long* prof;  // optional per-iteration phase clocks of CTA 0 (16 per iteration)
+};
+
+#define STAMP(i)                                                       \
+  do {                                                                 \
+    if (a.prof && blockIdx.x == 0 && threadIdx.x == 0 && it < 4096)    \
+      a.prof[(long)it * 32 + (i)] = clock64();                         \
+  } while (0)
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid barrier on per-CTA epoch flags (host zeroes them per launch): every CTA
+// publishes its epoch with a release store, warp 0 of every CTA polls all flags.
+// No atomics, so arrivals do not serialise on one L2 address.  A bounded spin
+// turns a lost CTA into a trap (reported launch error) instead of a hang.
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid barrier: cooperative-groups grid sync (measured on B200 with 148 CTAs:
+// 1.3 us, against 1.8 us for an atomic counter and 2.8 us for per-CTA flags polled
+// by every CTA; scripts/micro/bar.cu).  `flags`/`epoch` are kept for the spin-guarded
+// fallback path below.
+__device__ __forceinline__ void grid_barrier(unsigned* flags, unsigned& epoch) {
+  (void)flags;
+  ++epoch;
+  cooperative_groups::this_grid().sync();
+}
+
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+// Reduce entries [e0, e1) of an entry-major partial array part[e * G + c] over
+// the G CTAs: warp w takes chunks of EB consecutive entries, each lane issues all
+// of its loads (CTAs lane, lane+32, ..) before reducing; fixed order -> the same
+// bits in every lane of every CTA.  kind 0 sum, 1 min, 2 max.  G <= 160.
+template <int KD>
+__device__ __forceinline__ double op2(double a, double b) {
+  return KD == 0 ? a + b : (KD == 1 ? fmin(a, b) : fmax(a, b));
+}
+template <int KD>
+__device__ __forceinline__ double warp_op(double v) {
+  return KD == 0 ? warp_sum(v) : (KD == 1 ? warp_min(v) : warp_max(v));
+}
+template <int KD>
+__device__ __forceinline__ double op_id() {
+  return KD == 0 ? 0.0 : (KD == 1 ? 1.0 / 0.0 : -1.0 / 0.0);
+}
+
+template <int EB, int KD>
+__device__ __forceinline__ void reduce_entries(const double* part, int G, long e0, long e1,
+                                               double* out, bool out_global = false) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll 1
+  for (long eb = e0 + (long)wid * EB; eb < e1; eb += (long)NW * EB) {
+    double v[EB][5];
+#pragma unroll
+    for (int b = 0; b < EB; ++b)
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        const int c = lane + 32 * u;
+        v[b][u] = (eb + b < e1 && c < G) ? ldcg(part + (eb + b) * G + c) : op_id<KD>();
+      }
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
+      double s = v[b][0];
+#pragma unroll
+      for (int u = 1; u < 5; ++u) s = op2<KD>(s, v[b][u]);
+      s = warp_op<KD>(s);
+      if (lane == 0 && eb + b < e1) {
+        if (out_global)
+          __stcg(out + (eb + b - e0), s);
+        else
+          out[eb + b - e0] = s;
+      }
+    }
+  }
+}
+
+// Cholesky of a Q x Q smem matrix by warp 0 with the rows in registers (lane = row,
+// column j broadcast by shuffles); the strict upper triangle is zeroed and the
+// reciprocal diagonal 1/L_jj stored in dinv[Q].  Returns the failing pivot (-1: PD)
+// in every lane of warp 0.
+// (compile-time recursion keeps every row element in a register even where the
+// unroller would give up inside this large kernel)
+template <int J, int C, int Q>
+struct CholUpd {
+  static __device__ __forceinline__ void run(double (&a)[Q], int r) {
+    const double lcj = __shfl_sync(0xffffffffu, a[J], C);
+    if (r >= C) a[C] -= a[J] * lcj;
+    CholUpd<J, C + 1, Q>::run(a, r);
+  }
+};
+template <int J, int Q>
+struct CholUpd<J, Q, Q> {
+  static __device__ __forceinline__ void run(double (&)[Q], int) {}
+};
+template <int J, int Q>
+struct CholStep {
+  static __device__ __forceinline__ void run(double (&a)[Q], int r, int& fail, double& di_r) {
+    double pv = __shfl_sync(0xffffffffu, a[J], J);
+    if (fail < 0 && !(pv > 0.0)) fail = J;  // continue on a dummy pivot after a failure
+    if (fail >= 0) pv = 1.0;
+    const double di = rsqrt(pv);
+    if (r == J) {
+      a[J] = pv * di;
+      di_r = di;
+    } else if (r > J) {
+      a[J] = a[J] * di;
+    }
+    CholUpd<J, J + 1, Q>::run(a, r);
+    CholStep<J + 1, Q>::run(a, r, fail, di_r);
+  }
+};
+template <int Q>
+struct CholStep<Q, Q> {
+  static __device__ __forceinline__ void run(double (&)[Q], int, int&, double&) {}
+};
+
+template <int Q>
+__device__ __forceinline__ int warp_chol(double* A, double* dinv) {
+  const int r = threadIdx.x & 31;
+  double a[Q];
+#pragma unroll
+  for (int c = 0; c < Q; ++c) a[c] = (r < Q) ? A[r * Q + c] : 0.0;
+  int fail = -1;
+  double di_r = 0.0;
+  CholStep<0, Q>::run(a, r, fail, di_r);
+  if (r < Q) {
+#pragma unroll
+    for (int c = 0; c < Q; ++c) A[r * Q + c] = (c <= r) ? a[c] : 0.0;
+    dinv[r] = di_r;
+  }
+  return fail;
+}
+
+// Block reductions of NV values with the result in EVERY thread (fixed order).
+// Value q is min-reduced if bit q of MINM is set, max-reduced for MAXM, else summed.
+template <int Q, int NV, int MINM, int MAXM>
+struct BlockRed {
+  static constexpr int KD = ((MINM >> Q) & 1) ? 1 : (((MAXM >> Q) & 1) ? 2 : 0);
+  static __device__ __forceinline__ void warp_part(double (&v)[NV]) {
+    v[Q] = warp_op<KD>(v[Q]);
+    BlockRed<Q + 1, NV, MINM, MAXM>::warp_part(v);
+  }
+  static __device__ __forceinline__ void combine(double (&v)[NV], const double* sh) {
+    double r = sh[Q * NW];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) r = op2<KD>(r, sh[Q * NW + w]);
+    v[Q] = r;
+    BlockRed<Q + 1, NV, MINM, MAXM>::combine(v, sh);
+  }
+};
+template <int NV, int MINM, int MAXM>
+struct BlockRed<NV, NV, MINM, MAXM> {
+  static __device__ __forceinline__ void warp_part(double (&)[NV]) {}
+  static __device__ __forceinline__ void combine(double (&)[NV], const double*) {}
+};
+
+template <int NV, int MINM = 0, int MAXM = 0>
+__device__ __forceinline__ void block_reduce_all(double (&v)[NV], double* sh /* NV * NW */) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  BlockRed<0, NV, MINM, MAXM>::warp_part(v);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sh[q * NW + wid] = v[q];
+  }
+  __syncthreads();
+  BlockRed<0, NV, MINM, MAXM>::combine(v, sh);
+  __syncthreads();
+}
+
+__device__ __forceinline__ int pk(int a, int b, int k) {
+  if (a > b) {
+    const int t = a;
+    a = b;
+    b = t;
+  }
+  return a * k - a * (a - 1) / 2 + (b - a);
+}
+
+// Cholesky of a K x K SPD matrix in registers (lower), ok flag; small.cu order.
+template <int K>
+__device__ __forceinline__ bool reg_chol(double (&L)[K][K]) {
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double s = L[j][j];
+#pragma unroll
+    for (int p = 0; p < j; ++p) s -= L[j][p] * L[j][p];
+    if (!(s > 0.0)) ok = false;
+    const double d = sqrt(fmax(s, 1e-300));
+    L[j][j] = d;
+#pragma unroll
+    for (int r = j + 1; r < K; ++r) {
+      double t = L[r][j];
+#pragma unroll
+      for (int p = 0; p < j; ++p) t -= L[r][p] * L[j][p];
+      L[r][j] = t / d;
+    }
+  }
+  return ok;
+}
+
+template <int K>
+__device__ __forceinline__ void reg_inv_lower(const double (&L)[K][K], double (&Li)[K][K]) {
+#pragma unroll
+  for (int c = 0; c < K; ++c)
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      if (a < c) {
+        Li[a][c] = 0.0;
+      } else {
+        double s = (a == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int p = 0; p < a; ++p)
+          if (p >= c) s -= L[a][p] * Li[p][c];
+        Li[a][c] = s / L[a][a];
+      }
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void reg_solve(const double (&L)[K][K], const double (&b)[K],
+                                          double (&out)[K]) {
+  double z[K];
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    double s = b[a];
+#pragma unroll
+    for (int p = 0; p < a; ++p) s -= L[a][p] * z[p];
+    z[a] = s / L[a][a];
+  }
+#pragma unroll
+  for (int a = K - 1; a >= 0; --a) {
+    double s = z[a];
+#pragma unroll
+    for (int p = a + 1; p < K; ++p) s -= L[p][a] * out[p];
+    out[a] = s / L[a][a];
+  }
+}
+
+__device__ __forceinline__ double nudge(double old, double d, double a, double tau) {
+  const double nv = old + a * d;
+  return (nv > 0.0) ? nv : (1.0 - tau) * old;
+}
+
+// per-CTA workspace layout (doubles) in PArgs::work
+struct WLayout {
+  long pa, pb, pc, pd, pg, total;
+};
+__host__ __device__ inline WLayout wlayout(long G, long m, int K) {
+  const long KK = K * (K + 1) / 2, N = m * K;
+  WLayout w;
+  const long sa = KK * KK + 2 * K * K + 1;
+  w.pa = 0;
+  w.pb = w.pa + G * sa;
+  w.pc = w.pb + G * 9;
+  w.pd = w.pc + 2 * G * 2 * TB;
+  w.pg = w.pd + G * 8;
+  w.total = w.pg + G * N;
+  return w;
+}
+
+template <int K>
+__host__ __device__ inline long smem_doubles(long nrm, long m, bool with_m) {
+  const long KK = K * (K + 1) / 2, N = m * K;
+  long d = 4 * N + m * KK + nrm * (7 * K + K * K + KK);
+  if (with_m) d += nrm * m;
+  return d;
+}
+
+template <int K, typename T>
+__global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
+  constexpr int KK = K * (K + 1) / 2, Q = K * K;
+  constexpr int SA = KK * KK + 2 * K * K + 1;  // phase-A partial stride
+  const long n = a.n, m = a.m, N = m * K;
+  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  const long r0 = (long)cta * n / G, r1 = (long)(cta + 1) * n / G;
+  const int nr = (int)(r1 - r0);
+  const long nrm = (n + G - 1) / G;
+  const double mux = a.wx * a.mu, muy = a.wy * a.mu;
+  const WLayout wl = wlayout(G, m, K);
+  double* PA = a.work + wl.pa;
+  double* PB = a.work + wl.pb;
+  double* PC = a.work + wl.pc;
+  double* PD = a.work + wl.pd;
+  double* PG = a.work + wl.pg;
+
+  extern __shared__ double sm[];
+  double* Ys = sm;
+  double* Ss = Ys + N;
+  double* gYs = Ss + N;
+  double* Ts = gYs + N;  // t_j, then dY
+  double* dinv = Ts + N;
+  double* xs = dinv + m * KK;
+  double* rs = xs + nrm * K;
+  double* gxs = rs + nrm * K;
+  double* dxs = gxs + nrm * K;
+  double* drs = dxs + nrm * K;
+  double* hs = drs + nrm * K;
+  double* gs = hs + nrm * K;
+  double* Ls = gs + nrm * K;
+  double* As = Ls + nrm * K * K;
+  double* Ms = As + nrm * KK;  // own rows of M (when m_in_smem)
+
+  __shared__ double ZHX[SA];  // Z (packed kk x kk), H, X^T X, failing R1 row
+  double* Zs = ZHX;
+  double* Hs = Zs + KK * KK;
+  double* XtXs = Hs + K * K;
+  __shared__ double Gdy[K * K], gy[K * K], dGi[Q], dHi[Q];
+  __shared__ double Gm[Q * Q], Zbm[Q * Q], T1[Q * Q], Hm[Q * Q], u[Q], w[Q], w2[Q];
+  __shared__ double red[16 * NW];
+  __shared__ double scal[24];  // [0..2] ysc, [3..5] gtp,a1max,a2max, [6..11] quartic
+  __shared__ double kx[8];     // X-part KKT sums + fsq (after phase E)
+  __shared__ double bars[2 * TB];
+  __shared__ int s_fail, s_t;
+  __shared__ int ia[KK], ic[KK];
+
+  // ---- load the state --------------------------------------------------------
+  #pragma unroll 1
+  for (int e = tid; e < KK; e += PT) {
+    for (int p = 0; p < K; ++p)
+      for (int q = p; q < K; ++q)
+        if (pk(p, q, K) == e) {
+          ia[e] = p;
+          ic[e] = q;
+        }
+  }
+  #pragma unroll 1
+  for (long e = tid; e < N; e += PT) {
+    Ys[e] = a.Yt[e];
+    Ss[e] = a.S[e];
+    gYs[e] = a.gY[e];
+  }
+  #pragma unroll 1
+  for (long e = tid; e < (long)nr * K; e += PT) {
+    xs[e] = a.X[r0 * K + e];
+    rs[e] = a.R[r0 * K + e];
+    gxs[e] = a.gX[r0 * K + e];
+  }
+  const T* Mg = (const T*)a.M;
+  if (a.m_in_smem)
+    #pragma unroll 1
+    for (long e = tid; e < (long)nr * m; e += PT) Ms[e] = (double)Mg[r0 * m + e];
+  __syncthreads();
+  // own rows of M through one generic pointer (shared memory when staged, else the
+  // fp64 global rows; the host only allows fp32 M when it is staged)
+  const double* Mp = a.m_in_smem ? Ms : (const double*)a.M + r0 * m;
+
+  unsigned epoch = 0;
+  int it = 0;
+  int status = 0;
+  for (;;) {
+    // ======== phase A: rows -> R1 factors, h, g; partials of Z, H, X^T X ========
+    STAMP(0);
+    #pragma unroll 1
+    for (int e = wid; e < K * K; e += NW) {
+      const int p = e / K, q = e % K;
+      double s = 0.0;
+      #pragma unroll 1
+      for (long j = lane; j < m; j += 32) s = fma(Ys[j * K + p], Ys[j * K + q], s);
+      s = warp_sum(s);
+      if (lane == 0) gy[e] = s;
+    }
+    __syncthreads();
+    double badA = 1.0 / 0.0;
+    #pragma unroll 1
+    for (int rr = tid; rr < nr; rr += PT) {
+      const long i = r0 + rr;
+      double x[K], L[K][K], b[K], hv[K], gv[K];
+#pragma unroll
+      for (int p = 0; p < K; ++p) x[p] = xs[rr * K + p];
+#pragma unroll
+      for (int p = 0; p < K; ++p)
+#pragma unroll
+        for (int c = 0; c < K; ++c) L[p][c] = (c <= p) ? gy[p * K + c] : 0.0;
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        L[p][p] += a.rho + rs[rr * K + p] / x[p];
+        b[p] = mux / x[p] - gxs[rr * K + p];
+      }
+      if (!reg_chol<K>(L)) badA = fmin(badA, (double)i);
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        double s = b[p];
+#pragma unroll
+        for (int q = 0; q < p; ++q) s -= L[p][q] * hv[q];
+        hv[p] = s / L[p][p];
+      }
+#pragma unroll
+      for (int p = K - 1; p >= 0; --p) {
+        double s = hv[p];
+#pragma unroll
+        for (int q = p + 1; q < K; ++q) s -= L[q][p] * gv[q];
+        gv[p] = s / L[p][p];
+      }
+      double Li[K][K];
+      reg_inv_lower<K>(L, Li);
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        hs[rr * K + p] = hv[p];
+        gs[rr * K + p] = gv[p];
+#pragma unroll
+        for (int c = 0; c < K; ++c) Ls[(rr * K + p) * K + c] = (c <= p) ? L[p][c] : 0.0;
+#pragma unroll
+        for (int c = p; c < K; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if (q >= c) s = fma(Li[q][p], Li[q][c], s);
+          As[rr * KK + (p * K - p * (p - 1) / 2 + (c - p))] = s;
+        }
+      }
+    }
+    {
+      double v[1] = {badA};
+      block_reduce_all<1, 1, 0>(v, red);
+      badA = v[0];
+    }
+    #pragma unroll 1
+    for (int e = tid; e < SA; e += PT) {
+      double s = 0.0;
+      if (e < KK * KK) {
+        const int ab = e / KK, pq = e % KK;
+        const int p = ia[pq], q = ic[pq];
+        #pragma unroll 1
+        for (int rr = 0; rr < nr; ++rr) s = fma(As[rr * KK + ab], xs[rr * K + p] * xs[rr * K + q], s);
+      } else if (e < KK * KK + K * K) {
+        const int qq = e - KK * KK, p = qq / K, c = qq % K;
+        #pragma unroll 1
+        for (int rr = 0; rr < nr; ++rr) s = fma(xs[rr * K + p], gs[rr * K + c], s);
+      } else if (e < KK * KK + 2 * K * K) {
+        const int qq = e - KK * KK - K * K, p = qq / K, c = qq % K;
+        #pragma unroll 1
+        for (int rr = 0; rr < nr; ++rr) s = fma(xs[rr * K + p], xs[rr * K + c], s);
+      } else {
+        s = badA;
+      }
+      __stcg(PA + (long)e * G + cta, s);
+    }
+    STAMP(1);
+    grid_barrier(a.bar, epoch);
+    STAMP(2);
+
+    // ======== phase B: decision, Y side, row directions, quartic partials ========
+    {
+      constexpr int NGY = (2048 + PT - 1) / PT;
+      double gyv[NGY];
+      if (it > 0) {
+#pragma unroll
+        for (int q = 0; q < NGY; ++q) {
+          const long e = tid + (long)q * PT;
+          gyv[q] = e < N ? ldcg(a.gY + e) : 0.0;
+        }
+      }
+      constexpr int EBA = (SA + NW - 1) / NW < 8 ? (SA + NW - 1) / NW : 8;
+      reduce_entries<EBA, 0>(PA, G, 0, SA - 1, ZHX);
+      reduce_entries<1, 1>(PA, G, SA - 1, SA, ZHX + SA - 1);
+      if (it > 0) {
+#pragma unroll
+        for (int q = 0; q < NGY; ++q) {
+          const long e = tid + (long)q * PT;
+          if (e < N) gYs[e] = gyv[q];
+        }
+      }
+    }
+    __syncthreads();
+    STAMP(16);
+    if (it > 0) {
+      // KKT sums at the current point: X part from phase E, Y part replicated
+      double v[6] = {0.0, 0.0, 0.0, 0.0, -1.0 / 0.0, -1.0 / 0.0};
+      #pragma unroll 1
+      for (long e = tid; e < N; e += PT) {
+        const double y = Ys[e], s = Ss[e], g = gYs[e];
+        const double ys = y * s;
+        v[0] = fma(g - s, g - s, v[0]);
+        v[1] = fma(ys - muy, ys - muy, v[1]);
+        v[2] = fma(ys, ys, v[2]);
+        v[3] += ys;
+        v[4] = fmax(v[4], fabs(g));
+        v[5] = fmax(v[5], y);
+      }
+      STAMP(17);
+      block_reduce_all<6, 0, 0x30>(v, red);
+      const double st = sqrt(fmax(kx[1] + v[0], 0.0));
+      const double e_mu = fmax(st, sqrt(fmax(kx[2] + v[1], 0.0)));
+      const double e_0 = fmax(st, sqrt(fmax(kx[3] + v[2], 0.0)));
+      if (cta == 0 && tid == 0) {
+        double* rec = a.logv + (long)(it - 1) * LOGW;
+        rec[3] = kx[0];
+        rec[4] = e_mu;
+        rec[5] = e_0;
+        a.sc[0] = kx[0];
+        a.sc[16] = kx[1];
+        a.sc[17] = kx[2];
+        a.sc[18] = kx[3];
+        a.sc[19] = kx[4];
+        a.sc[20] = v[0];
+        a.sc[21] = v[1];
+        a.sc[22] = v[2];
+        a.sc[23] = v[3];
+        a.sc[24] = kx[5];
+        a.sc[25] = v[4];
+        a.sc[26] = kx[6];
+        a.sc[27] = v[5];
+      }
+      if (!(e_mu > a.eps_mu) || it >= a.max_iters) {
+        status = 0;
+        break;
+      }
+    }
+    if (ZHX[SA - 1] < 1.0 / 0.0) {
+      if (cta == 0 && tid == 0) a.fcodes[0] = (int)ZHX[SA - 1];
+      status = 1;
+      break;
+    }
+    // commit this iteration's row factors (the predictor reuses the last ones)
+    #pragma unroll 1
+    for (long e = tid; e < (long)nr * K * K; e += PT) a.L[r0 * K * K + e] = Ls[e];
+    #pragma unroll 1
+    for (long e = tid; e < (long)nr * K; e += PT) a.Xf[r0 * K + e] = xs[e];
+    if (cta == 0)
+      #pragma unroll 1
+      for (long e = tid; e < N; e += PT) a.Ytf[e] = Ys[e];
+
+    STAMP(3);
+    // ---- Y side (replicated): rhs, D_j, t_j = D_j^{-1} rhs_j, D_j^{-1} packed
+    int badD = 0x7F7F7F7F;
+    #pragma unroll 1
+    for (long j = tid; j < m; j += PT) {
+      double y[K], L[K][K], rhs[K], tv[K];
+#pragma unroll
+      for (int p = 0; p < K; ++p) y[p] = Ys[j * K + p];
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        double ra = 0.0;
+#pragma unroll
+        for (int c = 0; c < K; ++c) ra = fma(Hs[p * K + c], y[c], ra);
+        rhs[p] = (muy / y[p] - gYs[j * K + p]) - ra;
+      }
+#pragma unroll
+      for (int p = 0; p < K; ++p)
+#pragma unroll
+        for (int c = 0; c < K; ++c) L[p][c] = (c <= p) ? XtXs[p * K + c] : 0.0;
+#pragma unroll
+      for (int p = 0; p < K; ++p) L[p][p] += a.rho + Ss[j * K + p] / y[p];
+      if (!reg_chol<K>(L)) badD = min(badD, (int)j);
+      double Li[K][K];
+      reg_inv_lower<K>(L, Li);
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        if (cta == 0) {
+#pragma unroll
+          for (int c = 0; c < K; ++c) a.LD[(j * K + p) * K + c] = (c <= p) ? L[p][c] : 0.0;
+        }
+#pragma unroll
+        for (int c = p; c < K; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if (q >= c) s = fma(Li[q][p], Li[q][c], s);
+          dinv[j * KK + (p * K - p * (p - 1) / 2 + (c - p))] = s;
+        }
+      }
+      reg_solve<K>(L, rhs, tv);
+#pragma unroll
+      for (int p = 0; p < K; ++p) Ts[j * K + p] = tv[p];
+    }
+    {
+      double v[1] = {(double)badD};
+      block_reduce_all<1, 1, 0>(v, red);
+      badD = (int)v[0];
+    }
+    STAMP(4);
+    // G = sum_j (y_j y_j^T) (x) D_j^{-1} (packed), u = U^T t
+    {
+      constexpr int NE = KK * KK + Q, EPW = (NE + NW - 1) / NW;
+      int o1[EPW], o2[EPW], o3[EPW];
+      double sacc[EPW];
+#pragma unroll
+      for (int i = 0; i < EPW; ++i) {
+        const int e = wid + NW * i;
+        sacc[i] = 0.0;
+        if (e < KK * KK) {
+          const int ab = e / KK, pq = e % KK;
+          o1[i] = ia[ab];
+          o2[i] = ic[ab];
+          o3[i] = pq;
+        } else {
+          const int qq = e - KK * KK;
+          o1[i] = qq / K;
+          o2[i] = qq % K;
+          o3[i] = -1;
+        }
+      }
+      #pragma unroll 1
+      for (long j = lane; j < m; j += 32) {
+#pragma unroll
+        for (int i = 0; i < EPW; ++i) {
+          const int e = wid + NW * i;
+          if (e < KK * KK) {
+            const double yy = Ys[j * K + o1[i]] * Ys[j * K + o2[i]];
+            sacc[i] = fma(yy, dinv[j * KK + o3[i]], sacc[i]);
+          } else if (e < NE) {
+            sacc[i] = fma(Ys[j * K + o1[i]], Ts[j * K + o2[i]], sacc[i]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < EPW; ++i) {
+        const int e = wid + NW * i;
+        const double v = warp_sum(sacc[i]);
+        if (lane == 0) {
+          if (e < KK * KK)
+            T1[e] = v;
+          else if (e < NE)
+            u[e - KK * KK] = v;
+        }
+      }
+    }
+    __syncthreads();
+    STAMP(18);
+    #pragma unroll 1
+    for (int e = tid; e < Q * Q; e += PT) {
+      const int r = e / Q, c = e % Q;
+      const int p = r / K, q = r % K, b = c / K, d = c % K;
+      const int pb_ = pk(p, b, K), qd = pk(q, d, K);
+      Gm[e] = T1[pb_ * KK + qd];
+      Zbm[e] = Zs[pb_ * KK + qd];
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int f = warp_chol<Q>(Gm, dGi);
+      if (tid == 0) s_fail = f;
+    }
+    __syncthreads();
+    STAMP(19);
+    #pragma unroll 1
+    for (int e = tid; e < Q * Q; e += PT) {
+      const int r = e / Q, c = e % Q;
+      double s = 0.0;
+      for (int q = c; q < Q; ++q) s = fma(Zbm[r * Q + q], Gm[q * Q + c], s);
+      T1[e] = s;
+    }
+    __syncthreads();
+    STAMP(20);
+    #pragma unroll 1
+    for (int e = tid; e < Q * Q; e += PT) {
+      const int r = e / Q, c = e % Q;
+      double s = 0.0;
+      for (int q = r; q < Q; ++q) s = fma(Gm[q * Q + r], T1[q * Q + c], s);
+      Hm[e] = (r == c ? 1.0 : 0.0) - s;
+    }
+    __syncthreads();
+    STAMP(21);
+    if (tid < 32) {
+      const int f = warp_chol<Q>(Hm, dHi);
+      if (tid == 0 && s_fail < 0) s_fail = f;
+    }
+    __syncthreads();
+    STAMP(22);
+    if (cta == 0)
+      #pragma unroll 1
+      for (int e = tid; e < Q * Q; e += PT) {
+        a.LG[e] = Gm[e];
+        a.LH[e] = Hm[e];
+        a.Zb[e] = Zbm[e];
+      }
+    if (s_fail >= 0 || badD != 0x7F7F7F7F) {
+      if (cta == 0 && tid == 0) {
+        a.fcodes[1] = s_fail;
+        a.fcodes[2] = badD;
+      }
+      status = 1;
+      break;
+    }
+    STAMP(23);
+    // w = LG^{-T} LH^{-T} LH^{-1} LG^T Zb u: warp 0, lane = row; the triangular
+    // solves go column by column (one division + one shuffle per step)
+    if (tid < 32) {
+      const int r = tid;
+      double v = 0.0;
+      if (r < Q)
+        for (int c = 0; c < Q; ++c) v = fma(Zbm[r * Q + c], u[c], v);
+      if (r < Q) w[r] = v;
+      __syncwarp();
+      double acc = 0.0;
+      if (r < Q)
+        for (int q = r; q < Q; ++q) acc = fma(Gm[q * Q + r], w[q], acc);
+      double z = 0.0;
+      for (int j = 0; j < Q; ++j) {  // LH z = LG^T Zb u
+        double zj = (r == j) ? acc * dHi[j] : 0.0;
+        zj = __shfl_sync(0xffffffffu, zj, j);
+        if (r == j) z = zj;
+        if (r > j && r < Q) acc -= Hm[r * Q + j] * zj;
+      }
+      acc = z;
+      for (int j = Q - 1; j >= 0; --j) {  // LH^T z2 = z
+        double zj = (r == j) ? acc * dHi[j] : 0.0;
+        zj = __shfl_sync(0xffffffffu, zj, j);
+        if (r == j) z = zj;
+        if (r < j) acc -= Hm[j * Q + r] * zj;
+      }
+      acc = z;
+      for (int j = Q - 1; j >= 0; --j) {  // LG^T w = z2
+        double zj = (r == j) ? acc * dGi[j] : 0.0;
+        zj = __shfl_sync(0xffffffffu, zj, j);
+        if (r == j) z = zj;
+        if (r < j) acc -= Gm[j * Q + r] * zj;
+      }
+      __syncwarp();
+      if (r < Q) w[r] = z;
+    }
+    __syncthreads();
+    STAMP(5);
+    // dY_j = t_j + D_j^{-1}(W^T y_j); Y-side scalars
+    {
+      double v[3] = {0.0, 1.0 / 0.0, 1.0 / 0.0};
+      #pragma unroll 1
+      for (long j = tid; j < m; j += PT) {
+        double rv[K], out[K], y[K];
+#pragma unroll
+        for (int p = 0; p < K; ++p) y[p] = Ys[j * K + p];
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < K; ++c) s = fma(y[c], w[c * K + p], s);
+          rv[p] = s;
+        }
+#pragma unroll
+        for (int p = 0; p < K; ++p) {  // D_j^{-1} (W^T y_j) with the packed inverse
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < K; ++c) s = fma(dinv[j * KK + pk(p, c, K)], rv[c], s);
+          out[p] = s;
+        }
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const double d = Ts[j * K + p] + out[p];
+          Ts[j * K + p] = d;
+          const double s = Ss[j * K + p];
+          const double ds = muy / y[p] - s - (s / y[p]) * d;
+          v[0] = fma(d, gYs[j * K + p] - muy / y[p], v[0]);
+          if (d < 0.0) v[1] = fmin(v[1], -a.tau * y[p] / d);
+          if (ds < 0.0) v[2] = fmin(v[2], -a.tau * s / ds);
+        }
+      }
+      block_reduce_all<3, 0x6, 0>(v, red);
+      if (tid == 0) {
+        scal[0] = v[0];
+        scal[1] = v[1];
+        scal[2] = v[2];
+      }
+    }
+    #pragma unroll 1
+    for (int e = wid; e < K * K; e += NW) {  // Gdy = sum_j y_j dy_j^T
+      const int p = e / K, c = e % K;
+      double s = 0.0;
+      #pragma unroll 1
+      for (long j = lane; j < m; j += 32) s = fma(Ys[j * K + p], Ts[j * K + c], s);
+      s = warp_sum(s);
+      if (lane == 0) Gdy[e] = s;
+    }
+    __syncthreads();
+    STAMP(6);
+    // ---- rows: dX, dR (back substitution), X-side scalars
+    double pb[9] = {0.0, 1.0 / 0.0, 1.0 / 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    #pragma unroll 1
+    for (int rr = tid; rr < nr; rr += PT) {
+      double L[K][K], v[K], q[K], t[K], dx[K], x[K];
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        x[p] = xs[rr * K + p];
+#pragma unroll
+        for (int c = 0; c < K; ++c) L[p][c] = Ls[(rr * K + p) * K + c];
+      }
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < K; ++b) s = fma(Gdy[p * K + b], x[b], s);
+        v[p] = s;
+      }
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        double s = v[p];
+#pragma unroll
+        for (int c = 0; c < p; ++c) s -= L[p][c] * q[c];
+        q[p] = s / L[p][p];
+      }
+#pragma unroll
+      for (int p = 0; p < K; ++p) t[p] = hs[rr * K + p] - q[p];
+#pragma unroll
+      for (int p = K - 1; p >= 0; --p) {
+        double s = t[p];
+#pragma unroll
+        for (int c = p + 1; c < K; ++c) s -= L[c][p] * dx[c];
+        dx[p] = s / L[p][p];
+      }
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        const double r = rs[rr * K + p], d = dx[p];
+        const double dr = mux / x[p] - r - (r / x[p]) * d;
+        dxs[rr * K + p] = d;
+        drs[rr * K + p] = dr;
+        pb[0] = fma(d, gxs[rr * K + p] - mux / x[p], pb[0]);
+        if (d < 0.0) pb[1] = fmin(pb[1], -a.tau * x[p] / d);
+        if (dr < 0.0) pb[2] = fmin(pb[2], -a.tau * r / dr);
+      }
+    }
+    __syncthreads();
+    STAMP(7);
+    // ---- quartic partials over own rows x all columns (F recomputed from M)
+    #pragma unroll 1
+    for (long e = tid; e < (long)nr * m; e += PT) {
+      const int rr = (int)(e / m);
+      const long j = e - (long)rr * m;
+      double fv = -Mp[(long)rr * m + j];
+#pragma unroll
+      for (int p = 0; p < K; ++p) fv = fma(xs[rr * K + p], Ys[j * K + p], fv);
+      double bv = 0.0, cv = 0.0;
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        const double x = xs[rr * K + p], dx = dxs[rr * K + p];
+        const double y = Ys[j * K + p], dy = Ts[j * K + p];
+        bv = fma(dx, y, fma(x, dy, bv));
+        cv = fma(dx, dy, cv);
+      }
+      pb[3] = fma(fv, fv, pb[3]);
+      pb[4] = fma(fv, bv, pb[4]);
+      pb[5] = fma(bv, bv, pb[5]);
+      pb[6] = fma(fv, cv, pb[6]);
+      pb[7] = fma(bv, cv, pb[7]);
+      pb[8] = fma(cv, cv, pb[8]);
+    }
+    {
+      block_reduce_all<9, 0x6, 0>(pb, red);
+#pragma unroll
+      for (int q = 0; q < 9; ++q)
+        if (tid == q) __stcg(PB + (long)q * G + cta, pb[q]);
+    }
+    STAMP(8);
+    grid_barrier(a.bar, epoch);
+    STAMP(9);
+
+    // ======== phase C: Armijo (quartic + barrier trials in batches) ========
+    // [3] gtp_x [4] a1x [5] a2x [6..11] quartic
+    reduce_entries<2, 1>(PB, G, 1, 3, scal + 4);
+    reduce_entries<1, 0>(PB, G, 0, 1, scal + 3);
+    reduce_entries<1, 0>(PB, G, 3, 9, scal + 6);
+    __syncthreads();
+    const double gtp = scal[3] + scal[0];
+    const double a1max = fmin(fmin(1.0, scal[4]), scal[1]);
+    const double a2max = fmin(fmin(1.0, scal[5]), scal[2]);
+    const double ab = scal[7], bb = scal[8], ac = scal[9], bc = scal[10], cc = scal[11];
+    int tsel = -1;
+    for (int batch = 0;; ++batch) {
+      const int t0 = batch * TB;
+      // warp q = trial t0 + q; lanes stride this CTA's x entries and its slice of y.
+      // (2^-t a1max num) / den == 2^-t ((a1max num) / den) exactly, so one division
+      // per entry gives the oracle's (alpha dv) / v bit for bit.
+      const int tq = t0 + wid;
+      double ax = 0.0, ay = 0.0;
+      if (tq < a.ntrials) {
+        #pragma unroll 1
+        for (long e = lane; e < (long)nr * K; e += 32)
+          ax += log1p(ldexp((a1max * dxs[e]) / xs[e], -tq));
+        const long y0 = (long)cta * N / G, y1 = (long)(cta + 1) * N / G;
+        #pragma unroll 1
+        for (long e = y0 + lane; e < y1; e += 32) ay += log1p(ldexp((a1max * Ts[e]) / Ys[e], -tq));
+      }
+      ax = warp_sum(ax);
+      ay = warp_sum(ay);
+      double* pc = PC + (long)(batch & 1) * G * 2 * TB;
+      if (lane == 0) {
+        __stcg(pc + (long)(2 * wid) * G + cta, ax);
+        __stcg(pc + (long)(2 * wid + 1) * G + cta, ay);
+      }
+      STAMP(10);
+      grid_barrier(a.bar, epoch);
+      reduce_entries<2, 0>(pc, G, 0, 2 * TB, bars);
+      __syncthreads();
+      if (tid == 0) {
+        // same arithmetic as armijo_pick (csrc/small.cu) / the host loop
+        const double c2 = __dadd_rn(__dmul_rn(0.5, bb), ac);
+        int t = t0, res = -1;
+        for (; t < t0 + TB; ++t) {
+          if (t > a.max_bt) {
+            res = -3;  // stall
+            break;
+          }
+          const double a1 = ldexp(a1max, -t);  // == a1max / 2^t exactly
+          const double q2 = __dmul_rn(a1, a1), q3 = __dmul_rn(q2, a1), q4 = __dmul_rn(q3, a1);
+          double quad = __dadd_rn(__dmul_rn(a1, ab), __dmul_rn(q2, c2));
+          quad = __dadd_rn(quad, __dmul_rn(q3, bc));
+          quad = __dadd_rn(quad, __dmul_rn(__dmul_rn(0.5, q4), cc));
+          const double bar = __dadd_rn(__dmul_rn(a.wx, bars[2 * (t - t0)]),
+                                       __dmul_rn(a.wy, bars[2 * (t - t0) + 1]));
+          const double dphi = __dsub_rn(quad, __dmul_rn(a.mu, bar));
+          if (dphi <= __dmul_rn(__dmul_rn(a.eta, a1), gtp)) {
+            res = t;
+            break;
+          }
+        }
+        s_t = (res == -1 && t > a.max_bt) ? -3 : res;
+      }
+      __syncthreads();
+      tsel = s_t;
+      if (tsel != -1) break;
+    }
+    if (tsel == -3) {
+      if (cta == 0 && tid == 0) {
+        double* rec = a.logv + (long)it * LOGW;
+        rec[0] = (double)(a.max_bt + 1);
+        rec[1] = 0.0;
+        rec[2] = 0.0;
+      }
+      status = 2;
+      break;
+    }
+    STAMP(11);
+    const double a1 = ldexp(a1max, -tsel);
+    const double a2 = a2max;
+
+    // ======== phase D: update, residual, graX, graY / KKT / ||F||^2 partials ====
+    #pragma unroll 1
+    for (long e = tid; e < N; e += PT) {
+      const double y = Ys[e], s = Ss[e], d = Ts[e];
+      const double ds = muy / y - s - (s / y) * d;
+      Ys[e] = nudge(y, d, a1, a.tau);
+      Ss[e] = nudge(s, ds, a2, a.tau);
+    }
+    #pragma unroll 1
+    for (long e = tid; e < (long)nr * K; e += PT) {
+      xs[e] = nudge(xs[e], dxs[e], a1, a.tau);
+      rs[e] = nudge(rs[e], drs[e], a2, a.tau);
+    }
+    __syncthreads();
+    double kv[7] = {0.0, 0.0, 0.0, 0.0, 0.0, -1.0 / 0.0, -1.0 / 0.0};  // fsq, k0..k3, kg, kx
+    #pragma unroll 1
+    for (int rr = wid; rr < nr; rr += NW) {
+      const long i = r0 + rr;
+      double x[K], g[K];
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        x[p] = xs[rr * K + p];
+        g[p] = 0.0;
+      }
+      #pragma unroll 1
+      for (long j = lane; j < m; j += 32) {
+        double fv = -Mp[(long)rr * m + j];
+#pragma unroll
+        for (int p = 0; p < K; ++p) fv = fma(x[p], Ys[j * K + p], fv);
+        a.Fout[i * m + j] = fv;
+        kv[0] = fma(fv, fv, kv[0]);
+#pragma unroll
+        for (int p = 0; p < K; ++p) g[p] = fma(fv, Ys[j * K + p], g[p]);
+      }
+#pragma unroll
+      for (int p = 0; p < K; ++p) g[p] = warp_sum(g[p]);
+      if (lane == 0) {
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          gxs[rr * K + p] = g[p];
+          const double r = rs[rr * K + p];
+          const double xr = x[p] * r;
+          kv[1] = fma(g[p] - r, g[p] - r, kv[1]);
+          kv[2] = fma(xr - mux, xr - mux, kv[2]);
+          kv[3] = fma(xr, xr, kv[3]);
+          kv[4] += xr;
+          kv[5] = fmax(kv[5], fabs(g[p]));
+          kv[6] = fmax(kv[6], x[p]);
+        }
+      }
+    }
+    #pragma unroll 1
+    for (long j = tid; j < m; j += PT) {
+      double acc[K];
+#pragma unroll
+      for (int p = 0; p < K; ++p) acc[p] = 0.0;
+      #pragma unroll 1
+      for (int rr = 0; rr < nr; ++rr) {
+        double fv = -Mp[(long)rr * m + j];
+#pragma unroll
+        for (int p = 0; p < K; ++p) fv = fma(xs[rr * K + p], Ys[j * K + p], fv);
+#pragma unroll
+        for (int p = 0; p < K; ++p) acc[p] = fma(fv, xs[rr * K + p], acc[p]);
+      }
+#pragma unroll
+      for (int p = 0; p < K; ++p) __stcg(PG + (j * K + p) * G + cta, acc[p]);
+    }
+    {
+      block_reduce_all<7, 0, 0x60>(kv, red);
+#pragma unroll
+      for (int q = 0; q < 7; ++q)
+        if (tid == q) __stcg(PD + (long)q * G + cta, kv[q]);
+    }
+    if (cta == 0 && tid == 0) {
+      double* rec = a.logv + (long)it * LOGW;
+      unsigned long long tns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+      rec[0] = (double)tsel;
+      rec[1] = a1;
+      rec[2] = a2;
+      rec[6] = (double)tns;
+    }
+    STAMP(12);
+    grid_barrier(a.bar, epoch);
+    STAMP(13);
+
+    // ======== phase E: graY slice totals; X-part KKT sums and ||F||^2 ========
+    {
+      const long e0 = (long)cta * N / G, e1 = (long)(cta + 1) * N / G;
+      reduce_entries<2, 0>(PG, G, e0, e1, a.gY + e0, true);
+      reduce_entries<1, 0>(PD, G, 0, 5, kx);
+      reduce_entries<1, 2>(PD, G, 5, 7, kx + 5);
+    }
+    STAMP(14);
+    ++it;
+    // the barrier after the next phase A publishes graY
+  }
+
+  // ---- write the state back ----------------------------------------------------
+  __syncthreads();
+  #pragma unroll 1
+  for (long e = tid; e < (long)nr * K; e += PT) {
+    a.X[r0 * K + e] = xs[e];
+    a.R[r0 * K + e] = rs[e];
+    a.gX[r0 * K + e] = gxs[e];
+  }
+  if (cta == 0) {
+    #pragma unroll 1
+    for (long e = tid; e < N; e += PT) {
+      a.Yt[e] = Ys[e];
+      a.S[e] = Ss[e];
+    }
+    if (tid == 0) {
+      a.status[0] = it;
+      a.status[1] = status;
+    }
+  }
+}
+
+template <int K>
+long p_smem_bytes(long n, long m, int G, bool with_m) {
+  const long nrm = (n + G - 1) / G;
+  return smem_doubles<K>(nrm, m, with_m) * (long)sizeof(double);
+}
+
+constexpr long SMEM_CAP = 200 * 1024;  // dynamic part; the static part is < 16 KB
+
+int p_grid(long n) {
+  long g = (n + 15) / 16;
+  if (g > 148) g = 148;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace
+
+#define NMFB_PK(k, MACRO)               \
+  switch (k) {                          \
+    MACRO(1) MACRO(2) MACRO(3) MACRO(4) \
+    default: return 0;                  \
+  }
+
+extern "C" int nmfb_persist_supported(long n, long m, long k, int grid) {
+  if (k < 1 || k > 4 || m < 1 || n < 1 || m * k > 2048) return 0;
+  const int G = grid > 0 ? grid : p_grid(n);
+  if ((n + G - 1) / G > 4096) return 0;
+#define CASE(KK_) \
+  case KK_: return p_smem_bytes<KK_>(n, m, G, false) <= SMEM_CAP ? 1 : 0;
+  NMFB_PK(k, CASE)
+#undef CASE
+}
+
+extern "C" long nmfb_persist_work_len(long n, long m, long k, int grid) {
+  const int G = grid > 0 ? grid : p_grid(n);
+  return wlayout(G, m, (int)k).total;
+}
+
+// One cooperative launch = the Gauss-Newton inner loop (see the file header).
+// log: max_iters x 8 doubles [t, alpha1, alpha2, ||F||^2, E_mu, E_0, globaltimer ns, -];
+// status (device int[2]): [iterations done, exit code].
+extern "C" int nmfb_ipm_persist(const void* M, int m_is_f32, long n, long m, long k, double* X,
+                                double* R, double* gX, double* Yt, double* S, double* gY,
+                                double* Fout, double* L, double* Xf, double* Ytf, double* LD,
+                                double* LG, double* LH, double* Zb, double mu, double wx,
+                                double wy, double rho, double tau, double eta, double eps_mu,
+                                int max_bt, int ntrials, int max_iters, double* sc, int* fcodes,
+                                double* logv, int* status, double* work, unsigned int* bar,
+                                int grid, long long* prof, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!nmfb_persist_supported(n, m, k, grid)) return NMFB_EUNSUPPORTED;
+  if (max_iters < 1) return NMFB_EINVAL;
+  const int G = grid > 0 ? grid : p_grid(n);
+  PArgs a;
+  a.M = M;
+  a.n = n;
+  a.m = m;
+  a.X = X;
+  a.R = R;
+  a.gX = gX;
+  a.Yt = Yt;
+  a.S = S;
+  a.gY = gY;
+  a.Fout = Fout;
+  a.L = L;
+  a.Xf = Xf;
+  a.Ytf = Ytf;
+  a.LD = LD;
+  a.LG = LG;
+  a.LH = LH;
+  a.Zb = Zb;
+  a.sc = sc;
+  a.logv = logv;
+  a.work = work;
+  a.fcodes = fcodes;
+  a.status = status;
+  a.bar = bar;
+  a.mu = mu;
+  a.wx = wx;
+  a.wy = wy;
+  a.rho = rho;
+  a.tau = tau;
+  a.eta = eta;
+  a.eps_mu = eps_mu;
+  a.max_bt = max_bt;
+  a.ntrials = ntrials;
+  a.max_iters = max_iters;
+  a.prof = prof;
+  cudaMemsetAsync(bar, 0, (size_t)G * sizeof(unsigned int), st);
+  void* args[] = {&a};
+  cudaError_t err = cudaSuccess;
+#define LAUNCH(KK_, T_)                                                                        \
+  {                                                                                            \
+    const bool wm = p_smem_bytes<KK_>(n, m, G, true) <= SMEM_CAP;                             \
+    if (!wm && m_is_f32) return NMFB_EUNSUPPORTED;                                            \
+    a.m_in_smem = wm ? 1 : 0;                                                                  \
+    const long bytes = p_smem_bytes<KK_>(n, m, G, wm);                                        \
+    cudaFuncSetAttribute(k_ipm_persist<KK_, T_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)bytes);                                                          \
+    ++g_nmfb_launches;                                                                         \
+    err = cudaLaunchCooperativeKernel((const void*)k_ipm_persist<KK_, T_>, dim3(G), dim3(PT), \
+                                      args, (size_t)bytes, st);                                \
+  }
+#define CASE(KK_)            \
+  case KK_:                  \
+    if (m_is_f32)            \
+      LAUNCH(KK_, float)     \
+    else                     \
+      LAUNCH(KK_, double)    \
+    break;
+  switch (k) {
+    CASE(1) CASE(2) CASE(3) CASE(4)
+    default: return NMFB_EUNSUPPORTED;
+  }
+#undef CASE
+#undef LAUNCH
+  if (err != cudaSuccess) return NMFB_ELAUNCH;
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}

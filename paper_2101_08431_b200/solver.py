@@ -66,6 +66,9 @@ class Problem:
         self.event_times = []  # resolved durations (ms) of instrumented launches in graphs
         self.graph_timing_failed = False
         self.graph_kernel_launches = 0  # library kernels executed inside replayed graphs
+        self.persist_iters = 0  # IPM iterations run inside persistent launches
+        self.persist_seconds = 0.0
+        self.persist_prof = None  # optional int64 (4096, 16) phase clocks (scripts/)
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         if isinstance(M, np.ndarray):
             if M.dtype not in (np.float64, np.float32):
@@ -355,6 +358,15 @@ class IpmEngine:
         if self.small:
             self.swork = b(max(P.lib.nmfb_small_work_len(n, m, k), 1))
             self.tickets = torch.zeros(8, dtype=torch.int32, device=P.dev)
+        # persistent inner loop (csrc/persist.cu): one cooperative launch per inner loop
+        self.persist = self.small and p.persistent and \
+            bool(P.lib.nmfb_persist_supported(n, m, k, p.persist_grid))
+        if self.persist:
+            self.pwork = b(P.lib.nmfb_persist_work_len(n, m, k, p.persist_grid))
+            self.pbar = torch.zeros(160, dtype=torch.int32, device=P.dev)  # barrier flags
+            self.pstat = torch.zeros(2, dtype=torch.int32, device=P.dev)
+            self.pfc0 = torch.tensor([_NONE, -1, _NONE], dtype=torch.int32, device=P.dev)
+            self.plog = None
         self.Pbuf = None
         self.W = None
         aw = max(P.lib.nmfb_atb_work_len(n, self.kk, self.kk),
@@ -452,6 +464,55 @@ class IpmEngine:
         self.fact_F, self.have_fact, self.fact_full, self.fact_dense = state[0], True, False, False
         self.last_dense = False
         self.fi = state[0] ^ 1
+
+    def persist_run(self, eps_mu, budget, res, t0):
+        """Run the Gauss-Newton inner loop in one cooperative launch (csrc/persist.cu).
+
+        Appends the iterations to ``res`` and returns (exit code, E_mu, E_0, fsq, sums):
+        code 0 = inner loop finished (E(.;mu) <= eps_mu or the budget), 1 = a
+        factorization failed at the current point (no step taken), 2 = Armijo stall."""
+        P, p = self.P, self.p
+        n, m, k = self.n, self.m, self.k
+        if self.plog is None or self.plog.shape[0] < budget:
+            self.plog = P.buf(budget, 8)
+        P.iscal[2:5].copy_(self.pfc0)
+        fout = self.F[self.fi ^ 1]
+        h0 = time.perf_counter()
+        P._call("nmfb_ipm_persist", _p(P.M), P.f32, n, m, k, _p(self.X), _p(self.R),
+                _p(self.gX), _p(self.Yt), _p(self.S), _p(self.gY), _p(fout), _p(self.L),
+                _p(self.Xf), _p(self.Ytf), _p(self.LD), _p(self.LG), _p(self.LH),
+                _p(self.lrwork), self.mu, self.wx, self.wy, self.rho, p.tau, p.eta, eps_mu,
+                p.max_backtracks, NTRIALS, budget, _p(P.dscal), _p(P.iscal[2:]), _p(self.plog),
+                _p(self.pstat), _p(self.pwork), _p(self.pbar), p.persist_grid,
+                _p(P.persist_prof) if P.persist_prof is not None else None, P.stream,
+                tag="persist")
+        st = self.pstat.cpu().numpy()
+        iters, code = int(st[0]), int(st[1])
+        nrec = iters + (1 if code == 2 else 0)
+        log = self.plog[:nrec].cpu().numpy() if nrec else np.zeros((0, 8))
+        v, iv = P.readback(28, 5)
+        h1 = time.perf_counter()
+        P.persist_iters += iters
+        if iters:
+            ns_last = log[iters - 1, 6]
+            for i in range(iters):
+                ti = (h1 - t0) - (ns_last - log[i, 6]) * 1e-9
+                res.trace.append((ti, 0.5 * log[i, 3], log[i, 5], self.mu, log[i, 1], log[i, 2],
+                                  int(log[i, 0])))
+                res.armijo_t.append(int(log[i, 0]))
+                res.flags.append(False)
+            res.iters += iters
+            # the kernel left F at the current point in F[fi ^ 1] and the last
+            # Gauss-Newton factorization (L, Xf, Ytf, LD, LG, LH, Zb) for the predictor
+            self.fact_F = self.fi
+            self.fi ^= 1
+            self.have_fact, self.fact_full, self.fact_dense = True, False, False
+            self.last_dense = False
+        if code == 2:
+            res.armijo_t.append(int(log[nrec - 1, 0]))
+        e_mu, e_zero = kkt_from_sums(v[16:28])
+        P.persist_seconds += h1 - h0
+        return code, iters, (e_mu, e_zero, v[0], v[16:28])
 
     def _ensure_full_buffers(self):
         if self.Pbuf is None:
@@ -672,7 +733,21 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                 else:
                     eng.flag = False
             force_dense = False
-            if not ok and eng.use_graphs:
+            if not ok and eng.persist:
+                code, done, kkt = eng.persist_run(eps_mu, cap - res.iters, res, t0)
+                if done:
+                    e_mu, e_zero, fsq, sums = kkt
+                if code == 2:
+                    raise LineSearchStall(f"Armijo backtracking exceeded {p.max_backtracks}")
+                if code == 0:
+                    continue
+                # a factorization failed at the current point (no step was taken):
+                # redo this iteration eagerly with the dense Schur solve
+                force_dense = True
+                res.dense_fallbacks += 1
+            if force_dense:
+                pass
+            elif not ok and eng.use_graphs:
                 eng.gn_iteration_graph()
                 v, iv = P.readback(28, 5)
                 for e0, e1 in eng.graphs[eng.last_graph][1]:

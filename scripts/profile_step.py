@@ -18,4 +18,6 @@ for rep in range(2):
     X, Yt, R, S, mu, rho = solver.transition(P, X, Yt, 1e-7)
     eng, r2 = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(fixed_iters=iters))
     torch.cuda.synchronize()
-    print("rep", rep, "launches", P.lib.nmfb_launch_count(), "sweeps", r1.sweeps, "ipm", r2.iters)
+    print("rep", rep, "launches", P.lib.nmfb_launch_count(), "sweeps", r1.sweeps, "ipm", r2.iters,
+          "stage1_s %.5f ipm_s %.5f per_iter_ms %.4f" % (r1.seconds, r2.seconds,
+                                                         1e3 * r2.seconds / max(1, r2.iters)))

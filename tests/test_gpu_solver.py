@@ -99,6 +99,47 @@ def test_ipm_parity(mods, name, barrier, iters, eps, solve, resid):
         assert any(r.flags), "the full-Hessian path was not exercised"
 
 
+@pytest.mark.parametrize("name,barrier,iters,eps,path", [
+    ("c1", "paper", 40, 1e-7, "graph"), ("c1", "balanced", 50, 1e-5, "graph"),
+    ("c2", "balanced", 35, 1e-6, "graph"), ("c1", "balanced", 50, 1e-5, "eager"),
+    ("c2", "balanced", 35, 1e-6, "persist-g16"), ("c2", "paper", 40, 1e-6, "persist-g148"),
+    ("c1", "balanced", 60, 1e-7, "persist-g7")])
+def test_ipm_parity_paths(mods, name, barrier, iters, eps, path):
+    """The same Gauss-Newton iterations through each device path: the persistent
+    cooperative loop (csrc/persist.cu, several grid sizes), the graph-replayed six
+    kernels (csrc/small.cu) and the eager general pipeline (csrc/ipm.cu + lowrank.cu)."""
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = _instance(data, name)
+    k = X0.shape[1]
+    ro = D.run_stage1(M, X0, Y0.T.copy())
+    st = D.transition(ro.X, ro.Yt, M, eps)
+    P = solver.Problem(M, k)
+    X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), eps)
+    kw = dict(fixed_iters=iters, barrier=barrier)
+    if path == "graph":
+        kw.update(persistent=False)
+    elif path == "eager":
+        kw.update(persistent=False, fused_small=False, use_graphs=False)
+    else:
+        kw.update(persist_grid=int(path.split("-g")[1]))
+    eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(**kw))
+    if path.startswith("persist"):
+        assert P.persist_iters > 0
+    else:
+        assert P.persist_iters == 0
+    D.set_schur_backend("numpy")
+    try:
+        ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=iters, barrier=barrier))
+    finally:
+        D.set_schur_backend("c")
+    assert r.iters == ro2.iters and r.outer == ro2.outer
+    assert r.armijo_t == ro2.armijo_t
+    assert r.flags == ro2.flags
+    for a, b in ((eng.X, ro2.state.X), (eng.Yt, ro2.state.Yt)):
+        assert rel(a.cpu().numpy(), b) < TOL_IPM
+    assert abs(eng.mu - ro2.state.mu) <= TOL_IPM * ro2.state.mu
+
+
 def test_two_stage_c1(mods):
     data, solver, IpmParams, Stage1Config = mods
     M, X0, Y0 = _instance(data, "c1")
