@@ -11,7 +11,7 @@ import os
 from .errors import NativeLibraryError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libnmfb200.so")
+SO_PATH = os.environ.get("NMFB_SO") or os.path.join(_HERE, "libnmfb200.so")  # NMFB_SO: A/B builds
 
 P = ctypes.c_void_p
 L = ctypes.c_long

@@ -49,10 +49,12 @@ struct PArgs {
   long long* prof;  // optional per-iteration phase clocks of CTA 0 (16 per iteration)
 };
 
-#define STAMP(i)                                                       \
-  do {                                                                 \
-    if (a.prof && blockIdx.x == 0 && threadIdx.x == 0 && it < 4096)    \
-      a.prof[(long)it * 32 + (i)] = clock64();                         \
+// all lanes of warp 0 store the same stamp: no intra-warp divergence (a lane-0-only
+// store left the warp diverged at the next shuffles and distorted what it measured)
+#define STAMP(i)                                                            \
+  do {                                                                      \
+    if (a.prof && blockIdx.x == 0 && threadIdx.x < 32 && it < 4096)         \
+      a.prof[(long)it * 40 + (i)] = clock64();                              \
   } while (0)
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -118,6 +120,7 @@ __device__ __forceinline__ void reduce_entries(const double* part, int G, long e
         const int c = lane + 32 * u;
         v[b][u] = (eb + b < e1 && c < G) ? ldcg(part + (eb + b) * G + c) : op_id<KD>();
       }
+    __syncwarp();
 #pragma unroll
     for (int b = 0; b < EB; ++b) {
       double s = v[b][0];
@@ -144,7 +147,8 @@ template <int J, int C, int Q>
 struct CholUpd {
   static __device__ __forceinline__ void run(double (&a)[Q], int r) {
     const double lcj = __shfl_sync(0xffffffffu, a[J], C);
-    if (r >= C) a[C] -= a[J] * lcj;
+    const double upd = a[C] - a[J] * lcj;
+    a[C] = (r >= C) ? upd : a[C];
     CholUpd<J, C + 1, Q>::run(a, r);
   }
 };
@@ -159,12 +163,9 @@ struct CholStep {
     if (fail < 0 && !(pv > 0.0)) fail = J;  // continue on a dummy pivot after a failure
     if (fail >= 0) pv = 1.0;
     const double di = rsqrt(pv);
-    if (r == J) {
-      a[J] = pv * di;
-      di_r = di;
-    } else if (r > J) {
-      a[J] = a[J] * di;
-    }
+    // selects, not branches: the warp stays converged for the shuffles
+    a[J] = (r == J) ? pv * di : ((r > J) ? a[J] * di : a[J]);
+    di_r = (r == J) ? di : di_r;
     CholUpd<J, J + 1, Q>::run(a, r);
     CholStep<J + 1, Q>::run(a, r, fail, di_r);
   }
@@ -177,6 +178,7 @@ struct CholStep<Q, Q> {
 template <int Q>
 __device__ __forceinline__ int warp_chol(double* A, double* dinv) {
   const int r = threadIdx.x & 31;
+  __syncwarp();
   double a[Q];
 #pragma unroll
   for (int c = 0; c < Q; ++c) a[c] = (r < Q) ? A[r * Q + c] : 0.0;
@@ -217,6 +219,7 @@ struct BlockRed<NV, NV, MINM, MAXM> {
 template <int NV, int MINM = 0, int MAXM = 0>
 __device__ __forceinline__ void block_reduce_all(double (&v)[NV], double* sh /* NV * NW */) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncwarp();
   BlockRed<0, NV, MINM, MAXM>::warp_part(v);
   __syncthreads();
   if (lane == 0) {
@@ -690,7 +693,9 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     }
     __syncthreads();
     if (tid < 32) {
+      STAMP(24);
       const int f = warp_chol<Q>(Gm, dGi);
+      STAMP(25);
       if (tid == 0) s_fail = f;
     }
     __syncthreads();
@@ -714,7 +719,9 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     __syncthreads();
     STAMP(21);
     if (tid < 32) {
+      STAMP(26);
       const int f = warp_chol<Q>(Hm, dHi);
+      STAMP(27);
       if (tid == 0 && s_fail < 0) s_fail = f;
     }
     __syncthreads();
@@ -739,6 +746,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     // solves go column by column (one division + one shuffle per step)
     if (tid < 32) {
       const int r = tid;
+      __syncwarp();
       double v = 0.0;
       if (r < Q)
         for (int c = 0; c < Q; ++c) v = fma(Zbm[r * Q + c], u[c], v);
@@ -747,26 +755,35 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
       double acc = 0.0;
       if (r < Q)
         for (int q = r; q < Q; ++q) acc = fma(Gm[q * Q + r], w[q], acc);
+      __syncwarp();
       double z = 0.0;
+      const double hdi = (r < Q) ? dHi[r] : 0.0, gdi = (r < Q) ? dGi[r] : 0.0;
+#pragma unroll 1
       for (int j = 0; j < Q; ++j) {  // LH z = LG^T Zb u
-        double zj = (r == j) ? acc * dHi[j] : 0.0;
-        zj = __shfl_sync(0xffffffffu, zj, j);
-        if (r == j) z = zj;
-        if (r > j && r < Q) acc -= Hm[r * Q + j] * zj;
+        const double zj = __shfl_sync(0xffffffffu, acc * hdi, j);
+        const double hij = (r < Q) ? Hm[r * Q + j] : 0.0;
+        const double nacc = acc - hij * zj;
+        z = (r == j) ? zj : z;
+        acc = (r > j && r < Q) ? nacc : acc;
       }
+      STAMP(28);
       acc = z;
+#pragma unroll 1
       for (int j = Q - 1; j >= 0; --j) {  // LH^T z2 = z
-        double zj = (r == j) ? acc * dHi[j] : 0.0;
-        zj = __shfl_sync(0xffffffffu, zj, j);
-        if (r == j) z = zj;
-        if (r < j) acc -= Hm[j * Q + r] * zj;
+        const double zj = __shfl_sync(0xffffffffu, acc * hdi, j);
+        const double hji = (r < Q) ? Hm[j * Q + r] : 0.0;
+        const double nacc = acc - hji * zj;
+        z = (r == j) ? zj : z;
+        acc = (r < j) ? nacc : acc;
       }
       acc = z;
+#pragma unroll 1
       for (int j = Q - 1; j >= 0; --j) {  // LG^T w = z2
-        double zj = (r == j) ? acc * dGi[j] : 0.0;
-        zj = __shfl_sync(0xffffffffu, zj, j);
-        if (r == j) z = zj;
-        if (r < j) acc -= Gm[j * Q + r] * zj;
+        const double zj = __shfl_sync(0xffffffffu, acc * gdi, j);
+        const double gji = (r < Q) ? Gm[j * Q + r] : 0.0;
+        const double nacc = acc - gji * zj;
+        z = (r == j) ? zj : z;
+        acc = (r < j) ? nacc : acc;
       }
       __syncwarp();
       if (r < Q) w[r] = z;
