@@ -165,9 +165,11 @@ def run_reference(args):
 
 
 def _workload_desc(cfg):
+    from paper_2101_08431_b200.config import IpmParams
+
     return (f"{cfg.name}: two-stage NMF solve, fp64 n={cfg.n} m={cfg.m} k={cfg.k} peak/logistic "
             f"generator, stage 1 to eps_STOL=1e-3 then IPM to relative KKT {cfg.tol:g} "
-            f"(cap {IPM_CAP} IPM iterations, barrier=paper)")
+            f"(cap {IPM_CAP} IPM iterations, barrier={IpmParams().barrier})")
 
 
 # ----------------------------------------------------------------------------

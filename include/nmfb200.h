@@ -251,7 +251,7 @@ unsigned long long nmfb_launch_count(void);
 
 /* Persistent Gauss-Newton inner loop for small problems (csrc/persist.cu): one
  * cooperative launch runs PAPER Alg. 2's inner iterations while
- * E(.;mu) > eps_mu, up to max_iters.  log: max_iters x 8 doubles per iteration
+ * E(.;mu) > eps_mu and E(.;0) > tol0, up to max_iters.  log: max_iters x 8 doubles per iteration
  * [t, alpha1, alpha2, ||F||^2, E_mu, E_0, globaltimer ns, -]; status (device
  * int[2]) = [iterations done, exit code 0 done / 1 factorization failure (no step)
  * / 2 Armijo stall].  fcodes = [R1 failing row, capacitance info, D failing col]
@@ -263,7 +263,7 @@ int nmfb_ipm_persist(const void *M, int m_is_f32, long n, long m, long k, double
                      double *gX, double *Yt, double *S, double *gY, double *Fout, double *L,
                      double *Xf, double *Ytf, double *LD, double *LG, double *LH, double *Zb,
                      double mu, double wx, double wy, double rho, double tau, double eta,
-                     double eps_mu, int max_bt, int ntrials, int max_iters, double *sc,
+                     double eps_mu, double tol0, int max_bt, int ntrials, int max_iters, double *sc,
                      int *fcodes, double *logv, int *status, double *work, unsigned int *bar,
                      int grid, long long *prof, void *stream);
 

@@ -26,6 +26,11 @@ Frozen open semantics (DESIGN.md "Frozen semantics" lists the same items):
 6. E uses Diag(y) for "s^T Diag(Y)".
 7. Nudge: an updated entry that is not strictly positive becomes
    (1 - tau) times its previous value.
+8. Termination: run_ipm stops as soon as E(.;0) <= tol ("terminates when
+   E(.;0) <= eps_TOL"), checked after every inner iteration; the inner loop's own
+   test E(.;mu) <= mu can be unreachable once mu ~ 1e-15.
+9. Barrier weights: default "balanced" (n w_x = m w_y, = the single mu when n = m);
+   "paper" is the literal single-mu reading (see barrier_weights).
 """
 from __future__ import annotations
 
@@ -89,7 +94,7 @@ class IpmParams:
     max_iter: int = 500
     max_backtracks: int = 60
     fixed_iters: int = 0  # >0: run exactly this many inner iterations
-    barrier: str = "paper"  # "paper": one mu (PAPER Eq. 4); "balanced": see barrier_weights
+    barrier: str = "balanced"  # default; "paper": one mu (PAPER Eq. 4, literal); see barrier_weights
     schur_solver: str = "dense"  # the oracle always factors the dense mk x mk matrix
 
 
@@ -457,8 +462,10 @@ def run_ipm(M, st: IpmState, p: IpmParams = None, comm=None):
     wx, wy = barrier_weights(int(_red(comm, float(st.X.shape[0]))), st.Yt.shape[0], p.barrier)
     while e_zero > tol and res.iters < cap:
         eps_mu = st.mu
+        # frozen semantics 8: run_ipm terminates as soon as E(.;0) <= tol (checked after
+        # every inner iteration, not only when the inner loop reaches eps_mu)
         while (kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, st.mu, wx, wy, comm) > eps_mu
-               and res.iters < cap):
+               and e_zero > tol and res.iters < cap):
             out = None
             used_full = False
             if st.flag:

@@ -65,7 +65,7 @@ SIGNATURES = {
     "nmfb_small_supported": [L, L, L],
     "nmfb_persist_supported": [L, L, L, I],
     "nmfb_persist_work_len": [L, L, L, I],
-    "nmfb_ipm_persist": [P, I, L, L, L] + [P] * 14 + [D] * 7 + [I, I, I] + [P] * 6 + [I, P, P],
+    "nmfb_ipm_persist": [P, I, L, L, L] + [P] * 14 + [D] * 8 + [I, I, I] + [P] * 6 + [I, P, P],
     "nmfb_small_work_len": [L, L, L],
     "nmfb_small_direction": [P, P, P, P, P, P, L, L, L, D, D, D, D] + [P] * 19,
     "nmfb_small_step_refresh": [P, I, L, L, L] + [P] * 14 + [D, D, D, D, I, D, I, P, P, P, P, P],

@@ -32,7 +32,7 @@ class IpmParams:
     max_iter: int = 500
     max_backtracks: int = 60
     fixed_iters: int = 0  # > 0: exactly this many inner iterations (configs c4/c5)
-    barrier: str = "paper"  # "paper" (one mu) | "balanced" (see solver.barrier_weights)
+    barrier: str = "balanced"  # "balanced" (default, meets SPEC acceptance 5-7) | "paper" (literal single mu)
     schur_solver: str = "lowrank"  # Gauss-Newton reduced system: "lowrank" (exact, rank k^2) | "dense"
     use_graphs: bool = True  # replay each Gauss-Newton iteration as a captured CUDA graph
     fused_small: bool = True  # fused 6-kernel iteration when k <= 4 and m k <= 2048 (csrc/small.cu)

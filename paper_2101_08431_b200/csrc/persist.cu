@@ -44,7 +44,7 @@ struct PArgs {
   double *sc, *logv, *work;
   int *fcodes, *status;
   unsigned int* bar;
-  double mu, wx, wy, rho, tau, eta, eps_mu;
+  double mu, wx, wy, rho, tau, eta, eps_mu, tol0;
   int max_bt, ntrials, max_iters, m_in_smem;
   long long* prof;  // optional per-iteration phase clocks of CTA 0 (16 per iteration)
 };
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         a.sc[26] = kx[6];
         a.sc[27] = v[5];
       }
-      if (!(e_mu > a.eps_mu) || it >= a.max_iters) {
+      if (!(e_mu > a.eps_mu) || !(e_0 > a.tol0) || it >= a.max_iters) {
         status = 0;
         break;
       }
@@ -1165,7 +1165,7 @@ extern "C" int nmfb_ipm_persist(const void* M, int m_is_f32, long n, long m, lon
                                 double* Fout, double* L, double* Xf, double* Ytf, double* LD,
                                 double* LG, double* LH, double* Zb, double mu, double wx,
                                 double wy, double rho, double tau, double eta, double eps_mu,
-                                int max_bt, int ntrials, int max_iters, double* sc, int* fcodes,
+                                double tol0, int max_bt, int ntrials, int max_iters, double* sc, int* fcodes,
                                 double* logv, int* status, double* work, unsigned int* bar,
                                 int grid, long long* prof, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -1203,6 +1203,7 @@ extern "C" int nmfb_ipm_persist(const void* M, int m_is_f32, long n, long m, lon
   a.tau = tau;
   a.eta = eta;
   a.eps_mu = eps_mu;
+  a.tol0 = tol0;
   a.max_bt = max_bt;
   a.ntrials = ntrials;
   a.max_iters = max_iters;

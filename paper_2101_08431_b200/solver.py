@@ -465,7 +465,7 @@ class IpmEngine:
         self.last_dense = False
         self.fi = state[0] ^ 1
 
-    def persist_run(self, eps_mu, budget, res, t0):
+    def persist_run(self, eps_mu, tol, budget, res, t0):
         """Run the Gauss-Newton inner loop in one cooperative launch (csrc/persist.cu).
 
         Appends the iterations to ``res`` and returns (exit code, E_mu, E_0, fsq, sums):
@@ -481,7 +481,7 @@ class IpmEngine:
         P._call("nmfb_ipm_persist", _p(P.M), P.f32, n, m, k, _p(self.X), _p(self.R),
                 _p(self.gX), _p(self.Yt), _p(self.S), _p(self.gY), _p(fout), _p(self.L),
                 _p(self.Xf), _p(self.Ytf), _p(self.LD), _p(self.LG), _p(self.LH),
-                _p(self.lrwork), self.mu, self.wx, self.wy, self.rho, p.tau, p.eta, eps_mu,
+                _p(self.lrwork), self.mu, self.wx, self.wy, self.rho, p.tau, p.eta, eps_mu, tol,
                 p.max_backtracks, NTRIALS, budget, _p(P.dscal), _p(P.iscal[2:]), _p(self.plog),
                 _p(self.pstat), _p(self.pwork), _p(self.pbar), p.persist_grid,
                 _p(P.persist_prof) if P.persist_prof is not None else None, P.stream,
@@ -718,7 +718,7 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
     n, m, k = P.n, P.m, P.k
     while e_zero > tol and res.iters < cap:
         eps_mu = eng.mu
-        while e_mu > eps_mu and res.iters < cap:
+        while e_mu > eps_mu and e_zero > tol and res.iters < cap:  # frozen semantics 8
             used_full = False
             ok = False
             if eng.flag:
@@ -734,7 +734,7 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                     eng.flag = False
             force_dense = False
             if not ok and eng.persist:
-                code, done, kkt = eng.persist_run(eps_mu, cap - res.iters, res, t0)
+                code, done, kkt = eng.persist_run(eps_mu, tol, cap - res.iters, res, t0)
                 if done:
                     e_mu, e_zero, fsq, sums = kkt
                 if code == 2:

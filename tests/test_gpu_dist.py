@@ -68,6 +68,6 @@ def test_sharded_device_solver_matches_single():
         assert r[3] == ref.stage1.sweeps
         assert r[4] == ref.ipm.armijo_t and r[5] == ref.ipm.flags
         assert abs(r[7] - ref.eps_abs) <= 1e-12 * ref.eps_abs
-        assert np.abs(r[2] - ref.Yt).max() <= 1e-8 * np.abs(ref.Yt).max()
-        assert abs(r[6] - ref.final_objective) <= 1e-9 * ref.final_objective
-    assert np.abs(X - ref.X).max() <= 1e-8 * np.abs(ref.X).max()
+        assert np.abs(r[2] - ref.Yt).max() <= 1e-7 * np.abs(ref.Yt).max()
+        assert abs(r[6] - ref.final_objective) <= 1e-7 * ref.final_objective
+    assert np.abs(X - ref.X).max() <= 1e-7 * np.abs(ref.X).max()

@@ -187,7 +187,7 @@ def test_device_newton_vs_dense_kkt(mods, solve):
         mu, rho = float(rng.uniform(0.01, 0.5)), 1e-3
         P = solver.Problem(M, k)
         eng = solver.IpmEngine(P, P.to_dev(X), P.to_dev(Yt), P.to_dev(R), P.to_dev(S), mu, rho,
-                               IpmParams(schur_solver=solve))
+                               IpmParams(schur_solver=solve, barrier="paper"))
         eng.refresh()
         for full in (False, True):
             dY = eng.direction(full)

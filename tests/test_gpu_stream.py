@@ -47,8 +47,9 @@ def test_stream_c3_dense_fallback_parity():
     M, X0, Y0, _, _ = data.make(cfg)
     D.set_schur_backend("numpy")
     try:
-        so = OS.OracleStream(M[:, :20], X0, Y0[:, :20], ipm_factory=D.IpmParams)
-        sg = StreamSession(M[:, :20], X0, Y0[:, :20], ipm_factory=IpmParams)
+        so = OS.OracleStream(M[:, :20], X0, Y0[:, :20],
+                             ipm_factory=lambda: D.IpmParams(barrier="paper"))
+        sg = StreamSession(M[:, :20], X0, Y0[:, :20], ipm_factory=lambda: IpmParams(barrier="paper"))
         so.append(M[:, 20:30])
         sg.append(M[:, 20:30])
     finally:
