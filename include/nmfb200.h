@@ -138,8 +138,9 @@ int nmfb_schur_assemble(const double *Yt, const double *S, long m, long k, const
                         void *stream);
 
 /* full-C residual term: A -= sum_i f_ij f_il Rinv_i (lower block triangle) */
+long nmfb_term4_work_len(long n, long m, long k);
 int nmfb_schur_term4(const double *F, long n, long m, long k, const double *Apk, double *A,
-                     void *stream);
+                     double *work, long work_len, void *stream);
 
 /* rhs = muy/y - graY - r_acc, r_acc_j = H y_j (+ (F^T g)_j when FtG != NULL)
  * (rhs_reduce, _kernels_numba.py:146) */
@@ -266,6 +267,15 @@ int nmfb_ipm_persist(const void *M, int m_is_f32, long n, long m, long k, double
                      double eps_mu, double tol0, int max_bt, int ntrials, int max_iters, double *sc,
                      int *fcodes, double *logv, int *status, double *work, unsigned int *bar,
                      int grid, long long *prof, void *stream);
+
+
+/* Up to four k x k Grams out_q = A_q^T B_q over the same rows (row-major fp64 inputs,
+ * unused slots NULL); deterministic.  work >= nmfb_grams_work_len(rows, k, count). */
+long nmfb_grams_work_len(long rows, long k, long count);
+int nmfb_grams(int count, const double *A0, const double *B0, double *O0, const double *A1,
+               const double *B1, double *O1, const double *A2, const double *B2, double *O2,
+               const double *A3, const double *B3, double *O3, long rows, long k, double *work,
+               long work_len, void *stream);
 
 #ifdef __cplusplus
 }

@@ -43,7 +43,8 @@ SIGNATURES = {
     "nmfb_atb": [P, L, L, P, L, P, P, L, P],
     "nmfb_make_p": [P, P, L, L, P, P],
     "nmfb_schur_assemble": [P, P, L, L, P, P, D, P, P, P],
-    "nmfb_schur_term4": [P, L, L, L, P, P, P],
+    "nmfb_schur_term4": [P, L, L, L, P, P, P, L, P],
+    "nmfb_term4_work_len": [L, L, L],
     "nmfb_schur_rhs": [P, P, P, P, D, L, L, P, P],
     "nmfb_direction": [P, P, P, P, P, P, P, P, D, P, P, P, P, D, D, L, L, L, P, P, P, P, P, L, P],
     "nmfb_quartic": [P, L, L, L, P, P, P, P, P, P, P],
@@ -64,6 +65,8 @@ SIGNATURES = {
     "nmfb_ffree_quartic": [P, P, P, P, P, P, P, P, P, L, P, P],
     "nmfb_small_supported": [L, L, L],
     "nmfb_persist_supported": [L, L, L, I],
+    "nmfb_grams_work_len": [L, L, L],
+    "nmfb_grams": [I] + [P] * 12 + [L, L, P, L, P],
     "nmfb_persist_work_len": [L, L, L, I],
     "nmfb_ipm_persist": [P, I, L, L, L] + [P] * 14 + [D] * 8 + [I, I, I] + [P] * 6 + [I, P, P],
     "nmfb_small_work_len": [L, L, L],
@@ -74,7 +77,8 @@ SIGNATURES = {
 }
 RESTYPES = {"nmfb_colprod_work_len": ctypes.c_long, "nmfb_rowprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
             "nmfb_launch_count": ctypes.c_ulonglong, "nmfb_small_work_len": ctypes.c_long,
-            "nmfb_persist_work_len": ctypes.c_long}
+            "nmfb_persist_work_len": ctypes.c_long, "nmfb_grams_work_len": ctypes.c_long,
+            "nmfb_term4_work_len": ctypes.c_long}
 
 _lib = None
 

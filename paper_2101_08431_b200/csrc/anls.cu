@@ -583,6 +583,21 @@ __global__ void __launch_bounds__(256) k_sum_partials(const double* __restrict__
 }
 
 // grid for k_sum_partials over `rows` rows of width K
+// short outputs (k x k Grams) over many partials: one warp per element, lanes
+// stride the partials, fixed butterfly -> deterministic; all loads in flight
+__global__ void __launch_bounds__(256) k_sum_partials_warp(const double* __restrict__ part,
+                                                           int nparts, long len,
+                                                           double* __restrict__ out,
+                                                           double scale) {
+  const long e = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= len) return;
+  double v = 0.0;
+  for (int s = lane; s < nparts; s += 32) v += part[(long)s * len + e];
+  v = warp_sum(v);
+  if (lane == 0) out[e] = v * scale;
+}
+
 template <int K>
 inline unsigned sum_grid(long rows) {
   return (unsigned)((rows + (256 / K) - 1) / (256 / K));
@@ -697,8 +712,12 @@ int launch_rowprod(const T* A, long rows, long cols, const double* B, double* ou
     cudaFuncSetAttribute(k_rowprod_mma<NT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((unsigned)nch, (unsigned)nsplit);
     ++g_nmfb_launches, k_rowprod_mma<NT, T><<<grid, 256, smem, st>>>(A, rows, cols, B, K, rps, work);
-    ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(
-        work, (int)nch, rows * K, out, tol, scale);
+    if (!tol && rows * K <= 4096 && nch >= 32)
+      ++g_nmfb_launches, k_sum_partials_warp<<<(unsigned)((rows * K + 7) / 8), 256, 0, st>>>(
+          work, (int)nch, rows * K, out, scale);
+    else
+      ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(
+          work, (int)nch, rows * K, out, tol, scale);
     NMFB_CHECK_LAUNCH();
     return NMFB_OK;
   }
@@ -716,8 +735,12 @@ int launch_rowprod(const T* A, long rows, long cols, const double* B, double* ou
                          (int)smem);
     dim3 grid((unsigned)nch, (unsigned)nsplit);
     ++g_nmfb_launches, k_rowprod_split<K, RW, T><<<grid, 256, smem, st>>>(A, rows, cols, B, rps, work);
-    ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(
-        work, (int)nch, rows * K, out, tol, scale);
+    if (!tol && rows * K <= 4096 && nch >= 32)
+      ++g_nmfb_launches, k_sum_partials_warp<<<(unsigned)((rows * K + 7) / 8), 256, 0, st>>>(
+          work, (int)nch, rows * K, out, scale);
+    else
+      ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(
+          work, (int)nch, rows * K, out, tol, scale);
     NMFB_CHECK_LAUNCH();
     return NMFB_OK;
   }
@@ -763,8 +786,12 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
     dim3 grid((unsigned)((cols + CP_COLS - 1) / CP_COLS), (unsigned)ns);
     ++g_nmfb_launches, k_colprod_partial<K, T><<<grid, 256, 0, st>>>(A, rows, cols, B, stripe, work);
   }
-  ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(cols), 256, 0, st>>>(work, (int)ns, cols * K, out,
-                                                                   tol, scale);
+  if (!tol && cols * K <= 4096 && ns >= 32)  // Grams: warp per element
+    ++g_nmfb_launches, k_sum_partials_warp<<<(unsigned)((cols * K + 7) / 8), 256, 0, st>>>(
+        work, (int)ns, cols * K, out, scale);
+  else
+    ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(cols), 256, 0, st>>>(work, (int)ns, cols * K,
+                                                                     out, tol, scale);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

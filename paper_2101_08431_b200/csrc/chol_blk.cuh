@@ -1,0 +1,182 @@
+// Single-CTA blocked Cholesky for small dense SPD matrices (N <= 800), shared by
+// the rank-k^2 capacitance factors (lowrank.cu, N = k^2 <= 256) and the dense
+// Gauss-Newton / full-Hessian Schur system of small problems (dense.cu).
+//
+// In place, lower, row-major, matrix in global memory (L2 resident), 32-column
+// panels: warp 0 factors the diagonal block with its rows in registers (column
+// j broadcast by shuffles), every warp solves panel rows (four in flight, one
+// shuffle per column), and all threads apply the trailing update in 4 x 4
+// register tiles read from a transposed shared-memory copy of the panel.
+// Reciprocal pivots come from rsqrt; the strict upper triangle is zeroed.
+#pragma once
+#include "common.cuh"
+
+namespace {
+
+constexpr int CHOL_BLK_THREADS = 384;
+
+inline size_t chol_blk_smem(long N) {  // diagonal block (32 x 33) + transposed panel (32 x N)
+  return (size_t)(32 * 33 + 32 * (N + 2)) * sizeof(double);
+}
+
+template <int J, int C>
+struct BCholUpd {
+  static __device__ __forceinline__ void run(double (&a)[32], int r) {
+    const double lcj = __shfl_sync(0xffffffffu, a[J], C);
+    const double upd = a[C] - a[J] * lcj;
+    a[C] = (r >= C) ? upd : a[C];
+    BCholUpd<J, C + 1>::run(a, r);
+  }
+};
+template <int J>
+struct BCholUpd<J, 32> {
+  static __device__ __forceinline__ void run(double (&)[32], int) {}
+};
+template <int J>
+struct BCholStep {
+  static __device__ __forceinline__ void run(double (&a)[32], int r, int& fail, double& di_r) {
+    double pv = __shfl_sync(0xffffffffu, a[J], J);
+    if (fail < 0 && !(pv > 0.0)) fail = J;
+    if (fail >= 0) pv = 1.0;  // dummy pivot after a failure: no divergence, no break
+    const double di = rsqrt(pv);
+    a[J] = (r == J) ? pv * di : ((r > J) ? a[J] * di : a[J]);
+    di_r = (r == J) ? di : di_r;
+    BCholUpd<J, J + 1>::run(a, r);
+    BCholStep<J + 1>::run(a, r, fail, di_r);
+  }
+};
+template <>
+struct BCholStep<32> {
+  static __device__ __forceinline__ void run(double (&)[32], int, int&, double&) {}
+};
+
+// warp 0: the nb x nb diagonal block at (p0, p0), padded to 32 with identity
+__device__ __noinline__ void chol_diag_block(double* A, long N, int p0, int nb, double* sd,
+                                             double* dinv, int* sfail) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  double a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    a[c] = (lane < nb && c < nb) ? A[(long)(p0 + lane) * N + p0 + c] : (lane == c ? 1.0 : 0.0);
+  int fail = -1;
+  double di = 0.0;
+  BCholStep<0>::run(a, lane, fail, di);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const double v = (c <= lane) ? a[c] : 0.0;
+    if (lane < nb && c < nb) A[(long)(p0 + lane) * N + p0 + c] = v;
+    sd[lane * 33 + c] = v;
+  }
+  dinv[lane] = di;
+  if (lane == 0 && fail >= 0 && fail < nb) *sfail = p0 + fail;
+}
+
+// info: failure -> fail_base + pivot column; success -> -1 when set_ok.
+// skip_if_set: do nothing if *info >= 0 on entry (an earlier factorization failed).
+__global__ void __launch_bounds__(CHOL_BLK_THREADS) k_chol_blk(double* __restrict__ A, int N,
+                                                               int* __restrict__ info,
+                                                               int fail_base, int skip_if_set,
+                                                               int set_ok) {
+  extern __shared__ double smc[];
+  double* sd = smc;              // diagonal block, 32 x 33
+  double* pT = smc + 32 * 33;    // transposed panel: pT[i * LDT + (row - p0)]
+  __shared__ double dinv[32];
+  __shared__ int sfail;
+  if (skip_if_set && *info >= 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nwarp = (int)(blockDim.x >> 5);
+  const int LDT = N + 2;
+  if (tid == 0) sfail = -1;
+  __syncthreads();
+  for (int p0 = 0; p0 < N; p0 += 32) {
+    const int nb = min(32, N - p0);
+    if (wid == 0) chol_diag_block(A, N, p0, nb, sd, dinv, &sfail);
+    __syncthreads();
+    if (sfail >= 0) break;
+    // panel rows: L_rp = A_rp L_pp^{-T}, four rows per warp per column sweep
+    {
+      const double dl = dinv[lane];
+      const double* lrow = sd + lane * 33;
+      for (int rb = p0 + nb + 4 * wid; rb < N; rb += 4 * nwarp) {
+        double acc[4], x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[u] = (lane < nb && rb + u < N) ? A[(long)(rb + u) * N + p0 + lane] : 0.0;
+          x[u] = 0.0;
+        }
+        for (int j = 0; j < nb; ++j) {
+          const double lcj = (lane < nb) ? lrow[j] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double xj = __shfl_sync(0xffffffffu, acc[u] * dl, j);
+            const double nacc = acc[u] - lcj * xj;
+            x[u] = (lane == j) ? xj : x[u];
+            acc[u] = (lane > j) ? nacc : acc[u];
+          }
+        }
+        if (lane < nb) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (rb + u < N) {
+              A[(long)(rb + u) * N + p0 + lane] = x[u];
+              pT[lane * LDT + (rb + u - p0)] = x[u];
+            }
+        }
+      }
+    }
+    __syncthreads();
+    // trailing update of the lower triangle [b0, N)^2: row-major tile order, so a
+    // warp shares its row tile (broadcast) and streams consecutive column tiles
+    const int b0 = p0 + nb, n2 = N - b0;
+    if (n2 > 0) {
+      const int tt = (n2 + 3) >> 2;
+      const int ntile = tt * (tt + 1) / 2;
+      for (int t = tid; t < ntile; t += blockDim.x) {
+        int ti = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+        while (ti * (ti + 1) / 2 > t) --ti;
+        const int tj = t - ti * (ti + 1) / 2;
+        const int r0 = b0 + 4 * ti, c0 = b0 + 4 * tj;
+        const double* pr = pT + (r0 - p0);
+        const double* pc = pT + (c0 - p0);
+        double acc[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+        for (int i = 0; i < nb; ++i) {
+          double ar[4], bc[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            ar[u] = pr[i * LDT + u];
+            bc[u] = pc[i * LDT + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(ar[u], bc[v], acc[u][v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int r = r0 + u, c = c0 + v;
+            if (r < N && c <= r) A[(long)r * N + c] -= acc[u][v];
+          }
+      }
+    }
+    __syncthreads();
+  }
+  const int f = sfail;
+  for (int r = wid; r < N; r += nwarp)
+    for (int c = r + 1 + lane; c < N; c += 32) A[(long)r * N + c] = 0.0;
+  if (tid == 0) {
+    if (f >= 0)
+      *info = fail_base + f;
+    else if (set_ok)
+      *info = -1;
+  }
+}
+
+}  // namespace

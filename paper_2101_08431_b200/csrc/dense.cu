@@ -14,6 +14,7 @@
 // (diagonal solve + GEMV sweep) for large N.
 #include "common.cuh"
 #include "nmfb200.h"
+#include "chol_blk.cuh"
 
 namespace {
 
@@ -152,9 +153,41 @@ __global__ void __launch_bounds__(256) k_syrk_trailing(double* __restrict__ A, l
 // triangular solves with the factor (lower, row-major): forward L z = b,
 // backward L^T x = z, in place on b.  Single-CTA blocked variant.
 // ---------------------------------------------------------------------------
+// one warp solves the 32 x 32 diagonal block at c0 (nc <= 32 active columns):
+// the block is staged in shared memory with reciprocal pivots first, so the
+// column sweep is one shuffle + one FMA per step (no global loads or divides
+// on the dependency chain).  v (lane = row) holds b on entry, z on exit.
+__device__ __forceinline__ double trsv_diag_warp(const double* __restrict__ L, long N, long c0,
+                                                 int nc, int trans, double v, double* blk,
+                                                 double* rcp) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < 32 * 32; e += 32) {
+    const int r = e >> 5, c = e & 31;
+    blk[r * 33 + c] = (r < nc && c < nc) ? L[(c0 + r) * N + c0 + c] : 0.0;
+  }
+  __syncwarp();
+  rcp[lane] = lane < nc ? 1.0 / blk[lane * 33 + lane] : 0.0;
+  __syncwarp();
+  const double rl = rcp[lane];
+  if (!trans) {
+    for (int j = 0; j < nc; ++j) {
+      const double zj = __shfl_sync(0xffffffffu, v * rl, j);
+      const double nv = v - blk[lane * 33 + j] * zj;
+      v = (lane == j) ? zj : ((lane > j && lane < nc) ? nv : v);
+    }
+  } else {
+    for (int j = nc - 1; j >= 0; --j) {
+      const double zj = __shfl_sync(0xffffffffu, v * rl, j);
+      const double nv = v - blk[j * 33 + lane] * zj;
+      v = (lane == j) ? zj : (lane < j ? nv : v);
+    }
+  }
+  return v;
+}
+
 __global__ void __launch_bounds__(1024) k_trsv_single(const double* __restrict__ L, long N,
                                                       double* __restrict__ b, int trans) {
-  __shared__ double zb[32];
+  __shared__ double zb[32], sblk[32 * 33], srcp[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nw = blockDim.x >> 5;
   const long nblk = (N + 31) / 32;
@@ -165,19 +198,7 @@ __global__ void __launch_bounds__(1024) k_trsv_single(const double* __restrict__
     // 1) warp 0 solves the 32x32 diagonal block
     if (wid == 0) {
       double v = lane < nc ? b[c0 + lane] : 0.0;
-      if (!trans) {
-        for (int j = 0; j < nc; ++j) {
-          const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * N + c0 + j];
-          if (lane == j) v = zj;
-          if (lane > j && lane < nc) v -= L[(c0 + lane) * N + c0 + j] * zj;
-        }
-      } else {
-        for (int j = nc - 1; j >= 0; --j) {
-          const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * N + c0 + j];
-          if (lane == j) v = zj;
-          if (lane < j) v -= L[(c0 + j) * N + c0 + lane] * zj;
-        }
-      }
+      v = trsv_diag_warp(L, N, c0, nc, trans, v, sblk, srcp);
       if (lane < nc) {
         b[c0 + lane] = v;
         zb[lane] = v;
@@ -206,21 +227,10 @@ __global__ void __launch_bounds__(1024) k_trsv_single(const double* __restrict__
 // multi-CTA pieces for large N
 __global__ void k_trsv_diag(const double* __restrict__ L, long N, double* __restrict__ b, long c0,
                             int nc, int trans) {
+  __shared__ double sblk[32 * 33], srcp[32];
   const int lane = threadIdx.x;
   double v = lane < nc ? b[c0 + lane] : 0.0;
-  if (!trans) {
-    for (int j = 0; j < nc; ++j) {
-      const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * N + c0 + j];
-      if (lane == j) v = zj;
-      if (lane > j && lane < nc) v -= L[(c0 + lane) * N + c0 + j] * zj;
-    }
-  } else {
-    for (int j = nc - 1; j >= 0; --j) {
-      const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * N + c0 + j];
-      if (lane == j) v = zj;
-      if (lane < j) v -= L[(c0 + j) * N + c0 + lane] * zj;
-    }
-  }
+  v = trsv_diag_warp(L, N, c0, nc, trans, v, sblk, srcp);
   if (lane < nc) b[c0 + lane] = v;
 }
 
@@ -255,6 +265,13 @@ extern "C" int nmfb_dense_cholesky(double* A, long N, int* info, void* stream) {
     cudaFuncSetAttribute(k_syrk_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kTwoTiles);
     attr = true;
+  }
+  if (N <= 800) {  // one CTA, L2-resident matrix (csrc/chol_blk.cuh)
+    const size_t sm = chol_blk_smem(N);
+    cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    ++g_nmfb_launches, k_chol_blk<<<1, CHOL_BLK_THREADS, sm, st>>>(A, (int)N, info, 0, 0, 1);
+    NMFB_CHECK_LAUNCH();
+    return NMFB_OK;
   }
   cudaMemsetAsync(info, 0xFF, sizeof(int), st);  // -1: no failing pivot
   for (long k0 = 0; k0 < N; k0 += NB) {

@@ -337,31 +337,39 @@ __global__ void __launch_bounds__(256) k_schur_assemble(
   }
 }
 
-// full Hessian term 4: A[(j,p),(l,q)] -= sum_i f_ij f_il Ainv_i[p,q], j >= l
-template <int K>
+// full Hessian term 4: A[(j,p),(l,q)] -= sum_i f_ij f_il Ainv_i[p,q], j >= l.
+// grid (tile j, tile l, pq chunk x row split).  nsplit == 1: subtract in place;
+// else write part[split][j][l][pq] and k_term4_finish sums the splits in order.
+template <int K, int PQC>
 __global__ void __launch_bounds__(256) k_schur_term4(const double* __restrict__ F, long n, long m,
                                                      const double* __restrict__ Apk,
-                                                     double* __restrict__ A) {
+                                                     double* __restrict__ A, int nsplit,
+                                                     double* __restrict__ part) {
   constexpr int KK = K * (K + 1) / 2;
-  constexpr int PQC = 16;
   __shared__ double fj[32][16], fl[32][16], ap[32][PQC];
   const long tj = blockIdx.x, tl = blockIdx.y;
   if (tj < tl) return;
-  const int pq0 = blockIdx.z * PQC;
+  const int zc = blockIdx.z / nsplit, zs = blockIdx.z % nsplit;
+  const int pq0 = zc * PQC;
   const int npq = min(PQC, KK - pq0);
+  const long rps = (n + nsplit - 1) / nsplit;
+  const long i_beg = zs * rps, i_end = min(n, i_beg + rps);
   const int tid = threadIdx.x, jj = tid >> 4, ll = tid & 15;
   const long j = tj * 16 + jj, l = tl * 16 + ll;
   double acc[PQC];
 #pragma unroll
   for (int c = 0; c < PQC; ++c) acc[c] = 0.0;
-  for (long ib = 0; ib < n; ib += 32) {
-    const int nr = (int)min(32L, n - ib);
+  for (long ib = i_beg; ib < i_end; ib += 32) {
+    const int nr = (int)min(32L, i_end - ib);
     __syncthreads();
     for (int e = tid; e < 32 * 16; e += 256) {
       const int r = e >> 4, c = e & 15;
       const long jc = tj * 16 + c, lc = tl * 16 + c;
       fj[r][c] = (r < nr && jc < m) ? F[(ib + r) * m + jc] : 0.0;
       fl[r][c] = (r < nr && lc < m) ? F[(ib + r) * m + lc] : 0.0;
+    }
+    for (int e = tid; e < 32 * PQC; e += 256) {
+      const int r = e / PQC, c = e % PQC;
       ap[r][c] = (r < nr && c < npq) ? Apk[(ib + r) * KK + pq0 + c] : 0.0;
     }
     __syncthreads();
@@ -372,6 +380,10 @@ __global__ void __launch_bounds__(256) k_schur_term4(const double* __restrict__ 
     }
   }
   if (j >= m || l >= m || j < l) return;
+  if (nsplit > 1) {
+    for (int c = 0; c < npq; ++c) part[((long)zs * m * m + j * m + l) * KK + pq0 + c] = acc[c];
+    return;
+  }
   const long N = m * K;
   for (int c = 0; c < npq; ++c) {
     // unpack pq0 + c -> (p, q), p <= q
@@ -384,6 +396,29 @@ __global__ void __launch_bounds__(256) k_schur_term4(const double* __restrict__ 
     A[(j * K + p) * N + l * K + q] -= acc[c];
     if (p != q) A[(j * K + q) * N + l * K + p] -= acc[c];
   }
+}
+
+template <int K>
+__global__ void k_term4_finish(const double* __restrict__ part, long m, int nsplit,
+                               double* __restrict__ A) {
+  constexpr int KK = K * (K + 1) / 2;
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;  // (j, l, pq), j >= l
+  if (e >= m * m * KK) return;
+  const long jl = e / KK;
+  const int pqi = (int)(e % KK);
+  const long j = jl / m, l = jl % m;
+  if (j < l) return;
+  double s = 0.0;
+  for (int z = 0; z < nsplit; ++z) s += part[(long)z * m * m * KK + e];
+  int ee = pqi, p = 0;
+  while (ee >= K - p) {
+    ee -= K - p;
+    ++p;
+  }
+  const int q = p + ee;
+  const long N = m * K;
+  A[(j * K + p) * N + l * K + q] -= s;
+  if (p != q) A[(j * K + q) * N + l * K + p] -= s;
 }
 
 // P[i][(p,q,a)] = x_ip * Ainv_i[q,a]   (n x K^3, for W = F^T P)
@@ -844,6 +879,70 @@ __global__ void k_step_nudge_dev(double* __restrict__ v, const double* __restric
 
 constexpr int RED_BLOCKS = 296;  // fixed -> deterministic reductions
 
+// ---------------------------------------------------------------------------
+// Up to four k x k Grams A_q^T B_q over the same rows in one pass (the
+// residual-free IPM's small contractions): CTA = row block, 32-row chunks
+// staged in shared memory, thread per output; deterministic fixed-order finish.
+// ---------------------------------------------------------------------------
+struct GramSet {
+  const double* A[4];
+  const double* B[4];
+  double* out[4];
+  int count;
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) k_grams_partial(GramSet gs, long rows, long rows_per_cta,
+                                                       double* __restrict__ part) {
+  __shared__ double sa[4][32][K], sb[4][32][K];
+  constexpr int KK = K * K;
+  constexpr int U = (4 * KK + 255) / 256;
+  const int nq = gs.count, NO = nq * KK, tid = threadIdx.x;
+  const long i0 = (long)blockIdx.x * rows_per_cta, i1 = min(rows, i0 + rows_per_cta);
+  double acc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = 0.0;
+  for (long ib = i0; ib < i1; ib += 32) {
+    const int nr = (int)min(32L, i1 - ib);
+    __syncthreads();
+    for (int q = 0; q < nq; ++q)
+      for (int e = tid; e < nr * K; e += 256) {
+        sa[q][e / K][e % K] = gs.A[q][ib * K + e];
+        sb[q][e / K][e % K] = gs.B[q][ib * K + e];
+      }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = tid + 256 * u;
+      if (e < NO) {
+        const int q = e / KK, a = (e / K) % K, b = e % K;
+        double s = acc[u];
+        for (int r = 0; r < nr; ++r) s = fma(sa[q][r][a], sb[q][r][b], s);
+        acc[u] = s;
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int e = tid + 256 * u;
+    if (e < NO) part[(long)blockIdx.x * NO + e] = acc[u];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_grams_finish(GramSet gs, int KK,
+                                                      const double* __restrict__ part,
+                                                      int nparts) {
+  // one warp per output element, lanes stride the partials, fixed butterfly
+  const int NO = gs.count * KK;
+  const int e = (int)(((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= NO) return;
+  double s = 0.0;
+  for (int g = lane; g < nparts; g += 32) s += part[(long)g * NO + e];
+  s = warp_sum(s);
+  if (lane == 0) gs.out[e / KK][e % KK] = s;
+}
+
 }  // namespace
 
 #define NMFB_K_SWITCH(k, MACRO) \
@@ -993,16 +1092,40 @@ extern "C" int nmfb_schur_assemble(const double* Yt, const double* S, long m, lo
   return NMFB_OK;
 }
 
+static int term4_nsplit(long n, long m, long k) {
+  const long kk = k * (k + 1) / 2;
+  const long tiles = (m + 15) / 16;
+  const long active = tiles * (tiles + 1) / 2 * ((kk + 15) / 16);
+  long ns = (148 * 2 + active - 1) / active;
+  const long maxs = (n + 255) / 256;
+  if (ns > maxs) ns = maxs;
+  if (ns > 32) ns = 32;
+  return ns < 1 ? 1 : (int)ns;
+}
+
+extern "C" long nmfb_term4_work_len(long n, long m, long k) {
+  const int ns = term4_nsplit(n, m, k);
+  return ns > 1 ? (long)ns * m * m * (k * (k + 1) / 2) : 1;
+}
+
 extern "C" int nmfb_schur_term4(const double* F, long n, long m, long k, const double* Apk,
-                                double* A, void* stream) {
+                                double* A, double* work, long work_len, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const long kk = k * (k + 1) / 2;
   const long tiles = (m + 15) / 16;
-  dim3 grid((unsigned)tiles, (unsigned)tiles, (unsigned)((kk + 15) / 16));
-#define CASE(KK)                                                       \
-  case KK:                                                             \
-    ++g_nmfb_launches, k_schur_term4<KK><<<grid, 256, 0, st>>>(F, n, m, Apk, A);          \
-    break;
+  int ns = term4_nsplit(n, m, k);
+  if (ns > 1 && (long)ns * m * m * kk > work_len) ns = 1;
+  const long nchunk = (kk + 15) / 16;
+  dim3 grid((unsigned)tiles, (unsigned)tiles, (unsigned)(nchunk * ns));
+#define CASE(KK)                                                                               \
+  case KK: {                                                                                   \
+    constexpr int PQ = (KK * (KK + 1) / 2) < 16 ? (KK * (KK + 1) / 2) : 16;                   \
+    ++g_nmfb_launches, k_schur_term4<KK, PQ><<<grid, 256, 0, st>>>(F, n, m, Apk, A, ns, work); \
+    if (ns > 1)                                                                                \
+      ++g_nmfb_launches, k_term4_finish<KK><<<(unsigned)((m * m * kk + 255) / 256), 256, 0, st>>>( \
+          work, m, ns, A);                                                                     \
+    break;                                                                                     \
+  }
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
   NMFB_CHECK_LAUNCH();
@@ -1259,6 +1382,52 @@ extern "C" int nmfb_ffree_quartic(const double* A1, const double* A2, const doub
                                   double* sc, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   ++g_nmfb_launches, k_ffree_quartic<<<1, 32, 0, st>>>(A1, A2, XX, B1, B2, YY, Dgx, Dgy, Dmd, (int)k, sc);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// out_q = A_q^T B_q (k x k) for q < count <= 4; A_q, B_q (rows x k) row-major fp64.
+// work >= nmfb_grams_work_len(rows, k, count).
+static long grams_ctas(long rows) {
+  long g = (rows + 63) / 64;
+  if (g > 296) g = 296;
+  return g < 1 ? 1 : g;
+}
+extern "C" long nmfb_grams_work_len(long rows, long k, long count) {
+  return grams_ctas(rows) * count * k * k;
+}
+extern "C" int nmfb_grams(int count, const double* A0, const double* B0, double* O0,
+                          const double* A1, const double* B1, double* O1, const double* A2,
+                          const double* B2, double* O2, const double* A3, const double* B3,
+                          double* O3, long rows, long k, double* work, long work_len,
+                          void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (count < 1 || count > 4 || k < 1 || k > 16) return NMFB_EINVAL;
+  GramSet gs;
+  const double* As[4] = {A0, A1, A2, A3};
+  const double* Bs[4] = {B0, B1, B2, B3};
+  double* Os[4] = {O0, O1, O2, O3};
+  for (int q = 0; q < 4; ++q) {
+    gs.A[q] = As[q];
+    gs.B[q] = Bs[q];
+    gs.out[q] = Os[q];
+  }
+  gs.count = count;
+  if (rows <= 0) {
+    for (int q = 0; q < count; ++q) cudaMemsetAsync(Os[q], 0, sizeof(double) * k * k, st);
+    return NMFB_OK;
+  }
+  const long G = grams_ctas(rows);
+  if (G * count * k * k > work_len) return NMFB_ENOMEM;
+  const long rpc = (rows + G - 1) / G;
+#define CASE(KK_)                                                                             \
+  case KK_:                                                                                   \
+    ++g_nmfb_launches, k_grams_partial<KK_><<<(unsigned)G, 256, 0, st>>>(gs, rows, rpc, work); \
+    break;
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+  const int NO = count * (int)(k * k);
+  ++g_nmfb_launches, k_grams_finish<<<(NO + 7) / 8, 256, 0, st>>>(gs, (int)(k * k), work, (int)G);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

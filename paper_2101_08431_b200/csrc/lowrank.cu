@@ -14,6 +14,7 @@
 // dense factorization performs.  Cost O(m k^3 + k^6) instead of O(m^3 k^3).
 #include "common.cuh"
 #include "nmfb200.h"
+#include "chol_blk.cuh"
 
 namespace {
 
@@ -170,139 +171,65 @@ __global__ void k_d_correct(const double* __restrict__ LD, const double* __restr
   for (int a = 0; a < K; ++a) t[j * K + a] += v[a];
 }
 
-// in-place lower Cholesky of a Q x Q row-major matrix (smem or global) by one
-// CTA, two barriers per column; warps own rows of the trailing update and lanes
-// its columns (no integer division, contiguous accesses).  Returns the failing
-// pivot column or -1 (in every thread).
-__device__ int cta_cholesky(double* A, int Q, int* sfail) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-  const int nw = nt >> 5;
-  if (tid == 0) *sfail = -1;
-  __syncthreads();
-  for (int j = 0; j < Q; ++j) {
-    const double pv = A[j * Q + j];
-    if (!(pv > 0.0)) {
-      if (tid == 0) *sfail = j;
-      break;  // uniform: every thread read the same pivot
-    }
-    const double rd = 1.0 / sqrt(pv);
-    for (int r = j + 1 + tid; r < Q; r += nt) A[r * Q + j] *= rd;
-    __syncthreads();
-    if (tid == 0) A[j * Q + j] = pv * rd;
-    for (int r = j + 1 + wid; r < Q; r += nw) {
-      const double lrj = A[r * Q + j];
-      for (int c = j + 1 + lane; c <= r; c += 32) A[r * Q + c] -= lrj * A[c * Q + j];
-    }
-    __syncthreads();
-  }
-  __syncthreads();
-  const int f = *sfail;
-  __syncthreads();
-  return f;
-}
-
-// C[r][c] (Q x Q) += sum over the lower-triangular factor, 2x2 register tiles:
-//   mode 0: T1 = Zb L       (T1[r][c] = sum_{t >= c} Zb[r][t] L[t][c])
-//   mode 1: H  = I - L^T T1 (H[r][c]  = delta - sum_{t >= r} L[t][r] T1[t][c], c <= r)
-__device__ void cta_tri_gemm(const double* Zb_or_L, const double* Lm, double* out, int Q, int mode) {
-  const int half = (Q + 1) / 2;
-  for (int e = threadIdx.x; e < half * half; e += blockDim.x) {
-    const int r0 = 2 * (e / half), c0 = 2 * (e % half);
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    if (mode == 0) {
-      for (int t = c0; t < Q; ++t) {
-        const double z0 = Zb_or_L[r0 * Q + t];
-        const double z1 = (r0 + 1 < Q) ? Zb_or_L[(r0 + 1) * Q + t] : 0.0;
-        const double l0 = Lm[t * Q + c0];
-        const double l1 = (c0 + 1 < Q && t >= c0 + 1) ? Lm[t * Q + c0 + 1] : 0.0;
-        acc[0][0] = fma(z0, l0, acc[0][0]);
-        acc[0][1] = fma(z0, l1, acc[0][1]);
-        acc[1][0] = fma(z1, l0, acc[1][0]);
-        acc[1][1] = fma(z1, l1, acc[1][1]);
-      }
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b)
-          if (r0 + a < Q && c0 + b < Q) out[(r0 + a) * Q + c0 + b] = acc[a][b];
-    } else {
-      if (c0 > r0 + 1) {  // strictly upper tile: zeros
-#pragma unroll
-        for (int a = 0; a < 2; ++a)
-#pragma unroll
-          for (int b = 0; b < 2; ++b)
-            if (r0 + a < Q && c0 + b < Q) out[(r0 + a) * Q + c0 + b] = 0.0;
-        continue;
-      }
-      for (int t = r0; t < Q; ++t) {
-        const double l0 = Zb_or_L[t * Q + r0];
-        const double l1 = (r0 + 1 < Q && t >= r0 + 1) ? Zb_or_L[t * Q + r0 + 1] : 0.0;
-        const double t0 = Lm[t * Q + c0];
-        const double t1 = (c0 + 1 < Q) ? Lm[t * Q + c0 + 1] : 0.0;
-        acc[0][0] = fma(l0, t0, acc[0][0]);
-        acc[0][1] = fma(l0, t1, acc[0][1]);
-        acc[1][0] = fma(l1, t0, acc[1][0]);
-        acc[1][1] = fma(l1, t1, acc[1][1]);
-      }
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const int r = r0 + a, c = c0 + b;
-          if (r < Q && c < Q) out[r * Q + c] = (c <= r) ? ((r == c ? 1.0 : 0.0) - acc[a][b]) : 0.0;
-        }
-    }
-  }
-}
-
-// one CTA: LG = chol(G), H = I - LG^T Zb LG, LH = chol(H).  work: 2 Q^2 doubles
-// (Zb kept in work[0, Q^2) for the solves).  Small Q works in shared memory.
-__global__ void __launch_bounds__(1024) k_lowrank_factor(const double* __restrict__ Zpk,
-                                                         const double* __restrict__ Gpk, int k,
-                                                         double* __restrict__ LG,
-                                                         double* __restrict__ LH,
-                                                         double* __restrict__ Zb,
-                                                         double* __restrict__ T1g,
-                                                         int* __restrict__ info, int use_smem) {
-  extern __shared__ double smf[];
-  __shared__ int sfail;
+// ---------------------------------------------------------------------------
+// Blocked factorization path (nmfb_lowrank_factor): Q = k^2 up to 256.
+// ---------------------------------------------------------------------------
+// unpack packed Z and G into full Zb and lower G (Q x Q); info <- -1
+__global__ void k_lr_unpack(const double* __restrict__ Zpk, const double* __restrict__ Gpk, int k,
+                            double* __restrict__ Zb, double* __restrict__ Gl,
+                            int* __restrict__ info) {
   const int Q = k * k, KK = k * (k + 1) / 2;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  double* A = use_smem ? smf : LG;            // G -> L_G, later H -> L_H
-  double* T1 = use_smem ? smf + Q * Q : T1g;  // Zb L_G
-  for (int e = tid; e < Q * Q; e += nt) {
-    const int r = e / Q, c = e % Q;
-    const int a = r / k, p = r % k, b = c / k, q = c % k;
-    const int ab = pkx(a, b, k), pq = pkx(p, q, k);
-    Zb[e] = Zpk[ab * KK + pq];
-    A[e] = (c <= r) ? Gpk[ab * KK + pq] : 0.0;
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e == 0) *info = -1;
+  if (e >= (long)Q * Q) return;
+  const int r = (int)(e / Q), c = (int)(e % Q);
+  const int a = r / k, p = r % k, b = c / k, q = c % k;
+  const int ab = pkx(a, b, k), pq = pkx(p, q, k);
+  Zb[e] = Zpk[ab * KK + pq];
+  Gl[e] = (c <= r) ? Gpk[ab * KK + pq] : 0.0;
+}
+
+// 32 x 32 output tile per CTA:
+//   mode 0: C = Zb L            (T1)
+//   mode 1: C = I - L^T T1      (H; only the lower triangle is consumed)
+__global__ void __launch_bounds__(256) k_lr_gemm(const double* __restrict__ Am,
+                                                 const double* __restrict__ Bm, int Q, int mode,
+                                                 double* __restrict__ C,
+                                                 const int* __restrict__ info) {
+  __shared__ double As[32][33], Bs[32][33];
+  if (*info >= 1000000) return;  // G already failed
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int kk = 0; kk < Q; kk += 32) {
+    for (int e = tid; e < 32 * 32; e += 256) {
+      const int i = e >> 5, j = e & 31;
+      const int r = r0 + i, t = kk + j;
+      double av = 0.0;
+      if (r < Q && t < Q) av = mode == 0 ? Am[(long)r * Q + t] : Am[(long)t * Q + r];
+      As[i][j] = av;
+      const int tb = kk + i, c = c0 + j;
+      Bs[i][j] = (tb < Q && c < Q) ? Bm[(long)tb * Q + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) {
+      const double a0 = As[2 * ty][t], a1 = As[2 * ty + 1][t];
+      const double b0 = Bs[t][2 * tx], b1 = Bs[t][2 * tx + 1];
+      acc[0][0] = fma(a0, b0, acc[0][0]);
+      acc[0][1] = fma(a0, b1, acc[0][1]);
+      acc[1][0] = fma(a1, b0, acc[1][0]);
+      acc[1][1] = fma(a1, b1, acc[1][1]);
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  int f = cta_cholesky(A, Q, &sfail);
-  if (f >= 0) {
-    if (tid == 0) *info = 1000000 + f;  // G singular: Y^T rank deficient
-    return;
-  }
-  for (int e = tid; e < Q * Q; e += nt) {  // publish L_G (strict upper zero)
-    const int r = e / Q, c = e % Q;
-    const double v = (c <= r) ? A[e] : 0.0;
-    A[e] = v;
-    if (use_smem) LG[e] = v;
-  }
-  __syncthreads();
-  // T1 = Zb L_G, then H = I - L_G^T T1 (lower part) -> LH (global)
-  cta_tri_gemm(Zb, A, T1, Q, 0);
-  __syncthreads();
-  cta_tri_gemm(A, T1, LH, Q, 1);
-  __syncthreads();
-  double* B = use_smem ? smf : LH;
-  if (use_smem)
-    for (int e = tid; e < Q * Q; e += nt) B[e] = LH[e];
-  __syncthreads();
-  f = cta_cholesky(B, Q, &sfail);
-  if (use_smem)
-    for (int e = tid; e < Q * Q; e += nt) LH[e] = B[e];
-  if (tid == 0) *info = f;  // -1: reduced system positive definite
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int r = r0 + 2 * ty + u, c = c0 + 2 * tx + v;
+      if (r < Q && c < Q) C[(long)r * Q + c] = mode == 0 ? acc[u][v] : ((r == c ? 1.0 : 0.0) - acc[u][v]);
+    }
 }
 
 // blocked in-CTA triangular solve with a row-major lower factor L (Q x Q):
@@ -421,14 +348,20 @@ extern "C" int nmfb_d_factor(const double* XtX, const double* Yt, const double* 
 
 extern "C" int nmfb_lowrank_factor(const double* Zpk, const double* Gpk, long k, double* LG,
                                    double* LH, double* work, int* info, void* stream) {
+  // unpack -> chol(G) -> T1 = Zb LG -> H = I - LG^T T1 -> chol(H); Zb stays in work[0, Q^2)
   cudaStream_t st = (cudaStream_t)stream;
   const long Q = k * k;
-  const size_t smem = (size_t)2 * Q * Q * sizeof(double);
-  const int use_smem = smem <= 200 * 1024;
-  if (use_smem)
-    cudaFuncSetAttribute(k_lowrank_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  ++g_nmfb_launches, k_lowrank_factor<<<1, 1024, use_smem ? smem : 0, st>>>(
-      Zpk, Gpk, (int)k, LG, LH, work, work + Q * Q, info, use_smem);
+  if (Q > 256) return NMFB_EUNSUPPORTED;
+  double* Zb = work;
+  double* T1 = work + Q * Q;
+  const size_t csm = chol_blk_smem(Q);
+  cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+  ++g_nmfb_launches, k_lr_unpack<<<(unsigned)((Q * Q + 255) / 256), 256, 0, st>>>(Zpk, Gpk, (int)k, Zb, LG, info);
+  ++g_nmfb_launches, k_chol_blk<<<1, CHOL_BLK_THREADS, csm, st>>>(LG, (int)Q, info, 1000000, 0, 0);
+  const dim3 g((unsigned)((Q + 31) / 32), (unsigned)((Q + 31) / 32));
+  ++g_nmfb_launches, k_lr_gemm<<<g, 256, 0, st>>>(Zb, LG, (int)Q, 0, T1, info);
+  ++g_nmfb_launches, k_lr_gemm<<<g, 256, 0, st>>>(LG, T1, (int)Q, 1, LH, info);
+  ++g_nmfb_launches, k_chol_blk<<<1, CHOL_BLK_THREADS, csm, st>>>(LH, (int)Q, info, 0, 1, 1);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

@@ -92,6 +92,8 @@ class Problem:
                  L.nmfb_rowprod_work_len(n, m, k, self.f32), L.nmfb_rowprod_work_len(n, m, k, 0),
                  4096)
         self.cwork = torch.empty(cw, **f64)
+        self.gwork = torch.empty(max(self.lib.nmfb_grams_work_len(max(n, M.shape[1]), k, 4), 1),
+                                 **f64)
         nb = L.nmfb_ipm_reduce_blocks()
         self.rwork = torch.empty(max(64 * 2 * NTRIALS, 12 * nb, 3 * ((n + 127) // 128 + nb), 4096),
                                  **f64)
@@ -159,6 +161,22 @@ class Problem:
             return
         self._call("nmfb_colprod", _p(A), f32, rows, cols, _p(B), k, _p(out), _p(tol), 1.0,
                    _p(self.cwork), self.cwork.numel(), self.stream, tag=tag)
+
+    def grams(self, triples, rows, k, reduce=False):
+        """out_q = A_q^T B_q (k x k) for up to four (A, B, out) over the same rows, one pass.
+        reduce=True: rows are sharded -> all-reduce every out."""
+        args = []
+        for q in range(4):
+            if q < len(triples):
+                a, b, o = triples[q]
+                args += [_p(a), _p(b), _p(o)]
+            else:
+                args += [None, None, None]
+        self._call("nmfb_grams", len(triples), *args, rows, k, _p(self.gwork), self.gwork.numel(),
+                   self.stream)
+        if reduce and self.comm.active:
+            for _, _, o in triples:
+                self.comm.sum_(o)
 
     @property
     def ny_local(self):
@@ -331,10 +349,13 @@ class IpmEngine:
         self.Apk, self.XXpk = b(n, self.kk), b(n, self.kk)
         self.Z = b(self.kk, self.kk)
         self.GY, self.XtX, self.H, self.Gdy = b(k, k), b(k, k), b(k, k), b(k, k)
+        if self.ffree:  # the refresh's Grams at the current point (same buffers)
+            self.GY, self.XtX = self.fws["GY"], self.fws["XX"]
         N = m * k
         self.N = N
         self.dense_gn = p.schur_solver == "dense"
         self.A = None  # dense mk x mk reduced matrix: allocated on first full-C / dense use
+        self.t4work = None
         self.rhs = b(N)
         self.dYbuf = b(m, k)
         Q = k * k
@@ -540,8 +561,9 @@ class IpmEngine:
         n, m, k, N, s = self.n, self.m, self.k, self.N, P.stream
         mux, muy = self.wx * self.mu, self.wy * self.mu
         X, Yt, F = self.X, self.Yt, self.Fcur
-        P.colprod(Yt, m, k, Yt, k, self.GY)
-        P.colprod(X, n, k, X, k, self.XtX, reduce=True)
+        if not self.ffree:  # residual-free: YY^T and X^T X come from the refresh at this point
+            P.colprod(Yt, m, k, Yt, k, self.GY)
+            P.colprod(X, n, k, X, k, self.XtX, reduce=True)
         dense = full or self.dense_gn or force_dense
         P._call("nmfb_r1_factor", _p(self.GY), _p(X), _p(self.R), _p(self.gX), mux, self.rho, n,
                 k, _p(self.L), _p(self.h), _p(self.g), _p(self.Apk), _p(self.XXpk),
@@ -570,7 +592,10 @@ class IpmEngine:
             if full:
                 if self.comm.active and not self.comm.root:
                     self.A.zero_()  # rank 0 carries the replicated part, others only term 4
-                P._call("nmfb_schur_term4", _p(F), n, m, k, _p(self.Apk), _p(self.A), s)
+                if self.t4work is None:
+                    self.t4work = P.buf(max(P.lib.nmfb_term4_work_len(n, m, k), 1))
+                P._call("nmfb_schur_term4", _p(F), n, m, k, _p(self.Apk), _p(self.A),
+                        _p(self.t4work), self.t4work.numel(), s)
                 self.comm.sum_(self.A)
             P._call("nmfb_dense_cholesky", _p(self.A), N, _p(P.iscal[3:]), s)
             dY.copy_(self.rhs.view(m, k))
@@ -628,13 +653,9 @@ class IpmEngine:
         n, m, k = self.n, self.m, self.k
         X, Yt, dX = self.X, self.Yt, self.dX
         P.rowprod(P.M, n, m, dY, k, self.MdY, None, P.f32)
-        P.colprod(dX, n, k, dX, k, self.A1, reduce=True)
-        P.colprod(dX, n, k, X, k, self.A2, reduce=True)
-        P.colprod(dY, m, k, dY, k, self.B1)
-        P.colprod(Yt, m, k, dY, k, self.B2)
-        P.colprod(dX, n, k, self.gX, k, self.Dgx, reduce=True)
-        P.colprod(dY, m, k, self.gY, k, self.Dgy)
-        P.colprod(dX, n, k, self.MdY, k, self.Dmd, reduce=True)
+        P.grams([(dX, dX, self.A1), (dX, X, self.A2), (dX, self.gX, self.Dgx),
+                 (dX, self.MdY, self.Dmd)], n, k, reduce=True)
+        P.grams([(dY, dY, self.B1), (Yt, dY, self.B2), (dY, self.gY, self.Dgy)], m, k)
         P._call("nmfb_ffree_quartic", _p(self.A1), _p(self.A2), _p(self.XtX), _p(self.B1),
                 _p(self.B2), _p(self.GY), _p(self.Dgx), _p(self.Dgy), _p(self.Dmd), k,
                 _p(P.dscal), s)

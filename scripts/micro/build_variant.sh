@@ -1,7 +1,7 @@
 #!/bin/bash
-# usage: build_variant.sh <persist.cu variant> <out .so>   (other objects from build/nmfb200)
+# usage: build_variant.sh <variant .cu> <object name it replaces, e.g. persist.o> <out .so>
 set -e
 cd /root/repo
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I paper_2101_08431_b200/csrc -I include -c "$1" -o /tmp/variant_persist.o
-objs=$(ls build/nmfb200/*.o | grep -v persist.o)
-nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$2" $objs /tmp/variant_persist.o -lcudart
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I paper_2101_08431_b200/csrc -I include -c "$1" -o /tmp/variant_obj.o
+objs=$(ls build/nmfb200/*.o | grep -v "/$2\$")
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$3" $objs /tmp/variant_obj.o -lcudart
