@@ -737,12 +737,16 @@ extern "C" int nmfb_surface_nnls_batch(const double* ctc, const double* ctb, con
   if (nrhs == 0) return NMFB_OK;
   const int threads = 128;
   const int blocks = (int)((nrhs + threads - 1) / threads);
-  // warp per rhs (k_nnls_warp, exact-k template); NMFB_NNLS_THREAD=1 selects the
-  // thread-per-rhs kernel (same bits, kept as the reference formulation)
-  static const bool thread_kernel = [] {
+  // Same bits either way.  Warp per rhs (k_nnls_warp) wins when the batch cannot
+  // fill the GPU with one thread per rhs (B200: c4's 5000 Y columns 3.9x faster);
+  // thread per rhs (k_nnls) wins on large batches and k >= 12 (c4's 20000 rows,
+  // c5).  NMFB_NNLS_THREAD=1 / =0 forces one or the other.
+  static const int force = [] {
     const char* e = getenv("NMFB_NNLS_THREAD");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
+  const bool thread_kernel =
+      force >= 0 ? force == 1 : !((nrhs <= 8192 && k <= 12) || nrhs <= 2048);
 #define WCASE(KW, SEEDS, MODE)                                                                   \
   case KW: {                                                                                     \
     constexpr int WW = KW <= 4 ? 4 : (KW <= 8 ? 8 : 16);                                         \

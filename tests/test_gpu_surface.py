@@ -77,11 +77,13 @@ def _nmf_like(rng, nrhs, k, drift):
     return ctc, ctb, np.einsum("ij,ij->i", D, D), 1e-12 * np.maximum(1, np.abs(ctb).max(1))
 
 
-@pytest.mark.parametrize("k", (3, 4, 10, 16))
+@pytest.mark.parametrize("k,nrhs", [(3, 5000), (4, 5000), (10, 5000), (16, 5000), (4, 20000),
+                                     (10, 12000)])
 @pytest.mark.parametrize("mode", (0, 1, 2))
-def test_nnls_large_vs_oracle(K, k, mode):
+def test_nnls_large_vs_oracle(K, k, nrhs, mode):
+    """Bit-identical to the reference on both device formulations: warp per rhs
+    (small batches) and thread per rhs (batches > 8192 or k > 12)."""
     rng = np.random.default_rng(1000 + 10 * k + mode)
-    nrhs = 5000
     ctc, ctb, btb, tol = _nmf_like(rng, nrhs, k, 0.05)
     seed = ok.nnls_batch(ctc, ctb * 1.01, btb, np.zeros((nrhs, k), bool), 0, tol, 3 * k)[1]
     ref = ok.nnls_batch(ctc, ctb, btb, seed, mode, tol, 3 * k)
