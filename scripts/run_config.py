@@ -20,7 +20,7 @@ def main():
     ap.add_argument("name")
     ap.add_argument("--ipm", type=int, default=None)
     ap.add_argument("--sweeps", type=int, default=None)
-    ap.add_argument("--barrier", default="paper")
+    ap.add_argument("--barrier", default="balanced")
     a = ap.parse_args()
     cfg = data.CONFIGS[a.name]
     dev = torch.device("cuda", 0)
