@@ -277,6 +277,23 @@ int nmfb_grams(int count, const double *A0, const double *B0, double *O0, const 
                const double *A3, const double *B3, double *O3, long rows, long k, double *work,
                long work_len, void *stream);
 
+
+/* Persistent stage 1 for small problems (csrc/stage1_persist.cu, k <= 8): every ANLS
+ * sweep of run_stage1 in one cooperative launch, the same
+ * bit-exact NNLS as nmfb_surface_nnls_batch.  X (n x k), Yt (m x k), pX, pY are
+ * updated in place; Xn is unused scratch; Yn (m x k) is scratch; stX / stY receive
+ * the per-rhs NNLS status of the last sweep.  tol_fixed < 0: per-rhs tolerance
+ * 1e-12 max(1, ||ctb||_inf).  first_mode: 0 cold, 2 seeded from pX / pY.  fixed: run
+ * exactly max_sweeps.  logv: per sweep [0.5 sum r2, step, norm, -]; status (device
+ * int[3]) = [sweeps, converged, failed]. */
+int nmfb_stage1_persist_supported(long n, long m, long k);
+long nmfb_stage1_persist_work_len(long n, long m, long k);
+int nmfb_stage1_persist(const void *M, int m_is_f32, long n, long m, long k, double *X, double *Yt,
+                        double *Xn, double *Yn, uint8_t *pX, uint8_t *pY, const double *row_n2,
+                        const double *col_n2, int8_t *stX, int8_t *stY, double tol_fixed,
+                        int first_mode, int max_sweeps, int fixed, double eps_stol, double *logv,
+                        int *status, double *work, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

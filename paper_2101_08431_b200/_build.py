@@ -28,6 +28,7 @@ SOURCES = {
     "lowrank.cu": [],
     "small.cu": [],
     "persist.cu": [],
+    "stage1_persist.cu": ["-fmad=false"],
     "runtime.cu": [],
 }
 

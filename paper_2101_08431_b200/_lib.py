@@ -66,6 +66,9 @@ SIGNATURES = {
     "nmfb_small_supported": [L, L, L],
     "nmfb_persist_supported": [L, L, L, I],
     "nmfb_grams_work_len": [L, L, L],
+    "nmfb_stage1_persist_supported": [L, L, L],
+    "nmfb_stage1_persist_work_len": [L, L, L],
+    "nmfb_stage1_persist": [P, I, L, L, L] + [P] * 10 + [D, I, I, I, D, P, P, P, P],
     "nmfb_grams": [I] + [P] * 12 + [L, L, P, L, P],
     "nmfb_persist_work_len": [L, L, L, I],
     "nmfb_ipm_persist": [P, I, L, L, L] + [P] * 14 + [D] * 8 + [I, I, I] + [P] * 6 + [I, P, P],
@@ -78,7 +81,8 @@ SIGNATURES = {
 RESTYPES = {"nmfb_colprod_work_len": ctypes.c_long, "nmfb_rowprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
             "nmfb_launch_count": ctypes.c_ulonglong, "nmfb_small_work_len": ctypes.c_long,
             "nmfb_persist_work_len": ctypes.c_long, "nmfb_grams_work_len": ctypes.c_long,
-            "nmfb_term4_work_len": ctypes.c_long}
+            "nmfb_term4_work_len": ctypes.c_long,
+            "nmfb_stage1_persist_work_len": ctypes.c_long}
 
 _lib = None
 

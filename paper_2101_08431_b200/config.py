@@ -18,6 +18,7 @@ class Stage1Config:
     max_sweeps: int = 200
     tol_kkt: float | None = None  # None: 1e-12 * max(1, ||C^T d||_inf) per rhs
     fixed_sweeps: int = 0  # > 0: exactly this many sweeps, no step test (configs c4/c5)
+    persistent: bool = True  # small problems: all sweeps in one launch (csrc/stage1_persist.cu)
 
 
 @dataclass

@@ -11,6 +11,8 @@
 // All reductions use a fixed decomposition that depends only on the problem
 // shape, so results are bit-reproducible run to run.  M may be float64 or
 // float32 (config c5 stores M in fp32; products accumulate in fp64).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "nmfb200.h"
 
@@ -700,7 +702,12 @@ long rowprod_chunks(long cols) {
 template <int K, typename T>
 int launch_rowprod(const T* A, long rows, long cols, const double* B, double* out, double* tol,
                    double scale, double* work, long work_len, cudaStream_t st) {
-  if (rowprod_split(rows, cols) && (cols % 2 == 0) && K >= 5) {  // tensor-core streaming path
+  static const bool f32_simt = [] {
+    const char* e = getenv("NMFB_F32_SIMT");
+    return e && e[0] == '1';
+  }();
+  const bool use_mma = !(sizeof(T) == 4 && f32_simt);
+  if (use_mma && rowprod_split(rows, cols) && (cols % 2 == 0) && K >= 5) {  // tensor-core streaming path
     constexpr int NT = (K + 7) / 8;
     const long nch = (cols + MMA_CW - 1) / MMA_CW;
     if (nch * rows * K > work_len) return NMFB_ENOMEM;

@@ -21,6 +21,7 @@
 // formulations of the same quantities; these kernels are the parity surface.
 #include "common.cuh"
 #include "nmfb200.h"
+#include "nnls_warp.cuh"
 
 #include <climits>
 #include <cstdlib>
@@ -232,103 +233,6 @@ __global__ void __launch_bounds__(128) k_nnls(const double* __restrict__ ctc_g,
 }
 
 
-// --------------------------------------------------------------------------
-// nnls_batch, warp per right-hand side (production path, same bits as k_nnls):
-// lane j owns index j (d_j, x_j, w_j, z_j, row j of the passive Cholesky factor
-// and row j of ctc).  Every scalar goes through the reference's operation
-// sequence: column-oriented sweeps subtract terms in the reference's index
-// order, the backward solve gathers its terms in ascending order with
-// shuffles, argmax keeps the first maximum (ballot), and the file is compiled
-// with -fmad=false.  The passive set is a lane mask, uniform across the warp.
-// --------------------------------------------------------------------------
-// Several right-hand sides share a warp when k is small: segment width W (a power
-// of two >= k) carries one rhs; segments diverge freely (per-segment masks and
-// width-W shuffles), which interleaves independent dependency chains.
-template <int K, int W>
-struct WNnls {
-  double Lr[K];  // row `sl` of L (global column index)
-  double C[K];   // row `sl` of ctc
-  int sl;        // lane within the segment
-  unsigned sm;   // segment mask (lanes of this rhs)
-
-  __device__ __forceinline__ double sh(double v, int src) const { return __shfl_sync(sm, v, src, W); }
-
-  __device__ __forceinline__ bool factor(unsigned pm) {
-#pragma unroll
-    for (int c = 0; c < K; ++c) Lr[c] = 0.0;
-    bool ok = true;
-#pragma unroll
-    for (int gj = 0; gj < K; ++gj) {
-      if (!ok || !((pm >> gj) & 1u)) continue;
-      double acc = C[gj];  // lane gj: ctc[gj][gj]; lane gi: ctc[gi][gj]
-#pragma unroll
-      for (int gp = 0; gp < gj; ++gp) {
-        if (!((pm >> gp) & 1u)) continue;
-        const double ljp = sh(Lr[gp], gj);
-        acc = acc - Lr[gp] * ljp;
-      }
-      const double accj = sh(acc, gj);
-      if (accj <= 0.0) {
-        ok = false;
-        continue;
-      }
-      const double ljj = sqrt(accj);
-      const bool below = sl > gj && sl < K && ((pm >> sl) & 1u);
-      const double lij = acc / ljj;
-      Lr[gj] = (sl == gj) ? ljj : (below ? lij : Lr[gj]);
-    }
-    return ok;
-  }
-
-  // z <- (L L^T)^{-1} b on the passive lanes (chol_solve_small order)
-  __device__ __forceinline__ double solve(unsigned pm, double b) const {
-    double acc = b, zf = 0.0;
-#pragma unroll
-    for (int gi = 0; gi < K; ++gi) {
-      if (!((pm >> gi) & 1u)) continue;
-      const double zi = sh(acc / Lr[gi], gi);
-      zf = (sl == gi) ? zi : zf;
-      const double nacc = acc - Lr[gi] * zi;
-      acc = (sl > gi && sl < K && ((pm >> sl) & 1u)) ? nacc : acc;
-    }
-    double zb = 0.0;
-#pragma unroll
-    for (int gi = K - 1; gi >= 0; --gi) {
-      if (!((pm >> gi) & 1u)) continue;
-      double a = zf;
-#pragma unroll
-      for (int gp = gi + 1; gp < K; ++gp) {
-        if (!((pm >> gp) & 1u)) continue;
-        a = a - sh(Lr[gi] * zb, gp);  // L[gp][gi] z[gp], gp ascending
-      }
-      const double zi = a / Lr[gi];
-      zb = (sl == gi) ? zi : zb;
-    }
-    return zb;
-  }
-
-  // _passive_solve_refined: z = solve(d); r = d - C_PP z; z += solve(r)
-  __device__ __forceinline__ double solve_refined(unsigned pm, double d) const {
-    const double z = solve(pm, d);
-    double acc = d;
-#pragma unroll
-    for (int gp = 0; gp < K; ++gp) {
-      if (!((pm >> gp) & 1u)) continue;
-      acc = acc - C[gp] * sh(z, gp);
-    }
-    const double dz = solve(pm, acc);
-    return z + dz;
-  }
-
-  // w_j = d_j - sum_p ctc[j][p] x_p (p ascending, all p)
-  __device__ __forceinline__ double grad(double d, double x) const {
-    double acc = d;
-#pragma unroll
-    for (int p = 0; p < K; ++p) acc = acc - C[p] * sh(x, p);
-    return acc;
-  }
-};
-
 template <int K, int W>
 __global__ void __launch_bounds__(128) k_nnls_warp(const double* __restrict__ ctc_g,
                                                    const double* __restrict__ ctb,
@@ -351,109 +255,24 @@ __global__ void __launch_bounds__(128) k_nnls_warp(const double* __restrict__ ct
   s.sl = lane % W;
   s.sm = (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << (seg * W));
   const int sl = s.sl;
-  const unsigned sm = s.sm;
-  const int shift = seg * W;
   const bool own = sl < K;
 #pragma unroll
   for (int c = 0; c < K; ++c) s.C[c] = own ? ctc[sl * K + c] : 0.0;
   const double d = own ? ctb[t * K + sl] : 0.0;
-  const double tol_t = tol[t];
-  double x = 0.0, w = 0.0;
-  unsigned pm = 0u;
-  bool solved = false;
-  long nch = 0;
   const bool use_seed = (seed_mode == 2) || (seed_mode == 1 && t > 0);
-  if (use_seed) {
-    const bool spas = own && seeds[t * K + sl] != 0;
-    pm = (__ballot_sync(sm, spas) >> shift) & ((W == 32) ? 0xffffffffu : ((1u << W) - 1u));
-    if (pm == 0u) {
-      if (!__any_sync(sm, own && d > tol_t)) {
-        x = 0.0;
-        solved = true;
-      }
-    } else if (s.factor(pm)) {
-      const double z = s.solve_refined(pm, d);
-      const bool passive = own && ((pm >> sl) & 1u);
-      if (!__any_sync(sm, passive && z < 0.0)) {
-        x = passive ? z : 0.0;
-        const double wj = s.grad(d, x);
-        const bool bad = own && (passive ? (fabs(wj) > tol_t) : (wj > tol_t));
-        w = wj;
-        solved = !__any_sync(sm, bad);
-      }
-    }
-  }
-  int st = 0;
-  if (!solved) {
-    pm = 0u;
-    x = 0.0;
-    w = d;
-    for (;;) {
-      const bool cand = own && !((pm >> sl) & 1u) && w > tol_t;
-      double v = cand ? w : -1.0 / 0.0;
-#pragma unroll
-      for (int o = W / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(sm, v, o, W));
-      const unsigned hit = (__ballot_sync(sm, cand && w == v) >> shift);
-      const unsigned hits = (W == 32) ? hit : (hit & ((1u << W) - 1u));
-      if (hits == 0u) break;
-      const int jmax = __ffs(hits) - 1;  // first maximum, as the sequential scan
-      pm |= 1u << jmax;
-      nch += 1;
-      if (nch > max_changes) {
-        st = 1;
-        break;
-      }
-      for (;;) {
-        if (pm == 0u) break;
-        if (!s.factor(pm)) {
-          st = 2;
-          break;
-        }
-        const double z = s.solve_refined(pm, d);
-        const bool passive = own && ((pm >> sl) & 1u);
-        if (!__any_sync(sm, passive && z <= 0.0)) {
-          x = passive ? z : 0.0;
-          break;
-        }
-        const bool neg = passive && z <= 0.0;
-        const double ratio = neg ? x / (x - z) : 1.0 / 0.0;
-        double alpha = ratio;
-#pragma unroll
-        for (int o = W / 2; o > 0; o >>= 1) alpha = fmin(alpha, __shfl_xor_sync(sm, alpha, o, W));
-        alpha = alpha < 1.0 ? alpha : 1.0;
-        const double newx = x + alpha * (z - x);
-        const bool drop = neg && ratio <= alpha;
-        if (passive) x = drop ? 0.0 : (newx > 0.0 ? newx : 0.0);
-        const unsigned dmw = __ballot_sync(sm, drop) >> shift;
-        const unsigned dm = (W == 32) ? dmw : (dmw & ((1u << W) - 1u));
-        pm &= ~dm;
-        nch += __popc(dm);
-        if (nch > max_changes) {
-          st = 1;
-          break;
-        }
-      }
-      if (st != 0) break;
-      w = s.grad(d, x);
-    }
-  }
-  // outputs; r2 = btb - sum_j (2 x_j) d_j + sum_j x_j (ctc x)_j, j ascending
-  double acc2 = 0.0;
-#pragma unroll
-  for (int p = 0; p < K; ++p) acc2 = acc2 + s.C[p] * s.sh(x, p);
-  const double t1 = 2.0 * x * d, t2 = x * acc2;
-  double r2 = btb[t];
-#pragma unroll
-  for (int j = 0; j < K; ++j) r2 = r2 - s.sh(t1, j);
-#pragma unroll
-  for (int j = 0; j < K; ++j) r2 = r2 + s.sh(t2, j);
+  const bool sp = use_seed && own && seeds[t * K + sl] != 0;
+  double x, r2;
+  unsigned pm;
+  long nch;
+  int st;
+  nnls_seg_solve<K, W>(s, d, btb[t], tol[t], use_seed, sp, max_changes, x, pm, nch, r2, st);
   if (own) {
     x_out[t * K + sl] = x;
     p_out[t * K + sl] = ((pm >> sl) & 1u) ? 1 : 0;
   }
   if (sl == 0) {
     ch_out[t] = nch;
-    r2_out[t] = r2 > 0.0 ? r2 : 0.0;
+    r2_out[t] = r2;
     st_out[t] = (int8_t)st;
   }
 }

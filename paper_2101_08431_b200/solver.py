@@ -274,6 +274,9 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
     res = Stage1Result(None, None, None, None, 0, False)
     nsweeps = cfg.fixed_sweeps if cfg.fixed_sweeps > 0 else cfg.max_sweeps
     s = P.stream
+    if (cfg.persistent and not P.comm.active and nsweeps > 0
+            and P.lib.nmfb_stage1_persist_supported(n, m, k)):
+        return _stage1_persistent(P, X, Yt, pX, pY, Yn, stX, stY, have_carry, cfg, nsweeps, res, t0)
     for sweep in range(nsweeps):
         mode = 2 if (sweep > 0 or have_carry) else 0
         # X-update: C = Y^T, d = rows of M
@@ -317,6 +320,36 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
             res.converged = True
             break
     res.seconds = time.perf_counter() - t0
+    return X, Yt, pX, pY, res
+
+
+def _stage1_persistent(P, X, Yt, pX, pY, Yn, stX, stY, have_carry, cfg, nsweeps, res, t0):
+    """All sweeps of run_stage1 in one cooperative launch (csrc/stage1_persist.cu)."""
+    n, m, k = P.n, P.m, P.k
+    log = P.buf(nsweeps, 4)
+    stat = torch.zeros(3, dtype=torch.int32, device=P.dev)
+    work = P.buf(max(P.lib.nmfb_stage1_persist_work_len(n, m, k), 1))
+    tol = -1.0 if cfg.tol_kkt is None else float(cfg.tol_kkt)
+    P._call("nmfb_stage1_persist", _p(P.M), P.f32, n, m, k, _p(X), _p(Yt), None, _p(Yn),
+            _p(pX), _p(pY), _p(P.row_n2), _p(P.col_n2), _p(stX), _p(stY), tol,
+            2 if have_carry else 0, nsweeps, 1 if cfg.fixed_sweeps > 0 else 0, cfg.eps_stol,
+            _p(log), _p(stat), _p(work), P.stream, tag="stage1_persist")
+    st = stat.cpu().numpy()
+    sweeps, conv, failed = int(st[0]), bool(st[1]), bool(st[2])
+    if failed:
+        for which, arr in (("update_X", stX), ("update_Y", stY)):
+            bad = torch.nonzero(arr).flatten()
+            if bad.numel():
+                i = int(bad[0])
+                raise status_error(int(arr[i].item()), i, which)
+    lg = log[:sweeps].cpu().numpy()
+    t1 = time.perf_counter()
+    for i in range(sweeps):
+        res.trace.append((t0 + (t1 - t0) * (i + 1) / sweeps - t0, float(lg[i, 0]), float(lg[i, 1])))
+    res.sweeps = sweeps
+    res.converged = conv
+    res.seconds = time.perf_counter() - t0
+    P.stage1_persist_sweeps = getattr(P, "stage1_persist_sweeps", 0) + sweeps
     return X, Yt, pX, pY, res
 
 

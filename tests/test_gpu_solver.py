@@ -38,15 +38,22 @@ def _instance(data, name, n=None, m=None):
     return data.dense(n or cfg.n, m or cfg.m, cfg.k, cfg.seed)[:3]
 
 
-@pytest.mark.parametrize("name,n,m", [("c1", None, None), ("c2", None, None),
-                                      ("c3", None, 60), ("c4", 2000, 300)])
-def test_stage1_parity(mods, name, n, m):
+@pytest.mark.parametrize("name,n,m,persistent", [
+    ("c1", None, None, True), ("c2", None, None, True), ("c3", None, 60, True),
+    ("c4", 2000, 300, True), ("c2", None, None, False), ("c3", None, 500, True),
+    ("c3", None, 500, False)])
+def test_stage1_parity(mods, name, n, m, persistent):
+    """Same sweeps, passive sets and factors as the oracle, through the persistent
+    one-launch stage 1 (csrc/stage1_persist.cu, k <= 8) and the per-sweep kernels."""
     data, solver, IpmParams, Stage1Config = mods
     M, X0, Y0 = _instance(data, name, n, m)
     k = X0.shape[1]
-    cfg = Stage1Config(fixed_sweeps=8) if name == "c4" else Stage1Config()
+    cfg = Stage1Config(fixed_sweeps=8, persistent=persistent) if name == "c4" else \
+        Stage1Config(persistent=persistent)
     P = solver.Problem(M, k)
     X, Yt, pX, pY, r = solver.run_stage1(P, P.to_dev(X0), P.to_dev(Y0.T), cfg)
+    if persistent and k <= 8:
+        assert getattr(P, "stage1_persist_sweeps", 0) == r.sweeps
     ro = D.run_stage1(M, X0, Y0.T.copy(), D.Stage1Config(fixed_sweeps=cfg.fixed_sweeps))
     assert r.sweeps == ro.sweeps
     assert np.array_equal(pX.bool().cpu().numpy(), ro.pX)
