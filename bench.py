@@ -269,6 +269,9 @@ def run_b200(args):
     Mh = torch.from_numpy(M).pin_memory()
     e2e_ms, e2e_units = 0.0, 0
     ne2e = max(1, min(args.steps, 3))
+    # one untimed call first: the public API builds a fresh Problem per call, and the
+    # first one after the timed region pays the caching allocator's cudaMalloc
+    run_two_stage(Mh, X0, Y0, tol_rel=cfg.tol, ipm=IpmParams(max_iter=IPM_CAP), e_scale=e_scale)
     for _ in range(ne2e):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
