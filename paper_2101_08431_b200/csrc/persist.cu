@@ -137,6 +137,46 @@ __device__ __forceinline__ void reduce_entries(const double* part, int G, long e
   }
 }
 
+// As reduce_entries, with the reduction kind chosen per entry (kind_of(e): 0 sum,
+// 1 min, 2 max) so differently-typed partials share one round trip to L2.
+template <int EB, typename KF, bool OUTG = false>
+__device__ __forceinline__ void reduce_mixed(const double* part, int G, long e0, long e1,
+                                             double* out, KF kind_of, int warp_lo = 0,
+                                             int warp_n = NW) {
+  const int lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) - warp_lo;
+  if (wid < 0 || wid >= warp_n) return;
+#pragma unroll 1
+  for (long eb = e0 + (long)wid * EB; eb < e1; eb += (long)warp_n * EB) {
+    double v[EB][5];
+    int kd[EB];
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
+      kd[b] = (eb + b < e1) ? kind_of(eb + b) : 0;
+      const double idv = kd[b] == 0 ? 0.0 : (kd[b] == 1 ? 1.0 / 0.0 : -1.0 / 0.0);
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        const int c = lane + 32 * u;
+        v[b][u] = (eb + b < e1 && c < G) ? ldcg(part + (eb + b) * G + c) : idv;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
+      double s = v[b][0];
+#pragma unroll
+      for (int u = 1; u < 5; ++u)
+        s = kd[b] == 0 ? s + v[b][u] : (kd[b] == 1 ? fmin(s, v[b][u]) : fmax(s, v[b][u]));
+      s = kd[b] == 0 ? warp_sum(s) : (kd[b] == 1 ? warp_min(s) : warp_max(s));
+      if (lane == 0 && eb + b < e1) {
+        if (OUTG)
+          __stcg(out + (eb + b - e0), s);
+        else
+          out[eb + b - e0] = s;
+      }
+    }
+  }
+}
+
 // Cholesky of a Q x Q smem matrix by warp 0 with the rows in registers (lane = row,
 // column j broadcast by shuffles); the strict upper triangle is zeroed and the
 // reciprocal diagonal 1/L_jj stored in dinv[Q].  Returns the failing pivot (-1: PD)
@@ -517,8 +557,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         }
       }
       constexpr int EBA = (SA + NW - 1) / NW < 8 ? (SA + NW - 1) / NW : 8;
-      reduce_entries<EBA, 0>(PA, G, 0, SA - 1, ZHX);
-      reduce_entries<1, 1>(PA, G, SA - 1, SA, ZHX + SA - 1);
+      reduce_mixed<EBA>(PA, G, 0, SA, ZHX, [&](long e) { return e == SA - 1 ? 1 : 0; });
       if (it > 0) {
 #pragma unroll
         for (int q = 0; q < NGY; ++q) {
@@ -923,9 +962,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
 
     // ======== phase C: Armijo (quartic + barrier trials in batches) ========
     // [3] gtp_x [4] a1x [5] a2x [6..11] quartic
-    reduce_entries<2, 1>(PB, G, 1, 3, scal + 4);
-    reduce_entries<1, 0>(PB, G, 0, 1, scal + 3);
-    reduce_entries<1, 0>(PB, G, 3, 9, scal + 6);
+    reduce_mixed<2>(PB, G, 0, 9, scal + 3, [](long e) { return (e == 1 || e == 2) ? 1 : 0; });
     __syncthreads();
     const double gtp = scal[3] + scal[0];
     const double a1max = fmin(fmin(1.0, scal[4]), scal[1]);
@@ -958,29 +995,37 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
       grid_barrier(a.bar, epoch);
       reduce_entries<2, 0>(pc, G, 0, 2 * TB, bars);
       __syncthreads();
-      if (tid == 0) {
-        // same arithmetic as armijo_pick (csrc/small.cu) / the host loop
+      if (tid < 32) {
+        // lane q evaluates trial t0 + q with the arithmetic of armijo_pick (csrc/small.cu)
+        // and of the host loop; the first lane that accepts (or passes max_bt) decides
         const double c2 = __dadd_rn(__dmul_rn(0.5, bb), ac);
-        int t = t0, res = -1;
-        for (; t < t0 + TB; ++t) {
+        const int t = t0 + lane;
+        bool acc = false, stall = false;
+        if (lane < TB) {
           if (t > a.max_bt) {
-            res = -3;  // stall
-            break;
-          }
-          const double a1 = ldexp(a1max, -t);  // == a1max / 2^t exactly
-          const double q2 = __dmul_rn(a1, a1), q3 = __dmul_rn(q2, a1), q4 = __dmul_rn(q3, a1);
-          double quad = __dadd_rn(__dmul_rn(a1, ab), __dmul_rn(q2, c2));
-          quad = __dadd_rn(quad, __dmul_rn(q3, bc));
-          quad = __dadd_rn(quad, __dmul_rn(__dmul_rn(0.5, q4), cc));
-          const double bar = __dadd_rn(__dmul_rn(a.wx, bars[2 * (t - t0)]),
-                                       __dmul_rn(a.wy, bars[2 * (t - t0) + 1]));
-          const double dphi = __dsub_rn(quad, __dmul_rn(a.mu, bar));
-          if (dphi <= __dmul_rn(__dmul_rn(a.eta, a1), gtp)) {
-            res = t;
-            break;
+            stall = true;
+          } else {
+            const double a1 = ldexp(a1max, -t);  // == a1max / 2^t exactly
+            const double q2 = __dmul_rn(a1, a1), q3 = __dmul_rn(q2, a1), q4 = __dmul_rn(q3, a1);
+            double quad = __dadd_rn(__dmul_rn(a1, ab), __dmul_rn(q2, c2));
+            quad = __dadd_rn(quad, __dmul_rn(q3, bc));
+            quad = __dadd_rn(quad, __dmul_rn(__dmul_rn(0.5, q4), cc));
+            const double bar = __dadd_rn(__dmul_rn(a.wx, bars[2 * lane]),
+                                         __dmul_rn(a.wy, bars[2 * lane + 1]));
+            const double dphi = __dsub_rn(quad, __dmul_rn(a.mu, bar));
+            acc = dphi <= __dmul_rn(__dmul_rn(a.eta, a1), gtp);
           }
         }
-        s_t = (res == -1 && t > a.max_bt) ? -3 : res;
+        const unsigned hit = __ballot_sync(0xffffffffu, acc || stall);
+        if (lane == 0) {
+          if (hit == 0u) {
+            s_t = -1;
+          } else {
+            const int q = __ffs(hit) - 1;
+            const bool st_q = (t0 + q) > a.max_bt;
+            s_t = st_q ? -3 : t0 + q;
+          }
+        }
       }
       __syncthreads();
       tsel = s_t;
@@ -1015,57 +1060,78 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     }
     __syncthreads();
     double kv[7] = {0.0, 0.0, 0.0, 0.0, 0.0, -1.0 / 0.0, -1.0 / 0.0};  // fsq, k0..k3, kg, kx
-    #pragma unroll 1
-    for (int rr = wid; rr < nr; rr += NW) {
-      const long i = r0 + rr;
-      double x[K], g[K];
+    // warps [0, NW/2): rows, two per warp in flight (F, graX, ||F||^2, X-part KKT);
+    // warps [NW/2, NW): graY partials, thread per column; the two run concurrently
+    if (wid < NW / 2) {
+      constexpr int HW = NW / 2;
+#pragma unroll 1
+      for (int rb = wid; rb < nr; rb += 2 * HW) {
+        const int rr2[2] = {rb, rb + HW};
+        double x[2][K], g[2][K];
 #pragma unroll
-      for (int p = 0; p < K; ++p) {
-        x[p] = xs[rr * K + p];
-        g[p] = 0.0;
-      }
-      #pragma unroll 1
-      for (long j = lane; j < m; j += 32) {
-        double fv = -Mp[(long)rr * m + j];
+        for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int p = 0; p < K; ++p) fv = fma(x[p], Ys[j * K + p], fv);
-        a.Fout[i * m + j] = fv;
-        kv[0] = fma(fv, fv, kv[0]);
+          for (int p = 0; p < K; ++p) {
+            x[u][p] = rr2[u] < nr ? xs[rr2[u] * K + p] : 0.0;
+            g[u][p] = 0.0;
+          }
+#pragma unroll 1
+        for (long j = lane; j < m; j += 32) {
+          double y[K];
 #pragma unroll
-        for (int p = 0; p < K; ++p) g[p] = fma(fv, Ys[j * K + p], g[p]);
-      }
+          for (int p = 0; p < K; ++p) y[p] = Ys[j * K + p];
 #pragma unroll
-      for (int p = 0; p < K; ++p) g[p] = warp_sum(g[p]);
-      if (lane == 0) {
+          for (int u = 0; u < 2; ++u) {
+            if (rr2[u] >= nr) continue;
+            double fv = -Mp[(long)rr2[u] * m + j];
 #pragma unroll
-        for (int p = 0; p < K; ++p) {
-          gxs[rr * K + p] = g[p];
-          const double r = rs[rr * K + p];
-          const double xr = x[p] * r;
-          kv[1] = fma(g[p] - r, g[p] - r, kv[1]);
-          kv[2] = fma(xr - mux, xr - mux, kv[2]);
-          kv[3] = fma(xr, xr, kv[3]);
-          kv[4] += xr;
-          kv[5] = fmax(kv[5], fabs(g[p]));
-          kv[6] = fmax(kv[6], x[p]);
+            for (int p = 0; p < K; ++p) fv = fma(x[u][p], y[p], fv);
+            a.Fout[(r0 + rr2[u]) * m + j] = fv;
+            kv[0] = fma(fv, fv, kv[0]);
+#pragma unroll
+            for (int p = 0; p < K; ++p) g[u][p] = fma(fv, y[p], g[u][p]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int p = 0; p < K; ++p) g[u][p] = warp_sum(g[u][p]);
+        if (lane == 0) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (rr2[u] >= nr) continue;
+#pragma unroll
+            for (int p = 0; p < K; ++p) {
+              gxs[rr2[u] * K + p] = g[u][p];
+              const double r = rs[rr2[u] * K + p];
+              const double xr = x[u][p] * r;
+              kv[1] = fma(g[u][p] - r, g[u][p] - r, kv[1]);
+              kv[2] = fma(xr - mux, xr - mux, kv[2]);
+              kv[3] = fma(xr, xr, kv[3]);
+              kv[4] += xr;
+              kv[5] = fmax(kv[5], fabs(g[u][p]));
+              kv[6] = fmax(kv[6], x[u][p]);
+            }
+          }
         }
       }
-    }
-    #pragma unroll 1
-    for (long j = tid; j < m; j += PT) {
-      double acc[K];
+    } else {
+#pragma unroll 1
+      for (long j = tid - PT / 2; j < m; j += PT / 2) {
+        double acc[K];
 #pragma unroll
-      for (int p = 0; p < K; ++p) acc[p] = 0.0;
-      #pragma unroll 1
-      for (int rr = 0; rr < nr; ++rr) {
-        double fv = -Mp[(long)rr * m + j];
+        for (int p = 0; p < K; ++p) acc[p] = 0.0;
+#pragma unroll 1
+        for (int rr = 0; rr < nr; ++rr) {
+          double fv = -Mp[(long)rr * m + j];
 #pragma unroll
-        for (int p = 0; p < K; ++p) fv = fma(xs[rr * K + p], Ys[j * K + p], fv);
+          for (int p = 0; p < K; ++p) fv = fma(xs[rr * K + p], Ys[j * K + p], fv);
 #pragma unroll
-        for (int p = 0; p < K; ++p) acc[p] = fma(fv, xs[rr * K + p], acc[p]);
+          for (int p = 0; p < K; ++p) acc[p] = fma(fv, xs[rr * K + p], acc[p]);
+        }
+#pragma unroll
+        for (int p = 0; p < K; ++p) __stcg(PG + (j * K + p) * G + cta, acc[p]);
       }
-#pragma unroll
-      for (int p = 0; p < K; ++p) __stcg(PG + (j * K + p) * G + cta, acc[p]);
     }
     {
       block_reduce_all<7, 0, 0x60>(kv, red);
@@ -1089,9 +1155,10 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     // ======== phase E: graY slice totals; X-part KKT sums and ||F||^2 ========
     {
       const long e0 = (long)cta * N / G, e1 = (long)(cta + 1) * N / G;
-      reduce_entries<2, 0>(PG, G, e0, e1, a.gY + e0, true);
-      reduce_entries<1, 0>(PD, G, 0, 5, kx);
-      reduce_entries<1, 2>(PD, G, 5, 7, kx + 5);
+      // the slice of graY on warps 0..3 and the KKT / ||F||^2 partials on warps 4..7
+      auto sum_kind = [](long) { return 0; };
+      reduce_mixed<2, decltype(sum_kind), true>(PG, G, e0, e1, a.gY + e0, sum_kind, 0, NW / 2);
+      reduce_mixed<1>(PD, G, 0, 7, kx, [](long e) { return e >= 5 ? 2 : 0; }, NW / 2, NW / 2);
     }
     STAMP(14);
     ++it;
