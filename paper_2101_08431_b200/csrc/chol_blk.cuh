@@ -9,6 +9,8 @@
 // register tiles read from a transposed shared-memory copy of the panel.
 // Reciprocal pivots come from rsqrt; the strict upper triangle is zeroed.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace {
@@ -172,6 +174,157 @@ __global__ void __launch_bounds__(CHOL_BLK_THREADS) k_chol_blk(double* __restric
   for (int r = wid; r < N; r += nwarp)
     for (int c = r + 1 + lane; c < N; c += 32) A[(long)r * N + c] = 0.0;
   if (tid == 0) {
+    if (f >= 0)
+      *info = fail_base + f;
+    else if (set_ok)
+      *info = -1;
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Multi-CTA variant (cooperative launch) for 128 < N <= 4096: per 32-column panel
+// the panel rows are solved by every CTA's warps (four rows per warp in flight)
+// and the trailing update is split into 32 x 32 tiles over the CTAs; the CTA that
+// owns the next diagonal tile factors it right after updating it, so a panel costs
+// two grid barriers.  Same numerics as k_chol_blk's diagonal block and panel solve;
+// the trailing update sums the panel's 32 products before subtracting.
+// ---------------------------------------------------------------------------
+constexpr int CHOL_COOP_THREADS = 256;
+
+__device__ __forceinline__ void coop_sync() {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+  }
+  cooperative_groups::this_grid().sync();
+}
+
+__global__ void __launch_bounds__(CHOL_COOP_THREADS) k_chol_coop(double* __restrict__ A, int N,
+                                                                 int* __restrict__ info,
+                                                                 int fail_base, int set_ok,
+                                                                 double* __restrict__ dinv_g,
+                                                                 int* __restrict__ fail_g) {
+  __shared__ double sd[32 * 33];   // diagonal block L_pp (row-major) for the panel solve
+  __shared__ double pr[32][33], pc[32][33];
+  __shared__ double dinv[32];
+  __shared__ int sfail;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int G = gridDim.x, cta = blockIdx.x;
+  constexpr int NWC = CHOL_COOP_THREADS / 32;
+  if (cta == 0 && tid == 0) *fail_g = -1;
+  // first diagonal block
+  if (cta == 0) {
+    if (tid == 0) sfail = -1;
+    __syncthreads();
+    if (wid == 0) chol_diag_block(A, N, 0, min(32, N), sd, dinv, &sfail);
+    __syncthreads();
+    if (tid < 32) dinv_g[tid] = dinv[tid];
+    if (tid == 0) *fail_g = sfail;
+  }
+  coop_sync();
+  for (int p0 = 0; p0 < N; p0 += 32) {
+    const int nb = min(32, N - p0);
+    if (__ldcg(fail_g) >= 0) break;  // uniform
+    // stage L_pp and 1/L_jj
+    for (int e = tid; e < 32 * 32; e += CHOL_COOP_THREADS) {
+      const int r = e >> 5, c = e & 31;
+      sd[r * 33 + c] = (r < nb && c < nb) ? __ldcg(A + (long)(p0 + r) * N + p0 + c) : 0.0;
+    }
+    if (tid < 32) dinv[tid] = __ldcg(dinv_g + tid);
+    __syncthreads();
+    // panel rows [p0 + nb, N): warps across all CTAs, four rows each in flight
+    {
+      const double dl = dinv[lane];
+      const double* lrow = sd + lane * 33;
+      const long gw = (long)cta * NWC + wid, nwt = (long)G * NWC;
+      for (long rb = p0 + nb + 4 * gw; rb < N; rb += 4 * nwt) {
+        double acc[4], x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          acc[u] = (lane < nb && rb + u < N) ? __ldcg(A + (rb + u) * N + p0 + lane) : 0.0;
+          x[u] = 0.0;
+        }
+        for (int j = 0; j < nb; ++j) {
+          const double lcj = (lane < nb) ? lrow[j] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double xj = __shfl_sync(0xffffffffu, acc[u] * dl, j);
+            const double nacc = acc[u] - lcj * xj;
+            x[u] = (lane == j) ? xj : x[u];
+            acc[u] = (lane > j) ? nacc : acc[u];
+          }
+        }
+        if (lane < nb) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (rb + u < N) __stcg(A + (rb + u) * N + p0 + lane, x[u]);
+        }
+      }
+    }
+    coop_sync();
+    // trailing update in 32 x 32 tiles (lower triangle of [b0, N)^2); tile 0 is the
+    // next diagonal block: its owner (CTA 0) factors it right away
+    const int b0 = p0 + nb, n2 = N - b0;
+    if (n2 > 0) {
+      const int T = (n2 + 31) / 32;
+      const int ntile = T * (T + 1) / 2;
+      for (int t = cta; t < ntile; t += G) {
+        int ti = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+        while (ti * (ti + 1) / 2 > t) --ti;
+        const int tj = t - ti * (ti + 1) / 2;
+        const int R0 = b0 + 32 * ti, C0 = b0 + 32 * tj;
+        __syncthreads();
+        for (int e = tid; e < 32 * 32; e += CHOL_COOP_THREADS) {
+          const int r = e >> 5, i = e & 31;
+          pr[r][i] = (R0 + r < N && i < nb) ? __ldcg(A + (long)(R0 + r) * N + p0 + i) : 0.0;
+          pc[r][i] = (C0 + r < N && i < nb) ? __ldcg(A + (long)(C0 + r) * N + p0 + i) : 0.0;
+        }
+        __syncthreads();
+        const int ty = tid >> 4, tx = tid & 15;
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+          const double a0 = pr[2 * ty][i], a1 = pr[2 * ty + 1][i];
+          const double c0v = pc[2 * tx][i], c1v = pc[2 * tx + 1][i];
+          acc[0][0] = fma(a0, c0v, acc[0][0]);
+          acc[0][1] = fma(a0, c1v, acc[0][1]);
+          acc[1][0] = fma(a1, c0v, acc[1][0]);
+          acc[1][1] = fma(a1, c1v, acc[1][1]);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int r = R0 + 2 * ty + u, c = C0 + 2 * tx + v;
+            if (r < N && c <= r) {  // written by another CTA last panel: read through L2
+              const long q = (long)r * N + c;
+              A[q] = __ldcg(A + q) - acc[u][v];
+            }
+          }
+        if (t == 0) {  // next diagonal block: factor it now (CTA 0)
+          __syncthreads();
+          __threadfence_block();
+          if (tid == 0) sfail = -1;
+          __syncthreads();
+          if (wid == 0) chol_diag_block(A, N, b0, min(32, N - b0), sd, dinv, &sfail);
+          __syncthreads();
+          if (tid < 32) dinv_g[tid] = dinv[tid];
+          if (tid == 0 && sfail >= 0) *fail_g = sfail;
+        }
+      }
+    }
+    coop_sync();
+  }
+  // zero the strict upper triangle, report
+  const long gt = (long)cta * CHOL_COOP_THREADS + tid, nt = (long)G * CHOL_COOP_THREADS;
+  for (long e = gt; e < (long)N * N; e += nt) {
+    const int r = (int)(e / N), c = (int)(e % N);
+    if (c > r) A[e] = 0.0;
+  }
+  if (cta == 0 && tid == 0) {
+    const int f = __ldcg(fail_g);
     if (f >= 0)
       *info = fail_base + f;
     else if (set_ok)

@@ -266,6 +266,24 @@ extern "C" int nmfb_dense_cholesky(double* A, long N, int* info, void* stream) {
                          (int)kTwoTiles);
     attr = true;
   }
+  if (N > 128 && N <= 4096) {  // multi-CTA cooperative panels (csrc/chol_blk.cuh)
+    static double* scratch = nullptr;  // 32 reciprocal pivots + failure flag
+    if (!scratch && cudaMalloc(&scratch, 64 * sizeof(double)) != cudaSuccess) return NMFB_ENOMEM;
+    const int T = (int)((N - 32 + 31) / 32);
+    int G = T * (T + 1) / 2;
+    if (G > 148) G = 148;
+    if (G < 8) G = 8;
+    double* dg = scratch;
+    int* fg = reinterpret_cast<int*>(scratch + 32);
+    int n32 = (int)N, base = 0, setok = 1;
+    void* args[] = {&A, &n32, &info, &base, &setok, &dg, &fg};
+    ++g_nmfb_launches;
+    if (cudaLaunchCooperativeKernel((const void*)k_chol_coop, dim3(G), dim3(CHOL_COOP_THREADS),
+                                    args, 0, st) != cudaSuccess)
+      return NMFB_ELAUNCH;
+    NMFB_CHECK_LAUNCH();
+    return NMFB_OK;
+  }
   if (N <= 800) {  // one CTA, L2-resident matrix (csrc/chol_blk.cuh)
     const size_t sm = chol_blk_smem(N);
     cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
