@@ -192,6 +192,10 @@ __global__ void __launch_bounds__(CHOL_BLK_THREADS) k_chol_blk(double* __restric
 // ---------------------------------------------------------------------------
 constexpr int CHOL_COOP_THREADS = 256;
 
+// 32 reciprocal pivots + the failure word of the cooperative factorization (a
+// device global, so a launch inside CUDA-graph capture needs no allocation)
+__device__ double g_coop_scratch[64];
+
 __device__ __forceinline__ void coop_sync() {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -203,8 +207,9 @@ __device__ __forceinline__ void coop_sync() {
 __global__ void __launch_bounds__(CHOL_COOP_THREADS) k_chol_coop(double* __restrict__ A, int N,
                                                                  int* __restrict__ info,
                                                                  int fail_base, int set_ok,
-                                                                 double* __restrict__ dinv_g,
-                                                                 int* __restrict__ fail_g) {
+                                                                 int skip_if_set) {
+  double* dinv_g = g_coop_scratch;
+  int* fail_g = reinterpret_cast<int*>(g_coop_scratch + 32);
   __shared__ double sd[32 * 33];   // diagonal block L_pp (row-major) for the panel solve
   __shared__ double pr[32][33], pc[32][33];
   __shared__ double dinv[32];
@@ -212,6 +217,7 @@ __global__ void __launch_bounds__(CHOL_COOP_THREADS) k_chol_coop(double* __restr
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int G = gridDim.x, cta = blockIdx.x;
   constexpr int NWC = CHOL_COOP_THREADS / 32;
+  if (skip_if_set && *info >= 0) return;  // every CTA sees the same word: uniform exit
   if (cta == 0 && tid == 0) *fail_g = -1;
   // first diagonal block
   if (cta == 0) {
@@ -330,6 +336,28 @@ __global__ void __launch_bounds__(CHOL_COOP_THREADS) k_chol_coop(double* __restr
     else if (set_ok)
       *info = -1;
   }
+}
+
+// launch helper: one CTA for N <= 128, cooperative panels above
+inline int launch_chol(double* A, int N, int* info, int fail_base, int skip_if_set, int set_ok,
+                       cudaStream_t st) {
+  if (N <= 128) {
+    const size_t sm = chol_blk_smem(N);
+    cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    ++g_nmfb_launches, k_chol_blk<<<1, CHOL_BLK_THREADS, sm, st>>>(A, N, info, fail_base,
+                                                                   skip_if_set, set_ok);
+    return NMFB_OK;
+  }
+  const int T = (N - 32 + 31) / 32;
+  int G = T * (T + 1) / 2;
+  if (G > 148) G = 148;
+  if (G < 8) G = 8;
+  void* args[] = {&A, &N, &info, &fail_base, &set_ok, &skip_if_set};
+  ++g_nmfb_launches;
+  if (cudaLaunchCooperativeKernel((const void*)k_chol_coop, dim3(G), dim3(CHOL_COOP_THREADS), args,
+                                  0, st) != cudaSuccess)
+    return NMFB_ELAUNCH;
+  return NMFB_OK;
 }
 
 }  // namespace

@@ -189,7 +189,6 @@ __global__ void __launch_bounds__(1024) k_trsv_single(const double* __restrict__
                                                       double* __restrict__ b, int trans) {
   __shared__ double zb[32], sblk[32 * 33], srcp[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nw = blockDim.x >> 5;
   const long nblk = (N + 31) / 32;
   for (long bb = 0; bb < nblk; ++bb) {
     const long blk = trans ? (nblk - 1 - bb) : bb;
@@ -199,24 +198,31 @@ __global__ void __launch_bounds__(1024) k_trsv_single(const double* __restrict__
     if (wid == 0) {
       double v = lane < nc ? b[c0 + lane] : 0.0;
       v = trsv_diag_warp(L, N, c0, nc, trans, v, sblk, srcp);
-      if (lane < nc) {
-        b[c0 + lane] = v;
-        zb[lane] = v;
-      }
+      if (lane < nc) b[c0 + lane] = v;
+      zb[lane] = lane < nc ? v : 0.0;
     }
     __syncthreads();
-    // 2) every warp updates the remaining rows
+    // 2) the remaining entries, one thread each: its 32 L values are loaded together
+    //    (all in flight), then one FMA chain
     if (!trans) {
-      for (long r = c0 + nc + wid; r < N; r += nw) {
-        double s = lane < nc ? L[r * N + c0 + lane] * zb[lane] : 0.0;
-        s = warp_sum(s);
-        if (lane == 0) b[r] -= s;
+      for (long r = c0 + nc + tid; r < N; r += blockDim.x) {
+        double l[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) l[c] = c < nc ? L[r * N + c0 + c] : 0.0;
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) s = fma(l[c], zb[c], s);
+        b[r] -= s;
       }
     } else {
-      // b[c] -= sum_{r in blk} L[r, c] z[r] for c < c0
+      // b[c] -= sum_{r in blk} L[r, c] z[r] for c < c0 (coalesced across threads)
       for (long c = tid; c < c0; c += blockDim.x) {
+        double l[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) l[r] = r < nc ? L[(c0 + r) * N + c] : 0.0;
         double s = 0.0;
-        for (int r = 0; r < nc; ++r) s = fma(L[(c0 + r) * N + c], zb[r], s);
+#pragma unroll
+        for (int r = 0; r < 32; ++r) s = fma(l[r], zb[r], s);
         b[c] -= s;
       }
     }
@@ -266,28 +272,9 @@ extern "C" int nmfb_dense_cholesky(double* A, long N, int* info, void* stream) {
                          (int)kTwoTiles);
     attr = true;
   }
-  if (N > 128 && N <= 4096) {  // multi-CTA cooperative panels (csrc/chol_blk.cuh)
-    static double* scratch = nullptr;  // 32 reciprocal pivots + failure flag
-    if (!scratch && cudaMalloc(&scratch, 64 * sizeof(double)) != cudaSuccess) return NMFB_ENOMEM;
-    const int T = (int)((N - 32 + 31) / 32);
-    int G = T * (T + 1) / 2;
-    if (G > 148) G = 148;
-    if (G < 8) G = 8;
-    double* dg = scratch;
-    int* fg = reinterpret_cast<int*>(scratch + 32);
-    int n32 = (int)N, base = 0, setok = 1;
-    void* args[] = {&A, &n32, &info, &base, &setok, &dg, &fg};
-    ++g_nmfb_launches;
-    if (cudaLaunchCooperativeKernel((const void*)k_chol_coop, dim3(G), dim3(CHOL_COOP_THREADS),
-                                    args, 0, st) != cudaSuccess)
-      return NMFB_ELAUNCH;
-    NMFB_CHECK_LAUNCH();
-    return NMFB_OK;
-  }
-  if (N <= 800) {  // one CTA, L2-resident matrix (csrc/chol_blk.cuh)
-    const size_t sm = chol_blk_smem(N);
-    cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    ++g_nmfb_launches, k_chol_blk<<<1, CHOL_BLK_THREADS, sm, st>>>(A, (int)N, info, 0, 0, 1);
+  if (N <= 4096) {  // csrc/chol_blk.cuh: one CTA up to 128, cooperative panels above
+    const int rc = launch_chol(A, (int)N, info, 0, 0, 1, st);
+    if (rc != NMFB_OK) return rc;
     NMFB_CHECK_LAUNCH();
     return NMFB_OK;
   }

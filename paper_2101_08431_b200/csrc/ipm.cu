@@ -20,7 +20,6 @@
 
 namespace {
 
-constexpr int KK_MAX = NMFB_MAX_K * (NMFB_MAX_K + 1) / 2;
 
 __device__ __forceinline__ int pk(int a, int b, int k) {
   // packed index of (a, b), a <= b, row-major upper triangle

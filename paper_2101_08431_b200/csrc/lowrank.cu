@@ -355,13 +355,13 @@ extern "C" int nmfb_lowrank_factor(const double* Zpk, const double* Gpk, long k,
   double* Zb = work;
   double* T1 = work + Q * Q;
   const size_t csm = chol_blk_smem(Q);
-  cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   ++g_nmfb_launches, k_lr_unpack<<<(unsigned)((Q * Q + 255) / 256), 256, 0, st>>>(Zpk, Gpk, (int)k, Zb, LG, info);
-  ++g_nmfb_launches, k_chol_blk<<<1, CHOL_BLK_THREADS, csm, st>>>(LG, (int)Q, info, 1000000, 0, 0);
+  (void)csm;
+  launch_chol(LG, (int)Q, info, 1000000, 0, 0, st);
   const dim3 g((unsigned)((Q + 31) / 32), (unsigned)((Q + 31) / 32));
   ++g_nmfb_launches, k_lr_gemm<<<g, 256, 0, st>>>(Zb, LG, (int)Q, 0, T1, info);
   ++g_nmfb_launches, k_lr_gemm<<<g, 256, 0, st>>>(LG, T1, (int)Q, 1, LH, info);
-  ++g_nmfb_launches, k_chol_blk<<<1, CHOL_BLK_THREADS, csm, st>>>(LH, (int)Q, info, 0, 1, 1);
+  launch_chol(LH, (int)Q, info, 0, 1, 1, st);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

@@ -57,30 +57,9 @@ struct PArgs {
       a.prof[(long)it * 40 + (i)] = clock64();                              \
   } while (0)
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Grid barrier on per-CTA epoch flags (host zeroes them per launch): every CTA
-// publishes its epoch with a release store, warp 0 of every CTA polls all flags.
-// No atomics, so arrivals do not serialise on one L2 address.  A bounded spin
-// turns a lost CTA into a trap (reported launch error) instead of a hang.
-__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // Grid barrier: cooperative-groups grid sync (measured on B200 with 148 CTAs:
 // 1.3 us, against 1.8 us for an atomic counter and 2.8 us for per-CTA flags polled
-// by every CTA; scripts/micro/bar.cu).  `flags`/`epoch` are kept for the spin-guarded
-// fallback path below.
+// by every CTA; scripts/micro/bar.cu).  `epoch` counts barriers (debugging aid).
 __device__ __forceinline__ void grid_barrier(unsigned* flags, unsigned& epoch) {
   (void)flags;
   ++epoch;
@@ -411,7 +390,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   double* Hs = Zs + KK * KK;
   double* XtXs = Hs + K * K;
   __shared__ double Gdy[K * K], gy[K * K], dGi[Q], dHi[Q];
-  __shared__ double Gm[Q * Q], Zbm[Q * Q], T1[Q * Q], Hm[Q * Q], u[Q], w[Q], w2[Q];
+  __shared__ double Gm[Q * Q], Zbm[Q * Q], T1[Q * Q], Hm[Q * Q], u[Q], w[Q];
   __shared__ double red[16 * NW];
   __shared__ double scal[24];  // [0..2] ysc, [3..5] gtp,a1max,a2max, [6..11] quartic
   __shared__ double kx[8];     // X-part KKT sums + fsq (after phase E)

@@ -77,7 +77,6 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
   double* tl = cb + CB * K;   // CB tolerances
   double* Ms = tl + CB;       // own rows of M (optional)
   __shared__ double gyy[K * K], gxx[K * K], scal[8], red[4 * SNW];
-  __shared__ int s_fail;
 
   for (long e = tid; e < N; e += ST) Ys[e] = a.Yt[e];
   for (long e = tid; e < (long)nr * K; e += ST) Xs[e] = a.X[r0 * K + e];
