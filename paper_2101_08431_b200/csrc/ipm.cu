@@ -639,14 +639,18 @@ __global__ void __launch_bounds__(256) k_quartic_rows(const double* __restrict__
 
 // barrier increments for every backtracking trial t (blockIdx.y):
 //   part[t][b][0] = sum log1p(alpha_t dx/x), part[t][b][1] = same over y
+// one CTA column per trial (blockIdx.y = t): the log1p are FP64-issue bound and one
+// trial per CTA gives the most parallelism (batching trials per CTA with a shared
+// division measured slower on B200); terms are the oracle's log1p((alpha dv) / v)
 __global__ void __launch_bounds__(256) k_barrier_trials(const double* __restrict__ X,
                                                         const double* __restrict__ dX, long nx,
                                                         const double* __restrict__ Yt,
                                                         const double* __restrict__ dYt, long ny,
                                                         const double* __restrict__ alpha_max,
-                                                        double* __restrict__ part) {
+                                                        int ntrials, double* __restrict__ part) {
   __shared__ double sh[32];
   const int t = blockIdx.y;
+  if (t >= ntrials) return;
   const double alpha = ldexp(*alpha_max, -t);
   double sx = 0.0, sy = 0.0;
   const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1193,7 +1197,7 @@ extern "C" int nmfb_barrier_trials(const double* X, const double* dX, long nx, c
   const int nb = 64;
   if (work_len < 2L * nb * ntrials) return NMFB_ENOMEM;
   dim3 grid(nb, ntrials);
-  ++g_nmfb_launches, k_barrier_trials<<<grid, 256, 0, st>>>(X, dX, nx, Yt, dYt, ny, alpha_max, work);
+  ++g_nmfb_launches, k_barrier_trials<<<grid, 256, 0, st>>>(X, dX, nx, Yt, dYt, ny, alpha_max, ntrials, work);
   ++g_nmfb_launches, k_finish_trials<<<(2 * ntrials * 32 + 255) / 256, 256, 0, st>>>(work, nb, ntrials, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
@@ -1329,29 +1333,35 @@ __global__ void k_ffree_quartic(const double* __restrict__ A1, const double* __r
                                 const double* __restrict__ B2, const double* __restrict__ YY,
                                 const double* __restrict__ Dgx, const double* __restrict__ Dgy,
                                 const double* __restrict__ Dmd, int k, double* __restrict__ sc) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  auto tr = [k](const double* P, const double* Q, bool qt) {  // tr(P Q) or tr(P Q^T)
-    double s = 0.0;
-    for (int a = 0; a < k; ++a)
-      for (int b = 0; b < k; ++b) s = fma(P[a * k + b], qt ? Q[a * k + b] : Q[b * k + a], s);
-    return s;
-  };
-  auto diag = [k](const double* P) {
-    double s = 0.0;
-    for (int a = 0; a < k; ++a) s += P[a * k + a];
-    return s;
-  };
-  const double ab = diag(Dgx) + diag(Dgy);
-  const double ac = tr(A2, B2, false) - diag(Dmd);
-  const double bb = tr(A1, YY, false) + tr(XX, B1, false) + 2.0 * tr(A2, B2, true);
-  const double bc = tr(A1, B2, true) + tr(A2, B1, true);
-  const double cc = tr(A1, B1, false);
-  sc[10] = sc[0];
-  sc[11] = ab;
-  sc[12] = bb;
-  sc[13] = ac;
-  sc[14] = bc;
-  sc[15] = cc;
+  // one warp: lanes stride the k x k entries of every trace, fixed butterfly sums
+  const int lane = threadIdx.x & 31;
+  double t[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) t[q] = 0.0;
+  for (int e = lane; e < k * k; e += 32) {
+    const int a = e / k, b = e % k, et = b * k + a;
+    t[0] = fma(A2[e], B2[et], t[0]);  // tr(A2 B2)
+    t[1] = fma(A1[e], YY[et], t[1]);  // tr(A1 YY)
+    t[2] = fma(XX[e], B1[et], t[2]);  // tr(XX B1)
+    t[3] = fma(A2[e], B2[e], t[3]);   // tr(A2 B2^T)
+    t[4] = fma(A1[e], B2[e], t[4]);   // tr(A1 B2^T)
+    t[5] = fma(A2[e], B1[e], t[5]);   // tr(A2 B1^T)
+    t[6] = fma(A1[e], B1[et], t[6]);  // tr(A1 B1)
+  }
+  for (int a = lane; a < k; a += 32) {
+    t[7] += Dgx[a * k + a] + Dgy[a * k + a];
+    t[8] += Dmd[a * k + a];
+  }
+#pragma unroll
+  for (int q = 0; q < 9; ++q) t[q] = warp_sum(t[q]);
+  if (lane == 0) {
+    sc[10] = sc[0];
+    sc[11] = t[7];
+    sc[12] = t[1] + t[2] + 2.0 * t[3];
+    sc[13] = t[0] - t[8];
+    sc[14] = t[4] + t[5];
+    sc[15] = t[6];
+  }
 }
 
 extern "C" int nmfb_ffree_grad_rows(const double* V, const double* G, const double* MV, long rows,

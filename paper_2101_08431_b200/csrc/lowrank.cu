@@ -241,18 +241,22 @@ __device__ void cta_trsv(const double* L, int Q, double* b, int trans) {
     const int blk = trans ? (nblk - 1 - bb) : bb;
     const int c0 = blk * 32, nc = min(32, Q - c0);
     if (wid == 0) {
+      // reciprocal pivots first, then one shuffle + one FMA per column step
       double v = lane < nc ? b[c0 + lane] : 0.0;
+      const double rl = lane < nc ? 1.0 / L[(c0 + lane) * Q + c0 + lane] : 0.0;
       if (!trans) {
         for (int j = 0; j < nc; ++j) {
-          const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * Q + c0 + j];
-          if (lane == j) v = zj;
-          if (lane > j && lane < nc) v -= L[(c0 + lane) * Q + c0 + j] * zj;
+          const double zj = __shfl_sync(0xffffffffu, v * rl, j);
+          const double lij = (lane < nc) ? L[(c0 + lane) * Q + c0 + j] : 0.0;
+          const double nv = v - lij * zj;
+          v = (lane == j) ? zj : ((lane > j && lane < nc) ? nv : v);
         }
       } else {
         for (int j = nc - 1; j >= 0; --j) {
-          const double zj = __shfl_sync(0xffffffffu, v, j) / L[(c0 + j) * Q + c0 + j];
-          if (lane == j) v = zj;
-          if (lane < j) v -= L[(c0 + j) * Q + c0 + lane] * zj;
+          const double zj = __shfl_sync(0xffffffffu, v * rl, j);
+          const double lji = (lane < nc) ? L[(c0 + j) * Q + c0 + lane] : 0.0;
+          const double nv = v - lji * zj;
+          v = (lane == j) ? zj : (lane < j ? nv : v);
         }
       }
       if (lane < nc) b[c0 + lane] = v;

@@ -95,7 +95,7 @@ class Problem:
         self.gwork = torch.empty(max(self.lib.nmfb_grams_work_len(max(n, M.shape[1]), k, 4), 1),
                                  **f64)
         nb = L.nmfb_ipm_reduce_blocks()
-        self.rwork = torch.empty(max(64 * 2 * NTRIALS, 12 * nb, 3 * ((n + 127) // 128 + nb), 4096),
+        self.rwork = torch.empty(max(148 * 2 * NTRIALS, 12 * nb, 3 * ((n + 127) // 128 + nb), 4096),
                                  **f64)
         self.row_n2 = torch.empty(n, **f64)
         self.col_n2 = torch.empty(m, **f64)
