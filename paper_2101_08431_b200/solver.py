@@ -13,6 +13,7 @@ NativeLibraryError.
 from __future__ import annotations
 
 import math
+import os
 import time
 
 import numpy as np
@@ -356,6 +357,9 @@ def _stage1_persistent(P, X, Yt, pX, pY, Yn, stX, stY, have_carry, cfg, nsweeps,
 # ============================================================================
 # stage 2 (Algorithm 2 + the Hessian switch of Algorithm 3)
 # ============================================================================
+_GRAPH_DEBUG = bool(os.environ.get("NMFB_GRAPH_DEBUG"))
+
+
 class IpmEngine:
     """Device state and kernels of one interior-point solve."""
 
@@ -405,6 +409,7 @@ class IpmEngine:
         self.fact_F = 0
         self.graphs = {}
         self.graph_pool = None
+        self.capture_stream = None
         self.use_graphs = p.use_graphs and not P.comm.active and not self.dense_gn
         # fused small-problem iteration (csrc/small.cu) for c1-c3-sized problems
         self.small = bool(P.lib.nmfb_small_supported(n, m, k)) and not P.comm.active \
@@ -503,8 +508,35 @@ class IpmEngine:
             g = torch.cuda.CUDAGraph()
             self.P.captured_events = []
             c0 = self.P.lib.nmfb_launch_count()
-            with torch.cuda.graph(g, pool=self.graph_pool):
-                self.gn_iteration_launch()
+            # Capture on a side stream directly: torch.cuda.graph() would also
+            # synchronize and empty the caching allocator on every capture, which
+            # forces the next allocations back through cudaMalloc (tens of ms at
+            # c4/c5 sizes, more than the graph saves over a short run).
+            if _GRAPH_DEBUG:
+                torch.cuda.synchronize(self.P.dev)
+                tg = time.perf_counter()
+            if self.capture_stream is None:
+                self.capture_stream = torch.cuda.Stream(self.P.dev)
+            cur = torch.cuda.current_stream(self.P.dev)
+            self.capture_stream.wait_stream(cur)
+            with torch.cuda.stream(self.capture_stream):
+                if self.graph_pool is None:
+                    g.capture_begin()
+                else:
+                    g.capture_begin(pool=self.graph_pool)
+                try:
+                    self.gn_iteration_launch()
+                finally:
+                    g.capture_end()
+            cur.wait_stream(self.capture_stream)
+            if _GRAPH_DEBUG:
+                torch.cuda.synchronize(self.P.dev)
+                tc = time.perf_counter()
+                g.replay()
+                torch.cuda.synchronize(self.P.dev)
+                print(f"[nmfb graph] capture {1e3 * (tc - tg):.2f} ms, first replay "
+                      f"{1e3 * (time.perf_counter() - tc):.2f} ms, pool "
+                      f"{torch.cuda.memory_reserved(self.P.dev) / 2**20:.0f} MiB", flush=True)
             nk = self.P.lib.nmfb_launch_count() - c0
             self.graph_pool = g.pool()
             self.graphs[key] = (g, self.P.captured_events, nk)

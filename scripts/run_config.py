@@ -56,6 +56,8 @@ def main():
         ti = time.perf_counter() - t
         out.update(ipm_iters=r2.iters, ipm_s=ti, ipm_iters_per_s=r2.iters / ti,
                    ipm_outer=r2.outer, armijo_t=r2.armijo_t, full_hessian=r2.flags,
+                   ipm_ms_per_iter_steady=(1e3 * (r2.trace[-1][0] - r2.trace[1][0]) / (len(r2.trace) - 2)
+                                           if len(r2.trace) > 2 else None),
                    kkt_E0=r2.trace[-1][2] if r2.trace else None,
                    objective_after_ipm=r2.trace[-1][1] if r2.trace else None,
                    small_path=bool(eng.small))
