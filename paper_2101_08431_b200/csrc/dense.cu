@@ -185,7 +185,9 @@ __device__ __forceinline__ double trsv_diag_warp(const double* __restrict__ L, l
   return v;
 }
 
-__global__ void __launch_bounds__(1024) k_trsv_single(const double* __restrict__ L, long N,
+constexpr int TRSV_T = 256;  // 1024 threads spilled the 32-entry row to local memory
+
+__global__ void __launch_bounds__(TRSV_T) k_trsv_single(const double* __restrict__ L, long N,
                                                       double* __restrict__ b, int trans) {
   __shared__ double zb[32], sblk[32 * 33], srcp[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -298,8 +300,8 @@ extern "C" int nmfb_dense_solve(const double* L, long N, double* b, void* stream
   cudaStream_t st = (cudaStream_t)stream;
   if (N <= 0) return NMFB_EINVAL;
   if (N <= 4096) {
-    ++g_nmfb_launches, k_trsv_single<<<1, 1024, 0, st>>>(L, N, b, 0);
-    ++g_nmfb_launches, k_trsv_single<<<1, 1024, 0, st>>>(L, N, b, 1);
+    ++g_nmfb_launches, k_trsv_single<<<1, TRSV_T, 0, st>>>(L, N, b, 0);
+    ++g_nmfb_launches, k_trsv_single<<<1, TRSV_T, 0, st>>>(L, N, b, 1);
   } else {
     for (long c0 = 0; c0 < N; c0 += 32) {
       const int nc = (int)min(32L, N - c0);

@@ -100,17 +100,28 @@ __device__ __forceinline__ void reduce_entries(const double* part, int G, long e
         v[b][u] = (eb + b < e1 && c < G) ? ldcg(part + (eb + b) * G + c) : op_id<KD>();
       }
     __syncwarp();
+    double s[EB];
 #pragma unroll
     for (int b = 0; b < EB; ++b) {
-      double s = v[b][0];
+      s[b] = v[b][0];
 #pragma unroll
-      for (int u = 1; u < 5; ++u) s = op2<KD>(s, v[b][u]);
-      s = warp_op<KD>(s);
+      for (int u = 1; u < 5; ++u) s[b] = op2<KD>(s[b], v[b][u]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // level-major: the EB shuffles issue together
+      double t[EB];
+#pragma unroll
+      for (int b = 0; b < EB; ++b) t[b] = __shfl_xor_sync(0xffffffffu, s[b], o);
+#pragma unroll
+      for (int b = 0; b < EB; ++b) s[b] = op2<KD>(s[b], t[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
       if (lane == 0 && eb + b < e1) {
         if (out_global)
-          __stcg(out + (eb + b - e0), s);
+          __stcg(out + (eb + b - e0), s[b]);
         else
-          out[eb + b - e0] = s;
+          out[eb + b - e0] = s[b];
       }
     }
   }
@@ -139,18 +150,30 @@ __device__ __forceinline__ void reduce_mixed(const double* part, int G, long e0,
       }
     }
     __syncwarp();
+    double s[EB];
 #pragma unroll
     for (int b = 0; b < EB; ++b) {
-      double s = v[b][0];
+      s[b] = v[b][0];
 #pragma unroll
       for (int u = 1; u < 5; ++u)
-        s = kd[b] == 0 ? s + v[b][u] : (kd[b] == 1 ? fmin(s, v[b][u]) : fmax(s, v[b][u]));
-      s = kd[b] == 0 ? warp_sum(s) : (kd[b] == 1 ? warp_min(s) : warp_max(s));
+        s[b] = kd[b] == 0 ? s[b] + v[b][u] : (kd[b] == 1 ? fmin(s[b], v[b][u]) : fmax(s[b], v[b][u]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // level-major: the EB shuffles issue together
+      double t[EB];
+#pragma unroll
+      for (int b = 0; b < EB; ++b) t[b] = __shfl_xor_sync(0xffffffffu, s[b], o);
+#pragma unroll
+      for (int b = 0; b < EB; ++b)
+        s[b] = kd[b] == 0 ? s[b] + t[b] : (kd[b] == 1 ? fmin(s[b], t[b]) : fmax(s[b], t[b]));
+    }
+#pragma unroll
+    for (int b = 0; b < EB; ++b) {
       if (lane == 0 && eb + b < e1) {
         if (OUTG)
-          __stcg(out + (eb + b - e0), s);
+          __stcg(out + (eb + b - e0), s[b]);
         else
-          out[eb + b - e0] = s;
+          out[eb + b - e0] = s[b];
       }
     }
   }
@@ -214,40 +237,90 @@ __device__ __forceinline__ int warp_chol(double* A, double* dinv) {
 
 // Block reductions of NV values with the result in EVERY thread (fixed order).
 // Value q is min-reduced if bit q of MINM is set, max-reduced for MAXM, else summed.
-template <int Q, int NV, int MINM, int MAXM>
-struct BlockRed {
-  static constexpr int KD = ((MINM >> Q) & 1) ? 1 : (((MAXM >> Q) & 1) ? 2 : 0);
-  static __device__ __forceinline__ void warp_part(double (&v)[NV]) {
-    v[Q] = warp_op<KD>(v[Q]);
-    BlockRed<Q + 1, NV, MINM, MAXM>::warp_part(v);
-  }
-  static __device__ __forceinline__ void combine(double (&v)[NV], const double* sh) {
-    double r = sh[Q * NW];
-#pragma unroll
-    for (int w = 1; w < NW; ++w) r = op2<KD>(r, sh[Q * NW + w]);
-    v[Q] = r;
-    BlockRed<Q + 1, NV, MINM, MAXM>::combine(v, sh);
-  }
-};
+// The warp stage is level-major so the NV independent shuffles of a level issue
+// back to back (value-major chains ran one after another: 1.5 us for 9 values);
+// per value the arithmetic is warp_sum / warp_min / warp_max's exactly.
 template <int NV, int MINM, int MAXM>
-struct BlockRed<NV, NV, MINM, MAXM> {
-  static __device__ __forceinline__ void warp_part(double (&)[NV]) {}
-  static __device__ __forceinline__ void combine(double (&)[NV], const double*) {}
+__device__ __forceinline__ void warp_reduce_multi(double (&v)[NV]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double t[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) t[q] = __shfl_xor_sync(0xffffffffu, v[q], o);
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+      v[q] = ((MINM >> q) & 1) ? fmin(v[q], t[q]) : (((MAXM >> q) & 1) ? fmax(v[q], t[q]) : v[q] + t[q]);
+  }
+}
+
+// Warp stage of block_reduce_all: recursive halving over NP = 2^LG >= NV slots
+// (at offset o a lane keeps one half of its slots and ships the other half to lane
+// ^ o), then plain butterflies over the remaining lane bits: NP - 1 + 5 - LG
+// shuffles instead of 5 NV.  Afterwards lane l holds the warp total of value
+// (l >> (5 - LG)) in v[0].  Deterministic and identical in every CTA.
+template <int NV, int MINM, int MAXM>
+struct WarpHalve {
+  static constexpr int LG = NV <= 1 ? 0 : NV <= 2 ? 1 : NV <= 4 ? 2 : NV <= 8 ? 3 : NV <= 16 ? 4 : 5;
+  static constexpr int NP = 1 << LG;
+  static __device__ __forceinline__ double opk(int idx, double a, double b) {
+    return ((MINM >> idx) & 1) ? fmin(a, b) : (((MAXM >> idx) & 1) ? fmax(a, b) : a + b);
+  }
+  static __device__ __forceinline__ double run(const double (&in)[NV]) {
+    const int lane = threadIdx.x & 31;
+    double v[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) v[q] = q < NV ? in[q] : 0.0;
+    int base = 0;
+#pragma unroll
+    for (int st = 0; st < LG; ++st) {
+      const int o = 16 >> st, c = NP >> (st + 1);  // slots kept after this step
+      const bool up = (lane & o) != 0;
+      if (up) base += c;
+#pragma unroll
+      for (int i = 0; i < c; ++i) {
+        const double send = up ? v[i] : v[i + c];
+        const double keep = up ? v[i + c] : v[i];
+        const double recv = __shfl_xor_sync(0xffffffffu, send, o);
+        v[i] = opk(base + i, keep, recv);
+      }
+    }
+#pragma unroll
+    for (int o = 16 >> LG; o > 0; o >>= 1) v[0] = opk(base, v[0], __shfl_xor_sync(0xffffffffu, v[0], o));
+    return v[0];
+  }
 };
 
+// Block reduction of NV values with the result in EVERY thread (fixed order).
+// Value q is min-reduced if bit q of MINM is set, max-reduced for MAXM, else summed.
+// sh: two buffers of 16 NW + 16 doubles, alternated by `phase` (every thread toggles it
+// identically): a buffer is rewritten two reductions later, after the intermediate
+// reduction's barriers, which every thread reaches only once it has read it.
+// (The previous form - value-major warp_sum chains, then every thread folding all
+// NV x NW warp partials - was bound by shuffle and LDS issue: 1.5 us for 9 values.)
 template <int NV, int MINM = 0, int MAXM = 0>
-__device__ __forceinline__ void block_reduce_all(double (&v)[NV], double* sh /* NV * NW */) {
+__device__ __forceinline__ void block_reduce_all(double (&v)[NV], double* sh, int& phase) {
+  static_assert(NV <= 16, "block_reduce_all: NV <= 16");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  using WH = WarpHalve<NV, MINM, MAXM>;
+  double* b = sh + phase * (16 * NW + 16);
+  double* res = b + 16 * NW;
+  phase ^= 1;
   __syncwarp();
-  BlockRed<0, NV, MINM, MAXM>::warp_part(v);
+  const double wv = WH::run(v);
+  constexpr int SH = 5 - WH::LG;
+  const int idx = lane >> SH;
+  if ((lane & ((1 << SH) - 1)) == 0 && idx < NV) b[idx * NW + wid] = wv;
   __syncthreads();
-  if (lane == 0) {
+  if (threadIdx.x < NV) {
+    const int q = threadIdx.x;
+    double r = b[q * NW];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) sh[q * NW + wid] = v[q];
+    for (int w = 1; w < NW; ++w) r = WH::opk(q, r, b[q * NW + w]);
+    res[q] = r;
   }
   __syncthreads();
-  BlockRed<0, NV, MINM, MAXM>::combine(v, sh);
-  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = res[q];
 }
 
 __device__ __forceinline__ int pk(int a, int b, int k) {
@@ -360,7 +433,13 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   const long r0 = (long)cta * n / G, r1 = (long)(cta + 1) * n / G;
   const int nr = (int)(r1 - r0);
   const long nrm = (n + G - 1) / G;
+  // this CTA's slice of the m k Y-side entries (barrier trials, graY totals)
+  const long y0 = (long)cta * (m * K) / G, y1 = (long)(cta + 1) * (m * K) / G;
   const double mux = a.wx * a.mu, muy = a.wy * a.mu;
+  // column-per-thread passes over the own rows: q_rs threads per column when m < PT
+  const int q_rs = m >= PT ? 1 : PT / (int)m;
+  const long q_j0 = m >= PT ? tid : tid % (int)m;
+  const int q_roff = m >= PT ? 0 : tid / (int)m;
   const WLayout wl = wlayout(G, m, K);
   double* PA = a.work + wl.pa;
   double* PB = a.work + wl.pb;
@@ -374,6 +453,11 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   double* gYs = Ss + N;
   double* Ts = gYs + N;  // t_j, then dY
   double* dinv = Ts + N;
+  // Y-side arrays live in shared memory component-major (SoA: entry (j, p) at p m + j)
+  // so lanes striding j read consecutive words; global Y^T / S / graY stay (m, k)
+  // row-major.  dinv (packed D_j^{-1}) likewise: entry (j, c) at c m + j.
+#define YI(j, p) ((long)(p) * m + (j))
+#define DI(j, c) ((long)(c) * m + (j))
   double* xs = dinv + m * KK;
   double* rs = xs + nrm * K;
   double* gxs = rs + nrm * K;
@@ -391,7 +475,8 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   double* XtXs = Hs + K * K;
   __shared__ double Gdy[K * K], gy[K * K], dGi[Q], dHi[Q];
   __shared__ double Gm[Q * Q], Zbm[Q * Q], T1[Q * Q], Hm[Q * Q], u[Q], w[Q];
-  __shared__ double red[16 * NW];
+  __shared__ double red[2 * (16 * NW + 16)];
+  int rph = 0;  // block_reduce_all buffer phase
   __shared__ double scal[24];  // [0..2] ysc, [3..5] gtp,a1max,a2max, [6..11] quartic
   __shared__ double kx[8];     // X-part KKT sums + fsq (after phase E)
   __shared__ double bars[2 * TB];
@@ -410,9 +495,10 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   }
   #pragma unroll 1
   for (long e = tid; e < N; e += PT) {
-    Ys[e] = a.Yt[e];
-    Ss[e] = a.S[e];
-    gYs[e] = a.gY[e];
+    const long so = YI(e / K, e % K);
+    Ys[so] = a.Yt[e];
+    Ss[so] = a.S[e];
+    gYs[so] = a.gY[e];
   }
   #pragma unroll 1
   for (long e = tid; e < (long)nr * K; e += PT) {
@@ -440,11 +526,12 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
       const int p = e / K, q = e % K;
       double s = 0.0;
       #pragma unroll 1
-      for (long j = lane; j < m; j += 32) s = fma(Ys[j * K + p], Ys[j * K + q], s);
+      for (long j = lane; j < m; j += 32) s = fma(Ys[YI(j, p)], Ys[YI(j, q)], s);
       s = warp_sum(s);
       if (lane == 0) gy[e] = s;
     }
     __syncthreads();
+    STAMP(33);
     double badA = 1.0 / 0.0;
     #pragma unroll 1
     for (int rr = tid; rr < nr; rr += PT) {
@@ -494,11 +581,13 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         }
       }
     }
+    STAMP(31);
     {
       double v[1] = {badA};
-      block_reduce_all<1, 1, 0>(v, red);
+      block_reduce_all<1, 1, 0>(v, red, rph);
       badA = v[0];
     }
+    STAMP(32);
     #pragma unroll 1
     for (int e = tid; e < SA; e += PT) {
       double s = 0.0;
@@ -541,7 +630,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
 #pragma unroll
         for (int q = 0; q < NGY; ++q) {
           const long e = tid + (long)q * PT;
-          if (e < N) gYs[e] = gyv[q];
+          if (e < N) gYs[YI(e / K, e % K)] = gyv[q];
         }
       }
     }
@@ -562,7 +651,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         v[5] = fmax(v[5], y);
       }
       STAMP(17);
-      block_reduce_all<6, 0, 0x30>(v, red);
+      block_reduce_all<6, 0, 0x30>(v, red, rph);
       const double st = sqrt(fmax(kx[1] + v[0], 0.0));
       const double e_mu = fmax(st, sqrt(fmax(kx[2] + v[1], 0.0)));
       const double e_0 = fmax(st, sqrt(fmax(kx[3] + v[2], 0.0)));
@@ -602,7 +691,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     for (long e = tid; e < (long)nr * K; e += PT) a.Xf[r0 * K + e] = xs[e];
     if (cta == 0)
       #pragma unroll 1
-      for (long e = tid; e < N; e += PT) a.Ytf[e] = Ys[e];
+      for (long e = tid; e < N; e += PT) a.Ytf[e] = Ys[YI(e / K, e % K)];
 
     STAMP(3);
     // ---- Y side (replicated): rhs, D_j, t_j = D_j^{-1} rhs_j, D_j^{-1} packed
@@ -611,20 +700,20 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     for (long j = tid; j < m; j += PT) {
       double y[K], L[K][K], rhs[K], tv[K];
 #pragma unroll
-      for (int p = 0; p < K; ++p) y[p] = Ys[j * K + p];
+      for (int p = 0; p < K; ++p) y[p] = Ys[YI(j, p)];
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         double ra = 0.0;
 #pragma unroll
         for (int c = 0; c < K; ++c) ra = fma(Hs[p * K + c], y[c], ra);
-        rhs[p] = (muy / y[p] - gYs[j * K + p]) - ra;
+        rhs[p] = (muy / y[p] - gYs[YI(j, p)]) - ra;
       }
 #pragma unroll
       for (int p = 0; p < K; ++p)
 #pragma unroll
         for (int c = 0; c < K; ++c) L[p][c] = (c <= p) ? XtXs[p * K + c] : 0.0;
 #pragma unroll
-      for (int p = 0; p < K; ++p) L[p][p] += a.rho + Ss[j * K + p] / y[p];
+      for (int p = 0; p < K; ++p) L[p][p] += a.rho + Ss[YI(j, p)] / y[p];
       if (!reg_chol<K>(L)) badD = min(badD, (int)j);
       double Li[K][K];
       reg_inv_lower<K>(L, Li);
@@ -640,16 +729,16 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
 #pragma unroll
           for (int q = 0; q < K; ++q)
             if (q >= c) s = fma(Li[q][p], Li[q][c], s);
-          dinv[j * KK + (p * K - p * (p - 1) / 2 + (c - p))] = s;
+          dinv[DI(j, (p * K - p * (p - 1) / 2 + (c - p)))] = s;
         }
       }
       reg_solve<K>(L, rhs, tv);
 #pragma unroll
-      for (int p = 0; p < K; ++p) Ts[j * K + p] = tv[p];
+      for (int p = 0; p < K; ++p) Ts[YI(j, p)] = tv[p];
     }
     {
       double v[1] = {(double)badD};
-      block_reduce_all<1, 1, 0>(v, red);
+      block_reduce_all<1, 1, 0>(v, red, rph);
       badD = (int)v[0];
     }
     STAMP(4);
@@ -680,17 +769,18 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         for (int i = 0; i < EPW; ++i) {
           const int e = wid + NW * i;
           if (e < KK * KK) {
-            const double yy = Ys[j * K + o1[i]] * Ys[j * K + o2[i]];
-            sacc[i] = fma(yy, dinv[j * KK + o3[i]], sacc[i]);
+            const double yy = Ys[YI(j, o1[i])] * Ys[YI(j, o2[i])];
+            sacc[i] = fma(yy, dinv[DI(j, o3[i])], sacc[i]);
           } else if (e < NE) {
-            sacc[i] = fma(Ys[j * K + o1[i]], Ts[j * K + o2[i]], sacc[i]);
+            sacc[i] = fma(Ys[YI(j, o1[i])], Ts[YI(j, o2[i])], sacc[i]);
           }
         }
       }
+      warp_reduce_multi<EPW, 0, 0>(sacc);
 #pragma unroll
       for (int i = 0; i < EPW; ++i) {
         const int e = wid + NW * i;
-        const double v = warp_sum(sacc[i]);
+        const double v = sacc[i];
         if (lane == 0) {
           if (e < KK * KK)
             T1[e] = v;
@@ -815,7 +905,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
       for (long j = tid; j < m; j += PT) {
         double rv[K], out[K], y[K];
 #pragma unroll
-        for (int p = 0; p < K; ++p) y[p] = Ys[j * K + p];
+        for (int p = 0; p < K; ++p) y[p] = Ys[YI(j, p)];
 #pragma unroll
         for (int p = 0; p < K; ++p) {
           double s = 0.0;
@@ -827,21 +917,21 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         for (int p = 0; p < K; ++p) {  // D_j^{-1} (W^T y_j) with the packed inverse
           double s = 0.0;
 #pragma unroll
-          for (int c = 0; c < K; ++c) s = fma(dinv[j * KK + pk(p, c, K)], rv[c], s);
+          for (int c = 0; c < K; ++c) s = fma(dinv[DI(j, pk(p, c, K))], rv[c], s);
           out[p] = s;
         }
 #pragma unroll
         for (int p = 0; p < K; ++p) {
-          const double d = Ts[j * K + p] + out[p];
-          Ts[j * K + p] = d;
-          const double s = Ss[j * K + p];
+          const double d = Ts[YI(j, p)] + out[p];
+          Ts[YI(j, p)] = d;
+          const double s = Ss[YI(j, p)];
           const double ds = muy / y[p] - s - (s / y[p]) * d;
-          v[0] = fma(d, gYs[j * K + p] - muy / y[p], v[0]);
+          v[0] = fma(d, gYs[YI(j, p)] - muy / y[p], v[0]);
           if (d < 0.0) v[1] = fmin(v[1], -a.tau * y[p] / d);
           if (ds < 0.0) v[2] = fmin(v[2], -a.tau * s / ds);
         }
       }
-      block_reduce_all<3, 0x6, 0>(v, red);
+      block_reduce_all<3, 0x6, 0>(v, red, rph);
       if (tid == 0) {
         scal[0] = v[0];
         scal[1] = v[1];
@@ -853,7 +943,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
       const int p = e / K, c = e % K;
       double s = 0.0;
       #pragma unroll 1
-      for (long j = lane; j < m; j += 32) s = fma(Ys[j * K + p], Ts[j * K + c], s);
+      for (long j = lane; j < m; j += 32) s = fma(Ys[YI(j, p)], Ts[YI(j, c)], s);
       s = warp_sum(s);
       if (lane == 0) Gdy[e] = s;
     }
@@ -907,30 +997,43 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     __syncthreads();
     STAMP(7);
     // ---- quartic partials over own rows x all columns (F recomputed from M)
-    #pragma unroll 1
-    for (long e = tid; e < (long)nr * m; e += PT) {
-      const int rr = (int)(e / m);
-      const long j = e - (long)rr * m;
-      double fv = -Mp[(long)rr * m + j];
+    // thread = one column j (its y_j, dy_j in registers) x every RS-th own row: the
+    // row operands are warp broadcasts and M's row segment is contiguous, so the
+    // pass reads shared memory once per element (the element-major loop re-read
+    // y_j and dy_j per element and was bound by shared-memory wavefronts)
+    if (q_roff < q_rs) {
+      #pragma unroll 1
+      for (long j = q_j0; j < m; j += PT) {
+        double y[K], dy[K];
 #pragma unroll
-      for (int p = 0; p < K; ++p) fv = fma(xs[rr * K + p], Ys[j * K + p], fv);
-      double bv = 0.0, cv = 0.0;
+        for (int p = 0; p < K; ++p) {
+          y[p] = Ys[YI(j, p)];
+          dy[p] = Ts[YI(j, p)];
+        }
+        #pragma unroll 1
+        for (int rr = q_roff; rr < nr; rr += q_rs) {
+          double fv = -Mp[(long)rr * m + j];
 #pragma unroll
-      for (int p = 0; p < K; ++p) {
-        const double x = xs[rr * K + p], dx = dxs[rr * K + p];
-        const double y = Ys[j * K + p], dy = Ts[j * K + p];
-        bv = fma(dx, y, fma(x, dy, bv));
-        cv = fma(dx, dy, cv);
+          for (int p = 0; p < K; ++p) fv = fma(xs[rr * K + p], y[p], fv);
+          double bv = 0.0, cv = 0.0;
+#pragma unroll
+          for (int p = 0; p < K; ++p) {
+            const double x = xs[rr * K + p], dx = dxs[rr * K + p];
+            bv = fma(dx, y[p], fma(x, dy[p], bv));
+            cv = fma(dx, dy[p], cv);
+          }
+          pb[3] = fma(fv, fv, pb[3]);
+          pb[4] = fma(fv, bv, pb[4]);
+          pb[5] = fma(bv, bv, pb[5]);
+          pb[6] = fma(fv, cv, pb[6]);
+          pb[7] = fma(bv, cv, pb[7]);
+          pb[8] = fma(cv, cv, pb[8]);
+        }
       }
-      pb[3] = fma(fv, fv, pb[3]);
-      pb[4] = fma(fv, bv, pb[4]);
-      pb[5] = fma(bv, bv, pb[5]);
-      pb[6] = fma(fv, cv, pb[6]);
-      pb[7] = fma(bv, cv, pb[7]);
-      pb[8] = fma(cv, cv, pb[8]);
     }
+    STAMP(34);
     {
-      block_reduce_all<9, 0x6, 0>(pb, red);
+      block_reduce_all<9, 0x6, 0>(pb, red, rph);
 #pragma unroll
       for (int q = 0; q < 9; ++q)
         if (tid == q) __stcg(PB + (long)q * G + cta, pb[q]);
@@ -959,12 +1062,15 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         #pragma unroll 1
         for (long e = lane; e < (long)nr * K; e += 32)
           ax += log1p(ldexp((a1max * dxs[e]) / xs[e], -tq));
-        const long y0 = (long)cta * N / G, y1 = (long)(cta + 1) * N / G;
         #pragma unroll 1
         for (long e = y0 + lane; e < y1; e += 32) ay += log1p(ldexp((a1max * Ts[e]) / Ys[e], -tq));
       }
-      ax = warp_sum(ax);
-      ay = warp_sum(ay);
+      {
+        double axy[2] = {ax, ay};
+        warp_reduce_multi<2, 0, 0>(axy);
+        ax = axy[0];
+        ay = axy[1];
+      }
       double* pc = PC + (long)(batch & 1) * G * 2 * TB;
       if (lane == 0) {
         __stcg(pc + (long)(2 * wid) * G + cta, ax);
@@ -1038,6 +1144,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
       rs[e] = nudge(rs[e], drs[e], a2, a.tau);
     }
     __syncthreads();
+    STAMP(29);
     double kv[7] = {0.0, 0.0, 0.0, 0.0, 0.0, -1.0 / 0.0, -1.0 / 0.0};  // fsq, k0..k3, kg, kx
     // warps [0, NW/2): rows, two per warp in flight (F, graX, ||F||^2, X-part KKT);
     // warps [NW/2, NW): graY partials, thread per column; the two run concurrently
@@ -1058,38 +1165,41 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         for (long j = lane; j < m; j += 32) {
           double y[K];
 #pragma unroll
-          for (int p = 0; p < K; ++p) y[p] = Ys[j * K + p];
+          for (int p = 0; p < K; ++p) y[p] = Ys[YI(j, p)];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             if (rr2[u] >= nr) continue;
             double fv = -Mp[(long)rr2[u] * m + j];
 #pragma unroll
             for (int p = 0; p < K; ++p) fv = fma(x[u][p], y[p], fv);
-            a.Fout[(r0 + rr2[u]) * m + j] = fv;
             kv[0] = fma(fv, fv, kv[0]);
 #pragma unroll
             for (int p = 0; p < K; ++p) g[u][p] = fma(fv, y[p], g[u][p]);
           }
         }
+        {
+          // recursive-halving warp sums of the 2K row gradients; the lane that ends
+          // up holding entry (u, p) also does its KKT terms
+          using WH = WarpHalve<2 * K, 0, 0>;
+          double gf[2 * K];
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-          for (int p = 0; p < K; ++p) g[u][p] = warp_sum(g[u][p]);
-        if (lane == 0) {
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (rr2[u] >= nr) continue;
-#pragma unroll
-            for (int p = 0; p < K; ++p) {
-              gxs[rr2[u] * K + p] = g[u][p];
-              const double r = rs[rr2[u] * K + p];
-              const double xr = x[u][p] * r;
-              kv[1] = fma(g[u][p] - r, g[u][p] - r, kv[1]);
+          for (int q = 0; q < 2 * K; ++q) gf[q] = g[q / K][q % K];
+          const double gq = WH::run(gf);
+          constexpr int SH = 5 - WH::LG;
+          const int q = lane >> SH;
+          if ((lane & ((1 << SH) - 1)) == 0 && q < 2 * K) {
+            const int u = q / K, p = q - u * K;
+            const int rr = rb + u * HW;
+            if (rr < nr) {
+              gxs[rr * K + p] = gq;
+              const double r = rs[rr * K + p], xv = xs[rr * K + p];
+              const double xr = xv * r;
+              kv[1] = fma(gq - r, gq - r, kv[1]);
               kv[2] = fma(xr - mux, xr - mux, kv[2]);
               kv[3] = fma(xr, xr, kv[3]);
               kv[4] += xr;
-              kv[5] = fmax(kv[5], fabs(g[u][p]));
-              kv[6] = fmax(kv[6], x[u][p]);
+              kv[5] = fmax(kv[5], fabs(gq));
+              kv[6] = fmax(kv[6], xv);
             }
           }
         }
@@ -1097,14 +1207,17 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     } else {
 #pragma unroll 1
       for (long j = tid - PT / 2; j < m; j += PT / 2) {
-        double acc[K];
+        double acc[K], yj[K];
 #pragma unroll
-        for (int p = 0; p < K; ++p) acc[p] = 0.0;
-#pragma unroll 1
+        for (int p = 0; p < K; ++p) {
+          acc[p] = 0.0;
+          yj[p] = Ys[YI(j, p)];
+        }
+#pragma unroll 4
         for (int rr = 0; rr < nr; ++rr) {
           double fv = -Mp[(long)rr * m + j];
 #pragma unroll
-          for (int p = 0; p < K; ++p) fv = fma(xs[rr * K + p], Ys[j * K + p], fv);
+          for (int p = 0; p < K; ++p) fv = fma(xs[rr * K + p], yj[p], fv);
 #pragma unroll
           for (int p = 0; p < K; ++p) acc[p] = fma(fv, xs[rr * K + p], acc[p]);
         }
@@ -1112,8 +1225,9 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         for (int p = 0; p < K; ++p) __stcg(PG + (j * K + p) * G + cta, acc[p]);
       }
     }
+    STAMP(30);
     {
-      block_reduce_all<7, 0, 0x60>(kv, red);
+      block_reduce_all<7, 0, 0x60>(kv, red, rph);
 #pragma unroll
       for (int q = 0; q < 7; ++q)
         if (tid == q) __stcg(PD + (long)q * G + cta, kv[q]);
@@ -1133,7 +1247,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
 
     // ======== phase E: graY slice totals; X-part KKT sums and ||F||^2 ========
     {
-      const long e0 = (long)cta * N / G, e1 = (long)(cta + 1) * N / G;
+      const long e0 = y0, e1 = y1;
       // the slice of graY on warps 0..3 and the KKT / ||F||^2 partials on warps 4..7
       auto sum_kind = [](long) { return 0; };
       reduce_mixed<2, decltype(sum_kind), true>(PG, G, e0, e1, a.gY + e0, sum_kind, 0, NW / 2);
@@ -1146,6 +1260,20 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
 
   // ---- write the state back ----------------------------------------------------
   __syncthreads();
+  if (it > 0) {
+    // F = X Y - M at the final point, with phase D's expression (phase D no longer
+    // stores F every iteration: only the last one is consumed by the host)
+    #pragma unroll 1
+    for (int rr = q_roff; rr < nr && q_roff < q_rs; rr += q_rs) {
+      #pragma unroll 1
+      for (long j = q_j0; j < m; j += PT) {
+        double fv = -Mp[(long)rr * m + j];
+#pragma unroll
+        for (int p = 0; p < K; ++p) fv = fma(xs[rr * K + p], Ys[YI(j, p)], fv);
+        a.Fout[(r0 + rr) * m + j] = fv;
+      }
+    }
+  }
   #pragma unroll 1
   for (long e = tid; e < (long)nr * K; e += PT) {
     a.X[r0 * K + e] = xs[e];
@@ -1155,8 +1283,8 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   if (cta == 0) {
     #pragma unroll 1
     for (long e = tid; e < N; e += PT) {
-      a.Yt[e] = Ys[e];
-      a.S[e] = Ss[e];
+      a.Yt[e] = Ys[YI(e / K, e % K)];
+      a.S[e] = Ss[YI(e / K, e % K)];
     }
     if (tid == 0) {
       a.status[0] = it;
@@ -1164,6 +1292,8 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     }
   }
 }
+#undef YI
+#undef DI
 
 template <int K>
 long p_smem_bytes(long n, long m, int G, bool with_m) {

@@ -28,5 +28,18 @@ for N in (100, 256, 300, 800, 2000):
     L = w.cpu().numpy()
     err = np.abs(L @ L.T - A).max() / np.abs(A).max()
     upper = np.abs(np.triu(L, 1)).max()
-    print(f"N={N:5d}: {min(ts):8.1f} us  rc={rc} info={int(info.item())} relerr {err:.2e} upper {upper:.1e}",
-          flush=True)
+    rhs = torch.as_tensor(rng.standard_normal(N)).cuda()
+    tss = []
+    for rep in range(5):
+        x = rhs.clone()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.nmfb_dense_solve(w.data_ptr(), N, x.data_ptr(), s)
+        e1.record()
+        e1.synchronize()
+        tss.append(e0.elapsed_time(e1) * 1e3)
+    xs = np.linalg.solve(A, rhs.cpu().numpy())
+    serr = np.abs(x.cpu().numpy() - xs).max() / np.abs(xs).max()
+    print(f"N={N:5d}: chol {min(ts):8.1f} us  rc={rc} info={int(info.item())} relerr {err:.2e} "
+          f"upper {upper:.1e} | solve (fwd+back) {min(tss):8.1f} us relerr {serr:.2e}", flush=True)

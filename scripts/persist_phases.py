@@ -27,7 +27,7 @@ for rep in range(2):
                              IpmParams(fixed_iters=200, persist_grid=grid, barrier=barrier))
     torch.cuda.synchronize()
 pr = P.persist_prof.cpu().numpy()[20:180].astype(np.float64)
-d = np.diff(pr[:, :15], axis=1).mean(axis=0) / 1.965e3  # us at 1965 MHz
+d = np.median(np.diff(pr[:, :15], axis=1), axis=0) / 1.965e3  # us at 1965 MHz
 print(name, barrier, "grid", grid, "m", m, "per-iteration us:", round(float(d.sum()), 2),
       "wall ms/it", round(1e3 * P.persist_seconds / max(P.persist_iters, 1), 4))
 for nm, v in zip(names, d):
@@ -36,8 +36,11 @@ sub = {"B: reduce->gY sync": (2, 16), "B: KKT local": (16, 17), "B: KKT reduce+c
        "C: G accumulate": (4, 18), "C: unpack+chol G": (18, 19), "C: T1": (19, 20),
        "C: Hm": (20, 21), "C: chol H": (21, 22), "C: writes+check": (22, 23),
        "C: w solve": (23, 5), "chol G inside": (24, 25), "chol H inside": (26, 27),
-       "w: matvec+fwd": (23, 28), "w: 2 back": (28, 5)}
+       "w: matvec+fwd": (23, 28), "w: 2 back": (28, 5),
+       "A: YY^T": (0, 33), "A: row factors": (33, 31), "A: badA reduce": (31, 32), "A: partials": (32, 1),
+       "Q: pass": (7, 34), "Q: reduce+store": (34, 8),
+       "D: nudge": (11, 29), "D: rows/graY": (29, 30), "D: reduce+store": (30, 12)}
 for nm, (i, j) in sub.items():
-    print(f"  {nm:22s} {float(np.mean(pr[:, j] - pr[:, i])) / 1.965e3:8.2f}")
+    print(f"  {nm:22s} {float(np.median(pr[:, j] - pr[:, i])) / 1.965e3:8.2f}")
 print("armijo t histogram:", np.bincount(np.array(r2.armijo_t)).tolist())
 
