@@ -333,8 +333,11 @@ __device__ __forceinline__ int pk(int a, int b, int k) {
 }
 
 // Cholesky of a K x K SPD matrix in registers (lower), ok flag; small.cu order.
+// rd[j] = 1 / L[j][j] (one rsqrt per pivot): every later "/ L[j][j]" of the row and
+// column factors becomes a multiply, which takes the IEEE division sequences (and
+// their slow-path calls) off the per-iteration dependency chains.
 template <int K>
-__device__ __forceinline__ bool reg_chol(double (&L)[K][K]) {
+__device__ __forceinline__ bool reg_chol(double (&L)[K][K], double (&rd)[K]) {
   bool ok = true;
 #pragma unroll
   for (int j = 0; j < K; ++j) {
@@ -342,21 +345,24 @@ __device__ __forceinline__ bool reg_chol(double (&L)[K][K]) {
 #pragma unroll
     for (int p = 0; p < j; ++p) s -= L[j][p] * L[j][p];
     if (!(s > 0.0)) ok = false;
-    const double d = sqrt(fmax(s, 1e-300));
-    L[j][j] = d;
+    const double sp = fmax(s, 1e-300);
+    const double di = rsqrt(sp);
+    L[j][j] = sp * di;
+    rd[j] = di;
 #pragma unroll
     for (int r = j + 1; r < K; ++r) {
       double t = L[r][j];
 #pragma unroll
       for (int p = 0; p < j; ++p) t -= L[r][p] * L[j][p];
-      L[r][j] = t / d;
+      L[r][j] = t * di;
     }
   }
   return ok;
 }
 
 template <int K>
-__device__ __forceinline__ void reg_inv_lower(const double (&L)[K][K], double (&Li)[K][K]) {
+__device__ __forceinline__ void reg_inv_lower(const double (&L)[K][K], const double (&rd)[K],
+                                              double (&Li)[K][K]) {
 #pragma unroll
   for (int c = 0; c < K; ++c)
 #pragma unroll
@@ -368,28 +374,28 @@ __device__ __forceinline__ void reg_inv_lower(const double (&L)[K][K], double (&
 #pragma unroll
         for (int p = 0; p < a; ++p)
           if (p >= c) s -= L[a][p] * Li[p][c];
-        Li[a][c] = s / L[a][a];
+        Li[a][c] = s * rd[a];
       }
     }
 }
 
 template <int K>
-__device__ __forceinline__ void reg_solve(const double (&L)[K][K], const double (&b)[K],
-                                          double (&out)[K]) {
+__device__ __forceinline__ void reg_solve(const double (&L)[K][K], const double (&rd)[K],
+                                          const double (&b)[K], double (&out)[K]) {
   double z[K];
 #pragma unroll
   for (int a = 0; a < K; ++a) {
     double s = b[a];
 #pragma unroll
     for (int p = 0; p < a; ++p) s -= L[a][p] * z[p];
-    z[a] = s / L[a][a];
+    z[a] = s * rd[a];
   }
 #pragma unroll
   for (int a = K - 1; a >= 0; --a) {
     double s = z[a];
 #pragma unroll
     for (int p = a + 1; p < K; ++p) s -= L[p][a] * out[p];
-    out[a] = s / L[a][a];
+    out[a] = s * rd[a];
   }
 }
 
@@ -408,7 +414,7 @@ __host__ __device__ inline WLayout wlayout(long G, long m, int K) {
   const long sa = KK * KK + 2 * K * K + 1;
   w.pa = 0;
   w.pb = w.pa + G * sa;
-  w.pc = w.pb + G * 9;
+  w.pc = w.pb + G * (9 + 2 * TB);  // 9 direction/quartic sums + the speculative trial batch
   w.pd = w.pc + 2 * G * 2 * TB;
   w.pg = w.pd + G * 8;
   w.total = w.pg + G * N;
@@ -418,7 +424,7 @@ __host__ __device__ inline WLayout wlayout(long G, long m, int K) {
 template <int K>
 __host__ __device__ inline long smem_doubles(long nrm, long m, bool with_m) {
   const long KK = K * (K + 1) / 2, N = m * K;
-  long d = 4 * N + m * KK + nrm * (7 * K + K * K + KK);
+  long d = 4 * N + m * KK + nrm * (8 * K + K * K + KK);
   if (with_m) d += nrm * m;
   return d;
 }
@@ -467,7 +473,8 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   double* gs = hs + nrm * K;
   double* Ls = gs + nrm * K;
   double* As = Ls + nrm * K * K;
-  double* Ms = As + nrm * KK;  // own rows of M (when m_in_smem)
+  double* rds = As + nrm * KK;  // 1 / L_i,pp of the row factors
+  double* Ms = rds + nrm * K;   // own rows of M (when m_in_smem)
 
   __shared__ double ZHX[SA];  // Z (packed kk x kk), H, X^T X, failing R1 row
   double* Zs = ZHX;
@@ -480,6 +487,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   __shared__ double scal[24];  // [0..2] ysc, [3..5] gtp,a1max,a2max, [6..11] quartic
   __shared__ double kx[8];     // X-part KKT sums + fsq (after phase E)
   __shared__ double bars[2 * TB];
+  __shared__ double pbv[9 + 2 * TB];  // reduced phase-B partials (+ speculative trial sums)
   __shared__ int s_fail, s_t;
   __shared__ int ia[KK], ic[KK];
 
@@ -515,6 +523,25 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   // fp64 global rows; the host only allows fp32 M when it is staged)
   const double* Mp = a.m_in_smem ? Ms : (const double*)a.M + r0 * m;
 
+  // Partial barrier sums of trial tq over this CTA's x entries and its slice of y
+  // (warp-uniform tq; lanes stride the entries).  (2^-t a1m num) / den ==
+  // 2^-t ((a1m num) / den) exactly, so one division per entry gives the oracle's
+  // (alpha dv) / v bit for bit.
+  auto trial_sums = [&](int tq, double a1m, double& ax, double& ay) {
+    ax = 0.0;
+    ay = 0.0;
+    if (tq < a.ntrials) {
+      #pragma unroll 1
+      for (long e = lane; e < (long)nr * K; e += 32) ax += log1p(ldexp((a1m * dxs[e]) / xs[e], -tq));
+      #pragma unroll 1
+      for (long e = y0 + lane; e < y1; e += 32) ay += log1p(ldexp((a1m * Ts[e]) / Ys[e], -tq));
+    }
+    double axy[2] = {ax, ay};
+    warp_reduce_multi<2, 0, 0>(axy);
+    ax = axy[0];
+    ay = axy[1];
+  };
+
   unsigned epoch = 0;
   int it = 0;
   int status = 0;
@@ -545,28 +572,31 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         for (int c = 0; c < K; ++c) L[p][c] = (c <= p) ? gy[p * K + c] : 0.0;
 #pragma unroll
       for (int p = 0; p < K; ++p) {
-        L[p][p] += a.rho + rs[rr * K + p] / x[p];
-        b[p] = mux / x[p] - gxs[rr * K + p];
+        const double ix = 1.0 / x[p];
+        L[p][p] += a.rho + rs[rr * K + p] * ix;
+        b[p] = mux * ix - gxs[rr * K + p];
       }
-      if (!reg_chol<K>(L)) badA = fmin(badA, (double)i);
+      double rd[K];
+      if (!reg_chol<K>(L, rd)) badA = fmin(badA, (double)i);
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         double s = b[p];
 #pragma unroll
         for (int q = 0; q < p; ++q) s -= L[p][q] * hv[q];
-        hv[p] = s / L[p][p];
+        hv[p] = s * rd[p];
       }
 #pragma unroll
       for (int p = K - 1; p >= 0; --p) {
         double s = hv[p];
 #pragma unroll
         for (int q = p + 1; q < K; ++q) s -= L[q][p] * gv[q];
-        gv[p] = s / L[p][p];
+        gv[p] = s * rd[p];
       }
       double Li[K][K];
-      reg_inv_lower<K>(L, Li);
+      reg_inv_lower<K>(L, rd, Li);
 #pragma unroll
       for (int p = 0; p < K; ++p) {
+        rds[rr * K + p] = rd[p];
         hs[rr * K + p] = hv[p];
         gs[rr * K + p] = gv[p];
 #pragma unroll
@@ -698,7 +728,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     int badD = 0x7F7F7F7F;
     #pragma unroll 1
     for (long j = tid; j < m; j += PT) {
-      double y[K], L[K][K], rhs[K], tv[K];
+      double y[K], L[K][K], rhs[K], tv[K], iy[K];
 #pragma unroll
       for (int p = 0; p < K; ++p) y[p] = Ys[YI(j, p)];
 #pragma unroll
@@ -706,17 +736,19 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         double ra = 0.0;
 #pragma unroll
         for (int c = 0; c < K; ++c) ra = fma(Hs[p * K + c], y[c], ra);
-        rhs[p] = (muy / y[p] - gYs[YI(j, p)]) - ra;
+        iy[p] = 1.0 / y[p];
+        rhs[p] = (muy * iy[p] - gYs[YI(j, p)]) - ra;
       }
 #pragma unroll
       for (int p = 0; p < K; ++p)
 #pragma unroll
         for (int c = 0; c < K; ++c) L[p][c] = (c <= p) ? XtXs[p * K + c] : 0.0;
 #pragma unroll
-      for (int p = 0; p < K; ++p) L[p][p] += a.rho + Ss[YI(j, p)] / y[p];
-      if (!reg_chol<K>(L)) badD = min(badD, (int)j);
+      for (int p = 0; p < K; ++p) L[p][p] += a.rho + Ss[YI(j, p)] * iy[p];
+      double rd[K];
+      if (!reg_chol<K>(L, rd)) badD = min(badD, (int)j);
       double Li[K][K];
-      reg_inv_lower<K>(L, Li);
+      reg_inv_lower<K>(L, rd, Li);
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         if (cta == 0) {
@@ -732,7 +764,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
           dinv[DI(j, (p * K - p * (p - 1) / 2 + (c - p)))] = s;
         }
       }
-      reg_solve<K>(L, rhs, tv);
+      reg_solve<K>(L, rd, rhs, tv);
 #pragma unroll
       for (int p = 0; p < K; ++p) Ts[YI(j, p)] = tv[p];
     }
@@ -953,10 +985,11 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     double pb[9] = {0.0, 1.0 / 0.0, 1.0 / 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     #pragma unroll 1
     for (int rr = tid; rr < nr; rr += PT) {
-      double L[K][K], v[K], q[K], t[K], dx[K], x[K];
+      double L[K][K], v[K], q[K], t[K], dx[K], x[K], rd[K];
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         x[p] = xs[rr * K + p];
+        rd[p] = rds[rr * K + p];
 #pragma unroll
         for (int c = 0; c < K; ++c) L[p][c] = Ls[(rr * K + p) * K + c];
       }
@@ -972,7 +1005,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         double s = v[p];
 #pragma unroll
         for (int c = 0; c < p; ++c) s -= L[p][c] * q[c];
-        q[p] = s / L[p][p];
+        q[p] = s * rd[p];
       }
 #pragma unroll
       for (int p = 0; p < K; ++p) t[p] = hs[rr * K + p] - q[p];
@@ -981,7 +1014,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         double s = t[p];
 #pragma unroll
         for (int c = p + 1; c < K; ++c) s -= L[c][p] * dx[c];
-        dx[p] = s / L[p][p];
+        dx[p] = s * rd[p];
       }
 #pragma unroll
       for (int p = 0; p < K; ++p) {
@@ -1032,6 +1065,21 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
       }
     }
     STAMP(34);
+    // Speculative first trial batch: a1max = min(1, y ratio, x ratio) where only the
+    // x ratio still needs the grid; with a1s = min(1, y ratio) (replicated) the
+    // partial barrier sums of trials 0..TB-1 ride along with this barrier.  After it,
+    // a1max == a1s (the x rows did not bind, the common case) makes them exact and
+    // phase C skips one grid barrier and one L2 round trip; otherwise phase C
+    // recomputes the batch with the true a1max.
+    {
+      const double a1s = fmin(1.0, scal[1]);
+      double ax, ay;
+      trial_sums(wid, a1s, ax, ay);
+      if (lane == 0) {
+        __stcg(PB + (long)(9 + 2 * wid) * G + cta, ax);
+        __stcg(PB + (long)(10 + 2 * wid) * G + cta, ay);
+      }
+    }
     {
       block_reduce_all<9, 0x6, 0>(pb, red, rph);
 #pragma unroll
@@ -1044,42 +1092,35 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
 
     // ======== phase C: Armijo (quartic + barrier trials in batches) ========
     // [3] gtp_x [4] a1x [5] a2x [6..11] quartic
-    reduce_mixed<2>(PB, G, 0, 9, scal + 3, [](long e) { return (e == 1 || e == 2) ? 1 : 0; });
+    reduce_mixed<4>(PB, G, 0, 9 + 2 * TB, pbv, [](long e) { return (e == 1 || e == 2) ? 1 : 0; });
     __syncthreads();
-    const double gtp = scal[3] + scal[0];
-    const double a1max = fmin(fmin(1.0, scal[4]), scal[1]);
-    const double a2max = fmin(fmin(1.0, scal[5]), scal[2]);
-    const double ab = scal[7], bb = scal[8], ac = scal[9], bc = scal[10], cc = scal[11];
+    const double gtp = pbv[0] + scal[0];
+    const double a1s = fmin(1.0, scal[1]);
+    const double a1max = fmin(fmin(1.0, pbv[1]), scal[1]);
+    const double a2max = fmin(fmin(1.0, pbv[2]), scal[2]);
+    const double ab = pbv[4], bb = pbv[5], ac = pbv[6], bc = pbv[7], cc = pbv[8];
+    const bool spec_ok = (a1max == a1s);
     int tsel = -1;
     for (int batch = 0;; ++batch) {
       const int t0 = batch * TB;
-      // warp q = trial t0 + q; lanes stride this CTA's x entries and its slice of y.
-      // (2^-t a1max num) / den == 2^-t ((a1max num) / den) exactly, so one division
-      // per entry gives the oracle's (alpha dv) / v bit for bit.
-      const int tq = t0 + wid;
-      double ax = 0.0, ay = 0.0;
-      if (tq < a.ntrials) {
-        #pragma unroll 1
-        for (long e = lane; e < (long)nr * K; e += 32)
-          ax += log1p(ldexp((a1max * dxs[e]) / xs[e], -tq));
-        #pragma unroll 1
-        for (long e = y0 + lane; e < y1; e += 32) ay += log1p(ldexp((a1max * Ts[e]) / Ys[e], -tq));
+      const double* bsum = pbv + 9;
+      if (batch > 0 || !spec_ok) {
+        // warp q = trial t0 + q
+        double ax, ay;
+        trial_sums(t0 + wid, a1max, ax, ay);
+        double* pc = PC + (long)(batch & 1) * G * 2 * TB;
+        if (lane == 0) {
+          __stcg(pc + (long)(2 * wid) * G + cta, ax);
+          __stcg(pc + (long)(2 * wid + 1) * G + cta, ay);
+        }
+        STAMP(10);
+        grid_barrier(a.bar, epoch);
+        reduce_entries<2, 0>(pc, G, 0, 2 * TB, bars);
+        __syncthreads();
+        bsum = bars;
+      } else {
+        STAMP(10);
       }
-      {
-        double axy[2] = {ax, ay};
-        warp_reduce_multi<2, 0, 0>(axy);
-        ax = axy[0];
-        ay = axy[1];
-      }
-      double* pc = PC + (long)(batch & 1) * G * 2 * TB;
-      if (lane == 0) {
-        __stcg(pc + (long)(2 * wid) * G + cta, ax);
-        __stcg(pc + (long)(2 * wid + 1) * G + cta, ay);
-      }
-      STAMP(10);
-      grid_barrier(a.bar, epoch);
-      reduce_entries<2, 0>(pc, G, 0, 2 * TB, bars);
-      __syncthreads();
       if (tid < 32) {
         // lane q evaluates trial t0 + q with the arithmetic of armijo_pick (csrc/small.cu)
         // and of the host loop; the first lane that accepts (or passes max_bt) decides
@@ -1095,8 +1136,8 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
             double quad = __dadd_rn(__dmul_rn(a1, ab), __dmul_rn(q2, c2));
             quad = __dadd_rn(quad, __dmul_rn(q3, bc));
             quad = __dadd_rn(quad, __dmul_rn(__dmul_rn(0.5, q4), cc));
-            const double bar = __dadd_rn(__dmul_rn(a.wx, bars[2 * lane]),
-                                         __dmul_rn(a.wy, bars[2 * lane + 1]));
+            const double bar = __dadd_rn(__dmul_rn(a.wx, bsum[2 * lane]),
+                                         __dmul_rn(a.wy, bsum[2 * lane + 1]));
             const double dphi = __dsub_rn(quad, __dmul_rn(a.mu, bar));
             acc = dphi <= __dmul_rn(__dmul_rn(a.eta, a1), gtp);
           }
