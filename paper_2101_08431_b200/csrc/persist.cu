@@ -424,7 +424,7 @@ __host__ __device__ inline WLayout wlayout(long G, long m, int K) {
 template <int K>
 __host__ __device__ inline long smem_doubles(long nrm, long m, bool with_m) {
   const long KK = K * (K + 1) / 2, N = m * K;
-  long d = 4 * N + m * KK + nrm * (8 * K + K * K + KK);
+  long d = 6 * N + m * KK + nrm * (10 * K + 2 * K * K + KK);  // + double-buffered factorization snapshots
   if (with_m) d += nrm * m;
   return d;
 }
@@ -471,8 +471,12 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   double* drs = dxs + nrm * K;
   double* hs = drs + nrm * K;
   double* gs = hs + nrm * K;
-  double* Ls = gs + nrm * K;
-  double* As = Ls + nrm * K * K;
+  // row factors and the factorization point (X rows, Y) double-buffered by iteration
+  // parity: the last step's factorization is committed to global memory once, at exit
+  double* Lsb = gs + nrm * K;
+  double* xsnap = Lsb + 2 * nrm * K * K;
+  double* Ysnap = xsnap + 2 * nrm * K;
+  double* As = Ysnap + 2 * N;
   double* rds = As + nrm * KK;  // 1 / L_i,pp of the row factors
   double* Ms = rds + nrm * K;   // own rows of M (when m_in_smem)
 
@@ -545,9 +549,19 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   unsigned epoch = 0;
   int it = 0;
   int status = 0;
+  int fact_it = -1;  // iteration whose factorization (L, X rows, Y) is committed at exit
   for (;;) {
     // ======== phase A: rows -> R1 factors, h, g; partials of Z, H, X^T X ========
     STAMP(0);
+    double* Ls = Lsb + (long)(it & 1) * nrm * K * K;
+    {
+      double* ysn = Ysnap + (long)(it & 1) * N;
+      double* xsn = xsnap + (long)(it & 1) * nrm * K;
+      #pragma unroll 1
+      for (long e = tid; e < N; e += PT) ysn[e] = Ys[e];
+      #pragma unroll 1
+      for (long e = tid; e < (long)nr * K; e += PT) xsn[e] = xs[e];
+    }
     #pragma unroll 1
     for (int e = wid; e < K * K; e += NW) {
       const int p = e / K, q = e % K;
@@ -706,22 +720,16 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
       }
       if (!(e_mu > a.eps_mu) || !(e_0 > a.tol0) || it >= a.max_iters) {
         status = 0;
+        fact_it = it - 1;  // the factorization of the last step taken
         break;
       }
     }
     if (ZHX[SA - 1] < 1.0 / 0.0) {
       if (cta == 0 && tid == 0) a.fcodes[0] = (int)ZHX[SA - 1];
       status = 1;
+      fact_it = it - 1;
       break;
     }
-    // commit this iteration's row factors (the predictor reuses the last ones)
-    #pragma unroll 1
-    for (long e = tid; e < (long)nr * K * K; e += PT) a.L[r0 * K * K + e] = Ls[e];
-    #pragma unroll 1
-    for (long e = tid; e < (long)nr * K; e += PT) a.Xf[r0 * K + e] = xs[e];
-    if (cta == 0)
-      #pragma unroll 1
-      for (long e = tid; e < N; e += PT) a.Ytf[e] = Ys[YI(e / K, e % K)];
 
     STAMP(3);
     // ---- Y side (replicated): rhs, D_j, t_j = D_j^{-1} rhs_j, D_j^{-1} packed
@@ -879,6 +887,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         a.fcodes[2] = badD;
       }
       status = 1;
+      fact_it = it;
       break;
     }
     STAMP(23);
@@ -1043,7 +1052,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
           y[p] = Ys[YI(j, p)];
           dy[p] = Ts[YI(j, p)];
         }
-        #pragma unroll 1
+        #pragma unroll 2
         for (int rr = q_roff; rr < nr; rr += q_rs) {
           double fv = -Mp[(long)rr * m + j];
 #pragma unroll
@@ -1165,6 +1174,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         rec[2] = 0.0;
       }
       status = 2;
+      fact_it = it;
       break;
     }
     STAMP(11);
@@ -1187,16 +1197,19 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     __syncthreads();
     STAMP(29);
     double kv[7] = {0.0, 0.0, 0.0, 0.0, 0.0, -1.0 / 0.0, -1.0 / 0.0};  // fsq, k0..k3, kg, kx
-    // warps [0, NW/2): rows, two per warp in flight (F, graX, ||F||^2, X-part KKT);
+    // warps [0, NW/2): rows, RPW per warp in flight (F, graX, ||F||^2, X-part KKT);
     // warps [NW/2, NW): graY partials, thread per column; the two run concurrently
     if (wid < NW / 2) {
       constexpr int HW = NW / 2;
+      constexpr int RPW = K <= 2 ? 4 : 3;  // c2: 20-21 rows per CTA in two passes
 #pragma unroll 1
-      for (int rb = wid; rb < nr; rb += 2 * HW) {
-        const int rr2[2] = {rb, rb + HW};
-        double x[2][K], g[2][K];
+      for (int rb = wid; rb < nr; rb += RPW * HW) {
+        int rr2[RPW];
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
+        for (int u = 0; u < RPW; ++u) rr2[u] = rb + u * HW;
+        double x[RPW][K], g[RPW][K];
+#pragma unroll
+        for (int u = 0; u < RPW; ++u)
 #pragma unroll
           for (int p = 0; p < K; ++p) {
             x[u][p] = rr2[u] < nr ? xs[rr2[u] * K + p] : 0.0;
@@ -1208,7 +1221,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
 #pragma unroll
           for (int p = 0; p < K; ++p) y[p] = Ys[YI(j, p)];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < RPW; ++u) {
             if (rr2[u] >= nr) continue;
             double fv = -Mp[(long)rr2[u] * m + j];
 #pragma unroll
@@ -1221,14 +1234,14 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
         {
           // recursive-halving warp sums of the 2K row gradients; the lane that ends
           // up holding entry (u, p) also does its KKT terms
-          using WH = WarpHalve<2 * K, 0, 0>;
-          double gf[2 * K];
+          using WH = WarpHalve<RPW * K, 0, 0>;
+          double gf[RPW * K];
 #pragma unroll
-          for (int q = 0; q < 2 * K; ++q) gf[q] = g[q / K][q % K];
+          for (int q = 0; q < RPW * K; ++q) gf[q] = g[q / K][q % K];
           const double gq = WH::run(gf);
           constexpr int SH = 5 - WH::LG;
           const int q = lane >> SH;
-          if ((lane & ((1 << SH) - 1)) == 0 && q < 2 * K) {
+          if ((lane & ((1 << SH) - 1)) == 0 && q < RPW * K) {
             const int u = q / K, p = q - u * K;
             const int rr = rb + u * HW;
             if (rr < nr) {
@@ -1301,6 +1314,19 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
 
   // ---- write the state back ----------------------------------------------------
   __syncthreads();
+  if (fact_it >= 0) {  // the predictor reuses the last step's factorization
+    const double* Lc = Lsb + (long)(fact_it & 1) * nrm * K * K;
+    const double* xsn = xsnap + (long)(fact_it & 1) * nrm * K;
+    #pragma unroll 1
+    for (long e = tid; e < (long)nr * K * K; e += PT) a.L[r0 * K * K + e] = Lc[e];
+    #pragma unroll 1
+    for (long e = tid; e < (long)nr * K; e += PT) a.Xf[r0 * K + e] = xsn[e];
+    if (cta == 0) {
+      const double* ysn = Ysnap + (long)(fact_it & 1) * N;
+      #pragma unroll 1
+      for (long e = tid; e < N; e += PT) a.Ytf[e] = ysn[YI(e / K, e % K)];
+    }
+  }
   if (it > 0) {
     // F = X Y - M at the final point, with phase D's expression (phase D no longer
     // stores F every iteration: only the last one is consumed by the host)
