@@ -74,6 +74,20 @@ int nmfb_surface_back_substitute(const double *x_rows, const double *y_cols, con
  * fixed decomposition (bit-reproducible).  `work` buffers are caller-owned
  * scratch of at least the stated length (doubles). */
 
+/* nnls_batch (same arguments, results and codes as nmfb_surface_nnls_batch) with a
+ * caller workspace `ftab` of nmfb_nnls_ftab_len(k) doubles (0 when k > 12: the table
+ * is then not used).  The passive Cholesky factor of every subset of {0..k-1} is
+ * computed once per call in the reference's operation order and shared by all
+ * right-hand sides and Lawson-Hanson trips -- the reference's factor cache keyed by
+ * the passive signature (_kernels_numba.py:296-298, 334-349) -- so the bits match. */
+long nmfb_nnls_ftab_len(long k);
+int nmfb_nnls_batch_ws(const double *ctc, const double *ctb, const double *btb,
+                       const uint8_t *warm_passive, int warm_mode, const double *tol,
+                       long max_changes, long nrhs, long k, double *x, uint8_t *passive,
+                       long long *changes, double *resid2, int8_t *status,
+                       uint8_t *seed_scratch, int *flag_scratch, double *ftab, long ftab_len,
+                       void *stream);
+
 /* out (rows, k) = scale * A B, A (rows, cols), B (cols, k); tol[i] =
  * 1e-12 max(1, ||out_i||_inf) when tol != NULL; work >= nmfb_rowprod_work_len.
  * Replaces the driver products M Y^T (update_X) and F Y^T. */

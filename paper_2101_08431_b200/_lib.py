@@ -27,6 +27,8 @@ SIGNATURES = {
     "nmfb_surface_rhs_reduce": [P, P, P, P, P, L, L, L, I, P, P],
     "nmfb_surface_back_substitute": [P, P, P, P, P, P, L, L, L, I, P, P],
     # production entries
+    "nmfb_nnls_ftab_len": [L],
+    "nmfb_nnls_batch_ws": [P, P, P, P, I, P, L, L, L, P, P, P, P, P, P, P, P, L, P],
     "nmfb_rowprod_work_len": [L, L, L, I],
     "nmfb_rowprod": [P, I, L, L, P, L, P, P, D, P, L, P],
     "nmfb_colprod_work_len": [L, L, L],
@@ -78,7 +80,7 @@ SIGNATURES = {
     "nmfb_lowrank_factor": [P, P, L, P, P, P, P, P],
     "nmfb_lowrank_solve": [P, P, P, P, P, L, L, P, P, P, P, P, L, P],
 }
-RESTYPES = {"nmfb_colprod_work_len": ctypes.c_long, "nmfb_rowprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
+RESTYPES = {"nmfb_nnls_ftab_len": ctypes.c_long, "nmfb_colprod_work_len": ctypes.c_long, "nmfb_rowprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
             "nmfb_launch_count": ctypes.c_ulonglong, "nmfb_small_work_len": ctypes.c_long,
             "nmfb_persist_work_len": ctypes.c_long, "nmfb_grams_work_len": ctypes.c_long,
             "nmfb_term4_work_len": ctypes.c_long,

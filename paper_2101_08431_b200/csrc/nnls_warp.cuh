@@ -27,10 +27,23 @@ struct WNnls {
   double C[K];   // row `sl` of ctc
   int sl;        // lane within the segment
   unsigned sm;   // segment mask (lanes of this rhs)
+  // optional factor table (csrc/surface.cu k_factor_table): T[(pm K + i) K + j] is the
+  // passive factor of subset pm in global indices, okf[pm] its PD flag.  The same
+  // operation sequence computed once per subset instead of once per rhs and trip
+  // (the reference's factor cache keyed by the passive signature,
+  // _kernels_numba.py:296-298, 334-349).
+  const double* T = nullptr;
+  const double* okf = nullptr;
 
   __device__ __forceinline__ double sh(double v, int src) const { return __shfl_sync(sm, v, src, W); }
 
   __device__ __forceinline__ bool factor(unsigned pm) {
+    if (T != nullptr) {
+      const double* row = T + ((long)pm * K + (sl < K ? sl : 0)) * K;
+#pragma unroll
+      for (int c = 0; c < K; ++c) Lr[c] = sl < K ? __ldg(row + c) : 0.0;
+      return __ldg(okf + pm) != 0.0;
+    }
 #pragma unroll
     for (int c = 0; c < K; ++c) Lr[c] = 0.0;
     bool ok = true;

@@ -233,6 +233,286 @@ __global__ void __launch_bounds__(128) k_nnls(const double* __restrict__ ctc_g,
 }
 
 
+// Passive Cholesky factors of every subset pm of {0..K-1}, one W-lane warp segment
+// per subset running WNnls::factor (the bit-exact column-oriented factor of
+// k_nnls_warp), scattered to global indices: T[(pm K + i) K + j], zero outside the
+// passive rows/columns; okf[pm] = 1 when every pivot is positive.
+template <int K, int W>
+__global__ void __launch_bounds__(128) k_factor_table(const double* __restrict__ ctc_g,
+                                                      double* __restrict__ T,
+                                                      double* __restrict__ okf) {
+  constexpr int SEGS = 32 / W;
+  __shared__ double ctc[K * K];
+  for (int i = threadIdx.x; i < K * K; i += blockDim.x) ctc[i] = ctc_g[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, seg = lane / W;
+  const long pm = ((long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * SEGS + seg;
+  if (pm >= (1L << K)) return;  // segment-uniform
+  WNnls<K, W> s;
+  s.sl = lane % W;
+  s.sm = (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << (seg * W));
+  const bool own = s.sl < K;
+#pragma unroll
+  for (int c = 0; c < K; ++c) s.C[c] = own ? ctc[s.sl * K + c] : 0.0;
+  const bool ok = s.factor((unsigned)pm);
+  if (own) {
+    double* row = T + (pm * K + s.sl) * K;
+#pragma unroll
+    for (int c = 0; c < K; ++c) row[c] = s.Lr[c];
+  }
+  if (s.sl == 0) okf[pm] = ok ? 1.0 : 0.0;
+}
+
+// nnls_batch, one thread per rhs with every per-rhs vector in registers (exact K,
+// fully unrolled) and the passive factors read from the subset table.  The
+// passive set is a bit mask; loops run over all K indices in ascending order and
+// skip non-passive terms with selects (acc stays bit-identical to the
+// reference's loop over passive positions), so a warp stays converged inside a
+// Lawson-Hanson trip and issues ~K^2 instructions per trip for 32 right-hand
+// sides (the warp-per-rhs kernel issues that per rhs).
+constexpr int TAB_T = 64;  // threads per block of k_nnls_tab
+
+template <int K>
+struct TNnls {
+  static constexpr int KT = K * (K + 1) / 2;
+  const double* C;  // ctc (K x K, shared memory: broadcast reads)
+  double* sL;       // this thread's staged factor: packed lower entry e at sL[e * TAB_T]
+  double d[K];
+
+  __device__ __forceinline__ static bool bit(unsigned pm, int i) { return (pm >> i) & 1u; }
+  __device__ __forceinline__ static constexpr int tri(int i, int j) { return i * (i + 1) / 2 + j; }
+  __device__ __forceinline__ double l(int i, int j) const { return sL[tri(i, j) * TAB_T]; }
+
+  // stage the table factor of subset pm: every entry is an asynchronous global ->
+  // shared copy (cp.async, no registers), all in flight together, so a trip pays
+  // one gather round trip instead of a divergent global load inside every step of
+  // the solves (or one round trip per row)
+  __device__ __forceinline__ void stage(const double* __restrict__ T, unsigned pm) {
+    const double* Lt = T + (long)pm * K * K;
+    const unsigned base = (unsigned)__cvta_generic_to_shared(sL);
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                         base + (unsigned)(tri(i, j) * TAB_T * sizeof(double))),
+                     "l"(Lt + i * K + j)
+                     : "memory");
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  }
+
+  // _chol_solve_small (:247-258) on the passive indices with the staged factor
+  __device__ __forceinline__ void solve(unsigned pm, const double (&b)[K], double (&z)[K]) const {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double acc = b[i];
+#pragma unroll
+      for (int p = 0; p < i; ++p) {
+        const double t = acc - l(i, p) * z[p];
+        acc = bit(pm, p) ? t : acc;
+      }
+      z[i] = bit(pm, i) ? acc / l(i, i) : 0.0;
+    }
+    asm volatile("" ::: "memory");
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+      double acc = z[i];
+#pragma unroll
+      for (int p = i + 1; p < K; ++p) {
+        const double t = acc - l(p, i) * z[p];
+        acc = bit(pm, p) ? t : acc;
+      }
+      z[i] = bit(pm, i) ? acc / l(i, i) : 0.0;
+    }
+  }
+
+  // _passive_solve_refined (:261-274): z = solve(d); r = d - C_PP z; z += solve(r)
+  __device__ __forceinline__ void solve_refined(const double* __restrict__ T, unsigned pm,
+                                                double (&z)[K]) {
+    stage(T, pm);
+    // compiler memory barriers: the two solves re-read the staged factor instead
+    // of keeping all K(K+1)/2 entries live in registers between them
+    asm volatile("" ::: "memory");
+    solve(pm, d, z);
+    asm volatile("" ::: "memory");
+    double r[K], dz[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      double acc = d[a];
+#pragma unroll
+      for (int b = 0; b < K; ++b) {
+        const double t = acc - C[a * K + b] * z[b];
+        acc = bit(pm, b) ? t : acc;
+      }
+      r[a] = acc;
+    }
+    solve(pm, r, dz);
+#pragma unroll
+    for (int a = 0; a < K; ++a) z[a] = bit(pm, a) ? z[a] + dz[a] : 0.0;
+  }
+
+  // w_j = d_j - sum_p ctc[j][p] x_p over ALL p (the reference's dual loop)
+  __device__ __forceinline__ void grad(const double (&x)[K], double (&w)[K]) const {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double acc = d[j];
+#pragma unroll
+      for (int p = 0; p < K; ++p) acc -= C[j * K + p] * x[p];
+      w[j] = acc;
+    }
+  }
+};
+
+template <int K>
+__global__ void __launch_bounds__(TAB_T) k_nnls_tab(const double* __restrict__ ctc_g,
+                                                  const double* __restrict__ ctb,
+                                                  const double* __restrict__ btb,
+                                                  const uint8_t* __restrict__ seeds, int seed_mode,
+                                                  const double* __restrict__ tol, long max_changes,
+                                                  long nrhs, double* __restrict__ x_out,
+                                                  uint8_t* __restrict__ p_out,
+                                                  long long* __restrict__ ch_out,
+                                                  double* __restrict__ r2_out,
+                                                  int8_t* __restrict__ st_out,
+                                                  const double* __restrict__ T) {
+  __shared__ double ctc[K * K];
+  __shared__ double sLall[TNnls<K>::KT * TAB_T];
+  for (int i = threadIdx.x; i < K * K; i += blockDim.x) ctc[i] = ctc_g[i];
+  __syncthreads();
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrhs) return;
+  const double* okf = T + ((long)K * K << K);
+  TNnls<K> s;
+  s.C = ctc;
+  s.sL = sLall + threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < K; ++j) s.d[j] = ctb[t * K + j];
+  const double tol_t = tol[t];
+  double x[K], z[K], w[K];
+  unsigned pm = 0u;
+  long nch = 0;
+  bool solved = false;
+  const bool use_seed = (seed_mode == 2) || (seed_mode == 1 && t > 0);
+  if (use_seed) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) pm |= (seeds[t * K + j] != 0 ? 1u : 0u) << j;
+    if (pm == 0u) {
+      bool ok = true;
+#pragma unroll
+      for (int j = 0; j < K; ++j) ok = ok && !(s.d[j] > tol_t);
+      if (ok) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) x[j] = 0.0;
+        solved = true;
+      }
+    } else if (__ldg(okf + pm) != 0.0) {
+      s.solve_refined(T, pm, z);
+      bool feas = true;
+#pragma unroll
+      for (int a = 0; a < K; ++a) feas = feas && !(TNnls<K>::bit(pm, a) && z[a] < 0.0);
+      if (feas) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) x[j] = TNnls<K>::bit(pm, j) ? z[j] : 0.0;
+        s.grad(x, w);
+        bool dual_ok = true;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          dual_ok = dual_ok && !(TNnls<K>::bit(pm, j) ? (fabs(w[j]) > tol_t) : (w[j] > tol_t));
+        solved = dual_ok;
+      }
+    }
+  }
+  int st = 0;
+  if (!solved) {
+    // cold Lawson-Hanson start (:377-461)
+    pm = 0u;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      x[j] = 0.0;
+      w[j] = s.d[j];
+    }
+    for (;;) {
+      int jmax = -1;
+      double wmax = tol_t;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const bool c = !TNnls<K>::bit(pm, j) && w[j] > wmax;
+        wmax = c ? w[j] : wmax;
+        jmax = c ? j : jmax;
+      }
+      if (jmax < 0) break;
+      pm |= 1u << jmax;
+      nch += 1;
+      if (nch > max_changes) {
+        st = 1;
+        break;
+      }
+      for (;;) {
+        if (pm == 0u) break;
+        if (__ldg(okf + pm) == 0.0) {
+          st = 2;
+          break;
+        }
+        s.solve_refined(T, pm, z);
+        bool all_pos = true;
+#pragma unroll
+        for (int a = 0; a < K; ++a) all_pos = all_pos && !(TNnls<K>::bit(pm, a) && z[a] <= 0.0);
+        if (all_pos) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) x[j] = TNnls<K>::bit(pm, j) ? z[j] : 0.0;
+          break;
+        }
+        double alpha = 1.0;
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          if (TNnls<K>::bit(pm, a) && z[a] <= 0.0) {
+            const double ratio = x[a] / (x[a] - z[a]);
+            alpha = ratio < alpha ? ratio : alpha;
+          }
+        }
+        unsigned drop = 0u;
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          if (!TNnls<K>::bit(pm, a)) continue;
+          const double xa = x[a];
+          const double newx = xa + alpha * (z[a] - xa);
+          if (z[a] <= 0.0 && xa / (xa - z[a]) <= alpha) {
+            x[a] = 0.0;
+            drop |= 1u << a;
+          } else {
+            x[a] = newx > 0.0 ? newx : 0.0;
+          }
+        }
+        pm &= ~drop;
+        nch += __popc(drop);
+        if (nch > max_changes) {
+          st = 1;
+          break;
+        }
+      }
+      if (st != 0) break;
+      s.grad(x, w);
+    }
+  }
+  double r2 = btb[t];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    x_out[t * K + j] = x[j];
+    p_out[t * K + j] = TNnls<K>::bit(pm, j) ? 1 : 0;
+    r2 -= 2.0 * x[j] * s.d[j];
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double acc = 0.0;
+#pragma unroll
+    for (int p = 0; p < K; ++p) acc += ctc[j * K + p] * x[p];
+    r2 += x[j] * acc;
+  }
+  ch_out[t] = nch;
+  r2_out[t] = r2 > 0.0 ? r2 : 0.0;
+  st_out[t] = (int8_t)st;
+}
+
 template <int K, int W>
 __global__ void __launch_bounds__(128) k_nnls_warp(const double* __restrict__ ctc_g,
                                                    const double* __restrict__ ctb,
@@ -243,7 +523,8 @@ __global__ void __launch_bounds__(128) k_nnls_warp(const double* __restrict__ ct
                                                    uint8_t* __restrict__ p_out,
                                                    long long* __restrict__ ch_out,
                                                    double* __restrict__ r2_out,
-                                                   int8_t* __restrict__ st_out) {
+                                                   int8_t* __restrict__ st_out,
+                                                   const double* __restrict__ ftab = nullptr) {
   constexpr int SEGS = 32 / W;
   __shared__ double ctc[K * K];
   for (int i = threadIdx.x; i < K * K; i += blockDim.x) ctc[i] = ctc_g[i];
@@ -252,6 +533,10 @@ __global__ void __launch_bounds__(128) k_nnls_warp(const double* __restrict__ ct
   const long t = ((long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * SEGS + seg;
   if (t >= nrhs) return;  // segment-uniform
   WNnls<K, W> s;
+  if (ftab != nullptr) {
+    s.T = ftab;
+    s.okf = ftab + ((long)K * K << K);
+  }
   s.sl = lane % W;
   s.sm = (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << (seg * W));
   const int sl = s.sl;
@@ -545,15 +830,41 @@ int kbucket(long k) { return k <= 4 ? 4 : (k <= 8 ? 8 : 16); }
     default: CALL(16); break;    \
   }
 
-extern "C" int nmfb_surface_nnls_batch(const double* ctc, const double* ctb, const double* btb,
-                                       const uint8_t* warm_passive, int warm_mode,
-                                       const double* tol, long max_changes, long nrhs, long k,
-                                       double* x, uint8_t* passive, long long* changes,
-                                       double* resid2, int8_t* status, uint8_t* seed_scratch,
-                                       int* flag_scratch, void* stream_) {
+constexpr int FTAB_MAXK = 12;  // 4096 subsets x 144 doubles = 4.7 MB
+
+static long ftab_len_k(long k) { return (k < 1 || k > FTAB_MAXK) ? 0 : (k * k + 1) << k; }
+
+extern "C" long nmfb_nnls_ftab_len(long k) { return ftab_len_k(k); }
+
+static int nnls_batch_impl(const double* ctc, const double* ctb, const double* btb,
+                           const uint8_t* warm_passive, int warm_mode, const double* tol,
+                           long max_changes, long nrhs, long k, double* x, uint8_t* passive,
+                           long long* changes, double* resid2, int8_t* status,
+                           uint8_t* seed_scratch, int* flag_scratch, double* ftab, long ftab_len,
+                           void* stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   if (k < 1 || k > NMFB_MAX_K || nrhs < 0 || warm_mode < 0 || warm_mode > 2) return NMFB_EINVAL;
   if (nrhs == 0) return NMFB_OK;
+  // factor table of every passive subset (k <= FTAB_MAXK, caller workspace)
+  const double* ft = nullptr;
+  if (ftab != nullptr && ftab_len_k(k) > 0 && ftab_len >= ftab_len_k(k)) {
+    const unsigned nsub = 1u << k;
+#define FTCASE(KK)                                                                            \
+  case KK: {                                                                                  \
+    constexpr int WW = KK <= 4 ? 4 : (KK <= 8 ? 8 : 16);                                      \
+    const unsigned per_blk = 4u * (32 / WW);                                                  \
+    ++g_nmfb_launches, k_factor_table<KK, WW><<<(nsub + per_blk - 1) / per_blk, 128, 0,       \
+                                                stream>>>(ctc, ftab, ftab + ((long)KK * KK << KK)); \
+    break;                                                                                    \
+  }
+    switch (k) {
+      FTCASE(1) FTCASE(2) FTCASE(3) FTCASE(4) FTCASE(5) FTCASE(6) FTCASE(7) FTCASE(8)
+      FTCASE(9) FTCASE(10) FTCASE(11) FTCASE(12)
+      default: break;
+    }
+#undef FTCASE
+    ft = ftab;
+  }
   const int threads = 128;
   const int blocks = (int)((nrhs + threads - 1) / threads);
   // Same bits either way.  Warp per rhs (k_nnls_warp) wins when the batch cannot
@@ -565,7 +876,7 @@ extern "C" int nmfb_surface_nnls_batch(const double* ctc, const double* ctb, con
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
   const bool thread_kernel =
-      force >= 0 ? force == 1 : !((nrhs <= 8192 && k <= 12) || nrhs <= 2048);
+      force >= 0 ? force == 1 : (ft == nullptr && !((nrhs <= 8192 && k <= 12) || nrhs <= 2048));
 #define WCASE(KW, SEEDS, MODE)                                                                   \
   case KW: {                                                                                     \
     constexpr int WW = KW <= 4 ? 4 : (KW <= 8 ? 8 : 16);                                         \
@@ -573,11 +884,24 @@ extern "C" int nmfb_surface_nnls_batch(const double* ctc, const double* ctb, con
     ++g_nmfb_launches, k_nnls_warp<KW, WW><<<(unsigned)((nrhs + per_blk - 1) / per_blk), 128, 0, \
                                              stream>>>(ctc, ctb, btb, SEEDS, MODE, tol,           \
                                              max_changes, nrhs, x, passive, changes, resid2,     \
-                                             status);                                            \
+                                             status, ft);                                        \
     break;                                                                                       \
   }
+#define TCASE(KT, SEEDS, MODE)                                                                  \
+  case KT:                                                                                      \
+    ++g_nmfb_launches, k_nnls_tab<KT><<<(unsigned)((nrhs + TAB_T - 1) / TAB_T), TAB_T, 0, stream>>>( \
+        ctc, ctb, btb, SEEDS, MODE, tol, max_changes, nrhs, x, passive, changes, resid2, status, \
+        ft);                                                                                    \
+    break;
 #define LAUNCH_NNLS(KK, SEEDS, MODE)                                                        \
-  if (thread_kernel) {                                                                      \
+  if (ft != nullptr && force < 0) {                                                         \
+    switch (k) {                                                                            \
+      TCASE(1, SEEDS, MODE) TCASE(2, SEEDS, MODE) TCASE(3, SEEDS, MODE) TCASE(4, SEEDS, MODE) \
+      TCASE(5, SEEDS, MODE) TCASE(6, SEEDS, MODE) TCASE(7, SEEDS, MODE) TCASE(8, SEEDS, MODE) \
+      TCASE(9, SEEDS, MODE) TCASE(10, SEEDS, MODE) TCASE(11, SEEDS, MODE) TCASE(12, SEEDS, MODE) \
+      default: return NMFB_EINVAL;                                                          \
+    }                                                                                       \
+  } else if (thread_kernel) {                                                               \
     ++g_nmfb_launches, k_nnls<KK><<<blocks, threads, 0, stream>>>(ctc, ctb, btb, SEEDS, MODE, tol, max_changes, \
                                              nrhs, (int)k, x, passive, changes, resid2, status); \
   } else {                                                                                  \
@@ -622,7 +946,30 @@ extern "C" int nmfb_surface_nnls_batch(const double* ctc, const double* ctb, con
   }
 #undef LAUNCH_NNLS
 #undef WCASE
+#undef TCASE
   return NMFB_OK;
+}
+
+extern "C" int nmfb_surface_nnls_batch(const double* ctc, const double* ctb, const double* btb,
+                                       const uint8_t* warm_passive, int warm_mode,
+                                       const double* tol, long max_changes, long nrhs, long k,
+                                       double* x, uint8_t* passive, long long* changes,
+                                       double* resid2, int8_t* status, uint8_t* seed_scratch,
+                                       int* flag_scratch, void* stream) {
+  return nnls_batch_impl(ctc, ctb, btb, warm_passive, warm_mode, tol, max_changes, nrhs, k, x,
+                         passive, changes, resid2, status, seed_scratch, flag_scratch, nullptr, 0,
+                         stream);
+}
+
+extern "C" int nmfb_nnls_batch_ws(const double* ctc, const double* ctb, const double* btb,
+                                  const uint8_t* warm_passive, int warm_mode, const double* tol,
+                                  long max_changes, long nrhs, long k, double* x,
+                                  uint8_t* passive, long long* changes, double* resid2,
+                                  int8_t* status, uint8_t* seed_scratch, int* flag_scratch,
+                                  double* ftab, long ftab_len, void* stream) {
+  return nnls_batch_impl(ctc, ctb, btb, warm_passive, warm_mode, tol, max_changes, nrhs, k, x,
+                         passive, changes, resid2, status, seed_scratch, flag_scratch, ftab,
+                         ftab_len, stream);
 }
 
 extern "C" int nmfb_surface_block_cholesky(const double* blocks_in, long nb, long k,

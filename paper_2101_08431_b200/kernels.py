@@ -143,10 +143,13 @@ def back_substitute(x_rows, y_cols, l, h, dy_rows, resid, full):
     return a.out(dx)
 
 
-def nnls_batch(ctc, ctb, btb, warm_passive, warm_mode, tol, max_changes):
+def nnls_batch(ctc, ctb, btb, warm_passive, warm_mode, tol, max_changes, *, table=True):
     """_kernels_numba.py:277-477 -> (x, passive, changes, resid2, status).
 
     status per rhs: 0 solved, 1 change cap exceeded, 2 rank-deficient passive set.
+    table (keyword-only extension): for k <= 12 factor every passive subset once per
+    call (nmfb_nnls_batch_ws, the reference's factor cache); False runs the
+    per-rhs factorizing kernels of nmfb_surface_nnls_batch.  Same bits either way.
     """
     a = _Args(ctc, ctb, btb, warm_passive, tol)
     C, B, BB, T = a.f64(ctc), a.f64(ctb), a.f64(btb), a.f64(tol)
@@ -162,7 +165,14 @@ def nnls_batch(ctc, ctb, btb, warm_passive, warm_mode, tol, max_changes):
     if int(warm_mode) == 1:
         seed = torch.empty((nrhs, k), dtype=torch.uint8, device=dev)
         flag = torch.empty(1, dtype=torch.int32, device=dev)
-    _lib.call("nmfb_surface_nnls_batch", _ptr(C), _ptr(B), _ptr(BB), _ptr(W), int(warm_mode),
-              _ptr(T), int(max_changes), nrhs, k, _ptr(x), _ptr(p), _ptr(ch), _ptr(r2), _ptr(st),
-              _ptr(seed), _ptr(flag), _stream())
+    flen = int(_lib.load().nmfb_nnls_ftab_len(k)) if table else 0
+    if flen > 0:
+        ftab = torch.empty(flen, dtype=torch.float64, device=dev)
+        _lib.call("nmfb_nnls_batch_ws", _ptr(C), _ptr(B), _ptr(BB), _ptr(W), int(warm_mode),
+                  _ptr(T), int(max_changes), nrhs, k, _ptr(x), _ptr(p), _ptr(ch), _ptr(r2),
+                  _ptr(st), _ptr(seed), _ptr(flag), _ptr(ftab), flen, _stream())
+    else:
+        _lib.call("nmfb_surface_nnls_batch", _ptr(C), _ptr(B), _ptr(BB), _ptr(W),
+                  int(warm_mode), _ptr(T), int(max_changes), nrhs, k, _ptr(x), _ptr(p), _ptr(ch),
+                  _ptr(r2), _ptr(st), _ptr(seed), _ptr(flag), _stream())
     return a.out(x), a.out(p, "bool"), a.out(ch), a.out(r2), a.out(st)

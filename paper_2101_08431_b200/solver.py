@@ -104,6 +104,9 @@ class Problem:
                    _p(self.cwork), self.cwork.numel(), self.stream)
         self.comm.sum_(self.col_n2)
         self.mnorm2_local = float(self.row_n2.sum().item())  # ||M_rank||^2 (F-free objective)
+        # factor table of every passive subset for the NNLS batches (k <= 12)
+        self.ftab_len = int(L.nmfb_nnls_ftab_len(k)) if os.environ.get("NMFB_NNLS_TABLE", "1") != "0" else 0
+        self.ftab = torch.empty(max(self.ftab_len, 1), **f64) if self.ftab_len else None
         self.dscal = torch.zeros(256, **f64)
         self.iscal = torch.zeros(16, dtype=torch.int32, device=self.dev)
         self.hscal = torch.zeros(256, dtype=torch.float64).pin_memory()
@@ -285,15 +288,17 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
         P.rowprod(P.M, n, m, Yt, k, ctbX, tolX, P.f32)
         if tol_fixed is not None:
             tolX.fill_(float(tol_fixed))
-        P._call("nmfb_surface_nnls_batch", _p(GY), _p(ctbX), _p(P.row_n2), _p(pX), mode,
-                _p(tolX), 3 * k, n, k, _p(Xn), _p(pXn), _p(chX), _p(r2X), _p(stX), None, None, s)
+        P._call("nmfb_nnls_batch_ws", _p(GY), _p(ctbX), _p(P.row_n2), _p(pX), mode,
+                _p(tolX), 3 * k, n, k, _p(Xn), _p(pXn), _p(chX), _p(r2X), _p(stX), None, None,
+                _p(P.ftab), P.ftab_len, s)
         # Y-update: C = X, d = columns of M; row contractions all-reduced
         P.colprod(Xn, n, k, Xn, k, GX, reduce=True)
         P.colprod(P.M, n, m, Xn, k, ctbY, tolY, P.f32, reduce=True)
         if tol_fixed is not None:
             tolY.fill_(float(tol_fixed))
-        P._call("nmfb_surface_nnls_batch", _p(GX), _p(ctbY), _p(P.col_n2), _p(pY), mode,
-                _p(tolY), 3 * k, m, k, _p(Yn), _p(pYn), _p(chY), _p(r2Y), _p(stY), None, None, s)
+        P._call("nmfb_nnls_batch_ws", _p(GX), _p(ctbY), _p(P.col_n2), _p(pY), mode,
+                _p(tolY), 3 * k, m, k, _p(Yn), _p(pYn), _p(chY), _p(r2Y), _p(stY), None, None,
+                _p(P.ftab), P.ftab_len, s)
         ny = P.ny_local
         P._call("nmfb_stage1_stats", _p(X), _p(Xn), n * k, _p(Yt), _p(Yn), m * k * ny, _p(r2Y),
                 m * ny, _p(P.dscal), _p(P.rwork), P.rwork.numel(), s)

@@ -57,12 +57,16 @@ def test_schur_rhs_backsub(golden, K, shape, full):
     assert np.array_equal(K.back_substitute(x, y, l, h, dy, f, full), golden[f"{tag}_dx{full}"])
 
 
-def test_nnls_golden(golden, K):
+@pytest.mark.parametrize("table", (True, False))
+def test_nnls_golden(golden, K, table):
+    """Both device formulations against the reference's own outputs: the subset
+    factor table + register thread kernel (k <= 12) and the per-rhs factorizing
+    kernels of nmfb_surface_nnls_batch."""
     for c in range(int(golden["nnls_count"])):
         pre = f"nnls{c}_"
         k, mode, mc = (int(v) for v in golden[pre + "meta"])
         out = K.nnls_batch(golden[pre + "ctc"], golden[pre + "ctb"], golden[pre + "btb"],
-                           golden[pre + "seed"], mode, golden[pre + "tol"], mc)
+                           golden[pre + "seed"], mode, golden[pre + "tol"], mc, table=table)
         for name, v in zip(("x", "p", "ch", "r2", "st"), out):
             ref = golden[pre + name]
             assert v.shape == ref.shape and v.dtype == ref.dtype, (c, name)
@@ -77,19 +81,40 @@ def _nmf_like(rng, nrhs, k, drift):
     return ctc, ctb, np.einsum("ij,ij->i", D, D), 1e-12 * np.maximum(1, np.abs(ctb).max(1))
 
 
-@pytest.mark.parametrize("k,nrhs", [(3, 5000), (4, 5000), (10, 5000), (16, 5000), (4, 20000),
-                                     (10, 12000)])
+@pytest.mark.parametrize("k,nrhs", [(3, 5000), (4, 5000), (10, 5000), (12, 4000), (16, 5000),
+                                     (4, 20000), (10, 12000)])
 @pytest.mark.parametrize("mode", (0, 1, 2))
-def test_nnls_large_vs_oracle(K, k, nrhs, mode):
-    """Bit-identical to the reference on both device formulations: warp per rhs
-    (small batches) and thread per rhs (batches > 8192 or k > 12)."""
+@pytest.mark.parametrize("table", (True, False))
+def test_nnls_large_vs_oracle(K, k, nrhs, mode, table):
+    """Bit-identical to the reference on every device formulation: the subset
+    factor table + register thread kernel (k <= 12), warp per rhs (small batches)
+    and thread per rhs (batches > 8192 or k > 12)."""
     rng = np.random.default_rng(1000 + 10 * k + mode)
     ctc, ctb, btb, tol = _nmf_like(rng, nrhs, k, 0.05)
     seed = ok.nnls_batch(ctc, ctb * 1.01, btb, np.zeros((nrhs, k), bool), 0, tol, 3 * k)[1]
     ref = ok.nnls_batch(ctc, ctb, btb, seed, mode, tol, 3 * k)
-    out = K.nnls_batch(ctc, ctb, btb, seed, mode, tol, 3 * k)
+    out = K.nnls_batch(ctc, ctb, btb, seed, mode, tol, 3 * k, table=table)
     for name, a, b in zip(("x", "p", "ch", "r2", "st"), out, ref):
         assert np.array_equal(a, b), (name, k, mode)
+
+
+@pytest.mark.parametrize("k", (2, 5, 10))
+def test_nnls_table_cold_and_rank_deficient(K, k):
+    """Table path on cold starts with many Lawson-Hanson trips, the change cap
+    (status 1) and a rank-deficient Gram (status 2: failing subsets in the table)."""
+    rng = np.random.default_rng(77 + k)
+    nrhs = 3000
+    C = rng.uniform(0, 1, (3 * k + 4, k))
+    C[:, -1] = C[:, 0]  # duplicated column: every subset holding both is not PD
+    D = rng.standard_normal((nrhs, 3 * k + 4))
+    ctc, ctb = C.T @ C, D @ C
+    btb = np.einsum("ij,ij->i", D, D)
+    tol = 1e-12 * np.maximum(1, np.abs(ctb).max(1))
+    for mc in (3 * k, 2):
+        ref = ok.nnls_batch(ctc, ctb, btb, np.zeros((nrhs, k), bool), 0, tol, mc)
+        out = K.nnls_batch(ctc, ctb, btb, np.zeros((nrhs, k), bool), 0, tol, mc)
+        for name, a, b in zip(("x", "p", "ch", "r2", "st"), out, ref):
+            assert np.array_equal(a, b), (name, k, mc)
 
 
 def test_nnls_chain_many_switches(K):
