@@ -847,6 +847,13 @@ extern "C" int nmfb_colprod(const void* A, int a_is_f32, long rows, long cols, c
   cudaStream_t st = (cudaStream_t)stream;
   if (rows < 0 || cols < 0) return NMFB_EINVAL;
   if (cols == 0) return NMFB_OK;
+  // k x k Grams (X^T X, Y Y^T, X^T g, Y dY^T ...): one pass of the multi-Gram kernel
+  // (csrc/ipm.cu nmfb_grams, 64 rows per CTA + warp-per-entry finish) instead of the
+  // column-tiled split-K product, whose 64-column tiles run 2 of 32 lanes at cols = k
+  if (!a_is_f32 && cols == k && tol == nullptr && scale == 1.0 && rows > 0 &&
+      nmfb_grams_work_len(rows, k, 1) <= work_len)
+    return nmfb_grams(1, (const double*)A, B, out, nullptr, nullptr, nullptr, nullptr, nullptr,
+                      nullptr, nullptr, nullptr, nullptr, rows, k, work, work_len, stream);
 #define CASE(KK)                                                                                \
   case KK:                                                                                      \
     return a_is_f32 ? launch_colprod<KK, float>((const float*)A, rows, cols, B, out, tol, scale, \

@@ -157,15 +157,21 @@ __global__ void __launch_bounds__(256) k_syrk_trailing(double* __restrict__ A, l
 // the block is staged in shared memory with reciprocal pivots first, so the
 // column sweep is one shuffle + one FMA per step (no global loads or divides
 // on the dependency chain).  v (lane = row) holds b on entry, z on exit.
-__device__ __forceinline__ double trsv_diag_warp(const double* __restrict__ L, long N, long c0,
-                                                 int nc, int trans, double v, double* blk,
-                                                 double* rcp) {
-  const int lane = threadIdx.x & 31;
-  for (int e = lane; e < 32 * 32; e += 32) {
+__device__ __forceinline__ void trsv_load_blk(const double* __restrict__ L, long N, long c0,
+                                              int nc, double* blk, int t0, int nt) {
+  for (int e = t0; e < 32 * 32; e += nt) {
     const int r = e >> 5, c = e & 31;
     blk[r * 33 + c] = (r < nc && c < nc) ? L[(c0 + r) * N + c0 + c] : 0.0;
   }
-  __syncwarp();
+}
+
+// one warp solves the 32 x 32 diagonal block staged in blk (nc <= 32 active
+// columns) with reciprocal pivots, so the column sweep is one shuffle + one FMA per
+// step (no global loads or divides on the dependency chain).  v (lane = row) holds
+// b on entry, z on exit.
+__device__ __forceinline__ double trsv_diag_solve(int nc, int trans, double v, const double* blk,
+                                                  double* rcp) {
+  const int lane = threadIdx.x & 31;
   rcp[lane] = lane < nc ? 1.0 / blk[lane * 33 + lane] : 0.0;
   __syncwarp();
   const double rl = rcp[lane];
@@ -185,51 +191,100 @@ __device__ __forceinline__ double trsv_diag_warp(const double* __restrict__ L, l
   return v;
 }
 
+__device__ __forceinline__ double trsv_diag_warp(const double* __restrict__ L, long N, long c0,
+                                                 int nc, int trans, double v, double* blk,
+                                                 double* rcp) {
+  trsv_load_blk(L, N, c0, nc, blk, threadIdx.x & 31, 32);
+  __syncwarp();
+  return trsv_diag_solve(nc, trans, v, blk, rcp);
+}
+
 constexpr int TRSV_T = 256;  // 1024 threads spilled the 32-entry row to local memory
 
+// Single-CTA blocked solve.  Per 32-column block: warp 0 solves the diagonal block
+// (staged in shared memory one step ahead) while warps 1..7 load the next diagonal
+// block and the L entries of their update rows into registers -- neither depends on
+// the solution -- so after one barrier the update is 32 FMAs from registers.  The
+// L2 round trips overlap the serial diagonal sweep instead of following it.
+// The right-hand side lives in shared memory for the whole solve (dynamic, N doubles).
 __global__ void __launch_bounds__(TRSV_T) k_trsv_single(const double* __restrict__ L, long N,
-                                                      double* __restrict__ b, int trans) {
-  __shared__ double zb[32], sblk[32 * 33], srcp[32];
+                                                      double* __restrict__ bg, int trans) {
+  __shared__ double zb[32], sblk[2][32 * 33], srcp[32];
+  extern __shared__ double b[];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (long e = tid; e < N; e += TRSV_T) b[e] = bg[e];
   const long nblk = (N + 31) / 32;
+  constexpr int UT = TRSV_T - 32;  // update threads (warps 1..7)
+  {
+    const long blk0 = trans ? (nblk - 1) : 0;
+    trsv_load_blk(L, N, blk0 * 32, (int)min(32L, N - blk0 * 32), sblk[0], tid, TRSV_T);
+  }
+  __syncthreads();
   for (long bb = 0; bb < nblk; ++bb) {
     const long blk = trans ? (nblk - 1 - bb) : bb;
     const long c0 = blk * 32;
     const int nc = (int)min(32L, N - c0);
-    // 1) warp 0 solves the 32x32 diagonal block
+    const int cur = (int)(bb & 1);
+    double l[32];
+    long r_first = -1;  // the first update row (or column) of this thread, prefetched
     if (wid == 0) {
       double v = lane < nc ? b[c0 + lane] : 0.0;
-      v = trsv_diag_warp(L, N, c0, nc, trans, v, sblk, srcp);
+      v = trsv_diag_solve(nc, trans, v, sblk[cur], srcp);
       if (lane < nc) b[c0 + lane] = v;
       zb[lane] = lane < nc ? v : 0.0;
+    } else {
+      if (bb + 1 < nblk) {
+        const long nb = trans ? (blk - 1) : (blk + 1);
+        trsv_load_blk(L, N, nb * 32, (int)min(32L, N - nb * 32), sblk[cur ^ 1], tid - 32, UT);
+      }
+      if (!trans) {
+        const long r = c0 + nc + (tid - 32);
+        if (r < N) {
+          r_first = r;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) l[c] = c < nc ? L[r * N + c0 + c] : 0.0;
+        }
+      } else {
+        const long c = tid - 32;
+        if (c < c0) {
+          r_first = c;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) l[r] = r < nc ? L[(c0 + r) * N + c] : 0.0;
+        }
+      }
     }
     __syncthreads();
-    // 2) the remaining entries, one thread each: its 32 L values are loaded together
-    //    (all in flight), then one FMA chain
-    if (!trans) {
-      for (long r = c0 + nc + tid; r < N; r += blockDim.x) {
-        double l[32];
+    if (r_first >= 0) {
+      double s = 0.0;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) l[c] = c < nc ? L[r * N + c0 + c] : 0.0;
+      for (int c = 0; c < 32; ++c) s = fma(l[c], zb[c], s);
+      b[r_first] -= s;
+    }
+    // remaining update rows / columns (N > 256 + 32): all threads, loaded after the solve
+    if (!trans) {
+      for (long r = c0 + nc + UT + tid; r < N; r += TRSV_T) {
+        double lr[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) lr[c] = c < nc ? L[r * N + c0 + c] : 0.0;
         double s = 0.0;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) s = fma(l[c], zb[c], s);
+        for (int c = 0; c < 32; ++c) s = fma(lr[c], zb[c], s);
         b[r] -= s;
       }
     } else {
-      // b[c] -= sum_{r in blk} L[r, c] z[r] for c < c0 (coalesced across threads)
-      for (long c = tid; c < c0; c += blockDim.x) {
-        double l[32];
+      for (long c = UT + tid; c < c0; c += TRSV_T) {
+        double lr[32];
 #pragma unroll
-        for (int r = 0; r < 32; ++r) l[r] = r < nc ? L[(c0 + r) * N + c] : 0.0;
+        for (int r = 0; r < 32; ++r) lr[r] = r < nc ? L[(c0 + r) * N + c] : 0.0;
         double s = 0.0;
 #pragma unroll
-        for (int r = 0; r < 32; ++r) s = fma(l[r], zb[r], s);
+        for (int r = 0; r < 32; ++r) s = fma(lr[r], zb[r], s);
         b[c] -= s;
       }
     }
     __syncthreads();
   }
+  for (long e = tid; e < N; e += TRSV_T) bg[e] = b[e];
 }
 
 // multi-CTA pieces for large N
@@ -300,8 +355,15 @@ extern "C" int nmfb_dense_solve(const double* L, long N, double* b, void* stream
   cudaStream_t st = (cudaStream_t)stream;
   if (N <= 0) return NMFB_EINVAL;
   if (N <= 4096) {
-    ++g_nmfb_launches, k_trsv_single<<<1, TRSV_T, 0, st>>>(L, N, b, 0);
-    ++g_nmfb_launches, k_trsv_single<<<1, TRSV_T, 0, st>>>(L, N, b, 1);
+    const size_t sm = (size_t)N * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_trsv_single, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(4096 * sizeof(double)));
+      attr = true;
+    }
+    ++g_nmfb_launches, k_trsv_single<<<1, TRSV_T, sm, st>>>(L, N, b, 0);
+    ++g_nmfb_launches, k_trsv_single<<<1, TRSV_T, sm, st>>>(L, N, b, 1);
   } else {
     for (long c0 = 0; c0 < N; c0 += 32) {
       const int nc = (int)min(32L, N - c0);
