@@ -285,6 +285,9 @@ int nmfb_ipm_persist(const void *M, int m_is_f32, long n, long m, long k, double
 
 /* Up to four k x k Grams out_q = A_q^T B_q over the same rows (row-major fp64 inputs,
  * unused slots NULL); deterministic.  work >= nmfb_grams_work_len(rows, k, count). */
+/* creates the per-device cuBLAS handle used by nmfb_atb for large A^T B (plain
+ * DGEMM); call once outside CUDA-graph capture (later calls are capturable). */
+int nmfb_blas_init(void *stream);
 long nmfb_grams_work_len(long rows, long k, long count);
 int nmfb_grams(int count, const double *A0, const double *B0, double *O0, const double *A1,
                const double *B1, double *O1, const double *A2, const double *B2, double *O2,

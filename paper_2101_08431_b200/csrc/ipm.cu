@@ -15,6 +15,8 @@
 // identity gives r_acc_j = H y_j with H = sum_i x_i (L_i^{-T} h_i)^T and the
 // back-substitution q_i = L_i^{-1} (sum_j y_j dy_j^T) x_i.  The full-Hessian
 // extra terms use W = F^T P (m x k^3 GEMM) and a residual-weighted SYRK.
+#include <cublas_v2.h>
+
 #include "common.cuh"
 #include "nmfb200.h"
 
@@ -1022,6 +1024,38 @@ extern "C" long nmfb_atb_work_len(long rows, long ca, long cb) {
 }
 
 // out (ca x cb) = A^T B; A (rows x ca), B (rows x cb)
+// cuBLAS handle per device for the plain tall-skinny GEMMs A^T B of nmfb_atb (the
+// rank-k^2 capacitance Grams: n x k(k+1)/2 operands, K = n up to 200000).  Created
+// outside graph capture with a fixed workspace so later calls are capturable.
+static cublasHandle_t atb_handle(cudaStream_t st) {
+  static cublasHandle_t h[64] = {};
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= 64) return nullptr;
+  if (!h[d]) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    cublasHandle_t hh;
+    if (cublasCreate(&hh) != CUBLAS_STATUS_SUCCESS) return nullptr;
+    void* ws = nullptr;
+    const size_t wsb = 32u << 20;
+    if (cudaMalloc(&ws, wsb) != cudaSuccess) {
+      cublasDestroy(hh);
+      return nullptr;
+    }
+    cublasSetWorkspace(hh, ws, wsb);
+    cublasSetAtomicsMode(hh, CUBLAS_ATOMICS_NOT_ALLOWED);  // deterministic
+    h[d] = hh;
+  }
+  return h[d];
+}
+
+// creates the cuBLAS handle of the current device (call outside graph capture)
+extern "C" int nmfb_blas_init(void* stream) {
+  return atb_handle((cudaStream_t)stream) != nullptr ? NMFB_OK : NMFB_ELAUNCH;
+}
+
 extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, long cb,
                         double* out, double* work, long work_len, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -1029,6 +1063,21 @@ extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, lo
   if (rows <= 0) {
     cudaMemsetAsync(out, 0, sizeof(double) * ca * cb, st);
     return NMFB_OK;
+  }
+  // large products: cuBLAS DGEMM on the FP64 tensor cores.  Row-major out = A^T B is
+  // column-major out^T = B_c A_c^T with A_c = A^T (ca x rows), B_c (cb x rows).
+  if (2.0 * (double)rows * (double)ca * (double)cb >= 5e7 && rows <= 0x7fffffffL) {
+    cublasHandle_t h = atb_handle(st);
+    if (h != nullptr) {
+      cublasSetStream(h, st);
+      const double one = 1.0, zero = 0.0;
+      if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)cb, (int)ca, (int)rows, &one, B, (int)cb,
+                      A, (int)ca, &zero, out, (int)cb) == CUBLAS_STATUS_SUCCESS) {
+        ++g_nmfb_launches;
+        NMFB_CHECK_LAUNCH();
+        return NMFB_OK;
+      }
+    }
   }
   const long tiles = ((ca + 31) / 32) * ((cb + 31) / 32);
   long ns = (148 * 4 + tiles - 1) / tiles;

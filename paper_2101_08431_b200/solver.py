@@ -104,6 +104,7 @@ class Problem:
                    _p(self.cwork), self.cwork.numel(), self.stream)
         self.comm.sum_(self.col_n2)
         self.mnorm2_local = float(self.row_n2.sum().item())  # ||M_rank||^2 (F-free objective)
+        self._call("nmfb_blas_init", self.stream)  # cuBLAS handle, outside any graph capture
         # factor table of every passive subset for the NNLS batches (k <= 12)
         self.ftab_len = int(L.nmfb_nnls_ftab_len(k)) if os.environ.get("NMFB_NNLS_TABLE", "1") != "0" else 0
         self.ftab = torch.empty(max(self.ftab_len, 1), **f64) if self.ftab_len else None
