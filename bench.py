@@ -324,8 +324,9 @@ def run_b200(args):
                      "algorithmic_bytes": nbytes, "peak_source": peak_src,
                      "traffic_source": ncu["source"] if ncu else None,
                      "note": "latency-bound: c2's M (2.4 MB) is held in shared memory for the "
-                             "whole launch, each iteration is a chain of 4 grid barriers and "
-                             "k^2-sized serial solves; aux reports the HBM-bound c4 products"},
+                             "whole launch, each iteration is a chain of 3 grid barriers (a 4th "
+                             "only when Armijo backtracks past 7 halvings) and k^2-sized serial "
+                             "solves; aux reports the HBM-bound c4 products"},
         "fp64_dgemm_tflops_measured": fp64_peak,
         "gpu_launches": int(launches),
         "clocks": clk,
