@@ -63,6 +63,22 @@ def test_stage1_parity(mods, name, n, m, persistent):
     assert abs(r.trace[-1][1] - ro.trace[-1][1]) <= TOL_STAGE1 * ro.trace[-1][1]
 
 
+def test_stage1_parity_c4_full(mods):
+    """Config c4 at full size (20000 x 5000, k = 10): 6 sweeps through the subset
+    factor-table NNLS, bit-identical passive sets to the oracle, factors within 1e-10."""
+    data, solver, IpmParams, Stage1Config = mods
+    cfg = data.CONFIGS["c4"]
+    M, X0, Y0, _, _ = data.make(cfg)
+    P = solver.Problem(M, cfg.k)
+    X, Yt, pX, pY, r = solver.run_stage1(P, P.to_dev(X0), P.to_dev(Y0.T),
+                                         Stage1Config(fixed_sweeps=6))
+    ro = D.run_stage1(M, X0, Y0.T.copy(), D.Stage1Config(fixed_sweeps=6))
+    assert np.array_equal(pX.bool().cpu().numpy(), ro.pX)
+    assert np.array_equal(pY.bool().cpu().numpy(), ro.pY)
+    assert rel(X.cpu().numpy(), ro.X) < TOL_STAGE1
+    assert rel(Yt.cpu().numpy(), ro.Yt) < TOL_STAGE1
+
+
 def test_stage1_fp32_storage(mods):
     """c5-style fp32 M (fp64 accumulate/solve) vs the fp64 oracle on the rounded M: 1e-4."""
     data, solver, IpmParams, Stage1Config = mods
