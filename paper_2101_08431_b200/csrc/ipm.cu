@@ -84,46 +84,58 @@ __global__ void __launch_bounds__(256) k_residual_rows(const T* __restrict__ M, 
 // ---------------------------------------------------------------------------
 // per-row small linear algebra (thread per row i)
 // ---------------------------------------------------------------------------
+// Reciprocal pivots: rd[j] = 1 / L[j][j] from one rsqrt per column, so the column
+// scalings and the triangular solves multiply instead of dividing (K(K+1)/2 + 2K
+// IEEE division sequences per row taken off the dependency chains).
 template <int K>
-__device__ __forceinline__ bool chol_row(double (&L)[K][K]) {
+__device__ __forceinline__ bool chol_row(double (&L)[K][K], double (&rd)[K]) {
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     double s = L[j][j];
 #pragma unroll
     for (int p = 0; p < j; ++p) s -= L[j][p] * L[j][p];
     if (!(s > 0.0)) return false;
-    const double d = sqrt(s);
-    L[j][j] = d;
+    const double di = rsqrt(s);
+    L[j][j] = s * di;
+    rd[j] = di;
 #pragma unroll
     for (int i = j + 1; i < K; ++i) {
       double t = L[i][j];
 #pragma unroll
       for (int p = 0; p < j; ++p) t -= L[i][p] * L[j][p];
-      L[i][j] = t / d;
+      L[i][j] = t * di;
     }
   }
   return true;
 }
 
 template <int K>
-__device__ __forceinline__ void fwd_row(const double (&L)[K][K], const double* b, double* z) {
+__device__ __forceinline__ void recip_diag(const double (&L)[K][K], double (&rd)[K]) {
+#pragma unroll
+  for (int i = 0; i < K; ++i) rd[i] = 1.0 / L[i][i];
+}
+
+template <int K>
+__device__ __forceinline__ void fwd_row(const double (&L)[K][K], const double (&rd)[K],
+                                        const double* b, double* z) {
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     double s = b[i];
 #pragma unroll
     for (int p = 0; p < i; ++p) s -= L[i][p] * z[p];
-    z[i] = s / L[i][i];
+    z[i] = s * rd[i];
   }
 }
 
 template <int K>
-__device__ __forceinline__ void bwd_row(const double (&L)[K][K], const double* b, double* z) {
+__device__ __forceinline__ void bwd_row(const double (&L)[K][K], const double (&rd)[K],
+                                        const double* b, double* z) {
 #pragma unroll
   for (int i = K - 1; i >= 0; --i) {
     double s = b[i];
 #pragma unroll
     for (int p = i + 1; p < K; ++p) s -= L[p][i] * z[p];
-    z[i] = s / L[i][i];
+    z[i] = s * rd[i];
   }
 }
 
@@ -153,15 +165,17 @@ __global__ void __launch_bounds__(128) k_r1_factor(const double* __restrict__ GY
     for (int c = 0; c < K; ++c) L[a][c] = (c <= a) ? gy[a * K + c] : 0.0;
 #pragma unroll
   for (int p = 0; p < K; ++p) {
-    L[p][p] += rho + R[i * K + p] / x[p];
-    b[p] = mux / x[p] - gX[i * K + p];
+    const double ix = 1.0 / x[p];
+    L[p][p] += rho + R[i * K + p] * ix;
+    b[p] = mux * ix - gX[i * K + p];
   }
-  if (!chol_row<K>(L)) {
+  double rd[K];
+  if (!chol_row<K>(L, rd)) {
     atomicMin(bad, (int)i);
     return;
   }
-  fwd_row<K>(L, b, hv);
-  bwd_row<K>(L, hv, gv);
+  fwd_row<K>(L, rd, b, hv);
+  bwd_row<K>(L, rd, hv, gv);
 #pragma unroll
   for (int a = 0; a < K; ++a) {
     h[i * K + a] = hv[a];
@@ -182,7 +196,7 @@ __global__ void __launch_bounds__(128) k_r1_factor(const double* __restrict__ GY
 #pragma unroll
         for (int p = 0; p < a; ++p)
           if (p >= c) s -= L[a][p] * Li[p][c];
-        Li[a][c] = s / L[a][a];
+        Li[a][c] = s * rd[a];
       }
     }
   }
@@ -215,8 +229,10 @@ __global__ void k_hg_rows(const double* __restrict__ Lin, const double* __restri
 #pragma unroll
     for (int c = 0; c < K; ++c) L[a][c] = Lin[(i * K + a) * K + c];
   }
-  fwd_row<K>(L, b, hv);
-  bwd_row<K>(L, hv, gv);
+  double rd[K];
+  recip_diag<K>(L, rd);
+  fwd_row<K>(L, rd, b, hv);
+  bwd_row<K>(L, rd, hv, gv);
 #pragma unroll
   for (int a = 0; a < K; ++a) {
     h[i * K + a] = hv[a];
@@ -491,10 +507,12 @@ __global__ void __launch_bounds__(128) k_dir_rows(const double* __restrict__ Lin
       for (int b = 0; b < K; ++b) s = fma(gd[a * K + b], Xf[i * K + b], s);
       v[a] = s;
     }
-    fwd_row<K>(L, v, q);
+    double rd[K];
+    recip_diag<K>(L, rd);
+    fwd_row<K>(L, rd, v, q);
 #pragma unroll
     for (int a = 0; a < K; ++a) t[a] = h[i * K + a] - q[a];
-    bwd_row<K>(L, t, dx);
+    bwd_row<K>(L, rd, t, dx);
 #pragma unroll
     for (int a = 0; a < K; ++a) {
       const double x = X[i * K + a], r = R[i * K + a];
@@ -1066,7 +1084,7 @@ extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, lo
   }
   // large products: cuBLAS DGEMM on the FP64 tensor cores.  Row-major out = A^T B is
   // column-major out^T = B_c A_c^T with A_c = A^T (ca x rows), B_c (cb x rows).
-  if (2.0 * (double)rows * (double)ca * (double)cb >= 5e7 && rows <= 0x7fffffffL) {
+  if (2.0 * (double)rows * (double)ca * (double)cb >= 1e7 && rows <= 0x7fffffffL) {
     cublasHandle_t h = atb_handle(st);
     if (h != nullptr) {
       cublasSetStream(h, st);

@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(128) k_d_factor(const double* __restrict__ XtX
 #pragma unroll
     for (int c = 0; c < K; ++c) L[a][c] = (c <= a) ? xx[a * K + c] : 0.0;
 #pragma unroll
-  for (int p = 0; p < K; ++p) L[p][p] += rho + S[j * K + p] / y[p];
+  for (int p = 0; p < K; ++p) L[p][p] += rho + S[j * K + p] * (1.0 / y[p]);
+  double rd[K];  // reciprocal pivots (one rsqrt per column; multiplies below)
 #pragma unroll
   for (int c = 0; c < K; ++c) {
     double s = L[c][c];
@@ -60,14 +61,15 @@ __global__ void __launch_bounds__(128) k_d_factor(const double* __restrict__ XtX
       atomicMin(bad, (int)j);
       return;
     }
-    const double d = sqrt(s);
-    L[c][c] = d;
+    const double di = rsqrt(s);
+    L[c][c] = s * di;
+    rd[c] = di;
 #pragma unroll
     for (int i = c + 1; i < K; ++i) {
       double t = L[i][c];
 #pragma unroll
       for (int p = 0; p < c; ++p) t -= L[i][p] * L[c][p];
-      L[i][c] = t / d;
+      L[i][c] = t * di;
     }
   }
 #pragma unroll
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(128) k_d_factor(const double* __restrict__ XtX
 #pragma unroll
         for (int p = 0; p < a; ++p)
           if (p >= c) s -= L[a][p] * Li[p][c];
-        Li[a][c] = s / L[a][a];
+        Li[a][c] = s * rd[a];
       }
     }
   constexpr int KK = K * (K + 1) / 2;
@@ -117,19 +119,22 @@ __global__ void k_d_solve(const double* __restrict__ LD, const double* __restric
 #pragma unroll
     for (int c = 0; c < K; ++c) L[a][c] = LD[(j * K + a) * K + c];
   }
+  double rd[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) rd[i] = 1.0 / L[i][i];  // independent: off the solve chains
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     double s = v[i];
 #pragma unroll
     for (int p = 0; p < i; ++p) s -= L[i][p] * z[p];
-    z[i] = s / L[i][i];
+    z[i] = s * rd[i];
   }
 #pragma unroll
   for (int i = K - 1; i >= 0; --i) {
     double s = z[i];
 #pragma unroll
     for (int p = i + 1; p < K; ++p) s -= L[p][i] * v[p];
-    v[i] = s / L[i][i];
+    v[i] = s * rd[i];
   }
 #pragma unroll
   for (int a = 0; a < K; ++a) t[j * K + a] = v[a];
@@ -153,19 +158,22 @@ __global__ void k_d_correct(const double* __restrict__ LD, const double* __restr
 #pragma unroll
     for (int c = 0; c < K; ++c) L[p][c] = LD[(j * K + p) * K + c];
   }
+  double rd[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) rd[i] = 1.0 / L[i][i];  // independent: off the solve chains
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     double s = v[i];
 #pragma unroll
     for (int p = 0; p < i; ++p) s -= L[i][p] * z[p];
-    z[i] = s / L[i][i];
+    z[i] = s * rd[i];
   }
 #pragma unroll
   for (int i = K - 1; i >= 0; --i) {
     double s = z[i];
 #pragma unroll
     for (int p = i + 1; p < K; ++p) s -= L[p][i] * v[p];
-    v[i] = s / L[i][i];
+    v[i] = s * rd[i];
   }
 #pragma unroll
   for (int a = 0; a < K; ++a) t[j * K + a] += v[a];

@@ -438,6 +438,16 @@ class IpmEngine:
                  P.lib.nmfb_atb_work_len(m, self.kk, self.kk),
                  0 if self.ffree else P.lib.nmfb_atb_work_len(n, m, k ** 3), 1)
         self.awork = b(aw)
+        if self.use_graphs:
+            # the capacitance Grams' first cuBLAS calls (library init, kernel load) run
+            # eagerly here, not inside the first graph capture (~0.4 s there at c4);
+            # the outputs are recomputed by every direction
+            self.Apk.zero_()
+            self.YYpk.zero_()
+            for A_, rows_, B_, O_ in ((self.Apk, n, self.XXpk, self.Z),
+                                      (self.YYpk, m, self.Dinvpk, self.Gpk)):
+                P._call("nmfb_atb", _p(A_), rows_, self.kk, _p(A_), self.kk, _p(O_),
+                        _p(self.awork), self.awork.numel(), P.stream)
 
     # -- helpers -------------------------------------------------------------
     @property
