@@ -186,6 +186,15 @@ int nmfb_barrier_trials(const double *X, const double *dX, long nx, const double
  * coefficients, barrier sums) and writes alpha1, t, alpha2 (graph-capturable). */
 int nmfb_armijo_select(double *sc, double mu, double wx, double wy, double eta,
                        int max_backtracks, const int *fcodes, void *stream);
+/* nmfb_barrier_trials + nmfb_armijo_select with lazy trial batches: trials 0..7, a
+ * device pre-check, the remaining trials only when it did not decide (their launches
+ * return at once otherwise), then the full search -- the same accepted t.  Uses
+ * sc[31] as the decided flag; graph-capturable; single rank (the X-side trial sums
+ * are not all-reduced). */
+int nmfb_armijo_lazy(const double *X, const double *dX, long nx, const double *Yt,
+                     const double *dYt, long ny, double *sc, int ntrials, double mu, double wx,
+                     double wy, double eta, int max_backtracks, const int *fcodes, double *work,
+                     long work_len, void *stream);
 /* as nmfb_step_nudge with alpha read from device memory */
 int nmfb_step_nudge_dev(double *v, const double *dv, long len, const double *alpha, double tau,
                         void *stream);

@@ -54,6 +54,7 @@ SIGNATURES = {
     "nmfb_barrier_trials": [P, P, L, P, P, L, P, I, P, P, L, P],
     "nmfb_step_nudge": [P, P, L, D, D, P],
     "nmfb_armijo_select": [P, D, D, D, D, I, P, P],
+    "nmfb_armijo_lazy": [P, P, L, P, P, L, P, I, D, D, D, D, I, P, P, L, P],
     "nmfb_step_nudge_dev": [P, P, L, P, D, P],
     "nmfb_kkt_sums": [P, P, P, L, P, P, P, L, D, D, P, P, P],
     "nmfb_affine_mu": [P, P, P, P, L, P, P, P, P, L, D, D, P, P, P],

@@ -667,9 +667,12 @@ __global__ void __launch_bounds__(256) k_barrier_trials(const double* __restrict
                                                         const double* __restrict__ Yt,
                                                         const double* __restrict__ dYt, long ny,
                                                         const double* __restrict__ alpha_max,
-                                                        int ntrials, double* __restrict__ part) {
+                                                        int ntrials, double* __restrict__ part,
+                                                        int t0 = 0,
+                                                        const double* __restrict__ skip = nullptr) {
   __shared__ double sh[32];
-  const int t = blockIdx.y;
+  if (skip != nullptr && *skip != 0.0) return;  // Armijo already decided (lazy batches)
+  const int t = t0 + blockIdx.y;
   if (t >= ntrials) return;
   const double alpha = ldexp(*alpha_max, -t);
   double sx = 0.0, sy = 0.0;
@@ -688,11 +691,13 @@ __global__ void __launch_bounds__(256) k_barrier_trials(const double* __restrict
 
 // out[t*2 + c] = sum_b part[t][b][c]  (one warp per (t, c), fixed order)
 __global__ void k_finish_trials(const double* __restrict__ part, int nb, int nt,
-                                double* __restrict__ out) {
+                                double* __restrict__ out, int t0 = 0,
+                                const double* __restrict__ skip = nullptr) {
+  if (skip != nullptr && *skip != 0.0) return;
   const int lane = threadIdx.x & 31;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= 2 * nt) return;
-  const int t = w >> 1, c = w & 1;
+  const int t = t0 + (w >> 1), c = w & 1;
+  if (t >= nt) return;
   double v = 0.0;
   for (int b = lane; b < nb; b += 32) v += part[((long)t * nb + b) * 2 + c];
   v = warp_sum(v);
@@ -849,9 +854,14 @@ __global__ void k_fill(double* __restrict__ v, long len, double c) {
 // solver.run_ipm): first t with dphi(a1max 2^-t) <= eta a 2^-t gtp.
 // sc layout: [4] gtp, [5] a1max, [6] a2max, [10..15] quartic, [32 + 2t (+1)] barrier sums.
 // Writes sc[1] = alpha1 (0 when stalled), sc[2] = t (max_bt + 1 when stalled), sc[3] = alpha2.
+// t_lim < 0: full search (t = 0 .. max_bt).  t_lim >= 0 (lazy pre-check): search
+// t < t_lim only and record in sc[31] whether that decided (1) or the remaining
+// trials are needed (0).  With sc[31] == 1 on entry to a full search, nothing to do.
 __global__ void k_armijo_select(double* __restrict__ sc, double mu, double wx, double wy,
-                                double eta, int max_bt, const int* __restrict__ fcodes) {
+                                double eta, int max_bt, const int* __restrict__ fcodes,
+                                int t_lim = -1, int honor_decided = 0) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (honor_decided && sc[31] != 0.0) return;
   // fcodes = [R1 failing row, reduced-system info, D failing column]: on any
   // factorization failure take no step (t = -2) so the host can redo the
   // direction with the dense Schur solve
@@ -859,6 +869,7 @@ __global__ void k_armijo_select(double* __restrict__ sc, double mu, double wx, d
     sc[1] = 0.0;
     sc[2] = -2.0;
     sc[3] = 0.0;
+    if (t_lim >= 0) sc[31] = 1.0;
     return;
   }
   const double gtp = sc[4], a1max = sc[5];
@@ -878,11 +889,16 @@ __global__ void k_armijo_select(double* __restrict__ sc, double mu, double wx, d
     const double dphi = __dsub_rn(quad, __dmul_rn(mu, bar));
     if (dphi <= __dmul_rn(__dmul_rn(eta, a1), gtp)) break;
     ++t;
+    if (t_lim >= 0 && t >= t_lim && t <= max_bt) {  // undecided within the first batch
+      sc[31] = 0.0;
+      return;
+    }
     if (t > max_bt) {
       a1 = 0.0;
       break;
     }
   }
+  if (t_lim >= 0) sc[31] = 1.0;
   sc[1] = a1;
   sc[2] = (double)t;
   sc[3] = (t > max_bt) ? 0.0 : sc[6];
@@ -1313,6 +1329,40 @@ extern "C" int nmfb_fill(double* v, long len, double c, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (len <= 0) return NMFB_OK;
   ++g_nmfb_launches, k_fill<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(v, len, c);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// Barrier trials + Armijo selection with lazy trial batches (graph-capturable): trials
+// 0..7 first, a device pre-check of those, then trials 8.. only when it did not
+// decide (the later launches return at once otherwise) and the full search.  The
+// accepted t is the full search's: the pre-check runs the same arithmetic on the
+// same sums, and the barrier sums of a trial do not depend on the batching.
+extern "C" int nmfb_armijo_lazy(const double* X, const double* dX, long nx, const double* Yt,
+                                const double* dYt, long ny, double* sc, int ntrials, double mu,
+                                double wx, double wy, double eta, int max_backtracks,
+                                const int* fcodes, double* work, long work_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = 64, TB = 8;
+  if (ntrials < 1 || work_len < 2L * nb * ntrials) return NMFB_ENOMEM;
+  const double* alpha_max = sc + 5;
+  double* bars = sc + 32;
+  const int tb = ntrials < TB ? ntrials : TB;
+  ++g_nmfb_launches, k_barrier_trials<<<dim3(nb, tb), 256, 0, st>>>(X, dX, nx, Yt, dYt, ny,
+                                                                    alpha_max, ntrials, work, 0, nullptr);
+  ++g_nmfb_launches, k_finish_trials<<<(2 * tb * 32 + 255) / 256, 256, 0, st>>>(work, nb, tb, bars,
+                                                                             0, nullptr);
+  ++g_nmfb_launches, k_armijo_select<<<1, 32, 0, st>>>(sc, mu, wx, wy, eta, max_backtracks, fcodes,
+                                                       tb, 0);
+  if (ntrials > tb) {
+    const int rest = ntrials - tb;
+    ++g_nmfb_launches, k_barrier_trials<<<dim3(nb, rest), 256, 0, st>>>(
+        X, dX, nx, Yt, dYt, ny, alpha_max, ntrials, work, tb, sc + 31);
+    ++g_nmfb_launches, k_finish_trials<<<(2 * rest * 32 + 255) / 256, 256, 0, st>>>(
+        work, nb, ntrials, bars, tb, sc + 31);
+  }
+  ++g_nmfb_launches, k_armijo_select<<<1, 32, 0, st>>>(sc, mu, wx, wy, eta, max_backtracks, fcodes,
+                                                       -1, 1);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

@@ -501,10 +501,16 @@ class IpmEngine:
             self.fi ^= 1
             return
         dY = self.direction(False)
-        self.armijo_launch(dY)
         s = P.stream
-        P._call("nmfb_armijo_select", _p(P.dscal), self.mu, self.wx, self.wy, p.eta,
-                p.max_backtracks, _p(P.iscal[2:]), s)
+        if self.comm.active:
+            self.armijo_launch(dY)
+            P._call("nmfb_armijo_select", _p(P.dscal), self.mu, self.wx, self.wy, p.eta,
+                    p.max_backtracks, _p(P.iscal[2:]), s)
+        else:  # quartic, then barrier trials in lazy batches + the device selection
+            self.armijo_launch(dY, trials=False)
+            P._call("nmfb_armijo_lazy", _p(self.X), _p(self.dX), n * k, _p(self.Yt), _p(dY), m * k,
+                    _p(P.dscal), NTRIALS, self.mu, self.wx, self.wy, p.eta, p.max_backtracks,
+                    _p(P.iscal[2:]), _p(P.rwork), P.rwork.numel(), s)
         self.remember_factorization(False)  # the factorization's X, Y (before the step)
         a1p, a2p = P.dscal[1:2], P.dscal[3:4]
         P._call("nmfb_step_nudge_dev", _p(self.X), _p(self.dX), n * k, _p(a1p), p.tau, s)
@@ -711,15 +717,18 @@ class IpmEngine:
         self.comm.min_(d[5:7])
         d[4:5].copy_(d[7:8] + d[8:9])
 
-    def armijo_launch(self, dY):
-        """Quartic coefficients + all backtracking barrier sums in two launches."""
+    def armijo_launch(self, dY, trials=True):
+        """Quartic coefficients + all backtracking barrier sums in two launches
+        (trials=False: quartic only; the caller runs nmfb_armijo_lazy)."""
         P, s = self.P, self.P.stream
         n, m, k = self.n, self.m, self.k
         if self.ffree:
-            self._armijo_free(dY)
+            self._armijo_free(dY, trials)
             return
         P._call("nmfb_quartic", _p(self.Fcur), n, m, k, _p(self.X), _p(self.dX), _p(self.Yt),
                 _p(dY), _p(P.dscal[10:]), _p(P.rwork), s)
+        if not trials:
+            return
         P._call("nmfb_barrier_trials", _p(self.X), _p(self.dX), n * k, _p(self.Yt), _p(dY), m * k,
                 _p(P.dscal[5:]), NTRIALS, _p(P.dscal[32:]), _p(P.rwork), P.rwork.numel(), s)
         if self.comm.active:
@@ -728,7 +737,7 @@ class IpmEngine:
             self.comm.sum_(bx)
             P.dscal[32:32 + 2 * NTRIALS].view(NTRIALS, 2)[:, 0].copy_(bx)
 
-    def _armijo_free(self, dY):
+    def _armijo_free(self, dY, trials=True):
         """Quartic coefficients from k x k Grams + one streaming pass M dY^T."""
         P, s = self.P, self.P.stream
         n, m, k = self.n, self.m, self.k
@@ -740,6 +749,8 @@ class IpmEngine:
         P._call("nmfb_ffree_quartic", _p(self.A1), _p(self.A2), _p(self.XtX), _p(self.B1),
                 _p(self.B2), _p(self.GY), _p(self.Dgx), _p(self.Dgy), _p(self.Dmd), k,
                 _p(P.dscal), s)
+        if not trials:
+            return
         P._call("nmfb_barrier_trials", _p(X), _p(dX), n * k, _p(Yt), _p(dY), m * k,
                 _p(P.dscal[5:]), NTRIALS, _p(P.dscal[32:]), _p(P.rwork), P.rwork.numel(), s)
         if self.comm.active:
