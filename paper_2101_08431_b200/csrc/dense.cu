@@ -12,6 +12,8 @@
 // SchurNotPositiveDefinite.  No pivoting, no silent regularisation.
 // Triangular solves: a single-CTA blocked solver for small N, multi-CTA
 // (diagonal solve + GEMV sweep) for large N.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "nmfb200.h"
 #include "chol_blk.cuh"
@@ -287,6 +289,80 @@ __global__ void __launch_bounds__(TRSV_T) k_trsv_single(const double* __restrict
   for (long e = tid; e < N; e += TRSV_T) bg[e] = b[e];
 }
 
+// Cooperative solve for large N (mk up to 4096; c3's dense Schur fallbacks): ONE grid
+// barrier per 32-column block.  Round b: CTA 0 applies z_b to block b+1's rows and
+// solves block b+1's diagonal (a ~2 us chain) while CTAs 1..G-1 apply z_b to every
+// row beyond block b+1 (all of L streams through the SMs once per solve); the
+// transposed solve runs the same schedule on columns from the end.  The right-hand
+// side stays in global memory (L2), read with ld.global.cg after each barrier.
+__global__ void __launch_bounds__(256) k_trsv_coop(const double* __restrict__ L, long N,
+                                                   double* __restrict__ b, int trans) {
+  __shared__ double sblk[32 * 33], srcp[32], zs[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const long nblk = (N + 31) / 32;
+  auto blk_of = [&](long bb) { return trans ? (nblk - 1 - bb) : bb; };
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  if (cta == 0 && wid == 0) {  // block 0 (forward) / the last block (transposed)
+    const long c0 = blk_of(0) * 32;
+    const int nc = (int)min(32L, N - c0);
+    double v = lane < nc ? b[c0 + lane] : 0.0;
+    v = trsv_diag_warp(L, N, c0, nc, trans, v, sblk, srcp);
+    if (lane < nc) b[c0 + lane] = v;
+  }
+  grid.sync();
+  for (long bb = 0; bb + 1 < nblk; ++bb) {
+    const long p0 = blk_of(bb) * 32;  // solved block
+    const int np = (int)min(32L, N - p0);
+    const long n0 = blk_of(bb + 1) * 32;  // next block
+    const int nn = (int)min(32L, N - n0);
+    if (tid < 32) zs[tid] = tid < np ? __ldcg(b + p0 + tid) : 0.0;
+    __syncthreads();
+    if (cta == 0) {
+      if (wid == 0) {
+        double v = lane < nn ? __ldcg(b + n0 + lane) : 0.0;
+        double s = 0.0;
+        if (lane < nn) {
+          if (!trans) {
+#pragma unroll 8
+            for (int c = 0; c < np; ++c) s = fma(L[(n0 + lane) * N + p0 + c], zs[c], s);
+          } else {
+#pragma unroll 8
+            for (int r = 0; r < np; ++r) s = fma(L[(p0 + r) * N + n0 + lane], zs[r], s);
+          }
+        }
+        v -= s;
+        v = trsv_diag_warp(L, N, n0, nn, trans, v, sblk, srcp);
+        if (lane < nn) b[n0 + lane] = v;
+      }
+    } else {
+      const long gt = (long)(cta - 1) * 256 + tid, gn = (long)(G - 1) * 256;
+      if (!trans) {
+        for (long r = n0 + nn + gt; r < N; r += gn) {
+          double l[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) l[c] = c < np ? L[r * N + p0 + c] : 0.0;
+          double s = 0.0;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) s = fma(l[c], zs[c], s);
+          b[r] = __ldcg(b + r) - s;
+        }
+      } else {
+        for (long c = gt; c < n0; c += gn) {
+          double l[32];
+#pragma unroll
+          for (int r = 0; r < 32; ++r) l[r] = r < np ? L[(p0 + r) * N + c] : 0.0;
+          double s = 0.0;
+#pragma unroll
+          for (int r = 0; r < 32; ++r) s = fma(l[r], zs[r], s);
+          b[c] = __ldcg(b + c) - s;
+        }
+      }
+    }
+    grid.sync();
+  }
+}
+
 // multi-CTA pieces for large N
 __global__ void k_trsv_diag(const double* __restrict__ L, long N, double* __restrict__ b, long c0,
                             int nc, int trans) {
@@ -354,6 +430,20 @@ extern "C" int nmfb_dense_cholesky(double* A, long N, int* info, void* stream) {
 extern "C" int nmfb_dense_solve(const double* L, long N, double* b, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (N <= 0) return NMFB_EINVAL;
+  if (N > 640 && N <= 65536) {  // cooperative: one grid barrier per block
+    int G = (int)((N - 32 + 255) / 256) + 1;
+    if (G > 148) G = 148;
+    if (G < 2) G = 2;
+    for (int trans = 0; trans < 2; ++trans) {
+      void* args[] = {(void*)&L, &N, &b, &trans};
+      ++g_nmfb_launches;
+      if (cudaLaunchCooperativeKernel((const void*)k_trsv_coop, dim3(G), dim3(256), args, 0, st) !=
+          cudaSuccess)
+        return NMFB_ELAUNCH;
+    }
+    NMFB_CHECK_LAUNCH();
+    return NMFB_OK;
+  }
   if (N <= 4096) {
     const size_t sm = (size_t)N * sizeof(double);
     static bool attr = false;
