@@ -15,6 +15,9 @@ from paper_2101_08431_b200.config import IpmParams, Stage1Config  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 cfg = data.CONFIGS[name]
 M, X0, Y0, _, _ = data.make(cfg)
+if len(sys.argv) > 2:  # column prefix (c3 chunk sizes)
+    mm = int(sys.argv[2])
+    M, Y0 = M[:, :mm], Y0[:, :mm]
 P = solver.Problem(M, cfg.k)
 X0d, Yt0d = P.to_dev(X0), P.to_dev(Y0.T)
 e_scale = max(1.0, solver.kkt_error_primal_only_dev(P, X0d, Yt0d)[0])
@@ -64,6 +67,6 @@ for rep in range(3):
     t3 = time.perf_counter()
 print(f"total {1e3 * (t3 - t0):.3f} ms: stage1 {1e3 * (t1 - t0):.3f} transition {1e3 * (t2 - t1):.3f} "
       f"ipm {1e3 * (t3 - t2):.3f} (iters {r2.iters}, outer {r2.outer}, fullH {sum(r2.flags)}, "
-      f"dense fallbacks {r2.dense_fallbacks})")
+      f"dense fallbacks {r2.dense_fallbacks}, persist iters {P.persist_iters})")
 for k_, v in sorted(acc.items(), key=lambda x: -x[1]):
     print(f"  {k_:24s} {cnt[k_]:4d} calls {1e3 * v:9.3f} ms")
