@@ -313,6 +313,8 @@ int nmfb_grams(int count, const double *A0, const double *B0, double *O0, const 
  * exactly max_sweeps.  logv: per sweep [0.5 sum r2, step, norm, -]; status (device
  * int[3]) = [sweeps, converged, failed]. */
 int nmfb_stage1_persist_supported(long n, long m, long k);
+/* profiling hook: per-sweep phase clocks of CTA 0 (prof[sweep * 16 + i]); NULL disables */
+int nmfb_stage1_set_prof(long long *prof);
 long nmfb_stage1_persist_work_len(long n, long m, long k);
 int nmfb_stage1_persist(const void *M, int m_is_f32, long n, long m, long k, double *X, double *Yt,
                         double *Xn, double *Yn, uint8_t *pX, uint8_t *pY, const double *row_n2,

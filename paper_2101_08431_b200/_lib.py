@@ -28,6 +28,7 @@ SIGNATURES = {
     "nmfb_surface_back_substitute": [P, P, P, P, P, P, L, L, L, I, P, P],
     # production entries
     "nmfb_nnls_ftab_len": [L],
+    "nmfb_stage1_set_prof": [P],
     "nmfb_blas_init": [P],
     "nmfb_nnls_batch_ws": [P, P, P, P, I, P, L, L, L, P, P, P, P, P, P, P, P, L, P],
     "nmfb_rowprod_work_len": [L, L, L, I],

@@ -228,6 +228,247 @@ __device__ __forceinline__ void nnls_seg_solve(WNnls<K, W>& s, double d, double 
   st_out = st;
 }
 
+
+// --------------------------------------------------------------------------
+// nnls_batch, one THREAD per right-hand side with every per-rhs vector in
+// registers (exact K, fully unrolled) and the passive factors read from a table of
+// all 2^K subsets (built by the same column-oriented factor as WNnls, so the bits
+// match).  The passive set is a bit mask; loops run over all K indices in
+// ascending order and skip non-passive terms with selects (acc stays bit-identical
+// to the reference's loop over passive positions), so a warp stays converged
+// inside a Lawson-Hanson trip.
+//   STAGED = true : T is the global table; the current subset's factor is staged
+//                   into this thread's shared-memory slot (packed, stride TAB_T) by
+//                   cp.async once per trip (csrc/surface.cu k_nnls_tab)
+//   STAGED = false: T is a (small) table in shared memory, read in place
+//                   (csrc/stage1_persist.cu)
+// --------------------------------------------------------------------------
+constexpr int TAB_T = 64;  // threads per block of k_nnls_tab
+
+template <int K, bool STAGED>
+struct TNnls {
+  static constexpr int KT = K * (K + 1) / 2;
+  const double* C;     // ctc (K x K, shared memory: broadcast reads)
+  double* sL;          // STAGED: this thread's slot, packed entry e at sL[e * TAB_T]
+  const double* Lt;    // !STAGED: the current subset's K x K factor (shared memory)
+  double d[K];
+
+  __device__ __forceinline__ static bool bit(unsigned pm, int i) { return (pm >> i) & 1u; }
+  __device__ __forceinline__ static constexpr int tri(int i, int j) { return i * (i + 1) / 2 + j; }
+  __device__ __forceinline__ double l(int i, int j) const {
+    return STAGED ? sL[tri(i, j) * TAB_T] : Lt[i * K + j];
+  }
+
+  __device__ __forceinline__ void stage(const double* __restrict__ T, unsigned pm) {
+    if (!STAGED) {
+      Lt = T + (long)pm * K * K;
+      return;
+    }
+    // every entry an asynchronous global -> shared copy, all in flight together
+    const double* Lg = T + (long)pm * K * K;
+    const unsigned base = (unsigned)__cvta_generic_to_shared(sL);
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                         base + (unsigned)(tri(i, j) * TAB_T * sizeof(double))),
+                     "l"(Lg + i * K + j)
+                     : "memory");
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  }
+
+  // _chol_solve_small (:247-258) on the passive indices
+  __device__ __forceinline__ void solve(unsigned pm, const double (&b)[K], double (&z)[K]) const {
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      double acc = b[i];
+#pragma unroll
+      for (int p = 0; p < i; ++p) {
+        const double t = acc - l(i, p) * z[p];
+        acc = bit(pm, p) ? t : acc;
+      }
+      z[i] = bit(pm, i) ? acc / l(i, i) : 0.0;
+    }
+    asm volatile("" ::: "memory");
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+      double acc = z[i];
+#pragma unroll
+      for (int p = i + 1; p < K; ++p) {
+        const double t = acc - l(p, i) * z[p];
+        acc = bit(pm, p) ? t : acc;
+      }
+      z[i] = bit(pm, i) ? acc / l(i, i) : 0.0;
+    }
+  }
+
+  // _passive_solve_refined (:261-274): z = solve(d); r = d - C_PP z; z += solve(r)
+  __device__ __forceinline__ void solve_refined(const double* __restrict__ T, unsigned pm,
+                                                double (&z)[K]) {
+    stage(T, pm);
+    // compiler memory barriers: the two solves re-read the factor instead of keeping
+    // all K(K+1)/2 entries live in registers between them
+    asm volatile("" ::: "memory");
+    solve(pm, d, z);
+    asm volatile("" ::: "memory");
+    double r[K], dz[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      double acc = d[a];
+#pragma unroll
+      for (int b = 0; b < K; ++b) {
+        const double t = acc - C[a * K + b] * z[b];
+        acc = bit(pm, b) ? t : acc;
+      }
+      r[a] = acc;
+    }
+    solve(pm, r, dz);
+#pragma unroll
+    for (int a = 0; a < K; ++a) z[a] = bit(pm, a) ? z[a] + dz[a] : 0.0;
+  }
+
+  // w_j = d_j - sum_p ctc[j][p] x_p over ALL p (the reference's dual loop)
+  __device__ __forceinline__ void grad(const double (&x)[K], double (&w)[K]) const {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double acc = d[j];
+#pragma unroll
+      for (int p = 0; p < K; ++p) acc -= C[j * K + p] * x[p];
+      w[j] = acc;
+    }
+  }
+};
+
+// One bit-exact nnls_batch solve (warm try :306-375, cold Lawson-Hanson :377-461,
+// residual :468-476) for the rhs in s.d.  okf[pm] != 0: subset pm's factor is PD.
+template <int K, bool STAGED>
+__device__ __forceinline__ void tnnls_solve(TNnls<K, STAGED>& s, const double* __restrict__ T,
+                                            const double* __restrict__ okf, double btb,
+                                            double tol_t, bool use_seed, unsigned seed_pm,
+                                            long max_changes, double (&x)[K], unsigned& pm_out,
+                                            long& nch_out, double& r2_out, int& st_out) {
+  using TN = TNnls<K, STAGED>;
+  double z[K], w[K];
+  unsigned pm = 0u;
+  long nch = 0;
+  bool solved = false;
+  if (use_seed) {
+    pm = seed_pm;
+    if (pm == 0u) {
+      bool ok = true;
+#pragma unroll
+      for (int j = 0; j < K; ++j) ok = ok && !(s.d[j] > tol_t);
+      if (ok) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) x[j] = 0.0;
+        solved = true;
+      }
+    } else if (okf[pm] != 0.0) {
+      s.solve_refined(T, pm, z);
+      bool feas = true;
+#pragma unroll
+      for (int a = 0; a < K; ++a) feas = feas && !(TN::bit(pm, a) && z[a] < 0.0);
+      if (feas) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) x[j] = TN::bit(pm, j) ? z[j] : 0.0;
+        s.grad(x, w);
+        bool dual_ok = true;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+          dual_ok = dual_ok && !(TN::bit(pm, j) ? (fabs(w[j]) > tol_t) : (w[j] > tol_t));
+        solved = dual_ok;
+      }
+    }
+  }
+  int st = 0;
+  if (!solved) {
+    pm = 0u;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      x[j] = 0.0;
+      w[j] = s.d[j];
+    }
+    for (;;) {
+      int jmax = -1;
+      double wmax = tol_t;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const bool c = !TN::bit(pm, j) && w[j] > wmax;
+        wmax = c ? w[j] : wmax;
+        jmax = c ? j : jmax;
+      }
+      if (jmax < 0) break;
+      pm |= 1u << jmax;
+      nch += 1;
+      if (nch > max_changes) {
+        st = 1;
+        break;
+      }
+      for (;;) {
+        if (pm == 0u) break;
+        if (okf[pm] == 0.0) {
+          st = 2;
+          break;
+        }
+        s.solve_refined(T, pm, z);
+        bool all_pos = true;
+#pragma unroll
+        for (int a = 0; a < K; ++a) all_pos = all_pos && !(TN::bit(pm, a) && z[a] <= 0.0);
+        if (all_pos) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) x[j] = TN::bit(pm, j) ? z[j] : 0.0;
+          break;
+        }
+        double alpha = 1.0;
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          if (TN::bit(pm, a) && z[a] <= 0.0) {
+            const double ratio = x[a] / (x[a] - z[a]);
+            alpha = ratio < alpha ? ratio : alpha;
+          }
+        }
+        unsigned drop = 0u;
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          if (!TN::bit(pm, a)) continue;
+          const double xa = x[a];
+          const double newx = xa + alpha * (z[a] - xa);
+          if (z[a] <= 0.0 && xa / (xa - z[a]) <= alpha) {
+            x[a] = 0.0;
+            drop |= 1u << a;
+          } else {
+            x[a] = newx > 0.0 ? newx : 0.0;
+          }
+        }
+        pm &= ~drop;
+        nch += __popc(drop);
+        if (nch > max_changes) {
+          st = 1;
+          break;
+        }
+      }
+      if (st != 0) break;
+      s.grad(x, w);
+    }
+  }
+  // resid2 = btb - sum_j (2 x_j) d_j + sum_j x_j (ctc x)_j, j ascending (:468-476)
+  double r2 = btb;
+#pragma unroll
+  for (int j = 0; j < K; ++j) r2 -= 2.0 * x[j] * s.d[j];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    double acc = 0.0;
+#pragma unroll
+    for (int p = 0; p < K; ++p) acc += s.C[j * K + p] * x[p];
+    r2 += x[j] * acc;
+  }
+  pm_out = pm;
+  nch_out = nch;
+  r2_out = r2 > 0.0 ? r2 : 0.0;
+  st_out = st;
+}
+
 #undef FULLM
 
 }  // namespace

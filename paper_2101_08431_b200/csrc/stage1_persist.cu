@@ -39,7 +39,16 @@ struct S1Args {
   int* status;   // [sweeps done, converged, failed]
   double* work;
   int m_in_smem;
+  long long* prof;  // optional per-sweep phase clocks of CTA 0 (scripts/stage1_phases.py)
 };
+
+long long* g_s1_prof = nullptr;  // set by nmfb_stage1_set_prof (profiling only)
+
+#define S1STAMP(i)                                                                  \
+  do {                                                                              \
+    if (a.prof && blockIdx.x == 0 && threadIdx.x < 32 && sweep < 512)               \
+      a.prof[(long)sweep * 16 + (i)] = clock64();                                   \
+  } while (0)
 
 __device__ __forceinline__ void gsync() { cooperative_groups::this_grid().sync(); }
 
@@ -77,6 +86,27 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
   double* tl = cb + CB * K;   // CB tolerances
   double* Ms = tl + CB;       // own rows of M (optional)
   __shared__ double gyy[K * K], gxx[K * K], scal[8], red[4 * SNW];
+  // k <= 6: the passive factor of every subset (2^K), rebuilt per half sweep, and a
+  // thread-per-rhs register NNLS (tnnls_solve) instead of warp segments
+  constexpr bool TAB = K <= 6;
+  constexpr int KT = TAB ? K : 1;
+  __shared__ double tab[(1 << KT) * KT * KT + (1 << KT)];
+  auto build_tab = [&](const double* C) {
+    const int seg = lane / W;
+    WNnls<K, W> f;
+    f.sl = lane % W;
+    f.sm = (W == 32) ? 0xffffffffu : (((1u << W) - 1u) << (seg * W));
+    const bool own = f.sl < K;
+#pragma unroll
+    for (int c = 0; c < K; ++c) f.C[c] = own ? C[f.sl * K + c] : 0.0;
+    for (int pm = wid * SEGS + seg; pm < (1 << K); pm += SNW * SEGS) {  // segment-uniform
+      const bool ok = f.factor((unsigned)pm);
+      if (own)
+#pragma unroll
+        for (int c = 0; c < K; ++c) tab[(pm * K + f.sl) * K + c] = f.Lr[c];
+      if (f.sl == 0) tab[(K * K << K) + pm] = ok ? 1.0 : 0.0;
+    }
+  };
 
   for (long e = tid; e < N; e += ST) Ys[e] = a.Yt[e];
   for (long e = tid; e < (long)nr * K; e += ST) Xs[e] = a.X[r0 * K + e];
@@ -89,6 +119,7 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
   int sweep = 0, converged = 0, failed = 0;
   for (;;) {
     const int mode = (sweep > 0) ? 2 : a.first_mode;
+    S1STAMP(0);
     // ---------------- X half ----------------
     for (int e = wid; e < K * K; e += SNW) {  // Y Y^T, lanes stride the columns
       const int p = e / K, q = e % K;
@@ -104,13 +135,40 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
       cb[e] = s;
     }
     __syncthreads();
+    S1STAMP(1);
     for (int rr = tid; rr < nr; rr += ST) {
       double t = 0.0;
       for (int p = 0; p < K; ++p) t = fmax(t, fabs(cb[rr * K + p]));
       tl[rr] = a.tol_fixed >= 0.0 ? a.tol_fixed : 1e-12 * fmax(1.0, t);
     }
     __syncthreads();
-    {
+    if (TAB) {
+      build_tab(gyy);
+      __syncthreads();
+      for (int rr = tid; rr < nr; rr += ST) {
+        const long i = r0 + rr;
+        TNnls<K, false> ts;
+        ts.C = gyy;
+        unsigned seed = 0u;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          ts.d[j] = cb[rr * K + j];
+          seed |= (mode == 2 && a.pX[i * K + j] != 0 ? 1u : 0u) << j;
+        }
+        double x[K], r2;
+        unsigned pm;
+        long nch;
+        int st;
+        tnnls_solve<K, false>(ts, tab, tab + (K * K << K), a.row_n2[i], tl[rr], mode == 2, seed,
+                              3 * K, x, pm, nch, r2, st);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          Xn[rr * K + j] = x[j];
+          a.pX[i * K + j] = ((pm >> j) & 1u) ? 1 : 0;
+        }
+        a.stX[i] = (int8_t)st;
+      }
+    } else {
       const int seg = lane / W;
       WNnls<K, W> s;
       s.sl = lane % W;
@@ -136,6 +194,7 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
       }
     }
     __syncthreads();
+    S1STAMP(2);
     // partials: G_X = Xn^T Xn, ctbY = M_rows^T Xn, ||dX||^2, ||X||^2, failure flag
     for (long e = tid; e < NA; e += ST) {
       double s = 0.0;
@@ -159,7 +218,9 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
       }
       __stcg(PA + e * G + cta, s);
     }
+    S1STAMP(3);
     gsync();
+    S1STAMP(4);
     // ---------------- Y half (this CTA's column slice) ----------------
     for (int e = wid; e < K * K; e += SNW) {
       const double v = s1_cta_sum(PA, G, e);
@@ -176,8 +237,40 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
       tl[cc] = a.tol_fixed >= 0.0 ? a.tol_fixed : 1e-12 * fmax(1.0, t);
     }
     __syncthreads();
+    S1STAMP(5);
     double ydx = 0.0, yy = 0.0, yr2 = 0.0, yfail = 0.0;  // per-thread (segment lane 0)
-    {
+    if (TAB) {
+      build_tab(gxx);
+      __syncthreads();
+      for (int cc = tid; cc < nc; cc += ST) {
+        const long j = c0 + cc;
+        TNnls<K, false> ts;
+        ts.C = gxx;
+        unsigned seed = 0u;
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          ts.d[q] = cb[cc * K + q];
+          seed |= (mode == 2 && a.pY[j * K + q] != 0 ? 1u : 0u) << q;
+        }
+        double y[K], r2;
+        unsigned pm;
+        long nch;
+        int st;
+        tnnls_solve<K, false>(ts, tab, tab + (K * K << K), a.col_n2[j], tl[cc], mode == 2, seed,
+                              3 * K, y, pm, nch, r2, st);
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          a.Yn[j * K + q] = y[q];
+          a.pY[j * K + q] = ((pm >> q) & 1u) ? 1 : 0;
+          const double yo = Ys[j * K + q];
+          ydx = ydx + (y[q] - yo) * (y[q] - yo);
+          yy = yy + yo * yo;
+        }
+        a.stY[j] = (int8_t)st;
+        yr2 = yr2 + r2;
+        if (st != 0) yfail = 1.0;
+      }
+    } else {
       const int seg = lane / W;
       WNnls<K, W> s;
       s.sl = lane % W;
@@ -224,7 +317,9 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
         __stcg(PB + (long)tid * G + cta, s);
       }
     }
+    S1STAMP(6);
     gsync();
+    S1STAMP(7);
     // ---------------- sweep statistics, convergence, reload ----------------
     for (int e = wid; e < 7; e += SNW) {
       double v;
@@ -237,6 +332,7 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
       if (lane == 0) scal[e] = v;
     }
     __syncthreads();
+    S1STAMP(8);
     const double step = sqrt(scal[0] + scal[3]);
     const double nrmv = sqrt(scal[1] + scal[4]);
     const double obj = 0.5 * scal[5];
@@ -253,6 +349,8 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
     for (long e = tid; e < (long)nr * K; e += ST) Xs[e] = Xn[e];
     for (long e = tid; e < N; e += ST) Ys[e] = __ldcg(a.Yn + e);
     __syncthreads();
+    if (a.prof && blockIdx.x == 0 && threadIdx.x < 32 && sweep - 1 < 512)
+      a.prof[(long)(sweep - 1) * 16 + 9] = clock64();
     if (failed || converged || sweep >= a.max_sweeps) break;
   }
   for (long e = tid; e < (long)nr * K; e += ST) a.X[r0 * K + e] = Xs[e];
@@ -338,6 +436,7 @@ extern "C" int nmfb_stage1_persist(const void* M, int m_is_f32, long n, long m, 
   a.logv = logv;
   a.status = status;
   a.work = work;
+  a.prof = g_s1_prof;
   void* args[] = {&a};
   cudaError_t err = cudaSuccess;
 #define LAUNCH(KK_, WW_, T_)                                                                     \
@@ -364,5 +463,11 @@ extern "C" int nmfb_stage1_persist(const void* M, int m_is_f32, long n, long m, 
 #undef LAUNCH
   if (err != cudaSuccess) return NMFB_ELAUNCH;
   NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// profiling hook: per-sweep clock64 stamps of CTA 0 into prof[sweep * 16 + i] (NULL: off)
+extern "C" int nmfb_stage1_set_prof(long long* prof) {
+  g_s1_prof = prof;
   return NMFB_OK;
 }

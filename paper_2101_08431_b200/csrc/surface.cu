@@ -270,99 +270,6 @@ __global__ void __launch_bounds__(128) k_factor_table(const double* __restrict__
 // reference's loop over passive positions), so a warp stays converged inside a
 // Lawson-Hanson trip and issues ~K^2 instructions per trip for 32 right-hand
 // sides (the warp-per-rhs kernel issues that per rhs).
-constexpr int TAB_T = 64;  // threads per block of k_nnls_tab
-
-template <int K>
-struct TNnls {
-  static constexpr int KT = K * (K + 1) / 2;
-  const double* C;  // ctc (K x K, shared memory: broadcast reads)
-  double* sL;       // this thread's staged factor: packed lower entry e at sL[e * TAB_T]
-  double d[K];
-
-  __device__ __forceinline__ static bool bit(unsigned pm, int i) { return (pm >> i) & 1u; }
-  __device__ __forceinline__ static constexpr int tri(int i, int j) { return i * (i + 1) / 2 + j; }
-  __device__ __forceinline__ double l(int i, int j) const { return sL[tri(i, j) * TAB_T]; }
-
-  // stage the table factor of subset pm: every entry is an asynchronous global ->
-  // shared copy (cp.async, no registers), all in flight together, so a trip pays
-  // one gather round trip instead of a divergent global load inside every step of
-  // the solves (or one round trip per row)
-  __device__ __forceinline__ void stage(const double* __restrict__ T, unsigned pm) {
-    const double* Lt = T + (long)pm * K * K;
-    const unsigned base = (unsigned)__cvta_generic_to_shared(sL);
-#pragma unroll
-    for (int i = 0; i < K; ++i)
-#pragma unroll
-      for (int j = 0; j <= i; ++j)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
-                         base + (unsigned)(tri(i, j) * TAB_T * sizeof(double))),
-                     "l"(Lt + i * K + j)
-                     : "memory");
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-  }
-
-  // _chol_solve_small (:247-258) on the passive indices with the staged factor
-  __device__ __forceinline__ void solve(unsigned pm, const double (&b)[K], double (&z)[K]) const {
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-      double acc = b[i];
-#pragma unroll
-      for (int p = 0; p < i; ++p) {
-        const double t = acc - l(i, p) * z[p];
-        acc = bit(pm, p) ? t : acc;
-      }
-      z[i] = bit(pm, i) ? acc / l(i, i) : 0.0;
-    }
-    asm volatile("" ::: "memory");
-#pragma unroll
-    for (int i = K - 1; i >= 0; --i) {
-      double acc = z[i];
-#pragma unroll
-      for (int p = i + 1; p < K; ++p) {
-        const double t = acc - l(p, i) * z[p];
-        acc = bit(pm, p) ? t : acc;
-      }
-      z[i] = bit(pm, i) ? acc / l(i, i) : 0.0;
-    }
-  }
-
-  // _passive_solve_refined (:261-274): z = solve(d); r = d - C_PP z; z += solve(r)
-  __device__ __forceinline__ void solve_refined(const double* __restrict__ T, unsigned pm,
-                                                double (&z)[K]) {
-    stage(T, pm);
-    // compiler memory barriers: the two solves re-read the staged factor instead
-    // of keeping all K(K+1)/2 entries live in registers between them
-    asm volatile("" ::: "memory");
-    solve(pm, d, z);
-    asm volatile("" ::: "memory");
-    double r[K], dz[K];
-#pragma unroll
-    for (int a = 0; a < K; ++a) {
-      double acc = d[a];
-#pragma unroll
-      for (int b = 0; b < K; ++b) {
-        const double t = acc - C[a * K + b] * z[b];
-        acc = bit(pm, b) ? t : acc;
-      }
-      r[a] = acc;
-    }
-    solve(pm, r, dz);
-#pragma unroll
-    for (int a = 0; a < K; ++a) z[a] = bit(pm, a) ? z[a] + dz[a] : 0.0;
-  }
-
-  // w_j = d_j - sum_p ctc[j][p] x_p over ALL p (the reference's dual loop)
-  __device__ __forceinline__ void grad(const double (&x)[K], double (&w)[K]) const {
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      double acc = d[j];
-#pragma unroll
-      for (int p = 0; p < K; ++p) acc -= C[j * K + p] * x[p];
-      w[j] = acc;
-    }
-  }
-};
-
 template <int K>
 __global__ void __launch_bounds__(TAB_T) k_nnls_tab(const double* __restrict__ ctc_g,
                                                   const double* __restrict__ ctb,
@@ -376,140 +283,35 @@ __global__ void __launch_bounds__(TAB_T) k_nnls_tab(const double* __restrict__ c
                                                   int8_t* __restrict__ st_out,
                                                   const double* __restrict__ T) {
   __shared__ double ctc[K * K];
-  __shared__ double sLall[TNnls<K>::KT * TAB_T];
+  __shared__ double sLall[TNnls<K, true>::KT * TAB_T];
   for (int i = threadIdx.x; i < K * K; i += blockDim.x) ctc[i] = ctc_g[i];
   __syncthreads();
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nrhs) return;
   const double* okf = T + ((long)K * K << K);
-  TNnls<K> s;
+  TNnls<K, true> s;
   s.C = ctc;
   s.sL = sLall + threadIdx.x;
 #pragma unroll
   for (int j = 0; j < K; ++j) s.d[j] = ctb[t * K + j];
-  const double tol_t = tol[t];
-  double x[K], z[K], w[K];
-  unsigned pm = 0u;
-  long nch = 0;
-  bool solved = false;
   const bool use_seed = (seed_mode == 2) || (seed_mode == 1 && t > 0);
-  if (use_seed) {
+  unsigned seed_pm = 0u;
+  if (use_seed)
 #pragma unroll
-    for (int j = 0; j < K; ++j) pm |= (seeds[t * K + j] != 0 ? 1u : 0u) << j;
-    if (pm == 0u) {
-      bool ok = true;
-#pragma unroll
-      for (int j = 0; j < K; ++j) ok = ok && !(s.d[j] > tol_t);
-      if (ok) {
-#pragma unroll
-        for (int j = 0; j < K; ++j) x[j] = 0.0;
-        solved = true;
-      }
-    } else if (__ldg(okf + pm) != 0.0) {
-      s.solve_refined(T, pm, z);
-      bool feas = true;
-#pragma unroll
-      for (int a = 0; a < K; ++a) feas = feas && !(TNnls<K>::bit(pm, a) && z[a] < 0.0);
-      if (feas) {
-#pragma unroll
-        for (int j = 0; j < K; ++j) x[j] = TNnls<K>::bit(pm, j) ? z[j] : 0.0;
-        s.grad(x, w);
-        bool dual_ok = true;
-#pragma unroll
-        for (int j = 0; j < K; ++j)
-          dual_ok = dual_ok && !(TNnls<K>::bit(pm, j) ? (fabs(w[j]) > tol_t) : (w[j] > tol_t));
-        solved = dual_ok;
-      }
-    }
-  }
-  int st = 0;
-  if (!solved) {
-    // cold Lawson-Hanson start (:377-461)
-    pm = 0u;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      x[j] = 0.0;
-      w[j] = s.d[j];
-    }
-    for (;;) {
-      int jmax = -1;
-      double wmax = tol_t;
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const bool c = !TNnls<K>::bit(pm, j) && w[j] > wmax;
-        wmax = c ? w[j] : wmax;
-        jmax = c ? j : jmax;
-      }
-      if (jmax < 0) break;
-      pm |= 1u << jmax;
-      nch += 1;
-      if (nch > max_changes) {
-        st = 1;
-        break;
-      }
-      for (;;) {
-        if (pm == 0u) break;
-        if (__ldg(okf + pm) == 0.0) {
-          st = 2;
-          break;
-        }
-        s.solve_refined(T, pm, z);
-        bool all_pos = true;
-#pragma unroll
-        for (int a = 0; a < K; ++a) all_pos = all_pos && !(TNnls<K>::bit(pm, a) && z[a] <= 0.0);
-        if (all_pos) {
-#pragma unroll
-          for (int j = 0; j < K; ++j) x[j] = TNnls<K>::bit(pm, j) ? z[j] : 0.0;
-          break;
-        }
-        double alpha = 1.0;
-#pragma unroll
-        for (int a = 0; a < K; ++a) {
-          if (TNnls<K>::bit(pm, a) && z[a] <= 0.0) {
-            const double ratio = x[a] / (x[a] - z[a]);
-            alpha = ratio < alpha ? ratio : alpha;
-          }
-        }
-        unsigned drop = 0u;
-#pragma unroll
-        for (int a = 0; a < K; ++a) {
-          if (!TNnls<K>::bit(pm, a)) continue;
-          const double xa = x[a];
-          const double newx = xa + alpha * (z[a] - xa);
-          if (z[a] <= 0.0 && xa / (xa - z[a]) <= alpha) {
-            x[a] = 0.0;
-            drop |= 1u << a;
-          } else {
-            x[a] = newx > 0.0 ? newx : 0.0;
-          }
-        }
-        pm &= ~drop;
-        nch += __popc(drop);
-        if (nch > max_changes) {
-          st = 1;
-          break;
-        }
-      }
-      if (st != 0) break;
-      s.grad(x, w);
-    }
-  }
-  double r2 = btb[t];
+    for (int j = 0; j < K; ++j) seed_pm |= (seeds[t * K + j] != 0 ? 1u : 0u) << j;
+  double x[K], r2;
+  unsigned pm;
+  long nch;
+  int st;
+  tnnls_solve<K, true>(s, T, okf, btb[t], tol[t], use_seed, seed_pm, max_changes, x, pm, nch, r2,
+                       st);
 #pragma unroll
   for (int j = 0; j < K; ++j) {
     x_out[t * K + j] = x[j];
-    p_out[t * K + j] = TNnls<K>::bit(pm, j) ? 1 : 0;
-    r2 -= 2.0 * x[j] * s.d[j];
-  }
-#pragma unroll
-  for (int j = 0; j < K; ++j) {
-    double acc = 0.0;
-#pragma unroll
-    for (int p = 0; p < K; ++p) acc += ctc[j * K + p] * x[p];
-    r2 += x[j] * acc;
+    p_out[t * K + j] = TNnls<K, true>::bit(pm, j) ? 1 : 0;
   }
   ch_out[t] = nch;
-  r2_out[t] = r2 > 0.0 ? r2 : 0.0;
+  r2_out[t] = r2;
   st_out[t] = (int8_t)st;
 }
 
