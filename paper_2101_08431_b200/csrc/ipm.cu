@@ -1054,7 +1054,12 @@ extern "C" long nmfb_atb_work_len(long rows, long ca, long cb) {
   const long max_ns = (rows + 255) / 256;
   if (ns > max_ns) ns = max_ns;
   if (ns < 1) ns = 1;
-  return ns * ca * cb;
+  long len = ns * ca * cb;
+  if (ca == cb && ca <= 16 && rows > 0) {  // small square products run as a Gram (nmfb_grams)
+    const long g = nmfb_grams_work_len(rows, ca, 1);
+    if (g > len) len = g;
+  }
+  return len;
 }
 
 // out (ca x cb) = A^T B; A (rows x ca), B (rows x cb)
@@ -1098,6 +1103,13 @@ extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, lo
     cudaMemsetAsync(out, 0, sizeof(double) * ca * cb, st);
     return NMFB_OK;
   }
+  // small square products (the packed k(k+1)/2-wide capacitance Grams of c1-c3): the
+  // multi-Gram kernel (64 rows per CTA, warp-per-entry finish) instead of 32 x 32
+  // tiles with 2 of 8 x 32 threads busy
+  if (ca == cb && ca <= 16 && 2.0 * (double)rows * (double)ca * (double)cb < 1e7 &&
+      nmfb_grams_work_len(rows, ca, 1) <= work_len)
+    return nmfb_grams(1, A, B, out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                      nullptr, nullptr, rows, ca, work, work_len, stream);
   // large products: cuBLAS DGEMM on the FP64 tensor cores.  Row-major out = A^T B is
   // column-major out^T = B_c A_c^T with A_c = A^T (ca x rows), B_c (cb x rows).
   if (2.0 * (double)rows * (double)ca * (double)cb >= 1e7 && rows <= 0x7fffffffL) {
