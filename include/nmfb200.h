@@ -186,6 +186,12 @@ int nmfb_barrier_trials(const double *X, const double *dX, long nx, const double
  * coefficients, barrier sums) and writes alpha1, t, alpha2 (graph-capturable). */
 int nmfb_armijo_select(double *sc, double mu, double wx, double wy, double eta,
                        int max_backtracks, const int *fcodes, void *stream);
+/* graph capture helper: while mu_dev != NULL, r1_factor / schur_rhs / direction /
+ * kkt_sums / armijo_select / armijo_lazy read [mu, wx mu, wy mu] from mu_dev at run
+ * time instead of their scalar arguments (a captured iteration then replays for any
+ * mu); pass NULL after the capture. */
+int nmfb_set_mu_source(const double *mu_dev);
+
 /* nmfb_barrier_trials + nmfb_armijo_select with lazy trial batches: trials 0..7, a
  * device pre-check, the remaining trials only when it did not decide (their launches
  * return at once otherwise), then the full search -- the same accepted t.  Uses

@@ -30,6 +30,7 @@ SIGNATURES = {
     "nmfb_nnls_ftab_len": [L],
     "nmfb_stage1_set_prof": [P],
     "nmfb_blas_init": [P],
+    "nmfb_set_mu_source": [P],
     "nmfb_nnls_batch_ws": [P, P, P, P, I, P, L, L, L, P, P, P, P, P, P, P, P, L, P],
     "nmfb_rowprod_work_len": [L, L, L, I],
     "nmfb_rowprod": [P, I, L, L, P, L, P, P, D, P, L, P],

@@ -20,6 +20,12 @@
 #include "common.cuh"
 #include "nmfb200.h"
 
+// Barrier value source for CUDA-graph capture (nmfb_set_mu_source): while set,
+// the mu-dependent launches below bake this device pointer ([mu, wx mu, wy mu]) into
+// their arguments instead of the scalar values, so one captured iteration replays
+// for any mu (the host rewrites the three doubles before a replay).
+static const double* g_mu_dev = nullptr;
+
 namespace {
 
 
@@ -150,7 +156,9 @@ __global__ void __launch_bounds__(128) k_r1_factor(const double* __restrict__ GY
                                                    double* __restrict__ h, double* __restrict__ g,
                                                    double* __restrict__ Apk,
                                                    double* __restrict__ XXpk,
-                                                   int* __restrict__ bad) {
+                                                   int* __restrict__ bad,
+    const double* __restrict__ mu_dev) {
+  if (mu_dev != nullptr) mux = mu_dev[1];  // graph replays: barrier value from device memory
   __shared__ double gy[K * K];
   for (int e = threadIdx.x; e < K * K; e += blockDim.x) gy[e] = GY[e];
   __syncthreads();
@@ -456,7 +464,9 @@ __global__ void k_make_p(const double* __restrict__ X, const double* __restrict_
 template <int K>
 __global__ void k_schur_rhs(const double* __restrict__ Yt, const double* __restrict__ gY,
                             const double* __restrict__ H, const double* __restrict__ FtG,
-                            double muy, long m, double* __restrict__ rhs) {
+                            double muy, long m, double* __restrict__ rhs,
+    const double* __restrict__ mu_dev) {
+  if (mu_dev != nullptr) muy = mu_dev[2];
   const long j = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= m) return;
 #pragma unroll
@@ -487,7 +497,9 @@ __global__ void __launch_bounds__(128) k_dir_rows(const double* __restrict__ Lin
                                                   const double* __restrict__ gX, double mux,
                                                   double tau, long n, double* __restrict__ dX,
                                                   double* __restrict__ dR,
-                                                  double* __restrict__ part) {
+                                                  double* __restrict__ part,
+    const double* __restrict__ mu_dev) {
+  if (mu_dev != nullptr) mux = mu_dev[1];
   __shared__ double gd[K * K];
   __shared__ double sh[32];
   for (int e = threadIdx.x; e < K * K; e += blockDim.x) gd[e] = Gdy[e];
@@ -542,7 +554,9 @@ __global__ void __launch_bounds__(256) k_dir_cols(const double* __restrict__ Yt,
                                                   const double* __restrict__ dY, double muy,
                                                   double tau, long len,
                                                   double* __restrict__ dS,
-                                                  double* __restrict__ part) {
+                                                  double* __restrict__ part,
+    const double* __restrict__ mu_dev) {
+  if (mu_dev != nullptr) muy = mu_dev[2];
   __shared__ double sh[32];
   double gtp = 0.0, a1 = 1.0 / 0.0, a2 = 1.0 / 0.0;
   for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < len;
@@ -726,7 +740,12 @@ __global__ void __launch_bounds__(256) k_kkt_partial(const double* __restrict__ 
                                                      const double* __restrict__ S,
                                                      const double* __restrict__ gY, long ny,
                                                      double mux, double muy,
-                                                     double* __restrict__ part) {
+                                                     double* __restrict__ part,
+    const double* __restrict__ mu_dev) {
+  if (mu_dev != nullptr) {
+    mux = mu_dev[1];
+    muy = mu_dev[2];
+  }
   __shared__ double sh[32];
   double v[12];
 #pragma unroll
@@ -859,7 +878,9 @@ __global__ void k_fill(double* __restrict__ v, long len, double c) {
 // trials are needed (0).  With sc[31] == 1 on entry to a full search, nothing to do.
 __global__ void k_armijo_select(double* __restrict__ sc, double mu, double wx, double wy,
                                 double eta, int max_bt, const int* __restrict__ fcodes,
-                                int t_lim = -1, int honor_decided = 0) {
+                                int t_lim = -1, int honor_decided = 0,
+                                const double* __restrict__ mu_dev = nullptr) {
+  if (mu_dev != nullptr) mu = mu_dev[0];
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (honor_decided && sc[31] != 0.0) return;
   // fcodes = [R1 failing row, reduced-system info, D failing column]: on any
@@ -1025,7 +1046,7 @@ extern "C" int nmfb_r1_factor(const double* GY, const double* X, const double* R
   const int blocks = (int)((n + 127) / 128);
 #define CASE(KK)                                                                               \
   case KK:                                                                                     \
-    ++g_nmfb_launches, k_r1_factor<KK><<<blocks, 128, 0, st>>>(GY, X, R, gX, mux, rho, n, L, h, g, Apk, XXpk, bad); \
+    ++g_nmfb_launches, k_r1_factor<KK><<<blocks, 128, 0, st>>>(GY, X, R, gX, mux, rho, n, L, h, g, Apk, XXpk, bad, g_mu_dev); \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
@@ -1237,7 +1258,7 @@ extern "C" int nmfb_schur_rhs(const double* Yt, const double* gY, const double* 
   const unsigned blocks = (unsigned)((m + 127) / 128);
 #define CASE(KK)                                                                  \
   case KK:                                                                        \
-    ++g_nmfb_launches, k_schur_rhs<KK><<<blocks, 128, 0, st>>>(Yt, gY, H, FtG, muy, m, rhs);        \
+    ++g_nmfb_launches, k_schur_rhs<KK><<<blocks, 128, 0, st>>>(Yt, gY, H, FtG, muy, m, rhs, g_mu_dev); \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
@@ -1258,11 +1279,11 @@ extern "C" int nmfb_direction(const double* L, const double* Xf, const double* h
   if (work_len < 3L * (rb + RED_BLOCKS)) return NMFB_ENOMEM;
 #define CASE(KK)                                                                              \
   case KK:                                                                                    \
-    ++g_nmfb_launches, k_dir_rows<KK><<<rb, 128, 0, st>>>(L, Xf, h, Gdy, FdY, X, R, gX, mux, tau, n, dX, dR, work); \
+    ++g_nmfb_launches, k_dir_rows<KK><<<rb, 128, 0, st>>>(L, Xf, h, Gdy, FdY, X, R, gX, mux, tau, n, dX, dR, work, g_mu_dev); \
     break;
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
-  ++g_nmfb_launches, k_dir_cols<<<RED_BLOCKS, 256, 0, st>>>(Yt, S, gY, dY, muy, tau, m * k, dS, work + 3 * rb);
+  ++g_nmfb_launches, k_dir_cols<<<RED_BLOCKS, 256, 0, st>>>(Yt, S, gY, dY, muy, tau, m * k, dS, work + 3 * rb, g_mu_dev);
   ++g_nmfb_launches, k_finish_dir<<<1, 256, 0, st>>>(work, rb, work + 3 * rb, RED_BLOCKS, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
@@ -1312,7 +1333,7 @@ extern "C" int nmfb_kkt_sums(const double* X, const double* R, const double* gX,
                              const double* Yt, const double* S, const double* gY, long ny,
                              double mux, double muy, double* out, double* work, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  ++g_nmfb_launches, k_kkt_partial<<<RED_BLOCKS, 256, 0, st>>>(X, R, gX, nx, Yt, S, gY, ny, mux, muy, work);
+  ++g_nmfb_launches, k_kkt_partial<<<RED_BLOCKS, 256, 0, st>>>(X, R, gX, nx, Yt, S, gY, ny, mux, muy, work, g_mu_dev);
   ++g_nmfb_launches, k_finish_kkt<<<1, 256, 0, st>>>(work, RED_BLOCKS, out);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
@@ -1365,7 +1386,7 @@ extern "C" int nmfb_armijo_lazy(const double* X, const double* dX, long nx, cons
   ++g_nmfb_launches, k_finish_trials<<<(2 * tb * 32 + 255) / 256, 256, 0, st>>>(work, nb, tb, bars,
                                                                              0, nullptr);
   ++g_nmfb_launches, k_armijo_select<<<1, 32, 0, st>>>(sc, mu, wx, wy, eta, max_backtracks, fcodes,
-                                                       tb, 0);
+                                                       tb, 0, g_mu_dev);
   if (ntrials > tb) {
     const int rest = ntrials - tb;
     ++g_nmfb_launches, k_barrier_trials<<<dim3(nb, rest), 256, 0, st>>>(
@@ -1374,7 +1395,7 @@ extern "C" int nmfb_armijo_lazy(const double* X, const double* dX, long nx, cons
         work, nb, ntrials, bars, tb, sc + 31);
   }
   ++g_nmfb_launches, k_armijo_select<<<1, 32, 0, st>>>(sc, mu, wx, wy, eta, max_backtracks, fcodes,
-                                                       -1, 1);
+                                                       -1, 1, g_mu_dev);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -1382,7 +1403,8 @@ extern "C" int nmfb_armijo_lazy(const double* X, const double* dX, long nx, cons
 extern "C" int nmfb_armijo_select(double* sc, double mu, double wx, double wy, double eta,
                                   int max_backtracks, const int* fcodes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  ++g_nmfb_launches, k_armijo_select<<<1, 32, 0, st>>>(sc, mu, wx, wy, eta, max_backtracks, fcodes);
+  ++g_nmfb_launches, k_armijo_select<<<1, 32, 0, st>>>(sc, mu, wx, wy, eta, max_backtracks, fcodes,
+                                                       -1, 0, g_mu_dev);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }
@@ -1567,5 +1589,10 @@ extern "C" int nmfb_grams(int count, const double* A0, const double* B0, double*
   const int NO = count * (int)(k * k);
   ++g_nmfb_launches, k_grams_finish<<<(NO + 7) / 8, 256, 0, st>>>(gs, (int)(k * k), work, (int)G);
   NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_set_mu_source(const double* mu_dev) {
+  g_mu_dev = mu_dev;
   return NMFB_OK;
 }

@@ -414,6 +414,7 @@ class IpmEngine:
         self.fact_full = False
         self.fact_F = 0
         self.graphs = {}
+        self.mu_dev = None  # [mu, wx mu, wy mu] read by the captured general-path kernels
         self.graph_pool = None
         self.capture_stream = None
         self.use_graphs = p.use_graphs and not P.comm.active and not self.dense_gn
@@ -520,8 +521,20 @@ class IpmEngine:
         self.refresh_launch()
 
     def gn_iteration_graph(self):
-        """Replay (capturing on first use) the GN iteration graph for the current state."""
-        key = (self.fi, self.mu)
+        """Replay (capturing on first use) the GN iteration graph for the current state.
+
+        General path: the barrier value is read from device memory by the captured
+        kernels (nmfb_set_mu_source during capture), so one graph per F buffer serves
+        every mu; the fused small path bakes mu and is keyed by it."""
+        if not self.small:
+            if self.mu_dev is None:
+                self.mu_dev = self.P.buf(3)
+                self.mu_host = torch.zeros(3, dtype=torch.float64).pin_memory()
+            self.mu_host[0] = self.mu
+            self.mu_host[1] = self.wx * self.mu
+            self.mu_host[2] = self.wy * self.mu
+            self.mu_dev.copy_(self.mu_host, non_blocking=True)
+        key = (self.fi,) if not self.small else (self.fi, self.mu)
         g = self.graphs.get(key)
         state = (self.fi, self.fact_F, self.have_fact, self.fact_full, self.fact_dense)
         if g is None:
@@ -547,8 +560,11 @@ class IpmEngine:
                 else:
                     g.capture_begin(pool=self.graph_pool)
                 try:
+                    if not self.small:
+                        self.P.lib.nmfb_set_mu_source(self.mu_dev.data_ptr())
                     self.gn_iteration_launch()
                 finally:
+                    self.P.lib.nmfb_set_mu_source(None)
                     g.capture_end()
             cur.wait_stream(self.capture_stream)
             if _GRAPH_DEBUG:
