@@ -951,10 +951,16 @@ struct GramSet {
   int count;
 };
 
+// One chunk of up to GR_CH rows per CTA: every A_q / B_q row segment of the chunk is
+// copied to shared memory with cp.async in one round (all loads in flight), then
+// thread per output entry.  (The 32-row double-barrier chunks of the first version
+// paid three L2/HBM round trips per CTA: 10 us at c4's 20000 rows.)
+constexpr int GR_CH = 128;
+
 template <int K>
 __global__ void __launch_bounds__(256) k_grams_partial(GramSet gs, long rows, long rows_per_cta,
                                                        double* __restrict__ part) {
-  __shared__ double sa[4][32][K], sb[4][32][K];
+  extern __shared__ __align__(16) double gsm[];  // [count][2][GR_CH][K]
   constexpr int KK = K * K;
   constexpr int U = (4 * KK + 255) / 256;
   const int nq = gs.count, NO = nq * KK, tid = threadIdx.x;
@@ -962,23 +968,33 @@ __global__ void __launch_bounds__(256) k_grams_partial(GramSet gs, long rows, lo
   double acc[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) acc[u] = 0.0;
-  for (long ib = i0; ib < i1; ib += 32) {
-    const int nr = (int)min(32L, i1 - ib);
+  for (long ib = i0; ib < i1; ib += GR_CH) {
+    const int nr = (int)min((long)GR_CH, i1 - ib);
     __syncthreads();
-    for (int q = 0; q < nq; ++q)
+    for (int q = 0; q < nq; ++q) {
+      double* sa = gsm + (long)(2 * q) * GR_CH * K;
+      double* sb = sa + GR_CH * K;
+      const double* ga = gs.A[q] + ib * K;
+      const double* gb = gs.B[q] + ib * K;
       for (int e = tid; e < nr * K; e += 256) {
-        sa[q][e / K][e % K] = gs.A[q][ib * K + e];
-        sb[q][e / K][e % K] = gs.B[q][ib * K + e];
+        const unsigned da = (unsigned)__cvta_generic_to_shared(sa + e);
+        const unsigned db = (unsigned)__cvta_generic_to_shared(sb + e);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(da), "l"(ga + e) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(db), "l"(gb + e) : "memory");
       }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = tid + 256 * u;
       if (e < NO) {
         const int q = e / KK, a = (e / K) % K, b = e % K;
-        double s = acc[u];
-        for (int r = 0; r < nr; ++r) s = fma(sa[q][r][a], sb[q][r][b], s);
-        acc[u] = s;
+        const double* sa = gsm + (long)(2 * q) * GR_CH * K;
+        const double* sb = sa + GR_CH * K;
+        double s0 = acc[u];
+        for (int r = 0; r < nr; ++r) s0 = fma(sa[r * K + a], sb[r * K + b], s0);
+        acc[u] = s0;
       }
     }
   }
@@ -1549,7 +1565,7 @@ extern "C" int nmfb_ffree_quartic(const double* A1, const double* A2, const doub
 // out_q = A_q^T B_q (k x k) for q < count <= 4; A_q, B_q (rows x k) row-major fp64.
 // work >= nmfb_grams_work_len(rows, k, count).
 static long grams_ctas(long rows) {
-  long g = (rows + 63) / 64;
+  long g = (rows + GR_CH - 1) / GR_CH;
   if (g > 296) g = 296;
   return g < 1 ? 1 : g;
 }
@@ -1580,10 +1596,22 @@ extern "C" int nmfb_grams(int count, const double* A0, const double* B0, double*
   const long G = grams_ctas(rows);
   if (G * count * k * k > work_len) return NMFB_ENOMEM;
   const long rpc = (rows + G - 1) / G;
+  static const bool attrs = [] {  // once, on the first (eager) call: 4 Grams of k = 16
+#define SETA(KK_)                                                                             \
+    cudaFuncSetAttribute(k_grams_partial<KK_>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                         (int)(8 * GR_CH * KK_ * sizeof(double)));
+    SETA(1) SETA(2) SETA(3) SETA(4) SETA(5) SETA(6) SETA(7) SETA(8) SETA(9) SETA(10) SETA(11)
+    SETA(12) SETA(13) SETA(14) SETA(15) SETA(16)
+#undef SETA
+    return true;
+  }();
+  (void)attrs;
 #define CASE(KK_)                                                                             \
-  case KK_:                                                                                   \
-    ++g_nmfb_launches, k_grams_partial<KK_><<<(unsigned)G, 256, 0, st>>>(gs, rows, rpc, work); \
-    break;
+  case KK_: {                                                                                 \
+    const size_t sm = (size_t)count * 2 * GR_CH * KK_ * sizeof(double);                       \
+    ++g_nmfb_launches, k_grams_partial<KK_><<<(unsigned)G, 256, sm, st>>>(gs, rows, rpc, work); \
+    break;                                                                                    \
+  }
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
   const int NO = count * (int)(k * k);
