@@ -242,28 +242,37 @@ __global__ void __launch_bounds__(256) k_lr_gemm(const double* __restrict__ Am,
 
 // blocked in-CTA triangular solve with a row-major lower factor L (Q x Q):
 // trans = 0: L z = b, trans = 1: L^T z = b; z overwrites b (shared memory).
+// The diagonal block's row (column) of each lane is loaded into registers before the
+// sweep, so a column step is one shuffle + one FMA; the off-diagonal update is one
+// thread per row (column) with a 32-term FMA chain instead of a warp reduction per row.
 __device__ void cta_trsv(const double* L, int Q, double* b, int trans) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nblk = (Q + 31) / 32;
   for (int bb = 0; bb < nblk; ++bb) {
     const int blk = trans ? (nblk - 1 - bb) : bb;
     const int c0 = blk * 32, nc = min(32, Q - c0);
     if (wid == 0) {
-      // reciprocal pivots first, then one shuffle + one FMA per column step
       double v = lane < nc ? b[c0 + lane] : 0.0;
       const double rl = lane < nc ? 1.0 / L[(c0 + lane) * Q + c0 + lane] : 0.0;
+      double lr[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        lr[j] = (lane < nc && j < nc) ? (trans ? L[(c0 + j) * Q + c0 + lane] : L[(c0 + lane) * Q + c0 + j])
+                                      : 0.0;
       if (!trans) {
-        for (int j = 0; j < nc; ++j) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (j >= nc) break;
           const double zj = __shfl_sync(0xffffffffu, v * rl, j);
-          const double lij = (lane < nc) ? L[(c0 + lane) * Q + c0 + j] : 0.0;
-          const double nv = v - lij * zj;
+          const double nv = v - lr[j] * zj;
           v = (lane == j) ? zj : ((lane > j && lane < nc) ? nv : v);
         }
       } else {
-        for (int j = nc - 1; j >= 0; --j) {
+#pragma unroll
+        for (int j = 31; j >= 0; --j) {
+          if (j >= nc) continue;
           const double zj = __shfl_sync(0xffffffffu, v * rl, j);
-          const double lji = (lane < nc) ? L[(c0 + j) * Q + c0 + lane] : 0.0;
-          const double nv = v - lji * zj;
+          const double nv = v - lr[j] * zj;
           v = (lane == j) ? zj : (lane < j ? nv : v);
         }
       }
@@ -271,10 +280,10 @@ __device__ void cta_trsv(const double* L, int Q, double* b, int trans) {
     }
     __syncthreads();
     if (!trans) {
-      for (int r = c0 + nc + wid; r < Q; r += nw) {
-        double acc = lane < nc ? L[r * Q + c0 + lane] * b[c0 + lane] : 0.0;
-        acc = warp_sum(acc);
-        if (lane == 0) b[r] -= acc;
+      for (int r = c0 + nc + tid; r < Q; r += blockDim.x) {
+        double acc = 0.0;
+        for (int c = 0; c < nc; ++c) acc = fma(L[r * Q + c0 + c], b[c0 + c], acc);
+        b[r] -= acc;
       }
     } else {
       for (int c = tid; c < c0; c += blockDim.x) {
