@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
   constexpr int KT = TAB ? K : 1;
   __shared__ double tab[(1 << KT) * KT * KT + (1 << KT)];
   auto build_tab = [&](const double* C) {
+    if constexpr (!TAB) return;
     const int seg = lane / W;
     WNnls<K, W> f;
     f.sl = lane % W;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
       tl[rr] = a.tol_fixed >= 0.0 ? a.tol_fixed : 1e-12 * fmax(1.0, t);
     }
     __syncthreads();
-    if (TAB) {
+    if constexpr (TAB) {
       build_tab(gyy);
       __syncthreads();
       for (int rr = tid; rr < nr; rr += ST) {
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
     __syncthreads();
     S1STAMP(5);
     double ydx = 0.0, yy = 0.0, yr2 = 0.0, yfail = 0.0;  // per-thread (segment lane 0)
-    if (TAB) {
+    if constexpr (TAB) {
       build_tab(gxx);
       __syncthreads();
       for (int cc = tid; cc < nc; cc += ST) {
