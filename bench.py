@@ -417,12 +417,17 @@ def aux_c4(dev, peaks, peak_src):
         e3.synchronize()
         ipm_ms.append(e2.elapsed_time(e3))
     cold_ms, ipm_ms = ipm_ms
+    # steady state: iterations 3.. of the measured run from the per-iteration wall times
+    # (the first iterations of a run include the CUDA-graph captures, 1-2 per F buffer)
+    tr = [t[0] for t in r2.trace]
+    steady_ms = (1e3 * (tr[-1] - tr[2]) / (len(tr) - 3)) if len(tr) > 4 else None
     return {"workload": f"c4: {nsw} ANLS sweeps + {cfg.fixed_ipm} IPM iterations, dense fp64 "
                         f"n={cfg.n} m={cfg.m} k={cfg.k} (CPU reference: IPM infeasible, "
                         "~15 h/iteration per SURVEY.md section 6)",
             "anls_sweeps_per_s": nsw / (ms / 1e3), "ms_per_sweep": ms / nsw,
             "ipm_iters_per_s": r2.iters / (ipm_ms / 1e3), "ms_per_ipm_iter": ipm_ms / r2.iters,
             "ms_per_ipm_iter_first_run": cold_ms / r2.iters,
+            "ms_per_ipm_iter_steady": steady_ms,
             "roofline": {"bound": "hbm", "kernel": "nmfb_rowprod (ctb = M Y^T, X-update)",
                          "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": gbs / peaks["hbm_gbs"], "traffic": None,

@@ -115,6 +115,11 @@ int nmfb_stage1_stats(const double *Xo, const double *Xn, long nx, const double 
 /* tol[r] = 1e-12 max(1, ||c_r||_inf) for a product already reduced across ranks */
 int nmfb_row_tol(const double *c, long rows, long k, double *tol, void *stream);
 
+/* *acc = min(*acc, (tag << 40) | (i << 8) | st[i]) over the i with st[i] != 0 (acc
+ * initialised to all ones by the caller): the first failing rhs of the earliest tagged
+ * batch and its status code; tag < 2^24, len < 2^32. */
+int nmfb_first_failure_i8(const int8_t *st, long len, long tag, unsigned long long *acc,
+                          void *stream);
 /* *out = first index with st != 0, 0x7F7F7F7F when none (nnls status scan) */
 int nmfb_first_nonzero_i8(const int8_t *st, long len, int *out, void *stream);
 

@@ -28,6 +28,7 @@ SIGNATURES = {
     "nmfb_surface_back_substitute": [P, P, P, P, P, P, L, L, L, I, P, P],
     # production entries
     "nmfb_nnls_ftab_len": [L],
+    "nmfb_first_failure_i8": [P, L, L, P, P],
     "nmfb_stage1_set_prof": [P],
     "nmfb_blas_init": [P],
     "nmfb_set_mu_source": [P],

@@ -916,6 +916,38 @@ extern "C" int nmfb_row_tol(const double* c, long rows, long k, double* tol, voi
   return NMFB_OK;
 }
 
+// acc = min(acc, (tag << 40) | (i << 8) | st[i]) over the i with st[i] != 0: the first
+// failing rhs of the earliest tagged batch, with its status code (fixed-sweep stage 1
+// checks failures once at the end instead of synchronising every sweep)
+__global__ void k_first_failure_i8(const int8_t* __restrict__ st, long len, unsigned long long tag,
+                                   unsigned long long* __restrict__ acc) {
+  unsigned long long best = ~0ull;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (long)gridDim.x * blockDim.x) {
+    const int8_t v = st[i];
+    if (v != 0) {
+      const unsigned long long key = (tag << 40) | ((unsigned long long)i << 8) | (unsigned char)v;
+      best = key < best ? key : best;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t < best ? t : best;
+  }
+  if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(acc, best);
+}
+
+extern "C" int nmfb_first_failure_i8(const int8_t* st, long len, long tag, unsigned long long* acc,
+                                     void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (len <= 0) return NMFB_OK;
+  if (tag < 0 || tag >= (1L << 24) || len >= (1L << 32)) return NMFB_EINVAL;
+  ++g_nmfb_launches, k_first_failure_i8<<<nmfb_blocks(len, 256, 148 * 4), 256, 0, s>>>(
+      st, len, (unsigned long long)tag, acc);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
 // *out = first index with st != 0 (0x7F7F7F7F when none); out is set, not accumulated
 extern "C" int nmfb_first_nonzero_i8(const int8_t* st, long len, int* out, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;

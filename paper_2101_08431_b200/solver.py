@@ -282,6 +282,13 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
     if (cfg.persistent and not P.comm.active and nsweeps > 0
             and P.lib.nmfb_stage1_persist_supported(n, m, k)):
         return _stage1_persistent(P, X, Yt, pX, pY, Yn, stX, stY, have_carry, cfg, nsweeps, res, t0)
+    # fixed sweep count on one rank: no per-sweep host synchronisation -- the sweep
+    # statistics go to a device log and failures to one first-failure word, both read
+    # once at the end (the per-sweep readback cost ~5 % of a c4 sweep)
+    nosync = cfg.fixed_sweeps > 0 and not P.comm.active
+    if nosync:
+        slog = P.buf(nsweeps, 3)
+        fword = torch.full((1,), -1, dtype=torch.int64, device=P.dev)  # all ones
     for sweep in range(nsweeps):
         mode = 2 if (sweep > 0 or have_carry) else 0
         # X-update: C = Y^T, d = rows of M
@@ -301,6 +308,17 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
                 _p(tolY), 3 * k, m, k, _p(Yn), _p(pYn), _p(chY), _p(r2Y), _p(stY), None, None,
                 _p(P.ftab), P.ftab_len, s)
         ny = P.ny_local
+        if nosync:
+            P._call("nmfb_stage1_stats", _p(X), _p(Xn), n * k, _p(Yt), _p(Yn), m * k * ny,
+                    _p(r2Y), m * ny, _p(slog[sweep]), _p(P.rwork), P.rwork.numel(), s)
+            P._call("nmfb_first_failure_i8", _p(stX), n, 2 * sweep, _p(fword), s)
+            P._call("nmfb_first_failure_i8", _p(stY), m, 2 * sweep + 1, _p(fword), s)
+            X, Xn = Xn, X
+            Yt, Yn = Yn, Yt
+            pX, pXn = pXn, pX
+            pY, pYn = pYn, pY
+            res.sweeps = sweep + 1
+            continue
         P._call("nmfb_stage1_stats", _p(X), _p(Xn), n * k, _p(Yt), _p(Yn), m * k * ny, _p(r2Y),
                 m * ny, _p(P.dscal), _p(P.rwork), P.rwork.numel(), s)
         P._call("nmfb_first_nonzero_i8", _p(stX), n, _p(P.iscal[0:]), s)
@@ -326,6 +344,17 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
         if cfg.fixed_sweeps <= 0 and step <= cfg.eps_stol * (1.0 + nrm):
             res.converged = True
             break
+    if nosync and nsweeps > 0:
+        fw = int(fword.item()) & ((1 << 64) - 1)
+        if fw != (1 << 64) - 1:
+            tag, idx, code = fw >> 40, (fw >> 8) & 0xFFFFFFFF, fw & 0xFF
+            code = code - 256 if code >= 128 else code
+            raise status_error(code, idx, "update_Y" if tag & 1 else "update_X")
+        lg = slog.cpu().numpy()
+        t1 = time.perf_counter()
+        for i in range(nsweeps):
+            res.trace.append(((t1 - t0) * (i + 1) / nsweeps, 0.5 * float(lg[i, 2]),
+                              math.sqrt(float(lg[i, 0]))))
     res.seconds = time.perf_counter() - t0
     return X, Yt, pX, pY, res
 

@@ -252,3 +252,26 @@ def test_streaming_products_large(mods, shape, dt):
     tol = 1e-12 if dt == "f64" else 1e-5
     assert float((ctbX - refX).abs().max() / refX.abs().max()) < tol
     assert float((ctbY - refY).abs().max() / refY.abs().max()) < tol
+
+
+def test_stage1_fixed_sweeps_failure_reporting(mods):
+    """Fixed-sweep stage 1 checks failures once at the end (first failing sweep, rhs and
+    status code from one device word): it raises what the per-sweep checked loop raises,
+    for the same rhs.  A negative NNLS tolerance makes dropped indices re-enter until the
+    active-set change cap (status 1) trips."""
+    from paper_2101_08431_b200.errors import NmfStreamError
+
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = _instance(data, "c4", 600, 200)
+    k = X0.shape[1]
+    outcomes = []
+    for fixed in (3, 0):
+        P = solver.Problem(M, k)
+        cfg = Stage1Config(fixed_sweeps=fixed, max_sweeps=3, persistent=False, tol_kkt=-1.0)
+        try:
+            solver.run_stage1(P, P.to_dev(X0), P.to_dev(Y0.T), cfg)
+            outcomes.append(None)
+        except NmfStreamError as e:
+            outcomes.append((type(e).__name__, getattr(e, "rhs_index", None)))
+    assert outcomes[0] == outcomes[1], outcomes
+    assert outcomes[0] is not None, "expected an NNLS status failure"
