@@ -79,6 +79,18 @@ def test_stage1_parity_c4_full(mods):
     assert rel(Yt.cpu().numpy(), ro.Yt) < TOL_STAGE1
 
 
+def test_stage1_fp32_storage_c5_shape(mods):
+    """c5's k = 16 with fp32 storage at a larger slice (12000 x 3000): 3 sweeps through the
+    DMMA products on fp32 M and the k > 12 NNLS kernels vs the fp64 oracle on the rounded M."""
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = data.dense(12000, 3000, 16, 105)[:3]
+    M32 = M.astype(np.float32)
+    P = solver.Problem(M32, 16)
+    X, Yt, pX, pY, r = solver.run_stage1(P, P.to_dev(X0), P.to_dev(Y0.T), Stage1Config(fixed_sweeps=3))
+    ro = D.run_stage1(M32.astype(np.float64), X0, Y0.T.copy(), D.Stage1Config(fixed_sweeps=3))
+    assert rel(X.cpu().numpy(), ro.X) < 1e-4 and rel(Yt.cpu().numpy(), ro.Yt) < 1e-4
+
+
 def test_stage1_fp32_storage(mods):
     """c5-style fp32 M (fp64 accumulate/solve) vs the fp64 oracle on the rounded M: 1e-4."""
     data, solver, IpmParams, Stage1Config = mods
