@@ -138,7 +138,8 @@ def test_ipm_parity(mods, name, barrier, iters, eps, solve, resid):
     ("c1", "paper", 40, 1e-7, "graph"), ("c1", "balanced", 50, 1e-5, "graph"),
     ("c2", "balanced", 35, 1e-6, "graph"), ("c1", "balanced", 50, 1e-5, "eager"),
     ("c2", "balanced", 35, 1e-6, "persist-g16"), ("c2", "paper", 40, 1e-6, "persist-g148"),
-    ("c1", "balanced", 60, 1e-7, "persist-g7")])
+    ("c1", "balanced", 60, 1e-7, "persist-g7"), ("c1", "balanced", 60, 1e-7, "ggraph"),
+    ("c2", "paper", 40, 1e-6, "ggraph")])
 def test_ipm_parity_paths(mods, name, barrier, iters, eps, path):
     """The same Gauss-Newton iterations through each device path: the persistent
     cooperative loop (csrc/persist.cu, several grid sizes), the graph-replayed six
@@ -155,6 +156,8 @@ def test_ipm_parity_paths(mods, name, barrier, iters, eps, path):
         kw.update(persistent=False)
     elif path == "eager":
         kw.update(persistent=False, fused_small=False, use_graphs=False)
+    elif path == "ggraph":  # general pipeline replayed as graphs, mu read from device memory
+        kw.update(persistent=False, fused_small=False, use_graphs=True)
     else:
         kw.update(persist_grid=int(path.split("-g")[1]))
     eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(**kw))
@@ -287,3 +290,28 @@ def test_stage1_fixed_sweeps_failure_reporting(mods):
             outcomes.append((type(e).__name__, getattr(e, "rhs_index", None)))
     assert outcomes[0] == outcomes[1], outcomes
     assert outcomes[0] is not None, "expected an NNLS status failure"
+
+
+
+def test_general_graph_matches_eager_across_mu(mods):
+    """The general-path iteration graph reads the barrier value from device memory
+    (nmfb_set_mu_source at capture), so one graph per F buffer serves every mu: over
+    iterations that cross several outer (mu) updates it gives the eager pipeline's bits."""
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = _instance(data, "c1")
+    k = X0.shape[1]
+    ro = D.run_stage1(M, X0, Y0.T.copy())
+    outs = []
+    for graphs in (True, False):
+        P = solver.Problem(M, k)
+        X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), 1e-7)
+        eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho,
+                                IpmParams(fixed_iters=60, persistent=False, fused_small=False,
+                                          use_graphs=graphs))
+        outs.append((r.outer, r.armijo_t, eng.mu, eng.X.cpu().numpy(), eng.Yt.cpu().numpy(),
+                     len(eng.graphs)))
+    (o1, t1, mu1, X1, Y1, ng), (o2, t2, mu2, X2, Y2, _) = outs
+    assert o1 == o2 and o1 >= 2, "the run should cross outer (mu) updates"
+    assert ng <= 2, "one graph per F buffer"
+    assert t1 == t2 and mu1 == mu2
+    assert np.array_equal(X1, X2) and np.array_equal(Y1, Y2)
