@@ -52,3 +52,28 @@ def test_dense_cholesky_reports_failing_pivot(lib, N):
     assert lib.nmfb_dense_cholesky(d.data_ptr(), N, info.data_ptr(), s) == 0
     torch.cuda.synchronize()
     assert 0 <= int(info.item()) <= N // 2
+
+
+def test_first_failure_word(lib):
+    """nmfb_first_failure_i8 keeps the earliest (tag, index) failure and its status code
+    across several batches (the fixed-sweep stage-1 failure report)."""
+    import torch
+
+    s = torch.cuda.current_stream().cuda_stream
+    acc = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    st = torch.zeros(5000, dtype=torch.int8, device="cuda")
+    assert lib.nmfb_first_failure_i8(st.data_ptr(), 5000, 0, acc.data_ptr(), s) == 0
+    assert int(acc.item()) == -1  # nothing failed
+    st[4000] = 2
+    st[1234] = 1
+    assert lib.nmfb_first_failure_i8(st.data_ptr(), 5000, 7, acc.data_ptr(), s) == 0
+    st2 = torch.zeros(300, dtype=torch.int8, device="cuda")
+    st2[299] = 2
+    assert lib.nmfb_first_failure_i8(st2.data_ptr(), 300, 9, acc.data_ptr(), s) == 0
+    w = int(acc.item()) & ((1 << 64) - 1)
+    assert (w >> 40, (w >> 8) & 0xFFFFFFFF, w & 0xFF) == (7, 1234, 1)
+    st3 = torch.zeros(10, dtype=torch.int8, device="cuda")
+    st3[3] = 2
+    assert lib.nmfb_first_failure_i8(st3.data_ptr(), 10, 2, acc.data_ptr(), s) == 0
+    w = int(acc.item()) & ((1 << 64) - 1)
+    assert (w >> 40, (w >> 8) & 0xFFFFFFFF, w & 0xFF) == (2, 3, 2)
