@@ -424,7 +424,7 @@ __host__ __device__ inline WLayout wlayout(long G, long m, int K) {
 template <int K>
 __host__ __device__ inline long smem_doubles(long nrm, long m, bool with_m) {
   const long KK = K * (K + 1) / 2, N = m * K;
-  long d = 6 * N + m * KK + nrm * (10 * K + 2 * K * K + KK);  // + double-buffered factorization snapshots
+  long d = 4 * N + m * KK + nrm * (10 * K + 2 * K * K + KK);  // + double-buffered row-factor snapshots
   if (with_m) d += nrm * m;
   return d;
 }
@@ -475,8 +475,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
   // parity: the last step's factorization is committed to global memory once, at exit
   double* Lsb = gs + nrm * K;
   double* xsnap = Lsb + 2 * nrm * K * K;
-  double* Ysnap = xsnap + 2 * nrm * K;
-  double* As = Ysnap + 2 * N;
+  double* As = xsnap + 2 * nrm * K;
   double* rds = As + nrm * KK;  // 1 / L_i,pp of the row factors
   double* Ms = rds + nrm * K;   // own rows of M (when m_in_smem)
 
@@ -555,10 +554,7 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     STAMP(0);
     double* Ls = Lsb + (long)(it & 1) * nrm * K * K;
     {
-      double* ysn = Ysnap + (long)(it & 1) * N;
       double* xsn = xsnap + (long)(it & 1) * nrm * K;
-      #pragma unroll 1
-      for (long e = tid; e < N; e += PT) ysn[e] = Ys[e];
       #pragma unroll 1
       for (long e = tid; e < (long)nr * K; e += PT) xsn[e] = xs[e];
     }
@@ -730,6 +726,11 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
       fact_it = it - 1;
       break;
     }
+    // the factorization point's Y for the predictor (replicated: CTA 0 writes it; the
+    // row-side snapshots are double-buffered in shared memory and written at exit)
+    if (cta == 0)
+      #pragma unroll 1
+      for (long e = tid; e < N; e += PT) a.Ytf[e] = Ys[YI(e / K, e % K)];
 
     STAMP(3);
     // ---- Y side (replicated): rhs, D_j, t_j = D_j^{-1} rhs_j, D_j^{-1} packed
@@ -1321,11 +1322,6 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
     for (long e = tid; e < (long)nr * K * K; e += PT) a.L[r0 * K * K + e] = Lc[e];
     #pragma unroll 1
     for (long e = tid; e < (long)nr * K; e += PT) a.Xf[r0 * K + e] = xsn[e];
-    if (cta == 0) {
-      const double* ysn = Ysnap + (long)(fact_it & 1) * N;
-      #pragma unroll 1
-      for (long e = tid; e < N; e += PT) a.Ytf[e] = ysn[YI(e / K, e % K)];
-    }
   }
   if (it > 0) {
     // F = X Y - M at the final point, with phase D's expression (phase D no longer
@@ -1368,7 +1364,7 @@ long p_smem_bytes(long n, long m, int G, bool with_m) {
   return smem_doubles<K>(nrm, m, with_m) * (long)sizeof(double);
 }
 
-constexpr long SMEM_CAP = 200 * 1024;  // dynamic part; the static part is < 16 KB
+constexpr long SMEM_CAP = 210 * 1024;  // dynamic part; static <= 15 KB, 227 KB per CTA in all
 
 int p_grid(long n) {
   long g = (n + 15) / 16;
