@@ -783,50 +783,64 @@ __global__ void __launch_bounds__(PT, 1) k_ipm_persist(PArgs a) {
       badD = (int)v[0];
     }
     STAMP(4);
-    // G = sum_j (y_j y_j^T) (x) D_j^{-1} (packed), u = U^T t
+    // G = sum_j (y_j y_j^T) (x) D_j^{-1} (packed), u = U^T t.  G is an outer product per
+    // column: warp w < GW owns two rows ab of G and forms all KK columns pq from one
+    // load of D_j^{-1} (KK words) and two y_j y_j^T products, so a column costs KK + 4
+    // shared-memory loads for 2 KK FMAs (one entry per warp and lane-strided columns
+    // cost three loads per FMA and made this pass shared-memory bound at m = 500);
+    // the other warps form u.
     {
-      constexpr int NE = KK * KK + Q, EPW = (NE + NW - 1) / NW;
-      int o1[EPW], o2[EPW], o3[EPW];
-      double sacc[EPW];
+      constexpr int GW = (KK + 1) / 2;
+      static_assert(GW < NW, "G rows need fewer warps than the CTA has");
+      if (wid < GW) {
+        const int ab0 = 2 * wid, ab1 = (2 * wid + 1 < KK) ? 2 * wid + 1 : 2 * wid;
+        const int a0 = ia[ab0], b0 = ic[ab0], a1 = ia[ab1], b1 = ic[ab1];
+        double acc[2 * KK];
 #pragma unroll
-      for (int i = 0; i < EPW; ++i) {
-        const int e = wid + NW * i;
-        sacc[i] = 0.0;
-        if (e < KK * KK) {
-          const int ab = e / KK, pq = e % KK;
-          o1[i] = ia[ab];
-          o2[i] = ic[ab];
-          o3[i] = pq;
-        } else {
-          const int qq = e - KK * KK;
-          o1[i] = qq / K;
-          o2[i] = qq % K;
-          o3[i] = -1;
-        }
-      }
-      #pragma unroll 1
-      for (long j = lane; j < m; j += 32) {
+        for (int q = 0; q < 2 * KK; ++q) acc[q] = 0.0;
+        #pragma unroll 1
+        for (long j = lane; j < m; j += 32) {
+          const double yy0 = Ys[YI(j, a0)] * Ys[YI(j, b0)];
+          const double yy1 = Ys[YI(j, a1)] * Ys[YI(j, b1)];
 #pragma unroll
-        for (int i = 0; i < EPW; ++i) {
-          const int e = wid + NW * i;
-          if (e < KK * KK) {
-            const double yy = Ys[YI(j, o1[i])] * Ys[YI(j, o2[i])];
-            sacc[i] = fma(yy, dinv[DI(j, o3[i])], sacc[i]);
-          } else if (e < NE) {
-            sacc[i] = fma(Ys[YI(j, o1[i])], Ts[YI(j, o2[i])], sacc[i]);
+          for (int pq = 0; pq < KK; ++pq) {
+            const double dv = dinv[DI(j, pq)];
+            acc[pq] = fma(yy0, dv, acc[pq]);
+            acc[KK + pq] = fma(yy1, dv, acc[KK + pq]);
           }
         }
-      }
-      warp_reduce_multi<EPW, 0, 0>(sacc);
+        using WH = WarpHalve<2 * KK, 0, 0>;
+        const double tot = WH::run(acc);
+        constexpr int SH = 5 - WH::LG;
+        const int q = lane >> SH;
+        if ((lane & ((1 << SH) - 1)) == 0 && q < 2 * KK) {
+          const int ab = q < KK ? ab0 : ab1;
+          if (q < KK || 2 * wid + 1 < KK) T1[ab * KK + (q % KK)] = tot;
+        }
+      } else {
+        constexpr int NUW = NW - GW, EPU = (Q + NUW - 1) / NUW;
+        double sacc[EPU];
+        int o1[EPU], o2[EPU];
 #pragma unroll
-      for (int i = 0; i < EPW; ++i) {
-        const int e = wid + NW * i;
-        const double v = sacc[i];
+        for (int i2 = 0; i2 < EPU; ++i2) {
+          const int e = (wid - GW) + NUW * i2;
+          sacc[i2] = 0.0;
+          o1[i2] = (e < Q ? e : 0) / K;
+          o2[i2] = (e < Q ? e : 0) % K;
+        }
+        #pragma unroll 1
+        for (long j = lane; j < m; j += 32) {
+#pragma unroll
+          for (int i2 = 0; i2 < EPU; ++i2)
+            sacc[i2] = fma(Ys[YI(j, o1[i2])], Ts[YI(j, o2[i2])], sacc[i2]);
+        }
+        warp_reduce_multi<EPU, 0, 0>(sacc);
         if (lane == 0) {
-          if (e < KK * KK)
-            T1[e] = v;
-          else if (e < NE)
-            u[e - KK * KK] = v;
+#pragma unroll
+          for (int i2 = 0; i2 < EPU; ++i2) {
+            const int e = (wid - GW) + NUW * i2;
+            if (e < Q) u[e] = sacc[i2];
+          }
         }
       }
     }
