@@ -292,7 +292,7 @@ unsigned long long nmfb_launch_count(void);
  * / 2 Armijo stall].  fcodes = [R1 failing row, capacitance info, D failing col]
  * (host initialises 0x7F7F7F7F, -1, 0x7F7F7F7F).  grid = 0: automatic.  prof
  * (optional, may be NULL): 16 clock64 stamps per iteration from CTA 0 (phase timing). */
-int nmfb_persist_supported(long n, long m, long k, int grid);
+int nmfb_persist_supported(long n, long m, long k, int grid, int m_is_f32);
 long nmfb_persist_work_len(long n, long m, long k, int grid);
 int nmfb_ipm_persist(const void *M, int m_is_f32, long n, long m, long k, double *X, double *R,
                      double *gX, double *Yt, double *S, double *gY, double *Fout, double *L,
@@ -323,7 +323,7 @@ int nmfb_grams(int count, const double *A0, const double *B0, double *O0, const 
  * 1e-12 max(1, ||ctb||_inf).  first_mode: 0 cold, 2 seeded from pX / pY.  fixed: run
  * exactly max_sweeps.  logv: per sweep [0.5 sum r2, step, norm, -]; status (device
  * int[3]) = [sweeps, converged, failed]. */
-int nmfb_stage1_persist_supported(long n, long m, long k);
+int nmfb_stage1_persist_supported(long n, long m, long k, int m_is_f32);
 /* profiling hook: per-sweep phase clocks of CTA 0 (prof[sweep * 16 + i]); NULL disables */
 int nmfb_stage1_set_prof(long long *prof);
 long nmfb_stage1_persist_work_len(long n, long m, long k);

@@ -71,9 +71,9 @@ SIGNATURES = {
     "nmfb_ffree_fsq": [P, D, P, P, L, P, P, P],
     "nmfb_ffree_quartic": [P, P, P, P, P, P, P, P, P, L, P, P],
     "nmfb_small_supported": [L, L, L],
-    "nmfb_persist_supported": [L, L, L, I],
+    "nmfb_persist_supported": [L, L, L, I, I],
     "nmfb_grams_work_len": [L, L, L],
-    "nmfb_stage1_persist_supported": [L, L, L],
+    "nmfb_stage1_persist_supported": [L, L, L, I],
     "nmfb_stage1_persist_work_len": [L, L, L],
     "nmfb_stage1_persist": [P, I, L, L, L] + [P] * 10 + [D, I, I, I, D, P, P, P, P],
     "nmfb_grams": [I] + [P] * 12 + [L, L, P, L, P],

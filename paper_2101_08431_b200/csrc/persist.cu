@@ -1380,9 +1380,24 @@ long p_smem_bytes(long n, long m, int G, bool with_m) {
 
 constexpr long SMEM_CAP = 210 * 1024;  // dynamic part; static <= 15 KB, 227 KB per CTA in all
 
+constexpr int P_MAX_GRID = 160;  // 5 lanes x 32 CTAs in reduce_entries, pbar length
+
+// one CTA per SM (the cooperative launch needs every CTA resident)
+int p_max_grid() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1)
+      sms = 1;
+  }
+  return sms < P_MAX_GRID ? sms : P_MAX_GRID;
+}
+
 int p_grid(long n) {
   long g = (n + 15) / 16;
-  if (g > 148) g = 148;
+  const int cap = p_max_grid();
+  if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
 }
@@ -1395,12 +1410,16 @@ int p_grid(long n) {
     default: return 0;                  \
   }
 
-extern "C" int nmfb_persist_supported(long n, long m, long k, int grid) {
+extern "C" int nmfb_persist_supported(long n, long m, long k, int grid, int m_is_f32) {
   if (k < 1 || k > 4 || m < 1 || n < 1 || m * k > 2048) return 0;
+  // the fixed-order partial reductions sum at most P_MAX_GRID CTAs and every CTA must
+  // be co-resident (one per SM)
+  if (grid < 0 || grid > p_max_grid()) return 0;
   const int G = grid > 0 ? grid : p_grid(n);
   if ((n + G - 1) / G > 4096) return 0;
+  // fp32 M is only read from shared memory (no fp32 global path): it must fit
 #define CASE(KK_) \
-  case KK_: return p_smem_bytes<KK_>(n, m, G, false) <= SMEM_CAP ? 1 : 0;
+  case KK_: return p_smem_bytes<KK_>(n, m, G, m_is_f32 != 0) <= SMEM_CAP ? 1 : 0;
   NMFB_PK(k, CASE)
 #undef CASE
 }
@@ -1422,7 +1441,7 @@ extern "C" int nmfb_ipm_persist(const void* M, int m_is_f32, long n, long m, lon
                                 double* logv, int* status, double* work, unsigned int* bar,
                                 int grid, long long* prof, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (!nmfb_persist_supported(n, m, k, grid)) return NMFB_EUNSUPPORTED;
+  if (!nmfb_persist_supported(n, m, k, grid, m_is_f32)) return NMFB_EUNSUPPORTED;
   if (max_iters < 1) return NMFB_EINVAL;
   const int G = grid > 0 ? grid : p_grid(n);
   PArgs a;

@@ -366,8 +366,15 @@ __global__ void __launch_bounds__(ST, 1) k_stage1_persist(S1Args a) {
 }
 
 int s1_grid(long n) {
+  static int sms = 0;  // one CTA per SM (cooperative launch)
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1)
+      sms = 1;
+  }
   long g = (n + 15) / 16;
-  if (g > 148) g = 148;
+  if (g > sms) g = sms;
   return g < 1 ? 1 : (int)g;
 }
 
@@ -390,12 +397,13 @@ constexpr long S1_SMEM_CAP = 200 * 1024;
     default: return NMFB_EUNSUPPORTED;                                                           \
   }
 
-extern "C" int nmfb_stage1_persist_supported(long n, long m, long k) {
+extern "C" int nmfb_stage1_persist_supported(long n, long m, long k, int m_is_f32) {
   if (k < 1 || k > 8 || n < 1 || m < 1 || m * k > 4096) return 0;
   const int G = s1_grid(n);
   if ((n + G - 1) / G > 1024) return 0;
+  // fp32 M is only read from shared memory (no fp32 global path): it must fit
 #define CASE(KK_, WW_) \
-  case KK_: return s1_smem<KK_>(n, m, G, false) <= S1_SMEM_CAP ? 1 : 0;
+  case KK_: return s1_smem<KK_>(n, m, G, m_is_f32 != 0) <= S1_SMEM_CAP ? 1 : 0;
   NMFB_S1_K(k, CASE)
 #undef CASE
 }
@@ -412,7 +420,7 @@ extern "C" int nmfb_stage1_persist(const void* M, int m_is_f32, long n, long m, 
                                    int fixed, double eps_stol, double* logv, int* status,
                                    double* work, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (!nmfb_stage1_persist_supported(n, m, k)) return NMFB_EUNSUPPORTED;
+  if (!nmfb_stage1_persist_supported(n, m, k, m_is_f32)) return NMFB_EUNSUPPORTED;
   if (max_sweeps < 1) return NMFB_EINVAL;
   const int G = s1_grid(n);
   S1Args a;

@@ -17,7 +17,7 @@
 //   rhs_reduce           :146-178  one thread per column j
 //   back_substitute      :181-224  one thread per row i
 //
-// The production IPM path (ipm.cu / schur.cu) uses re-associated O(n k^4)
+// The production IPM path (ipm.cu, lowrank.cu, persist.cu) uses re-associated O(n k^4)
 // formulations of the same quantities; these kernels are the parity surface.
 #include "common.cuh"
 #include "nmfb200.h"

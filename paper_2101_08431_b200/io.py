@@ -37,11 +37,11 @@ def load_matrix(path, format: str = "csv", header: bool = False) -> np.ndarray:
                 try:
                     vals.append(float(c))
                 except ValueError:
-                    raise ParseError(f"not a decimal real: {c!r}", ln, col) from None
+                    raise ParseError(f"not a decimal real: {c!r} (line {ln}, column {col})", ln, col) from None
             if width is None:
                 width = len(vals)
             elif len(vals) != width:
-                raise RaggedRows(f"expected {width} values, found {len(vals)}", ln)
+                raise RaggedRows(f"expected {width} values, found {len(vals)} (line {ln})", ln)
             rows.append(vals)
     if not rows:
         raise ParseError("empty matrix file", 1, 1)

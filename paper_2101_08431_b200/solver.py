@@ -280,7 +280,7 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
     nsweeps = cfg.fixed_sweeps if cfg.fixed_sweeps > 0 else cfg.max_sweeps
     s = P.stream
     if (cfg.persistent and not P.comm.active and nsweeps > 0
-            and P.lib.nmfb_stage1_persist_supported(n, m, k)):
+            and P.lib.nmfb_stage1_persist_supported(n, m, k, int(P.f32))):
         return _stage1_persistent(P, X, Yt, pX, pY, Yn, stX, stY, have_carry, cfg, nsweeps, res, t0)
     # fixed sweep count on one rank: no per-sweep host synchronisation -- the sweep
     # statistics go to a device log and failures to one first-failure word, both read
@@ -455,7 +455,7 @@ class IpmEngine:
             self.tickets = torch.zeros(8, dtype=torch.int32, device=P.dev)
         # persistent inner loop (csrc/persist.cu): one cooperative launch per inner loop
         self.persist = self.small and p.persistent and \
-            bool(P.lib.nmfb_persist_supported(n, m, k, p.persist_grid))
+            bool(P.lib.nmfb_persist_supported(n, m, k, p.persist_grid, int(P.f32)))
         if self.persist:
             self.pwork = b(P.lib.nmfb_persist_work_len(n, m, k, p.persist_grid))
             self.pbar = torch.zeros(160, dtype=torch.int32, device=P.dev)  # barrier flags
