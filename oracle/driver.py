@@ -31,6 +31,18 @@ Frozen open semantics (DESIGN.md "Frozen semantics" lists the same items):
    test E(.;mu) <= mu can be unreachable once mu ~ 1e-15.
 9. Barrier weights: default "balanced" (n w_x = m w_y, = the single mu when n = m);
    "paper" is the literal single-mu reading (see barrier_weights).
+10. Hessian switch: default "inertia".  Algorithm 3 sets flag = (sigma <= sigma_c) after
+   every outer iteration; with the flag set the direction uses the full coupling C
+   (PAPER.md:564-590).  "paper": a full-C direction that is not positive definite or not
+   a descent direction clears the flag and the iteration uses C-bar (Alg. 3 literally).
+   "inertia": such a direction is recomputed with both diagonal blocks shifted,
+   rho -> rho + delta, delta = 0, then delta_last / 3 (or rho when there is no previous
+   shift), growing 4x until the Schur matrix factors and the direction is descent
+   (INERTIA_MAX_TRIES attempts, then the C-bar fallback of "paper").  The literal rule
+   stalls on the BASELINE peak instances: along the rotational ambiguity of the
+   factorisation the residual coupling dominates the curvature, the Gauss-Newton
+   direction overshoots (Armijo t = 6-7 for hundreds of iterations) and the full C is
+   indefinite there ("Reaching the tolerance").
 """
 from __future__ import annotations
 
@@ -43,6 +55,7 @@ from scipy.linalg import solve_triangular
 
 from oracle import kernels as _KC
 from oracle import kernels_np as _KN
+from oracle import lowrank as _LR
 
 
 class _Kernels:
@@ -95,7 +108,9 @@ class IpmParams:
     max_backtracks: int = 60
     fixed_iters: int = 0  # >0: run exactly this many inner iterations
     barrier: str = "balanced"  # default; "paper": one mu (PAPER Eq. 4, literal); see barrier_weights
-    schur_solver: str = "dense"  # the oracle always factors the dense mk x mk matrix
+    hessian: str = "inertia"  # "inertia" (default) | "paper" (frozen semantics 10)
+    schur_solver: str = "dense"  # "dense" mk x mk Cholesky | "lowrank" (oracle.lowrank, GN only)
+    residual: str = "dense"  # "dense" (form F) | "free" (oracle.lowrank products; GN only)
 
 
 @dataclass
@@ -139,6 +154,9 @@ def gradients(X, Yt, M, comm=None):
     """graX = vec(Y F^T) -> (n,k) = F Y^T; graY = vec(X^T F) -> (m,k)."""
     F = X @ Yt.T - M
     return F, F @ Yt, _red(comm, F.T @ X)
+
+
+_gradients = gradients
 
 
 def kkt_error(X, Yt, R, S, graX, graY, mu, wx=1.0, wy=1.0, comm=None):
@@ -414,6 +432,34 @@ def _nudge(new, old, tau):
     return new
 
 
+INERTIA_GROW = 4.0
+INERTIA_SHRINK = 3.0
+INERTIA_MAX_TRIES = 40
+
+
+def full_direction(M, st: IpmState, F, gX, gY, wx, wy, p: IpmParams, delta_last, comm=None):
+    """Full-coupling direction under frozen semantics 10.
+
+    Returns (out, delta): out is newton_direction's tuple, or None when the full
+    coupling is rejected ("paper": first failure; "inertia": every shift failed)."""
+    rho0 = st.rho
+    delta = 0.0
+    tries = 1 if p.hessian == "paper" else INERTIA_MAX_TRIES
+    try:
+        for _ in range(tries):
+            st.rho = rho0 + delta
+            out = newton_direction(M, st, F, gX, gY, True, wx, wy, comm)
+            if out is not None and out[4] < 0.0:
+                return out, delta
+            if delta > 0.0:
+                delta *= INERTIA_GROW
+            else:
+                delta = delta_last / INERTIA_SHRINK if delta_last > 0.0 else rho0
+    finally:
+        st.rho = rho0
+    return None, delta_last
+
+
 @dataclass
 class IpmResult:
     state: IpmState
@@ -424,6 +470,7 @@ class IpmResult:
     trace: list = field(default_factory=list)
     armijo_t: list = field(default_factory=list)
     flags: list = field(default_factory=list)
+    deltas: list = field(default_factory=list)  # inertia shift of each full-coupling iteration
     seconds: float = 0.0
 
 
@@ -448,10 +495,62 @@ def predictor_sigma(st: IpmState, gX, gY, fact: Factorization, p: IpmParams, com
     return min((mu_aff / mu_bar) ** 3, p.sigma_cap)
 
 
+def predictor_sigma_lowrank(st: IpmState, gX, gY, fac, p: IpmParams, comm=None):
+    """predictor_sigma with the rank-k^2 factorization (same Eqs. 7-8)."""
+    X, Yt, R, S = st.X, st.Yt, st.R, st.S
+    n, k = X.shape
+    m = Yt.shape[0]
+    dx, dy, dr, ds, _ = _LR.solve(fac, X, Yt, R, S, gX, gY, 0.0, 0.0, lambda a: _red(comm, a))
+    a1 = _ftb2(X, dx, Yt, dy, 1.0, comm)
+    a2 = _ftb2(R, dr, S, ds, 1.0, comm)
+    nk = int(_red(comm, float(n))) * k + m * k
+    xs = _red(comm, np.array([np.vdot(X + a1 * dx, R + a2 * dr), np.vdot(X, R)]))
+    mu_aff = (float(xs[0]) + float(np.vdot(Yt + a1 * dy, S + a2 * ds))) / nk
+    mu_bar = (float(xs[1]) + float(np.vdot(Yt, S))) / nk
+    return min((mu_aff / mu_bar) ** 3, p.sigma_cap)
+
+
+def _gn_direction(M, st, F, gX, gY, wx, wy, p, comm):
+    """Gauss-Newton direction: dense Schur system, or the rank-k^2 identity."""
+    if p.schur_solver != "lowrank":
+        return newton_direction(M, st, F, gX, gY, False, wx, wy, comm)
+    red = lambda a: _red(comm, a)  # noqa: E731
+    try:
+        fac = _LR.factor(st.X, st.Yt, st.R, st.S, st.rho, red)
+    except _LR.NotPD as e:
+        raise OracleError(f"NotPositiveDefinite (low-rank Gauss-Newton system: {e})") from None
+    dx, dy, dr, ds, gtp = _LR.solve(fac, st.X, st.Yt, st.R, st.S, gX, gY, wx * st.mu,
+                                    wy * st.mu, red)
+    return dx, dy, dr, ds, gtp, fac
+
+
 def run_ipm(M, st: IpmState, p: IpmParams = None, comm=None):
-    """SPEC.md:337 run_ipm: Algorithm 2 nested loops + Algorithm 3 switch."""
+    """SPEC.md:337 run_ipm: Algorithm 2 nested loops + Algorithm 3 switch.
+
+    ``p.residual == "free"`` / ``p.schur_solver == "lowrank"``: the same iteration with
+    the residual-free products and the rank-k^2 Schur identity of ``oracle.lowrank``
+    (instances whose F or dense Schur matrix does not fit; Gauss-Newton coupling only,
+    as on the device)."""
     p = p or IpmParams()
     t0 = time.perf_counter()
+    free = p.residual == "free"
+    red = lambda a: _red(comm, a)  # noqa: E731
+    Mn2 = red(float(np.vdot(M, M))) if free else 0.0
+
+    def gradients(X, Yt, M, comm):  # noqa: F811  (residual-free or dense)
+        if free:
+            fsq, gX_, gY_ = _LR.gradients_free(X, Yt, M, Mn2, red)
+            return fsq, gX_, gY_
+        return _gradients(X, Yt, M, comm)
+
+    def fnorm2(F):
+        return F if free else red(float(np.vdot(F, F)))
+
+    def quartic(X, Yt, dX, dYt, gX, gY):
+        if free:
+            return _LR.quartic_free(X, Yt, dX, dYt, gX, gY, M, red)
+        return quartic_coeffs(X, Yt, dX, dYt, M, comm)
+
     F, gX, gY = gradients(st.X, st.Yt, M, comm)
     E0 = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0, comm=comm)
     res = IpmResult(st, 0, 0, False, E0)
@@ -459,6 +558,7 @@ def run_ipm(M, st: IpmState, p: IpmParams = None, comm=None):
     tol = 0.0 if p.fixed_iters > 0 else p.eps_tol
     fact = None
     e_zero = E0
+    delta_last = 0.0
     wx, wy = barrier_weights(int(_red(comm, float(st.X.shape[0]))), st.Yt.shape[0], p.barrier)
     while e_zero > tol and res.iters < cap:
         eps_mu = st.mu
@@ -468,19 +568,20 @@ def run_ipm(M, st: IpmState, p: IpmParams = None, comm=None):
                and e_zero > tol and res.iters < cap):
             out = None
             used_full = False
-            if st.flag:
-                out = newton_direction(M, st, F, gX, gY, True, wx, wy, comm)
-                if out is None or out[4] >= 0.0:
+            if st.flag and not free:
+                out, delta = full_direction(M, st, F, gX, gY, wx, wy, p, delta_last, comm)
+                if out is None:
                     st.flag = False
-                    out = None
                 else:
                     used_full = True
+                    delta_last = delta
+                    res.deltas.append(delta)
             if out is None:
-                out = newton_direction(M, st, F, gX, gY, False, wx, wy, comm)
+                out = _gn_direction(M, st, F, gX, gY, wx, wy, p, comm)
             dx, dy, dr, ds, gtp, fact = out
             a1max = _ftb2(st.X, dx, st.Yt, dy, p.tau, comm)
             a2max = _ftb2(st.R, dr, st.S, ds, p.tau, comm)
-            coef = quartic_coeffs(st.X, st.Yt, dx, dy, M, comm)
+            coef = quartic(st.X, st.Yt, dx, dy, gX, gY)
             t = 0
             while True:
                 a1 = a1max / (2.0 ** t)
@@ -498,17 +599,20 @@ def run_ipm(M, st: IpmState, p: IpmParams = None, comm=None):
             res.flags.append(used_full)
             F, gX, gY = gradients(st.X, st.Yt, M, comm)
             e_zero = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0, comm=comm)
-            res.trace.append((time.perf_counter() - t0, 0.5 * _red(comm, float(np.vdot(F, F))),
-                              e_zero, st.mu, a1, a2max, t))
+            res.trace.append((time.perf_counter() - t0, 0.5 * fnorm2(F), e_zero, st.mu, a1,
+                              a2max, t))
         res.outer += 1
         e_zero = kkt_error(st.X, st.Yt, st.R, st.S, gX, gY, 0.0, comm=comm)
         if e_zero <= tol or res.iters >= cap:
             break
         if fact is None:  # no Newton solve yet: factor at the current point
-            fact = newton_direction(M, st, F, gX, gY, False, wx, wy, comm)[5]
-        sigma = predictor_sigma(st, gX, gY, fact, p, comm)
+            fact = _gn_direction(M, st, F, gX, gY, wx, wy, p, comm)[5]
+        if isinstance(fact, _LR.LowrankFactor):
+            sigma = predictor_sigma_lowrank(st, gX, gY, fact, p, comm)
+        else:
+            sigma = predictor_sigma(st, gX, gY, fact, p, comm)
         st.mu = sigma * st.mu
-        st.flag = sigma <= p.sigma_c
+        st.flag = sigma <= p.sigma_c and not free
     res.converged = e_zero <= tol
     res.state = st
     res.seconds = time.perf_counter() - t0

@@ -34,6 +34,10 @@ class IpmParams:
     max_backtracks: int = 60
     fixed_iters: int = 0  # > 0: exactly this many inner iterations (configs c4/c5)
     barrier: str = "balanced"  # "balanced" (default, meets SPEC acceptance 5-7) | "paper" (literal single mu)
+    # full-coupling directions while the Algorithm-3 flag is set: "inertia" (default) shifts
+    # rho until the Schur matrix factors and the direction is descent; "paper" clears the
+    # flag on the first failure (DESIGN.md frozen semantics 10)
+    hessian: str = "inertia"
     schur_solver: str = "lowrank"  # Gauss-Newton reduced system: "lowrank" (exact, rank k^2) | "dense"
     use_graphs: bool = True  # replay each Gauss-Newton iteration as a captured CUDA graph
     fused_small: bool = True  # fused 6-kernel iteration when k <= 4 and m k <= 2048 (csrc/small.cu)
@@ -72,6 +76,7 @@ class IpmResult:
     trace: list = field(default_factory=list)  # (seconds, objective, E0, mu, a1, a2, t)
     armijo_t: list = field(default_factory=list)
     flags: list = field(default_factory=list)
+    deltas: list = field(default_factory=list)  # inertia shift of each full-coupling iteration
     seconds: float = 0.0
     dense_fallbacks: int = 0  # GN iterations re-solved densely after a low-rank PD failure
 

@@ -28,6 +28,10 @@ from .errors import (DegenerateFactor, LineSearchStall, NativeLibraryError,
 
 _NONE = 0x7F7F7F7F
 NTRIALS = 61  # t = 0..60
+# inertia shift of the full-coupling direction (frozen semantics 10, oracle/driver.py)
+INERTIA_GROW = 4.0
+INERTIA_SHRINK = 3.0
+INERTIA_MAX_TRIES = 40
 
 
 def _p(t):
@@ -682,7 +686,7 @@ class IpmEngine:
                 _p(self.lrwork), self.m, self.k, _p(rhs), _p(dY), _p(self.uvec), _p(self.wvec),
                 _p(P.cwork), P.cwork.numel(), P.stream)
 
-    def direction(self, full, force_dense=False):
+    def direction(self, full, force_dense=False, rho=None):
         """Newton direction; scalars land in dscal[4:7], codes in iscal[2:4].
 
         Gauss-Newton coupling: exact low-rank solve of the reduced system
@@ -693,11 +697,12 @@ class IpmEngine:
         n, m, k, N, s = self.n, self.m, self.k, self.N, P.stream
         mux, muy = self.wx * self.mu, self.wy * self.mu
         X, Yt, F = self.X, self.Yt, self.Fcur
+        rho = self.rho if rho is None else rho  # rho + inertia shift (frozen semantics 10)
         if not self.ffree:  # residual-free: YY^T and X^T X come from the refresh at this point
             P.colprod(Yt, m, k, Yt, k, self.GY)
             P.colprod(X, n, k, X, k, self.XtX, reduce=True)
         dense = full or self.dense_gn or force_dense
-        P._call("nmfb_r1_factor", _p(self.GY), _p(X), _p(self.R), _p(self.gX), mux, self.rho, n,
+        P._call("nmfb_r1_factor", _p(self.GY), _p(X), _p(self.R), _p(self.gX), mux, rho, n,
                 k, _p(self.L), _p(self.h), _p(self.g), _p(self.Apk), _p(self.XXpk),
                 _p(P.iscal[2:]), s)
         self.comm.min_(P.iscal[2:3])
@@ -720,7 +725,7 @@ class IpmEngine:
         if dense:
             self._ensure_dense()
             P._call("nmfb_schur_assemble", _p(Yt), _p(self.S), m, k, _p(self.Z), _p(self.XtX),
-                    self.rho, _p(W), _p(self.A), s)
+                    rho, _p(W), _p(self.A), s)
             if full:
                 if self.comm.active and not self.comm.root:
                     self.A.zero_()  # rank 0 carries the replicated part, others only term 4
@@ -733,7 +738,7 @@ class IpmEngine:
             dY.copy_(self.rhs.view(m, k))
             P._call("nmfb_dense_solve", _p(self.A), N, _p(dY), s)
         else:
-            P._call("nmfb_d_factor", _p(self.XtX), _p(Yt), _p(self.S), self.rho, m, k,
+            P._call("nmfb_d_factor", _p(self.XtX), _p(Yt), _p(self.S), rho, m, k,
                     _p(self.LD), _p(self.Dinvpk), _p(self.YYpk), _p(P.iscal[4:]), s)
             P._call("nmfb_atb", _p(self.YYpk), m, self.kk, _p(self.Dinvpk), self.kk, _p(self.Gpk),
                     _p(self.awork), self.awork.numel(), s)
@@ -873,6 +878,7 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
     tol = 0.0 if p.fixed_iters > 0 else p.eps_tol
     e_mu, e_zero, fsq, sums = eng.refresh()
     res = IpmResult(0, 0, False, e_zero, eng.mu, False)
+    delta_last = 0.0
     n, m, k = P.n, P.m, P.k
     while e_zero > tol and res.iters < cap:
         eps_mu = eng.mu
@@ -880,13 +886,24 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
             used_full = False
             ok = False
             if eng.flag:
-                dY = eng.direction(True)
-                eng.armijo_launch(dY)
-                v, iv = P.readback(32 + 2 * NTRIALS, 4)
-                if int(iv[2]) != _NONE:
-                    raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
-                if int(iv[3]) < 0 and v[4] < 0.0:
-                    ok, used_full = True, True
+                # full coupling C; frozen semantics 10: "paper" clears the
+                # flag on the first non-PD / non-descent direction, "inertia" shifts rho
+                delta = 0.0
+                for _ in range(1 if p.hessian == "paper" else INERTIA_MAX_TRIES):
+                    dY = eng.direction(True, rho=eng.rho + delta)
+                    v, iv = P.readback(9, 4)
+                    if int(iv[2]) != _NONE:
+                        raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
+                    if int(iv[3]) < 0 and v[4] < 0.0:
+                        ok, used_full = True, True
+                        break
+                    delta = (delta * INERTIA_GROW if delta > 0.0 else
+                             (delta_last / INERTIA_SHRINK if delta_last > 0.0 else eng.rho))
+                if ok:
+                    delta_last = delta
+                    res.deltas.append(delta)
+                    eng.armijo_launch(dY)
+                    v, iv = P.readback(32 + 2 * NTRIALS, 4)
                     eng.remember_factorization(True)
                 else:
                     eng.flag = False
