@@ -146,25 +146,26 @@ def cpu_step(M, X0, Y0, eps_abs, sweeps, ipm_iters):
     return r1.sweeps + r2.iters, t2 - t0, t1 - t0, t2 - t1
 
 
-def cpu_reference_formulation(M, X0, Y0, eps_abs, rows=40, mk_chol=6000):
-    """The reference's literal stage-2 cost at c4, extrapolated from a timed row slice:
-    GN schur_reduce (NumPy backend, _kernels_numpy.py:50-94) over ``rows`` rows scaled
-    to n, and a dense Cholesky of order ``mk_chol`` scaled (N/mk_chol)^3 to N = m k."""
+def cpu_reference_formulation(M, X0, Y0, rows=200, m_s=400, mk_chol=6000):
+    """The reference's literal stage-2 cost at c4, extrapolated from timed slices:
+    GN schur_reduce (NumPy backend, _kernels_numpy.py:50-94; O(n m^2 k^2), S is allocated
+    per call) on ``rows`` rows x ``m_s`` columns scaled by (n/rows)(m/m_s)^2, and a dense
+    Cholesky of order ``mk_chol`` scaled by (m k / mk_chol)^3."""
     from oracle import driver as D
     from oracle import kernels_np as KN
 
     n, k = X0.shape
     m = Y0.shape[1]
     X = np.maximum(X0[:rows], 1e-3)
-    Yt = np.ascontiguousarray(Y0.T)
+    Yt = np.ascontiguousarray(Y0[:, :m_s].T)
     R = np.full_like(X, 1e-2)
     blocks = (Yt.T @ Yt)[None] + np.einsum("ip,pq->ipq", R / X, np.eye(k))
     L, _ = D.K.block_cholesky(blocks)
     h = np.ones((rows, k))
-    F = X @ Yt.T - M[:rows]
+    F = X @ Yt.T - M[:rows, :m_s]
     t = time.perf_counter()
     KN.schur_reduce(X, Yt, L, h, F, False)
-    t_schur = (time.perf_counter() - t) * n / rows
+    t_schur = (time.perf_counter() - t) * (n / rows) * (m / m_s) ** 2
     a = np.random.default_rng(0).standard_normal((mk_chol, mk_chol))
     a = a @ a.T + mk_chol * np.eye(mk_chol)
     t = time.perf_counter()
@@ -172,9 +173,10 @@ def cpu_reference_formulation(M, X0, Y0, eps_abs, rows=40, mk_chol=6000):
     t_chol = (time.perf_counter() - t) * (m * k / mk_chol) ** 3
     return {"seconds_per_ipm_iteration": t_schur + t_chol, "schur_reduce_s": t_schur,
             "dense_cholesky_s": t_chol,
-            "how": f"schur_reduce (NumPy backend, GN) timed on {rows} of {n} rows and scaled by "
-                   f"n/{rows}; dense Cholesky timed at order {mk_chol}, scaled by "
-                   f"({m * k}/{mk_chol})^3; S itself would take {(m * k) ** 2 * 8 / 1e9:.0f} GB"}
+            "how": f"schur_reduce (NumPy backend, Gauss-Newton) timed on {rows} rows x {m_s} "
+                   f"columns and scaled by (n/{rows})(m/{m_s})^2; dense Cholesky timed at order "
+                   f"{mk_chol} and scaled by ({m * k}/{mk_chol})^3; S itself would need "
+                   f"{(m * k) ** 2 * 8 / 1e9:.0f} GB"}
 
 
 def run_reference(args):
@@ -195,7 +197,7 @@ def run_reference(args):
         u, s, a, b = cpu_step(M, X0, Y0, eps_abs, cfg.fixed_sweeps, cfg.fixed_ipm)
         units, secs, s1, s2 = units + u, secs + s, s1 + a, s2 + b
     value = units / secs
-    extra = cpu_reference_formulation(M, X0, Y0, eps_abs)
+    extra = cpu_reference_formulation(M, X0, Y0)
     sample = (f"{WORKLOAD}: the full step ({cfg.fixed_sweeps} sweeps + {cfg.fixed_ipm} IPM "
               "iterations) per step, oracle port: reference-pinned C NNLS kernels (1 thread), "
               "NumPy/BLAS products, stage 2 via the rank-k^2 Schur identity")

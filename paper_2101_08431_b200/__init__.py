@@ -11,12 +11,13 @@ from .errors import *  # noqa: F401,F403
 
 
 def run_two_stage(M, X0, Y0, tol_rel=1e-10, cfg=None, ipm=None, tp=None, stage="two_stage",
-                  **kw):
-    """SPEC.md:411 run_two_stage on the B200 (see solver.run_two_stage)."""
+                  s1=None, **kw):
+    """SPEC.md:411 run_two_stage on the B200 (see solver.run_two_stage).  ``cfg`` (or its
+    alias ``s1``) is the Stage1Config, ``ipm`` the IpmParams, ``tp`` the TransitionParams."""
     from . import solver
 
-    return solver.run_two_stage(M, X0, Y0, tol_rel=tol_rel, s1=cfg, ipm=ipm, tp=tp, stage=stage,
-                                **kw)
+    return solver.run_two_stage(M, X0, Y0, tol_rel=tol_rel, s1=s1 or cfg, ipm=ipm, tp=tp,
+                                stage=stage, **kw)
 
 
 __all__ = ["run_two_stage", "Stage1Config", "IpmParams", "TransitionParams", "SolveReport"]

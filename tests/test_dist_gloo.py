@@ -36,7 +36,7 @@ def _worker(rank, world, port, M, X0, Y0, iters, barrier, out_q):
         comm = Comm.from_env()
         a, b = row_range(M.shape[0], world, rank)
         rep = D.run_two_stage(M[a:b], X0[a:b], Y0, tol_rel=1e-10,
-                              ipm=D.IpmParams(fixed_iters=iters, barrier=barrier), comm=comm)
+                              ipm=D.IpmParams(fixed_iters=iters, barrier=barrier, hessian="paper"), comm=comm)
         out_q.put((rank, a, b, rep.X, rep.Yt, rep.stage1.sweeps, rep.stage1.pX, rep.stage1.pY,
                    rep.ipm.armijo_t, rep.ipm.flags, rep.objective, rep.kkt))
     finally:
@@ -62,7 +62,7 @@ def test_sharded_two_stage_matches_single(barrier):
     D.set_schur_backend("numpy")
     try:
         ref = D.run_two_stage(M, X0, Y0, tol_rel=1e-10,
-                              ipm=D.IpmParams(fixed_iters=iters, barrier=barrier))
+                              ipm=D.IpmParams(fixed_iters=iters, barrier=barrier, hessian="paper"))
     finally:
         D.set_schur_backend("c")
     world = 2

@@ -37,7 +37,7 @@ def _worker(rank, world, port, M, X0, Y0, iters, q):
         comm = Comm.from_env()
         a, b = row_range(M.shape[0], world, rank)
         rep = solver.run_two_stage(M[a:b], X0[a:b], Y0, tol_rel=1e-10,
-                                   ipm=IpmParams(fixed_iters=iters), comm=comm)
+                                   ipm=IpmParams(fixed_iters=iters, hessian="paper"), comm=comm)
         q.put((rank, rep.X, rep.Yt, rep.stage1.sweeps, rep.ipm.armijo_t, rep.ipm.flags,
                rep.final_objective, rep.eps_abs))
     finally:
@@ -52,7 +52,7 @@ def test_sharded_device_solver_matches_single():
 
     M, X0, Y0, _, _ = data.peaks(600, 50, 3, 91)
     iters = 15
-    ref = solver.run_two_stage(M, X0, Y0, tol_rel=1e-10, ipm=IpmParams(fixed_iters=iters))
+    ref = solver.run_two_stage(M, X0, Y0, tol_rel=1e-10, ipm=IpmParams(fixed_iters=iters, hessian="paper"))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()

@@ -118,10 +118,10 @@ def test_ipm_parity(mods, name, barrier, iters, eps, solve, resid):
     assert abs(mu - st.mu) <= 1e-12 * st.mu
     eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho,
                             IpmParams(fixed_iters=iters, barrier=barrier, schur_solver=solve,
-                                      residual=resid))
+                                      residual=resid, hessian="paper"))
     D.set_schur_backend("numpy")
     try:
-        ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=iters, barrier=barrier))
+        ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=iters, barrier=barrier, hessian="paper"))
     finally:
         D.set_schur_backend("c")
     assert r.iters == ro2.iters and r.outer == ro2.outer
@@ -151,7 +151,7 @@ def test_ipm_parity_paths(mods, name, barrier, iters, eps, path):
     st = D.transition(ro.X, ro.Yt, M, eps)
     P = solver.Problem(M, k)
     X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), eps)
-    kw = dict(fixed_iters=iters, barrier=barrier)
+    kw = dict(fixed_iters=iters, barrier=barrier, hessian="paper")
     if path == "graph":
         kw.update(persistent=False)
     elif path == "eager":
@@ -167,7 +167,7 @@ def test_ipm_parity_paths(mods, name, barrier, iters, eps, path):
         assert P.persist_iters == 0
     D.set_schur_backend("numpy")
     try:
-        ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=iters, barrier=barrier))
+        ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=iters, barrier=barrier, hessian="paper"))
     finally:
         D.set_schur_backend("c")
     assert r.iters == ro2.iters and r.outer == ro2.outer
@@ -181,8 +181,8 @@ def test_ipm_parity_paths(mods, name, barrier, iters, eps, path):
 def test_two_stage_c1(mods):
     data, solver, IpmParams, Stage1Config = mods
     M, X0, Y0 = _instance(data, "c1")
-    rep = solver.run_two_stage(M, X0, Y0, tol_rel=1e-10, ipm=IpmParams(max_iter=80))
-    ref = D.run_two_stage(M, X0, Y0, tol_rel=1e-10, ipm=D.IpmParams(max_iter=80))
+    rep = solver.run_two_stage(M, X0, Y0, tol_rel=1e-10, ipm=IpmParams(max_iter=80, hessian="paper"))
+    ref = D.run_two_stage(M, X0, Y0, tol_rel=1e-10, ipm=D.IpmParams(max_iter=80, hessian="paper"))
     assert rep.stage1.sweeps == ref.stage1.sweeps
     assert rep.ipm.iters == ref.ipm.iters and rep.ipm.armijo_t == ref.ipm.armijo_t
     assert abs(rep.eps_abs - ref.eps_abs) <= 1e-12 * ref.eps_abs
@@ -198,10 +198,10 @@ def test_dense_k10_ipm_small(mods):
     st = D.transition(ro.X, ro.Yt, M, 1e-7)
     P = solver.Problem(M, 10)
     X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), 1e-7)
-    eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(fixed_iters=8, residual="free"))
+    eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(fixed_iters=8, residual="free", hessian="paper"))
     D.set_schur_backend("numpy")
     try:
-        ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=8))
+        ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=8, hessian="paper"))
     finally:
         D.set_schur_backend("c")
     assert r.armijo_t == ro2.armijo_t and r.flags == ro2.flags
@@ -315,3 +315,49 @@ def test_general_graph_matches_eager_across_mu(mods):
     assert ng <= 2, "one graph per F buffer"
     assert t1 == t2 and mu1 == mu2
     assert np.array_equal(X1, X2) and np.array_equal(Y1, Y2)
+
+
+def test_c4_full_size_step_parity(mods):
+    """BASELINE c4 at full size (20000 x 5000, k = 10): the bench step's 50 fixed sweeps
+    (identical passive sets, factors 1e-10) and its 20 IPM iterations (residual-free,
+    rank-k^2 Schur solve) against the oracle's CPU restatement (oracle/lowrank.py)."""
+    data, solver, IpmParams, Stage1Config = mods
+    cfg = data.CONFIGS["c4"]
+    M, X0, Y0 = _instance(data, "c4")
+    P = solver.Problem(M, cfg.k)
+    X, Yt, pX, pY, r = solver.run_stage1(P, P.to_dev(X0), P.to_dev(Y0.T),
+                                         Stage1Config(fixed_sweeps=cfg.fixed_sweeps))
+    ro = D.run_stage1(M, X0, Y0.T.copy(), D.Stage1Config(fixed_sweeps=cfg.fixed_sweeps))
+    assert np.array_equal(pX.bool().cpu().numpy(), ro.pX)
+    assert np.array_equal(pY.bool().cpu().numpy(), ro.pY)
+    assert rel(X.cpu().numpy(), ro.X) < TOL_STAGE1 and rel(Yt.cpu().numpy(), ro.Yt) < TOL_STAGE1
+    eps = 1e-7
+    st = D.transition(ro.X, ro.Yt, M, eps)
+    X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), eps)
+    assert abs(mu - st.mu) <= 1e-12 * st.mu
+    eng, r2 = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(fixed_iters=cfg.fixed_ipm))
+    assert eng.ffree
+    ro2 = D.run_ipm(M, st, D.IpmParams(fixed_iters=cfg.fixed_ipm, schur_solver="lowrank",
+                                       residual="free"))
+    assert r2.armijo_t == ro2.armijo_t and r2.outer == ro2.outer
+    for a, b in ((eng.X, ro2.state.X), (eng.Yt, ro2.state.Yt), (eng.R, ro2.state.R)):
+        assert rel(a.cpu().numpy(), b) < 1e-9
+    assert abs(r2.trace[-1][1] - ro2.trace[-1][1]) <= 1e-10 * ro2.trace[-1][1]
+
+
+def test_c5_shape_fp32_ipm(mods):
+    """c5 family (fp32 M storage, k = 16) stage 2 on a 12000 x 3000 slice: 5 IPM iterations
+    (residual-free, k^2 = 256 capacitance) against the fp64 oracle on the rounded M, 1e-4."""
+    data, solver, IpmParams, Stage1Config = mods
+    M, X0, Y0 = data.dense(12000, 3000, 16, 105)[:3]
+    M32 = M.astype(np.float32)
+    M64 = M32.astype(np.float64)
+    ro = D.run_stage1(M64, X0, Y0.T.copy(), D.Stage1Config(fixed_sweeps=4))
+    st = D.transition(ro.X, ro.Yt, M64, 1e-7)
+    P = solver.Problem(M32, 16)
+    X, Yt, R, S, mu, rho = solver.transition(P, P.to_dev(ro.X), P.to_dev(ro.Yt), 1e-7)
+    eng, r = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(fixed_iters=5, residual="free"))
+    ro2 = D.run_ipm(M64, st, D.IpmParams(fixed_iters=5, schur_solver="lowrank", residual="free"))
+    assert r.armijo_t == ro2.armijo_t
+    for a, b in ((eng.X, ro2.state.X), (eng.Yt, ro2.state.Yt)):
+        assert rel(a.cpu().numpy(), b) < 1e-4

@@ -15,8 +15,8 @@ def test_stream_parity_small():
     M, X0, Y0, _, _ = data.peaks(600, 60, 4, 103)
     D.set_schur_backend("numpy")
     try:
-        so = OS.OracleStream(M[:, :20], X0, Y0[:, :20], ipm_factory=lambda: D.IpmParams(fixed_iters=6))
-        sg = StreamSession(M[:, :20], X0, Y0[:, :20], ipm_factory=lambda: IpmParams(fixed_iters=6))
+        so = OS.OracleStream(M[:, :20], X0, Y0[:, :20], ipm_factory=lambda: D.IpmParams(fixed_iters=6, hessian="paper"))
+        sg = StreamSession(M[:, :20], X0, Y0[:, :20], ipm_factory=lambda: IpmParams(fixed_iters=6, hessian="paper"))
         for m0 in range(20, 60, 10):
             so.append(M[:, m0:m0 + 10])
             sg.append(M[:, m0:m0 + 10])
@@ -48,8 +48,8 @@ def test_stream_c3_dense_fallback_parity():
     D.set_schur_backend("numpy")
     try:
         so = OS.OracleStream(M[:, :20], X0, Y0[:, :20],
-                             ipm_factory=lambda: D.IpmParams(barrier="paper"))
-        sg = StreamSession(M[:, :20], X0, Y0[:, :20], ipm_factory=lambda: IpmParams(barrier="paper"))
+                             ipm_factory=lambda: D.IpmParams(barrier="paper", hessian="paper"))
+        sg = StreamSession(M[:, :20], X0, Y0[:, :20], ipm_factory=lambda: IpmParams(barrier="paper", hessian="paper"))
         so.append(M[:, 20:30])
         sg.append(M[:, 20:30])
     finally:
