@@ -103,6 +103,15 @@ int nmfb_colprod(const void *A, int a_is_f32, long rows, long cols, const double
                  double *out, double *tol, double scale, double *work, long work_len,
                  void *stream);
 
+/* Both streaming products of one pass over A (rows, cols), cols even: outR (rows, k) =
+ * A B1 with B1 (cols, k), and outC (cols, k) = A^T B2 with B2 (rows, k).  The stage-2
+ * Armijo pass M dY^T / M^T dX (residual-free mode; the refresh then updates M Y^T and
+ * M^T X incrementally).  Deterministic.  work >= nmfb_dualprod_work_len. */
+long nmfb_dualprod_work_len(long rows, long cols, long k);
+int nmfb_dualprod(const void *A, int a_is_f32, long rows, long cols, const double *B1,
+                  const double *B2, long k, double *outR, double *outC, double *work,
+                  long work_len, void *stream);
+
 /* btb of both half-sweeps: squared row and column norms of M. */
 int nmfb_sqnorms(const void *A, int a_is_f32, long rows, long cols, double *row_out,
                  double *col_out, double *work, long work_len, void *stream);
@@ -206,6 +215,15 @@ int nmfb_armijo_lazy(const double *X, const double *dX, long nx, const double *Y
                      const double *dYt, long ny, double *sc, int ntrials, double mu, double wx,
                      double wy, double eta, int max_backtracks, const int *fcodes, double *work,
                      long work_len, void *stream);
+/* nmfb_step_nudge that ORs 1 into *flag when an entry was nudged; alpha from alpha_dev
+ * when it is not NULL */
+int nmfb_step_nudge_flag(double *v, const double *dv, long len, const double *alpha_dev,
+                         double alpha, double tau, int *flag, void *stream);
+/* residual-free refresh after a clean step (*flag == 0): MY += a MdY (nlen entries),
+ * MX += a MtdX (mlen entries), a = *alpha_dev or alpha; nothing when *flag != 0 */
+int nmfb_ffree_advance(double *MY, const double *MdY, long nlen, double *MX, const double *MtdX,
+                       long mlen, const double *alpha_dev, double alpha, const int *flag,
+                       void *stream);
 /* as nmfb_step_nudge with alpha read from device memory */
 int nmfb_step_nudge_dev(double *v, const double *dv, long len, const double *alpha, double tau,
                         void *stream);

@@ -59,6 +59,8 @@ SIGNATURES = {
     "nmfb_armijo_select": [P, D, D, D, D, I, P, P],
     "nmfb_armijo_lazy": [P, P, L, P, P, L, P, I, D, D, D, D, I, P, P, L, P],
     "nmfb_step_nudge_dev": [P, P, L, P, D, P],
+    "nmfb_step_nudge_flag": [P, P, L, P, D, D, P, P],
+    "nmfb_ffree_advance": [P, P, L, P, P, L, P, D, P, P],
     "nmfb_kkt_sums": [P, P, P, L, P, P, P, L, D, D, P, P, P],
     "nmfb_affine_mu": [P, P, P, P, L, P, P, P, P, L, D, D, P, P, P],
     "nmfb_clamp_min": [P, L, D, P],
@@ -72,6 +74,8 @@ SIGNATURES = {
     "nmfb_ffree_quartic": [P, P, P, P, P, P, P, P, P, L, P, P],
     "nmfb_small_supported": [L, L, L],
     "nmfb_persist_supported": [L, L, L, I, I],
+    "nmfb_dualprod_work_len": [L, L, L],
+    "nmfb_dualprod": [P, I, L, L, P, P, L, P, P, P, L, P],
     "nmfb_grams_work_len": [L, L, L],
     "nmfb_stage1_persist_supported": [L, L, L, I],
     "nmfb_stage1_persist_work_len": [L, L, L],
@@ -85,7 +89,7 @@ SIGNATURES = {
     "nmfb_lowrank_factor": [P, P, L, P, P, P, P, P],
     "nmfb_lowrank_solve": [P, P, P, P, P, L, L, P, P, P, P, P, L, P],
 }
-RESTYPES = {"nmfb_nnls_ftab_len": ctypes.c_long, "nmfb_colprod_work_len": ctypes.c_long, "nmfb_rowprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
+RESTYPES = {"nmfb_dualprod_work_len": ctypes.c_long, "nmfb_nnls_ftab_len": ctypes.c_long, "nmfb_colprod_work_len": ctypes.c_long, "nmfb_rowprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
             "nmfb_launch_count": ctypes.c_ulonglong, "nmfb_small_work_len": ctypes.c_long,
             "nmfb_persist_work_len": ctypes.c_long, "nmfb_grams_work_len": ctypes.c_long,
             "nmfb_term4_work_len": ctypes.c_long,

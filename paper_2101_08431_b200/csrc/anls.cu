@@ -803,6 +803,190 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
   return NMFB_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Dual streaming product: ONE pass over M gives both
+//     outR = M B1   (rows x K; B1: cols x K, e.g. M dY^T)
+//     outC = M^T B2 (cols x K; B2: rows x K, e.g. M^T dX)
+// The stage-2 Armijo pass and the incremental refresh (M Y'^T = M Y^T + a M dY^T,
+// M^T X' = M^T X + a M^T dX, paper_2101_08431_b200/solver.py) need exactly these two.
+//
+// CTA = 256-column chunk x row split; warp w owns columns [32w, 32w+32) of the chunk
+// and walks the split's rows in 8-row tiles.  For every 8 x 32 region the warp issues
+// the column-product loads (lane = 4g+t: rows {t, 4+t}, columns 16h + 2g, +1) and the
+// row-product loads (row g, columns 8q + 2t, +1) of the same 2 KB (the second set is
+// an L1 hit), so every byte of M comes from HBM once and both products run on the FP64
+// tensor pipe (DMMA m8n8k4, fragment conventions as k_rowprod_mma / k_colprod_mma).
+// Column partials stay in registers for the whole split; row partials (8 tiles = 64
+// rows per warp) are exchanged through shared memory and summed over the 8 warps in a
+// fixed order, so the result is deterministic.  Partials: partR[chunk][row][p],
+// partC[split][col][p]; the fixed-order k_sum_partials finishes both.
+// ---------------------------------------------------------------------------
+constexpr int DP_CW = 256;  // columns per chunk (8 warps x 32)
+constexpr int DP_RB = 64;   // rows per exchange block (8 tiles of 8)
+
+template <int NT, typename T>
+__global__ void __launch_bounds__(256, 2) k_dualprod_mma(const T* __restrict__ A, long rows,
+                                                         long cols, const double* __restrict__ B1,
+                                                         const double* __restrict__ B2, int K,
+                                                         long rows_per_split,
+                                                         double* __restrict__ partR,
+                                                         double* __restrict__ partC) {
+  extern __shared__ __align__(16) double dsm[];
+  double* sB = dsm;                        // [CW/8][2][NT][32] B1 fragments of the chunk
+  double* xb = dsm + DP_CW / 8 * 2 * NT * 32;  // [8 warps][DP_RB][NT*8] row-partial exchange
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const long j0 = (long)blockIdx.x * DP_CW;
+  for (int e = tid; e < DP_CW / 8 * 2 * NT * 32; e += 256) {
+    const int l = e & 31, se = (e >> 5) / NT, nt = (e >> 5) % NT;
+    const int sidx = se >> 1, ee = se & 1;
+    const long col = j0 + 8 * sidx + 2 * (l & 3) + ee;
+    const int pp = nt * 8 + (l >> 2);
+    sB[e] = (col < cols && pp < K) ? B1[col * K + pp] : 0.0;
+  }
+  __syncthreads();
+  const long jw = j0 + 32 * warp;  // this warp's first column
+  const long rb = (long)blockIdx.y * rows_per_split;
+  const long re = min(rows, rb + rows_per_split);
+  bool cok[2], rokc[4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) cok[h] = jw + 16 * h + 2 * g < cols;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) rokc[q] = jw + 8 * q + 2 * t < cols;
+  double accC[2][2][NT][2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int par = 0; par < 2; ++par)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) accC[h][par][nt][0] = accC[h][par][nt][1] = 0.0;
+  const double2 z2 = make_double2(0.0, 0.0);
+  double* xw = xb + (long)warp * DP_RB * NT * 8;
+  for (long r0 = rb; r0 < re; r0 += DP_RB) {
+#pragma unroll 2
+    for (int rt = 0; rt < DP_RB / 8; ++rt) {
+      const long rbase = r0 + 8 * rt;
+      double accR[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) accR[nt][0] = accR[nt][1] = 0.0;
+      // column-product operands: rows rbase + t, rbase + 4 + t
+      double2 ac[2][2];
+      double b2[2][NT];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const long i = rbase + 4 * u + t;
+        const bool ok = i < re;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          ac[u][h] = (ok && cok[h]) ? ld2<T>(A + i * cols + jw + 16 * h + 2 * g) : z2;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          b2[u][nt] = (ok && nt * 8 + g < K) ? __ldg(B2 + i * K + nt * 8 + g) : 0.0;
+      }
+      // row-product operands: row rbase + g, columns 8q + 2t (+1)
+      double2 ar[4];
+      {
+        const long i = rbase + g;
+        const bool ok = i < re;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          ar[q] = (ok && rokc[q]) ? ld2<T>(A + i * cols + jw + 8 * q + 2 * t) : z2;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            dmma(accC[h][0][nt][0], accC[h][0][nt][1], ac[u][h].x, b2[u][nt]);
+            dmma(accC[h][1][nt][0], accC[h][1][nt][1], ac[u][h].y, b2[u][nt]);
+          }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int grp = 4 * warp + q;  // 8-column group inside the chunk
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double b0 = sB[((2 * grp) * NT + nt) * 32 + lane];
+          const double b1 = sB[((2 * grp + 1) * NT + nt) * 32 + lane];
+          dmma(accR[nt][0], accR[nt][1], ar[q].x, b0);
+          dmma(accR[nt][0], accR[nt][1], ar[q].y, b1);
+        }
+      }
+      // this warp's 32-column share of the tile's row products -> exchange buffer
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        *reinterpret_cast<double2*>(xw + (8 * rt + g) * NT * 8 + nt * 8 + 2 * t) =
+            make_double2(accR[nt][0], accR[nt][1]);
+    }
+    // fixed-order sum of the 8 warps' shares of the block's 64 rows
+    __syncthreads();
+    for (int e = tid; e < DP_RB * K; e += 256) {
+      const int rr = e / K, pp = e - rr * K;
+      const long row = r0 + rr;
+      if (row >= re) continue;
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += xb[((long)w * DP_RB + rr) * NT * 8 + pp];
+      partR[((long)blockIdx.x * rows + row) * K + pp] = v;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+      const long j = jw + 16 * h + 2 * g + par;
+      if (j >= cols) continue;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int pp = nt * 8 + 2 * t + c;
+          if (pp < K) partC[((long)blockIdx.y * cols + j) * K + pp] = accC[h][par][nt][c];
+        }
+    }
+}
+
+struct DualGrid {
+  long nch, nsplit, rps;
+};
+
+inline DualGrid dual_grid(long rows, long cols) {
+  DualGrid d;
+  d.nch = (cols + DP_CW - 1) / DP_CW;
+  long nsplit = (148 * 2 * 2 + d.nch - 1) / d.nch;  // ~2 waves of 2 CTAs per SM
+  long rps = (rows + nsplit - 1) / nsplit;
+  rps = ((rps + DP_RB - 1) / DP_RB) * DP_RB;
+  d.rps = rps;
+  d.nsplit = (rows + rps - 1) / rps;
+  return d;
+}
+
+template <int K, typename T>
+int launch_dualprod(const T* A, long rows, long cols, const double* B1, const double* B2,
+                    double* outR, double* outC, double* work, long work_len, cudaStream_t st) {
+  static_assert(K >= 1 && K <= 16, "K");
+  constexpr int NT = (K + 7) / 8;
+  const DualGrid d = dual_grid(rows, cols);
+  const long needR = d.nch * rows * K, needC = d.nsplit * cols * K;
+  if (needR + needC > work_len) return NMFB_ENOMEM;
+  double* partR = work;
+  double* partC = work + needR;
+  const size_t smem = (size_t)(DP_CW / 8 * 2 * NT * 32 + 8 * DP_RB * NT * 8) * sizeof(double);
+  cudaFuncSetAttribute(k_dualprod_mma<NT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  dim3 grid((unsigned)d.nch, (unsigned)d.nsplit);
+  ++g_nmfb_launches, k_dualprod_mma<NT, T><<<grid, 256, smem, st>>>(A, rows, cols, B1, B2, K,
+                                                                      d.rps, partR, partC);
+  ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(partR, (int)d.nch,
+                                                                         rows * K, outR, nullptr, 1.0);
+  ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(cols), 256, 0, st>>>(partC, (int)d.nsplit,
+                                                                         cols * K, outC, nullptr, 1.0);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
 }  // namespace
 
 #define NMFB_K_SWITCH(k, MACRO) \
@@ -860,6 +1044,33 @@ extern "C" int nmfb_colprod(const void* A, int a_is_f32, long rows, long cols, c
                                                 work, work_len, st)                             \
                     : launch_colprod<KK, double>((const double*)A, rows, cols, B, out, tol,     \
                                                  scale, work, work_len, st);
+  NMFB_K_SWITCH(k, CASE)
+#undef CASE
+}
+
+extern "C" long nmfb_dualprod_work_len(long rows, long cols, long k) {
+  if (rows <= 0 || cols <= 0) return 1;
+  const DualGrid d = dual_grid(rows, cols);
+  return d.nch * rows * k + d.nsplit * cols * k;
+}
+
+extern "C" int nmfb_dualprod(const void* A, int a_is_f32, long rows, long cols, const double* B1,
+                             const double* B2, long k, double* outR, double* outC, double* work,
+                             long work_len, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rows < 0 || cols < 0) return NMFB_EINVAL;
+  if (rows == 0 || cols == 0) {
+    if (rows) cudaMemsetAsync(outR, 0, sizeof(double) * rows * k, st);
+    if (cols) cudaMemsetAsync(outC, 0, sizeof(double) * cols * k, st);
+    return NMFB_OK;
+  }
+  if (cols % 2) return NMFB_EUNSUPPORTED;  // 2-wide vector loads of M rows
+#define CASE(KK)                                                                                \
+  case KK:                                                                                      \
+    return a_is_f32 ? launch_dualprod<KK, float>((const float*)A, rows, cols, B1, B2, outR, outC, \
+                                                 work, work_len, st)                            \
+                    : launch_dualprod<KK, double>((const double*)A, rows, cols, B1, B2, outR,   \
+                                                  outC, work, work_len, st);
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
 }

@@ -937,6 +937,42 @@ __global__ void k_step_nudge_dev(double* __restrict__ v, const double* __restric
   }
 }
 
+// step with the nudge rule that also reports whether any entry was nudged
+// (flag: the residual-free refresh may then not advance M Y^T / M^T X incrementally)
+__global__ void k_step_nudge_flag(double* __restrict__ v, const double* __restrict__ dv, long len,
+                                  const double* __restrict__ alpha_dev, double alpha, double tau,
+                                  int* __restrict__ flag) {
+  const double a = alpha_dev ? *alpha_dev : alpha;
+  int nudged = 0;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+       e += (long)gridDim.x * blockDim.x) {
+    const double old = v[e];
+    const double nv = old + a * dv[e];
+    const bool ok = nv > 0.0;
+    v[e] = ok ? nv : (1.0 - tau) * old;
+    nudged |= !ok;
+  }
+  if (__syncthreads_or(nudged) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+// residual-free refresh after a clean step: M Y'^T = M Y^T + a M dY^T and
+// M^T X' = M^T X + a M^T dX (both products came from the Armijo pass at the
+// previous point); a nudged step (flag != 0) leaves them for a full recompute
+__global__ void k_ffree_advance(double* __restrict__ MY, const double* __restrict__ MdY, long nlen,
+                                double* __restrict__ MX, const double* __restrict__ MtdX, long mlen,
+                                const double* __restrict__ alpha_dev, double alpha,
+                                const int* __restrict__ flag) {
+  if (*flag) return;
+  const double a = alpha_dev ? *alpha_dev : alpha;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < nlen + mlen;
+       e += (long)gridDim.x * blockDim.x) {
+    if (e < nlen)
+      MY[e] = fma(a, MdY[e], MY[e]);
+    else
+      MX[e - nlen] = fma(a, MtdX[e - nlen], MX[e - nlen]);
+  }
+}
+
 constexpr int RED_BLOCKS = 296;  // fixed -> deterministic reductions
 
 // ---------------------------------------------------------------------------
@@ -1421,6 +1457,27 @@ extern "C" int nmfb_armijo_select(double* sc, double mu, double wx, double wy, d
   cudaStream_t st = (cudaStream_t)stream;
   ++g_nmfb_launches, k_armijo_select<<<1, 32, 0, st>>>(sc, mu, wx, wy, eta, max_backtracks, fcodes,
                                                        -1, 0, g_mu_dev);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_step_nudge_flag(double* v, const double* dv, long len, const double* alpha_dev,
+                                    double alpha, double tau, int* flag, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (len <= 0) return NMFB_OK;
+  ++g_nmfb_launches, k_step_nudge_flag<<<nmfb_blocks(len, 256, 148 * 8), 256, 0, st>>>(
+      v, dv, len, alpha_dev, alpha, tau, flag);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_ffree_advance(double* MY, const double* MdY, long nlen, double* MX,
+                                  const double* MtdX, long mlen, const double* alpha_dev,
+                                  double alpha, const int* flag, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nlen + mlen <= 0) return NMFB_OK;
+  ++g_nmfb_launches, k_ffree_advance<<<nmfb_blocks(nlen + mlen, 256, 148 * 8), 256, 0, st>>>(
+      MY, MdY, nlen, MX, MtdX, mlen, alpha_dev, alpha, flag);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

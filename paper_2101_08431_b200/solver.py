@@ -216,14 +216,16 @@ class Problem:
         """Use the residual-free formulation when an n x m fp64 residual is large."""
         return self.n * self.m >= (1 << 25)
 
-    def gradients_free(self, X, Yt, gX, gY, ws, out_index=0):
+    def gradients_free(self, X, Yt, gX, gY, ws, out_index=0, passes=True):
         """graX, graY and ||F||^2 without forming F (csrc/ipm.cu "F-free"):
-        three small Grams plus M Y^T and X^T M (two streaming passes over M)."""
+        three small Grams plus M Y^T and X^T M (two streaming passes over M;
+        passes=False: ws["MY"], ws["MX"] already hold them at (X, Yt))."""
         n, m, k, s = self.n, self.m, self.k, self.stream
         self.colprod(Yt, m, k, Yt, k, ws["GY"])
         self.colprod(X, n, k, X, k, ws["XX"], reduce=True)
-        self.rowprod(self.M, n, m, Yt, k, ws["MY"], None, self.f32)
-        self.colprod(self.M, n, m, X, k, ws["MX"], None, self.f32, reduce=True)
+        if passes:
+            self.rowprod(self.M, n, m, Yt, k, ws["MY"], None, self.f32)
+            self.colprod(self.M, n, m, X, k, ws["MX"], None, self.f32, reduce=True)
         self._call("nmfb_ffree_grad_rows", _p(X), _p(ws["GY"]), _p(ws["MY"]), n, k, _p(gX),
                    _p(ws["part"]), s)
         self._call("nmfb_ffree_fsq", _p(ws["part"]), self.mnorm2_local,
@@ -232,6 +234,13 @@ class Problem:
         self.comm.sum_(self.dscal[out_index:out_index + 1])
         self._call("nmfb_ffree_grad_rows", _p(Yt), _p(ws["XX"]), _p(ws["MX"]), m, k, _p(gY),
                    _p(ws["part2"]), s)
+
+    def dualprod(self, B1, B2, outR, outC, work, reduce=True):
+        """outR = M B1 (rows), outC = M^T B2 (all-reduced over row shards): one pass."""
+        self._call("nmfb_dualprod", _p(self.M), self.f32, self.n, self.m, _p(B1), _p(B2), self.k,
+                   _p(outR), _p(outC), _p(work), work.numel(), self.stream)
+        if reduce:
+            self.comm.sum_(outC)
 
     def free_workspace(self):
         n, m, k = self.n, self.m, self.k
@@ -417,6 +426,13 @@ class IpmEngine:
         if self.ffree:
             self.fws = P.free_workspace()
             self.MdY = b(n, k)
+            # one-pass Armijo products (M dY^T, M^T dX) and the incremental refresh of
+            # M Y^T / M^T X (csrc/anls.cu k_dualprod_mma, csrc/ipm.cu k_ffree_advance)
+            self.dual = (m % 2 == 0) and os.environ.get("NMFB_DUALPROD", "1") != "0"
+            if self.dual:
+                self.MtdX = b(m, k)
+                self.dwork = b(max(P.lib.nmfb_dualprod_work_len(n, m, k), 1))
+            self.mvalid = False  # fws["MY"], fws["MX"] hold M Y^T, M^T X at the current point
             self.A1, self.A2, self.B1, self.B2 = b(k, k), b(k, k), b(k, k), b(k, k)
             self.Dgx, self.Dgy, self.Dmd = b(k, k), b(k, k), b(k, k)
         self.fi = 0  # index of F at the current point
@@ -492,7 +508,10 @@ class IpmEngine:
         """Launch gradients + KKT sums at the current point (no host sync)."""
         P = self.P
         if self.ffree:
-            P.gradients_free(self.X, self.Yt, self.gX, self.gY, self.fws, out_index=0)
+            passes = not (self.dual and self.mvalid)
+            P.gradients_free(self.X, self.Yt, self.gX, self.gY, self.fws, out_index=0,
+                             passes=passes)
+            self.mvalid = self.dual
             P.kkt_sums(self.X, self.R, self.gX, self.Yt, self.S, self.gY, self.wx * self.mu,
                        self.wy * self.mu, at=16)
             return
@@ -546,12 +565,52 @@ class IpmEngine:
                     _p(P.dscal), NTRIALS, self.mu, self.wx, self.wy, p.eta, p.max_backtracks,
                     _p(P.iscal[2:]), _p(P.rwork), P.rwork.numel(), s)
         self.remember_factorization(False)  # the factorization's X, Y (before the step)
-        a1p, a2p = P.dscal[1:2], P.dscal[3:4]
-        P._call("nmfb_step_nudge_dev", _p(self.X), _p(self.dX), n * k, _p(a1p), p.tau, s)
-        P._call("nmfb_step_nudge_dev", _p(self.Yt), _p(dY), m * k, _p(a1p), p.tau, s)
-        P._call("nmfb_step_nudge_dev", _p(self.R), _p(self.dR), n * k, _p(a2p), p.tau, s)
-        P._call("nmfb_step_nudge_dev", _p(self.S), _p(self.dS), m * k, _p(a2p), p.tau, s)
+        self.take_step(dY, P.dscal[1:2], 0.0, P.dscal[3:4], 0.0)
         self.refresh_launch()
+
+    def take_step(self, dY, a1_dev, a1, a2_dev, a2):
+        """x, y += a1 (dx, dy); r, s += a2 (dr, ds) with the nudge rule (SPEC.md:359);
+        step lengths from device memory (graph path) or host scalars.  Residual-free dual
+        mode: M Y^T / M^T X advance with the step unless an entry was nudged (iscal[5]
+        then reports it and the host recomputes them, see run_ipm)."""
+        P, p = self.P, self.p
+        n, m, k, s = self.n, self.m, self.k, P.stream
+        if self.ffree and self.dual:
+            P.iscal[5:6].zero_()
+            fl = _p(P.iscal[5:])
+            P._call("nmfb_step_nudge_flag", _p(self.X), _p(self.dX), n * k, _p(a1_dev), a1, p.tau,
+                    fl, s)
+            P._call("nmfb_step_nudge_flag", _p(self.Yt), _p(dY), m * k, _p(a1_dev), a1, p.tau,
+                    fl, s)
+            if self.comm.active:  # a nudge on any rank invalidates the reduced M^T X
+                self.comm.max_(P.iscal[5:6])
+            P._call("nmfb_ffree_advance", _p(self.fws["MY"]), _p(self.MdY), n * k,
+                    _p(self.fws["MX"]), _p(self.MtdX), m * k, _p(a1_dev), a1, fl, s)
+        elif a1_dev is not None:
+            P._call("nmfb_step_nudge_dev", _p(self.X), _p(self.dX), n * k, _p(a1_dev), p.tau, s)
+            P._call("nmfb_step_nudge_dev", _p(self.Yt), _p(dY), m * k, _p(a1_dev), p.tau, s)
+        else:
+            P._call("nmfb_step_nudge", _p(self.X), _p(self.dX), n * k, a1, p.tau, s)
+            P._call("nmfb_step_nudge", _p(self.Yt), _p(dY), m * k, a1, p.tau, s)
+        if a2_dev is not None:
+            P._call("nmfb_step_nudge_dev", _p(self.R), _p(self.dR), n * k, _p(a2_dev), p.tau, s)
+            P._call("nmfb_step_nudge_dev", _p(self.S), _p(self.dS), m * k, _p(a2_dev), p.tau, s)
+        else:
+            P._call("nmfb_step_nudge", _p(self.R), _p(self.dR), n * k, a2, p.tau, s)
+            P._call("nmfb_step_nudge", _p(self.S), _p(self.dS), m * k, a2, p.tau, s)
+
+    def check_advance(self, flag=None):
+        """After a residual-free dual-mode step: if an entry was nudged (iscal[5], or the
+        value ``flag`` already read back), recompute M Y^T and M^T X (two passes) and the
+        KKT sums -> new (e_mu, e_0, fsq, sums); None when the incremental refresh held."""
+        if not (self.ffree and self.dual):
+            return None
+        if flag is None:
+            flag = int(self.P.readback(0, 6)[1][5])
+        if int(flag) == 0:
+            return None
+        self.mvalid = False
+        return self.refresh()
 
     def gn_iteration_graph(self):
         """Replay (capturing on first use) the GN iteration graph for the current state.
@@ -788,11 +847,15 @@ class IpmEngine:
             P.dscal[32:32 + 2 * NTRIALS].view(NTRIALS, 2)[:, 0].copy_(bx)
 
     def _armijo_free(self, dY, trials=True):
-        """Quartic coefficients from k x k Grams + one streaming pass M dY^T."""
+        """Quartic coefficients from k x k Grams + one streaming pass over M (M dY^T, and
+        with the dual product also M^T dX for the next incremental refresh)."""
         P, s = self.P, self.P.stream
         n, m, k = self.n, self.m, self.k
         X, Yt, dX = self.X, self.Yt, self.dX
-        P.rowprod(P.M, n, m, dY, k, self.MdY, None, P.f32)
+        if self.dual:
+            P.dualprod(dY, dX, self.MdY, self.MtdX, self.dwork)
+        else:
+            P.rowprod(P.M, n, m, dY, k, self.MdY, None, P.f32)
         P.grams([(dX, dX, self.A1), (dX, X, self.A2), (dX, self.gX, self.Dgx),
                  (dX, self.MdY, self.Dmd)], n, k, reduce=True)
         P.grams([(dY, dY, self.B1), (Yt, dY, self.B2), (dY, self.gY, self.Dgy)], m, k)
@@ -924,7 +987,7 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                 pass
             elif not ok and eng.use_graphs:
                 eng.gn_iteration_graph()
-                v, iv = P.readback(28, 5)
+                v, iv = P.readback(28, 6)
                 for e0, e1 in eng.graphs[eng.last_graph][1]:
                     try:
                         P.event_times.append(e0.elapsed_time(e1))
@@ -954,6 +1017,9 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                 res.flags.append(False)
                 e_mu, e_zero = kkt_from_sums(v[16:28])
                 fsq, sums = v[0], v[16:28]
+                redo = eng.check_advance(iv[5])
+                if redo is not None:
+                    e_mu, e_zero, fsq, sums = redo
                 res.trace.append((time.perf_counter() - t0, 0.5 * fsq, e_zero, eng.mu, a1, a2max, t))
                 continue
             if not ok:
@@ -988,15 +1054,14 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
                 t += 1
                 if t > p.max_backtracks:
                     raise LineSearchStall(f"Armijo backtracking exceeded {p.max_backtracks}")
-            s = P.stream
-            P._call("nmfb_step_nudge", _p(eng.X), _p(eng.dX), n * k, a1, p.tau, s)
-            P._call("nmfb_step_nudge", _p(eng.Yt), _p(dY), m * k, a1, p.tau, s)
-            P._call("nmfb_step_nudge", _p(eng.R), _p(eng.dR), n * k, a2max, p.tau, s)
-            P._call("nmfb_step_nudge", _p(eng.S), _p(eng.dS), m * k, a2max, p.tau, s)
+            eng.take_step(dY, None, a1, None, a2max)
             res.iters += 1
             res.armijo_t.append(t)
             res.flags.append(used_full)
             e_mu, e_zero, fsq, sums = eng.refresh()
+            redo = eng.check_advance()
+            if redo is not None:
+                e_mu, e_zero, fsq, sums = redo
             res.trace.append((time.perf_counter() - t0, 0.5 * fsq, e_zero, eng.mu, a1, a2max, t))
         res.outer += 1
         if e_zero <= tol or res.iters >= cap:

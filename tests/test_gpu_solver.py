@@ -244,7 +244,8 @@ def test_device_newton_vs_dense_kkt(mods, solve):
 
 @pytest.mark.parametrize("shape,dt", [((8192, 4096, 10), "f64"), ((8200, 5002, 3), "f64"),
                                       ((6000, 2304, 16), "f64"), ((8192, 4096, 16), "f32"),
-                                      ((4100, 3001, 7), "f64")])
+                                      ((4100, 3001, 7), "f64"), ((1000, 250, 10), "f64"),
+                                      ((333, 1026, 9), "f32")])
 def test_streaming_products_large(mods, shape, dt):
     """HBM-streaming product kernels (split-K / tensor-core paths) vs fp64 reference products."""
     import torch
@@ -267,6 +268,18 @@ def test_streaming_products_large(mods, shape, dt):
     tol = 1e-12 if dt == "f64" else 1e-5
     assert float((ctbX - refX).abs().max() / refX.abs().max()) < tol
     assert float((ctbY - refY).abs().max() / refY.abs().max()) < tol
+    if m % 2 == 0:  # one-pass dual product (k_dualprod_mma): M B1 and M^T B2 together
+        B1 = torch.rand((m, k), generator=g, device="cuda", dtype=torch.float64) - 0.5
+        B2 = torch.rand((n, k), generator=g, device="cuda", dtype=torch.float64) - 0.5
+        oR, oC = P.buf(n, k), P.buf(m, k)
+        work = P.buf(P.lib.nmfb_dualprod_work_len(n, m, k))
+        P.dualprod(B1, B2, oR, oC, work)
+        rR, rC = M64 @ B1, M64.t() @ B2
+        assert float((oR - rR).abs().max() / rR.abs().max()) < tol
+        assert float((oC - rC).abs().max() / rC.abs().max()) < tol
+        oR2, oC2 = P.buf(n, k), P.buf(m, k)
+        P.dualprod(B1, B2, oR2, oC2, work)
+        assert torch.equal(oR, oR2) and torch.equal(oC, oC2)  # deterministic
 
 
 def test_stage1_fixed_sweeps_failure_reporting(mods):
