@@ -335,7 +335,10 @@ def run_b200(args):
             torch.distributed.destroy_process_group()
         return 0
     peaks, peak_src = _peaks()
-    fp64_peak = measure_fp64_peak(dev)
+    try:
+        fp64_peak = measure_fp64_peak(dev)
+    except Exception:  # noqa: BLE001
+        fp64_peak = float("nan")
     avg_ms = float(np.mean(kt)) if kt else float("nan")
     # k_rowprod_mma (ctb = M Y^T): algorithmic bytes per launch = one read of this rank's
     # rows of M + Y + the (rows x k) output + the per-row tolerance; 2 rows m k flops
@@ -404,8 +407,10 @@ def run_b200(args):
 def measure_fp64_peak(dev):
     import torch
 
-    a = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
-    b = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    # deterministic operands (no RNG: the default generator is tied to the solver's graphs)
+    a = torch.arange(8192 * 8192, dtype=torch.float64, device=dev).reshape(8192, 8192)
+    a = torch.sin(a * 1e-3)
+    b = torch.cos(a.t() * 0.5)
     for _ in range(2):
         torch.matmul(a, b)
     torch.cuda.synchronize()

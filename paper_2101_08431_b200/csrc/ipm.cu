@@ -15,10 +15,18 @@
 // identity gives r_acc_j = H y_j with H = sum_i x_i (L_i^{-T} h_i)^T and the
 // back-substitution q_i = L_i^{-1} (sum_j y_j dy_j^T) x_i.  The full-Hessian
 // extra terms use W = F^T P (m x k^3 GEMM) and a residual-weighted SYRK.
-#include <cublas_v2.h>
 
 #include "common.cuh"
 #include "nmfb200.h"
+
+namespace {
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+}  // namespace
+
 
 // Barrier value source for CUDA-graph capture (nmfb_set_mu_source): while set,
 // the mu-dependent launches below bake this device pointer ([mu, wx mu, wy mu]) into
@@ -293,6 +301,62 @@ __global__ void k_sum_parts(const double* __restrict__ part, int nparts, long le
   double v = 0.0;
   for (int s = 0; s < nparts; ++s) v += part[(long)s * len + e];
   out[e] = v;
+}
+
+// ---------------------------------------------------------------------------
+// out (ca x cb) = A^T B for tall operands (rows >> ca, cb): split-K over row stripes on
+// the FP64 tensor pipe (DMMA m8n8k4).  CTA = 64 x 64 output tile x one row stripe; the
+// stripe's rows are staged 32 at a time in shared memory (row pitch 72 doubles: the
+// fragment reads of 4 rows x 8 columns hit each bank pair at most twice = 2 wavefronts);
+// warp w owns output rows 8w..8w+7 (8 n-tiles).  Partials per stripe, fixed-order sum.
+// Replaces cuBLAS DGEMM for the rank-k^2 capacitance Grams Z = sum_i Rinv_i (x) x_i x_i^T,
+// G = sum_j y_j y_j^T (x) D_j^{-1} and the full-Hessian W = F^T P.
+// ---------------------------------------------------------------------------
+constexpr int ATB_T = 64, ATB_R = 32, ATB_LD = 72;
+
+__global__ void __launch_bounds__(256) k_atb_mma(const double* __restrict__ A, long rows, long ca,
+                                                 const double* __restrict__ B, long cb,
+                                                 long stripe, double* __restrict__ part) {
+  __shared__ __align__(16) double sa[ATB_R * ATB_LD];
+  __shared__ __align__(16) double sb[ATB_R * ATB_LD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const long a0 = (long)blockIdx.x * ATB_T, b0 = (long)blockIdx.y * ATB_T;
+  const long s = blockIdx.z;
+  const long i_beg = s * stripe, i_end = min(rows, i_beg + stripe);
+  double acc[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (long ib = i_beg; ib < i_end; ib += ATB_R) {
+    const int nr = (int)min((long)ATB_R, i_end - ib);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < ATB_R * ATB_T / 256; ++q) {
+      const int e = tid + 256 * q;
+      const int r = e >> 6, c = e & 63;
+      sa[r * ATB_LD + c] = (r < nr && a0 + c < ca) ? __ldg(A + (ib + r) * ca + a0 + c) : 0.0;
+      sb[r * ATB_LD + c] = (r < nr && b0 + c < cb) ? __ldg(B + (ib + r) * cb + b0 + c) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < ATB_R / 4; ++kk) {
+      const double af = sa[(4 * kk + t) * ATB_LD + 8 * warp + g];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const double bf = sb[(4 * kk + t) * ATB_LD + 8 * j + g];
+        dmma_f64(acc[j][0], acc[j][1], af, bf);
+      }
+    }
+  }
+  const long a = a0 + 8 * warp + g;
+  if (a >= ca) return;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const long b = b0 + 8 * j + 2 * t + c;
+      if (b < cb) part[(s * ca + a) * cb + b] = acc[j][c];
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1128,6 +1192,17 @@ extern "C" long nmfb_atb_work_len(long rows, long ca, long cb) {
   if (ns > max_ns) ns = max_ns;
   if (ns < 1) ns = 1;
   long len = ns * ca * cb;
+  {  // k_atb_mma stripes (see nmfb_atb)
+    const long t64 = ((ca + 63) / 64) * ((cb + 63) / 64);
+    long n2 = (148 * 2 + t64 - 1) / t64;
+    const long mx = (rows + 127) / 128;
+    if (n2 > mx) n2 = mx;
+    if (n2 < 1) n2 = 1;
+    long stripe = (rows + n2 - 1) / n2;
+    stripe = ((stripe + 31) / 32) * 32;
+    n2 = stripe > 0 ? (rows + stripe - 1) / stripe : 1;
+    if (n2 * ca * cb > len) len = n2 * ca * cb;
+  }
   if (ca == cb && ca <= 16 && rows > 0) {  // small square products run as a Gram (nmfb_grams)
     const long g = nmfb_grams_work_len(rows, ca, 1);
     if (g > len) len = g;
@@ -1135,37 +1210,12 @@ extern "C" long nmfb_atb_work_len(long rows, long ca, long cb) {
   return len;
 }
 
-// out (ca x cb) = A^T B; A (rows x ca), B (rows x cb)
-// cuBLAS handle per device for the plain tall-skinny GEMMs A^T B of nmfb_atb (the
-// rank-k^2 capacitance Grams: n x k(k+1)/2 operands, K = n up to 200000).  Created
-// outside graph capture with a fixed workspace so later calls are capturable.
-static cublasHandle_t atb_handle(cudaStream_t st) {
-  static cublasHandle_t h[64] = {};
-  int d = 0;
-  cudaGetDevice(&d);
-  if (d < 0 || d >= 64) return nullptr;
-  if (!h[d]) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cs);
-    if (cs != cudaStreamCaptureStatusNone) return nullptr;
-    cublasHandle_t hh;
-    if (cublasCreate(&hh) != CUBLAS_STATUS_SUCCESS) return nullptr;
-    void* ws = nullptr;
-    const size_t wsb = 32u << 20;
-    if (cudaMalloc(&ws, wsb) != cudaSuccess) {
-      cublasDestroy(hh);
-      return nullptr;
-    }
-    cublasSetWorkspace(hh, ws, wsb);
-    cublasSetAtomicsMode(hh, CUBLAS_ATOMICS_NOT_ALLOWED);  // deterministic
-    h[d] = hh;
-  }
-  return h[d];
-}
-
-// creates the cuBLAS handle of the current device (call outside graph capture)
+// out (ca x cb) = A^T B; A (rows x ca), B (rows x cb).  No library GEMM: the large
+// products run on k_atb_mma (FP64 tensor cores), the small square ones on nmfb_grams.
+// Kept for ABI compatibility (it created the cuBLAS handle of earlier versions).
 extern "C" int nmfb_blas_init(void* stream) {
-  return atb_handle((cudaStream_t)stream) != nullptr ? NMFB_OK : NMFB_ELAUNCH;
+  (void)stream;
+  return NMFB_OK;
 }
 
 extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, long cb,
@@ -1183,19 +1233,24 @@ extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, lo
       nmfb_grams_work_len(rows, ca, 1) <= work_len)
     return nmfb_grams(1, A, B, out, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                       nullptr, nullptr, rows, ca, work, work_len, stream);
-  // large products: cuBLAS DGEMM on the FP64 tensor cores.  Row-major out = A^T B is
-  // column-major out^T = B_c A_c^T with A_c = A^T (ca x rows), B_c (cb x rows).
-  if (2.0 * (double)rows * (double)ca * (double)cb >= 1e7 && rows <= 0x7fffffffL) {
-    cublasHandle_t h = atb_handle(st);
-    if (h != nullptr) {
-      cublasSetStream(h, st);
-      const double one = 1.0, zero = 0.0;
-      if (cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)cb, (int)ca, (int)rows, &one, B, (int)cb,
-                      A, (int)ca, &zero, out, (int)cb) == CUBLAS_STATUS_SUCCESS) {
-        ++g_nmfb_launches;
-        NMFB_CHECK_LAUNCH();
-        return NMFB_OK;
-      }
+  // large products: split-K DMMA (k_atb_mma), fixed-order finish
+  if (2.0 * (double)rows * (double)ca * (double)cb >= 1e6) {
+    const long tiles = ((ca + ATB_T - 1) / ATB_T) * ((cb + ATB_T - 1) / ATB_T);
+    long ns = (148 * 2 + tiles - 1) / tiles;
+    const long max_ns = (rows + 127) / 128;
+    if (ns > max_ns) ns = max_ns;
+    if (ns < 1) ns = 1;
+    long stripe = (rows + ns - 1) / ns;
+    stripe = ((stripe + ATB_R - 1) / ATB_R) * ATB_R;
+    ns = (rows + stripe - 1) / stripe;
+    if (ns * ca * cb <= work_len) {
+      dim3 grid((unsigned)((ca + ATB_T - 1) / ATB_T), (unsigned)((cb + ATB_T - 1) / ATB_T),
+                (unsigned)ns);
+      ++g_nmfb_launches, k_atb_mma<<<grid, 256, 0, st>>>(A, rows, ca, B, cb, stripe, work);
+      ++g_nmfb_launches, k_sum_parts<<<(unsigned)((ca * cb + 255) / 256), 256, 0, st>>>(
+          work, (int)ns, ca * cb, out);
+      NMFB_CHECK_LAUNCH();
+      return NMFB_OK;
     }
   }
   const long tiles = ((ca + 31) / 32) * ((cb + 31) / 32);
