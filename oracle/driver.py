@@ -208,14 +208,36 @@ def update_X(X, Yt, M, pX, mode, cfg, row_norm2, comm=None):
 
 
 def update_Y(X, Yt, M, pY, mode, cfg, col_norm2, comm=None):
-    """columns of Y <- NNLS(C = X, d = M_:,j) (Grams summed over ranks)."""
+    """columns of Y <- NNLS(C = X, d = M_:,j) (Grams summed over ranks).
+
+    With ``comm``: every rank solves its column range (dist.row_range over m) and the
+    columns are all-gathered, as the device solver does (paper_2101_08431_b200/dist.py)."""
     ctc = _red(comm, X.T @ X)
     ctb = _red(comm, M.T @ X)
     tol = _nnls_tol(ctb, cfg.tol_kkt)
     k = X.shape[1]
-    y, p, ch, r2, st = K.nnls_batch(ctc, ctb, col_norm2, pY, mode, tol, 3 * k)
+    if comm is None or not comm.active:
+        y, p, ch, r2, st = K.nnls_batch(ctc, ctb, col_norm2, pY, mode, tol, 3 * k)
+        _raise_status(st, "update_Y")
+        return y, p, ch, r2
+    import torch
+
+    from paper_2101_08431_b200.dist import row_range
+
+    m = ctb.shape[0]
+    a, b = row_range(m, comm.world, comm.rank)
+    ys, ps, chs, r2s, sts = K.nnls_batch(ctc, ctb[a:b].copy(), col_norm2[a:b].copy(),
+                                         pY[a:b].copy(), mode, tol[a:b].copy(), 3 * k)
+    out = []
+    for loc, shape, dt in ((ys, (m, k), torch.float64), (ps, (m, k), torch.uint8),
+                           (chs, (m,), torch.int64), (r2s, (m,), torch.float64),
+                           (sts, (m,), torch.int8)):
+        t = torch.zeros(shape, dtype=dt)
+        t[a:b] = torch.as_tensor(np.asarray(loc)).to(dt).reshape((b - a,) + shape[1:])
+        out.append(comm.allgather_rows(t).numpy())
+    y, p, ch, r2, st = out
     _raise_status(st, "update_Y")
-    return y, p, ch, r2
+    return y, p.astype(bool), ch, r2
 
 
 @dataclass

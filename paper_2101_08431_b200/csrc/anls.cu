@@ -825,7 +825,7 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
 constexpr int DP_CW = 256;  // columns per chunk (8 warps x 32)
 constexpr int DP_RB = 64;   // rows per exchange block (8 tiles of 8)
 
-template <int NT, typename T>
+template <int NT, typename T, bool SH>
 __global__ void __launch_bounds__(256, 2) k_dualprod_mma(const T* __restrict__ A, long rows,
                                                          long cols, const double* __restrict__ B1,
                                                          const double* __restrict__ B2, int K,
@@ -884,9 +884,22 @@ __global__ void __launch_bounds__(256, 2) k_dualprod_mma(const T* __restrict__ A
         for (int nt = 0; nt < NT; ++nt)
           b2[u][nt] = (ok && nt * 8 + g < K) ? __ldg(B2 + i * K + nt * 8 + g) : 0.0;
       }
-      // row-product operands: row rbase + g, columns 8q + 2t (+1)
+      // row-product operands: row rbase + g, columns 8q + 2t (+1).  SH: permuted out of
+      // the column-product registers (lane 16(q&1) + 4t + (g&3) holds them in
+      // ac[g>>2][q>>1]); else a second load of the same bytes (L1)
       double2 ar[4];
-      {
+      if constexpr (SH) {
+        const bool hi = (g >> 2) != 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int src = 16 * (q & 1) + 4 * t + (g & 3);
+          const double x0 = __shfl_sync(0xffffffffu, ac[0][q >> 1].x, src);
+          const double y0 = __shfl_sync(0xffffffffu, ac[0][q >> 1].y, src);
+          const double x1 = __shfl_sync(0xffffffffu, ac[1][q >> 1].x, src);
+          const double y1 = __shfl_sync(0xffffffffu, ac[1][q >> 1].y, src);
+          ar[q] = hi ? make_double2(x1, y1) : make_double2(x0, y0);
+        }
+      } else {
         const long i = rbase + g;
         const bool ok = i < re;
 #pragma unroll
@@ -974,11 +987,22 @@ int launch_dualprod(const T* A, long rows, long cols, const double* B1, const do
   double* partR = work;
   double* partC = work + needR;
   const size_t smem = (size_t)(DP_CW / 8 * 2 * NT * 32 + 8 * DP_RB * NT * 8) * sizeof(double);
-  cudaFuncSetAttribute(k_dualprod_mma<NT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  static const int variant = [] {
+    const char* e = getenv("NMFB_DUAL_VARIANT");
+    return e ? atoi(e) : 1;
+  }();
   dim3 grid((unsigned)d.nch, (unsigned)d.nsplit);
-  ++g_nmfb_launches, k_dualprod_mma<NT, T><<<grid, 256, smem, st>>>(A, rows, cols, B1, B2, K,
-                                                                      d.rps, partR, partC);
+  if (variant == 1) {
+    cudaFuncSetAttribute(k_dualprod_mma<NT, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    ++g_nmfb_launches, k_dualprod_mma<NT, T, true><<<grid, 256, smem, st>>>(
+        A, rows, cols, B1, B2, K, d.rps, partR, partC);
+  } else {
+    cudaFuncSetAttribute(k_dualprod_mma<NT, T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    ++g_nmfb_launches, k_dualprod_mma<NT, T, false><<<grid, 256, smem, st>>>(
+        A, rows, cols, B1, B2, K, d.rps, partR, partC);
+  }
   ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(partR, (int)d.nch,
                                                                          rows * K, outR, nullptr, 1.0);
   ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(cols), 256, 0, st>>>(partC, (int)d.nsplit,

@@ -294,6 +294,20 @@ __global__ void __launch_bounds__(256) k_atb_partial(const double* __restrict__ 
   }
 }
 
+// out[e] = sum_s part[s][e]: one warp per entry, lanes stride the partials, fixed butterfly
+__global__ void __launch_bounds__(256) k_sum_parts_warp(const double* __restrict__ part,
+                                                        int nparts, long len,
+                                                        double* __restrict__ out) {
+  const long e = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (e >= len) return;
+  double v = 0.0;
+  for (int s = lane; s < nparts; s += 32) v += part[(long)s * len + e];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) out[e] = v;
+}
+
 __global__ void k_sum_parts(const double* __restrict__ part, int nparts, long len,
                             double* __restrict__ out) {
   const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1194,7 +1208,7 @@ extern "C" long nmfb_atb_work_len(long rows, long ca, long cb) {
   long len = ns * ca * cb;
   {  // k_atb_mma stripes (see nmfb_atb)
     const long t64 = ((ca + 63) / 64) * ((cb + 63) / 64);
-    long n2 = (148 * 2 + t64 - 1) / t64;
+    long n2 = (148 + t64 - 1) / t64;
     const long mx = (rows + 127) / 128;
     if (n2 > mx) n2 = mx;
     if (n2 < 1) n2 = 1;
@@ -1236,7 +1250,7 @@ extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, lo
   // large products: split-K DMMA (k_atb_mma), fixed-order finish
   if (2.0 * (double)rows * (double)ca * (double)cb >= 1e6) {
     const long tiles = ((ca + ATB_T - 1) / ATB_T) * ((cb + ATB_T - 1) / ATB_T);
-    long ns = (148 * 2 + tiles - 1) / tiles;
+    long ns = (148 + tiles - 1) / tiles;  // one wave
     const long max_ns = (rows + 127) / 128;
     if (ns > max_ns) ns = max_ns;
     if (ns < 1) ns = 1;
@@ -1247,7 +1261,7 @@ extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, lo
       dim3 grid((unsigned)((ca + ATB_T - 1) / ATB_T), (unsigned)((cb + ATB_T - 1) / ATB_T),
                 (unsigned)ns);
       ++g_nmfb_launches, k_atb_mma<<<grid, 256, 0, st>>>(A, rows, ca, B, cb, stripe, work);
-      ++g_nmfb_launches, k_sum_parts<<<(unsigned)((ca * cb + 255) / 256), 256, 0, st>>>(
+      ++g_nmfb_launches, k_sum_parts_warp<<<(unsigned)((ca * cb * 32 + 255) / 256), 256, 0, st>>>(
           work, (int)ns, ca * cb, out);
       NMFB_CHECK_LAUNCH();
       return NMFB_OK;

@@ -13,9 +13,12 @@ replicated.  The exchanges are exactly the contractions over rows:
                        fraction-to-boundary minima                 min
                        maxima for the transition                   max
 
-The Y-side NNLS, the reduced (k^2 capacitance or dense mk) solve and all
-replicated updates run redundantly on every rank with identical inputs, so
-their (deterministic) results are identical everywhere and need no
+The Y-side NNLS of stage 1 is split by columns: every rank solves the columns
+row_range(m, world, rank) of the all-reduced X^T M and the columns (with their
+passive sets, residuals and statuses) are all-gathered (north_star: "each solves
+m/p ... followed by an allgather").  The stage-2 reduced (k^2 capacitance or dense
+mk) solve and the replicated updates run redundantly on every rank with identical
+inputs, so their (deterministic) results are identical everywhere and need no
 broadcast.  ``Comm`` wraps torch.distributed (NCCL on GPUs, gloo on CPU);
 ``Comm.single()`` is the no-op used on one GPU.
 """
@@ -77,6 +80,26 @@ class Comm:
         import torch.distributed as dist
 
         return self._ar(t, dist.ReduceOp.MIN) if self.world > 1 else t
+
+    def allgather_rows(self, t: torch.Tensor) -> torch.Tensor:
+        """t (rows, ...): every rank filled rows row_range(rows, world, rank); afterwards
+        every rank holds all rows (padded equal-size all_gather; NCCL or gloo)."""
+        if self.world == 1 or t.shape[0] == 0:
+            return t
+        import torch.distributed as dist
+
+        rows = t.shape[0]
+        chunk = (rows + self.world - 1) // self.world
+        a, b = row_range(rows, self.world, self.rank)
+        send = torch.zeros((chunk,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        send[: b - a] = t[a:b]
+        recv = [torch.empty_like(send) for _ in range(self.world)]
+        dist.all_gather(recv, send, group=self.group)
+        for r in range(self.world):
+            ar, br = row_range(rows, self.world, r)
+            if r != self.rank:
+                t[ar:br] = recv[r][: br - ar]
+        return t
 
     def sum_float(self, v: float, device=None) -> float:
         if self.world == 1:

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .dist import Comm
+from .dist import Comm, row_range
 from .config import (IpmParams, IpmResult, SolveReport, Stage1Config, Stage1Result,
                      TransitionParams)
 from .errors import (DegenerateFactor, LineSearchStall, NativeLibraryError,
@@ -317,9 +317,20 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
         P.colprod(P.M, n, m, Xn, k, ctbY, tolY, P.f32, reduce=True)
         if tol_fixed is not None:
             tolY.fill_(float(tol_fixed))
-        P._call("nmfb_nnls_batch_ws", _p(GX), _p(ctbY), _p(P.col_n2), _p(pY), mode,
-                _p(tolY), 3 * k, m, k, _p(Yn), _p(pYn), _p(chY), _p(r2Y), _p(stY), None, None,
-                _p(P.ftab), P.ftab_len, s)
+        if P.comm.active:
+            # columns split over the ranks, then all-gathered (dist.py)
+            c0, c1 = row_range(m, P.comm.world, P.comm.rank)
+            if c1 > c0:
+                P._call("nmfb_nnls_batch_ws", _p(GX), _p(ctbY[c0:]), _p(P.col_n2[c0:]),
+                        _p(pY[c0:]), mode, _p(tolY[c0:]), 3 * k, c1 - c0, k, _p(Yn[c0:]),
+                        _p(pYn[c0:]), _p(chY[c0:]), _p(r2Y[c0:]), _p(stY[c0:]), None, None,
+                        _p(P.ftab), P.ftab_len, s)
+            for t_ in (Yn, pYn, r2Y, stY):
+                P.comm.allgather_rows(t_)
+        else:
+            P._call("nmfb_nnls_batch_ws", _p(GX), _p(ctbY), _p(P.col_n2), _p(pY), mode,
+                    _p(tolY), 3 * k, m, k, _p(Yn), _p(pYn), _p(chY), _p(r2Y), _p(stY), None, None,
+                    _p(P.ftab), P.ftab_len, s)
         ny = P.ny_local
         if nosync:
             P._call("nmfb_stage1_stats", _p(X), _p(Xn), n * k, _p(Yt), _p(Yn), m * k * ny,
