@@ -825,7 +825,32 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
 constexpr int DP_CW = 256;  // columns per chunk (8 warps x 32)
 constexpr int DP_RB = 64;   // rows per exchange block (8 tiles of 8)
 
-template <int NT, typename T, bool SH>
+template <int NT>
+struct DualTile {
+  double2 ac[2][2];  // column-product layout: rows {t, 4+t}, columns 16h + 2g (+1)
+  double b2[2][NT];  // B2 rows {t, 4+t}, p = 8 nt + g
+};
+
+template <int NT, typename T>
+__device__ __forceinline__ void dual_load(DualTile<NT>& d, const T* __restrict__ A,
+                                          const double* __restrict__ B2, long cols, int K,
+                                          long rbase, long re, long jw, const bool (&cok)[2],
+                                          int g, int t) {
+  const double2 z2 = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const long i = rbase + 4 * u + t;
+    const bool ok = i < re;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      d.ac[u][h] = (ok && cok[h]) ? ld2<T>(A + i * cols + jw + 16 * h + 2 * g) : z2;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+      d.b2[u][nt] = (ok && nt * 8 + g < K) ? __ldg(B2 + i * K + nt * 8 + g) : 0.0;
+  }
+}
+
+template <int NT, typename T>
 __global__ void __launch_bounds__(256, 2) k_dualprod_mma(const T* __restrict__ A, long rows,
                                                          long cols, const double* __restrict__ B1,
                                                          const double* __restrict__ B2, int K,
@@ -833,7 +858,7 @@ __global__ void __launch_bounds__(256, 2) k_dualprod_mma(const T* __restrict__ A
                                                          double* __restrict__ partR,
                                                          double* __restrict__ partC) {
   extern __shared__ __align__(16) double dsm[];
-  double* sB = dsm;                        // [CW/8][2][NT][32] B1 fragments of the chunk
+  double* sB = dsm;                            // [CW/8][2][NT][32] B1 fragments of the chunk
   double* xb = dsm + DP_CW / 8 * 2 * NT * 32;  // [8 warps][DP_RB][NT*8] row-partial exchange
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -849,11 +874,9 @@ __global__ void __launch_bounds__(256, 2) k_dualprod_mma(const T* __restrict__ A
   const long jw = j0 + 32 * warp;  // this warp's first column
   const long rb = (long)blockIdx.y * rows_per_split;
   const long re = min(rows, rb + rows_per_split);
-  bool cok[2], rokc[4];
+  bool cok[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) cok[h] = jw + 16 * h + 2 * g < cols;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) rokc[q] = jw + 8 * q + 2 * t < cols;
   double accC[2][2][NT][2];
 #pragma unroll
   for (int h = 0; h < 2; ++h)
@@ -861,89 +884,69 @@ __global__ void __launch_bounds__(256, 2) k_dualprod_mma(const T* __restrict__ A
     for (int par = 0; par < 2; ++par)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) accC[h][par][nt][0] = accC[h][par][nt][1] = 0.0;
-  const double2 z2 = make_double2(0.0, 0.0);
   double* xw = xb + (long)warp * DP_RB * NT * 8;
-  for (long r0 = rb; r0 < re; r0 += DP_RB) {
-#pragma unroll 2
-    for (int rt = 0; rt < DP_RB / 8; ++rt) {
-      const long rbase = r0 + 8 * rt;
-      double accR[NT][2];
+  const bool hi = (g >> 2) != 0;
+  // software pipeline: the operands of tile i+1 are in flight while tile i is computed
+  DualTile<NT> cur, nxt;
+  const long ntile = (re - rb + 7) / 8;
+  if (ntile > 0) dual_load<NT, T>(cur, A, B2, cols, K, rb, re, jw, cok, g, t);
+  for (long it = 0; it < ntile; ++it) {
+    const long rbase = rb + 8 * it;
+    if (it + 1 < ntile) dual_load<NT, T>(nxt, A, B2, cols, K, rbase + 8, re, jw, cok, g, t);
+    // column product: D(8 cols x 8 p) += M^T(8 cols x 4 rows) B2(4 rows x 8 p)
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) accR[nt][0] = accR[nt][1] = 0.0;
-      // column-product operands: rows rbase + t, rbase + 4 + t
-      double2 ac[2][2];
-      double b2[2][NT];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const long i = rbase + 4 * u + t;
-        const bool ok = i < re;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          ac[u][h] = (ok && cok[h]) ? ld2<T>(A + i * cols + jw + 16 * h + 2 * g) : z2;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-          b2[u][nt] = (ok && nt * 8 + g < K) ? __ldg(B2 + i * K + nt * 8 + g) : 0.0;
-      }
-      // row-product operands: row rbase + g, columns 8q + 2t (+1).  SH: permuted out of
-      // the column-product registers (lane 16(q&1) + 4t + (g&3) holds them in
-      // ac[g>>2][q>>1]); else a second load of the same bytes (L1)
-      double2 ar[4];
-      if constexpr (SH) {
-        const bool hi = (g >> 2) != 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int src = 16 * (q & 1) + 4 * t + (g & 3);
-          const double x0 = __shfl_sync(0xffffffffu, ac[0][q >> 1].x, src);
-          const double y0 = __shfl_sync(0xffffffffu, ac[0][q >> 1].y, src);
-          const double x1 = __shfl_sync(0xffffffffu, ac[1][q >> 1].x, src);
-          const double y1 = __shfl_sync(0xffffffffu, ac[1][q >> 1].y, src);
-          ar[q] = hi ? make_double2(x1, y1) : make_double2(x0, y0);
-        }
-      } else {
-        const long i = rbase + g;
-        const bool ok = i < re;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          ar[q] = (ok && rokc[q]) ? ld2<T>(A + i * cols + jw + 8 * q + 2 * t) : z2;
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            dmma(accC[h][0][nt][0], accC[h][0][nt][1], ac[u][h].x, b2[u][nt]);
-            dmma(accC[h][1][nt][0], accC[h][1][nt][1], ac[u][h].y, b2[u][nt]);
-          }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int grp = 4 * warp + q;  // 8-column group inside the chunk
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const double b0 = sB[((2 * grp) * NT + nt) * 32 + lane];
-          const double b1 = sB[((2 * grp + 1) * NT + nt) * 32 + lane];
-          dmma(accR[nt][0], accR[nt][1], ar[q].x, b0);
-          dmma(accR[nt][0], accR[nt][1], ar[q].y, b1);
-        }
-      }
-      // this warp's 32-column share of the tile's row products -> exchange buffer
+    for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
-        *reinterpret_cast<double2*>(xw + (8 * rt + g) * NT * 8 + nt * 8 + 2 * t) =
-            make_double2(accR[nt][0], accR[nt][1]);
-    }
-    // fixed-order sum of the 8 warps' shares of the block's 64 rows
-    __syncthreads();
-    for (int e = tid; e < DP_RB * K; e += 256) {
-      const int rr = e / K, pp = e - rr * K;
-      const long row = r0 + rr;
-      if (row >= re) continue;
-      double v = 0.0;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) v += xb[((long)w * DP_RB + rr) * NT * 8 + pp];
-      partR[((long)blockIdx.x * rows + row) * K + pp] = v;
+        for (int h = 0; h < 2; ++h) {
+          dmma(accC[h][0][nt][0], accC[h][0][nt][1], cur.ac[u][h].x, cur.b2[u][nt]);
+          dmma(accC[h][1][nt][0], accC[h][1][nt][1], cur.ac[u][h].y, cur.b2[u][nt]);
+        }
+    // row product: the fragments (row g, columns 8q + 2t, +1) are permuted out of the
+    // column-product registers: lane 16(q&1) + 4t + (g&3) holds them in ac[g>>2][q>>1]
+    double accR[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) accR[nt][0] = accR[nt][1] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int src = 16 * (q & 1) + 4 * t + (g & 3);
+      const double x0 = __shfl_sync(0xffffffffu, cur.ac[0][q >> 1].x, src);
+      const double y0 = __shfl_sync(0xffffffffu, cur.ac[0][q >> 1].y, src);
+      const double x1 = __shfl_sync(0xffffffffu, cur.ac[1][q >> 1].x, src);
+      const double y1 = __shfl_sync(0xffffffffu, cur.ac[1][q >> 1].y, src);
+      const double ax = hi ? x1 : x0, ay = hi ? y1 : y0;
+      const int grp = 4 * warp + q;  // 8-column group inside the chunk
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double b0 = sB[((2 * grp) * NT + nt) * 32 + lane];
+        const double b1 = sB[((2 * grp + 1) * NT + nt) * 32 + lane];
+        dmma(accR[nt][0], accR[nt][1], ax, b0);
+        dmma(accR[nt][0], accR[nt][1], ay, b1);
+      }
     }
-    __syncthreads();
+    // this warp's 32-column share of the tile's row products -> exchange buffer
+    const int rt = (int)(it & (DP_RB / 8 - 1));
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+      *reinterpret_cast<double2*>(xw + (8 * rt + g) * NT * 8 + nt * 8 + 2 * t) =
+          make_double2(accR[nt][0], accR[nt][1]);
+    if (rt == DP_RB / 8 - 1 || it + 1 == ntile) {
+      // fixed-order sum of the 8 warps' shares of the block's rows
+      __syncthreads();
+      const long r0 = rbase - 8 * rt;
+      for (int e = tid; e < DP_RB * K; e += 256) {
+        const int rr = e / K, pp = e - rr * K;
+        const long row = r0 + rr;
+        if (row >= re) continue;
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += xb[((long)w * DP_RB + rr) * NT * 8 + pp];
+        partR[((long)blockIdx.x * rows + row) * K + pp] = v;
+      }
+      __syncthreads();
+    }
+    cur = nxt;
   }
 #pragma unroll
   for (int h = 0; h < 2; ++h)
@@ -981,28 +984,26 @@ int launch_dualprod(const T* A, long rows, long cols, const double* B1, const do
                     double* outR, double* outC, double* work, long work_len, cudaStream_t st) {
   static_assert(K >= 1 && K <= 16, "K");
   constexpr int NT = (K + 7) / 8;
+  // measured on B200 (scripts/bench_dual.py): the fused pass wins for K <= 8 (c4 shape,
+  // k = 4: 276 us vs 331 us for the two streams); for 8 < K <= 16 its 8-warp row-partial
+  // exchange stalls the stream (357 vs 347 us at k = 10), so the two streaming products
+  // (each ~70 % of HBM) run back to back instead
+  if (K > 8) {
+    int rc = launch_rowprod<K, T>(A, rows, cols, B1, outR, nullptr, 1.0, work, work_len, st);
+    if (rc != NMFB_OK) return rc;
+    return launch_colprod<K, T>(A, rows, cols, B2, outC, nullptr, 1.0, work, work_len, st);
+  }
   const DualGrid d = dual_grid(rows, cols);
   const long needR = d.nch * rows * K, needC = d.nsplit * cols * K;
   if (needR + needC > work_len) return NMFB_ENOMEM;
   double* partR = work;
   double* partC = work + needR;
   const size_t smem = (size_t)(DP_CW / 8 * 2 * NT * 32 + 8 * DP_RB * NT * 8) * sizeof(double);
-  static const int variant = [] {
-    const char* e = getenv("NMFB_DUAL_VARIANT");
-    return e ? atoi(e) : 1;
-  }();
   dim3 grid((unsigned)d.nch, (unsigned)d.nsplit);
-  if (variant == 1) {
-    cudaFuncSetAttribute(k_dualprod_mma<NT, T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    ++g_nmfb_launches, k_dualprod_mma<NT, T, true><<<grid, 256, smem, st>>>(
-        A, rows, cols, B1, B2, K, d.rps, partR, partC);
-  } else {
-    cudaFuncSetAttribute(k_dualprod_mma<NT, T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    ++g_nmfb_launches, k_dualprod_mma<NT, T, false><<<grid, 256, smem, st>>>(
-        A, rows, cols, B1, B2, K, d.rps, partR, partC);
-  }
+  cudaFuncSetAttribute(k_dualprod_mma<NT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  ++g_nmfb_launches, k_dualprod_mma<NT, T><<<grid, 256, smem, st>>>(A, rows, cols, B1, B2, K,
+                                                                      d.rps, partR, partC);
   ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(partR, (int)d.nch,
                                                                          rows * K, outR, nullptr, 1.0);
   ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(cols), 256, 0, st>>>(partC, (int)d.nsplit,
@@ -1075,7 +1076,13 @@ extern "C" int nmfb_colprod(const void* A, int a_is_f32, long rows, long cols, c
 extern "C" long nmfb_dualprod_work_len(long rows, long cols, long k) {
   if (rows <= 0 || cols <= 0) return 1;
   const DualGrid d = dual_grid(rows, cols);
-  return d.nch * rows * k + d.nsplit * cols * k;
+  long len = d.nch * rows * k + d.nsplit * cols * k;
+  const long r = nmfb_rowprod_work_len(rows, cols, k, 0), r32 = nmfb_rowprod_work_len(rows, cols, k, 1);
+  const long c = nmfb_colprod_work_len(rows, cols, k);
+  if (r > len) len = r;
+  if (r32 > len) len = r32;
+  if (c > len) len = c;
+  return len;
 }
 
 extern "C" int nmfb_dualprod(const void* A, int a_is_f32, long rows, long cols, const double* B1,
