@@ -19,7 +19,7 @@ from oracle import driver as D
 
 class OracleStream:
     def __init__(self, M0, X0, Y0, tol_rel=1e-10, s1=None, ipm_factory=None):
-        self.M = np.array(M0, dtype=np.float64)
+        self.M = np.array(M0, dtype=np.float64)  # fp32 chunks are widened exactly
         self.tol_rel = tol_rel
         self.s1 = s1 or D.Stage1Config()
         self.ipm_factory = ipm_factory or D.IpmParams

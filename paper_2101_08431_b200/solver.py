@@ -59,8 +59,12 @@ def barrier_weights(n, m, barrier):
 class Problem:
     """M resident on one GPU plus every scratch buffer the solver needs."""
 
-    def __init__(self, M, k, device=None, comm: Comm | None = None):
-        """M: this rank's row block when ``comm`` spans several GPUs (dist.py)."""
+    def __init__(self, M, k, device=None, comm: Comm | None = None, m_capacity: int = 0):
+        """M: this rank's row block when ``comm`` spans several GPUs (dist.py).
+
+        m_capacity > m: room for appended columns (streaming, ``append_columns``): M lives
+        in one of two pre-allocated n x m_capacity buffers and every scratch buffer is sized
+        for m_capacity, so an append allocates nothing."""
         if not torch.cuda.is_available():
             raise NativeLibraryError("no CUDA device: the B200 solver has no CPU fallback")
         self.lib = _lib.load()
@@ -84,12 +88,21 @@ class Problem:
             self.M = self.M.double()
         self.f32 = int(self.M.dtype == torch.float32)
         self.n, self.m = self.M.shape
+        self.m_cap = max(int(m_capacity), self.m)
+        self._mbuf = None
+        if self.m_cap > self.m:
+            self._mbuf = [torch.empty(self.n * self.m_cap, dtype=self.M.dtype, device=self.dev)
+                          for _ in range(2)]
+            self._mcur = 0
+            view = self._mbuf[0][: self.n * self.m].view(self.n, self.m)
+            view.copy_(self.M)
+            self.M = view
         self.comm = comm or Comm.single()
         self.n_global = int(self.comm.sum_float(self.n, self.dev)) if self.comm.active else self.n
         self.k = int(k)
         if not 1 <= self.k <= 16:
             raise ValueError("k must be in [1, 16]")
-        n, m, k = self.n, self.m, self.k
+        n, m, k = self.n, self.m_cap, self.k
         f64 = dict(dtype=torch.float64, device=self.dev)
         L = self.lib
         cw = max(L.nmfb_colprod_work_len(n, m, k), L.nmfb_colprod_work_len(n, k, k),
@@ -97,15 +110,16 @@ class Problem:
                  L.nmfb_rowprod_work_len(n, m, k, self.f32), L.nmfb_rowprod_work_len(n, m, k, 0),
                  4096)
         self.cwork = torch.empty(cw, **f64)
-        self.gwork = torch.empty(max(self.lib.nmfb_grams_work_len(max(n, M.shape[1]), k, 4), 1),
+        self.gwork = torch.empty(max(self.lib.nmfb_grams_work_len(max(n, m), k, 4), 1),
                                  **f64)
         nb = L.nmfb_ipm_reduce_blocks()
         self.rwork = torch.empty(max(148 * 2 * NTRIALS, 12 * nb, 3 * ((n + 127) // 128 + nb), 4096),
                                  **f64)
         self.row_n2 = torch.empty(n, **f64)
-        self.col_n2 = torch.empty(m, **f64)
-        self._call("nmfb_sqnorms", _p(self.M), self.f32, n, m, _p(self.row_n2), _p(self.col_n2),
-                   _p(self.cwork), self.cwork.numel(), self.stream)
+        self._col_n2 = torch.empty(m, **f64)
+        self.col_n2 = self._col_n2[: self.m]
+        self._call("nmfb_sqnorms", _p(self.M), self.f32, n, self.m, _p(self.row_n2),
+                   _p(self.col_n2), _p(self.cwork), self.cwork.numel(), self.stream)
         self.comm.sum_(self.col_n2)
         self.mnorm2_local = float(self.row_n2.sum().item())  # ||M_rank||^2 (F-free objective)
         self._call("nmfb_blas_init", self.stream)  # cuBLAS handle, outside any graph capture
@@ -116,6 +130,34 @@ class Problem:
         self.iscal = torch.zeros(16, dtype=torch.int32, device=self.dev)
         self.hscal = torch.zeros(256, dtype=torch.float64).pin_memory()
         self.hint = torch.zeros(16, dtype=torch.int32).pin_memory()
+
+    def append_columns(self, Mnew):
+        """Append columns (n, c) -- host or device, fp32 or fp64 -- in place: the active
+        M moves once into the other pre-allocated buffer with the new columns behind it
+        (one device copy, no allocation), the squared row norms advance by the new block's
+        and its column norms are appended (csrc nmfb_sqnorms on the block only)."""
+        if isinstance(Mnew, np.ndarray):
+            Mnew = torch.from_numpy(np.ascontiguousarray(Mnew))
+        Mn = Mnew.to(self.dev, dtype=self.M.dtype).contiguous()
+        n, c = Mn.shape
+        if n != self.n:
+            raise ValueError("appended block must have the same rows")
+        m0, m1 = self.m, self.m + c
+        if self._mbuf is None or m1 > self.m_cap:
+            raise ValueError(f"column capacity {self.m_cap} exceeded ({m1})")
+        dst = self._mbuf[1 - self._mcur][: n * m1].view(n, m1)
+        dst[:, :m0].copy_(self.M)
+        dst[:, m0:].copy_(Mn)
+        self._mcur = 1 - self._mcur
+        self.M, self.m = dst, m1
+        rn = self.buf(n)
+        self.col_n2 = self._col_n2[:m1]
+        self._call("nmfb_sqnorms", _p(Mn), self.f32, n, c, _p(rn), _p(self.col_n2[m0:]),
+                   _p(self.cwork), self.cwork.numel(), self.stream)
+        self.comm.sum_(self.col_n2[m0:])
+        self.row_n2.add_(rn)
+        self.mnorm2_local = float(self.row_n2.sum().item())
+        return Mn
 
     # -- plumbing -----------------------------------------------------------
     @property
@@ -509,6 +551,19 @@ class IpmEngine:
                                       (self.YYpk, m, self.Dinvpk, self.Gpk)):
                 P._call("nmfb_atb", _p(A_), rows_, self.kk, _p(A_), self.kk, _p(O_),
                         _p(self.awork), self.awork.numel(), P.stream)
+
+    def reset(self, X, Yt, R, S, mu, p: IpmParams):
+        """Re-arm a cached engine at a new starting point (same problem, structure and rho):
+        buffers, factorizations and captured graphs are reused."""
+        self.X.copy_(X)
+        self.Yt.copy_(Yt)
+        self.R.copy_(R)
+        self.S.copy_(S)
+        self.mu, self.flag, self.p = float(mu), False, p
+        self.fi, self.fact_F, self.have_fact, self.fact_full = 0, 0, False, False
+        self.fact_dense = self.last_dense = False
+        if self.ffree:
+            self.mvalid = False
 
     # -- helpers -------------------------------------------------------------
     @property
@@ -947,7 +1002,35 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
     """
     p = p or IpmParams()
     t0 = time.perf_counter()
-    eng = IpmEngine(P, X, Yt, R, S, mu, rho, p)
+    eng = _engine(P, X, Yt, R, S, mu, rho, p)
+    try:
+        return eng, _run_ipm(P, eng, p, t0)
+    finally:  # the caller's tensors hold the final point (in-place contract)
+        for dst, src in ((X, eng.X), (Yt, eng.Yt), (R, eng.R), (S, eng.S)):
+            if dst is not src:
+                dst.copy_(src)
+
+
+def _engine(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams):
+    """The IpmEngine for this problem and parameter structure, cached on the Problem: a
+    repeated solve (bench steps, streaming chunks of the same width, restarts) reuses
+    its buffers and captured CUDA graphs instead of re-allocating and re-capturing."""
+    key = (P.m, P.M.data_ptr(), float(rho), p.barrier, p.schur_solver, p.residual,
+           p.use_graphs, p.fused_small, p.persistent, p.persist_grid, p.tau, p.eta,
+           p.max_backtracks)
+    cache = P.__dict__.setdefault("_engines", {})
+    eng = cache.get(key)
+    if eng is None:
+        if len(cache) >= 4:
+            cache.clear()
+        eng = IpmEngine(P, X.clone(), Yt.clone(), R.clone(), S.clone(), mu, rho, p)
+        cache[key] = eng
+    else:
+        eng.reset(X, Yt, R, S, mu, p)
+    return eng
+
+
+def _run_ipm(P: Problem, eng, p: IpmParams, t0):
     cap = p.fixed_iters if p.fixed_iters > 0 else p.max_iter
     tol = 0.0 if p.fixed_iters > 0 else p.eps_tol
     e_mu, e_zero, fsq, sums = eng.refresh()
@@ -1090,7 +1173,7 @@ def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
     res.converged = e_zero <= tol
     res.mu, res.flag = eng.mu, eng.flag
     res.seconds = time.perf_counter() - t0
-    return eng, res
+    return res
 
 
 def transition(P: Problem, X, Yt, eps_tol, tp: TransitionParams | None = None):
@@ -1155,6 +1238,14 @@ def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1: Stage1Config | None = None,
     X0n = X0 if isinstance(X0, torch.Tensor) else np.asarray(X0, dtype=np.float64)
     k = X0n.shape[1]
     P = problem or Problem(M, k, comm=comm)
+
+    def carry(c):
+        if c is None:
+            return None
+        if isinstance(c, torch.Tensor):
+            return c.to(P.dev, dtype=torch.uint8)
+        return torch.as_tensor(np.asarray(c, np.uint8)).to(P.dev)
+
     X = P.to_dev(X0)
     Yt = P.to_dev(Y0.T if not isinstance(Y0, torch.Tensor) else Y0.t())
     if e_scale is None:
@@ -1167,8 +1258,7 @@ def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1: Stage1Config | None = None,
         r1 = Stage1Result(None, None, None, None, 0, False)
         pXd = pYd = None
     else:
-        pXd = None if pX is None else torch.as_tensor(np.asarray(pX, np.uint8)).to(P.dev)
-        pYd = None if pY is None else torch.as_tensor(np.asarray(pY, np.uint8)).to(P.dev)
+        pXd, pYd = carry(pX), carry(pY)
         X, Yt, pXd, pYd, r1 = run_stage1(P, X, Yt, s1, pXd, pYd)
     r1.X, r1.Yt = X.cpu().numpy(), Yt.cpu().numpy()
     r1.pX = None if pXd is None else pXd.bool().cpu().numpy()
@@ -1181,6 +1271,9 @@ def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1: Stage1Config | None = None,
     eng, r2 = run_ipm(P, X, Yt, R, S, mu, rho, p)
     e_mu, e_zero, fsq, _ = eng.refresh()
     status = "Converged" if r2.converged else "IterationCap"
-    return SolveReport(status, eng.X.cpu().numpy(), eng.Yt.cpu().numpy(), eng.R.cpu().numpy(),
-                       eng.S.cpu().numpy(), 0.5 * fsq, e_zero, eps_abs, r1, r2, r1.seconds,
-                       r2.seconds)
+    rep = SolveReport(status, eng.X.cpu().numpy(), eng.Yt.cpu().numpy(), eng.R.cpu().numpy(),
+                      eng.S.cpu().numpy(), 0.5 * fsq, e_zero, eps_abs, r1, r2, r1.seconds,
+                      r2.seconds)
+    # device-resident final factors and stage-1 carries (streaming sessions continue from them)
+    rep.dev_state = {"X": eng.X, "Yt": eng.Yt, "pX": pXd, "pY": pYd}
+    return rep

@@ -9,6 +9,13 @@ DESIGN.md (item 8) and restated by oracle/stream.py for the parity tests:
     _kernels_numba.py:312-315), extends the passive-set carries and re-runs the
     two-stage solve warm from (X, Y) and the carries (stage-1 mode 2 from sweep 0).
 
+Device residency: one ``Problem`` for the whole session with room for ``m_max`` columns
+(M in two pre-allocated n x m_max buffers, every scratch buffer sized for m_max; an
+append moves M once into the other buffer behind which the new columns land, and
+advances the row / column norms by the new block only); X, Y and the passive-set
+carries stay on the device between chunks.  Chunks may be fp32 or fp64 (converted on
+the device to the session's storage type).
+
 Per-chunk wall times are recorded in ``chunks`` as (m, seconds, SolveReport).
 """
 from __future__ import annotations
@@ -25,59 +32,73 @@ from .errors import status_error
 
 class StreamSession:
     def __init__(self, M0, X0, Y0, tol_rel=1e-10, cfg: Stage1Config | None = None,
-                 ipm_factory=IpmParams):
+                 ipm_factory=IpmParams, m_max: int | None = None, dtype=torch.float64):
         self.tol_rel = tol_rel
         self.cfg = cfg or Stage1Config()
         self.ipm_factory = ipm_factory
         dev = torch.device("cuda", torch.cuda.current_device())
-        self.Md = torch.as_tensor(np.ascontiguousarray(M0, dtype=np.float64)).to(dev)
-        self.n = self.Md.shape[0]
-        self.k = np.asarray(X0).shape[1]
+        M0 = torch.as_tensor(np.ascontiguousarray(M0)) if isinstance(M0, np.ndarray) else M0
+        M0 = M0.to(dev, dtype=dtype)
+        self.n = M0.shape[0]
+        self.k = np.asarray(X0).shape[1] if not isinstance(X0, torch.Tensor) else X0.shape[1]
         self.chunks = []
         t0 = time.perf_counter()
-        P = solver.Problem(self.Md, self.k)
-        rep = solver.run_two_stage(self.Md, X0, Y0, tol_rel, self.cfg, self.ipm_factory(),
-                                   problem=P)
+        cap = max(int(m_max or 0), 2 * M0.shape[1])
+        self.P = solver.Problem(M0, self.k, m_capacity=cap)
+        rep = solver.run_two_stage(None, X0, Y0, tol_rel, self.cfg, self.ipm_factory(),
+                                   problem=self.P)
         torch.cuda.synchronize()
         self._keep(rep, time.perf_counter() - t0)
 
     def _keep(self, rep, secs):
-        self.X, self.Yt = rep.X, rep.Yt
-        self.pX, self.pY = rep.stage1.pX, rep.stage1.pY
-        self.chunks.append((self.Md.shape[1], secs, rep))
+        d = rep.dev_state
+        self.X, self.Yt, self.pX, self.pY = d["X"], d["Yt"], d["pX"], d["pY"]
+        self.chunks.append((self.P.m, secs, rep))
 
     @property
     def m(self):
-        return self.Md.shape[1]
+        return self.P.m
+
+    @property
+    def Md(self):
+        return self.P.M
+
+    def _grow(self, extra):
+        """Capacity exceeded: one new Problem with twice the room (rare)."""
+        P = self.P
+        self.P = solver.Problem(P.M, self.k, m_capacity=2 * (P.m + extra))
 
     def append(self, Mnew):
-        """Add columns (n, c) and re-solve warm; returns the chunk's SolveReport."""
+        """Add columns (n, c) -- host or device, fp32 or fp64 -- and re-solve warm;
+        returns the chunk's SolveReport."""
         t0 = time.perf_counter()
-        dev = self.Md.device
-        Mn = torch.as_tensor(np.ascontiguousarray(Mnew, dtype=np.float64)).to(dev)
-        c, k = Mn.shape[1], self.k
-        Pn = solver.Problem(Mn, k)  # btb = column norms of the new block
-        X = Pn.to_dev(self.X)
-        ctc, ctb, tol = Pn.buf(k, k), Pn.buf(c, k), Pn.buf(c)
-        Pn.colprod(X, self.n, k, X, k, ctc)
-        Pn.colprod(Mn, self.n, c, X, k, ctb, tol)
-        y, p = Pn.buf(c, k), Pn.buf(c, k, dtype=torch.uint8)
-        ch, r2 = Pn.buf(c, dtype=torch.int64), Pn.buf(c)
-        st = Pn.buf(c, dtype=torch.int8)
-        seed, flag = torch.zeros((c, k), dtype=torch.uint8, device=dev), Pn.buf(1, dtype=torch.int32)
+        c = Mnew.shape[1]
+        if self.P.m + c > self.P.m_cap:
+            self._grow(c)
+        P, k = self.P, self.k
+        m0 = P.m
+        Mn = P.append_columns(Mnew)  # (n, c) on the device in the storage type
+        X = self.X
+        ctc, ctb, tol = P.buf(k, k), P.buf(c, k), P.buf(c)
+        P.colprod(X, self.n, k, X, k, ctc)
+        P.colprod(Mn, self.n, c, X, k, ctb, tol, P.f32)
+        y, p = P.buf(c, k), P.buf(c, k, dtype=torch.uint8)
+        ch, r2 = P.buf(c, dtype=torch.int64), P.buf(c)
+        st = P.buf(c, dtype=torch.int8)
+        seed = torch.zeros((c, k), dtype=torch.uint8, device=P.dev)
+        flag = P.buf(1, dtype=torch.int32)
         _p = solver._p
-        Pn._call("nmfb_surface_nnls_batch", _p(ctc), _p(ctb), _p(Pn.col_n2), _p(seed), 1, _p(tol),
-                 3 * k, c, k, _p(y), _p(p), _p(ch), _p(r2), _p(st), _p(seed), _p(flag), Pn.stream)
+        P._call("nmfb_surface_nnls_batch", _p(ctc), _p(ctb), _p(P.col_n2[m0:]), _p(seed), 1,
+                _p(tol), 3 * k, c, k, _p(y), _p(p), _p(ch), _p(r2), _p(st), _p(seed), _p(flag),
+                P.stream)
         bad = torch.nonzero(st).flatten()
         if bad.numel():
             i = int(bad[0])
             raise status_error(int(st[i]), i, "stream append")
-        self.Md = torch.cat([self.Md, Mn], dim=1).contiguous()
-        Yt = np.vstack([self.Yt, y.cpu().numpy()])
-        pY = np.vstack([self.pY, p.bool().cpu().numpy()])
-        P = solver.Problem(self.Md, k)
-        rep = solver.run_two_stage(self.Md, self.X, Yt.T, self.tol_rel, self.cfg,
-                                   self.ipm_factory(), pX=self.pX, pY=pY, problem=P)
+        Yt = torch.cat([self.Yt, y])
+        pY = torch.cat([self.pY, p]) if self.pY is not None else None
+        rep = solver.run_two_stage(None, X, Yt.t(), self.tol_rel, self.cfg, self.ipm_factory(),
+                                   pX=self.pX, pY=pY, problem=P)
         torch.cuda.synchronize()
         self._keep(rep, time.perf_counter() - t0)
         return rep
