@@ -276,6 +276,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     launches0 = P.lib.nmfb_launch_count() + P.graph_kernel_launches
     total_ms, s1_ms, s2_ms, sweeps, iters, fobj = 0.0, 0.0, 0.0, 0, 0, float("nan")
+    torch.cuda.nvtx.range_push("bench_timed")  # ncu --nvtx-include bench_timed/ (launch lists)
     for _ in range(args.steps):
         ev, s, i, fobj = step()
         ev[2].synchronize()
@@ -284,6 +285,7 @@ def run_b200(args):
         s2_ms += ev[1].elapsed_time(ev[2])
         sweeps, iters = sweeps + s, iters + i
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     if ws > 1:
         torch.distributed.barrier()
     launches = P.lib.nmfb_launch_count() + P.graph_kernel_launches - launches0

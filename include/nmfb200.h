@@ -300,6 +300,12 @@ int nmfb_ffree_quartic(const double *A1, const double *A2, const double *XX, con
 
 /* number of kernel launches issued by this library so far (host counter) */
 unsigned long long nmfb_launch_count(void);
+/* Select the TMA-fed fp64 streaming products (1, default) or the register-direct DMMA
+ * kernels (0) for nmfb_rowprod / nmfb_colprod; -1 only queries.  Returns the previous
+ * setting.  (Both are deterministic; the row products are bit-identical.) */
+int nmfb_tma_products(int on);
+/* Name of the last CUDA error behind an NMFB_ELAUNCH return ("no error" if none). */
+const char *nmfb_last_cuda_error(void);
 
 
 /* Persistent Gauss-Newton inner loop for small problems (csrc/persist.cu): one

@@ -23,6 +23,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC,
 SOURCES = {
     "surface.cu": ["-fmad=false"],
     "anls.cu": [],
+    "tma_prod.cu": [],
     "ipm.cu": [],
     "dense.cu": [],
     "lowrank.cu": [],

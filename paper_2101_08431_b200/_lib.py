@@ -68,6 +68,8 @@ SIGNATURES = {
     "nmfb_dense_cholesky": [P, L, P, P],
     "nmfb_dense_solve": [P, L, P, P],
     "nmfb_launch_count": [],
+    "nmfb_last_cuda_error": [],
+    "nmfb_tma_products": [I],
     "nmfb_d_factor": [P, P, P, D, L, L, P, P, P, P, P],
     "nmfb_ffree_grad_rows": [P, P, P, L, L, P, P, P],
     "nmfb_ffree_fsq": [P, D, P, P, L, P, P, P],
@@ -90,7 +92,7 @@ SIGNATURES = {
     "nmfb_lowrank_solve": [P, P, P, P, P, L, L, P, P, P, P, P, L, P],
 }
 RESTYPES = {"nmfb_dualprod_work_len": ctypes.c_long, "nmfb_nnls_ftab_len": ctypes.c_long, "nmfb_colprod_work_len": ctypes.c_long, "nmfb_rowprod_work_len": ctypes.c_long, "nmfb_atb_work_len": ctypes.c_long,
-            "nmfb_launch_count": ctypes.c_ulonglong, "nmfb_small_work_len": ctypes.c_long,
+            "nmfb_launch_count": ctypes.c_ulonglong, "nmfb_last_cuda_error": ctypes.c_char_p, "nmfb_small_work_len": ctypes.c_long,
             "nmfb_persist_work_len": ctypes.c_long, "nmfb_grams_work_len": ctypes.c_long,
             "nmfb_term4_work_len": ctypes.c_long,
             "nmfb_stage1_persist_work_len": ctypes.c_long}

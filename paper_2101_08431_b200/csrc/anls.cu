@@ -15,10 +15,15 @@
 
 #include "common.cuh"
 #include "nmfb200.h"
+#include "tma_prod.cuh"
 
 unsigned long long g_nmfb_launches = 0;
 
 extern "C" unsigned long long nmfb_launch_count(void) { return g_nmfb_launches; }
+int g_nmfb_last_cuda_error = 0;
+extern "C" const char* nmfb_last_cuda_error(void) {
+  return cudaGetErrorString((cudaError_t)g_nmfb_last_cuda_error);
+}
 
 namespace {
 
@@ -707,6 +712,21 @@ int launch_rowprod(const T* A, long rows, long cols, const double* B, double* ou
     return e && e[0] == '1';
   }();
   const bool use_mma = !(sizeof(T) == 4 && f32_simt);
+  if (sizeof(T) == 8 && rowprod_split(rows, cols) && K >= 5) {  // TMA-fed DMMA (tma_prod.cu)
+    long nch = 0;
+    const int rc = tma_rowprod_f64((const double*)A, rows, cols, B, K, work, work_len, &nch, st);
+    if (rc == NMFB_OK) {
+      if (!tol && rows * K <= 4096 && nch >= 32)
+        ++g_nmfb_launches, k_sum_partials_warp<<<(unsigned)((rows * K + 7) / 8), 256, 0, st>>>(
+            work, (int)nch, rows * K, out, scale);
+      else
+        ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(
+            work, (int)nch, rows * K, out, tol, scale);
+      NMFB_CHECK_LAUNCH();
+      return NMFB_OK;
+    }
+    if (rc != NMFB_EUNSUPPORTED) return rc;
+  }
   if (use_mma && rowprod_split(rows, cols) && (cols % 2 == 0) && K >= 5) {  // tensor-core streaming path
     constexpr int NT = (K + 7) / 8;
     const long nch = (cols + MMA_CW - 1) / MMA_CW;
@@ -716,7 +736,7 @@ int launch_rowprod(const T* A, long rows, long cols, const double* B, double* ou
     long rps = (rows + nsplit - 1) / nsplit;
     rps = ((rps + 127) / 128) * 128;
     nsplit = (rows + rps - 1) / rps;
-    cudaFuncSetAttribute(k_rowprod_mma<NT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    nmfb_smem_attr(k_rowprod_mma<NT, T>, (int)smem);
     dim3 grid((unsigned)nch, (unsigned)nsplit);
     ++g_nmfb_launches, k_rowprod_mma<NT, T><<<grid, 256, smem, st>>>(A, rows, cols, B, K, rps, work);
     if (!tol && rows * K <= 4096 && nch >= 32)
@@ -738,8 +758,7 @@ int launch_rowprod(const T* A, long rows, long cols, const double* B, double* ou
     long rps = (rows + nsplit - 1) / nsplit;
     rps = ((rps + 8 * RW - 1) / (8 * RW)) * (8 * RW);
     nsplit = (rows + rps - 1) / rps;
-    cudaFuncSetAttribute(k_rowprod_split<K, RW, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    nmfb_smem_attr(k_rowprod_split<K, RW, T>, (int)smem);
     dim3 grid((unsigned)nch, (unsigned)nsplit);
     ++g_nmfb_launches, k_rowprod_split<K, RW, T><<<grid, 256, smem, st>>>(A, rows, cols, B, rps, work);
     if (!tol && rows * K <= 4096 && nch >= 32)
@@ -776,6 +795,21 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
   if (rows == 0) {
     cudaMemsetAsync(out, 0, sizeof(double) * cols * K, st);
     return NMFB_OK;
+  }
+  if (sizeof(T) == 8 && colprod_tiled(rows, cols) && K >= 5) {  // TMA-fed DMMA (tma_prod.cu)
+    long ns = 0;
+    const int rc = tma_colprod_f64((const double*)A, rows, cols, B, K, work, work_len, &ns, st);
+    if (rc == NMFB_OK) {
+      if (!tol && cols * K <= 4096 && ns >= 32)
+        ++g_nmfb_launches, k_sum_partials_warp<<<(unsigned)((cols * K + 7) / 8), 256, 0, st>>>(
+            work, (int)ns, cols * K, out, scale);
+      else
+        ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(cols), 256, 0, st>>>(
+            work, (int)ns, cols * K, out, tol, scale);
+      NMFB_CHECK_LAUNCH();
+      return NMFB_OK;
+    }
+    if (rc != NMFB_EUNSUPPORTED) return rc;
   }
   const long stripe = colprod_stripe(rows, cols);
   const long ns = (rows + stripe - 1) / stripe;
@@ -1000,8 +1034,7 @@ int launch_dualprod(const T* A, long rows, long cols, const double* B1, const do
   double* partC = work + needR;
   const size_t smem = (size_t)(DP_CW / 8 * 2 * NT * 32 + 8 * DP_RB * NT * 8) * sizeof(double);
   dim3 grid((unsigned)d.nch, (unsigned)d.nsplit);
-  cudaFuncSetAttribute(k_dualprod_mma<NT, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  nmfb_smem_attr(k_dualprod_mma<NT, T>, (int)smem);
   ++g_nmfb_launches, k_dualprod_mma<NT, T><<<grid, 256, smem, st>>>(A, rows, cols, B1, B2, K,
                                                                       d.rps, partR, partC);
   ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(partR, (int)d.nch,
@@ -1024,7 +1057,12 @@ int launch_dualprod(const T* A, long rows, long cols, const double* B1, const do
 extern "C" long nmfb_colprod_work_len(long rows, long cols, long k) {
   if (rows <= 0) return 1;
   const long stripe = colprod_stripe(rows, cols);
-  return ((rows + stripe - 1) / stripe) * cols * k;
+  long ns = (rows + stripe - 1) / stripe;
+  if (colprod_tiled(rows, cols)) {
+    const long nt = tma_colprod_splits(rows, cols);
+    if (nt > ns) ns = nt;
+  }
+  return ns * cols * k;
 }
 
 extern "C" long nmfb_rowprod_work_len(long rows, long cols, long k, int a_is_f32) {

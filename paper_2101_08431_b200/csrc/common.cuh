@@ -17,11 +17,53 @@ enum {
   NMFB_EUNSUPPORTED = -4,
 };
 
+// last CUDA error seen by NMFB_CHECK_LAUNCH (nmfb_last_cuda_error reports it)
+extern int g_nmfb_last_cuda_error;
+
 #define NMFB_CHECK_LAUNCH()                                   \
   do {                                                        \
     cudaError_t e__ = cudaGetLastError();                     \
-    if (e__ != cudaSuccess) return NMFB_ELAUNCH;              \
+    if (e__ != cudaSuccess) {                                 \
+      g_nmfb_last_cuda_error = (int)e__;                      \
+      return NMFB_ELAUNCH;                                    \
+    }                                                         \
   } while (0)
+
+// Dynamic shared memory opt-in.  The attribute is a per-function CAP, so a launch with
+// more dynamic smem than an earlier, smaller setting fails; always raising it to the
+// device's opt-in maximum keeps launches of one kernel at different sizes (problems of
+// different k / m in one process) valid.  The launch's own size still sets occupancy.
+static inline int nmfb_smem_optin_max() {
+  static int v = [] {
+    int d = 0, x = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&x, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+    return x;
+  }();
+  return v;
+}
+// per-kernel cap = opt-in maximum minus the kernel's static shared memory (a larger value
+// is rejected), memoised by function address (the function TYPE is shared by kernels with
+// the same signature)
+static inline int nmfb_smem_cap(const void* f) {
+  static const void* keys[256];
+  static int caps[256];
+  static int n = 0;
+  for (int i = 0; i < n; ++i)
+    if (keys[i] == f) return caps[i];
+  cudaFuncAttributes a;
+  int c = nmfb_smem_optin_max();
+  if (cudaFuncGetAttributes(&a, f) == cudaSuccess) c -= (int)a.sharedSizeBytes;
+  if (n < 256) keys[n] = f, caps[n] = c, ++n;
+  return c;
+}
+template <typename F>
+static inline void nmfb_smem_attr(F* f, size_t bytes) {
+  const int cap = nmfb_smem_cap((const void*)f);
+  // a request above the cap is passed through: the launch itself reports the error
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (long)bytes > cap ? (int)bytes : cap);
+}
 
 static inline int nmfb_blocks(long n, int threads, int cap = 148 * 32) {
   long b = (n + threads - 1) / threads;

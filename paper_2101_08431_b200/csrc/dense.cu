@@ -400,9 +400,8 @@ extern "C" int nmfb_dense_cholesky(double* A, long N, int* info, void* stream) {
   if (N <= 0) return NMFB_EINVAL;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_trsm_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTwoTiles);
-    cudaFuncSetAttribute(k_syrk_trailing, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kTwoTiles);
+    nmfb_smem_attr(k_trsm_panel, (int)kTwoTiles);
+    nmfb_smem_attr(k_syrk_trailing, (int)kTwoTiles);
     attr = true;
   }
   if (N <= 4096) {  // csrc/chol_blk.cuh: one CTA up to 128, cooperative panels above
@@ -448,8 +447,7 @@ extern "C" int nmfb_dense_solve(const double* L, long N, double* b, void* stream
     const size_t sm = (size_t)N * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_trsv_single, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(4096 * sizeof(double)));
+      nmfb_smem_attr(k_trsv_single, (int)(4096 * sizeof(double)));
       attr = true;
     }
     ++g_nmfb_launches, k_trsv_single<<<1, TRSV_T, sm, st>>>(L, N, b, 0);

@@ -1322,7 +1322,7 @@ extern "C" int nmfb_schur_assemble(const double* Yt, const double* S, long m, lo
   dim3 grid((unsigned)ltiles, (unsigned)jsplit);
 #define CASE(KK)                                                                              \
   case KK:                                                                                    \
-    cudaFuncSetAttribute(k_schur_assemble<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+    nmfb_smem_attr(k_schur_assemble<KK>, \
                          (int)smem);                                                          \
     ++g_nmfb_launches, k_schur_assemble<KK><<<grid, 256, smem, st>>>(Yt, S, m, Zpk, XtX, rho, W, TL, jchunk, A); \
     break;
@@ -1724,7 +1724,7 @@ extern "C" int nmfb_grams(int count, const double* A0, const double* B0, double*
   const long rpc = (rows + G - 1) / G;
   static const bool attrs = [] {  // once, on the first (eager) call: 4 Grams of k = 16
 #define SETA(KK_)                                                                             \
-    cudaFuncSetAttribute(k_grams_partial<KK_>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+    nmfb_smem_attr(k_grams_partial<KK_>, \
                          (int)(8 * GR_CH * KK_ * sizeof(double)));
     SETA(1) SETA(2) SETA(3) SETA(4) SETA(5) SETA(6) SETA(7) SETA(8) SETA(9) SETA(10) SETA(11)
     SETA(12) SETA(13) SETA(14) SETA(15) SETA(16)

@@ -408,7 +408,7 @@ extern "C" int nmfb_lowrank_solve(const double* LD, const double* Yt, const doub
   const int apply_smem = sm_full <= 200 * 1024;
   const size_t sm_apply = apply_smem ? sm_full : 2 * Q * sizeof(double);
   if (apply_smem)
-    cudaFuncSetAttribute(k_lowrank_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_apply);
+    nmfb_smem_attr(k_lowrank_apply, (int)sm_apply);
   ++g_nmfb_launches, k_lowrank_apply<<<1, 256, sm_apply, st>>>(LG, LH, Zb, (int)k, u, w, apply_smem);
 #define CASE(KK)                                                                           \
   case KK:                                                                                 \

@@ -1489,7 +1489,7 @@ extern "C" int nmfb_ipm_persist(const void* M, int m_is_f32, long n, long m, lon
     if (!wm && m_is_f32) return NMFB_EUNSUPPORTED;                                            \
     a.m_in_smem = wm ? 1 : 0;                                                                  \
     const long bytes = p_smem_bytes<KK_>(n, m, G, wm);                                        \
-    cudaFuncSetAttribute(k_ipm_persist<KK_, T_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+    nmfb_smem_attr(k_ipm_persist<KK_, T_>, \
                          (int)bytes);                                                          \
     ++g_nmfb_launches;                                                                         \
     err = cudaLaunchCooperativeKernel((const void*)k_ipm_persist<KK_, T_>, dim3(G), dim3(PT), \

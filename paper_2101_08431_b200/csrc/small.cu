@@ -1010,7 +1010,7 @@ extern "C" int nmfb_small_direction(const double* X, const double* R, const doub
   case KK_:                                                                                      \
     ++g_nmfb_launches, k_sx<KK_><<<bx, SX_THREADS, 0, st>>>(X, R, gX, Yt, m, mux, rho, n, L, h,   \
                                                             work, tickets + 0, Z, H, XtX, iscal); \
-    cudaFuncSetAttribute(k_sy<KK_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sy_smem);  \
+    nmfb_smem_attr(k_sy<KK_>, (int)sy_smem);  \
     ++g_nmfb_launches, k_sy<KK_><<<1, 256, sy_smem, st>>>(Yt, S, gY, XtX, H, Z, rho, muy, tau, m, \
                                                           LD, LG, LH, Zb, dY, dS, Gdy, ysc,      \
                                                           iscal + 1, iscal + 2);                 \
@@ -1049,13 +1049,13 @@ extern "C" int nmfb_small_step_refresh(const void* M, int m_is_f32, long n, long
         sc, mu, wx, wy, eta, max_bt, tau, fcodes, X, R, dX, dR, n * KK_, Yt, S, dY, dS, m * KK_,   \
         Xf, Ytf);  \
     if (m_is_f32) {                                                                                 \
-      cudaFuncSetAttribute(k_sres<KK_, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+      nmfb_smem_attr(k_sres<KK_, float>, \
                            (int)tile);                                                              \
       ++g_nmfb_launches, k_sres<KK_, float><<<br, 256, tile, st>>>(                                 \
           (const float*)M, n, m, X, Yt, Fnew, gX, gY, R, S, wx * mu, wy * mu, RB, work,             \
           tickets + 3, sc);                                                                         \
     } else {                                                                                        \
-      cudaFuncSetAttribute(k_sres<KK_, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+      nmfb_smem_attr(k_sres<KK_, double>, \
                            (int)tile);                                                              \
       ++g_nmfb_launches, k_sres<KK_, double><<<br, 256, tile, st>>>(                                \
           (const double*)M, n, m, X, Yt, Fnew, gX, gY, R, S, wx * mu, wy * mu, RB, work,            \

@@ -454,8 +454,7 @@ extern "C" int nmfb_stage1_persist(const void* M, int m_is_f32, long n, long m, 
     if (!wm && m_is_f32) return NMFB_EUNSUPPORTED;                                               \
     a.m_in_smem = wm ? 1 : 0;                                                                    \
     const long bytes = s1_smem<KK_>(n, m, G, wm);                                                \
-    cudaFuncSetAttribute(k_stage1_persist<KK_, WW_, T_>,                                         \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);               \
+    nmfb_smem_attr(k_stage1_persist<KK_, WW_, T_>, (size_t)bytes);                              \
     ++g_nmfb_launches;                                                                           \
     err = cudaLaunchCooperativeKernel((const void*)k_stage1_persist<KK_, WW_, T_>, dim3(G),      \
                                       dim3(ST), args, (size_t)bytes, st);                        \

@@ -1,0 +1,604 @@
+// TMA-fed streaming products over an fp64 M (configs c2-c4 and the fp64 streaming
+// session): ctb = M Y^T of the X-update and X^T M of the Y-update,
+// and the same two products in the residual-free stage 2 (M dY^T, M^T dX).
+//
+// Design (B200, sm_100a):
+//   * persistent grid, one CTA per SM; a static, contiguous range of work items per CTA
+//     (the decomposition depends only on the shape, so the split-K partials and their
+//     fixed-order sum are bit-reproducible run to run);
+//   * one producer warp issues cp.async.bulk.tensor (TMA) loads of 128-byte-wide boxes
+//     of M, 128B-swizzled, into a 4-stage shared-memory ring with full/empty mbarriers
+//     (128 KB in flight per SM: enough to cover HBM latency at the full rate without
+//     any register staging);
+//   * eight consumer warps read the fragments of FP64 tensor-core MMAs (DMMA m8n8k4)
+//     straight from the ring.  The swizzle (16-byte chunk c of 128-byte line r lives at
+//     c ^ (r & 7)) together with the lane -> row map below makes every 16-byte fragment
+//     load conflict-free: row product: lanes 4g..4g+3 read line sigma(g) = (g >> 1) |
+//     ((g & 1) << 2), so the two rows of a quarter-warp differ in bit 2; column product:
+//     the contraction rows of one MMA are the even (then the odd) lines 2t, so the eight
+//     lanes of a quarter-warp hit chunks g ^ 2t, all distinct.
+//
+// The row product accumulates each row's chunk in the same order as k_rowprod_mma
+// (csrc/anls.cu: ascending 8-column groups, the even then the odd column of each lane's
+// pair), so its partials are bit-identical to the register-direct kernel's.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "tma_prod.cuh"
+
+namespace {
+
+constexpr int NCW = 8;                  // consumer warps
+constexpr int NTHREADS = (NCW + 1) * 32;  // + one producer warp
+constexpr int STAGES = 4;
+constexpr int STAGE_BYTES = 32 * 1024;
+
+// ---- PTX helpers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT;\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(su32(dst)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ double2 lds128(const double* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(su32(p)));
+  return v;
+}
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// ring / barrier carving of the dynamic shared memory (1024-byte aligned for the swizzle)
+struct Carve {
+  double* ring;
+  uint64_t* full;
+  uint64_t* empty;
+  double* extra;
+};
+__device__ __forceinline__ Carve carve(uint8_t* raw) {
+  const uint32_t base = su32(raw);
+  const uint32_t pad = ((base + 1023u) & ~1023u) - base;
+  uint8_t* p = raw + pad;
+  Carve c;
+  c.ring = reinterpret_cast<double*>(p);
+  c.full = reinterpret_cast<uint64_t*>(p + STAGES * STAGE_BYTES);
+  c.empty = c.full + STAGES;
+  c.extra = reinterpret_cast<double*>(c.empty + STAGES);
+  return c;
+}
+
+__device__ __forceinline__ void init_barriers(const Carve& c) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&c.full[s], 1);
+      mbar_init(&c.empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// ---- row product ------------------------------------------------------------
+// item = (chunk of TMA_RP_CW columns, band of RP_BR rows), chunk-major.  A stage is
+// RP_SBOX boxes of 16 columns x RP_BR rows; consumer warp w owns rows [16 w, 16 w + 16)
+// of the band (two 8-row MMA tiles) and accumulates them over the chunk.
+//
+// NT = 8-wide output tiles on the tensor pipe.  TL > 0 (K = 8 + TL, 9 <= K <= 12): the
+// first 8 outputs go to DMMA and the last TL to the FP64 SIMT pipe (DFMA), a separate
+// pipe on sm_100a, instead of a second, mostly-padding DMMA tile: at K = 10 a quarter
+// of the products' tensor work disappears (the kernels run close to the DMMA limit).
+// The TL columns of every lane's row partials are summed over the four lanes of a
+// quad (fixed shuffle tree) when the band finishes.
+constexpr int RP_RT = 2;
+constexpr int RP_BR = NCW * 8 * RP_RT;       // 128 rows per band
+constexpr int RP_BOX = RP_BR * 16;           // doubles per box (16 KB)
+constexpr int RP_SBOX = STAGE_BYTES / (RP_BOX * 8);  // boxes per stage (2)
+constexpr int RP_NGRP = TMA_RP_CW / 8;       // 8-column groups per chunk
+
+template <int TL>
+struct TailPitch {
+  static constexpr int v = TL <= 2 ? 2 : 4;  // doubles per (group, t, ee) tail record
+};
+
+__device__ __forceinline__ double quad_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
+}
+
+template <int NT, int TL>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_rowprod_tma(const __grid_constant__ CUtensorMap map, long rows, long cols,
+                  const double* __restrict__ B, int K, long nitems, long nbands,
+                  double* __restrict__ part) {
+  static_assert(TL == 0 || NT == 1, "DFMA tail only after one DMMA tile");
+  constexpr int TP = TailPitch<TL>::v;
+  extern __shared__ uint8_t smem_raw[];
+  const Carve c = carve(smem_raw);
+  double* sB = c.extra;  // [RP_NGRP][2][NT][32] fragment order (as k_rowprod_mma)
+  double* sT = sB + RP_NGRP * 2 * NT * 32;  // [RP_NGRP][4 t][2 ee][TP]: B[8q+2t+ee][8+j]
+  init_barriers(c);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long i_beg = (long)blockIdx.x * nitems / gridDim.x;
+  const long i_end = (long)(blockIdx.x + 1) * nitems / gridDim.x;
+
+  if (warp == NCW) {  // ===== TMA producer =====
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (long it = i_beg; it < i_end; ++it) {
+        const long chunk = it / nbands, band = it - chunk * nbands;
+        const long j0 = chunk * TMA_RP_CW;
+        const int cw = (int)min((long)TMA_RP_CW, cols - j0);
+        const int nbox = (cw + 15) >> 4;
+        for (int b0 = 0; b0 < nbox; b0 += RP_SBOX) {
+          const int nb = min(RP_SBOX, nbox - b0);
+          mbar_wait(&c.empty[stage], phase ^ 1u);
+          mbar_expect_tx(&c.full[stage], (unsigned)(nb * RP_BOX * 8));
+          for (int b = 0; b < nb; ++b)
+            tma_load_2d(c.ring + ((size_t)stage * RP_SBOX + b) * RP_BOX, &map, &c.full[stage],
+                        (int)(j0 + 16 * (b0 + b)), (int)(band * RP_BR));
+          if (++stage == STAGES) stage = 0, phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int g = lane >> 2, t = lane & 3;
+  const int sig = (g >> 1) | ((g & 1) << 2);  // line of this lane's A-fragment row
+  int stage = 0;
+  unsigned phase = 0;
+  long cur_chunk = -1;
+  for (long it = i_beg; it < i_end; ++it) {
+    const long chunk = it / nbands, band = it - chunk * nbands;
+    const long j0 = chunk * TMA_RP_CW;
+    const int cw = (int)min((long)TMA_RP_CW, cols - j0);
+    const int nbox = (cw + 15) >> 4;
+    if (chunk != cur_chunk) {  // stage this chunk's B fragments (zero beyond cols / K)
+      consumers_sync();
+      const int ngrp = 2 * nbox;  // 8-column groups
+      // asynchronous 8-byte gathers (cp.async, zero-filled out of range): every element
+      // of the chunk is in flight at once instead of one dependent load per trip
+      for (int e = threadIdx.x; e < ngrp * 2 * NT * 32; e += NCW * 32) {
+        const int l = e & 31, se = (e >> 5) / NT, nt = (e >> 5) % NT;
+        const int sidx = se >> 1, ee = se & 1;
+        const long col = j0 + 8 * sidx + 2 * (l & 3) + ee;
+        const int pp = nt * 8 + (l >> 2);
+        const bool ok = col < cols && pp < K;
+        cp_async8(sB + e, ok ? B + col * K + pp : B, ok ? 8 : 0);
+      }
+      if (TL > 0)
+        for (int e = threadIdx.x; e < ngrp * 8 * TP; e += NCW * 32) {
+          const int j = e % TP, rec = e / TP;  // rec = (q * 4 + t) * 2 + ee
+          const long col = j0 + 8 * (rec >> 3) + 2 * ((rec >> 1) & 3) + (rec & 1);
+          const bool ok = col < cols && j < TL;
+          cp_async8(sT + e, ok ? B + col * K + 8 + j : B, ok ? 8 : 0);
+        }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      consumers_sync();
+      cur_chunk = chunk;
+    }
+    double acc[RP_RT][NT][2];
+    double tacc[RP_RT][TL > 0 ? TL : 1];
+#pragma unroll
+    for (int rt = 0; rt < RP_RT; ++rt) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[rt][nt][0] = acc[rt][nt][1] = 0.0;
+#pragma unroll
+      for (int j = 0; j < (TL > 0 ? TL : 1); ++j) tacc[rt][j] = 0.0;
+    }
+    for (int b0 = 0; b0 < nbox; b0 += RP_SBOX) {
+      const int nb = min(RP_SBOX, nbox - b0);
+      mbar_wait(&c.full[stage], phase);
+#pragma unroll
+      for (int b = 0; b < RP_SBOX; ++b) {
+        if (b < nb) {
+          const double* box = c.ring + ((size_t)stage * RP_SBOX + b) * RP_BOX;
+          double2 a[2][RP_RT];
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+            for (int rt = 0; rt < RP_RT; ++rt) {
+              const int r = 8 * (RP_RT * warp + rt) + sig;
+              a[kk][rt] = lds128(box + r * 16 + (((4 * kk + t) ^ sig) << 1));
+            }
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int q = 2 * (b0 + b) + kk;  // 8-column group within the chunk
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const double bx = sB[((2 * q) * NT + nt) * 32 + lane];
+              const double by = sB[((2 * q + 1) * NT + nt) * 32 + lane];
+#pragma unroll
+              for (int rt = 0; rt < RP_RT; ++rt) {
+                dmma(acc[rt][nt][0], acc[rt][nt][1], a[kk][rt].x, bx);
+                dmma(acc[rt][nt][0], acc[rt][nt][1], a[kk][rt].y, by);
+              }
+            }
+            if (TL > 0) {
+              const double* tr = sT + ((q * 4 + t) * 2) * TP;
+              double tx[TP], ty[TP];
+#pragma unroll
+              for (int j = 0; j < TP; j += 2) {
+                const double2 u = lds128(tr + j), v = lds128(tr + TP + j);
+                tx[j] = u.x, tx[j + 1] = u.y, ty[j] = v.x, ty[j + 1] = v.y;
+              }
+#pragma unroll
+              for (int rt = 0; rt < RP_RT; ++rt)
+#pragma unroll
+                for (int j = 0; j < (TL > 0 ? TL : 1); ++j)
+                  tacc[rt][j] = fma(a[kk][rt].y, ty[j], fma(a[kk][rt].x, tx[j], tacc[rt][j]));
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c.empty[stage]);
+      if (++stage == STAGES) stage = 0, phase ^= 1u;
+    }
+#pragma unroll
+    for (int rt = 0; rt < RP_RT; ++rt) {
+      const long row = band * RP_BR + 8 * (RP_RT * warp + rt) + sig;
+      double tsum[TL > 0 ? TL : 1];
+#pragma unroll
+      for (int j = 0; j < (TL > 0 ? TL : 1); ++j) tsum[j] = TL > 0 ? quad_sum(tacc[rt][j]) : 0.0;
+      if (row >= rows) continue;
+      double* dst = part + (chunk * rows + row) * K;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int pp = nt * 8 + 2 * t + e;
+          if (pp < K) dst[pp] = acc[rt][nt][e];
+        }
+      if (TL > 0 && t == 0)
+#pragma unroll
+        for (int j = 0; j < (TL > 0 ? TL : 1); ++j) dst[8 + j] = tsum[j];
+    }
+  }
+}
+
+// ---- column product ---------------------------------------------------------
+// item = (chunk of 128 columns, split of CP_BR-aligned rows), chunk-major.  A stage is
+// 8 boxes of 16 columns x 32 rows plus the stage's 32 rows of B (one bulk copy); consumer
+// warp w owns box w (16 columns of the chunk) and accumulates them over the split.  NT /
+// TL as in the row product (the TL tail columns summed over the quad at the item end).
+constexpr int CP_CW = 128;
+constexpr int CP_BR = 32;
+constexpr int CP_BOX = CP_BR * 16;  // doubles per box (4 KB)
+
+template <int NT, int TL, bool FULL>
+__device__ __forceinline__ void colprod_stage(const double* __restrict__ box,
+                                              const double* __restrict__ xs,
+                                              const double* __restrict__ B, int K, long r0,
+                                              long re, int g, int t, double (&acc)[2][NT][2],
+                                              double (&tacc)[2][TL > 0 ? TL : 1]) {
+#pragma unroll
+  for (int blk = 0; blk < CP_BR / 8; ++blk) {
+    const int ra = 8 * blk + 2 * t, rbb = ra + 1;  // lines 2t, 2t + 1 of the 8-row block
+    const double2 a0 = lds128(box + ra * 16 + ((g ^ (ra & 7)) << 1));
+    const double2 a1 = lds128(box + rbb * 16 + ((g ^ (rbb & 7)) << 1));
+    const long ia = r0 + ra, ib = ia + 1;
+    double b0[NT], b1[NT];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int pp = nt * 8 + g;
+      if (FULL) {
+        b0[nt] = pp < K ? xs[ra * K + pp] : 0.0;
+        b1[nt] = pp < K ? xs[rbb * K + pp] : 0.0;
+      } else {
+        b0[nt] = (ia < re && pp < K) ? __ldg(B + ia * K + pp) : 0.0;
+        b1[nt] = (ib < re && pp < K) ? __ldg(B + ib * K + pp) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      dmma(acc[0][nt][0], acc[0][nt][1], a0.x, b0[nt]);
+      dmma(acc[1][nt][0], acc[1][nt][1], a0.y, b0[nt]);
+      dmma(acc[0][nt][0], acc[0][nt][1], a1.x, b1[nt]);
+      dmma(acc[1][nt][0], acc[1][nt][1], a1.y, b1[nt]);
+    }
+    if (TL > 0) {
+#pragma unroll
+      for (int j = 0; j < (TL > 0 ? TL : 1); ++j) {
+        double xa, xb;
+        if (FULL) {
+          xa = xs[ra * K + 8 + j];
+          xb = xs[rbb * K + 8 + j];
+        } else {
+          xa = ia < re ? __ldg(B + ia * K + 8 + j) : 0.0;
+          xb = ib < re ? __ldg(B + ib * K + 8 + j) : 0.0;
+        }
+        tacc[0][j] = fma(a1.x, xb, fma(a0.x, xa, tacc[0][j]));
+        tacc[1][j] = fma(a1.y, xb, fma(a0.y, xa, tacc[1][j]));
+      }
+    }
+  }
+}
+
+template <int NT, int TL>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_colprod_tma(const __grid_constant__ CUtensorMap map, long rows, long cols,
+                  const double* __restrict__ B, int K, long nitems, long nsplit, long split_rows,
+                  double* __restrict__ part) {
+  static_assert(TL == 0 || NT == 1, "DFMA tail only after one DMMA tile");
+  extern __shared__ uint8_t smem_raw[];
+  const Carve c = carve(smem_raw);
+  double* sXs = c.extra;  // [STAGES][CP_BR][<= 16]: the stage's rows of B, dense (row pitch K)
+  init_barriers(c);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long i_beg = (long)blockIdx.x * nitems / gridDim.x;
+  const long i_end = (long)(blockIdx.x + 1) * nitems / gridDim.x;
+
+  if (warp == NCW) {  // ===== TMA producer =====
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (long it = i_beg; it < i_end; ++it) {
+        const long chunk = it / nsplit, s = it - chunk * nsplit;
+        const long rb = s * split_rows, re = min(rows, rb + split_rows);
+        for (long r0 = rb; r0 < re; r0 += CP_BR) {
+          // the stage's rows of B (contiguous rows x K doubles) ride on the same barrier
+          // when the whole 32-row block lies inside the split; otherwise consumers read them
+          // from global memory (split / matrix tail)
+          const bool bfull = r0 + CP_BR <= re;
+          const unsigned bbytes = bfull ? (unsigned)(CP_BR * K * 8) : 0u;
+          mbar_wait(&c.empty[stage], phase ^ 1u);
+          mbar_expect_tx(&c.full[stage], (unsigned)STAGE_BYTES + bbytes);
+          for (int b = 0; b < NCW; ++b)
+            tma_load_2d(c.ring + ((size_t)stage * NCW + b) * CP_BOX, &map, &c.full[stage],
+                        (int)(chunk * CP_CW + 16 * b), (int)r0);
+          if (bfull) bulk_load(sXs + (size_t)stage * CP_BR * 16, B + r0 * K, bbytes, &c.full[stage]);
+          if (++stage == STAGES) stage = 0, phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  const int g = lane >> 2, t = lane & 3;
+  int stage = 0;
+  unsigned phase = 0;
+  for (long it = i_beg; it < i_end; ++it) {
+    const long chunk = it / nsplit, s = it - chunk * nsplit;
+    const long rb = s * split_rows, re = min(rows, rb + split_rows);
+    double acc[2][NT][2];  // [column parity][n tile][2]
+    double tacc[2][TL > 0 ? TL : 1];
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[par][nt][0] = acc[par][nt][1] = 0.0;
+#pragma unroll
+      for (int j = 0; j < (TL > 0 ? TL : 1); ++j) tacc[par][j] = 0.0;
+    }
+    for (long r0 = rb; r0 < re; r0 += CP_BR) {
+      mbar_wait(&c.full[stage], phase);
+      const double* box = c.ring + ((size_t)stage * NCW + warp) * CP_BOX;
+      const double* xs = sXs + (size_t)stage * CP_BR * 16;
+      if (r0 + CP_BR <= re)
+        colprod_stage<NT, TL, true>(box, xs, B, K, r0, re, g, t, acc, tacc);
+      else
+        colprod_stage<NT, TL, false>(box, xs, B, K, r0, re, g, t, acc, tacc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c.empty[stage]);
+      if (++stage == STAGES) stage = 0, phase ^= 1u;
+    }
+#pragma unroll
+    for (int par = 0; par < 2; ++par) {
+      const long col = chunk * CP_CW + 16 * warp + 2 * g + par;
+      double tsum[TL > 0 ? TL : 1];
+#pragma unroll
+      for (int j = 0; j < (TL > 0 ? TL : 1); ++j) tsum[j] = TL > 0 ? quad_sum(tacc[par][j]) : 0.0;
+      if (col >= cols) continue;
+      double* dst = part + (s * cols + col) * K;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int pp = nt * 8 + 2 * t + e;
+          if (pp < K) dst[pp] = acc[par][nt][e];
+        }
+      if (TL > 0 && t == 0)
+#pragma unroll
+        for (int j = 0; j < (TL > 0 ? TL : 1); ++j) dst[8 + j] = tsum[j];
+    }
+  }
+}
+
+// ---- host side ----------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }();
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const double* A, long rows, long cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(double)};
+  const cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  static const CUtensorMapL2promotion promo = [] {
+    const char* e = getenv("NMFB_TMA_L2P");  // L2 fetch granularity (experiments)
+    const int v = e ? atoi(e) : 0;
+    return v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+         : v == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  }();
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)A, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int sms = [] {
+    int d = 0, v = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    return v > 0 ? v : 148;
+  }();
+  return sms;
+}
+
+bool shape_ok(const double* A, long rows, long cols) {
+  // TMA: 16-byte aligned base and row pitch, coordinates in int32
+  return ((uintptr_t)A % 16 == 0) && (cols % 2 == 0) && rows < (1L << 31) && cols < (1L << 31);
+}
+
+}  // namespace
+
+static int g_tma_prod = -1;  // -1: from NMFB_TMA_PROD (default on)
+
+bool tma_prod_enabled() {
+  if (g_tma_prod < 0) {
+    const char* e = getenv("NMFB_TMA_PROD");
+    g_tma_prod = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_tma_prod != 0;
+}
+
+extern "C" int nmfb_tma_products(int on) {
+  const int prev = tma_prod_enabled() ? 1 : 0;
+  if (on >= 0) g_tma_prod = on ? 1 : 0;
+  return prev;
+}
+
+int tma_rowprod_f64(const double* A, long rows, long cols, const double* B, int K, double* work,
+                    long work_len, long* nparts, cudaStream_t st) {
+  if (!tma_prod_enabled() || K < 1 || K > 16 || !shape_ok(A, rows, cols)) return NMFB_EUNSUPPORTED;
+  const long nch = (cols + TMA_RP_CW - 1) / TMA_RP_CW;
+  if (nch * rows * K > work_len) return NMFB_ENOMEM;
+  CUtensorMap map;
+  if (!make_map(&map, A, rows, cols, RP_BR)) return NMFB_EUNSUPPORTED;
+  const long nbands = (rows + RP_BR - 1) / RP_BR;
+  const long nitems = nch * nbands;
+  const int grid = (int)min((long)num_sms(), nitems);
+  const int NT = (K + 7) / 8;
+  const size_t smem = 1024 + STAGES * STAGE_BYTES + 2 * STAGES * 8 +
+                      (size_t)RP_NGRP * 2 * NT * 32 * sizeof(double) +
+                      (size_t)RP_NGRP * 8 * 4 * sizeof(double);
+#define RP_LAUNCH(NT_, TL_)                                                                     \
+  nmfb_smem_attr(k_rowprod_tma<NT_, TL_>, smem);                                                \
+  ++g_nmfb_launches, k_rowprod_tma<NT_, TL_><<<grid, NTHREADS, smem, st>>>(map, rows, cols, B, K, \
+                                                                           nitems, nbands, work)
+  switch (K) {
+    case 9: RP_LAUNCH(1, 1); break;
+    case 10: RP_LAUNCH(1, 2); break;
+    case 11: RP_LAUNCH(1, 3); break;
+    case 12: RP_LAUNCH(1, 4); break;
+    default:
+      if (NT == 1) {
+        RP_LAUNCH(1, 0);
+      } else {
+        RP_LAUNCH(2, 0);
+      }
+  }
+#undef RP_LAUNCH
+  *nparts = nch;
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+long tma_colprod_splits(long rows, long cols) {
+  const long nch = (cols + CP_CW - 1) / CP_CW;
+  // about 8 items per CTA over the whole grid, splits of whole 32-row boxes
+  long want = (8L * num_sms() + nch - 1) / nch;
+  if (want < 1) want = 1;
+  long sr = (rows + want - 1) / want;
+  sr = ((sr + CP_BR - 1) / CP_BR) * CP_BR;
+  if (sr < 4 * CP_BR) sr = 4 * CP_BR;
+  return (rows + sr - 1) / sr;
+}
+
+int tma_colprod_f64(const double* A, long rows, long cols, const double* B, int K, double* work,
+                    long work_len, long* nparts, cudaStream_t st) {
+  if (!tma_prod_enabled() || K < 1 || K > 16 || !shape_ok(A, rows, cols)) return NMFB_EUNSUPPORTED;
+  const long nch = (cols + CP_CW - 1) / CP_CW;
+  long ns = tma_colprod_splits(rows, cols);
+  long sr = (rows + ns - 1) / ns;
+  sr = ((sr + CP_BR - 1) / CP_BR) * CP_BR;
+  ns = (rows + sr - 1) / sr;
+  if (ns * cols * K > work_len) return NMFB_ENOMEM;
+  CUtensorMap map;
+  if (!make_map(&map, A, rows, cols, CP_BR)) return NMFB_EUNSUPPORTED;
+  const long nitems = nch * ns;
+  const int grid = (int)min((long)num_sms(), nitems);
+  const size_t smem = 1024 + STAGES * STAGE_BYTES + 2 * STAGES * 8 +
+                      (size_t)STAGES * CP_BR * 16 * sizeof(double);
+  if ((uintptr_t)B % 16) return NMFB_EUNSUPPORTED;  // bulk copies of B rows
+#define CP_LAUNCH(NT_, TL_)                                                                     \
+  nmfb_smem_attr(k_colprod_tma<NT_, TL_>, smem);                                                \
+  ++g_nmfb_launches, k_colprod_tma<NT_, TL_><<<grid, NTHREADS, smem, st>>>(map, rows, cols, B, K, \
+                                                                           nitems, ns, sr, work)
+  switch (K) {
+    case 9: CP_LAUNCH(1, 1); break;
+    case 10: CP_LAUNCH(1, 2); break;
+    case 11: CP_LAUNCH(1, 3); break;
+    case 12: CP_LAUNCH(1, 4); break;
+    default:
+      if (K <= 8) {
+        CP_LAUNCH(1, 0);
+      } else {
+        CP_LAUNCH(2, 0);
+      }
+  }
+#undef CP_LAUNCH
+  *nparts = ns;
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}

@@ -12,6 +12,7 @@ NativeLibraryError.
 """
 from __future__ import annotations
 
+import functools
 import math
 import os
 import time
@@ -32,6 +33,20 @@ NTRIALS = 61  # t = 0..60
 INERTIA_GROW = 4.0
 INERTIA_SHRINK = 3.0
 INERTIA_MAX_TRIES = 40
+
+
+def _nvtx(name):
+    """NVTX range around a solver phase (ncu --nvtx-include / nsys timelines)."""
+    def deco(f):
+        @functools.wraps(f)
+        def wrapped(*a, **kw):
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return f(*a, **kw)
+            finally:
+                torch.cuda.nvtx.range_pop()
+        return wrapped
+    return deco
 
 
 def _p(t):
@@ -183,7 +198,10 @@ class Problem:
             rc = getattr(self.lib, name)(*args)
         self.launches += 1
         if rc != 0:
-            raise NativeLibraryError(f"{name} returned {rc}")
+            why = ""
+            if rc == -2:  # NMFB_ELAUNCH: name the CUDA error behind it
+                why = " (" + self.lib.nmfb_last_cuda_error().decode() + ")"
+            raise NativeLibraryError(f"{name} returned {rc}{why}")
 
     def readback(self, nd, ni=0):
         """Copy dscal[:nd] / iscal[:ni] to pinned host memory and wait."""
@@ -307,6 +325,7 @@ def kkt_from_sums(v):
 # ============================================================================
 # stage 1 (Algorithm 1)
 # ============================================================================
+@_nvtx("nmfb/stage1")
 def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=None):
     """SPEC.md:209 run_stage1 on the device.  X (n,k), Yt (m,k) device fp64.
 
@@ -995,6 +1014,7 @@ class IpmEngine:
         return min((mu_aff / mu_bar) ** 3, p.sigma_cap)
 
 
+@_nvtx("nmfb/ipm")
 def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
     """SPEC.md:337 run_ipm on the device (Algorithm 2 + Algorithm 3 switch).
 
@@ -1176,6 +1196,7 @@ def _run_ipm(P: Problem, eng, p: IpmParams, t0):
     return res
 
 
+@_nvtx("nmfb/transition")
 def transition(P: Problem, X, Yt, eps_tol, tp: TransitionParams | None = None):
     """SPEC.md:393 / PAPER Eqs. 14-18 on the device -> (X, Yt, R, S, mu, rho)."""
     tp = tp or TransitionParams()
@@ -1223,6 +1244,7 @@ def kkt_error_primal_only_dev(P: Problem, X, Yt):
     return kkt_from_sums(v[16:28])[1], 0.5 * v[0]
 
 
+@_nvtx("nmfb/two_stage")
 def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1: Stage1Config | None = None,
                   ipm: IpmParams | None = None, tp: TransitionParams | None = None,
                   stage="two_stage", pX=None, pY=None, e_scale=None, problem: Problem | None = None,

@@ -48,7 +48,7 @@ for attr in ("direction", "persist_run", "predictor_sigma", "refresh", "armijo_l
 def step():
     X, Yt, pX, pY, r1 = solver.run_stage1(P, X0d, Yt0d, Stage1Config())
     X, Yt, R, S, mu, rho = solver.transition(P, X, Yt, eps_abs)
-    return solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(eps_tol=eps_abs, max_iter=500))
+    return solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(eps_tol=eps_abs, max_iter=1000))
 
 
 for rep in range(3):
@@ -62,7 +62,7 @@ for rep in range(3):
     X, Yt, R, S, mu, rho = solver.transition(P, X, Yt, eps_abs)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    eng, r2 = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(eps_tol=eps_abs, max_iter=500))
+    eng, r2 = solver.run_ipm(P, X, Yt, R, S, mu, rho, IpmParams(eps_tol=eps_abs, max_iter=1000))
     torch.cuda.synchronize()
     t3 = time.perf_counter()
 print(f"total {1e3 * (t3 - t0):.3f} ms: stage1 {1e3 * (t1 - t0):.3f} transition {1e3 * (t2 - t1):.3f} "
