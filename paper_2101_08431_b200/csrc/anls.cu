@@ -1022,6 +1022,18 @@ int launch_dualprod(const T* A, long rows, long cols, const double* B1, const do
   // k = 4: 276 us vs 331 us for the two streams); for 8 < K <= 16 its 8-warp row-partial
   // exchange stalls the stream (357 vs 347 us at k = 10), so the two streaming products
   // (each ~70 % of HBM) run back to back instead
+  if (sizeof(T) == 8 && K >= 5) {  // one TMA-fed pass (tma_prod.cu)
+    const int rc = tma_dualprod_f64((const double*)A, rows, cols, B1, B2, K, outR, outC, work,
+                                    work_len, st);
+    if (rc == NMFB_OK) {
+      const long nch = (cols + TMA_RP_CW - 1) / TMA_RP_CW;
+      ++g_nmfb_launches, k_sum_partials<K><<<sum_grid<K>(rows), 256, 0, st>>>(
+          work, (int)nch, rows * K, outR, nullptr, 1.0);
+      NMFB_CHECK_LAUNCH();
+      return NMFB_OK;
+    }
+    if (rc != NMFB_EUNSUPPORTED) return rc;
+  }
   if (K > 8) {
     int rc = launch_rowprod<K, T>(A, rows, cols, B1, outR, nullptr, 1.0, work, work_len, st);
     if (rc != NMFB_OK) return rc;
@@ -1117,6 +1129,8 @@ extern "C" long nmfb_dualprod_work_len(long rows, long cols, long k) {
   long len = d.nch * rows * k + d.nsplit * cols * k;
   const long r = nmfb_rowprod_work_len(rows, cols, k, 0), r32 = nmfb_rowprod_work_len(rows, cols, k, 1);
   const long c = nmfb_colprod_work_len(rows, cols, k);
+  const long tm = tma_dualprod_work_len(rows, cols, k);
+  if (tm > len) len = tm;
   if (r > len) len = r;
   if (r32 > len) len = r32;
   if (c > len) len = c;

@@ -87,7 +87,7 @@ __device__ __forceinline__ double2 lds128(const double* p) {
   return v;
 }
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -256,10 +256,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               const double bx = sB[((2 * q) * NT + nt) * 32 + lane];
               const double by = sB[((2 * q + 1) * NT + nt) * 32 + lane];
 #pragma unroll
-              for (int rt = 0; rt < RP_RT; ++rt) {
-                dmma(acc[rt][nt][0], acc[rt][nt][1], a[kk][rt].x, bx);
-                dmma(acc[rt][nt][0], acc[rt][nt][1], a[kk][rt].y, by);
-              }
+              for (int rt = 0; rt < RP_RT; ++rt) dmma(acc[rt][nt][0], acc[rt][nt][1], a[kk][rt].x, bx);
+#pragma unroll
+              for (int rt = 0; rt < RP_RT; ++rt) dmma(acc[rt][nt][0], acc[rt][nt][1], a[kk][rt].y, by);
             }
             if (TL > 0) {
               const double* tr = sT + ((q * 4 + t) * 2) * TP;
@@ -451,6 +450,342 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
+// ---- dual product -----------------------------------------------------------
+// ONE pass over M for both outR = M B1 (rows x K, B1: cols x K, e.g. M dY^T) and
+// outC = M^T B2 (cols x K, B2: rows x K, e.g. M^T dX) -- the two products of every
+// residual-free IPM iteration (solver.py _armijo_free + the incremental refresh).
+// item = (chunk of TMA_RP_CW columns, band of 64 rows), chunk-major, contiguous ranges per
+// CTA.  A stage is 8 boxes of 16 columns x 64 rows (64 KB, 2-stage ring).  Row part:
+// warp w owns rows [8 w, 8 w + 8) of the band (one MMA tile; B1 fragments resident per
+// chunk) and writes partR[chunk][row] when the band's chunk is done.  Column part: warp w
+// owns box w of every stage (columns 16 w .. 16 w + 15 of the stage's 128), i.e. boxes
+// {8 s + w} of the chunk, accumulated over the CTA's bands of the chunk in registers and
+// flushed to partC[cta][segment] when the chunk changes.  Both parts: one DMMA tile
+// (outputs 0..7) + the DFMA tail for K = 9..12, so the pass stays HBM-bound.
+constexpr int DU_BR = 64;
+constexpr int DU_BOX = DU_BR * 16;  // doubles per box (8 KB)
+constexpr int DU_STAGES = 2;
+constexpr int DU_STAGE_BYTES = NCW * DU_BOX * 8;  // 64 KB
+constexpr int DU_SEGS = 4;                        // chunk segments per CTA range
+constexpr int DU_CBOX = TMA_RP_CW / 16 / NCW;     // column boxes per warp per chunk (4)
+
+struct DualCarve {
+  double* ring;
+  uint64_t* full;
+  uint64_t* empty;
+  double* sB;   // [RP_NGRP][2][NT][32]
+  double* sT;   // [RP_NGRP][4][2][TP]
+  double* sX;   // [DU_STAGES][DU_BR][16]
+};
+
+template <int NT, int TL>
+__device__ __forceinline__ DualCarve dual_carve(uint8_t* raw) {
+  const uint32_t base = su32(raw);
+  const uint32_t pad = ((base + 1023u) & ~1023u) - base;
+  uint8_t* p = raw + pad;
+  DualCarve c;
+  c.ring = reinterpret_cast<double*>(p);
+  c.full = reinterpret_cast<uint64_t*>(p + DU_STAGES * DU_STAGE_BYTES);
+  c.empty = c.full + DU_STAGES;
+  c.sB = reinterpret_cast<double*>(c.empty + DU_STAGES);
+  c.sT = c.sB + RP_NGRP * 2 * NT * 32;
+  c.sX = c.sT + RP_NGRP * 8 * 4;
+  return c;
+}
+
+template <int NT, int TL>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_dualprod_tma(const __grid_constant__ CUtensorMap map, long rows, long cols,
+                   const double* __restrict__ B1, const double* __restrict__ B2, int K,
+                   long nitems, long nbands, double* __restrict__ partR,
+                   double* __restrict__ partC) {
+  static_assert(TL == 0 || NT == 1, "DFMA tail only after one DMMA tile");
+  constexpr int TP = TailPitch<TL>::v;
+  constexpr int TLA = TL > 0 ? TL : 1;
+  extern __shared__ uint8_t smem_raw[];
+  const DualCarve c = dual_carve<NT, TL>(smem_raw);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < DU_STAGES; ++s) {
+      mbar_init(&c.full[s], 1);
+      mbar_init(&c.empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long i_beg = (long)blockIdx.x * nitems / gridDim.x;
+  const long i_end = (long)(blockIdx.x + 1) * nitems / gridDim.x;
+  constexpr int SCOLS = NCW * 16;  // columns per stage (128)
+
+  if (warp == NCW) {  // ===== TMA producer =====
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (long it = i_beg; it < i_end; ++it) {
+        const long chunk = it / nbands, band = it - chunk * nbands;
+        const long j0 = chunk * TMA_RP_CW, r0 = band * DU_BR;
+        const int cw = (int)min((long)TMA_RP_CW, cols - j0);
+        const int nst = (cw + SCOLS - 1) / SCOLS;
+        const bool bfull = r0 + DU_BR <= rows;
+        for (int sidx = 0; sidx < nst; ++sidx) {
+          const int nbox = min(NCW, (cw - sidx * SCOLS + 15) >> 4);
+          const unsigned bbytes = bfull ? (unsigned)(DU_BR * K * 8) : 0u;
+          mbar_wait(&c.empty[stage], phase ^ 1u);
+          mbar_expect_tx(&c.full[stage], (unsigned)(nbox * DU_BOX * 8) + bbytes);
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d(c.ring + ((size_t)stage * NCW + b) * DU_BOX, &map, &c.full[stage],
+                        (int)(j0 + sidx * SCOLS + 16 * b), (int)r0);
+          if (bfull) bulk_load(c.sX + (size_t)stage * DU_BR * 16, B2 + r0 * K, bbytes, &c.full[stage]);
+          if (++stage == DU_STAGES) stage = 0, phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int g = lane >> 2, t = lane & 3;
+  const int sig = (g >> 1) | ((g & 1) << 2);
+  int stage = 0;
+  unsigned phase = 0;
+  long cur_chunk = -1;
+  int seg = -1;
+  double cacc[DU_CBOX][2][NT][2];  // column part: [box of this warp][parity][tile][2]
+  double ctacc[DU_CBOX][2][TLA];
+  auto zero_cols = [&]() {
+#pragma unroll
+    for (int q = 0; q < DU_CBOX; ++q)
+#pragma unroll
+      for (int par = 0; par < 2; ++par) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) cacc[q][par][nt][0] = cacc[q][par][nt][1] = 0.0;
+#pragma unroll
+        for (int j = 0; j < TLA; ++j) ctacc[q][par][j] = 0.0;
+      }
+  };
+  auto flush_cols = [&](long chunk) {  // partC[cta][seg][local column][p]
+    double* base = partC + ((long)blockIdx.x * DU_SEGS + seg) * (long)TMA_RP_CW * K;
+#pragma unroll
+    for (int q = 0; q < DU_CBOX; ++q)
+#pragma unroll
+      for (int par = 0; par < 2; ++par) {
+        double ts[TLA];
+#pragma unroll
+        for (int j = 0; j < TLA; ++j) ts[j] = TL > 0 ? quad_sum(ctacc[q][par][j]) : 0.0;
+        const int lc = (q * NCW + warp) * 16 + 2 * g + par;  // local column in the chunk
+        double* dst = base + (long)lc * K;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int pp = nt * 8 + 2 * t + e;
+            if (pp < K) dst[pp] = cacc[q][par][nt][e];
+          }
+        if (TL > 0 && t == 0)
+#pragma unroll
+          for (int j = 0; j < TLA; ++j) dst[8 + j] = ts[j];
+      }
+    (void)chunk;
+  };
+  zero_cols();
+  for (long it = i_beg; it < i_end; ++it) {
+    const long chunk = it / nbands, band = it - chunk * nbands;
+    const long j0 = chunk * TMA_RP_CW, r0 = band * DU_BR;
+    const int cw = (int)min((long)TMA_RP_CW, cols - j0);
+    const int nst = (cw + SCOLS - 1) / SCOLS;
+    const bool bfull = r0 + DU_BR <= rows;
+    if (chunk != cur_chunk) {
+      if (cur_chunk >= 0) {
+        flush_cols(cur_chunk);
+        zero_cols();
+      }
+      ++seg;
+      consumers_sync();
+      const int ngrp = 2 * ((cw + 15) >> 4);
+      for (int e = threadIdx.x; e < ngrp * 2 * NT * 32; e += NCW * 32) {
+        const int l = e & 31, se = (e >> 5) / NT, nt = (e >> 5) % NT;
+        const int sidx = se >> 1, ee = se & 1;
+        const long col = j0 + 8 * sidx + 2 * (l & 3) + ee;
+        const int pp = nt * 8 + (l >> 2);
+        const bool ok = col < cols && pp < K;
+        cp_async8(c.sB + e, ok ? B1 + col * K + pp : B1, ok ? 8 : 0);
+      }
+      if (TL > 0)
+        for (int e = threadIdx.x; e < ngrp * 8 * TP; e += NCW * 32) {
+          const int j = e % TP, rec = e / TP;
+          const long col = j0 + 8 * (rec >> 3) + 2 * ((rec >> 1) & 3) + (rec & 1);
+          const bool ok = col < cols && j < TL;
+          cp_async8(c.sT + e, ok ? B1 + col * K + 8 + j : B1, ok ? 8 : 0);
+        }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      consumers_sync();
+      cur_chunk = chunk;
+    }
+    // two independent accumulator sets per tile (even / odd column of each lane's pair):
+    // the DMMA chains are half as deep; summed when the band's chunk is done
+    double racc[NT][2], racc2[NT][2], rtacc[TLA], rtacc2[TLA];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) racc[nt][0] = racc[nt][1] = racc2[nt][0] = racc2[nt][1] = 0.0;
+#pragma unroll
+    for (int j = 0; j < TLA; ++j) rtacc[j] = rtacc2[j] = 0.0;
+    for (int sidx = 0; sidx < nst; ++sidx) {
+      const int nbox = min(NCW, (cw - sidx * SCOLS + 15) >> 4);
+      mbar_wait(&c.full[stage], phase);
+      const double* ring = c.ring + (size_t)stage * NCW * DU_BOX;
+      // -- row part: rows 8 warp + sig over the stage's boxes
+      for (int b = 0; b < nbox; ++b) {
+        const double* box = ring + (size_t)b * DU_BOX;
+        const int r = 8 * warp + sig;
+        const double2 a0 = lds128(box + r * 16 + ((t ^ sig) << 1));
+        const double2 a1 = lds128(box + r * 16 + (((4 + t) ^ sig) << 1));
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const double2 a = kk ? a1 : a0;
+          const int q = 2 * (sidx * NCW + b) + kk;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const double bx = c.sB[((2 * q) * NT + nt) * 32 + lane];
+            const double by = c.sB[((2 * q + 1) * NT + nt) * 32 + lane];
+            dmma(racc[nt][0], racc[nt][1], a.x, bx);
+            dmma(racc2[nt][0], racc2[nt][1], a.y, by);
+          }
+          if (TL > 0) {
+            const double* tr = c.sT + ((q * 4 + t) * 2) * TP;
+#pragma unroll
+            for (int j = 0; j < TLA; ++j) {
+              rtacc[j] = fma(a.x, tr[j], rtacc[j]);
+              rtacc2[j] = fma(a.y, tr[TP + j], rtacc2[j]);
+            }
+          }
+        }
+      }
+      // -- column part: box `warp` of the stage over its 64 rows
+      if (warp < nbox) {
+        const int q = sidx;  // this warp's column box index within the chunk = sidx * NCW + warp
+        const double* box = ring + (size_t)warp * DU_BOX;
+        const double* xs = c.sX + (size_t)stage * DU_BR * 16;
+#pragma unroll
+        for (int qq = 0; qq < DU_CBOX; ++qq) {
+          if (qq != q) continue;  // registers stay statically indexed
+          // the odd contraction rows accumulate into per-stage temporaries (independent
+          // DMMA chains), folded into the chunk accumulators after the stage
+          double u[2][NT][2], ut[2][TLA];
+#pragma unroll
+          for (int par = 0; par < 2; ++par) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) u[par][nt][0] = u[par][nt][1] = 0.0;
+#pragma unroll
+            for (int j = 0; j < TLA; ++j) ut[par][j] = 0.0;
+          }
+#pragma unroll 2
+          for (int blk = 0; blk < DU_BR / 8; ++blk) {
+            const int ra = 8 * blk + 2 * t, rbb = ra + 1;
+            const double2 a0 = lds128(box + ra * 16 + ((g ^ (ra & 7)) << 1));
+            const double2 a1 = lds128(box + rbb * 16 + ((g ^ (rbb & 7)) << 1));
+            const long ia = r0 + ra, ib = ia + 1;
+            double b0[NT], b1[NT];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const int pp = nt * 8 + g;
+              if (bfull) {
+                b0[nt] = pp < K ? xs[ra * K + pp] : 0.0;
+                b1[nt] = pp < K ? xs[rbb * K + pp] : 0.0;
+              } else {
+                b0[nt] = (ia < rows && pp < K) ? __ldg(B2 + ia * K + pp) : 0.0;
+                b1[nt] = (ib < rows && pp < K) ? __ldg(B2 + ib * K + pp) : 0.0;
+              }
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              dmma(cacc[qq][0][nt][0], cacc[qq][0][nt][1], a0.x, b0[nt]);
+              dmma(cacc[qq][1][nt][0], cacc[qq][1][nt][1], a0.y, b0[nt]);
+              dmma(u[0][nt][0], u[0][nt][1], a1.x, b1[nt]);
+              dmma(u[1][nt][0], u[1][nt][1], a1.y, b1[nt]);
+            }
+            if (TL > 0) {
+#pragma unroll
+              for (int j = 0; j < TLA; ++j) {
+                double xa, xb;
+                if (bfull) {
+                  xa = xs[ra * K + 8 + j];
+                  xb = xs[rbb * K + 8 + j];
+                } else {
+                  xa = ia < rows ? __ldg(B2 + ia * K + 8 + j) : 0.0;
+                  xb = ib < rows ? __ldg(B2 + ib * K + 8 + j) : 0.0;
+                }
+                ctacc[qq][0][j] = fma(a0.x, xa, ctacc[qq][0][j]);
+                ctacc[qq][1][j] = fma(a0.y, xa, ctacc[qq][1][j]);
+                ut[0][j] = fma(a1.x, xb, ut[0][j]);
+                ut[1][j] = fma(a1.y, xb, ut[1][j]);
+              }
+            }
+          }
+#pragma unroll
+          for (int par = 0; par < 2; ++par) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              cacc[qq][par][nt][0] += u[par][nt][0], cacc[qq][par][nt][1] += u[par][nt][1];
+#pragma unroll
+            for (int j = 0; j < TLA; ++j) ctacc[qq][par][j] += ut[par][j];
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c.empty[stage]);
+      if (++stage == DU_STAGES) stage = 0, phase ^= 1u;
+    }
+    {  // row partials of this (chunk, band)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) racc[nt][0] += racc2[nt][0], racc[nt][1] += racc2[nt][1];
+      double ts[TLA];
+#pragma unroll
+      for (int j = 0; j < TLA; ++j) ts[j] = TL > 0 ? quad_sum(rtacc[j] + rtacc2[j]) : 0.0;
+      const long row = r0 + 8 * warp + sig;
+      if (row < rows) {
+        double* dst = partR + (chunk * rows + row) * K;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int pp = nt * 8 + 2 * t + e;
+            if (pp < K) dst[pp] = racc[nt][e];
+          }
+        if (TL > 0 && t == 0)
+#pragma unroll
+          for (int j = 0; j < TLA; ++j) dst[8 + j] = ts[j];
+      }
+    }
+  }
+  if (cur_chunk >= 0) flush_cols(cur_chunk);
+}
+
+// outC[j][p] = sum over the CTAs whose item range meets column j's chunk (ascending CTA
+// order, fixed) of partC[cta][segment of that chunk][local column][p]
+__global__ void __launch_bounds__(256) k_sum_dual_cols(const double* __restrict__ partC, long cols,
+                                                       int K, long nitems, long nbands, int G,
+                                                       double* __restrict__ out) {
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cols * K) return;
+  const long j = e / K;
+  const int p = (int)(e - j * K);
+  const long chunk = j / TMA_RP_CW;
+  const long lc = j - chunk * TMA_RP_CW;
+  const long lo = chunk * nbands, hi = lo + nbands;  // the chunk's items [lo, hi)
+  // first CTA whose range [b N / G, (b + 1) N / G) ends after lo
+  long b = (long)((lo * (long)G) / nitems);
+  while (b > 0 && (b * nitems) / G > lo) --b;
+  while ((b + 1) * nitems / G <= lo) ++b;
+  double v = 0.0;
+  for (; b < G && (b * nitems) / G < hi; ++b) {
+    const long first = (b * nitems) / G;
+    const long fend = ((b + 1) * nitems) / G;
+    if (fend <= first) continue;  // empty range
+    const long seg = (lo > first ? lo : first) / nbands - first / nbands;
+    v += partC[((b * DU_SEGS + seg) * TMA_RP_CW + lc) * K + p];
+  }
+  out[e] = v;
+}
+
 // ---- host side ----------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -599,6 +934,59 @@ int tma_colprod_f64(const double* A, long rows, long cols, const double* B, int 
   }
 #undef CP_LAUNCH
   *nparts = ns;
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+long tma_dualprod_work_len(long rows, long cols, long k) {
+  const long nch = (cols + TMA_RP_CW - 1) / TMA_RP_CW;
+  return nch * rows * k + (long)num_sms() * DU_SEGS * TMA_RP_CW * k;
+}
+
+int tma_dualprod_f64(const double* A, long rows, long cols, const double* B1, const double* B2,
+                     int K, double* outR, double* outC, double* work, long work_len,
+                     cudaStream_t st) {
+  if (!tma_prod_enabled() || K < 5 || K > 16 || !shape_ok(A, rows, cols) || (uintptr_t)B2 % 16)
+    return NMFB_EUNSUPPORTED;
+  const long nch = (cols + TMA_RP_CW - 1) / TMA_RP_CW;
+  const long nbands = (rows + DU_BR - 1) / DU_BR;
+  const long nitems = nch * nbands;
+  const int G = (int)min((long)num_sms(), nitems);
+  // every CTA range must meet at most DU_SEGS chunks
+  if ((nitems + G - 1) / G + 1 > (long)(DU_SEGS - 1) * nbands + 1) return NMFB_EUNSUPPORTED;
+  if (tma_dualprod_work_len(rows, cols, K) > work_len) return NMFB_ENOMEM;
+  CUtensorMap map;
+  if (!make_map(&map, A, rows, cols, DU_BR)) return NMFB_EUNSUPPORTED;
+  double* partR = work;
+  double* partC = work + nch * rows * K;
+  const int NT = (K + 7) / 8;
+  const size_t smem = 1024 + DU_STAGES * DU_STAGE_BYTES + 2 * DU_STAGES * 8 +
+                      (size_t)RP_NGRP * 2 * NT * 32 * sizeof(double) +
+                      (size_t)RP_NGRP * 8 * 4 * sizeof(double) +
+                      (size_t)DU_STAGES * DU_BR * 16 * sizeof(double);
+#define DU_LAUNCH(NT_, TL_)                                                                      \
+  nmfb_smem_attr(k_dualprod_tma<NT_, TL_>, smem);                                                \
+  ++g_nmfb_launches, k_dualprod_tma<NT_, TL_><<<G, NTHREADS, smem, st>>>(map, rows, cols, B1, B2, \
+                                                                         K, nitems, nbands,      \
+                                                                         partR, partC)
+  static const int no_tail = [] {
+    const char* e = getenv("NMFB_DUAL_NOTAIL");
+    return e && e[0] == '1';
+  }();
+  switch (no_tail ? 0 : K) {
+    case 9: DU_LAUNCH(1, 1); break;
+    case 10: DU_LAUNCH(1, 2); break;  // K = 11, 12: two DMMA tiles (a 3-4 wide tail spills)
+    default:
+      if (NT == 1) {
+        DU_LAUNCH(1, 0);
+      } else {
+        DU_LAUNCH(2, 0);
+      }
+  }
+#undef DU_LAUNCH
+  ++g_nmfb_launches, k_sum_dual_cols<<<(unsigned)((cols * K + 255) / 256), 256, 0, st>>>(
+      partC, cols, K, nitems, nbands, G, outC);
+  (void)outR;  // the caller sums the row partials (fixed order, with its k_sum_partials)
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

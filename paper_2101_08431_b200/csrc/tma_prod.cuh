@@ -20,3 +20,10 @@ int tma_colprod_f64(const double* A, long rows, long cols, const double* B, int 
                     long work_len, long* nparts, cudaStream_t st);
 // number of row splits tma_colprod_f64 uses (work >= splits * cols * K)
 long tma_colprod_splits(long rows, long cols);
+// ONE pass over M for outR = M B1 (row partials left in work[0 : nch rows K] for the
+// caller's fixed-order k_sum_partials, nch = ceil(cols / TMA_RP_CW)) and outC = M^T B2
+// (finished here).  K in 5..16.
+long tma_dualprod_work_len(long rows, long cols, long k);
+int tma_dualprod_f64(const double* A, long rows, long cols, const double* B1, const double* B2,
+                     int K, double* outR, double* outC, double* work, long work_len,
+                     cudaStream_t st);

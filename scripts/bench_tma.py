@@ -58,13 +58,25 @@ def main():
             b = n * m * 8 + (n + m) * k * 8
             tr = timeit(lambda: P.rowprod(P.M, n, m, Yt, k, r, None, 0))
             tc = timeit(lambda: P.colprod(P.M, n, m, X, k, c, None, 0))
+            dw = torch.empty(P.lib.nmfb_dualprod_work_len(n, m, k), dtype=torch.float64,
+                             device=dev)
+            dr, dc = P.buf(n, k), P.buf(m, k)
+            P.dualprod(Yt, X, dr, dc, dw)
+            torch.cuda.synchronize()
+            outs[("dual", on)] = (dr.clone(), dc.clone())
+            td = timeit(lambda: P.dualprod(Yt, X, dr, dc, dw))
             res["tma" if on else "old"] = {"row_ms": tr, "row_frac": b / tr / 1e6 / PEAK,
-                                           "col_ms": tc, "col_frac": b / tc / 1e6 / PEAK}
+                                           "col_ms": tc, "col_frac": b / tc / 1e6 / PEAK,
+                                           "dual_ms": td, "dual_frac": b / td / 1e6 / PEAK}
         P.lib.nmfb_tma_products(1)
         rr, cr = M @ Yt, M.t() @ X
         res["row_bit_identical"] = bool(torch.equal(outs[1][0], outs[0][0]))
         res["row_relerr"] = float(((outs[1][0] - rr).abs().max() / rr.abs().max()).item())
         res["col_relerr"] = float(((outs[1][1] - cr).abs().max() / cr.abs().max()).item())
+        for on in (1, 0):
+            dr, dc = outs[("dual", on)]
+            res[f"dual_relerr_{on}"] = max(float(((dr - rr).abs().max() / rr.abs().max()).item()),
+                                           float(((dc - cr).abs().max() / cr.abs().max()).item()))
         res["col_relerr_old"] = float(((outs[0][1] - cr).abs().max() / cr.abs().max()).item())
         print(json.dumps(res), flush=True)
         del M, P

@@ -46,6 +46,13 @@ def test_tma_products_match_fp64(n, m, k):
                               rtol=1e-15, atol=0)
     if not 9 <= k <= 12:
         assert torch.equal(res[1][0], res[0][0]), "TMA row product not bit-identical"
+    # one-pass dual product (IPM: M dY^T and M^T dX together)
+    dw = torch.empty(P.lib.nmfb_dualprod_work_len(n, m, k), dtype=torch.float64, device=dev)
+    dr, dc = P.buf(n, k), P.buf(m, k)
+    P.dualprod(Yt, X, dr, dc, dw)
+    torch.cuda.synchronize()
+    assert ((dr - rr).abs().max() / rr.abs().max()).item() < 1e-13
+    assert ((dc - cr).abs().max() / cr.abs().max()).item() < 1e-13
 
 
 def test_smem_attribute_across_problem_sizes():
