@@ -325,7 +325,7 @@ def kkt_from_sums(v):
 # ============================================================================
 # stage 1 (Algorithm 1)
 # ============================================================================
-@_nvtx("nmfb/stage1")
+@_nvtx("nmfb.stage1")
 def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=None):
     """SPEC.md:209 run_stage1 on the device.  X (n,k), Yt (m,k) device fp64.
 
@@ -1014,7 +1014,7 @@ class IpmEngine:
         return min((mu_aff / mu_bar) ** 3, p.sigma_cap)
 
 
-@_nvtx("nmfb/ipm")
+@_nvtx("nmfb.ipm")
 def run_ipm(P: Problem, X, Yt, R, S, mu, rho, p: IpmParams | None = None):
     """SPEC.md:337 run_ipm on the device (Algorithm 2 + Algorithm 3 switch).
 
@@ -1196,7 +1196,7 @@ def _run_ipm(P: Problem, eng, p: IpmParams, t0):
     return res
 
 
-@_nvtx("nmfb/transition")
+@_nvtx("nmfb.transition")
 def transition(P: Problem, X, Yt, eps_tol, tp: TransitionParams | None = None):
     """SPEC.md:393 / PAPER Eqs. 14-18 on the device -> (X, Yt, R, S, mu, rho)."""
     tp = tp or TransitionParams()
@@ -1244,7 +1244,7 @@ def kkt_error_primal_only_dev(P: Problem, X, Yt):
     return kkt_from_sums(v[16:28])[1], 0.5 * v[0]
 
 
-@_nvtx("nmfb/two_stage")
+@_nvtx("nmfb.two_stage")
 def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1: Stage1Config | None = None,
                   ipm: IpmParams | None = None, tp: TransitionParams | None = None,
                   stage="two_stage", pX=None, pY=None, e_scale=None, problem: Problem | None = None,
