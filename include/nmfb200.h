@@ -304,6 +304,9 @@ unsigned long long nmfb_launch_count(void);
  * kernels (0) for nmfb_rowprod / nmfb_colprod; -1 only queries.  Returns the previous
  * setting.  (Both are deterministic; the row products are bit-identical.) */
 int nmfb_tma_products(int on);
+/* Select the tcgen05 (tf32 x 3 split, fp32 accumulate per 512-column chunk, fp64 partials)
+ * products for an fp32 M (1, default) or the FP64 DMMA kernels (0); -1 only queries. */
+int nmfb_tc_products(int on);
 /* Name of the last CUDA error behind an NMFB_ELAUNCH return ("no error" if none). */
 const char *nmfb_last_cuda_error(void);
 

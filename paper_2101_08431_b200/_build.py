@@ -24,6 +24,7 @@ SOURCES = {
     "surface.cu": ["-fmad=false"],
     "anls.cu": [],
     "tma_prod.cu": [],
+    "tc_prod.cu": [],
     "ipm.cu": [],
     "dense.cu": [],
     "lowrank.cu": [],

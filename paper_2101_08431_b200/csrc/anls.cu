@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "nmfb200.h"
+#include "tc_prod.cuh"
 #include "tma_prod.cuh"
 
 unsigned long long g_nmfb_launches = 0;
@@ -712,9 +713,11 @@ int launch_rowprod(const T* A, long rows, long cols, const double* B, double* ou
     return e && e[0] == '1';
   }();
   const bool use_mma = !(sizeof(T) == 4 && f32_simt);
-  if (sizeof(T) == 8 && rowprod_split(rows, cols) && K >= 5) {  // TMA-fed DMMA (tma_prod.cu)
+  if (rowprod_split(rows, cols) && K >= 5) {  // TMA-fed: DMMA (fp64 M) / tcgen05 tf32x3 (fp32 M)
     long nch = 0;
-    const int rc = tma_rowprod_f64((const double*)A, rows, cols, B, K, work, work_len, &nch, st);
+    const int rc = sizeof(T) == 8
+                       ? tma_rowprod_f64((const double*)A, rows, cols, B, K, work, work_len, &nch, st)
+                       : tc_rowprod_f32((const float*)A, rows, cols, B, K, work, work_len, &nch, st);
     if (rc == NMFB_OK) {
       if (!tol && rows * K <= 4096 && nch >= 32)
         ++g_nmfb_launches, k_sum_partials_warp<<<(unsigned)((rows * K + 7) / 8), 256, 0, st>>>(

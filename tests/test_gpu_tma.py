@@ -71,3 +71,24 @@ def test_smem_attribute_across_problem_sizes():
                               IpmParams(fixed_iters=3, schur_solver="lowrank", persistent=False,
                                         fused_small=False))
         assert r.iters == 3
+
+
+@pytest.mark.parametrize("n,m,k", [(4100, 2052, 10), (8192, 4096, 16), (5000, 3000, 5)])
+def test_tcgen05_rowprod_fp32(n, m, k):
+    """fp32 M (config c5 storage): the tcgen05 tf32 x 3 row product (csrc/tc_prod.cu) against
+    fp64 torch -- relative error ~2e-6 (tf32 split ~2^-21 per term, fp32 tensor-core
+    accumulation flushed to fp64 every 128 columns); bound 1e-5."""
+    from paper_2101_08431_b200 import solver
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(n * k)
+    M = torch.rand((n, m), generator=g, device=dev, dtype=torch.float32)
+    P = solver.Problem(M, k)
+    Yt = torch.rand((m, k), generator=g, device=dev, dtype=torch.float64)
+    assert P.lib.nmfb_tc_products(-1) == 1
+    r = P.buf(n, k)
+    P.rowprod(P.M, n, m, Yt, k, r, None, 1)
+    torch.cuda.synchronize()
+    rr = M.double() @ Yt
+    assert ((r - rr).abs().max() / rr.abs().max()).item() < 1e-5
