@@ -20,6 +20,12 @@ constexpr int CHOL_BLK_THREADS = 384;
 inline size_t chol_blk_smem(long N) {  // diagonal block (32 x 33) + transposed panel (32 x N)
   return (size_t)(32 * 33 + 32 * (N + 2)) * sizeof(double);
 }
+// N <= CHOL_STAGE_MAX: the whole matrix is staged in shared memory for the factorization
+// (every panel / trailing-update access hits shared memory instead of L2)
+constexpr int CHOL_STAGE_MAX = 128;
+inline size_t chol_blk_smem_staged(long N) {
+  return chol_blk_smem(N) + (N <= CHOL_STAGE_MAX ? (size_t)N * N * sizeof(double) : 0);
+}
 
 template <int J, int C>
 struct BCholUpd {
@@ -76,7 +82,7 @@ __device__ __noinline__ void chol_diag_block(double* A, long N, int p0, int nb, 
 
 // info: failure -> fail_base + pivot column; success -> -1 when set_ok.
 // skip_if_set: do nothing if *info >= 0 on entry (an earlier factorization failed).
-__global__ void __launch_bounds__(CHOL_BLK_THREADS) k_chol_blk(double* __restrict__ A, int N,
+__global__ void __launch_bounds__(CHOL_BLK_THREADS) k_chol_blk(double* __restrict__ Ag, int N,
                                                                int* __restrict__ info,
                                                                int fail_base, int skip_if_set,
                                                                int set_ok) {
@@ -89,6 +95,18 @@ __global__ void __launch_bounds__(CHOL_BLK_THREADS) k_chol_blk(double* __restric
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nwarp = (int)(blockDim.x >> 5);
   const int LDT = N + 2;
+  const bool staged = N <= CHOL_STAGE_MAX;
+  double* A = Ag;
+  if (staged) {  // the matrix into shared memory, all loads in flight
+    A = pT + 32 * LDT;
+    for (int e = tid; e < N * N; e += blockDim.x) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(A + e)),
+                     "l"(Ag + e)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  }
   if (tid == 0) sfail = -1;
   __syncthreads();
   for (int p0 = 0; p0 < N; p0 += 32) {
@@ -171,8 +189,16 @@ __global__ void __launch_bounds__(CHOL_BLK_THREADS) k_chol_blk(double* __restric
     __syncthreads();
   }
   const int f = sfail;
-  for (int r = wid; r < N; r += nwarp)
-    for (int c = r + 1 + lane; c < N; c += 32) A[(long)r * N + c] = 0.0;
+  if (staged) {
+    __syncthreads();
+    for (int e = tid; e < N * N; e += blockDim.x) {
+      const int r = e / N, c = e - (e / N) * N;
+      Ag[e] = c <= r ? A[e] : 0.0;
+    }
+  } else {
+    for (int r = wid; r < N; r += nwarp)
+      for (int c = r + 1 + lane; c < N; c += 32) A[(long)r * N + c] = 0.0;
+  }
   if (tid == 0) {
     if (f >= 0)
       *info = fail_base + f;
@@ -342,8 +368,8 @@ __global__ void __launch_bounds__(CHOL_COOP_THREADS) k_chol_coop(double* __restr
 inline int launch_chol(double* A, int N, int* info, int fail_base, int skip_if_set, int set_ok,
                        cudaStream_t st) {
   if (N <= 128) {
-    const size_t sm = chol_blk_smem(N);
-    cudaFuncSetAttribute(k_chol_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    const size_t sm = chol_blk_smem_staged(N);
+    nmfb_smem_attr(k_chol_blk, sm);
     ++g_nmfb_launches, k_chol_blk<<<1, CHOL_BLK_THREADS, sm, st>>>(A, N, info, fail_base,
                                                                    skip_if_set, set_ok);
     return NMFB_OK;

@@ -313,11 +313,21 @@ __global__ void __launch_bounds__(256) k_lowrank_apply(const double* __restrict_
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   if (use_smem) {
     double* sg = sm + 2 * Q;
-    double* shh = sg + Q * Q;
-    for (int e = tid; e < Q * Q; e += blockDim.x) {
-      sg[e] = LGg[e];
-      shh[e] = LHg[e];
+    double* shh = sg + ((Q * Q + 1) & ~1);  // 16-byte aligned for cp.async
+    // both factors in flight at once (cp.async), instead of one dependent load per trip
+    for (int e = 2 * tid; e < Q * Q; e += 2 * blockDim.x) {
+      if (e + 1 < Q * Q) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(sg + e)), "l"(LGg + e) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(shh + e)), "l"(LHg + e) : "memory");
+      } else {
+        sg[e] = LGg[e];
+        shh[e] = LHg[e];
+      }
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
     LG = sg;
     LH = shh;
   }
@@ -404,7 +414,7 @@ extern "C" int nmfb_lowrank_solve(const double* LD, const double* Yt, const doub
   int rc = nmfb_colprod(Yt, 0, m, k, dy, k, u, nullptr, 1.0, cwork, cwork_len, stream);
   if (rc != NMFB_OK) return rc;
   const long Q = k * k;
-  const size_t sm_full = (size_t)(2 * Q + 2 * Q * Q) * sizeof(double);
+  const size_t sm_full = (size_t)(2 * Q + 2 * Q * Q + 2) * sizeof(double);
   const int apply_smem = sm_full <= 200 * 1024;
   const size_t sm_apply = apply_smem ? sm_full : 2 * Q * sizeof(double);
   if (apply_smem)

@@ -760,30 +760,44 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 // outC[j][p] = sum over the CTAs whose item range meets column j's chunk (ascending CTA
-// order, fixed) of partC[cta][segment of that chunk][local column][p]
+// order, fixed) of partC[cta][segment of that chunk][local column][p].  One block row per
+// chunk (blockIdx.y): thread 0 lists the contributing (CTA, segment) slots once.
 __global__ void __launch_bounds__(256) k_sum_dual_cols(const double* __restrict__ partC, long cols,
                                                        int K, long nitems, long nbands, int G,
                                                        double* __restrict__ out) {
-  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= cols * K) return;
-  const long j = e / K;
-  const int p = (int)(e - j * K);
-  const long chunk = j / TMA_RP_CW;
-  const long lc = j - chunk * TMA_RP_CW;
-  const long lo = chunk * nbands, hi = lo + nbands;  // the chunk's items [lo, hi)
-  // first CTA whose range [b N / G, (b + 1) N / G) ends after lo
-  long b = (long)((lo * (long)G) / nitems);
-  while (b > 0 && (b * nitems) / G > lo) --b;
-  while ((b + 1) * nitems / G <= lo) ++b;
-  double v = 0.0;
-  for (; b < G && (b * nitems) / G < hi; ++b) {
-    const long first = (b * nitems) / G;
-    const long fend = ((b + 1) * nitems) / G;
-    if (fend <= first) continue;  // empty range
-    const long seg = (lo > first ? lo : first) / nbands - first / nbands;
-    v += partC[((b * DU_SEGS + seg) * TMA_RP_CW + lc) * K + p];
+  __shared__ int slot[256];
+  __shared__ int wcnt[8];
+  __shared__ int nslot;
+  const long chunk = blockIdx.y;
+  {  // thread b tests CTA b (G <= 256); ballot prefix keeps ascending CTA order
+    const int b = threadIdx.x, lane = b & 31, w = b >> 5;
+    const long lo = chunk * nbands, hi = lo + nbands;  // the chunk's items [lo, hi)
+    bool hit = false;
+    int sl = 0;
+    if (b < G) {
+      const long first = ((long)b * nitems) / G, fend = ((long)(b + 1) * nitems) / G;
+      hit = fend > first && fend > lo && first < hi;
+      if (hit) sl = (int)((long)b * DU_SEGS + (max(lo, first) / nbands - first / nbands));
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) wcnt[w] = __popc(m);
+    __syncthreads();
+    int base = 0;
+    for (int i = 0; i < w; ++i) base += wcnt[i];
+    if (hit) slot[base + __popc(m & ((1u << lane) - 1u))] = sl;
+    if (b == 255) {
+      int n = 0;
+      for (int i = 0; i < 8; ++i) n += wcnt[i];
+      nslot = n;
+    }
   }
-  out[e] = v;
+  __syncthreads();
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;  // element within the chunk
+  const long cw = min((long)TMA_RP_CW, cols - chunk * TMA_RP_CW);
+  if (e >= cw * K) return;
+  double v = 0.0;
+  for (int i = 0; i < nslot; ++i) v += partC[(long)slot[i] * TMA_RP_CW * K + e];
+  out[chunk * TMA_RP_CW * K + e] = v;
 }
 
 // ---- host side ----------------------------------------------------------------
@@ -955,6 +969,7 @@ int tma_dualprod_f64(const double* A, long rows, long cols, const double* B1, co
   // every CTA range must meet at most DU_SEGS chunks
   if ((nitems + G - 1) / G + 1 > (long)(DU_SEGS - 1) * nbands + 1) return NMFB_EUNSUPPORTED;
   if (tma_dualprod_work_len(rows, cols, K) > work_len) return NMFB_ENOMEM;
+  if (G > 256) return NMFB_EUNSUPPORTED;  // k_sum_dual_cols: one thread per CTA
   CUtensorMap map;
   if (!make_map(&map, A, rows, cols, DU_BR)) return NMFB_EUNSUPPORTED;
   double* partR = work;
@@ -984,8 +999,8 @@ int tma_dualprod_f64(const double* A, long rows, long cols, const double* B1, co
       }
   }
 #undef DU_LAUNCH
-  ++g_nmfb_launches, k_sum_dual_cols<<<(unsigned)((cols * K + 255) / 256), 256, 0, st>>>(
-      partC, cols, K, nitems, nbands, G, outC);
+  ++g_nmfb_launches, k_sum_dual_cols<<<dim3((unsigned)((TMA_RP_CW * K + 255) / 256), (unsigned)nch),
+                                        256, 0, st>>>(partC, cols, K, nitems, nbands, G, outC);
   (void)outR;  // the caller sums the row partials (fixed order, with its k_sum_partials)
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;

@@ -146,6 +146,24 @@ class Problem:
         self.hscal = torch.zeros(256, dtype=torch.float64).pin_memory()
         self.hint = torch.zeros(16, dtype=torch.int32).pin_memory()
 
+    def load(self, Mnew):
+        """Replace the data of M in place (same shape): one host-to-device copy into the
+        resident buffer (non-blocking from pinned memory), the squared row / column norms
+        recomputed on the device.  Buffers, tensor maps' targets and cached IPM engines (with
+        their CUDA graphs) stay valid -- the serving pattern for repeated solves."""
+        if isinstance(Mnew, np.ndarray):
+            Mnew = torch.from_numpy(np.ascontiguousarray(Mnew))
+        if tuple(Mnew.shape) != (self.n, self.m):
+            raise ValueError(f"load: shape {tuple(Mnew.shape)} != {(self.n, self.m)}")
+        self.M.copy_(Mnew.to(dtype=self.M.dtype), non_blocking=True)
+        self._call("nmfb_sqnorms", _p(self.M), self.f32, self.n, self.m, _p(self.row_n2),
+                   _p(self.col_n2), _p(self.cwork), self.cwork.numel(), self.stream)
+        self.comm.sum_(self.col_n2)
+        self.mnorm2_local = float(self.row_n2.sum().item())
+        for eng in self.__dict__.get("_engines", {}).values():
+            eng.mvalid = False  # incremental residual-free refresh restarts from M
+        return self
+
     def append_columns(self, Mnew):
         """Append columns (n, c) -- host or device, fp32 or fp64 -- in place: the active
         M moves once into the other pre-allocated buffer with the new columns behind it
@@ -1259,6 +1277,8 @@ def run_two_stage(M, X0, Y0, tol_rel=1e-10, s1: Stage1Config | None = None,
     """
     X0n = X0 if isinstance(X0, torch.Tensor) else np.asarray(X0, dtype=np.float64)
     k = X0n.shape[1]
+    if problem is not None and M is not None and M is not problem.M:
+        problem.load(M)  # new data into the resident problem (no allocation)
     P = problem or Problem(M, k, comm=comm)
 
     def carry(c):

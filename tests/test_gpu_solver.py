@@ -374,3 +374,22 @@ def test_c5_shape_fp32_ipm(mods):
     assert r.armijo_t == ro2.armijo_t
     for a, b in ((eng.X, ro2.state.X), (eng.Yt, ro2.state.Yt)):
         assert rel(a.cpu().numpy(), b) < 1e-4
+
+
+def test_problem_load_reuse(mods):
+    """run_two_stage(M_host, ..., problem=P) copies the new data into the resident problem
+    (Problem.load): same result as a fresh problem, for two different matrices in turn."""
+    data, solver, IpmParams, Stage1Config = mods
+    import torch
+
+    cfg = data.CONFIGS["c1"]
+    M1, X0, Y0, _, _ = data.make(cfg)
+    M2 = M1[:, ::-1].copy()  # another instance of the same shape
+    P = solver.Problem(M1, cfg.k)
+    for M in (M1, M2, M1):
+        ref = solver.run_two_stage(M, X0, Y0, tol_rel=cfg.tol, ipm=IpmParams(fixed_iters=15))
+        got = solver.run_two_stage(torch.from_numpy(M).pin_memory(), X0, Y0, tol_rel=cfg.tol,
+                                   ipm=IpmParams(fixed_iters=15), problem=P)
+        assert got.stage1.sweeps == ref.stage1.sweeps
+        assert np.array_equal(got.X, ref.X) and np.array_equal(got.Yt, ref.Yt)
+        assert got.final_objective == ref.final_objective
