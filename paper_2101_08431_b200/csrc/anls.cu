@@ -799,9 +799,11 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
     cudaMemsetAsync(out, 0, sizeof(double) * cols * K, st);
     return NMFB_OK;
   }
-  if (sizeof(T) == 8 && colprod_tiled(rows, cols) && K >= 5) {  // TMA-fed DMMA (tma_prod.cu)
+  if (colprod_tiled(rows, cols) && K >= 5) {  // TMA-fed DMMA (tma_prod.cu)
     long ns = 0;
-    const int rc = tma_colprod_f64((const double*)A, rows, cols, B, K, work, work_len, &ns, st);
+    const int rc = sizeof(T) == 8
+                       ? tma_colprod_f64((const double*)A, rows, cols, B, K, work, work_len, &ns, st)
+                       : tma_colprod_f32((const float*)A, rows, cols, B, K, work, work_len, &ns, st);
     if (rc == NMFB_OK) {
       if (!tol && cols * K <= 4096 && ns >= 32)
         ++g_nmfb_launches, k_sum_partials_warp<<<(unsigned)((cols * K + 7) / 8), 256, 0, st>>>(
@@ -1074,7 +1076,7 @@ extern "C" long nmfb_colprod_work_len(long rows, long cols, long k) {
   const long stripe = colprod_stripe(rows, cols);
   long ns = (rows + stripe - 1) / stripe;
   if (colprod_tiled(rows, cols)) {
-    const long nt = tma_colprod_splits(rows, cols);
+    const long nt = 2 * tma_colprod_splits(rows, cols);  // fp32: two row halves per split
     if (nt > ns) ns = nt;
   }
   return ns * cols * k;

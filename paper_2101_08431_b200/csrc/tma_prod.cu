@@ -450,6 +450,123 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
+// ---- column product, fp32 M (config c5) --------------------------------------
+// Same item / split scheme as k_colprod_tma; a stage is 4 boxes of 32 fp32 columns x 32
+// rows (16 KB) + the stage's 32 rows of B.  Warp w owns box (w & 3) and the row half
+// (w >> 2) of every stage; lane (g, t) reads a float4 (columns 4g .. 4g + 3) of the lines
+// 2t and 2t + 1 of each 8-row block -- under the 128B swizzle the eight lanes of a
+// quarter-warp hit the chunks g ^ 2t, all distinct -- and feeds four column parities to
+// the FP64 tensor cores (fp32 -> fp64 exactly).  The two row halves write separate
+// partials (2 per split), summed with the rest in k_sum_partials' fixed order.
+constexpr int CP32_CW = 128;
+constexpr int CP32_BR = 32;
+constexpr int CP32_BOX = CP32_BR * 32;  // floats per box (4 KB)
+
+template <int NT>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_colprod_tma_f32(const __grid_constant__ CUtensorMap map, long rows, long cols,
+                      const double* __restrict__ B, int K, long nitems, long nsplit,
+                      long split_rows, double* __restrict__ part) {
+  extern __shared__ uint8_t smem_raw[];
+  const Carve c = carve(smem_raw);
+  double* sXs = c.extra;  // [STAGES][CP32_BR][<= 16]
+  init_barriers(c);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long i_beg = (long)blockIdx.x * nitems / gridDim.x;
+  const long i_end = (long)(blockIdx.x + 1) * nitems / gridDim.x;
+  float* ring = reinterpret_cast<float*>(c.ring);
+  constexpr int SBYTES = 4 * CP32_BOX * 4;  // 16 KB of M per stage
+
+  if (warp == NCW) {  // ===== TMA producer =====
+    if (lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (long it = i_beg; it < i_end; ++it) {
+        const long chunk = it / nsplit, s = it - chunk * nsplit;
+        const long rb = s * split_rows, re = min(rows, rb + split_rows);
+        for (long r0 = rb; r0 < re; r0 += CP32_BR) {
+          const bool bfull = r0 + CP32_BR <= re;
+          const unsigned bbytes = bfull ? (unsigned)(CP32_BR * K * 8) : 0u;
+          mbar_wait(&c.empty[stage], phase ^ 1u);
+          mbar_expect_tx(&c.full[stage], (unsigned)SBYTES + bbytes);
+          for (int b = 0; b < 4; ++b)
+            tma_load_2d(ring + ((size_t)stage * 4 + b) * CP32_BOX, &map, &c.full[stage],
+                        (int)(chunk * CP32_CW + 32 * b), (int)r0);
+          if (bfull) bulk_load(sXs + (size_t)stage * CP32_BR * 16, B + r0 * K, bbytes, &c.full[stage]);
+          if (++stage == STAGES) stage = 0, phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  const int g = lane >> 2, t = lane & 3;
+  const int bx = warp & 3, rh = warp >> 2;  // box, row half of the stage
+  int stage = 0;
+  unsigned phase = 0;
+  for (long it = i_beg; it < i_end; ++it) {
+    const long chunk = it / nsplit, s = it - chunk * nsplit;
+    const long rb = s * split_rows, re = min(rows, rb + split_rows);
+    double acc[4][NT][2];  // [column parity][n tile][2]
+#pragma unroll
+    for (int par = 0; par < 4; ++par)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[par][nt][0] = acc[par][nt][1] = 0.0;
+    for (long r0 = rb; r0 < re; r0 += CP32_BR) {
+      mbar_wait(&c.full[stage], phase);
+      const float* box = ring + ((size_t)stage * 4 + bx) * CP32_BOX;
+      const double* xs = sXs + (size_t)stage * CP32_BR * 16;
+      const bool bfull = r0 + CP32_BR <= re;
+#pragma unroll
+      for (int bl = 0; bl < 2; ++bl) {
+        const int blk = 2 * rh + bl;
+        const int ra = 8 * blk + 2 * t, rbb = ra + 1;
+        const float4 f0 = *reinterpret_cast<const float4*>(box + ra * 32 + ((g ^ (ra & 7)) << 2));
+        const float4 f1 = *reinterpret_cast<const float4*>(box + rbb * 32 + ((g ^ (rbb & 7)) << 2));
+        const long ia = r0 + ra, ib = ia + 1;
+        double b0[NT], b1[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int pp = nt * 8 + g;
+          if (bfull) {
+            b0[nt] = pp < K ? xs[ra * K + pp] : 0.0;
+            b1[nt] = pp < K ? xs[rbb * K + pp] : 0.0;
+          } else {
+            b0[nt] = (ia < re && pp < K) ? __ldg(B + ia * K + pp) : 0.0;
+            b1[nt] = (ib < re && pp < K) ? __ldg(B + ib * K + pp) : 0.0;
+          }
+        }
+        const double a0[4] = {(double)f0.x, (double)f0.y, (double)f0.z, (double)f0.w};
+        const double a1[4] = {(double)f1.x, (double)f1.y, (double)f1.z, (double)f1.w};
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+          for (int par = 0; par < 4; ++par) dmma(acc[par][nt][0], acc[par][nt][1], a0[par], b0[nt]);
+#pragma unroll
+          for (int par = 0; par < 4; ++par) dmma(acc[par][nt][0], acc[par][nt][1], a1[par], b1[nt]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c.empty[stage]);
+      if (++stage == STAGES) stage = 0, phase ^= 1u;
+    }
+    // D row g of parity par <-> column 32 bx + 4 g + par of the chunk
+#pragma unroll
+    for (int par = 0; par < 4; ++par) {
+      const long col = chunk * CP32_CW + 32 * bx + 4 * g + par;
+      if (col >= cols) continue;
+      double* dst = part + ((2 * s + rh) * cols + col) * K;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int pp = nt * 8 + 2 * t + e;
+          if (pp < K) dst[pp] = acc[par][nt][e];
+        }
+    }
+  }
+}
+
 // ---- dual product -----------------------------------------------------------
 // ONE pass over M for both outR = M B1 (rows x K, B1: cols x K, e.g. M dY^T) and
 // outC = M^T B2 (cols x K, B2: rows x K, e.g. M^T dX) -- the two products of every
@@ -1002,6 +1119,47 @@ int tma_dualprod_f64(const double* A, long rows, long cols, const double* B1, co
   ++g_nmfb_launches, k_sum_dual_cols<<<dim3((unsigned)((TMA_RP_CW * K + 255) / 256), (unsigned)nch),
                                         256, 0, st>>>(partC, cols, K, nitems, nbands, G, outC);
   (void)outR;  // the caller sums the row partials (fixed order, with its k_sum_partials)
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+// fp32 M: the FP64 tensor-core column product fed by TMA (c5's M^T X / M^T dX)
+int tma_colprod_f32(const float* A, long rows, long cols, const double* B, int K, double* work,
+                    long work_len, long* nparts, cudaStream_t st) {
+  if (!tma_prod_enabled() || K < 1 || K > 16 || (uintptr_t)A % 16 || cols % 4 ||
+      rows >= (1L << 31) || cols >= (1L << 31) || (uintptr_t)B % 16)
+    return NMFB_EUNSUPPORTED;
+  const long nch = (cols + CP32_CW - 1) / CP32_CW;
+  long ns = tma_colprod_splits(rows, cols);
+  long sr = (rows + ns - 1) / ns;
+  sr = ((sr + CP32_BR - 1) / CP32_BR) * CP32_BR;
+  ns = (rows + sr - 1) / sr;
+  if (2 * ns * cols * K > work_len) return NMFB_ENOMEM;
+  auto fn = encode_fn();
+  if (!fn) return NMFB_EUNSUPPORTED;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+  const cuuint32_t box[2] = {32, (cuuint32_t)CP32_BR};
+  const cuuint32_t es[2] = {1, 1};
+  if (fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)A, dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return NMFB_EUNSUPPORTED;
+  const long nitems = nch * ns;
+  const int grid = (int)min((long)num_sms(), nitems);
+  const size_t smem = 1024 + STAGES * STAGE_BYTES + 2 * STAGES * 8 +
+                      (size_t)STAGES * CP32_BR * 16 * sizeof(double);
+  if (K <= 8) {
+    nmfb_smem_attr(k_colprod_tma_f32<1>, smem);
+    ++g_nmfb_launches, k_colprod_tma_f32<1><<<grid, NTHREADS, smem, st>>>(map, rows, cols, B, K,
+                                                                          nitems, ns, sr, work);
+  } else {
+    nmfb_smem_attr(k_colprod_tma_f32<2>, smem);
+    ++g_nmfb_launches, k_colprod_tma_f32<2><<<grid, NTHREADS, smem, st>>>(map, rows, cols, B, K,
+                                                                          nitems, ns, sr, work);
+  }
+  *nparts = 2 * ns;
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

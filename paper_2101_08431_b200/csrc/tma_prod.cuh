@@ -27,3 +27,6 @@ long tma_dualprod_work_len(long rows, long cols, long k);
 int tma_dualprod_f64(const double* A, long rows, long cols, const double* B1, const double* B2,
                      int K, double* outR, double* outC, double* work, long work_len,
                      cudaStream_t st);
+// fp32 M (c5): TMA-fed FP64 tensor-core column product; *nparts = 2 x the row splits
+int tma_colprod_f32(const float* A, long rows, long cols, const double* B, int K, double* work,
+                    long work_len, long* nparts, cudaStream_t st);
