@@ -38,8 +38,8 @@ import numpy as np  # noqa: E402
 
 WORKLOAD = "c4"
 UNIT = "solver iterations/s (ANLS sweeps + IPM iterations)"
-ROOF_ENTRY = "nmfb_rowprod"  # k_rowprod_mma: the dominant kernel of the c4 step
-# DRAM bytes per k_rowprod_mma launch at c4 (ncu --set full, cold cache); see profiles/
+ROOF_ENTRY = "nmfb_rowprod"  # k_rowprod_tma: the dominant HBM-bound kernel of the c4 step
+# DRAM bytes per k_rowprod_tma launch at c4 (ncu --set full, cold cache); see profiles/
 NCU_TRAFFIC = {"dram_bytes": None, "source": None}
 NCU_FILE = os.path.join(ROOT, "profiles", "r02_ncu_rowprod_c4.json")
 
@@ -352,7 +352,7 @@ def run_b200(args):
     except Exception:  # noqa: BLE001
         fp64_peak = float("nan")
     avg_ms = float(np.mean(kt)) if kt else float("nan")
-    # k_rowprod_mma (ctb = M Y^T): algorithmic bytes per launch = one read of this rank's
+    # k_rowprod_tma (ctb = M Y^T): algorithmic bytes per launch = one read of this rank's
     # rows of M + Y + the (rows x k) output + the per-row tolerance; 2 rows m k flops
     rows = b - a
     nbytes = rows * cfg.m * 8 + cfg.m * cfg.k * 8 + rows * cfg.k * 8 + rows * 8
@@ -375,8 +375,9 @@ def run_b200(args):
         "ms_per_sweep": s1_ms / max(sweeps, 1), "ms_per_ipm_iter": s2_ms / max(iters, 1),
         "objective_after_step": fobj,
         "roofline": {"bound": "hbm",
-                     "kernel": "k_rowprod_mma (nmfb_rowprod: M Y^T / M dY^T streaming product, "
-                               "FP64 tensor cores)",
+                     "kernel": "k_rowprod_tma + its fixed-order partial sum (nmfb_rowprod: "
+                               "ctb = M Y^T of every X-update; TMA-fed 128B-swizzled shared-"
+                               "memory ring, FP64 tensor cores + DFMA tail at k = 10)",
                      "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
                      "traffic": traffic, "traffic_source": traffic_src,

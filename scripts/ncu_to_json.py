@@ -24,7 +24,8 @@ def main(rep, out, name=""):
             v = r[h.index(key)].replace(",", "")
             u = units[h.index(key)]
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
-                     "usecond": 1e-6, "msecond": 1e-3, "second": 1}.get(u, 1)
+                     "usecond": 1e-6, "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6,
+                     "ms": 1e-3, "s": 1}.get(u, 1)
             return float(v) * scale
 
         launches.append({"kernel": r[h.index("Kernel Name")][:120],
