@@ -801,9 +801,14 @@ int launch_colprod(const T* A, long rows, long cols, const double* B, double* ou
   }
   if (colprod_tiled(rows, cols) && K >= 5) {  // TMA-fed DMMA (tma_prod.cu)
     long ns = 0;
-    const int rc = sizeof(T) == 8
-                       ? tma_colprod_f64((const double*)A, rows, cols, B, K, work, work_len, &ns, st)
-                       : tma_colprod_f32((const float*)A, rows, cols, B, K, work, work_len, &ns, st);
+    int rc = NMFB_EUNSUPPORTED;
+    if (sizeof(T) == 8)
+      rc = tma_colprod_f64((const double*)A, rows, cols, B, K, work, work_len, &ns, st);
+    else {
+      rc = tc_colprod_f32((const float*)A, rows, cols, B, K, work, work_len, &ns, st);
+      if (rc == NMFB_EUNSUPPORTED)
+        rc = tma_colprod_f32((const float*)A, rows, cols, B, K, work, work_len, &ns, st);
+    }
     if (rc == NMFB_OK) {
       if (!tol && cols * K <= 4096 && ns >= 32)
         ++g_nmfb_launches, k_sum_partials_warp<<<(unsigned)((cols * K + 7) / 8), 256, 0, st>>>(

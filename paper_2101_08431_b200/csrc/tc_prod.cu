@@ -128,6 +128,17 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
 // tf32 split of an fp32 value: hi = value with the low 13 mantissa bits cleared, lo = rest
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
@@ -196,7 +207,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < TC_STAGES; ++i) {
       mbar_init(&s.full[i], 1);
-      mbar_init(&s.conv[i], TC_NCONV);
+      mbar_init(&s.conv[i], 4);  // one converter group per stage
       mbar_init(&s.empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -286,8 +297,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int ct = threadIdx.x - 128;  // 0 .. 32 TC_NCONV - 1
     const bool epi = warp < 8;         // warps 4..7: one per TMEM lane quadrant
     const int q = warp & 3;            // TMEM lane quadrant of this warp
-    const int half = (warp - 4) >> 2;  // which 16 of the tile's 32 columns this warp converts
+    const int grp = (warp - 4) >> 2;   // converter group: stages alternate between the two groups
     const int r = 32 * q + lane;       // tile row (= TMEM lane) this thread converts
+    unsigned gcnt = 0;
     int st = 0, lo_i = 0;
     unsigned ph = 0;
     unsigned lo_ph[TC_LO] = {};
@@ -379,36 +391,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         cur_chunk = chunk;
       }
       for (int k = 0; k < nst; ++k) {
-        mbar_wait(&s.full[st], ph);
-        mbar_wait(&s.loe[lo_i], lo_ph[lo_i] ^ 1u);  // the MMAs TC_LO conversions back are done
+        const bool mine = (gcnt++ & 1) == grp;
         lo_ph[lo_i] ^= 1u;
-        tc_fence_after();
-        // this thread's row r, columns 16 half .. 16 half + 15 (chunks 4 half .. 4 half + 3)
-        const uint8_t* row = reinterpret_cast<const uint8_t*>(s.hi + (size_t)st * (TC_TILE / 4)) + r * 128;
-        uint32_t lo[16];
+        if (mine) {
+          mbar_wait(&s.full[st], ph);
+          mbar_wait(&s.loe[lo_i], lo_ph[lo_i]);  // the MMAs TC_LO conversions back are done
+          tc_fence_after();
+          // this thread's row r: all 32 columns (8 swizzled 16-byte chunks)
+          const uint8_t* row = reinterpret_cast<const uint8_t*>(s.hi + (size_t)st * (TC_TILE / 4)) + r * 128;
+          uint32_t lo[32];
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          const int ch = 4 * half + c4;
-          const float4 x = *reinterpret_cast<const float4*>(row + ((ch ^ (r & 7)) << 4));
-          float h_, l_;
-          split_tf32(x.x, h_, l_), lo[4 * c4 + 0] = __float_as_uint(l_);
-          split_tf32(x.y, h_, l_), lo[4 * c4 + 1] = __float_as_uint(l_);
-          split_tf32(x.z, h_, l_), lo[4 * c4 + 2] = __float_as_uint(l_);
-          split_tf32(x.w, h_, l_), lo[4 * c4 + 3] = __float_as_uint(l_);
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 x = *reinterpret_cast<const float4*>(row + ((c4 ^ (r & 7)) << 4));
+            float h_, l_;
+            split_tf32(x.x, h_, l_), lo[4 * c4 + 0] = __float_as_uint(l_);
+            split_tf32(x.y, h_, l_), lo[4 * c4 + 1] = __float_as_uint(l_);
+            split_tf32(x.z, h_, l_), lo[4 * c4 + 2] = __float_as_uint(l_);
+            split_tf32(x.w, h_, l_), lo[4 * c4 + 3] = __float_as_uint(l_);
+          }
+          const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + TC_LO_COL + (uint32_t)(lo_i * TC_BC);
+          tmem_st32(taddr, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s.conv[st]);
         }
-        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + TC_LO_COL +
-                               (uint32_t)(lo_i * TC_BC + 16 * half);
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-            "%13,%14,%15,%16};" ::"r"(taddr),
-            "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]),
-            "r"(lo[7]), "r"(lo[8]), "r"(lo[9]), "r"(lo[10]), "r"(lo[11]), "r"(lo[12]), "r"(lo[13]),
-            "r"(lo[14]), "r"(lo[15])
-            : "memory");
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s.conv[st]);
         if (++lo_i == TC_LO) lo_i = 0;
         if (++st == TC_STAGES) st = 0, ph ^= 1u;
         // the previous accumulator's epilogue, TC_EPI_LAG stages behind its last MMAs (they
@@ -423,6 +430,282 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             pend_chunk = -1;
           }
           pend_chunk = chunk, pend_band = band, pend_acc = acc, pend_last = (k == nst - 1);
+          pend_age = 0;
+          acc ^= 1;
+        }
+      }
+    }
+    if (epi && pend_chunk >= 0) epilogue();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TC_TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Column product for an fp32 M: part[split][col][p] = sum_{i in split} M[i][col] X[i][p]
+// (Y-update X^T M, graY, the IPM's M^T dX).  D = M^T X: the UMMA M dimension is 128
+// columns of M (TMEM lanes), K runs down the rows.  A stage is 32 rows x 128 columns:
+// four TMA boxes of 32 columns x 32 rows (128B swizzle), which is the canonical
+// MN-major SW128 operand (LBO = 4 KB between the 32-column boxes, SBO = 1 KB between
+// 8-row groups), plus the stage's 32 rows of X by one bulk copy.  Converters (8 warps)
+// write Ml (thread = column, 16 rows each) to tensor memory and [Xh | Xl]^T as the
+// K-major SW128 B operand of the stage; MMAs per 8 rows: Mh^T [Xh | Xl] (N = 32, A
+// MN-major from shared memory) and Ml^T Xh (N = 16, A from tensor memory).  Item =
+// (128-column chunk, row split), chunk-major, contiguous per CTA; accumulators flushed to
+// fp64 every TC_SUB stages (128 rows) like the row product.
+// ---------------------------------------------------------------------------
+constexpr int CT_BR = 32;                    // rows per stage (= K per stage)
+static_assert(64 + TC_LO * 2 * 32 <= 256, "TMEM columns: accumulators + Mh / Ml buffers");
+constexpr int CT_CW = 128;                   // columns per item (UMMA M)
+constexpr int CT_TILE = CT_BR * CT_CW * 4;   // 16 KB of M per stage
+constexpr int CT_XB = CT_BR * TC_N * 8;      // raw X rows per stage (<= 4 KB)
+constexpr int CT_BB = 2 * TC_N * CT_BR * 4;  // [Xh | Xl]^T tile per stage (4 KB)
+
+__host__ __device__ constexpr uint32_t ct_idesc_mn(int n) { return tc_idesc(n) | (1u << 15); }
+
+__device__ __forceinline__ uint64_t umma_desc_mn(uint32_t saddr, uint32_t lbo = 4096u,
+                                                  uint32_t sbo = 1024u) {  // MN-major SW128
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(lbo >> 4) << 16) |
+         ((uint64_t)(sbo >> 4) << 32) | ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
+}
+__device__ __forceinline__ void umma_tf32_mn32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(ct_idesc_mn(2 * TC_N)), "r"(accumulate)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_colprod_tc(const __grid_constant__ CUtensorMap map, long rows, long cols,
+                 const double* __restrict__ X, int K, long nitems, long nsplit, long split_rows,
+                 double* __restrict__ part, int dbg) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = su32(smem_raw);
+  uint8_t* sp = smem_raw + (((base + 1023u) & ~1023u) - base);
+  float* tiles = reinterpret_cast<float*>(sp);                                   // [ST][4 boxes]
+  uint8_t* bcat = sp + TC_STAGES * CT_TILE;                                       // [ST][4 KB]
+  double* xraw = reinterpret_cast<double*>(sp + TC_STAGES * (CT_TILE + CT_BB));  // [ST][<=4 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + TC_STAGES * (CT_TILE + CT_BB + CT_XB));
+  uint64_t* full = bars;
+  uint64_t* conv = bars + TC_STAGES;
+  uint64_t* empty = bars + 2 * TC_STAGES;
+  uint64_t* accf = bars + 3 * TC_STAGES;
+  uint64_t* acce = accf + 2;
+  uint64_t* loe = acce + 2;
+  uint32_t* tmem_base = reinterpret_cast<uint32_t*>(loe + TC_LO);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < TC_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&conv[i], 4);  // one converter group per stage
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&accf[i], 1);
+      mbar_init(&acce[i], 4);
+    }
+    for (int i = 0; i < TC_LO; ++i) mbar_init(&loe[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_base)),
+                 "n"(TC_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base;
+  const long i_beg = (long)blockIdx.x * nitems / gridDim.x;
+  const long i_end = (long)(blockIdx.x + 1) * nitems / gridDim.x;
+
+  if (warp == 0) {  // ===== TMA producer =====
+    if (lane == 0) {
+      int st = 0;
+      unsigned ph = 0;
+      for (long it = i_beg; it < i_end; ++it) {
+        const long chunk = it / nsplit, s = it - chunk * nsplit;
+        const long rb = s * split_rows, re = min(rows, rb + split_rows);
+        for (long r0 = rb; r0 < re; r0 += CT_BR) {
+          const bool xfull = r0 + CT_BR <= rows;
+          const unsigned xbytes = xfull ? (unsigned)(CT_BR * K * 8) : 0u;
+          mbar_wait(&empty[st], ph ^ 1u);
+          mbar_expect_tx(&full[st], (unsigned)CT_TILE + xbytes);
+          for (int b = 0; b < 4; ++b)
+            tma_load_2d(tiles + (size_t)st * (CT_TILE / 4) + b * (CT_BR * 32), &map, &full[st],
+                        (int)(chunk * CT_CW + 32 * b), (int)r0);
+          if (xfull)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+                "[%3];" ::"r"(su32(xraw + (size_t)st * (CT_XB / 8))),
+                "l"(X + r0 * K), "r"(xbytes), "r"(su32(&full[st]))
+                : "memory");
+          if (++st == TC_STAGES) st = 0, ph ^= 1u;
+        }
+      }
+    }
+  } else if (warp == 1) {  // ===== MMA issuer =====
+    if (lane == 0) {
+      int st = 0, lo_i = 0, acc = 0;
+      unsigned ph = 0;
+      unsigned aph[2] = {0u, 0u};
+      for (long it = i_beg; it < i_end; ++it) {
+        const long s = it % nsplit;
+        const long rb = s * split_rows, re = min(rows, rb + split_rows);
+        const int nst = (int)((re - rb + CT_BR - 1) / CT_BR);
+        for (int k0 = 0; k0 < nst; k0 += TC_SUB) {
+          mbar_wait(&acce[acc], aph[acc] ^ 1u);
+          aph[acc] ^= 1u;
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(acc * 2 * TC_N);
+          const int k1 = min(nst, k0 + TC_SUB);
+          for (int k = k0; k < k1; ++k) {
+            mbar_wait(&conv[st], ph);
+            tc_fence_after();
+            const uint32_t bt = su32(bcat) + st * CT_BB;
+            const uint32_t ah = tmem + TC_LO_COL + (uint32_t)(lo_i * 2 * CT_BR);  // Mh | Ml
+#pragma unroll
+            for (int kk = 0; kk < CT_BR / 8; ++kk) {
+              const uint64_t db = umma_desc(bt + kk * 32);
+              umma_tf32_ta<2 * TC_N>(d, ah + kk * 8, db, (k > k0 || kk) ? 1u : 0u);
+              if (!(dbg & 1)) umma_tf32_ta<TC_N>(d, ah + CT_BR + kk * 8, db, 1u);
+            }
+            umma_commit(&empty[st]);
+            umma_commit(&loe[lo_i]);
+            if (++lo_i == TC_LO) lo_i = 0;
+            if (++st == TC_STAGES) st = 0, ph ^= 1u;
+          }
+          umma_commit(&accf[acc]);
+          acc ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ===== converters + epilogue =====
+    const int ct = threadIdx.x - 128;
+    const bool epi = warp < 8;
+    const int q = warp & 3;            // TMEM lane quadrant = box of the stage
+    const int grp = (warp - 4) >> 2;   // converter group: stages alternate between the two groups
+    const int gt = threadIdx.x - 128 - 128 * grp;  // thread within the group (0..127)
+    unsigned gcnt = 0;
+    int st = 0, lo_i = 0, acc = 0;
+    unsigned ph = 0;
+    unsigned lo_ph[TC_LO] = {};
+    unsigned aph[2] = {0u, 0u};
+    double a64[TC_N];
+    long pend_chunk = -1, pend_s = -1;
+    int pend_acc = 0, pend_age = 0;
+    bool pend_last = false;
+    auto epilogue = [&]() {
+      const int a = pend_acc;
+      mbar_wait(&accf[a], aph[a]);
+      aph[a] ^= 1u;
+      tc_fence_after();
+      uint32_t v[2 * TC_N];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * 2 * TC_N);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+          "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+            "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+            "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+            "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[a]);
+#pragma unroll
+      for (int p = 0; p < TC_N; ++p)
+        a64[p] += (double)__uint_as_float(v[p]) + (double)__uint_as_float(v[TC_N + p]);
+      if (pend_last) {
+        const long col = pend_chunk * CT_CW + 32 * q + lane;
+        if (col < cols) {
+          double* dst = part + (pend_s * cols + col) * K;
+#pragma unroll
+          for (int p = 0; p < TC_N; ++p)
+            if (p < K) dst[p] = a64[p];
+        }
+#pragma unroll
+        for (int p = 0; p < TC_N; ++p) a64[p] = 0.0;
+      }
+    };
+#pragma unroll
+    for (int p = 0; p < TC_N; ++p) a64[p] = 0.0;
+    for (long it = i_beg; it < i_end; ++it) {
+      const long chunk = it / nsplit, s = it - chunk * nsplit;
+      const long rb = s * split_rows, re = min(rows, rb + split_rows);
+      const int nst = (int)((re - rb + CT_BR - 1) / CT_BR);
+      for (int k = 0; k < nst; ++k) {
+        const long r0 = rb + (long)k * CT_BR;
+        const bool mine = (gcnt++ & 1) == grp;
+        lo_ph[lo_i] ^= 1u;
+        if (mine) {
+          mbar_wait(&full[st], ph);
+          mbar_wait(&loe[lo_i], lo_ph[lo_i]);
+          tc_fence_after();
+          // Mh / Ml: this thread's column (lane of box q), the stage's 32 rows
+          const uint8_t* box = reinterpret_cast<const uint8_t*>(tiles + (size_t)st * (CT_TILE / 4)) +
+                               q * (CT_BR * 128);
+          uint32_t hi[32], lo[32];
+#pragma unroll
+          for (int r = 0; r < CT_BR; ++r) {
+            const float x = *reinterpret_cast<const float*>(
+                box + r * 128 + ((((lane >> 2) ^ (r & 7)) << 4) | ((lane & 3) << 2)));
+            float h_, l_;
+            split_tf32(x, h_, l_);
+            hi[r] = __float_as_uint(h_);
+            lo[r] = __float_as_uint(l_);
+          }
+          const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + TC_LO_COL +
+                                 (uint32_t)(lo_i * 2 * CT_BR);
+          tmem_st32(taddr, hi);
+          tmem_st32(taddr + CT_BR, lo);
+          // [Xh | Xl]^T: B operand rows p (hi) and 16 + p (lo), K = the stage's 32 rows
+          const double* xs = xraw + (size_t)st * (CT_XB / 8);
+          const bool xfull = r0 + CT_BR <= rows;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = gt + 128 * u;  // (r, p), p fastest
+            const int r = e >> 4, p = e & 15;
+            double xv = 0.0;
+            if (p < K) xv = xfull ? xs[r * K + p] : (r0 + r < rows ? __ldg(X + (r0 + r) * K + p) : 0.0);
+            const float xh = __uint_as_float(__float_as_uint((float)xv) & 0xFFFFE000u);
+            const float xl = (float)(xv - (double)xh);
+            uint8_t* bb = bcat + st * CT_BB;
+            *reinterpret_cast<float*>(bb + sw128_off(p, r, 2 * TC_N)) = xh;
+            *reinterpret_cast<float*>(bb + sw128_off(TC_N + p, r, 2 * TC_N)) = xl;
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          fence_async_smem();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[st]);
+        }
+        if (++lo_i == TC_LO) lo_i = 0;
+        if (++st == TC_STAGES) st = 0, ph ^= 1u;
+        if (pend_chunk >= 0 && ++pend_age > TC_EPI_LAG) {
+          if (epi) epilogue();
+          pend_chunk = -1;
+        }
+        if (k % TC_SUB == TC_SUB - 1 || k == nst - 1) {
+          if (pend_chunk >= 0) {
+            if (epi) epilogue();
+            pend_chunk = -1;
+          }
+          pend_chunk = chunk, pend_s = s, pend_acc = acc, pend_last = (k == nst - 1);
           pend_age = 0;
           acc ^= 1;
         }
@@ -518,6 +801,45 @@ int tc_rowprod_f32(const float* A, long rows, long cols, const double* B, int K,
   ++g_nmfb_launches, k_rowprod_tc<<<grid, TC_THREADS, smem, st>>>(map, rows, cols, B, K, nitems,
                                                                   nbands, work);
   *nparts = nch;
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+int tc_colprod_f32(const float* A, long rows, long cols, const double* X, int K, double* work,
+                   long work_len, long* nparts, cudaStream_t st) {
+  if (!tc_prod_enabled() || K < 1 || K > TC_N || (uintptr_t)A % 16 || (uintptr_t)X % 16 ||
+      cols % 4 || rows >= (1L << 31) || cols >= (1L << 31))
+    return NMFB_EUNSUPPORTED;
+  const long nch = (cols + CT_CW - 1) / CT_CW;
+  // about 8 items per CTA, splits of whole 128-row accumulator runs
+  long want = (8L * num_sms() + nch - 1) / nch;
+  if (want < 1) want = 1;
+  long sr = (rows + want - 1) / want;
+  sr = ((sr + 4 * CT_BR - 1) / (4 * CT_BR)) * (4 * CT_BR);
+  const long ns = (rows + sr - 1) / sr;
+  if (ns * cols * K > work_len) return NMFB_ENOMEM;
+  auto fn = encode_fn();
+  if (!fn) return NMFB_EUNSUPPORTED;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+  const cuuint32_t box[2] = {32, CT_BR};
+  const cuuint32_t es[2] = {1, 1};
+  if (fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)A, dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return NMFB_EUNSUPPORTED;
+  const long nitems = nch * ns;
+  const int grid = (int)min((long)num_sms(), nitems);
+  const size_t smem = 1024 + TC_STAGES * (CT_TILE + CT_BB + CT_XB) + 256;
+  nmfb_smem_attr(k_colprod_tc, smem);
+  static const int dbg = [] {
+    const char* e = getenv("NMFB_CT_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  ++g_nmfb_launches, k_colprod_tc<<<grid, TC_THREADS, smem, st>>>(map, rows, cols, X, K, nitems, ns,
+                                                                  sr, work, dbg);
+  *nparts = ns;
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

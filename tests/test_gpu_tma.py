@@ -74,7 +74,7 @@ def test_smem_attribute_across_problem_sizes():
 
 
 @pytest.mark.parametrize("n,m,k", [(4100, 2052, 10), (8192, 4096, 16), (5000, 3000, 5)])
-def test_tcgen05_rowprod_fp32(n, m, k):
+def test_tcgen05_products_fp32(n, m, k):
     """fp32 M (config c5 storage): the tcgen05 tf32 x 3 row product (csrc/tc_prod.cu) against
     fp64 torch -- relative error ~2e-6 (tf32 split ~2^-21 per term, fp32 tensor-core
     accumulation flushed to fp64 every 128 columns); bound 1e-5."""
@@ -86,9 +86,12 @@ def test_tcgen05_rowprod_fp32(n, m, k):
     M = torch.rand((n, m), generator=g, device=dev, dtype=torch.float32)
     P = solver.Problem(M, k)
     Yt = torch.rand((m, k), generator=g, device=dev, dtype=torch.float64)
+    X = torch.rand((n, k), generator=g, device=dev, dtype=torch.float64)
     assert P.lib.nmfb_tc_products(-1) == 1
-    r = P.buf(n, k)
+    r, c = P.buf(n, k), P.buf(m, k)
     P.rowprod(P.M, n, m, Yt, k, r, None, 1)
+    P.colprod(P.M, n, m, X, k, c, None, 1)  # k_colprod_tc (A = Mh / Ml from tensor memory)
     torch.cuda.synchronize()
-    rr = M.double() @ Yt
+    rr, cr = M.double() @ Yt, M.double().t() @ X
     assert ((r - rr).abs().max() / rr.abs().max()).item() < 1e-5
+    assert ((c - cr).abs().max() / cr.abs().max()).item() < 1e-5
