@@ -21,12 +21,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ipm", type=int, default=0, help="fixed IPM iterations per chunk (0: to tol/cap)")
     ap.add_argument("--barrier", default="balanced")
+    ap.add_argument("--cap", type=int, default=500, help="IPM iteration cap per chunk")
+    ap.add_argument("--hessian", default="inertia")
     ap.add_argument("--oracle-chunks", type=int, default=0)
     a = ap.parse_args()
     cfg = data.CONFIGS["c3"]
     M, X0, Y0, _, _ = data.make(cfg)
-    mk = (lambda: IpmParams(fixed_iters=a.ipm, barrier=a.barrier)) if a.ipm else \
-        (lambda: IpmParams(barrier=a.barrier))
+    mk = (lambda: IpmParams(fixed_iters=a.ipm, barrier=a.barrier, hessian=a.hessian)) if a.ipm else \
+        (lambda: IpmParams(barrier=a.barrier, max_iter=a.cap, hessian=a.hessian))
     # warm-up (module load, graph capture paths)
     StreamSession(M[:, :cfg.m_start], X0, Y0[:, :cfg.m_start], ipm_factory=mk)
     torch.cuda.synchronize()

@@ -71,3 +71,65 @@ def test_sharded_device_solver_matches_single():
         assert np.abs(r[2] - ref.Yt).max() <= 1e-7 * np.abs(ref.Yt).max()
         assert abs(r[6] - ref.final_objective) <= 1e-7 * ref.final_objective
     assert np.abs(X - ref.X).max() <= 1e-7 * np.abs(ref.X).max()
+
+
+def _nccl_worker(rank, world, port, M, X0, Y0, sweeps, iters, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        from paper_2101_08431_b200 import solver
+        from paper_2101_08431_b200.config import IpmParams, Stage1Config
+        from paper_2101_08431_b200.dist import Comm, row_range
+
+        comm = Comm.from_env()
+        a, b = row_range(M.shape[0], world, rank)
+        rep = solver.run_two_stage(M[a:b], X0[a:b], Y0, tol_rel=1e-10,
+                                   s1=Stage1Config(fixed_sweeps=sweeps),
+                                   ipm=IpmParams(fixed_iters=iters), comm=comm)
+        q.put((rank, rep.X, rep.Yt, rep.stage1.sweeps, rep.ipm.armijo_t, rep.ipm.flags,
+               rep.final_objective, rep.stage1.pX, rep.stage1.pY))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_two_gpus_c4_slice_matches_single():
+    """Row-sharded solve over NCCL on two GPUs (bench.py --gpus 2's path) on a c4-shaped
+    slice that takes the TMA products and the residual-free IPM: same sweeps, passive sets
+    and Armijo decisions as one GPU.  Skipped on single-GPU boxes."""
+    import torch
+    import torch.multiprocessing as mp
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs (NCCL cannot place two ranks on one device)")
+    from paper_2101_08431_b200 import data, solver
+    from paper_2101_08431_b200.config import IpmParams, Stage1Config
+
+    M, X0, Y0, _, _ = data.dense(8192, 4096, 10, 7)
+    sweeps, iters = 8, 6
+    ref = solver.run_two_stage(M, X0, Y0, tol_rel=1e-10, s1=Stage1Config(fixed_sweeps=sweeps),
+                               ipm=IpmParams(fixed_iters=iters))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, M, X0, Y0, sweeps, iters, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=900) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert np.array_equal(np.vstack([r[7] for r in res]), ref.stage1.pX)
+    for r in res:
+        assert r[3] == ref.stage1.sweeps
+        assert np.array_equal(r[8], ref.stage1.pY)
+        assert r[4] == ref.ipm.armijo_t and r[5] == ref.ipm.flags
+        assert abs(r[6] - ref.final_objective) <= 1e-9 * ref.final_objective
+    X = np.vstack([r[1] for r in res])
+    assert np.abs(X - ref.X).max() <= 1e-8 * np.abs(ref.X).max()
