@@ -81,6 +81,10 @@ int nmfb_surface_back_substitute(const double *x_rows, const double *y_cols, con
  * right-hand sides and Lawson-Hanson trips -- the reference's factor cache keyed by
  * the passive signature (_kernels_numba.py:296-298, 334-349) -- so the bits match. */
 long nmfb_nnls_ftab_len(long k);
+/* Build the subset factor table of ctc into ftab (for a later nmfb_nnls_batch_ws call with
+ * ftab_len negated = "table already built"), e.g. on a second stream concurrently with the
+ * product that computes ctb. */
+int nmfb_nnls_ftab_build(const double *ctc, long k, double *ftab, long ftab_len, void *stream);
 int nmfb_nnls_batch_ws(const double *ctc, const double *ctb, const double *btb,
                        const uint8_t *warm_passive, int warm_mode, const double *tol,
                        long max_changes, long nrhs, long k, double *x, uint8_t *passive,

@@ -71,6 +71,7 @@ SIGNATURES = {
     "nmfb_last_cuda_error": [],
     "nmfb_tma_products": [I],
     "nmfb_tc_products": [I],
+    "nmfb_nnls_ftab_build": [P, L, P, L, P],
     "nmfb_d_factor": [P, P, P, D, L, L, P, P, P, P, P],
     "nmfb_ffree_grad_rows": [P, P, P, L, L, P, P, P],
     "nmfb_ffree_fsq": [P, D, P, P, L, P, P, P],

@@ -647,9 +647,12 @@ static int nnls_batch_impl(const double* ctc, const double* ctb, const double* b
   cudaStream_t stream = (cudaStream_t)stream_;
   if (k < 1 || k > NMFB_MAX_K || nrhs < 0 || warm_mode < 0 || warm_mode > 2) return NMFB_EINVAL;
   if (nrhs == 0) return NMFB_OK;
-  // factor table of every passive subset (k <= FTAB_MAXK, caller workspace)
+  // factor table of every passive subset (k <= FTAB_MAXK, caller workspace); a negative
+  // ftab_len means the table was already built for this ctc (nmfb_nnls_ftab_build)
   const double* ft = nullptr;
-  if (ftab != nullptr && ftab_len_k(k) > 0 && ftab_len >= ftab_len_k(k)) {
+  if (ftab != nullptr && ftab_len < 0 && ftab_len_k(k) > 0 && -ftab_len >= ftab_len_k(k)) {
+    ft = ftab;
+  } else if (ftab != nullptr && ftab_len_k(k) > 0 && ftab_len >= ftab_len_k(k)) {
     const unsigned nsub = 1u << k;
 #define FTCASE(KK)                                                                            \
   case KK: {                                                                                  \
@@ -761,6 +764,31 @@ extern "C" int nmfb_surface_nnls_batch(const double* ctc, const double* ctb, con
   return nnls_batch_impl(ctc, ctb, btb, warm_passive, warm_mode, tol, max_changes, nrhs, k, x,
                          passive, changes, resid2, status, seed_scratch, flag_scratch, nullptr, 0,
                          stream);
+}
+
+// The subset factor table alone (for an NNLS batch launched later with -ftab_len): lets
+// the host build it on a second stream while the streaming product computes ctb.
+extern "C" int nmfb_nnls_ftab_build(const double* ctc, long k, double* ftab, long ftab_len,
+                                    void* stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (ftab == nullptr || ftab_len_k(k) <= 0 || ftab_len < ftab_len_k(k)) return NMFB_EINVAL;
+  const unsigned nsub = 1u << k;
+#define FTCASE(KK)                                                                            \
+  case KK: {                                                                                  \
+    constexpr int WW = KK <= 4 ? 4 : (KK <= 8 ? 8 : 16);                                      \
+    const unsigned per_blk = 4u * (32 / WW);                                                  \
+    ++g_nmfb_launches, k_factor_table<KK, WW><<<(nsub + per_blk - 1) / per_blk, 128, 0,       \
+                                                stream>>>(ctc, ftab, ftab + ((long)KK * KK << KK)); \
+    break;                                                                                    \
+  }
+  switch (k) {
+    FTCASE(1) FTCASE(2) FTCASE(3) FTCASE(4) FTCASE(5) FTCASE(6) FTCASE(7) FTCASE(8)
+    FTCASE(9) FTCASE(10) FTCASE(11) FTCASE(12)
+    default: return NMFB_EINVAL;
+  }
+#undef FTCASE
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
 }
 
 extern "C" int nmfb_nnls_batch_ws(const double* ctc, const double* ctb, const double* btb,

@@ -130,6 +130,7 @@ class Problem:
         nb = L.nmfb_ipm_reduce_blocks()
         self.rwork = torch.empty(max(148 * 2 * NTRIALS, 12 * nb, 3 * ((n + 127) // 128 + nb), 4096),
                                  **f64)
+        self.swork1 = torch.empty(max(4096, 3 * ((max(n, m) * k + 255) // 256 + 64)), **f64)
         self.row_n2 = torch.empty(n, **f64)
         self._col_n2 = torch.empty(m, **f64)
         self.col_n2 = self._col_n2[: self.m]
@@ -381,22 +382,71 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
     if nosync:
         slog = P.buf(nsweeps, 3)
         fword = torch.full((1,), -1, dtype=torch.int64, device=P.dev)  # all ones
+    # single rank: the subset factor tables (they depend only on the Gram) are built on a
+    # side stream while the streaming product computes ctb, and the fixed-sweep statistics
+    # run there behind the sweep (the kernels fit beside the persistent product kernels)
+    side = None
+    if nosync and P.ftab_len and os.environ.get("NMFB_S1_FORK", "1") != "0":
+        side = P.__dict__.get("_s1_side")
+        if side is None:
+            side = P._s1_side = torch.cuda.Stream(P.dev)
+            P._ftabY = torch.empty_like(P.ftab)
+        ftX, ftY = P.ftab, P._ftabY
+    ev_stats = None
+
+    def fork(C, rows_c, G, table):
+        """side stream: Gram G = C^T C, then its subset factor table (both only needed by
+        the NNLS batch, not by the streaming product running meanwhile)."""
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(P.dev))
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            # the multi-Gram kernel with its own workspace (P.gwork): the product running on
+            # the main stream meanwhile owns P.cwork
+            P.grams([(C, C, G)], rows_c, k)
+            P._call("nmfb_nnls_ftab_build", _p(G), k, _p(table), P.ftab_len, P.stream)
+        ev_t = torch.cuda.Event()
+        ev_t.record(side)
+        return ev_t
+
     for sweep in range(nsweeps):
         mode = 2 if (sweep > 0 or have_carry) else 0
+        cur = torch.cuda.current_stream(P.dev)
         # X-update: C = Y^T, d = rows of M (SPEC.md:191)
-        P.colprod(Yt, m, k, Yt, k, GY)
+        if side is not None:
+            ev_t = fork(Yt, m, GY, ftX)
+        else:
+            ev_t = None
+            P.colprod(Yt, m, k, Yt, k, GY)
         P.rowprod(P.M, n, m, Yt, k, ctbX, tolX, P.f32)
         if tol_fixed is not None:
             tolX.fill_(float(tol_fixed))
-        P._call("nmfb_nnls_batch_ws", _p(GY), _p(ctbX), _p(P.row_n2), _p(pX), mode,
-                _p(tolX), 3 * k, n, k, _p(Xn), _p(pXn), _p(chX), _p(r2X), _p(stX), None, None,
-                _p(P.ftab), P.ftab_len, s)
+        if ev_t is not None:
+            cur.wait_event(ev_t)
+            if ev_stats is not None:  # the previous sweep's statistics read X / stX
+                cur.wait_event(ev_stats)
+            P._call("nmfb_nnls_batch_ws", _p(GY), _p(ctbX), _p(P.row_n2), _p(pX), mode,
+                    _p(tolX), 3 * k, n, k, _p(Xn), _p(pXn), _p(chX), _p(r2X), _p(stX), None,
+                    None, _p(ftX), -P.ftab_len, s)
+        else:
+            P._call("nmfb_nnls_batch_ws", _p(GY), _p(ctbX), _p(P.row_n2), _p(pX), mode,
+                    _p(tolX), 3 * k, n, k, _p(Xn), _p(pXn), _p(chX), _p(r2X), _p(stX), None,
+                    None, _p(P.ftab), P.ftab_len, s)
         # Y-update: C = X, d = columns of M (SPEC.md:200); row contractions all-reduced
-        P.colprod(Xn, n, k, Xn, k, GX, reduce=True)
+        if side is not None:
+            ev_t = fork(Xn, n, GX, ftY)
+        else:
+            ev_t = None
+            P.colprod(Xn, n, k, Xn, k, GX, reduce=True)
         P.colprod(P.M, n, m, Xn, k, ctbY, tolY, P.f32, reduce=True)
         if tol_fixed is not None:
             tolY.fill_(float(tol_fixed))
-        if P.comm.active:
+        if ev_t is not None:
+            cur.wait_event(ev_t)
+            P._call("nmfb_nnls_batch_ws", _p(GX), _p(ctbY), _p(P.col_n2), _p(pY), mode,
+                    _p(tolY), 3 * k, m, k, _p(Yn), _p(pYn), _p(chY), _p(r2Y), _p(stY), None,
+                    None, _p(ftY), -P.ftab_len, s)
+        elif P.comm.active:
             # columns split over the ranks, then all-gathered (dist.py)
             c0, c1 = row_range(m, P.comm.world, P.comm.rank)
             if c1 > c0:
@@ -412,10 +462,19 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
                     _p(P.ftab), P.ftab_len, s)
         ny = P.ny_local
         if nosync:
-            P._call("nmfb_stage1_stats", _p(X), _p(Xn), n * k, _p(Yt), _p(Yn), m * k * ny,
-                    _p(r2Y), m * ny, _p(slog[sweep]), _p(P.rwork), P.rwork.numel(), s)
-            P._call("nmfb_first_failure_i8", _p(stX), n, 2 * sweep, _p(fword), s)
-            P._call("nmfb_first_failure_i8", _p(stY), m, 2 * sweep + 1, _p(fword), s)
+            if side is not None:  # behind the sweep, on the side stream
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                side.wait_event(ev)
+            with torch.cuda.stream(side if side is not None else cur):
+                ss = P.stream
+                P._call("nmfb_stage1_stats", _p(X), _p(Xn), n * k, _p(Yt), _p(Yn), m * k * ny,
+                        _p(r2Y), m * ny, _p(slog[sweep]), _p(P.swork1), P.swork1.numel(), ss)
+                P._call("nmfb_first_failure_i8", _p(stX), n, 2 * sweep, _p(fword), ss)
+                P._call("nmfb_first_failure_i8", _p(stY), m, 2 * sweep + 1, _p(fword), ss)
+            if side is not None:
+                ev_stats = torch.cuda.Event()
+                ev_stats.record(side)
             X, Xn = Xn, X
             Yt, Yn = Yn, Yt
             pX, pXn = pXn, pX
@@ -447,6 +506,8 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
         if cfg.fixed_sweeps <= 0 and step <= cfg.eps_stol * (1.0 + nrm):
             res.converged = True
             break
+    if ev_stats is not None:
+        torch.cuda.current_stream(P.dev).wait_event(ev_stats)
     if nosync and nsweeps > 0:
         fw = int(fword.item()) & ((1 << 64) - 1)
         if fw != (1 << 64) - 1:
@@ -578,6 +639,12 @@ class IpmEngine:
                  P.lib.nmfb_atb_work_len(m, self.kk, self.kk),
                  0 if self.ffree else P.lib.nmfb_atb_work_len(n, m, k ** 3), 1)
         self.awork = b(aw)
+        # the Y-side factor (D_j, the G capacitance Gram) runs on a second stream, concurrent
+        # with the X-side row factors / Z Gram (independent until the low-rank factorization);
+        # both branches are latency-bound kernels on a few SMs each
+        self.fork = (not self.comm.active) and os.environ.get("NMFB_IPM_FORK", "1") != "0"
+        self.awork2 = b(aw) if self.fork else None
+        self.side = torch.cuda.Stream(P.dev) if self.fork else None
         if self.use_graphs:
             # the capacitance Grams' first cuBLAS calls (library init, kernel load) run
             # eagerly here, not inside the first graph capture (~0.4 s there at c4);
@@ -864,6 +931,20 @@ class IpmEngine:
             P.colprod(Yt, m, k, Yt, k, self.GY)
             P.colprod(X, n, k, X, k, self.XtX, reduce=True)
         dense = full or self.dense_gn or force_dense
+        fork = self.fork and not dense
+        if fork:  # Y-side factor on the side stream (joined before nmfb_lowrank_factor)
+            cur = torch.cuda.current_stream(P.dev)
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            self.side.wait_event(ev)
+            with torch.cuda.stream(self.side):
+                ss = P.stream
+                P._call("nmfb_d_factor", _p(self.XtX), _p(Yt), _p(self.S), rho, m, k,
+                        _p(self.LD), _p(self.Dinvpk), _p(self.YYpk), _p(P.iscal[4:]), ss)
+                P._call("nmfb_atb", _p(self.YYpk), m, self.kk, _p(self.Dinvpk), self.kk,
+                        _p(self.Gpk), _p(self.awork2), self.awork2.numel(), ss)
+            ev_y = torch.cuda.Event()
+            ev_y.record(self.side)
         P._call("nmfb_r1_factor", _p(self.GY), _p(X), _p(self.R), _p(self.gX), mux, rho, n,
                 k, _p(self.L), _p(self.h), _p(self.g), _p(self.Apk), _p(self.XXpk),
                 _p(P.iscal[2:]), s)
@@ -900,10 +981,13 @@ class IpmEngine:
             dY.copy_(self.rhs.view(m, k))
             P._call("nmfb_dense_solve", _p(self.A), N, _p(dY), s)
         else:
-            P._call("nmfb_d_factor", _p(self.XtX), _p(Yt), _p(self.S), rho, m, k,
-                    _p(self.LD), _p(self.Dinvpk), _p(self.YYpk), _p(P.iscal[4:]), s)
-            P._call("nmfb_atb", _p(self.YYpk), m, self.kk, _p(self.Dinvpk), self.kk, _p(self.Gpk),
-                    _p(self.awork), self.awork.numel(), s)
+            if fork:
+                cur.wait_event(ev_y)
+            else:
+                P._call("nmfb_d_factor", _p(self.XtX), _p(Yt), _p(self.S), rho, m, k,
+                        _p(self.LD), _p(self.Dinvpk), _p(self.YYpk), _p(P.iscal[4:]), s)
+                P._call("nmfb_atb", _p(self.YYpk), m, self.kk, _p(self.Dinvpk), self.kk,
+                        _p(self.Gpk), _p(self.awork), self.awork.numel(), s)
             P._call("nmfb_lowrank_factor", _p(self.Z), _p(self.Gpk), k, _p(self.LG), _p(self.LH),
                     _p(self.lrwork), _p(P.iscal[3:]), s)
             self.lowrank_solve(self.rhs, dY, Yt)
