@@ -949,10 +949,22 @@ class IpmEngine:
                 k, _p(self.L), _p(self.h), _p(self.g), _p(self.Apk), _p(self.XXpk),
                 _p(P.iscal[2:]), s)
         self.comm.min_(P.iscal[2:3])
+        ev_rhs = None
+        if fork:  # H = X^T g and the Schur right-hand side on the side stream as well
+            ev_r1 = torch.cuda.Event()
+            ev_r1.record(cur)
+            self.side.wait_event(ev_r1)
+            with torch.cuda.stream(self.side):
+                P.grams([(X, self.g, self.H)], n, k)
+                P._call("nmfb_schur_rhs", _p(Yt), _p(self.gY), _p(self.H), None, muy, m, k,
+                        _p(self.rhs), P.stream)
+            ev_rhs = torch.cuda.Event()
+            ev_rhs.record(self.side)
         P._call("nmfb_atb", _p(self.Apk), n, self.kk, _p(self.XXpk), self.kk, _p(self.Z),
                 _p(self.awork), self.awork.numel(), s)
         self.comm.sum_(self.Z)
-        P.colprod(X, n, k, self.g, k, self.H, reduce=True)
+        if not fork:
+            P.colprod(X, n, k, self.g, k, self.H, reduce=True)
         W = FtG = None
         if full:
             self._ensure_full_buffers()
@@ -962,8 +974,9 @@ class IpmEngine:
             self.comm.sum_(self.W)
             P.colprod(F, n, m, self.g, k, self.FtG, reduce=True)
             W, FtG = self.W, self.FtG
-        P._call("nmfb_schur_rhs", _p(Yt), _p(self.gY), _p(self.H), _p(FtG), muy, m, k,
-                _p(self.rhs), s)
+        if not fork:
+            P._call("nmfb_schur_rhs", _p(Yt), _p(self.gY), _p(self.H), _p(FtG), muy, m, k,
+                    _p(self.rhs), s)
         dY = self.dYbuf
         if dense:
             self._ensure_dense()
@@ -990,6 +1003,8 @@ class IpmEngine:
                         _p(self.Gpk), _p(self.awork), self.awork.numel(), s)
             P._call("nmfb_lowrank_factor", _p(self.Z), _p(self.Gpk), k, _p(self.LG), _p(self.LH),
                     _p(self.lrwork), _p(P.iscal[3:]), s)
+            if ev_rhs is not None:
+                cur.wait_event(ev_rhs)
             self.lowrank_solve(self.rhs, dY, Yt)
         self.last_dense = dense
         P.colprod(Yt, m, k, dY, k, self.Gdy)
