@@ -155,26 +155,57 @@ __device__ __forceinline__ void bwd_row(const double (&L)[K][K], const double (&
 
 // R1_i = YY^T + rho I + diag(r_i / x_i) = L_i L_i^T; h_i = L_i^{-1}(mux/x_i - graX_i);
 // g_i = L_i^{-T} h_i; Apk_i = packed R1_i^{-1}; XXpk_i = packed x_i x_i^T.
+// Thread per row (arithmetic unchanged); the five per-row outputs (K^2 + 2K + K(K+1)
+// doubles) leave through a per-warp shared-memory stage so every global store of the warp
+// is contiguous (thread-per-row stores directly would touch 32 lines per instruction).
+constexpr int R1_THREADS = 64;
 template <int K>
-__global__ void __launch_bounds__(128) k_r1_factor(const double* __restrict__ GY,
-                                                   const double* __restrict__ X,
-                                                   const double* __restrict__ R,
-                                                   const double* __restrict__ gX, double mux,
-                                                   double rho, long n, double* __restrict__ Lout,
-                                                   double* __restrict__ h, double* __restrict__ g,
-                                                   double* __restrict__ Apk,
-                                                   double* __restrict__ XXpk,
-                                                   int* __restrict__ bad,
-    const double* __restrict__ mu_dev) {
+struct R1W {  // stage row pitch: K^2 (L) and K(K+1) (Apk | XXpk) doubles, + 1 against conflicts
+  static constexpr int v = K * (K + 1) + 1;
+};
+
+template <int K>
+__device__ __forceinline__ void r1_flush(double* __restrict__ stage, int lane, long row0, long n,
+                                         int width, double* __restrict__ out) {
+  __syncwarp();
+  const long nrow = min(32L, n - row0);
+  double* dst = out + row0 * width;
+  for (int e = lane; e < nrow * width; e += 32) {
+    const int r = e / width, c = e - (e / width) * width;
+    dst[e] = stage[r * (R1W<K>::v) + c];
+  }
+  __syncwarp();
+}
+
+template <int K>
+__global__ void __launch_bounds__(R1_THREADS) k_r1_factor(const double* __restrict__ GY,
+                                                          const double* __restrict__ X,
+                                                          const double* __restrict__ R,
+                                                          const double* __restrict__ gX,
+                                                          double mux, double rho, long n,
+                                                          double* __restrict__ Lout,
+                                                          double* __restrict__ h,
+                                                          double* __restrict__ g,
+                                                          double* __restrict__ Apk,
+                                                          double* __restrict__ XXpk,
+                                                          int* __restrict__ bad,
+                                                          const double* __restrict__ mu_dev) {
   if (mu_dev != nullptr) mux = mu_dev[1];  // graph replays: barrier value from device memory
+  extern __shared__ double r1s[];          // [warps][32][K^2 + 1] output stage
   __shared__ double gy[K * K];
   for (int e = threadIdx.x; e < K * K; e += blockDim.x) gy[e] = GY[e];
   __syncthreads();
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* stage = r1s + (size_t)wid * 32 * (R1W<K>::v);
+  double* srow = stage + lane * (R1W<K>::v);
+  const long row0 = (long)blockIdx.x * blockDim.x + 32 * wid;
+  if (row0 >= n) return;  // warp-uniform
+  const long i = row0 + lane;
+  const bool live = i < n;
+  const long ii = live ? i : row0;  // tail lanes recompute row0 (never stored)
   double x[K], L[K][K], b[K], hv[K], gv[K];
 #pragma unroll
-  for (int p = 0; p < K; ++p) x[p] = X[i * K + p];
+  for (int p = 0; p < K; ++p) x[p] = X[ii * K + p];
 #pragma unroll
   for (int a = 0; a < K; ++a)
 #pragma unroll
@@ -182,22 +213,32 @@ __global__ void __launch_bounds__(128) k_r1_factor(const double* __restrict__ GY
 #pragma unroll
   for (int p = 0; p < K; ++p) {
     const double ix = 1.0 / x[p];
-    L[p][p] += rho + R[i * K + p] * ix;
-    b[p] = mux * ix - gX[i * K + p];
+    L[p][p] += rho + R[ii * K + p] * ix;
+    b[p] = mux * ix - gX[ii * K + p];
   }
   double rd[K];
-  if (!chol_row<K>(L, rd)) {
-    atomicMin(bad, (int)i);
-    return;
-  }
+  const bool ok = chol_row<K>(L, rd);
+  if (live && !ok) atomicMin(bad, (int)i);
+  if (__all_sync(0xffffffffu, !ok)) return;
   fwd_row<K>(L, rd, b, hv);
   bwd_row<K>(L, rd, hv, gv);
+  // L (full K x K, zero upper)
 #pragma unroll
-  for (int a = 0; a < K; ++a) {
-    h[i * K + a] = hv[a];
-    g[i * K + a] = gv[a];
+  for (int a = 0; a < K; ++a)
 #pragma unroll
-    for (int c = 0; c < K; ++c) Lout[(i * K + a) * K + c] = (c <= a) ? L[a][c] : 0.0;
+    for (int c = 0; c < K; ++c) srow[a * K + c] = (c <= a) ? L[a][c] : 0.0;
+  r1_flush<K>(stage, lane, row0, n, K * K, Lout);
+#pragma unroll
+  for (int a = 0; a < K; ++a) srow[a] = hv[a], srow[K + a] = gv[a];
+  __syncwarp();
+  {  // h and g (two K-wide arrays)
+    const long nrow = min(32L, n - row0);
+    for (int e = lane; e < nrow * K; e += 32) {
+      const int r = e / K, c = e - (e / K) * K;
+      h[row0 * K + e] = stage[r * (R1W<K>::v) + c];
+      g[row0 * K + e] = stage[r * (R1W<K>::v) + K + c];
+    }
+    __syncwarp();
   }
   // Linv = L^{-1} (lower), then R1^{-1} = Linv^T Linv
   double Li[K][K];
@@ -226,9 +267,18 @@ __global__ void __launch_bounds__(128) k_r1_factor(const double* __restrict__ GY
       for (int p = 0; p < K; ++p)
         if (p >= c) s = fma(Li[p][a], Li[p][c], s);
       const int e = a * K - a * (a - 1) / 2 + (c - a);
-      Apk[i * KKc + e] = s;
-      XXpk[i * KKc + e] = x[a] * x[c];
+      srow[e] = s;
+      srow[KKc + e] = x[a] * x[c];
     }
+  __syncwarp();
+  {  // Apk and XXpk (two K(K+1)/2-wide arrays)
+    const long nrow = min(32L, n - row0);
+    for (int e = lane; e < nrow * KKc; e += 32) {
+      const int r = e / KKc, c = e - (e / KKc) * KKc;
+      Apk[row0 * KKc + e] = stage[r * (R1W<K>::v) + c];
+      XXpk[row0 * KKc + e] = stage[r * (R1W<K>::v) + KKc + c];
+    }
+  }
 }
 
 // h = L^{-1} b1, g = L^{-T} h for a given right-hand side (predictor reuse)
@@ -1173,11 +1223,14 @@ extern "C" int nmfb_r1_factor(const double* GY, const double* X, const double* R
   cudaStream_t st = (cudaStream_t)stream;
   if (n <= 0) return NMFB_EINVAL;
   cudaMemsetAsync(bad, 0x7F, sizeof(int), st);  // 0x7F7F7F7F: no failing row
-  const int blocks = (int)((n + 127) / 128);
+  const int blocks = (int)((n + R1_THREADS - 1) / R1_THREADS);
 #define CASE(KK)                                                                               \
-  case KK:                                                                                     \
-    ++g_nmfb_launches, k_r1_factor<KK><<<blocks, 128, 0, st>>>(GY, X, R, gX, mux, rho, n, L, h, g, Apk, XXpk, bad, g_mu_dev); \
-    break;
+  case KK: {                                                                                   \
+    const size_t sm = (size_t)(R1_THREADS / 32) * 32 * R1W<KK>::v * sizeof(double);         \
+    nmfb_smem_attr(k_r1_factor<KK>, sm);                                                       \
+    ++g_nmfb_launches, k_r1_factor<KK><<<blocks, R1_THREADS, sm, st>>>(GY, X, R, gX, mux, rho, n, L, h, g, Apk, XXpk, bad, g_mu_dev); \
+    break;                                                                                     \
+  }
   NMFB_K_SWITCH(k, CASE)
 #undef CASE
   NMFB_CHECK_LAUNCH();
