@@ -8,7 +8,7 @@ import torch  # noqa: E402
 from paper_2101_08431_b200 import _lib  # noqa: E402
 
 lib = _lib.load()
-for N in (64, 100, 128, 256, 300, 800, 2000):
+for N in (100, 160, 256, 300, 352, 800, 2000):
     rng = np.random.default_rng(N)
     B = rng.standard_normal((N, N))
     A = B @ B.T / N + np.eye(N)
