@@ -6,7 +6,11 @@ column-append session (BASELINE config c3).  The reference has no append API
   * append(M_new): new Y columns = NNLS(C = X, d = new columns of M) with warm
     mode 1 (the reference's "streaming chain", _kernels_numba.py:312-315),
     carries extended with their passive sets, then the two-stage solve warm
-    from (X, Y) and the carries (stage-1 mode 2 from its first sweep).
+    from (X, Y) and the carries (stage-1 mode 2 from its first sweep);
+  * one KKT scale for the whole session (frozen semantics 12): eps_abs = tol_rel *
+    max(1, E_primal(X0, Y0)) of the FIRST chunk's seeded start, kept for every chunk
+    (a warm start's own E_primal is below 1, which would turn the relative tolerance
+    into an absolute 1e-10).
 """
 from __future__ import annotations
 
@@ -25,7 +29,10 @@ class OracleStream:
         self.ipm_factory = ipm_factory or D.IpmParams
         self.chunks = []
         t0 = time.perf_counter()
-        rep = D.run_two_stage(self.M, X0, Y0, tol_rel, self.s1, self.ipm_factory())
+        self.e_scale = max(1.0, D.kkt_error_primal_only(
+            np.asarray(X0, dtype=np.float64), np.ascontiguousarray(np.asarray(Y0).T), self.M))
+        rep = D.run_two_stage(self.M, X0, Y0, tol_rel, self.s1, self.ipm_factory(),
+                              e_scale=self.e_scale)
         self._keep(rep, time.perf_counter() - t0)
 
     def _keep(self, rep, secs):
@@ -48,6 +55,6 @@ class OracleStream:
         Yt = np.vstack([self.Yt, y])
         pY = np.vstack([self.pY, p])
         rep = D.run_two_stage(self.M, self.X, Yt.T, self.tol_rel, self.s1, self.ipm_factory(),
-                              pX=self.pX, pY=pY)
+                              pX=self.pX, pY=pY, e_scale=self.e_scale)
         self._keep(rep, time.perf_counter() - t0)
         return rep

@@ -45,8 +45,13 @@ class StreamSession:
         t0 = time.perf_counter()
         cap = max(int(m_max or 0), 2 * M0.shape[1])
         self.P = solver.Problem(M0, self.k, m_capacity=cap)
+        # one KKT scale for the session (frozen semantics 12, oracle/stream.py): the first
+        # chunk's seeded start; a warm start's own E_primal < 1 would make tol_rel absolute
+        Xd = self.P.to_dev(X0)
+        Ytd = self.P.to_dev(Y0.T if not isinstance(Y0, torch.Tensor) else Y0.t())
+        self.e_scale = max(1.0, solver.kkt_error_primal_only_dev(self.P, Xd, Ytd)[0])
         rep = solver.run_two_stage(None, X0, Y0, tol_rel, self.cfg, self.ipm_factory(),
-                                   problem=self.P)
+                                   problem=self.P, e_scale=self.e_scale)
         torch.cuda.synchronize()
         self._keep(rep, time.perf_counter() - t0)
 
@@ -98,7 +103,7 @@ class StreamSession:
         Yt = torch.cat([self.Yt, y])
         pY = torch.cat([self.pY, p]) if self.pY is not None else None
         rep = solver.run_two_stage(None, X, Yt.t(), self.tol_rel, self.cfg, self.ipm_factory(),
-                                   pX=self.pX, pY=pY, problem=P)
+                                   pX=self.pX, pY=pY, problem=P, e_scale=self.e_scale)
         torch.cuda.synchronize()
         self._keep(rep, time.perf_counter() - t0)
         return rep
