@@ -238,25 +238,31 @@ __device__ __forceinline__ void nnls_seg_solve(WNnls<K, W>& s, double d, double 
 // to the reference's loop over passive positions), so a warp stays converged
 // inside a Lawson-Hanson trip.
 //   STAGED = true : T is the global table; the current subset's factor is staged
-//                   into this thread's shared-memory slot (packed, stride TAB_T) by
+//                   into this thread's shared-memory slot (packed, stride TabT<K>) by
 //                   cp.async once per trip (csrc/surface.cu k_nnls_tab)
 //   STAGED = false: T is a (small) table in shared memory, read in place
 //                   (csrc/stage1_persist.cu)
 // --------------------------------------------------------------------------
-constexpr int TAB_T = 64;  // threads per block of k_nnls_tab
+// threads per block of k_nnls_tab (= the stride of the per-thread factor slots): 64, or 32
+// above k = 12 so the K(K+1)/2-entry slots stay within the 48 KB of static shared memory
+template <int K>
+struct TabT {
+  static constexpr int v = K > 12 ? 32 : 64;
+};
 
 template <int K, bool STAGED>
 struct TNnls {
   static constexpr int KT = K * (K + 1) / 2;
   const double* C;     // ctc (K x K, shared memory: broadcast reads)
-  double* sL;          // STAGED: this thread's slot, packed entry e at sL[e * TAB_T]
+  static constexpr int TS = TabT<K>::v;
+  double* sL;          // STAGED: this thread's slot, packed entry e at sL[e * TS]
   const double* Lt;    // !STAGED: the current subset's K x K factor (shared memory)
   double d[K];
 
   __device__ __forceinline__ static bool bit(unsigned pm, int i) { return (pm >> i) & 1u; }
   __device__ __forceinline__ static constexpr int tri(int i, int j) { return i * (i + 1) / 2 + j; }
   __device__ __forceinline__ double l(int i, int j) const {
-    return STAGED ? sL[tri(i, j) * TAB_T] : Lt[i * K + j];
+    return STAGED ? sL[tri(i, j) * TS] : Lt[i * K + j];
   }
 
   __device__ __forceinline__ void stage(const double* __restrict__ T, unsigned pm) {
@@ -272,7 +278,7 @@ struct TNnls {
 #pragma unroll
       for (int j = 0; j <= i; ++j)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
-                         base + (unsigned)(tri(i, j) * TAB_T * sizeof(double))),
+                         base + (unsigned)(tri(i, j) * TS * sizeof(double))),
                      "l"(Lg + i * K + j)
                      : "memory");
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");

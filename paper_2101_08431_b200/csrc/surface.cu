@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(128) k_factor_table(const double* __restrict__
 // Lawson-Hanson trip and issues ~K^2 instructions per trip for 32 right-hand
 // sides (the warp-per-rhs kernel issues that per rhs).
 template <int K>
-__global__ void __launch_bounds__(TAB_T) k_nnls_tab(const double* __restrict__ ctc_g,
+__global__ void __launch_bounds__(TabT<K>::v) k_nnls_tab(const double* __restrict__ ctc_g,
                                                   const double* __restrict__ ctb,
                                                   const double* __restrict__ btb,
                                                   const uint8_t* __restrict__ seeds, int seed_mode,
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(TAB_T) k_nnls_tab(const double* __restrict__ c
                                                   int8_t* __restrict__ st_out,
                                                   const double* __restrict__ T) {
   __shared__ double ctc[K * K];
-  __shared__ double sLall[TNnls<K, true>::KT * TAB_T];
+  __shared__ double sLall[TNnls<K, true>::KT * TabT<K>::v];
   for (int i = threadIdx.x; i < K * K; i += blockDim.x) ctc[i] = ctc_g[i];
   __syncthreads();
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -632,7 +632,7 @@ int kbucket(long k) { return k <= 4 ? 4 : (k <= 8 ? 8 : 16); }
     default: CALL(16); break;    \
   }
 
-constexpr int FTAB_MAXK = 12;  // 4096 subsets x 144 doubles = 4.7 MB
+constexpr int FTAB_MAXK = 16;  // k = 12: 4096 subsets x 145 doubles = 4.8 MB; k = 16: 135 MB
 
 static long ftab_len_k(long k) { return (k < 1 || k > FTAB_MAXK) ? 0 : (k * k + 1) << k; }
 
@@ -664,7 +664,7 @@ static int nnls_batch_impl(const double* ctc, const double* ctb, const double* b
   }
     switch (k) {
       FTCASE(1) FTCASE(2) FTCASE(3) FTCASE(4) FTCASE(5) FTCASE(6) FTCASE(7) FTCASE(8)
-      FTCASE(9) FTCASE(10) FTCASE(11) FTCASE(12)
+      FTCASE(9) FTCASE(10) FTCASE(11) FTCASE(12) FTCASE(13) FTCASE(14) FTCASE(15) FTCASE(16)
       default: break;
     }
 #undef FTCASE
@@ -694,7 +694,7 @@ static int nnls_batch_impl(const double* ctc, const double* ctb, const double* b
   }
 #define TCASE(KT, SEEDS, MODE)                                                                  \
   case KT:                                                                                      \
-    ++g_nmfb_launches, k_nnls_tab<KT><<<(unsigned)((nrhs + TAB_T - 1) / TAB_T), TAB_T, 0, stream>>>( \
+    ++g_nmfb_launches, k_nnls_tab<KT><<<(unsigned)((nrhs + TabT<KT>::v - 1) / TabT<KT>::v), TabT<KT>::v, 0, stream>>>( \
         ctc, ctb, btb, SEEDS, MODE, tol, max_changes, nrhs, x, passive, changes, resid2, status, \
         ft);                                                                                    \
     break;
@@ -704,6 +704,7 @@ static int nnls_batch_impl(const double* ctc, const double* ctb, const double* b
       TCASE(1, SEEDS, MODE) TCASE(2, SEEDS, MODE) TCASE(3, SEEDS, MODE) TCASE(4, SEEDS, MODE) \
       TCASE(5, SEEDS, MODE) TCASE(6, SEEDS, MODE) TCASE(7, SEEDS, MODE) TCASE(8, SEEDS, MODE) \
       TCASE(9, SEEDS, MODE) TCASE(10, SEEDS, MODE) TCASE(11, SEEDS, MODE) TCASE(12, SEEDS, MODE) \
+      TCASE(13, SEEDS, MODE) TCASE(14, SEEDS, MODE) TCASE(15, SEEDS, MODE) TCASE(16, SEEDS, MODE) \
       default: return NMFB_EINVAL;                                                          \
     }                                                                                       \
   } else if (thread_kernel) {                                                               \
@@ -783,7 +784,7 @@ extern "C" int nmfb_nnls_ftab_build(const double* ctc, long k, double* ftab, lon
   }
   switch (k) {
     FTCASE(1) FTCASE(2) FTCASE(3) FTCASE(4) FTCASE(5) FTCASE(6) FTCASE(7) FTCASE(8)
-    FTCASE(9) FTCASE(10) FTCASE(11) FTCASE(12)
+    FTCASE(9) FTCASE(10) FTCASE(11) FTCASE(12) FTCASE(13) FTCASE(14) FTCASE(15) FTCASE(16)
     default: return NMFB_EINVAL;
   }
 #undef FTCASE

@@ -147,7 +147,7 @@ def nnls_batch(ctc, ctb, btb, warm_passive, warm_mode, tol, max_changes, *, tabl
     """_kernels_numba.py:277-477 -> (x, passive, changes, resid2, status).
 
     status per rhs: 0 solved, 1 change cap exceeded, 2 rank-deficient passive set.
-    table (keyword-only extension): for k <= 12 factor every passive subset once per
+    table (keyword-only extension): for k <= 16 factor every passive subset once per
     call (nmfb_nnls_batch_ws, the reference's factor cache); False runs the
     per-rhs factorizing kernels of nmfb_surface_nnls_batch.  Same bits either way.
     """

@@ -81,14 +81,14 @@ def _nmf_like(rng, nrhs, k, drift):
     return ctc, ctb, np.einsum("ij,ij->i", D, D), 1e-12 * np.maximum(1, np.abs(ctb).max(1))
 
 
-@pytest.mark.parametrize("k,nrhs", [(3, 5000), (4, 5000), (10, 5000), (12, 4000), (16, 5000),
-                                     (4, 20000), (10, 12000)])
+@pytest.mark.parametrize("k,nrhs", [(3, 5000), (4, 5000), (10, 5000), (12, 4000), (13, 3000),
+                                     (16, 5000), (4, 20000), (10, 12000), (16, 20000)])
 @pytest.mark.parametrize("mode", (0, 1, 2))
 @pytest.mark.parametrize("table", (True, False))
 def test_nnls_large_vs_oracle(K, k, nrhs, mode, table):
     """Bit-identical to the reference on every device formulation: the subset
-    factor table + register thread kernel (k <= 12), warp per rhs (small batches)
-    and thread per rhs (batches > 8192 or k > 12)."""
+    factor table + register thread kernel (k <= 16; 2^16 subsets = 135 MB at k = 16),
+    warp per rhs (small batches) and thread per rhs (no table, batches > 8192)."""
     rng = np.random.default_rng(1000 + 10 * k + mode)
     ctc, ctb, btb, tol = _nmf_like(rng, nrhs, k, 0.05)
     seed = ok.nnls_batch(ctc, ctb * 1.01, btb, np.zeros((nrhs, k), bool), 0, tol, 3 * k)[1]
@@ -98,7 +98,7 @@ def test_nnls_large_vs_oracle(K, k, nrhs, mode, table):
         assert np.array_equal(a, b), (name, k, mode)
 
 
-@pytest.mark.parametrize("k", (2, 5, 10))
+@pytest.mark.parametrize("k", (2, 5, 10, 16))
 def test_nnls_table_cold_and_rank_deficient(K, k):
     """Table path on cold starts with many Lawson-Hanson trips, the change cap
     (status 1) and a rank-deficient Gram (status 2: failing subsets in the table)."""
