@@ -35,8 +35,10 @@ def row_range(n: int, world: int, rank: int) -> tuple[int, int]:
 
 
 class Comm:
-    def __init__(self, group=None, world: int = 1, rank: int = 0):
-        self.group, self.world, self.rank = group, world, rank
+    def __init__(self, group=None, world: int = 1, rank: int = 0, force: bool = False):
+        # force: treat a one-rank group as sharded, so that every collective of the sharded
+        # path is issued (a one-GPU box exercising the NCCL path: tests/test_gpu_dist.py)
+        self.group, self.world, self.rank, self.force = group, world, rank, bool(force)
 
     @classmethod
     def single(cls):
@@ -47,19 +49,22 @@ class Comm:
         import torch.distributed as dist
 
         if dist.is_available() and dist.is_initialized():
-            return cls(None, dist.get_world_size(), dist.get_rank())
+            import os
+
+            return cls(None, dist.get_world_size(), dist.get_rank(),
+                       force=os.environ.get("NMFB_FORCE_COMM", "0") == "1")
         return cls.single()
 
     @property
     def active(self):
-        return self.world > 1
+        return self.world > 1 or self.force
 
     @property
     def root(self):
         return self.rank == 0
 
     def _ar(self, t: torch.Tensor, op):
-        if self.world == 1 or t.numel() == 0:
+        if not self.active or t.numel() == 0:
             return t
         import torch.distributed as dist
 
@@ -69,22 +74,22 @@ class Comm:
     def sum_(self, t):
         import torch.distributed as dist
 
-        return self._ar(t, dist.ReduceOp.SUM) if self.world > 1 else t
+        return self._ar(t, dist.ReduceOp.SUM) if self.active else t
 
     def max_(self, t):
         import torch.distributed as dist
 
-        return self._ar(t, dist.ReduceOp.MAX) if self.world > 1 else t
+        return self._ar(t, dist.ReduceOp.MAX) if self.active else t
 
     def min_(self, t):
         import torch.distributed as dist
 
-        return self._ar(t, dist.ReduceOp.MIN) if self.world > 1 else t
+        return self._ar(t, dist.ReduceOp.MIN) if self.active else t
 
     def allgather_rows(self, t: torch.Tensor) -> torch.Tensor:
         """t (rows, ...): every rank filled rows row_range(rows, world, rank); afterwards
         every rank holds all rows (padded equal-size all_gather; NCCL or gloo)."""
-        if self.world == 1 or t.shape[0] == 0:
+        if not self.active or t.shape[0] == 0:
             return t
         import torch.distributed as dist
 
@@ -102,7 +107,7 @@ class Comm:
         return t
 
     def sum_float(self, v: float, device=None) -> float:
-        if self.world == 1:
+        if not self.active:
             return float(v)
         t = torch.tensor([float(v)], dtype=torch.float64, device=device)
         return float(self.sum_(t).item())
