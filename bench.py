@@ -331,6 +331,40 @@ def run_b200(args):
             dt = float(tt.item())
         e2e_ms += dt
         e2e_units += rep.stage1.sweeps + rep.ipm.iters
+    # the same steps through the two-slot pipeline (public SolvePipeline): step i+1's H2D
+    # of M runs on the copy engine under step i's solve; every step's copies and read-backs
+    # stay inside the timed region
+    from paper_2101_08431_b200 import SolvePipeline
+
+    pipe_ms, pipe_units, pipe_err, npipe = None, 0, None, max(1, min(args.steps, 5))
+    try:
+        pipe = SolvePipeline(b - a, cfg.m, cfg.k, comm=comm, tol_rel=cfg.tol,
+                             s1=Stage1Config(fixed_sweeps=cfg.fixed_sweeps),
+                             ipm=IpmParams(fixed_iters=cfg.fixed_ipm), e_scale=e_scale)
+        for _ in range(2):  # warm both slots (engines, graphs)
+            pipe.submit(Mh, X0r, Y0)
+        for _ in range(2):
+            pipe.result()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pipe.submit(Mh, X0r, Y0)
+        for i in range(npipe):
+            if i + 1 < npipe:
+                pipe.submit(Mh, X0r, Y0)
+            rep = pipe.result()
+            pipe_units += rep.stage1.sweeps + rep.ipm.iters
+        torch.cuda.synchronize()
+        pipe_ms = 1e3 * (time.perf_counter() - t0)
+        if ws > 1:
+            tt = torch.tensor([pipe_ms], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            pipe_ms = float(tt.item())
+        pipe_obj = rep.final_objective
+        del pipe
+    except Exception as exc:  # noqa: BLE001  (the serial e2e number stands)
+        pipe_err = f"{type(exc).__name__}: {exc}"[:300]
     nk, mk = (b - a) * cfg.k, cfg.m * cfg.k
     h2d = Mr.nbytes + X0r.nbytes + Y0.nbytes
     d2h = 8 * (2 * (nk + mk) + 2 * (nk + mk)) + (nk + mk)  # stage-1 X/Y + passive sets, final X/Y/R/S
@@ -362,6 +396,25 @@ def run_b200(args):
     traffic, traffic_src = _ncu_traffic()
     if traffic is not None and ws > 1:
         traffic = traffic * rows / cfg.n
+    serial = {"value": e2e_units / (e2e_ms / 1e3), "ms_per_step": e2e_ms / ne2e, "steps": ne2e,
+              "how": "public run_two_stage(M_host, X0, Y0, problem=P): P allocated once "
+                     "outside the timed region, M (800 MB) copied from pinned host memory "
+                     "into it every step, then solved, stage-1 / final factors read back"}
+    if pipe_ms is not None:
+        e2e_obj = {"value": pipe_units / (pipe_ms / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                   "ms_per_step": pipe_ms / npipe, "steps": npipe,
+                   "objective_after_step": pipe_obj,
+                   "how": "public SolvePipeline (two resident problem slots): submit(M_host, "
+                          "X0, Y0) starts the step's H2D copy of M (800 MB, pinned) on the copy "
+                          "stream, result() solves it (run_two_stage on the slot) and reads the "
+                          "stage-1 / final factors back; step i+1 is submitted before step i is "
+                          "solved, so its copy runs under that solve.  The timed region holds "
+                          "every step's copies, the first one not overlapped",
+                   "serial": serial}
+    else:
+        e2e_obj = dict(serial, unit=UNIT, h2d_bytes_per_step=int(h2d),
+                       d2h_bytes_per_step=int(d2h), pipeline_error=pipe_err)
     line = {
         "metric": _metric(), "value": value, "unit": UNIT,
         "n_gpus": ws, "steps": args.steps, "warmup": max(3, args.warmup),
@@ -394,12 +447,7 @@ def run_b200(args):
         "fp64_dgemm_tflops_measured": fp64_peak,
         "gpu_launches": int(launches),
         "clocks": clk,
-        "e2e": {"value": e2e_units / (e2e_ms / 1e3), "unit": UNIT,
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_ms / ne2e,
-                "how": "public run_two_stage(M_host, X0, Y0, problem=P): P allocated once "
-                       "outside the timed region, M (800 MB) copied from pinned host memory "
-                       "into it every step, stage-1 / final factors read back"},
+        "e2e": e2e_obj,
         "aux": aux,
     }
     if ws == 1 and not args.no_cpu:

@@ -20,4 +20,12 @@ def run_two_stage(M, X0, Y0, tol_rel=1e-10, cfg=None, ipm=None, tp=None, stage="
                                 stage=stage, **kw)
 
 
-__all__ = ["run_two_stage", "Stage1Config", "IpmParams", "TransitionParams", "SolveReport"]
+def SolvePipeline(*a, **kw):
+    """Two resident problem slots; the next instance's host-to-device copy overlaps the
+    current solve (see pipeline.SolvePipeline)."""
+    from .pipeline import SolvePipeline as _SP
+
+    return _SP(*a, **kw)
+
+
+__all__ = ["run_two_stage", "SolvePipeline", "Stage1Config", "IpmParams", "TransitionParams", "SolveReport"]

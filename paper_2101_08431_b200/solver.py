@@ -162,6 +162,12 @@ class Problem:
         if tuple(Mnew.shape) != (self.n, self.m):
             raise ValueError(f"load: shape {tuple(Mnew.shape)} != {(self.n, self.m)}")
         self.M.copy_(Mnew.to(dtype=self.M.dtype), non_blocking=True)
+        return self.refresh_norms()
+
+    def refresh_norms(self):
+        """After the data of M changed in place (``load``, or a copy issued by the caller on
+        another stream and already awaited on this one: pipeline.SolvePipeline): squared row /
+        column norms, ||M||^2, and the cached engines' incremental products invalidated."""
         self._call("nmfb_sqnorms", _p(self.M), self.f32, self.n, self.m, _p(self.row_n2),
                    _p(self.col_n2), _p(self.cwork), self.cwork.numel(), self.stream)
         self.comm.sum_(self.col_n2)
