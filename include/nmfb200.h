@@ -254,6 +254,17 @@ int nmfb_fill(double *v, long len, double c, void *stream);
  * non-positive pivot column or -1.  Then (L L^T) x = b in place on b. */
 int nmfb_dense_cholesky(double *A, long N, int *info, void *stream);
 int nmfb_dense_solve(const double *L, long N, double *b, void *stream);
+/* Factor and forward-substitute in one launch (b <- L^{-1} b rides along as one more tile
+ * row of the dataflow Cholesky, csrc/dense_flow.cuh), then nmfb_dense_solve_back finishes
+ * b <- L^{-T} b: the spd_solve of SPEC.md:68 for the full-coupling directions, whose
+ * right-hand side is known before the factorization.  nmfb_dense_solve_mode: 1 forward,
+ * 2 backward, 3 both, with an existing factor (the predictor's reuse). */
+int nmfb_dense_cholesky_rhs(double *A, long N, double *b, int *info, void *stream);
+int nmfb_dense_solve_back(const double *L, long N, double *b, void *stream);
+int nmfb_dense_solve_mode(const double *L, long N, double *b, int mode, void *stream);
+/* profiling aid: buf (device, 8 int64 per tile, global tile order) receives globaltimer
+ * stamps of the dataflow factorization's phases; NULL switches it off */
+int nmfb_flow_profile(long long *buf);
 
 /* Exact low-rank Gauss-Newton reduced-system solve (replaces the dense mk x mk
  * spd_solve when the coupling is C-bar, PAPER Eq. 12): S = U Zb U^T with

@@ -67,6 +67,10 @@ SIGNATURES = {
     "nmfb_fill": [P, L, D, P],
     "nmfb_dense_cholesky": [P, L, P, P],
     "nmfb_dense_solve": [P, L, P, P],
+    "nmfb_dense_cholesky_rhs": [P, L, P, P, P],
+    "nmfb_dense_solve_back": [P, L, P, P],
+    "nmfb_dense_solve_mode": [P, L, P, I, P],
+    "nmfb_flow_profile": [P],
     "nmfb_launch_count": [],
     "nmfb_last_cuda_error": [],
     "nmfb_tma_products": [I],

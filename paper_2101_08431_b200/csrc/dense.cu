@@ -201,6 +201,10 @@ __device__ __forceinline__ double trsv_diag_warp(const double* __restrict__ L, l
   return trsv_diag_solve(nc, trans, v, blk, rcp);
 }
 
+}  // namespace
+#include "dense_flow.cuh"  // dataflow Cholesky / solves (uses trsv_diag_solve above)
+namespace {
+
 constexpr int TRSV_T = 256;  // 1024 threads spilled the 32-entry row to local memory
 
 // Single-CTA blocked solve.  Per 32-column block: warp 0 solves the diagonal block
@@ -395,6 +399,8 @@ __global__ void k_trsv_update(const double* __restrict__ L, long N, double* __re
 
 constexpr size_t kTwoTiles = 2 * NB * (NB + 1) * sizeof(double);
 
+extern "C" int nmfb_dense_solve_mode(const double* L, long N, double* b, int mode, void* stream);
+
 extern "C" int nmfb_dense_cholesky(double* A, long N, int* info, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (N <= 0) return NMFB_EINVAL;
@@ -403,6 +409,12 @@ extern "C" int nmfb_dense_cholesky(double* A, long N, int* info, void* stream) {
     nmfb_smem_attr(k_trsm_panel, (int)kTwoTiles);
     nmfb_smem_attr(k_syrk_trailing, (int)kTwoTiles);
     attr = true;
+  }
+  if (flow_chol_eligible(A, N, nullptr)) {  // csrc/dense_flow.cuh: tile dataflow, DMMA
+    const int rc = launch_chol_flow(A, (int)N, nullptr, info, 0, st);
+    if (rc != NMFB_OK) return rc;
+    NMFB_CHECK_LAUNCH();
+    return NMFB_OK;
   }
   if (N <= 4096) {  // csrc/chol_blk.cuh: one CTA up to 128, cooperative panels above
     const int rc = launch_chol(A, (int)N, info, 0, 0, 1, st);
@@ -425,10 +437,72 @@ extern "C" int nmfb_dense_cholesky(double* A, long N, int* info, void* stream) {
   return NMFB_OK;
 }
 
+// Factor A = L L^T in place and overwrite b with L^{-1} b in the same launch (the right-hand
+// side rides along as one more tile row); finish with nmfb_dense_solve_back.  Falls back to
+// the separate factorization + forward solve outside the dataflow kernel's range.
+extern "C" int nmfb_dense_cholesky_rhs(double* A, long N, double* b, int* info, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (N <= 0 || b == nullptr) return NMFB_EINVAL;
+  if (flow_chol_eligible(A, N, b)) {
+    const int rc = launch_chol_flow(A, (int)N, b, info, 0, st);
+    if (rc != NMFB_OK) return rc;
+    NMFB_CHECK_LAUNCH();
+    return NMFB_OK;
+  }
+  const int rc = nmfb_dense_cholesky(A, N, info, stream);
+  if (rc != NMFB_OK) return rc;
+  return nmfb_dense_solve_mode(A, N, b, 1, stream);
+}
+
+// profiling aid: 8 globaltimer stamps per tile of the dataflow factorization (null: off)
+extern "C" int nmfb_flow_profile(long long* buf) {
+  return cudaMemcpyToSymbol(g_flow_prof, &buf, sizeof(buf)) == cudaSuccess ? NMFB_OK : NMFB_ELAUNCH;
+}
+
+// b <- L^{-T} b (the second half of the solve after nmfb_dense_cholesky_rhs)
+extern "C" int nmfb_dense_solve_back(const double* L, long N, double* b, void* stream) {
+  return nmfb_dense_solve_mode(L, N, b, 2, stream);
+}
+
+// mode 1: b <- L^{-1} b, 2: b <- L^{-T} b, 3: both (the full solve)
+extern "C" int nmfb_dense_solve_mode(const double* L, long N, double* b, int mode, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (N <= 0 || mode < 1 || mode > 3) return NMFB_EINVAL;
+  if (flow_trsv_eligible(N)) {
+    const int rc = launch_trsv_flow(L, (int)N, b, mode, st);
+    if (rc != NMFB_OK) return rc;
+    NMFB_CHECK_LAUNCH();
+    return NMFB_OK;
+  }
+  if (N > 640 && N <= 65536) {
+    int G = (int)((N - 32 + 255) / 256) + 1;
+    if (G > 148) G = 148;
+    if (G < 2) G = 2;
+    for (int trans = 0; trans < 2; ++trans) {
+      if (!(mode & (1 << trans))) continue;
+      void* args[] = {(void*)&L, &N, &b, &trans};
+      ++g_nmfb_launches;
+      if (cudaLaunchCooperativeKernel((const void*)k_trsv_coop, dim3(G), dim3(256), args, 0, st) !=
+          cudaSuccess)
+        return NMFB_ELAUNCH;
+    }
+    NMFB_CHECK_LAUNCH();
+    return NMFB_OK;
+  }
+  if (N > 4096) return mode == 3 ? nmfb_dense_solve(L, N, b, stream) : NMFB_EUNSUPPORTED;
+  const size_t sm = (size_t)N * sizeof(double);
+  nmfb_smem_attr(k_trsv_single, (int)(4096 * sizeof(double)));
+  if (mode & 1) ++g_nmfb_launches, k_trsv_single<<<1, TRSV_T, sm, st>>>(L, N, b, 0);
+  if (mode & 2) ++g_nmfb_launches, k_trsv_single<<<1, TRSV_T, sm, st>>>(L, N, b, 1);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
 // in-place solve (L L^T) x = b using the factor from nmfb_dense_cholesky
 extern "C" int nmfb_dense_solve(const double* L, long N, double* b, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (N <= 0) return NMFB_EINVAL;
+  if (flow_trsv_eligible(N)) return nmfb_dense_solve_mode(L, N, b, 3, stream);
   if (N > 640 && N <= 65536) {  // cooperative: one grid barrier per block
     int G = (int)((N - 32 + 255) / 256) + 1;
     if (G > 148) G = 148;

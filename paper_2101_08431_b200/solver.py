@@ -13,6 +13,7 @@ NativeLibraryError.
 from __future__ import annotations
 
 import functools
+import gc
 import math
 import os
 import time
@@ -827,18 +828,27 @@ class IpmEngine:
                 self.capture_stream = torch.cuda.Stream(self.P.dev)
             cur = torch.cuda.current_stream(self.P.dev)
             self.capture_stream.wait_stream(cur)
-            with torch.cuda.stream(self.capture_stream):
-                if self.graph_pool is None:
-                    g.capture_begin()
-                else:
-                    g.capture_begin(pool=self.graph_pool)
-                try:
-                    if not self.small:
-                        self.P.lib.nmfb_set_mu_source(self.mu_dev.data_ptr())
-                    self.gn_iteration_launch()
-                finally:
-                    self.P.lib.nmfb_set_mu_source(None)
-                    g.capture_end()
+            # no cyclic garbage collection while the stream captures: collecting an old
+            # engine there destroys its CUDA graphs (cudaGraphExecDestroy is not permitted
+            # during a global-mode capture and invalidates this one)
+            gc_on = gc.isenabled()
+            gc.disable()
+            try:
+                with torch.cuda.stream(self.capture_stream):
+                    if self.graph_pool is None:
+                        g.capture_begin()
+                    else:
+                        g.capture_begin(pool=self.graph_pool)
+                    try:
+                        if not self.small:
+                            self.P.lib.nmfb_set_mu_source(self.mu_dev.data_ptr())
+                        self.gn_iteration_launch()
+                    finally:
+                        self.P.lib.nmfb_set_mu_source(None)
+                        g.capture_end()
+            finally:
+                if gc_on:
+                    gc.enable()
             cur.wait_stream(self.capture_stream)
             if _GRAPH_DEBUG:
                 torch.cuda.synchronize(self.P.dev)
@@ -1001,9 +1011,11 @@ class IpmEngine:
                 P._call("nmfb_schur_term4", _p(F), n, m, k, _p(self.Apk), _p(self.A),
                         _p(self.t4work), self.t4work.numel(), s)
                 self.comm.sum_(self.A)
-            P._call("nmfb_dense_cholesky", _p(self.A), N, _p(P.iscal[3:]), s)
+            # the right-hand side rides along the factorization (b <- L^{-1} b as one more
+            # tile row, csrc/dense_flow.cuh), then the backward half
             dY.copy_(self.rhs.view(m, k))
-            P._call("nmfb_dense_solve", _p(self.A), N, _p(dY), s)
+            P._call("nmfb_dense_cholesky_rhs", _p(self.A), N, _p(dY), _p(P.iscal[3:]), s)
+            P._call("nmfb_dense_solve_back", _p(self.A), N, _p(dY), s)
         else:
             if fork:
                 cur.wait_event(ev_y)

@@ -16,7 +16,7 @@ def lib():
     return _lib.load()
 
 
-@pytest.mark.parametrize("N", [100, 150, 300, 641, 1000, 2000])
+@pytest.mark.parametrize("N", [100, 130, 150, 300, 352, 641, 1000, 1760, 2000, 4096])
 def test_dense_cholesky_and_solve(lib, N):
     import torch
 
@@ -38,7 +38,51 @@ def test_dense_cholesky_and_solve(lib, N):
     assert np.abs(x.cpu().numpy() - xr).max() / np.abs(xr).max() < 1e-12
 
 
-@pytest.mark.parametrize("N", [120, 700])
+@pytest.mark.parametrize("N", [130, 300, 999, 1760, 2000])
+def test_dense_cholesky_rhs_and_modes(lib, N):
+    """The factorization with the right-hand side riding along (b <- L^{-1} b in the same
+    launch, csrc/dense_flow.cuh; odd N takes the fallback), the backward half, and the
+    three modes of the solve with an existing factor, against NumPy; run twice (the flags
+    and solution buffers are re-armed per launch) and bit-reproducible."""
+    import scipy.linalg as sla
+    import torch
+
+    rng = np.random.default_rng(N + 1)
+    B = rng.standard_normal((N, N))
+    A = B @ B.T / N + np.eye(N)
+    rhs = rng.standard_normal(N)
+    Lr = np.linalg.cholesky(A)
+    zr = sla.solve_triangular(Lr, rhs, lower=True)
+    xr = sla.solve_triangular(Lr.T, zr, lower=False)
+    s = torch.cuda.current_stream().cuda_stream
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    outs = []
+    for _ in range(2):
+        d = torch.as_tensor(A).cuda()
+        b = torch.as_tensor(rhs).cuda()
+        assert lib.nmfb_dense_cholesky_rhs(d.data_ptr(), N, b.data_ptr(), info.data_ptr(), s) == 0
+        z = b.cpu().numpy().copy()
+        assert int(info.item()) == -1
+        L = d.cpu().numpy()
+        assert np.abs(np.triu(L, 1)).max() == 0.0
+        assert np.abs(L - Lr).max() / np.abs(Lr).max() < 1e-13
+        assert np.abs(z - zr).max() / np.abs(zr).max() < 1e-12
+        assert lib.nmfb_dense_solve_back(d.data_ptr(), N, b.data_ptr(), s) == 0
+        x = b.cpu().numpy().copy()
+        assert np.abs(x - xr).max() / np.abs(xr).max() < 1e-12
+        outs.append((L, z, x))
+    for a, c in zip(outs[0], outs[1]):
+        assert np.array_equal(a, c)
+    for mode, want in ((1, zr), (3, xr)):
+        b = torch.as_tensor(rhs).cuda()
+        assert lib.nmfb_dense_solve_mode(d.data_ptr(), N, b.data_ptr(), mode, s) == 0
+        assert np.abs(b.cpu().numpy() - want).max() / np.abs(want).max() < 1e-12
+    b = torch.as_tensor(zr).cuda()
+    assert lib.nmfb_dense_solve_mode(d.data_ptr(), N, b.data_ptr(), 2, s) == 0
+    assert np.abs(b.cpu().numpy() - xr).max() / np.abs(xr).max() < 1e-12
+
+
+@pytest.mark.parametrize("N", [120, 700, 1760])
 def test_dense_cholesky_reports_failing_pivot(lib, N):
     import torch
 
@@ -50,6 +94,13 @@ def test_dense_cholesky_reports_failing_pivot(lib, N):
     info = torch.zeros(1, dtype=torch.int32, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
     assert lib.nmfb_dense_cholesky(d.data_ptr(), N, info.data_ptr(), s) == 0
+    torch.cuda.synchronize()
+    assert 0 <= int(info.item()) <= N // 2
+    # and the same through the fused entry (the solve still terminates on the failed factor)
+    d = torch.as_tensor(A).cuda()
+    b = torch.ones(N, dtype=torch.float64, device="cuda")
+    assert lib.nmfb_dense_cholesky_rhs(d.data_ptr(), N, b.data_ptr(), info.data_ptr(), s) == 0
+    assert lib.nmfb_dense_solve_back(d.data_ptr(), N, b.data_ptr(), s) == 0
     torch.cuda.synchronize()
     assert 0 <= int(info.item()) <= N // 2
 
