@@ -66,6 +66,36 @@ __device__ __forceinline__ void flow_dmma(double& d0, double& d1, double a, doub
                : "d"(a), "d"(b));
 }
 
+// 32 x 32 diagonal factor, one warp, row r = lane in registers (the arithmetic of
+// BCholStep, chol_blk.cuh, on the lower triangle) with the pivot chain software-pipelined:
+// the next pivot a[J+1][J+1] - l^2 is formed from two shuffles issued before this step's
+// column updates and its rsqrt is in flight while the remaining 30 - J updates issue.
+template <int J>
+struct FlowChol {
+  static __device__ __forceinline__ void run(double (&a)[32], int r, double pv, double di,
+                                             int& fail, double& di_r) {
+    a[J] = (r == J) ? pv * di : ((r > J) ? a[J] * di : a[J]);
+    di_r = (r == J) ? di : di_r;
+    if constexpr (J + 1 < 32) {
+      const double l1 = __shfl_sync(0xffffffffu, a[J], J + 1);      // L[J+1][J]
+      const double d1 = __shfl_sync(0xffffffffu, a[J + 1], J + 1);  // A[J+1][J+1] so far
+      double pv1 = d1 - l1 * l1;
+      if (fail < 0 && !(pv1 > 0.0)) fail = J + 1;
+      if (fail >= 0) pv1 = 1.0;
+      const double di1 = rsqrt(pv1);
+      // column updates a[C] -= L[r][J] L[C][J], C > J: every broadcast first, then the
+      // FMAs (entries above the diagonal, r < C, collect unused values)
+      double l[32];
+#pragma unroll
+      for (int C = J + 2; C < 32; ++C) l[C] = __shfl_sync(0xffffffffu, a[J], C);
+      a[J + 1] = a[J + 1] - a[J] * l1;
+#pragma unroll
+      for (int C = J + 2; C < 32; ++C) a[C] = a[C] - a[J] * l[C];
+      FlowChol<J + 1>::run(a, r, pv1, di1, fail, di_r);
+    }
+  }
+};
+
 // min(prog[i], prog[j]) seen by thread 0, broadcast; < 0: abort
 __device__ __forceinline__ int flow_peek(int i, int j, int* sh) {
   if (threadIdx.x == 0) {
@@ -180,6 +210,19 @@ __global__ void __launch_bounds__(FLOW_T) k_chol_flow(double* __restrict__ A, in
     double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
     bool dead = false;
     flow_stamp(prof, g, 0);
+    // A_ij itself (untouched input) on its way while the products accumulate; identity
+    // padding beyond N keeps the padded factor trivial
+    double aij[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int e = tid + h * FLOW_T, r = e >> 5, c = e & 31;
+      if (rrow)
+        aij[h] = (r == 0 && J0 + c < N) ? __ldcg(rhs + J0 + c) : 0.0;
+      else if (I0 + r < N && J0 + c < N)
+        aij[h] = __ldcg(A + (long)(I0 + r) * N + J0 + c);
+      else
+        aij[h] = (diag && r == c) ? 1.0 : 0.0;
+    }
     if (j > 0) {
       int known = flow_peek(i, j, &sh_v);
       dead = known < 0;
@@ -232,17 +275,11 @@ __global__ void __launch_bounds__(FLOW_T) k_chol_flow(double* __restrict__ A, in
     }
     if (dead) break;
     flow_stamp(prof, g, 1);
-    // tl = A_ij - sum (identity padding beyond N keeps the padded factor trivial)
-    for (int e = tid; e < 1024; e += FLOW_T) {
-      const int r = e >> 5, c = e & 31;
-      double v;
-      if (rrow)
-        v = (r == 0 && J0 + c < N) ? __ldcg(rhs + J0 + c) : 0.0;
-      else if (I0 + r < N && J0 + c < N)
-        v = __ldcg(A + (long)(I0 + r) * N + J0 + c);
-      else
-        v = (diag && r == c) ? 1.0 : 0.0;
-      tl[r * FLOW_LDS + c] = v;
+    // tl = A_ij - sum
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int e = tid + h * FLOW_T;
+      tl[(e >> 5) * FLOW_LDS + (e & 31)] = aij[h];
     }
     __syncthreads();
     {
@@ -262,7 +299,11 @@ __global__ void __launch_bounds__(FLOW_T) k_chol_flow(double* __restrict__ A, in
         for (int c = 0; c < 32; ++c) a[c] = tl[lane * FLOW_LDS + c];
         int fail = -1;
         double di = 0.0;
-        BCholStep<0>::run(a, lane, fail, di);
+        {
+          double pv = __shfl_sync(0xffffffffu, a[0], 0);
+          if (!(pv > 0.0)) fail = 0, pv = 1.0;
+          FlowChol<0>::run(a, lane, pv, rsqrt(pv), fail, di);
+        }
 #pragma unroll
         for (int c = 0; c < 32; ++c) tl[lane * FLOW_LDS + c] = (c <= lane) ? a[c] : 0.0;
         sdinv[lane] = di;
@@ -282,8 +323,9 @@ __global__ void __launch_bounds__(FLOW_T) k_chol_flow(double* __restrict__ A, in
       flow_stamp(prof, g, 3);
       for (int e = tid; e < 1024; e += FLOW_T) {
         const int r = e >> 5, c = e & 31;
-        lj[r * FLOW_LDS + c] = (J0 + r < N && J0 + c < N) ? __ldcg(A + (long)(J0 + r) * N + J0 + c)
-                                                          : (r == c ? 1.0 : 0.0);
+        // strictly lower part only: the sweeps scale by 1 / L_cc (sdinv) and must leave
+        // an entry alone once its column is reached
+        lj[r * FLOW_LDS + c] = (c < r && J0 + r < N) ? __ldcg(A + (long)(J0 + r) * N + J0 + c) : 0.0;
       }
       if (tid < 32) sdinv[tid] = __ldcg(g_flow_dinv + J0 + tid);
       __syncthreads();
@@ -291,25 +333,22 @@ __global__ void __launch_bounds__(FLOW_T) k_chol_flow(double* __restrict__ A, in
       {
         const double dl = sdinv[lane];
         const double* lrow = lj + lane * FLOW_LDS;
-        double acc[4], x[4];
+        // x_c = (a_c - sum_{c' < c} x_c' L[c][c']) / L_cc: lane c stops changing once the
+        // sweep passes column c (L[c][jj] = 0 for jj >= c in the staged copy)
+        double acc[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          acc[u] = tl[(4 * wid + u) * FLOW_LDS + lane];
-          x[u] = 0.0;
-        }
-#pragma unroll 4
-        for (int jj = 0; jj < 32; ++jj) {
+        for (int u = 0; u < 4; ++u) acc[u] = tl[(4 * wid + u) * FLOW_LDS + lane];
+#pragma unroll 8
+        for (int jj = 0; jj < 31; ++jj) {
           const double lcj = lrow[jj];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const double xj = __shfl_sync(0xffffffffu, acc[u] * dl, jj);
-            const double nacc = acc[u] - lcj * xj;
-            x[u] = (lane == jj) ? xj : x[u];
-            acc[u] = (lane > jj) ? nacc : acc[u];
+            acc[u] = acc[u] - lcj * xj;
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) tl[(4 * wid + u) * FLOW_LDS + lane] = x[u];
+        for (int u = 0; u < 4; ++u) tl[(4 * wid + u) * FLOW_LDS + lane] = acc[u] * dl;
       }
       __syncthreads();
       flow_stamp(prof, g, 5);
@@ -327,8 +366,7 @@ __global__ void __launch_bounds__(FLOW_T) k_chol_flow(double* __restrict__ A, in
     __syncthreads();
     flow_stamp(prof, g, 6);
     if (tid == 0) {
-      __threadfence();
-      flow_st(g_flow_prog + i, j + 1);
+      flow_st(g_flow_prog + i, j + 1);  // release: orders the CTA's writes (bar.sync above)
       flow_stamp(prof, g, 7);
       if (g == ntiles - 1) {  // the last tile depends on every diagonal tile
         const int f = flow_ld(&g_flow_fail);
