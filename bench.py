@@ -523,10 +523,11 @@ def aux_c2(dev):
             "solver_iterations_per_s": (rep.stage1.sweeps + r.iters) / s}
 
 
-def aux_c3(dev, cap=100):
+def aux_c3(dev, cap=500):
     """c3 streaming session (n = 3000, k = 4, chunks of 10 columns from m = 20 to 500), each
-    chunk solved warm with a per-chunk IPM budget of ``cap`` iterations: per-chunk time,
-    status and E(.;0) (relative KKT target 1e-10)."""
+    chunk solved warm with the specification's default cap of 500 IPM iterations
+    (SPEC.md:357): per-chunk time, status and E(.;0) (relative KKT target 1e-10).  The
+    prefixes are rank deficient for k = 4, so the chunks end at the cap."""
     import statistics
 
     import torch
@@ -573,7 +574,12 @@ def aux_c5(dev, ws, rank):
     P = solver.Problem(M, cfg.k, comm=comm)
     del M
     X0d, Yt0d = P.to_dev(X0), P.to_dev(Y0.T)
-    solver.run_stage1(P, X0d, Yt0d, Stage1Config(fixed_sweeps=1))
+    # warm-up: one sweep and three IPM iterations (the engine's buffers and both CUDA graphs
+    # exist before the timed region, as in the headline's warm-up steps)
+    Xw, Ytw, _, _, _ = solver.run_stage1(P, X0d, Yt0d, Stage1Config(fixed_sweeps=1))
+    Xw, Ytw, Rw, Sw, muw, rhow = solver.transition(P, Xw, Ytw, 1e-10)
+    solver.run_ipm(P, Xw, Ytw, Rw, Sw, muw, rhow, IpmParams(fixed_iters=3))
+    del Xw, Ytw, Rw, Sw
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -592,7 +598,7 @@ def aux_c5(dev, ws, rank):
         ms = [float(v) for v in t.tolist()]
     out = {"workload": f"c5: {cfg.fixed_sweeps} sweeps + {cfg.fixed_ipm} IPM iterations, fp32 M "
                        f"{cfg.n} x {cfg.m}, k={cfg.k}, rows sharded over {ws} GPU(s) (strong "
-                       "scaling; first IPM iterations include the engine's graph captures)",
+                       "scaling; engine and graphs warmed by three untimed iterations)",
            "anls_sweeps_per_s": cfg.fixed_sweeps / (ms[0] / 1e3),
            "ms_per_sweep": ms[0] / cfg.fixed_sweeps,
            "ipm_iters_per_s": r2.iters / (ms[1] / 1e3), "ms_per_ipm_iter": ms[1] / max(r2.iters, 1),

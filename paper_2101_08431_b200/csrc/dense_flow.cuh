@@ -325,7 +325,10 @@ __global__ void __launch_bounds__(FLOW_T) k_chol_flow(double* __restrict__ A, in
         const int r = e >> 5, c = e & 31;
         // strictly lower part only: the sweeps scale by 1 / L_cc (sdinv) and must leave
         // an entry alone once its column is reached
-        lj[r * FLOW_LDS + c] = (c < r && J0 + r < N) ? __ldcg(A + (long)(J0 + r) * N + J0 + c) : 0.0;
+        // and rows pre-scaled by 1 / L_rr, which takes the multiply off the sweep's chain
+        lj[r * FLOW_LDS + c] = (c < r && J0 + r < N) ? __ldcg(A + (long)(J0 + r) * N + J0 + c) *
+                                                           __ldcg(g_flow_dinv + J0 + r)
+                                                     : 0.0;
       }
       if (tid < 32) sdinv[tid] = __ldcg(g_flow_dinv + J0 + tid);
       __syncthreads();
@@ -333,22 +336,20 @@ __global__ void __launch_bounds__(FLOW_T) k_chol_flow(double* __restrict__ A, in
       {
         const double dl = sdinv[lane];
         const double* lrow = lj + lane * FLOW_LDS;
-        // x_c = (a_c - sum_{c' < c} x_c' L[c][c']) / L_cc: lane c stops changing once the
-        // sweep passes column c (L[c][jj] = 0 for jj >= c in the staged copy)
+        // x_c = a_c / L_cc - sum_{c' < c} x_c' (L[c][c'] / L_cc): lane c stops changing once
+        // the sweep passes column c (the staged copy is strictly lower)
         double acc[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] = tl[(4 * wid + u) * FLOW_LDS + lane];
+        for (int u = 0; u < 4; ++u) acc[u] = tl[(4 * wid + u) * FLOW_LDS + lane] * dl;
 #pragma unroll 8
         for (int jj = 0; jj < 31; ++jj) {
           const double lcj = lrow[jj];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double xj = __shfl_sync(0xffffffffu, acc[u] * dl, jj);
-            acc[u] = acc[u] - lcj * xj;
-          }
+          for (int u = 0; u < 4; ++u)
+            acc[u] = fma(-lcj, __shfl_sync(0xffffffffu, acc[u], jj), acc[u]);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) tl[(4 * wid + u) * FLOW_LDS + lane] = acc[u] * dl;
+        for (int u = 0; u < 4; ++u) tl[(4 * wid + u) * FLOW_LDS + lane] = acc[u];
       }
       __syncthreads();
       flow_stamp(prof, g, 5);
@@ -401,7 +402,7 @@ __device__ __forceinline__ double flow_poll(const double* p, bool& dead) {
 // mode 1: b <- L^{-1} b; 2: b <- L^{-T} b; 3: b <- (L L^T)^{-1} b.  One CTA per 32-row block.
 __global__ void __launch_bounds__(FLOW_T) k_trsv_flow(const double* __restrict__ L, int N,
                                                       double* __restrict__ b, int mode) {
-  __shared__ double blk[32 * 33], rcp[32], red[8][33], zs[32];
+  __shared__ double blk[32 * 33], bF[32 * 33], bT[32 * 33], rcp[32], red[8][33], zs[32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int T = (N + 31) / 32, j = blockIdx.x, J0 = 32 * j;
   const int nc = min(32, N - J0);
@@ -411,6 +412,17 @@ __global__ void __launch_bounds__(FLOW_T) k_trsv_flow(const double* __restrict__
     blk[r * 33 + c] = (r < nc && c < nc) ? L[(long)(J0 + r) * N + J0 + c] : 0.0;
   }
   if (tid < 32) zs[tid] = tid < nc ? b[J0 + tid] : 0.0;
+  __syncthreads();
+  if (tid < 32) rcp[tid] = tid < nc ? 1.0 / blk[tid * 33 + tid] : 0.0;
+  __syncthreads();
+  // strictly lower block scaled by rows (forward) and, transposed, by columns (backward):
+  // the sweeps are then one shuffle and one FMA per step
+  for (int e = tid; e < 32 * 32; e += FLOW_T) {
+    const int r = e >> 5, c = e & 31;
+    const double v = c < r ? blk[r * 33 + c] : 0.0;
+    bF[r * 33 + c] = v * rcp[r];
+    bT[c * 33 + r] = v * rcp[c];
+  }
   __syncthreads();
   if (mode & 1) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0}, cur[4], nxt[4];
@@ -437,8 +449,10 @@ __global__ void __launch_bounds__(FLOW_T) k_trsv_flow(const double* __restrict__
     }
     __syncthreads();
     if (wid == 0) {
-      double v = lane < nc ? zs[lane] - red[0][lane] : 0.0;
-      v = trsv_diag_solve(nc, 0, v, blk, rcp);
+      double v = lane < nc ? (zs[lane] - red[0][lane]) * rcp[lane] : 0.0;
+#pragma unroll 8
+      for (int jj = 0; jj < 31; ++jj)
+        v = fma(-bF[lane * 33 + jj], __shfl_sync(0xffffffffu, v, jj), v);
       v = lane < nc ? v : 0.0;
       __stcg(g_flow_z + J0 + lane, v);
       zs[lane] = v;
@@ -471,8 +485,10 @@ __global__ void __launch_bounds__(FLOW_T) k_trsv_flow(const double* __restrict__
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < 8; ++w) s += red[w][lane];
-      double v = lane < nc ? zs[lane] - s : 0.0;
-      v = trsv_diag_solve(nc, 1, v, blk, rcp);
+      double v = lane < nc ? (zs[lane] - s) * rcp[lane] : 0.0;
+#pragma unroll 8
+      for (int jj = 31; jj > 0; --jj)
+        v = fma(-bT[lane * 33 + jj], __shfl_sync(0xffffffffu, v, jj), v);
       v = lane < nc ? v : 0.0;
       __stcg(g_flow_x + J0 + lane, v);
       if (lane < nc) b[J0 + lane] = v;
