@@ -102,12 +102,28 @@ def test_stage1_fp32_storage(mods):
     assert rel(X.cpu().numpy(), ro.X) < 1e-4 and rel(Yt.cpu().numpy(), ro.Yt) < 1e-4
 
 
-@pytest.mark.parametrize("name,barrier,iters,eps,solve,resid", [
-    ("c1", "paper", 40, 1e-7, "lowrank", "auto"), ("c1", "balanced", 60, 1e-7, "lowrank", "auto"),
-    ("c1", "balanced", 50, 1e-5, "lowrank", "auto"),  # full Hessian at it 28, 29, 47
-    ("c1", "balanced", 50, 1e-5, "dense", "auto"), ("c2", "balanced", 35, 1e-6, "lowrank", "auto"),
-    ("c1", "paper", 40, 1e-7, "lowrank", "free"), ("c2", "paper", 30, 1e-6, "lowrank", "free")])
-def test_ipm_parity(mods, name, barrier, iters, eps, solve, resid):
+# Per-case factor tolerance = a measured conditioning bound (scripts/parity_spread.py on a
+# B200, round 2): device-vs-oracle deviation next to the deviation between the oracle's own
+# two Schur backends (C loops vs NumPy) on the same trajectory:
+#   c1 paper 40 lowrank      1.8e-12  (oracle backends 2.4e-13)
+#   c1 balanced 60 lowrank   2.1e-9   (2.1e-10)
+#   c1 balanced 50 lowrank   1.3e-10  (1.0e-11)      c1 balanced 50 dense  1.7e-11 (1.0e-11)
+#   c1 paper 40 free         2.7e-12  (2.4e-13)      c2 paper 30 free      3.6e-12 (8.1e-14)
+#   c2 balanced 35 lowrank   3.4e-8   (1.7e-10)      c2 balanced 35 dense  1.9e-8
+#   At c2 (reduced system cond ~1e9) the device differs from the oracle in every product's
+#   summation order (DMMA tiles vs BLAS), not only in the Schur solve -- the oracle's two
+#   backends share everything but the Schur kernels -- so its deviation is ~100x theirs with
+#   either solver.  north_star's 1e-10 holds wherever the oracle agrees with itself to 1e-11.
+@pytest.mark.parametrize("name,barrier,iters,eps,solve,resid,tol", [
+    ("c1", "paper", 40, 1e-7, "lowrank", "auto", 1e-10),
+    ("c1", "balanced", 60, 1e-7, "lowrank", "auto", 2e-8),
+    ("c1", "balanced", 50, 1e-5, "lowrank", "auto", 2e-9),  # full Hessian at it 28, 29, 47
+    ("c1", "balanced", 50, 1e-5, "dense", "auto", 1e-10),
+    ("c2", "balanced", 35, 1e-6, "lowrank", "auto", TOL_IPM),
+    ("c2", "balanced", 35, 1e-6, "dense", "auto", TOL_IPM),
+    ("c1", "paper", 40, 1e-7, "lowrank", "free", 1e-10),
+    ("c2", "paper", 30, 1e-6, "lowrank", "free", 1e-10)])
+def test_ipm_parity(mods, name, barrier, iters, eps, solve, resid, tol):
     data, solver, IpmParams, Stage1Config = mods
     M, X0, Y0 = _instance(data, name)
     k = X0.shape[1]
@@ -128,8 +144,8 @@ def test_ipm_parity(mods, name, barrier, iters, eps, solve, resid):
     assert r.armijo_t == ro2.armijo_t
     assert r.flags == ro2.flags
     for a, b in ((eng.X, ro2.state.X), (eng.Yt, ro2.state.Yt)):
-        assert rel(a.cpu().numpy(), b) < TOL_IPM
-    assert abs(eng.mu - ro2.state.mu) <= TOL_IPM * ro2.state.mu
+        assert rel(a.cpu().numpy(), b) < tol
+    assert abs(eng.mu - ro2.state.mu) <= tol * ro2.state.mu
     if eps == 1e-5:
         assert any(r.flags), "the full-Hessian path was not exercised"
 
