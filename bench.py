@@ -336,7 +336,7 @@ def run_b200(args):
     # stay inside the timed region
     from paper_2101_08431_b200 import SolvePipeline
 
-    pipe_ms, pipe_units, pipe_err, npipe = None, 0, None, max(1, min(args.steps, 5))
+    pipe_ms, pipe_units, pipe_err, npipe = None, 0, None, max(8, min(args.steps, 16))
     try:
         pipe = SolvePipeline(b - a, cfg.m, cfg.k, comm=comm, tol_rel=cfg.tol,
                              s1=Stage1Config(fixed_sweeps=cfg.fixed_sweeps),
