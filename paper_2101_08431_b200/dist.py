@@ -63,6 +63,23 @@ class Comm:
     def root(self):
         return self.rank == 0
 
+    @property
+    def graph_ok(self):
+        """Collectives of this communicator can be captured into a CUDA graph (NCCL: they are
+        stream-ordered kernels; gloo stages through the host and cannot)."""
+        if not self.active:
+            return True
+        import os
+
+        import torch.distributed as dist
+
+        if os.environ.get("NMFB_COMM_GRAPHS", "1") == "0":
+            return False
+        try:
+            return dist.get_backend(self.group) == "nccl"
+        except Exception:  # noqa: BLE001
+            return False
+
     def _ar(self, t: torch.Tensor, op):
         if not self.active or t.numel() == 0:
             return t

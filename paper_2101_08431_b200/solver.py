@@ -387,10 +387,12 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
     if (cfg.persistent and not P.comm.active and nsweeps > 0
             and P.lib.nmfb_stage1_persist_supported(n, m, k, int(P.f32))):
         return _stage1_persistent(P, X, Yt, pX, pY, Yn, stX, stY, have_carry, cfg, nsweeps, res, t0)
-    # fixed sweep count on one rank: no per-sweep host synchronisation -- the sweep
-    # statistics go to a device log and failures to one first-failure word, both read
-    # once at the end (the per-sweep readback cost ~5 % of a c4 sweep)
-    nosync = cfg.fixed_sweeps > 0 and not P.comm.active
+    # fixed sweep count: no per-sweep host synchronisation -- the sweep statistics go to a
+    # device log and failures to one first-failure word, both read once at the end (the
+    # per-sweep readback cost ~5 % of a c4 sweep on one rank, more on a shard).  Row-sharded:
+    # the log holds this rank's partial sums and is all-reduced once, the failure word is
+    # the minimum over the ranks (any rank's failure is reported on every rank)
+    nosync = cfg.fixed_sweeps > 0
     if nosync:
         slog = P.buf(nsweeps, 3)
         fword = torch.full((1,), -1, dtype=torch.int64, device=P.dev)  # all ones
@@ -398,7 +400,7 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
     # side stream while the streaming product computes ctb, and the fixed-sweep statistics
     # run there behind the sweep (the kernels fit beside the persistent product kernels)
     side = None
-    if nosync and P.ftab_len and os.environ.get("NMFB_S1_FORK", "1") != "0":
+    if nosync and not P.comm.active and P.ftab_len and os.environ.get("NMFB_S1_FORK", "1") != "0":
         side = P.__dict__.get("_s1_side")
         if side is None:
             side = P._s1_side = torch.cuda.Stream(P.dev)
@@ -521,6 +523,11 @@ def run_stage1(P: Problem, X, Yt, cfg: Stage1Config | None = None, pX=None, pY=N
     if ev_stats is not None:
         torch.cuda.current_stream(P.dev).wait_event(ev_stats)
     if nosync and nsweeps > 0:
+        if P.comm.active:
+            P.comm.sum_(slog)
+            fword.masked_fill_(fword < 0, (1 << 63) - 1)  # "none" sorts last
+            P.comm.min_(fword)
+            fword.masked_fill_(fword == (1 << 63) - 1, -1)
         fw = int(fword.item()) & ((1 << 64) - 1)
         if fw != (1 << 64) - 1:
             tag, idx, code = fw >> 40, (fw >> 8) & 0xFFFFFFFF, fw & 0xFF
@@ -629,7 +636,7 @@ class IpmEngine:
         self.mu_dev = None  # [mu, wx mu, wy mu] read by the captured general-path kernels
         self.graph_pool = None
         self.capture_stream = None
-        self.use_graphs = p.use_graphs and not P.comm.active and not self.dense_gn
+        self.use_graphs = p.use_graphs and P.comm.graph_ok and not self.dense_gn
         # fused small-problem iteration (csrc/small.cu) for c1-c3-sized problems
         self.small = bool(P.lib.nmfb_small_supported(n, m, k)) and not P.comm.active \
             and not self.dense_gn and p.fused_small and not self.ffree

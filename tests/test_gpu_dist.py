@@ -154,9 +154,12 @@ def _nccl_one_rank_worker(port, M, X0, Y0, sweeps, iters, f32, q):
         Md = torch.as_tensor(M).cuda()
         if f32:
             Md = Md.float()
-        rep = solver.run_two_stage(Md, X0, Y0, tol_rel=1e-10,
+        P = solver.Problem(Md, X0.shape[1], comm=comm)
+        rep = solver.run_two_stage(None, X0, Y0, tol_rel=1e-10,
                                    s1=Stage1Config(fixed_sweeps=sweeps),
-                                   ipm=IpmParams(fixed_iters=iters), comm=comm)
+                                   ipm=IpmParams(fixed_iters=iters), comm=comm, problem=P)
+        # the Gauss-Newton iterations replay CUDA graphs with the NCCL collectives captured
+        assert comm.graph_ok and P.graph_kernel_launches > 0
         q.put((rep.X, rep.Yt, rep.stage1.sweeps, rep.ipm.armijo_t, rep.ipm.flags,
                rep.final_objective, rep.stage1.pX, rep.stage1.pY))
     finally:
