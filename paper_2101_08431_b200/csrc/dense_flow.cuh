@@ -66,36 +66,6 @@ __device__ __forceinline__ void flow_dmma(double& d0, double& d1, double a, doub
                : "d"(a), "d"(b));
 }
 
-// 32 x 32 diagonal factor, one warp, row r = lane in registers (the arithmetic of
-// BCholStep, chol_blk.cuh, on the lower triangle) with the pivot chain software-pipelined:
-// the next pivot a[J+1][J+1] - l^2 is formed from two shuffles issued before this step's
-// column updates and its rsqrt is in flight while the remaining 30 - J updates issue.
-template <int J>
-struct FlowChol {
-  static __device__ __forceinline__ void run(double (&a)[32], int r, double pv, double di,
-                                             int& fail, double& di_r) {
-    a[J] = (r == J) ? pv * di : ((r > J) ? a[J] * di : a[J]);
-    di_r = (r == J) ? di : di_r;
-    if constexpr (J + 1 < 32) {
-      const double l1 = __shfl_sync(0xffffffffu, a[J], J + 1);      // L[J+1][J]
-      const double d1 = __shfl_sync(0xffffffffu, a[J + 1], J + 1);  // A[J+1][J+1] so far
-      double pv1 = d1 - l1 * l1;
-      if (fail < 0 && !(pv1 > 0.0)) fail = J + 1;
-      if (fail >= 0) pv1 = 1.0;
-      const double di1 = rsqrt(pv1);
-      // column updates a[C] -= L[r][J] L[C][J], C > J: every broadcast first, then the
-      // FMAs (entries above the diagonal, r < C, collect unused values)
-      double l[32];
-#pragma unroll
-      for (int C = J + 2; C < 32; ++C) l[C] = __shfl_sync(0xffffffffu, a[J], C);
-      a[J + 1] = a[J + 1] - a[J] * l1;
-#pragma unroll
-      for (int C = J + 2; C < 32; ++C) a[C] = a[C] - a[J] * l[C];
-      FlowChol<J + 1>::run(a, r, pv1, di1, fail, di_r);
-    }
-  }
-};
-
 // min(prog[i], prog[j]) seen by thread 0, broadcast; < 0: abort
 __device__ __forceinline__ int flow_peek(int i, int j, int* sh) {
   if (threadIdx.x == 0) {
