@@ -284,8 +284,18 @@ struct TNnls {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   }
 
-  // _chol_solve_small (:247-258) on the passive indices
-  __device__ __forceinline__ void solve(unsigned pm, const double (&b)[K], double (&z)[K]) const {
+  // RN(a / b) from the correctly rounded reciprocal r = RN(1 / b) (Markstein): q0 = RN(a r),
+  // the exact residual a - b q0 by FMA, one correction -- three dependent operations on the
+  // substitution's critical chain instead of the division sequence; bit-identical to a / b
+  __device__ __forceinline__ static double mdiv(double a, double b, double r) {
+    const double q0 = a * r;
+    const double e = fma(-b, q0, a);
+    return fma(e, r, q0);
+  }
+
+  // _chol_solve_small (:247-258) on the passive indices; ri[i] = RN(1 / l(i, i))
+  __device__ __forceinline__ void solve(unsigned pm, const double (&b)[K], double (&z)[K],
+                                        const double (&ri)[K]) const {
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       double acc = b[i];
@@ -294,7 +304,7 @@ struct TNnls {
         const double t = acc - l(i, p) * z[p];
         acc = bit(pm, p) ? t : acc;
       }
-      z[i] = bit(pm, i) ? acc / l(i, i) : 0.0;
+      z[i] = bit(pm, i) ? mdiv(acc, l(i, i), ri[i]) : 0.0;
     }
     asm volatile("" ::: "memory");
 #pragma unroll
@@ -305,7 +315,7 @@ struct TNnls {
         const double t = acc - l(p, i) * z[p];
         acc = bit(pm, p) ? t : acc;
       }
-      z[i] = bit(pm, i) ? acc / l(i, i) : 0.0;
+      z[i] = bit(pm, i) ? mdiv(acc, l(i, i), ri[i]) : 0.0;
     }
   }
 
@@ -316,7 +326,12 @@ struct TNnls {
     // compiler memory barriers: the two solves re-read the factor instead of keeping
     // all K(K+1)/2 entries live in registers between them
     asm volatile("" ::: "memory");
-    solve(pm, d, z);
+    // the K reciprocal pivots of this subset's factor, independent of one another (their
+    // latencies overlap), shared by the four substitutions of the refined solve
+    double ri[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) ri[i] = bit(pm, i) ? __drcp_rn(l(i, i)) : 0.0;
+    solve(pm, d, z, ri);
     asm volatile("" ::: "memory");
     double r[K], dz[K];
 #pragma unroll
@@ -329,7 +344,7 @@ struct TNnls {
       }
       r[a] = acc;
     }
-    solve(pm, r, dz);
+    solve(pm, r, dz, ri);
 #pragma unroll
     for (int a = 0; a < K; ++a) z[a] = bit(pm, a) ? z[a] + dz[a] : 0.0;
   }
