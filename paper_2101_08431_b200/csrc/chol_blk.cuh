@@ -65,10 +65,14 @@ struct BCholStep<32> {
 template <int J>
 struct FlowChol {
   static __device__ __forceinline__ void run(double (&a)[32], int r, double pv, double di,
-                                             int& fail, double& di_r) {
+                                             int& fail, double& di_r, int nb = 32) {
     a[J] = (r == J) ? pv * di : ((r > J) ? a[J] * di : a[J]);
     di_r = (r == J) ? di : di_r;
     if constexpr (J + 1 < 32) {
+      if (J + 1 >= nb) {  // identity padding beyond an nb-wide block: nothing left to do
+        di_r = (r > J) ? 1.0 : di_r;
+        return;
+      }
       const double l1 = __shfl_sync(0xffffffffu, a[J], J + 1);      // L[J+1][J]
       const double d1 = __shfl_sync(0xffffffffu, a[J + 1], J + 1);  // A[J+1][J+1] so far
       double pv1 = d1 - l1 * l1;
@@ -83,10 +87,136 @@ struct FlowChol {
       a[J + 1] = a[J + 1] - a[J] * l1;
 #pragma unroll
       for (int C = J + 2; C < 32; ++C) a[C] = a[C] - a[J] * l[C];
-      FlowChol<J + 1>::run(a, r, pv1, di1, fail, di_r);
+      FlowChol<J + 1>::run(a, r, pv1, di1, fail, di_r, nb);
     }
   }
 };
+
+// ---------------------------------------------------------------------------
+// k_chol_one: N <= 128 (the k^2 x k^2 capacitance factors G and H of every c4 Gauss-Newton
+// iteration, N = 100) with the whole matrix resident in shared memory, one CTA: staged by
+// cp.async (every element in flight at once), per 32-column panel the diagonal block by one
+// warp (FlowChol: pivot chain software-pipelined), the rows below by pre-scaled sweeps (one
+// shuffle + one FMA per step, four rows per warp in flight) and the trailing update on the
+// FP64 tensor cores (DMMA m8n8k4, 8 x 8 tiles of the lower triangle over the warps; leading
+// dimension 132 = conflict-free fragment loads).
+// ---------------------------------------------------------------------------
+constexpr int CHOL_ONE_T = 256;
+constexpr int CHOL_ONE_LD = 132;
+inline size_t chol_one_smem() {
+  return (size_t)(128 * CHOL_ONE_LD + 32 * 33 + 32) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(CHOL_ONE_T) k_chol_one(double* __restrict__ Ag, int N,
+                                                         int* __restrict__ info, int fail_base,
+                                                         int skip_if_set, int set_ok) {
+  extern __shared__ double so[];
+  double* As = so;                       // [Np][LD], Np = N rounded up to 8
+  double* lj = so + 128 * CHOL_ONE_LD;   // strictly lower diagonal block, rows scaled by 1/L_rr
+  double* sdinv = lj + 32 * 33;
+  __shared__ int sfail;
+  if (skip_if_set && *info >= 0) return;
+  constexpr int LD = CHOL_ONE_LD;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int Np = (N + 7) & ~7;
+  // lower triangle (and the diagonal 32-blocks) in flight at once; one warp per row
+  for (int r = wid; r < Np; r += CHOL_ONE_T / 32) {
+    const int cend = min(Np, ((r >> 5) + 1) * 32);
+    for (int cc = lane; cc < cend; cc += 32) {
+      if (r < N && cc < N)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(As + r * LD + cc)),
+                     "l"(Ag + (long)r * N + cc)
+                     : "memory");
+      else
+        As[r * LD + cc] = 0.0;
+    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  if (tid == 0) sfail = -1;
+  __syncthreads();
+  const int g8 = lane >> 2, t4 = lane & 3;
+  for (int p0 = 0; p0 < N; p0 += 32) {
+    const int nb = min(32, N - p0);
+    if (wid == 0) {
+      double a[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        a[c] = (lane < nb && c < nb) ? As[(p0 + lane) * LD + p0 + c] : (lane == c ? 1.0 : 0.0);
+      int fail = -1;
+      double di = 0.0;
+      {
+        double pv = __shfl_sync(0xffffffffu, a[0], 0);
+        if (!(pv > 0.0)) fail = 0, pv = 1.0;
+        FlowChol<0>::run(a, lane, pv, rsqrt(pv), fail, di, nb);
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const double v = (c <= lane) ? a[c] : 0.0;
+        if (lane < nb && c < nb) As[(p0 + lane) * LD + p0 + c] = v;
+        lj[lane * 33 + c] = (c < lane) ? v * di : 0.0;
+      }
+      sdinv[lane] = di;
+      if (lane == 0 && fail >= 0 && fail < nb) sfail = p0 + fail;
+    }
+    __syncthreads();
+    if (sfail >= 0) break;
+    const int b0 = p0 + nb;
+    if (b0 >= N) break;
+    {  // rows below the block: x_c = a_c / L_cc - sum_{c' < c} x_c' L[c][c'] / L_cc
+      const double dl = sdinv[lane];
+      const double* lrow = lj + lane * 33;
+      for (int rb = b0 + 4 * wid; rb < Np; rb += 4 * (CHOL_ONE_T / 32)) {
+        double acc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = As[(rb + u) * LD + p0 + lane] * dl;
+#pragma unroll 8
+        for (int jj = 0; jj < 31; ++jj) {
+          const double lcj = lrow[jj];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            acc[u] = fma(-lcj, __shfl_sync(0xffffffffu, acc[u], jj), acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) As[(rb + u) * LD + p0 + lane] = acc[u];
+      }
+    }
+    __syncthreads();
+    {  // trailing update of the lower triangle [b0, Np)^2 in 8 x 8 tiles
+      const int nt = (Np - b0) >> 3;
+      const int ntile = nt * (nt + 1) / 2;
+      for (int tIdx = wid; tIdx < ntile; tIdx += CHOL_ONE_T / 32) {
+        int ti = (int)((sqrtf(8.0f * (float)tIdx + 1.0f) - 1.0f) * 0.5f);
+        while ((ti + 1) * (ti + 2) / 2 <= tIdx) ++ti;
+        while (ti * (ti + 1) / 2 > tIdx) --ti;
+        const int tj = tIdx - ti * (ti + 1) / 2;
+        const int r0 = b0 + 8 * ti, c0 = b0 + 8 * tj;
+        const double* fa = As + (r0 + g8) * LD + p0 + t4;
+        const double* fb = As + (c0 + g8) * LD + p0 + t4;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          asm volatile(
+              "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(d0), "+d"(d1)
+              : "d"(fa[4 * ks]), "d"(fb[4 * ks]));
+        double* o = As + (r0 + g8) * LD + c0 + 2 * t4;
+        o[0] -= d0;
+        o[1] -= d1;
+      }
+    }
+    __syncthreads();
+  }
+  const int f = sfail;
+  for (int r = wid; r < N; r += CHOL_ONE_T / 32)
+    for (int cc = lane; cc < N; cc += 32) Ag[(long)r * N + cc] = cc <= r ? As[r * LD + cc] : 0.0;
+  if (tid == 0) {
+    if (f >= 0)
+      *info = fail_base + f;
+    else if (set_ok)
+      *info = -1;
+  }
+}
 
 // warp 0: the nb x nb diagonal block at (p0, p0), padded to 32 with identity
 __device__ __noinline__ void chol_diag_block(double* A, long N, int p0, int nb, double* sd,
@@ -397,6 +527,17 @@ __global__ void __launch_bounds__(CHOL_COOP_THREADS) k_chol_coop(double* __restr
 // launch helper: one CTA for N <= 128, cooperative panels above
 inline int launch_chol(double* A, int N, int* info, int fail_base, int skip_if_set, int set_ok,
                        cudaStream_t st) {
+  static const bool one = [] {
+    const char* e = getenv("NMFB_CHOL_ONE");
+    return !(e && e[0] == '0');
+  }();
+  if (N <= 128 && one) {
+    const size_t sm = chol_one_smem();
+    nmfb_smem_attr(k_chol_one, sm);
+    ++g_nmfb_launches, k_chol_one<<<1, CHOL_ONE_T, sm, st>>>(A, N, info, fail_base, skip_if_set,
+                                                              set_ok);
+    return NMFB_OK;
+  }
   if (N <= 128) {
     const size_t sm = chol_blk_smem_staged(N);
     nmfb_smem_attr(k_chol_blk, sm);

@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(FLOW_T) k_chol_flow(double* __restrict__ A, in
         {
           double pv = __shfl_sync(0xffffffffu, a[0], 0);
           if (!(pv > 0.0)) fail = 0, pv = 1.0;
-          FlowChol<0>::run(a, lane, pv, rsqrt(pv), fail, di);
+          FlowChol<0>::run(a, lane, pv, rsqrt(pv), fail, di, nb);
         }
 #pragma unroll
         for (int c = 0; c < 32; ++c) tl[lane * FLOW_LDS + c] = (c <= lane) ? a[c] : 0.0;
