@@ -252,44 +252,54 @@ __device__ void cta_trsv(const double* L, int Q, double* b, int trans) {
     const int blk = trans ? (nblk - 1 - bb) : bb;
     const int c0 = blk * 32, nc = min(32, Q - c0);
     if (wid == 0) {
-      double v = lane < nc ? b[c0 + lane] : 0.0;
+      // the block's row (column) of this lane, strictly off the diagonal and pre-scaled by
+      // 1 / L_ll: a sweep step is then one shuffle and one FMA (no multiply, no select on
+      // the dependent chain)
       const double rl = lane < nc ? 1.0 / L[(c0 + lane) * Q + c0 + lane] : 0.0;
+      double v = lane < nc ? b[c0 + lane] * rl : 0.0;
       double lr[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        lr[j] = (lane < nc && j < nc) ? (trans ? L[(c0 + j) * Q + c0 + lane] : L[(c0 + lane) * Q + c0 + j])
-                                      : 0.0;
+      for (int j = 0; j < 32; ++j) {
+        const bool in = lane < nc && j < nc && (trans ? j > lane : j < lane);
+        lr[j] = in ? (trans ? L[(c0 + j) * Q + c0 + lane] : L[(c0 + lane) * Q + c0 + j]) * rl : 0.0;
+      }
       if (!trans) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (j >= nc) break;
-          const double zj = __shfl_sync(0xffffffffu, v * rl, j);
-          const double nv = v - lr[j] * zj;
-          v = (lane == j) ? zj : ((lane > j && lane < nc) ? nv : v);
-        }
+        for (int j = 0; j < 31; ++j) v = fma(-lr[j], __shfl_sync(0xffffffffu, v, j), v);
       } else {
 #pragma unroll
-        for (int j = 31; j >= 0; --j) {
-          if (j >= nc) continue;
-          const double zj = __shfl_sync(0xffffffffu, v * rl, j);
-          const double nv = v - lr[j] * zj;
-          v = (lane == j) ? zj : (lane < j ? nv : v);
-        }
+        for (int j = 31; j > 0; --j) v = fma(-lr[j], __shfl_sync(0xffffffffu, v, j), v);
       }
       if (lane < nc) b[c0 + lane] = v;
     }
     __syncthreads();
     if (!trans) {
-      for (int r = c0 + nc + tid; r < Q; r += blockDim.x) {
-        double acc = 0.0;
-        for (int c = 0; c < nc; ++c) acc = fma(L[r * Q + c0 + c], b[c0 + c], acc);
-        b[r] -= acc;
+      for (int r = c0 + nc + tid; r < Q; r += blockDim.x) {  // four partial sums: the FMA
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;         // chain is a quarter as deep
+        const double* lp = L + r * Q + c0;
+        int c = 0;
+        for (; c + 3 < nc; c += 4) {
+          s0 = fma(lp[c], b[c0 + c], s0);
+          s1 = fma(lp[c + 1], b[c0 + c + 1], s1);
+          s2 = fma(lp[c + 2], b[c0 + c + 2], s2);
+          s3 = fma(lp[c + 3], b[c0 + c + 3], s3);
+        }
+        for (; c < nc; ++c) s0 = fma(lp[c], b[c0 + c], s0);
+        b[r] -= (s0 + s1) + (s2 + s3);
       }
     } else {
       for (int c = tid; c < c0; c += blockDim.x) {
-        double acc = 0.0;
-        for (int r = 0; r < nc; ++r) acc = fma(L[(c0 + r) * Q + c], b[c0 + r], acc);
-        b[c] -= acc;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        const double* lp = L + c0 * Q + c;
+        int r = 0;
+        for (; r + 3 < nc; r += 4) {
+          s0 = fma(lp[r * Q], b[c0 + r], s0);
+          s1 = fma(lp[(r + 1) * Q], b[c0 + r + 1], s1);
+          s2 = fma(lp[(r + 2) * Q], b[c0 + r + 2], s2);
+          s3 = fma(lp[(r + 3) * Q], b[c0 + r + 3], s3);
+        }
+        for (; r < nc; ++r) s0 = fma(lp[r * Q], b[c0 + r], s0);
+        b[c] -= (s0 + s1) + (s2 + s3);
       }
     }
     __syncthreads();
@@ -338,10 +348,17 @@ __global__ void __launch_bounds__(256) k_lowrank_apply(const double* __restrict_
     if (lane == 0) a[r] = acc;
   }
   __syncthreads();
-  for (int r = tid; r < Q; r += blockDim.x) {  // b = LG^T a
-    double acc = 0.0;
-    for (int t = r; t < Q; ++t) acc = fma(LG[t * Q + r], a[t], acc);
-    b[r] = acc;
+  for (int r = tid; r < Q; r += blockDim.x) {  // b = LG^T a (four partial sums)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int t = r;
+    for (; t + 3 < Q; t += 4) {
+      s0 = fma(LG[t * Q + r], a[t], s0);
+      s1 = fma(LG[(t + 1) * Q + r], a[t + 1], s1);
+      s2 = fma(LG[(t + 2) * Q + r], a[t + 2], s2);
+      s3 = fma(LG[(t + 3) * Q + r], a[t + 3], s3);
+    }
+    for (; t < Q; ++t) s0 = fma(LG[t * Q + r], a[t], s0);
+    b[r] = (s0 + s1) + (s2 + s3);
   }
   __syncthreads();
   cta_trsv(LH, Q, b, 0);
