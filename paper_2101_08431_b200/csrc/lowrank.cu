@@ -200,43 +200,74 @@ __global__ void k_lr_unpack(const double* __restrict__ Zpk, const double* __rest
 // 32 x 32 output tile per CTA:
 //   mode 0: C = Zb L            (T1)
 //   mode 1: C = I - L^T T1      (H; only the lower triangle is consumed)
+// Both operands' 32-row strips over the whole contraction are staged at once by cp.async
+// (A as [row][t], B transposed as [column][t], leading dimension = 4 mod 16: conflict-free
+// fragment loads), then the tile is 2 DMMA m8n8k4 chains per warp.
+inline int lr_gemm_ld(int Q) {
+  const int kp = (Q + 3) & ~3;
+  return kp + ((4 - (kp & 15)) & 15);
+}
 __global__ void __launch_bounds__(256) k_lr_gemm(const double* __restrict__ Am,
                                                  const double* __restrict__ Bm, int Q, int mode,
                                                  double* __restrict__ C,
-                                                 const int* __restrict__ info) {
-  __shared__ double As[32][33], Bs[32][33];
+                                                 const int* __restrict__ info, int LDK) {
+  extern __shared__ double gsm[];
+  double* As = gsm;             // [32][LDK]
+  double* Bt = gsm + 32 * LDK;  // [32][LDK]
   if (*info >= 1000000) return;  // G already failed
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  for (int kk = 0; kk < Q; kk += 32) {
-    for (int e = tid; e < 32 * 32; e += 256) {
-      const int i = e >> 5, j = e & 31;
-      const int r = r0 + i, t = kk + j;
-      double av = 0.0;
-      if (r < Q && t < Q) av = mode == 0 ? Am[(long)r * Q + t] : Am[(long)t * Q + r];
-      As[i][j] = av;
-      const int tb = kk + i, c = c0 + j;
-      Bs[i][j] = (tb < Q && c < Q) ? Bm[(long)tb * Q + c] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int t = 0; t < 32; ++t) {
-      const double a0 = As[2 * ty][t], a1 = As[2 * ty + 1][t];
-      const double b0 = Bs[t][2 * tx], b1 = Bs[t][2 * tx + 1];
-      acc[0][0] = fma(a0, b0, acc[0][0]);
-      acc[0][1] = fma(a0, b1, acc[0][1]);
-      acc[1][0] = fma(a1, b0, acc[1][0]);
-      acc[1][1] = fma(a1, b1, acc[1][1]);
-    }
-    __syncthreads();
+  const int Kp = (Q + 3) & ~3;
+  for (int e = tid; e < 32 * Kp; e += 256) {
+    // A: (i, t) with t fastest for mode 0 (rows of Zb), i fastest for mode 1 (L^T)
+    const int i = mode == 0 ? e / Kp : e & 31;
+    const int t = mode == 0 ? e - i * Kp : e >> 5;
+    const int r = r0 + i;
+    double* da = As + i * LDK + t;
+    if (r < Q && t < Q)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(da)),
+                   "l"(mode == 0 ? Am + (long)r * Q + t : Am + (long)t * Q + r)
+                   : "memory");
+    else
+      *da = 0.0;
+    // B: (t, j) with j fastest (rows of B), stored transposed
+    const int jb = e & 31, tb = e >> 5;
+    const int c = c0 + jb;
+    double* db = Bt + jb * LDK + tb;
+    if (tb < Q && c < Q)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(db)),
+                   "l"(Bm + (long)tb * Q + c)
+                   : "memory");
+    else
+      *db = 0.0;
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int br = wid >> 1, bc0 = 2 * (wid & 1);
+  const double* fa = As + (8 * br + g8) * LDK + t4;
+  const double* fb0 = Bt + (8 * bc0 + g8) * LDK + t4;
+  const double* fb1 = fb0 + 8 * LDK;
+  double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+  for (int ks = 0; ks < Kp; ks += 4) {
+    const double a = fa[ks];
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c00), "+d"(c01)
+                 : "d"(a), "d"(fb0[ks]));
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c10), "+d"(c11)
+                 : "d"(a), "d"(fb1[ks]));
+  }
+  const int r = r0 + 8 * br + g8;
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
-      const int r = r0 + 2 * ty + u, c = c0 + 2 * tx + v;
-      if (r < Q && c < Q) C[(long)r * Q + c] = mode == 0 ? acc[u][v] : ((r == c ? 1.0 : 0.0) - acc[u][v]);
+      const int c = c0 + 8 * (bc0 + h) + 2 * t4 + v;
+      const double acc = h ? (v ? c11 : c10) : (v ? c01 : c00);
+      if (r < Q && c < Q) C[(long)r * Q + c] = mode == 0 ? acc : ((r == c ? 1.0 : 0.0) - acc);
     }
 }
 
@@ -407,8 +438,11 @@ extern "C" int nmfb_lowrank_factor(const double* Zpk, const double* Gpk, long k,
   (void)csm;
   launch_chol(LG, (int)Q, info, 1000000, 0, 0, st);
   const dim3 g((unsigned)((Q + 31) / 32), (unsigned)((Q + 31) / 32));
-  ++g_nmfb_launches, k_lr_gemm<<<g, 256, 0, st>>>(Zb, LG, (int)Q, 0, T1, info);
-  ++g_nmfb_launches, k_lr_gemm<<<g, 256, 0, st>>>(LG, T1, (int)Q, 1, LH, info);
+  const int ldk = lr_gemm_ld((int)Q);
+  const size_t gsm = (size_t)2 * 32 * ldk * sizeof(double);
+  nmfb_smem_attr(k_lr_gemm, gsm);
+  ++g_nmfb_launches, k_lr_gemm<<<g, 256, gsm, st>>>(Zb, LG, (int)Q, 0, T1, info, ldk);
+  ++g_nmfb_launches, k_lr_gemm<<<g, 256, gsm, st>>>(LG, T1, (int)Q, 1, LH, info, ldk);
   launch_chol(LH, (int)Q, info, 0, 1, 1, st);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
