@@ -378,30 +378,62 @@ __global__ void k_sum_parts(const double* __restrict__ part, int nparts, long le
 // ---------------------------------------------------------------------------
 constexpr int ATB_T = 64, ATB_R = 32, ATB_LD = 72;
 
+constexpr int ATB_S = 3;  // cp.async ring stages of ATB_R rows (both operands)
+constexpr size_t ATB_SMEM = (size_t)ATB_S * 2 * ATB_R * ATB_LD * sizeof(double);
+
 __global__ void __launch_bounds__(256) k_atb_mma(const double* __restrict__ A, long rows, long ca,
                                                  const double* __restrict__ B, long cb,
                                                  long stripe, double* __restrict__ part) {
-  __shared__ __align__(16) double sa[ATB_R * ATB_LD];
-  __shared__ __align__(16) double sb[ATB_R * ATB_LD];
+  extern __shared__ __align__(16) double atb_sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const long a0 = (long)blockIdx.x * ATB_T, b0 = (long)blockIdx.y * ATB_T;
   const long s = blockIdx.z;
   const long i_beg = s * stripe, i_end = min(rows, i_beg + stripe);
+  const int nchunk = (int)((i_end - i_beg + ATB_R - 1) / ATB_R);
+  // chunk c of the stripe into ring stage c % ATB_S: every element its own 8-byte cp.async
+  // (rows of ca / cb doubles are not 16-byte aligned in general), zeros outside the operands
+  auto issue = [&](int c) {
+    if (c < nchunk) {
+      double* sa = atb_sm + (size_t)(c % ATB_S) * 2 * ATB_R * ATB_LD;
+      double* sb = sa + ATB_R * ATB_LD;
+      const long ib = i_beg + (long)c * ATB_R;
+      const int nr = (int)min((long)ATB_R, i_end - ib);
+#pragma unroll
+      for (int q = 0; q < ATB_R * ATB_T / 256; ++q) {
+        const int e = tid + 256 * q;
+        const int r = e >> 6, cc = e & 63;
+        double* da = sa + r * ATB_LD + cc;
+        double* db = sb + r * ATB_LD + cc;
+        if (r < nr && a0 + cc < ca)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(da)),
+                       "l"(A + (ib + r) * ca + a0 + cc)
+                       : "memory");
+        else
+          *da = 0.0;
+        if (r < nr && b0 + cc < cb)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(db)),
+                       "l"(B + (ib + r) * cb + b0 + cc)
+                       : "memory");
+        else
+          *db = 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   double acc[8][2];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
-  for (long ib = i_beg; ib < i_end; ib += ATB_R) {
-    const int nr = (int)min((long)ATB_R, i_end - ib);
-    __syncthreads();
 #pragma unroll
-    for (int q = 0; q < ATB_R * ATB_T / 256; ++q) {
-      const int e = tid + 256 * q;
-      const int r = e >> 6, c = e & 63;
-      sa[r * ATB_LD + c] = (r < nr && a0 + c < ca) ? __ldg(A + (ib + r) * ca + a0 + c) : 0.0;
-      sb[r * ATB_LD + c] = (r < nr && b0 + c < cb) ? __ldg(B + (ib + r) * cb + b0 + c) : 0.0;
-    }
+  for (int c = 0; c < ATB_S - 1; ++c) issue(c);
+  for (int c = 0; c < nchunk; ++c) {
+    issue(c + ATB_S - 1);  // the stage it overwrites was read two iterations ago (barrier below)
+    asm volatile("cp.async.wait_group %0;" ::"n"(ATB_S - 1) : "memory");
     __syncthreads();
+    const double* sa = atb_sm + (size_t)(c % ATB_S) * 2 * ATB_R * ATB_LD;
+    const double* sb = sa + ATB_R * ATB_LD;
 #pragma unroll
     for (int kk = 0; kk < ATB_R / 4; ++kk) {
       const double af = sa[(4 * kk + t) * ATB_LD + 8 * warp + g];
@@ -411,6 +443,7 @@ __global__ void __launch_bounds__(256) k_atb_mma(const double* __restrict__ A, l
         dmma_f64(acc[j][0], acc[j][1], af, bf);
       }
     }
+    __syncthreads();
   }
   const long a = a0 + 8 * warp + g;
   if (a >= ca) return;
@@ -1313,7 +1346,8 @@ extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, lo
     if (ns * ca * cb <= work_len) {
       dim3 grid((unsigned)((ca + ATB_T - 1) / ATB_T), (unsigned)((cb + ATB_T - 1) / ATB_T),
                 (unsigned)ns);
-      ++g_nmfb_launches, k_atb_mma<<<grid, 256, 0, st>>>(A, rows, ca, B, cb, stripe, work);
+      nmfb_smem_attr(k_atb_mma, ATB_SMEM);
+      ++g_nmfb_launches, k_atb_mma<<<grid, 256, ATB_SMEM, st>>>(A, rows, ca, B, cb, stripe, work);
       ++g_nmfb_launches, k_sum_parts_warp<<<(unsigned)((ca * cb * 32 + 255) / 256), 256, 0, st>>>(
           work, (int)ns, ca * cb, out);
       NMFB_CHECK_LAUNCH();
