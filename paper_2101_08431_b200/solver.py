@@ -943,7 +943,7 @@ class IpmEngine:
                 _p(self.lrwork), self.m, self.k, _p(rhs), _p(dY), _p(self.uvec), _p(self.wvec),
                 _p(P.cwork), P.cwork.numel(), P.stream)
 
-    def direction(self, full, force_dense=False, rho=None):
+    def direction(self, full, force_dense=False, rho=None, early=False):
         """Newton direction; scalars land in dscal[4:7], codes in iscal[2:4].
 
         Gauss-Newton coupling: exact low-rank solve of the reduced system
@@ -1022,6 +1022,15 @@ class IpmEngine:
             # tile row, csrc/dense_flow.cuh), then the backward half
             dY.copy_(self.rhs.view(m, k))
             P._call("nmfb_dense_cholesky_rhs", _p(self.A), N, _p(dY), _p(P.iscal[3:]), s)
+            if early:
+                # inertia tries (frozen semantics 10): two of three fail in the factorization;
+                # read its code now and skip the back substitution and the direction kernels
+                _, iv = P.readback(0, 4)
+                if int(iv[2]) != _NONE:
+                    raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
+                if int(iv[3]) >= 0:
+                    self.last_dense = dense
+                    return None
             P._call("nmfb_dense_solve_back", _p(self.A), N, _p(dY), s)
         else:
             if fork:
@@ -1214,13 +1223,14 @@ def _run_ipm(P: Problem, eng, p: IpmParams, t0):
                 # flag on the first non-PD / non-descent direction, "inertia" shifts rho
                 delta = 0.0
                 for _ in range(1 if p.hessian == "paper" else INERTIA_MAX_TRIES):
-                    dY = eng.direction(True, rho=eng.rho + delta)
-                    v, iv = P.readback(9, 4)
-                    if int(iv[2]) != _NONE:
-                        raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
-                    if int(iv[3]) < 0 and v[4] < 0.0:
-                        ok, used_full = True, True
-                        break
+                    dY = eng.direction(True, rho=eng.rho + delta, early=True)
+                    if dY is not None:  # None: the shifted Schur matrix did not factor
+                        v, iv = P.readback(9, 4)
+                        if int(iv[2]) != _NONE:
+                            raise NotPositiveDefinite("R1 block not positive definite", int(iv[2]))
+                        if int(iv[3]) < 0 and v[4] < 0.0:
+                            ok, used_full = True, True
+                            break
                     delta = (delta * INERTIA_GROW if delta > 0.0 else
                              (delta_last / INERTIA_SHRINK if delta_last > 0.0 else eng.rho))
                 if ok:
