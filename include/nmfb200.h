@@ -228,6 +228,16 @@ int nmfb_step_nudge_flag(double *v, const double *dv, long len, const double *al
 int nmfb_ffree_advance(double *MY, const double *MdY, long nlen, double *MX, const double *MtdX,
                        long mlen, const double *alpha_dev, double alpha, const int *flag,
                        void *stream);
+/* The whole update of SPEC.md:359 in one launch: x, y += a1 (dx, dy) with the nudge rule (a
+ * nudged entry ORs 1 into *flag when flag != NULL), r, s += a2 (dr, ds), and, when MY / MX are
+ * given (residual-free dual mode), M Y^T += a1 M dY^T and M^T X += a1 M^T dX (the caller
+ * recomputes both after a nudged step).  a1 / a2 from device memory when the pointer is
+ * not NULL. */
+int nmfb_step_all(double *X, const double *dX, long nk, double *Y, const double *dY, long mk,
+                  double *R, const double *dR, double *S, const double *dS, double *MY,
+                  const double *MdY, double *MX, const double *MtdX, const double *a1_dev,
+                  double a1, const double *a2_dev, double a2, double tau, int *flag,
+                  void *stream);
 /* as nmfb_step_nudge with alpha read from device memory */
 int nmfb_step_nudge_dev(double *v, const double *dv, long len, const double *alpha, double tau,
                         void *stream);

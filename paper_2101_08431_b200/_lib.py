@@ -61,6 +61,7 @@ SIGNATURES = {
     "nmfb_step_nudge_dev": [P, P, L, P, D, P],
     "nmfb_step_nudge_flag": [P, P, L, P, D, D, P, P],
     "nmfb_ffree_advance": [P, P, L, P, P, L, P, D, P, P],
+    "nmfb_step_all": [P, P, L, P, P, L, P, P, P, P, P, P, P, P, P, D, P, D, D, P, P],
     "nmfb_kkt_sums": [P, P, P, L, P, P, P, L, D, D, P, P, P],
     "nmfb_affine_mu": [P, P, P, P, L, P, P, P, P, L, D, D, P, P, P],
     "nmfb_clamp_min": [P, L, D, P],

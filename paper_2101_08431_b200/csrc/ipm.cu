@@ -1134,6 +1134,41 @@ __global__ void k_ffree_advance(double* __restrict__ MY, const double* __restric
   }
 }
 
+// The whole update (SPEC.md:359 nudge rule) in one launch: x, y += a1 (dx, dy) with the
+// nudge flag, r, s += a2 (dr, ds), and (residual-free dual mode) the incremental advance of
+// M Y^T / M^T X -- unconditional: a nudged step makes the host recompute both from M
+// (solver.check_advance), which overwrites them.  Segments [X | Y | R | S | MY | MX].
+struct StepAll {
+  double* v[6];
+  const double* dv[6];
+  long len[6];
+};
+__global__ void __launch_bounds__(256) k_step_all(StepAll sa, const double* __restrict__ a1_dev,
+                                                  double a1, const double* __restrict__ a2_dev,
+                                                  double a2, double tau, int* __restrict__ flag) {
+  const double s1 = a1_dev ? *a1_dev : a1, s2 = a2_dev ? *a2_dev : a2;
+  const long o1 = sa.len[0], o2 = o1 + sa.len[1], o3 = o2 + sa.len[2], o4 = o3 + sa.len[3],
+             o5 = o4 + sa.len[4], o6 = o5 + sa.len[5];
+  int nudged = 0;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < o6;
+       e += (long)gridDim.x * blockDim.x) {
+    const int q = e < o1 ? 0 : e < o2 ? 1 : e < o3 ? 2 : e < o4 ? 3 : e < o5 ? 4 : 5;
+    const long i = e - (q == 0 ? 0 : q == 1 ? o1 : q == 2 ? o2 : q == 3 ? o3 : q == 4 ? o4 : o5);
+    double* v = sa.v[q];
+    const double d = sa.dv[q][i];
+    if (q >= 4) {
+      v[i] = fma(s1, d, v[i]);
+    } else {
+      const double old = v[i];
+      const double nv = old + (q < 2 ? s1 : s2) * d;
+      const bool ok = nv > 0.0;
+      v[i] = ok ? nv : (1.0 - tau) * old;
+      nudged |= (q < 2) && !ok;
+    }
+  }
+  if (flag != nullptr && __syncthreads_or(nudged) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 constexpr int RED_BLOCKS = 296;  // fixed -> deterministic reductions
 
 // ---------------------------------------------------------------------------
@@ -1634,6 +1669,25 @@ extern "C" int nmfb_ffree_advance(double* MY, const double* MdY, long nlen, doub
   if (nlen + mlen <= 0) return NMFB_OK;
   ++g_nmfb_launches, k_ffree_advance<<<nmfb_blocks(nlen + mlen, 256, 148 * 8), 256, 0, st>>>(
       MY, MdY, nlen, MX, MtdX, mlen, alpha_dev, alpha, flag);
+  NMFB_CHECK_LAUNCH();
+  return NMFB_OK;
+}
+
+extern "C" int nmfb_step_all(double* X, const double* dX, long nk, double* Y, const double* dY,
+                             long mk, double* R, const double* dR, double* S, const double* dS,
+                             double* MY, const double* MdY, double* MX, const double* MtdX,
+                             const double* a1_dev, double a1, const double* a2_dev, double a2,
+                             double tau, int* flag, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  StepAll sa;
+  double* v[6] = {X, Y, R, S, MY, MX};
+  const double* dv[6] = {dX, dY, dR, dS, MdY, MtdX};
+  const long len[6] = {nk, mk, nk, mk, MY ? nk : 0, MX ? mk : 0};
+  long tot = 0;
+  for (int q = 0; q < 6; ++q) sa.v[q] = v[q], sa.dv[q] = dv[q], sa.len[q] = len[q], tot += len[q];
+  if (tot <= 0) return NMFB_OK;
+  ++g_nmfb_launches, k_step_all<<<nmfb_blocks(tot, 256, 148 * 8), 256, 0, st>>>(
+      sa, a1_dev, a1, a2_dev, a2, tau, flag);
   NMFB_CHECK_LAUNCH();
   return NMFB_OK;
 }

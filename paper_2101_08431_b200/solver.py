@@ -764,29 +764,19 @@ class IpmEngine:
         then reports it and the host recomputes them, see run_ipm)."""
         P, p = self.P, self.p
         n, m, k, s = self.n, self.m, self.k, P.stream
+        fl = my = mdy = mx = mtdx = None
         if self.ffree and self.dual:
             P.iscal[5:6].zero_()
-            fl = _p(P.iscal[5:])
-            P._call("nmfb_step_nudge_flag", _p(self.X), _p(self.dX), n * k, _p(a1_dev), a1, p.tau,
-                    fl, s)
-            P._call("nmfb_step_nudge_flag", _p(self.Yt), _p(dY), m * k, _p(a1_dev), a1, p.tau,
-                    fl, s)
-            if self.comm.active:  # a nudge on any rank invalidates the reduced M^T X
-                self.comm.max_(P.iscal[5:6])
-            P._call("nmfb_ffree_advance", _p(self.fws["MY"]), _p(self.MdY), n * k,
-                    _p(self.fws["MX"]), _p(self.MtdX), m * k, _p(a1_dev), a1, fl, s)
-        elif a1_dev is not None:
-            P._call("nmfb_step_nudge_dev", _p(self.X), _p(self.dX), n * k, _p(a1_dev), p.tau, s)
-            P._call("nmfb_step_nudge_dev", _p(self.Yt), _p(dY), m * k, _p(a1_dev), p.tau, s)
-        else:
-            P._call("nmfb_step_nudge", _p(self.X), _p(self.dX), n * k, a1, p.tau, s)
-            P._call("nmfb_step_nudge", _p(self.Yt), _p(dY), m * k, a1, p.tau, s)
-        if a2_dev is not None:
-            P._call("nmfb_step_nudge_dev", _p(self.R), _p(self.dR), n * k, _p(a2_dev), p.tau, s)
-            P._call("nmfb_step_nudge_dev", _p(self.S), _p(self.dS), m * k, _p(a2_dev), p.tau, s)
-        else:
-            P._call("nmfb_step_nudge", _p(self.R), _p(self.dR), n * k, a2, p.tau, s)
-            P._call("nmfb_step_nudge", _p(self.S), _p(self.dS), m * k, a2, p.tau, s)
+            fl = P.iscal[5:]
+            my, mdy, mx, mtdx = self.fws["MY"], self.MdY, self.fws["MX"], self.MtdX
+        # one launch: x, y (nudge flag), r, s and the incremental M Y^T / M^T X advance (a
+        # nudged step recomputes them: check_advance)
+        P._call("nmfb_step_all", _p(self.X), _p(self.dX), n * k, _p(self.Yt), _p(dY), m * k,
+                _p(self.R), _p(self.dR), _p(self.S), _p(self.dS), _p(my), _p(mdy), _p(mx),
+                _p(mtdx), _p(a1_dev), float(a1 or 0.0), _p(a2_dev), float(a2 or 0.0), p.tau,
+                _p(fl), s)
+        if fl is not None and self.comm.active:  # a nudge on any rank invalidates M^T X
+            self.comm.max_(P.iscal[5:6])
 
     def check_advance(self, flag=None):
         """After a residual-free dual-mode step: if an entry was nudged (iscal[5], or the
