@@ -268,7 +268,9 @@ int nmfb_dense_solve(const double *L, long N, double *b, void *stream);
  * row of the dataflow Cholesky, csrc/dense_flow.cuh), then nmfb_dense_solve_back finishes
  * b <- L^{-T} b: the spd_solve of SPEC.md:68 for the full-coupling directions, whose
  * right-hand side is known before the factorization.  nmfb_dense_solve_mode: 1 forward,
- * 2 backward, 3 both, with an existing factor (the predictor's reuse). */
+ * 2 backward, 3 both, with an existing factor (the predictor's reuse).
+ * The dense factor / solve entries keep their scratch in device globals: call them from one
+ * stream at a time per process. */
 int nmfb_dense_cholesky_rhs(double *A, long N, double *b, int *info, void *stream);
 int nmfb_dense_solve_back(const double *L, long N, double *b, void *stream);
 int nmfb_dense_solve_mode(const double *L, long N, double *b, int mode, void *stream);

@@ -22,6 +22,10 @@
 //
 // Every spin is bounded (clock64 budget): a broken dependency raises the abort word and
 // the factorization reports failure instead of hanging the device.
+//
+// The progress counters, reciprocal pivots and solution scratch are device globals (as
+// g_coop_scratch of the panel kernel: no allocation inside CUDA-graph capture), re-armed by
+// stream-ordered memsets before each launch: launches on ONE stream at a time per process.
 #pragma once
 #include <cooperative_groups.h>
 
