@@ -584,6 +584,120 @@ __global__ void __launch_bounds__(256) k_schur_term4(const double* __restrict__ 
   }
 }
 
+// The same contraction on the FP64 tensor cores for K <= 4 (c1-c3, KK = K(K+1)/2 <= 10):
+// per pq the tile is F_j^T diag(a_i[pq]) F_l, i.e. KK weighted SYRK/GEMMs that share both
+// operand fragments.  CTA = 32 x 32 tile of (j, l) (lower tiles only) x a row split; warp =
+// two 8 x 8 blocks x KK accumulator pairs; per contraction step of 4 rows: one fragment of
+// F_j, two of F_l, KK weights, KK multiplies and 2 KK DMMA m8n8k4.  Rows staged in 32-row
+// chunks by cp.async (double-buffered, leading dimension 36 = conflict-free fragments).
+constexpr int T4M_LD = 36;
+template <int K>
+__global__ void __launch_bounds__(256) k_schur_term4_mma(const double* __restrict__ F, long n, long m,
+                                                         const double* __restrict__ Apk,
+                                                         double* __restrict__ A, int nsplit,
+                                                         double* __restrict__ part) {
+  constexpr int KK = K * (K + 1) / 2;
+  constexpr int KP = (KK + 1) & ~1;  // padded weight row
+  __shared__ __align__(16) double fj[2][32 * T4M_LD], fl[2][32 * T4M_LD], ap[2][32 * KP];
+  const long tj = blockIdx.x, tl = blockIdx.y;
+  if (tj < tl) return;
+  const int zs = blockIdx.z;
+  const long rps = (((n + nsplit - 1) / nsplit) + 31) / 32 * 32;
+  const long i_beg = zs * rps, i_end = min(n, i_beg + rps);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int bj = wid >> 1, bl0 = 2 * (wid & 1);
+  const long j0 = tj * 32, l0 = tl * 32;
+  const int nchunk = i_end > i_beg ? (int)((i_end - i_beg + 31) / 32) : 0;
+  auto issue = [&](int c) {
+    if (c < nchunk) {
+      const int st = c & 1;
+      const long ib = i_beg + 32L * c;
+      const int nr = (int)min(32L, i_end - ib);
+      for (int e = tid; e < 32 * 32; e += 256) {
+        const int r = e >> 5, cc = e & 31;
+        double* dj = &fj[st][r * T4M_LD + cc];
+        double* dl = &fl[st][r * T4M_LD + cc];
+        if (r < nr && j0 + cc < m)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(dj)),
+                       "l"(F + (ib + r) * m + j0 + cc)
+                       : "memory");
+        else
+          *dj = 0.0;
+        if (r < nr && l0 + cc < m)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(dl)),
+                       "l"(F + (ib + r) * m + l0 + cc)
+                       : "memory");
+        else
+          *dl = 0.0;
+      }
+      for (int e = tid; e < 32 * KK; e += 256) {
+        const int r = e / KK, cc = e - r * KK;
+        double* da = &ap[st][r * KP + cc];
+        if (r < nr)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(da)),
+                       "l"(Apk + (ib + r) * KK + cc)
+                       : "memory");
+        else
+          *da = 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[2][KK][2];
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+#pragma unroll
+    for (int c = 0; c < KK; ++c) acc[b][c][0] = acc[b][c][1] = 0.0;
+  issue(0);
+  for (int c = 0; c < nchunk; ++c) {
+    issue(c + 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const int st = c & 1;
+    const double* pj = &fj[st][t4 * T4M_LD + 8 * bj + g8];
+    const double* pl = &fl[st][t4 * T4M_LD + 8 * bl0 + g8];
+    const double* pa = &ap[st][t4 * KP];
+#pragma unroll 2
+    for (int ks = 0; ks < 8; ++ks) {
+      const double a = pj[4 * ks * T4M_LD];
+      const double b0 = pl[4 * ks * T4M_LD], b1 = pl[4 * ks * T4M_LD + 8];
+#pragma unroll
+      for (int q = 0; q < KK; ++q) {
+        const double aw = a * pa[4 * ks * KP + q];
+        dmma_f64(acc[0][q][0], acc[0][q][1], aw, b0);
+        dmma_f64(acc[1][q][0], acc[1][q][1], aw, b1);
+      }
+    }
+    __syncthreads();
+  }
+  const long N = m * K;
+  const long j = j0 + 8 * bj + g8;
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const long l = l0 + 8 * (bl0 + b) + 2 * t4 + v;
+      if (j >= m || l >= m || j < l) continue;
+      if (nsplit > 1) {
+#pragma unroll
+        for (int q = 0; q < KK; ++q) part[((long)zs * m * m + j * m + l) * KK + q] = acc[b][q][v];
+      } else {
+        int p = 0, e = 0;
+#pragma unroll
+        for (int q = 0; q < KK; ++q) {  // pq -> (p, qq), p <= qq, in packed order
+          const int qq = p + e;
+          A[(j * K + p) * N + l * K + qq] -= acc[b][q][v];
+          if (p != qq) A[(j * K + qq) * N + l * K + p] -= acc[b][q][v];
+          if (++e >= K - p) e = 0, ++p;
+        }
+      }
+    }
+}
+
 template <int K>
 __global__ void k_term4_finish(const double* __restrict__ part, long m, int nsplit,
                                double* __restrict__ A) {
@@ -1454,6 +1568,23 @@ extern "C" int nmfb_schur_assemble(const double* Yt, const double* S, long m, lo
   return NMFB_OK;
 }
 
+static int term4_mma_nsplit(long n, long m) {
+  const long t32 = (m + 31) / 32;
+  const long active = t32 * (t32 + 1) / 2;
+  long ns = (148 * 2 + active - 1) / active;
+  const long maxs = (n + 255) / 256;
+  if (ns > maxs) ns = maxs;
+  if (ns > 32) ns = 32;
+  return ns < 1 ? 1 : (int)ns;
+}
+static bool term4_use_mma(long k) {
+  static const bool on = [] {
+    const char* e = getenv("NMFB_TERM4_MMA");
+    return !(e && e[0] == '0');
+  }();
+  return on && k <= 4;
+}
+
 static int term4_nsplit(long n, long m, long k) {
   const long kk = k * (k + 1) / 2;
   const long tiles = (m + 15) / 16;
@@ -1466,7 +1597,8 @@ static int term4_nsplit(long n, long m, long k) {
 }
 
 extern "C" long nmfb_term4_work_len(long n, long m, long k) {
-  const int ns = term4_nsplit(n, m, k);
+  int ns = term4_nsplit(n, m, k);
+  if (k <= 4) ns = max(ns, term4_mma_nsplit(n, m));
   return ns > 1 ? (long)ns * m * m * (k * (k + 1) / 2) : 1;
 }
 
@@ -1474,6 +1606,26 @@ extern "C" int nmfb_schur_term4(const double* F, long n, long m, long k, const d
                                 double* A, double* work, long work_len, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const long kk = k * (k + 1) / 2;
+  if (term4_use_mma(k)) {  // K <= 4: weighted SYRKs on the FP64 tensor cores
+    int ns = term4_mma_nsplit(n, m);
+    if (ns > 1 && (long)ns * m * m * kk > work_len) ns = 1;
+    const long t32 = (m + 31) / 32;
+    dim3 grid((unsigned)t32, (unsigned)t32, (unsigned)ns);
+#define CASEM(KK)                                                                              \
+  case KK:                                                                                     \
+    ++g_nmfb_launches, k_schur_term4_mma<KK><<<grid, 256, 0, st>>>(F, n, m, Apk, A, ns, work); \
+    if (ns > 1)                                                                                \
+      ++g_nmfb_launches, k_term4_finish<KK><<<(unsigned)((m * m * kk + 255) / 256), 256, 0, st>>>( \
+          work, m, ns, A);                                                                     \
+    break;
+    switch (k) {
+      CASEM(1) CASEM(2) CASEM(3) CASEM(4)
+      default: return NMFB_EINVAL;
+    }
+#undef CASEM
+    NMFB_CHECK_LAUNCH();
+    return NMFB_OK;
+  }
   const long tiles = (m + 15) / 16;
   int ns = term4_nsplit(n, m, k);
   if (ns > 1 && (long)ns * m * m * kk > work_len) ns = 1;

@@ -145,7 +145,8 @@ def test_ipm_parity(mods, name, barrier, iters, eps, solve, resid, tol):
     assert r.flags == ro2.flags
     for a, b in ((eng.X, ro2.state.X), (eng.Yt, ro2.state.Yt)):
         assert rel(a.cpu().numpy(), b) < tol
-    assert abs(eng.mu - ro2.state.mu) <= tol * ro2.state.mu
+    # mu = sigma mu with sigma = (mu_aff / mu)^3: a relative deviation of the iterate is cubed
+    assert abs(eng.mu - ro2.state.mu) <= 5.0 * tol * ro2.state.mu
     if eps == 1e-5:
         assert any(r.flags), "the full-Hessian path was not exercised"
 
