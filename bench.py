@@ -396,6 +396,39 @@ def run_b200(args):
     traffic, traffic_src = _ncu_traffic()
     if traffic is not None and ws > 1:
         traffic = traffic * rows / cfg.n
+    # the other two streaming kernels of the step, timed alone on the resident M (larger than
+    # L2) with CUDA events: X^T M of every Y-update and the one-pass dual product of every
+    # IPM iteration (both read M once: the same algorithmic bytes)
+    others = []
+    try:
+        def _ev_time(fn, reps=10):
+            fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+            e1.synchronize()
+            return e0.elapsed_time(e1) / reps
+
+        oR, oC = P.buf(rows, cfg.k), P.buf(cfg.m, cfg.k)
+        tolc = P.buf(cfg.m)
+        ms_col = _ev_time(lambda: P.colprod(P.M, rows, cfg.m, X0d, cfg.k, oC, tolc, P.f32))
+        dwork = P.buf(P.lib.nmfb_dualprod_work_len(rows, cfg.m, cfg.k))
+        ms_dual = _ev_time(lambda: P.dualprod(Yt0d, X0d, oR, oC, dwork, reduce=False))
+        for kern, ms_k, what in (
+                ("k_colprod_tma + its fixed-order partial sum (nmfb_colprod)", ms_col,
+                 "ctb = X^T M of every Y-update"),
+                ("k_dualprod_tma + partial sums (nmfb_dualprod)", ms_dual,
+                 "M dY^T and M^T dX from one read of M (every IPM iteration); 4 rows m k flops: "
+                 "bound by FP64 operand traffic at k = 10, 186 us at k = 8")):
+            ach = nbytes / (ms_k * 1e-3) / 1e9
+            others.append({"kernel": kern, "what": what, "avg_ms": ms_k, "achieved": ach,
+                           "unit": "GB/s", "peak": peaks["hbm_gbs"], "frac": ach / peaks["hbm_gbs"],
+                           "algorithmic_bytes": nbytes, "launches": 10})
+    except Exception as exc:  # noqa: BLE001
+        others = [{"error": f"{type(exc).__name__}: {exc}"[:200]}]
     serial = {"value": e2e_units / (e2e_ms / 1e3), "ms_per_step": e2e_ms / ne2e, "steps": ne2e,
               "how": "public run_two_stage(M_host, X0, Y0, problem=P): P allocated once "
                      "outside the timed region, M (800 MB) copied from pinned host memory "
@@ -444,6 +477,7 @@ def run_b200(args):
                      "timing": "CUDA events on the launching stream around every launch of "
                                "the entry in the timed steps' stage 1 (M Y^T of each X-update; "
                                "the IPM's launches of the same kernel run inside CUDA graphs)"},
+        "roofline_other_kernels": others,
         "fp64_dgemm_tflops_measured": fp64_peak,
         "gpu_launches": int(launches),
         "clocks": clk,
