@@ -296,14 +296,15 @@ struct TNnls {
   // _chol_solve_small (:247-258) on the passive indices; ri[i] = RN(1 / l(i, i))
   __device__ __forceinline__ void solve(unsigned pm, const double (&b)[K], double (&z)[K],
                                         const double (&ri)[K]) const {
+    // A non-passive index p contributes l * z[p] = (+0) * (+0): the subset table holds
+    // exact zeros off the passive rows / columns (WNnls::factor starts from Lr = 0) and
+    // z[p] is +0, and acc - (+0) == acc bit for bit -- so the reference's skip of
+    // non-passive positions needs no select on the dependent chain.
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       double acc = b[i];
 #pragma unroll
-      for (int p = 0; p < i; ++p) {
-        const double t = acc - l(i, p) * z[p];
-        acc = bit(pm, p) ? t : acc;
-      }
+      for (int p = 0; p < i; ++p) acc = acc - l(i, p) * z[p];
       z[i] = bit(pm, i) ? mdiv(acc, l(i, i), ri[i]) : 0.0;
     }
     asm volatile("" ::: "memory");
@@ -311,10 +312,7 @@ struct TNnls {
     for (int i = K - 1; i >= 0; --i) {
       double acc = z[i];
 #pragma unroll
-      for (int p = i + 1; p < K; ++p) {
-        const double t = acc - l(p, i) * z[p];
-        acc = bit(pm, p) ? t : acc;
-      }
+      for (int p = i + 1; p < K; ++p) acc = acc - l(p, i) * z[p];
       z[i] = bit(pm, i) ? mdiv(acc, l(i, i), ri[i]) : 0.0;
     }
   }
@@ -338,10 +336,7 @@ struct TNnls {
     for (int a = 0; a < K; ++a) {
       double acc = d[a];
 #pragma unroll
-      for (int b = 0; b < K; ++b) {
-        const double t = acc - C[a * K + b] * z[b];
-        acc = bit(pm, b) ? t : acc;
-      }
+      for (int b = 0; b < K; ++b) acc = acc - C[a * K + b] * z[b];  // z[b] = +0 off the passive set
       r[a] = acc;
     }
     solve(pm, r, dz, ri);
