@@ -281,7 +281,11 @@ struct TNnls {
                          base + (unsigned)(tri(i, j) * TS * sizeof(double))),
                      "l"(Lg + i * K + j)
                      : "memory");
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  // the staged factor is complete (no-op for the in-place table)
+  __device__ __forceinline__ void stage_wait() const {
+    if (STAGED) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   }
 
   // RN(a / b) from the correctly rounded reciprocal r = RN(1 / b) (Markstein): q0 = RN(a r),
@@ -318,9 +322,11 @@ struct TNnls {
   }
 
   // _passive_solve_refined (:261-274): z = solve(d); r = d - C_PP z; z += solve(r)
+  // staged == true: the caller already issued stage(T, pm) (beside its own loads)
   __device__ __forceinline__ void solve_refined(const double* __restrict__ T, unsigned pm,
-                                                double (&z)[K]) {
-    stage(T, pm);
+                                                double (&z)[K], bool staged = false) {
+    if (!staged) stage(T, pm);
+    stage_wait();
     // compiler memory barriers: the two solves re-read the factor instead of keeping
     // all K(K+1)/2 entries live in registers between them
     asm volatile("" ::: "memory");
@@ -380,8 +386,10 @@ __device__ __forceinline__ void tnnls_solve(TNnls<K, STAGED>& s, const double* _
         for (int j = 0; j < K; ++j) x[j] = 0.0;
         solved = true;
       }
-    } else if (okf[pm] != 0.0) {
-      s.solve_refined(T, pm, z);
+    } else if (s.stage(T, pm), okf[pm] == 0.0) {  // factor copy and the PD word in flight together
+      s.stage_wait();  // not PD: drain the copy before the cold start restages the slot
+    } else {
+      s.solve_refined(T, pm, z, true);
       bool feas = true;
 #pragma unroll
       for (int a = 0; a < K; ++a) feas = feas && !(TN::bit(pm, a) && z[a] < 0.0);
@@ -423,11 +431,13 @@ __device__ __forceinline__ void tnnls_solve(TNnls<K, STAGED>& s, const double* _
       }
       for (;;) {
         if (pm == 0u) break;
+        s.stage(T, pm);  // the subset's factor on its way while its PD word is read
         if (okf[pm] == 0.0) {
+          s.stage_wait();
           st = 2;
           break;
         }
-        s.solve_refined(T, pm, z);
+        s.solve_refined(T, pm, z, true);
         bool all_pos = true;
 #pragma unroll
         for (int a = 0; a < K; ++a) all_pos = all_pos && !(TN::bit(pm, a) && z[a] <= 0.0);
