@@ -87,3 +87,16 @@ def test_sharded_two_stage_matches_single(barrier):
         assert abs(r[10] - ref.objective) <= 1e-9 * ref.objective
     assert np.array_equal(pX, ref.stage1.pX)
     assert np.abs(X - ref.X).max() <= 1e-8 * np.abs(ref.X).max()
+
+
+def test_comm_flags_without_a_process_group():
+    """Comm.single() is inactive and graph-capturable; a forced one-rank communicator is
+    active (every collective of the sharded path is issued) and splits rows trivially."""
+    from paper_2101_08431_b200.dist import Comm, row_range
+
+    c = Comm.single()
+    assert not c.active and c.root and c.graph_ok
+    f = Comm(None, 1, 0, force=True)
+    assert f.active and f.root and f.world == 1
+    assert row_range(10, 1, 0) == (0, 10)
+    assert [row_range(10, 3, r) for r in range(3)] == [(0, 4), (4, 7), (7, 10)]
