@@ -766,7 +766,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             dmma(racc[nt][0], racc[nt][1], a.x, bx);
             dmma(racc2[nt][0], racc2[nt][1], a.y, by);
           }
-          if (TL > 0) {
+          if (TL == 2) {  // both tail records of the pair in two 16-byte loads (TP = 2)
+            const double* tr = c.sT + ((q * 4 + t) * 2) * TP;
+            const double2 t0 = lds128(tr), t1 = lds128(tr + 2);
+            rtacc[0] = fma(a.x, t0.x, rtacc[0]);
+            rtacc[1 % TLA] = fma(a.x, t0.y, rtacc[1 % TLA]);
+            rtacc2[0] = fma(a.y, t1.x, rtacc2[0]);
+            rtacc2[1 % TLA] = fma(a.y, t1.y, rtacc2[1 % TLA]);
+          } else if (TL > 0) {
             const double* tr = c.sT + ((q * 4 + t) * 2) * TP;
 #pragma unroll
             for (int j = 0; j < TLA; ++j) {
@@ -819,7 +826,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               dmma(u[0][nt][0], u[0][nt][1], a1.x, b1[nt]);
               dmma(u[1][nt][0], u[1][nt][1], a1.y, b1[nt]);
             }
-            if (TL > 0) {
+            if (TL == 2 && bfull) {  // K = 10: the two tail entries of a row in one 16-byte load
+              const double2 xa = lds128(xs + ra * K + 8), xb = lds128(xs + rbb * K + 8);
+              ctacc[qq][0][0] = fma(a0.x, xa.x, ctacc[qq][0][0]);
+              ctacc[qq][1][0] = fma(a0.y, xa.x, ctacc[qq][1][0]);
+              ut[0][0] = fma(a1.x, xb.x, ut[0][0]);
+              ut[1][0] = fma(a1.y, xb.x, ut[1][0]);
+              ctacc[qq][0][1 % TLA] = fma(a0.x, xa.y, ctacc[qq][0][1 % TLA]);
+              ctacc[qq][1][1 % TLA] = fma(a0.y, xa.y, ctacc[qq][1][1 % TLA]);
+              ut[0][1 % TLA] = fma(a1.x, xb.y, ut[0][1 % TLA]);
+              ut[1][1 % TLA] = fma(a1.y, xb.y, ut[1][1 % TLA]);
+            } else if (TL > 0) {
 #pragma unroll
               for (int j = 0; j < TLA; ++j) {
                 double xa, xb;
