@@ -69,9 +69,14 @@ struct FlowChol {
     a[J] = (r == J) ? pv * di : ((r > J) ? a[J] * di : a[J]);
     di_r = (r == J) ? di : di_r;
     if constexpr (J + 1 < 32) {
-      if (J + 1 >= nb) {  // identity padding beyond an nb-wide block: nothing left to do
-        di_r = (r > J) ? 1.0 : di_r;
-        return;
+      // identity padding beyond an nb-wide block: nothing left to do.  Tested every eighth
+      // column only -- a branch per column splits the unrolled chain into basic blocks and
+      // the next pivot's rsqrt no longer overlaps this column's updates
+      if constexpr ((J + 1) % 8 == 0) {
+        if (J + 1 >= nb) {
+          di_r = (r > J) ? 1.0 : di_r;
+          return;
+        }
       }
       const double l1 = __shfl_sync(0xffffffffu, a[J], J + 1);      // L[J+1][J]
       const double d1 = __shfl_sync(0xffffffffu, a[J + 1], J + 1);  // A[J+1][J+1] so far
