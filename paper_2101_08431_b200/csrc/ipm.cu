@@ -381,9 +381,13 @@ constexpr int ATB_T = 64, ATB_R = 32, ATB_LD = 72;
 constexpr int ATB_S = 3;  // cp.async ring stages of ATB_R rows (both operands)
 constexpr size_t ATB_SMEM = (size_t)ATB_S * 2 * ATB_R * ATB_LD * sizeof(double);
 
+// flat != 0 (one 64 x 64 tile covers both operands, 16-byte aligned bases): a chunk of 32 rows
+// is ONE contiguous run of 32 ca (32 cb) doubles, copied with 16-byte cp.async into a dense
+// [row][ca] layout -- 7 copies per thread and chunk instead of 32 element copies with their
+// address arithmetic (the element path spent ~1 us of a 2 us chunk issuing them at ca = 55)
 __global__ void __launch_bounds__(256) k_atb_mma(const double* __restrict__ A, long rows, long ca,
                                                  const double* __restrict__ B, long cb,
-                                                 long stripe, double* __restrict__ part) {
+                                                 long stripe, double* __restrict__ part, int flat) {
   extern __shared__ __align__(16) double atb_sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -399,6 +403,29 @@ __global__ void __launch_bounds__(256) k_atb_mma(const double* __restrict__ A, l
       double* sb = sa + ATB_R * ATB_LD;
       const long ib = i_beg + (long)c * ATB_R;
       const int nr = (int)min((long)ATB_R, i_end - ib);
+      if (flat) {
+        const int na = nr * (int)ca, nb = nr * (int)cb;
+        const double* ga = A + ib * ca;
+        const double* gb = B + ib * cb;
+        for (int e = 2 * tid; e < ATB_R * (int)ca; e += 512) {
+          if (e + 1 < na)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(sa + e)), "l"(ga + e) : "memory");
+          else {
+            sa[e] = e < na ? ga[e] : 0.0;
+            sa[e + 1] = 0.0;
+          }
+        }
+        for (int e = 2 * tid; e < ATB_R * (int)cb; e += 512) {
+          if (e + 1 < nb)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(sb + e)), "l"(gb + e) : "memory");
+          else {
+            sb[e] = e < nb ? gb[e] : 0.0;
+            sb[e + 1] = 0.0;
+          }
+        }
+      } else
 #pragma unroll
       for (int q = 0; q < ATB_R * ATB_T / 256; ++q) {
         const int e = tid + 256 * q;
@@ -434,13 +461,27 @@ __global__ void __launch_bounds__(256) k_atb_mma(const double* __restrict__ A, l
     __syncthreads();
     const double* sa = atb_sm + (size_t)(c % ATB_S) * 2 * ATB_R * ATB_LD;
     const double* sb = sa + ATB_R * ATB_LD;
+    if (flat) {
+      const int lda = (int)ca, ldb = (int)cb;
+      const bool va = 8 * warp + g < lda;
 #pragma unroll
-    for (int kk = 0; kk < ATB_R / 4; ++kk) {
-      const double af = sa[(4 * kk + t) * ATB_LD + 8 * warp + g];
+      for (int kk = 0; kk < ATB_R / 4; ++kk) {
+        const double af = va ? sa[(4 * kk + t) * lda + 8 * warp + g] : 0.0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const double bf = sb[(4 * kk + t) * ATB_LD + 8 * j + g];
-        dmma_f64(acc[j][0], acc[j][1], af, bf);
+        for (int j = 0; j < 8; ++j) {
+          const double bf = (8 * j + g < ldb) ? sb[(4 * kk + t) * ldb + 8 * j + g] : 0.0;
+          dmma_f64(acc[j][0], acc[j][1], af, bf);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < ATB_R / 4; ++kk) {
+        const double af = sa[(4 * kk + t) * ATB_LD + 8 * warp + g];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double bf = sb[(4 * kk + t) * ATB_LD + 8 * j + g];
+          dmma_f64(acc[j][0], acc[j][1], af, bf);
+        }
       }
     }
     __syncthreads();
@@ -1496,7 +1537,8 @@ extern "C" int nmfb_atb(const double* A, long rows, long ca, const double* B, lo
       dim3 grid((unsigned)((ca + ATB_T - 1) / ATB_T), (unsigned)((cb + ATB_T - 1) / ATB_T),
                 (unsigned)ns);
       nmfb_smem_attr(k_atb_mma, ATB_SMEM);
-      ++g_nmfb_launches, k_atb_mma<<<grid, 256, ATB_SMEM, st>>>(A, rows, ca, B, cb, stripe, work);
+      const int flat = (ca <= ATB_T && cb <= ATB_T && (((uintptr_t)A | (uintptr_t)B) & 15) == 0) ? 1 : 0;
+      ++g_nmfb_launches, k_atb_mma<<<grid, 256, ATB_SMEM, st>>>(A, rows, ca, B, cb, stripe, work, flat);
       ++g_nmfb_launches, k_sum_parts_warp<<<(unsigned)((ca * cb * 32 + 255) / 256), 256, 0, st>>>(
           work, (int)ns, ca * cb, out);
       NMFB_CHECK_LAUNCH();
